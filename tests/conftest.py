@@ -1,0 +1,25 @@
+import os
+import sys
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+if ROOT not in sys.path:
+    sys.path.insert(0, ROOT)
+
+
+def pytest_configure(config):
+    config.addinivalue_line("markers", "gpu: needs a CUDA device (B200, sm_100a)")
+    config.addinivalue_line("markers", "slow: long-running CPU test")
+
+
+@pytest.fixture(scope="session")
+def P4096():
+    from oracle import ref
+    return ref.bfv_params(4096, 2, 37)
+
+
+@pytest.fixture(scope="session")
+def P8192():
+    from oracle import ref
+    return ref.bfv_params(8192, 3, 37)

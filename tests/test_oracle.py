@@ -1,0 +1,318 @@
+"""Pins of the CPU oracle against what the paper and mathematics fix (-m "not gpu").
+
+Each test pins an oracle function to something other than itself: a closed form, a
+special case, an independent library routine (cryptography's ChaCha20, mpmath, numpy),
+brute force on tiny inputs, or the SPEC/paper worked example under tests/golden/.
+"""
+import json
+import os
+import random
+
+import numpy as np
+import pytest
+
+import synth
+from oracle import ref
+
+GOLDEN = os.path.join(os.path.dirname(__file__), "golden")
+
+
+# ------------------------------------------------------------------------------ params (O1)
+def _miller_rabin(n: int) -> bool:
+    """Deterministic Miller-Rabin for n < 3.3e24 (first 13 prime bases) -- independent of sympy."""
+    if n < 2:
+        return False
+    bases = [2, 3, 5, 7, 11, 13, 17, 19, 23, 29, 31, 37, 41]
+    for b in bases:
+        if n % b == 0:
+            return n == b
+    d, s = n - 1, 0
+    while d % 2 == 0:
+        d //= 2
+        s += 1
+    for a in bases:
+        x = pow(a, d, n)
+        if x in (1, n - 1):
+            continue
+        for _ in range(s - 1):
+            x = pow(x, 2, n)
+            if x == n - 1:
+                break
+        else:
+            return False
+    return True
+
+
+@pytest.mark.parametrize("N,L", [(4096, 2), (8192, 3)])
+def test_primes_are_the_largest_ntt_friendly(N, L):
+    P = ref.bfv_params(N, L, 37)
+    assert len(P.primes) == L
+    # largest first; every candidate p = 1 mod 2N between 2^50 and the last prime is checked
+    cand = ((1 << 50) - 1) // (2 * N) * (2 * N) + 1
+    found = []
+    while len(found) < L:
+        if _miller_rabin(cand):
+            found.append(cand)
+        cand -= 2 * N
+    assert tuple(found) == P.primes
+    for p, psi in zip(P.primes, P.psis):
+        assert p < (1 << 50) and p % (2 * N) == 1
+        assert pow(psi, N, p) == p - 1          # psi is a primitive 2N-th root: psi^N = -1
+        assert pow(psi, 2 * N, p) == 1
+
+
+def test_delta_closed_form(P4096, P8192):
+    for P in (P4096, P8192):
+        q, t = P.q, P.t
+        assert P.delta * t <= q < (P.delta + 1) * t
+        assert P.r_t == q - P.delta * t
+        assert all(dm == P.delta % p for dm, p in zip(P.delta_mod, P.primes))
+    # N=4096/L=2 shares its primes with N=8192/L=3 (both are = 1 mod 16384?) -- only if so:
+    assert 99 < P4096.q.bit_length() <= 100
+
+
+# ------------------------------------------------------------------------------ PRF (O2, C10)
+def _lib_chacha_u64(seed, domain, stream, count, first=0):
+    from cryptography.hazmat.primitives.ciphers import Cipher, algorithms
+    key = int(seed).to_bytes(8, "little") + bytes(24)
+    nonce12 = int(domain).to_bytes(4, "little") + int(stream).to_bytes(8, "little")
+    blk0 = first // 8
+    nblk = (first + count + 7) // 8 - blk0
+    nonce16 = blk0.to_bytes(4, "little") + nonce12
+    ks = Cipher(algorithms.ChaCha20(key, nonce16), mode=None).encryptor().update(bytes(64 * nblk))
+    words = np.frombuffer(ks, dtype="<u8")
+    off = first - 8 * blk0
+    return words[off:off + count].astype(np.uint64)
+
+
+@pytest.mark.parametrize("seed,domain,stream,count,first", [
+    (0, 1, 0, 64, 0), (0x230518396, 2, 5, 100, 3), (2**64 - 1, 4, 2**40 + 7, 37, 1001),
+    (12345, 3, 17, 8, 8 * 300)])
+def test_prf_matches_cryptography_chacha20(seed, domain, stream, count, first):
+    ours = ref.prf_u64(seed, domain, stream, count, first)
+    assert np.array_equal(ours, _lib_chacha_u64(seed, domain, stream, count, first))
+
+
+# ------------------------------------------------------------------------------ CDT (C8)
+def test_cdt_table_closed_form():
+    import mpmath
+    T = ref.cdt_table()
+    assert len(T) == 42 and T[-1] == 1 << 63
+    assert all(T[k] < T[k + 1] for k in range(20))          # strictly increasing in the bulk
+    assert all(T[k] <= T[k + 1] for k in range(41))         # saturates at 2^63 - 1 in the far tail
+    # moments of the table's distribution vs the closed-form discrete Gaussian
+    probs = [T[0]] + [T[k] - T[k - 1] for k in range(1, 42)]
+    var = sum(k * k * p for k, p in enumerate(probs)) / 2**63
+    mpmath.mp.dps = 40
+    rho = [mpmath.e ** (-(k * k) / mpmath.mpf("20.48")) for k in range(-41, 42)]
+    var_exact = sum((k - 41) ** 2 * r for k, r in enumerate(rho)) / sum(rho)
+    assert abs(var - float(var_exact)) < 1e-12
+    assert abs(var ** 0.5 - 3.2) < 0.01          # a discrete Gaussian of width 3.2 has std ~3.2
+    # P(E = 0) = 1/Z
+    assert abs(T[0] / 2**63 - float(1 / sum(rho))) < 1e-15
+
+
+def test_cdt_sampler_boundaries_and_moments(P4096):
+    import ctypes
+    T = ref._u64arr(ref.cdt_table())
+    one = ref.lib().or_cdt_sample_one
+    one.restype = ctypes.c_int64
+    for k in (0, 1, 5, 20):           # distinct table entries (the far tail saturates)
+        for sign in (0, 1):
+            u_in = (sign << 63) | (int(T[k]) - 1)
+            u_next = (sign << 63) | int(T[k])
+            s = -1 if sign else 1
+            assert one(ctypes.c_uint64(u_in), ref._p(T), 42) == s * k
+            assert one(ctypes.c_uint64(u_next), ref._p(T), 42) == s * (k + 1)
+    e = np.concatenate([ref.sample_e(P4096, 99, g) for g in range(25)]).astype(np.float64)
+    assert abs(e.mean()) < 0.05 and abs(e.std() - 3.2) < 0.04 and np.abs(e).max() <= 41
+
+
+# ------------------------------------------------------------------------------ encodings
+def test_encodings_golden():
+    g = json.load(open(os.path.join(GOLDEN, "encodings.json")))
+    N = g["N"]
+    for case in g["piA"]:
+        a = ref.encode_A(case["A"], N, case["r"])
+        assert a[:len(case["poly"])] == case["poly"] and not any(a[len(case["poly"]):])
+    for case in g["piB"]:
+        b = ref.encode_B(case["B"], N, case["m"])
+        assert b[:len(case["poly"])] == case["poly"] and not any(b[len(case["poly"]):])
+    pr = g["product"]
+    c = ref.negacyclic_mul_int(ref.encode_A(pr["A"], N, pr["r"]), ref.encode_B(pr["B"], N, pr["m"]), N)
+    assert c[:len(pr["poly"])] == pr["poly"]
+    assert ref.decode_C(c, pr["m"], pr["r"], pr["n"]) == pr["C"]
+
+
+@pytest.mark.parametrize("N,tile", [(64, (2, 4, 8)), (64, (4, 4, 4)), (64, (1, 64, 1)),
+                                    (64, (64, 1, 1)), (64, (1, 1, 64)), (128, (3, 5, 7))])
+def test_encodings_reconstruct_matmul_bruteforce(N, tile):
+    """No-collision property of Alg. 1: decode(pi_A(A) * pi_B(B)) = A.B over Z (brute force)."""
+    m, r, n = tile
+    rng = random.Random(N * 1000 + m * 100 + r * 10 + n)
+    for _ in range(5):
+        A = [[rng.randint(-50, 50) for _ in range(r)] for _ in range(m)]
+        B = [[rng.randint(-50, 50) for _ in range(n)] for _ in range(r)]
+        c = ref.negacyclic_mul_int(ref.encode_A(A, N, r), ref.encode_B(B, N, m), N)
+        AB = [[sum(A[i][j] * B[j][k] for j in range(r)) for k in range(n)] for i in range(m)]
+        assert ref.decode_C(c, m, r, n) == AB
+
+
+# ------------------------------------------------------------------------------ negacyclic products, NTT
+def test_negacyclic_special_cases(P4096):
+    N, p = P4096.N, P4096.primes[0]
+    a = np.zeros(N, np.uint64); a[N - 1] = 1
+    x = np.zeros(N, np.uint64); x[1] = 1
+    out = ref.negacyclic_mul(N, p, a, x)                       # x^(N-1) * x = -1
+    assert out[0] == p - 1 and not out[1:].any()
+    rng = np.random.default_rng(1)
+    b = rng.integers(0, p, N, dtype=np.uint64)
+    one = np.zeros(N, np.uint64); one[0] = 1
+    assert np.array_equal(ref.negacyclic_mul(N, p, one, b), b)   # 1 * b = b
+
+
+def test_schoolbook_vs_python_vs_numpy_fold():
+    N, p = 64, ref.ntt_primes(64, 1)[0]
+    rng = np.random.default_rng(2)
+    for _ in range(10):
+        a = rng.integers(0, p, N, dtype=np.uint64)
+        b = rng.integers(0, p, N, dtype=np.uint64)
+        c = ref.negacyclic_mul(N, p, a, b)
+        full = np.convolve(a.astype(object), b.astype(object))          # numpy, exact ints
+        fold = [(int(full[k]) - (int(full[k + N]) if k + N < len(full) else 0)) % p for k in range(N)]
+        assert [int(v) for v in c] == fold
+        assert [int(v) for v in c] == ref.negacyclic_mul_int([int(v) for v in a], [int(v) for v in b], N, p)
+
+
+@pytest.mark.parametrize("N", [16, 64])
+def test_oracle_ntt_fast_equals_definition(N):
+    p = ref.ntt_primes(N, 1)[0]
+    psi = ref.primitive_2n_root(p, N)
+    rng = np.random.default_rng(N)
+    a = rng.integers(0, p, N, dtype=np.uint64)
+    assert np.array_equal(ref.ntt(N, p, psi, a), ref.ntt_naive(N, p, psi, a))
+    x = np.zeros(N, np.uint64); x[1] = 1                    # NTT(x)_k = psi^(2k+1)
+    assert [int(v) for v in ref.ntt(N, p, psi, x)] == [pow(psi, 2 * k + 1, p) for k in range(N)]
+
+
+@pytest.mark.parametrize("N", [64, 1024, 4096])
+def test_oracle_ntt_roundtrip_and_convolution(N):
+    rng = np.random.default_rng(N + 7)
+    for p in ref.ntt_primes(N, 2):
+        psi = ref.primitive_2n_root(p, N)
+        a = rng.integers(0, p, N, dtype=np.uint64)
+        b = rng.integers(0, p, N, dtype=np.uint64)
+        assert np.array_equal(ref.intt(N, p, psi, ref.ntt(N, p, psi, a)), a)     # INTT o NTT = id
+        assert np.array_equal(ref.negacyclic_mul_ntt(N, p, psi, a, b), ref.negacyclic_mul(N, p, a, b))
+
+
+# ------------------------------------------------------------------------------ BFV encrypt / decrypt (O3, O4, O10)
+def test_keygen_ternary_and_balanced(P4096):
+    sk = ref.keygen(P4096, 7)
+    assert set(np.unique(sk)) <= {-1, 0, 1}
+    counts = [(sk == v).sum() for v in (-1, 0, 1)]
+    assert min(counts) > 1200      # (u mod 3) - 1 is near-uniform
+    assert np.array_equal(sk, ref.keygen(P4096, 7))   # deterministic per seed
+
+
+def test_encrypt_decrypt_roundtrip_exact_noise(P4096):
+    """Fresh ct: c0 + c1*s = Delta*b + e exactly, so Dec = pi_B(X tile) and the measured
+    noise equals the sampled error polynomial e (reading C8)."""
+    P, tile = P4096, (16, 32, 8)
+    X = synth.activations(11, 8, 64)
+    sk = ref.keygen(P, 3)
+    ct = ref.encrypt(P, tile, sk, X, 5)
+    pts, noise = ref.decrypt_full(P, sk, ct)
+    m, r, n = tile
+    for J in range(2):
+        g = J          # nK = 1
+        b = ref.encode_B([[int(X[k, J * r + j]) for k in range(n)] for j in range(r)], P.N, m)
+        assert pts[g] == b
+        assert noise[g] == [int(v) for v in ref.sample_e(P, 5, g)]
+    # encrypt(0) -> 0
+    ct0 = ref.encrypt(P, tile, sk, np.zeros((8, 64), np.uint64), 6)
+    pts0, _ = ref.decrypt_full(P, sk, ct0)
+    assert all(v == 0 for row in pts0 for v in row)
+
+
+def test_he_matmul_homomorphism_and_noise(P4096):
+    """Dec(he_matmul) = [sum_J pi_A(A_IJ) * pi_B(B_JK)]_t over Z and the
+    noise fits the Appendix C bound 2R*max|w|*(r_t + e_max) < Delta/2."""
+    P, tile = P4096, (16, 32, 8)
+    m, r, n = tile
+    X = synth.activations(21, 8, 64)
+    W = synth.stressed_weights(22, 64, 32, bound=1500)
+    sk = ref.keygen(P, 23)
+    ct_in = ref.encrypt(P, tile, sk, X, 24)
+    ct_out = ref.he_matmul(P, tile, W, ct_in, 8)
+    pts, noise = ref.decrypt_full(P, sk, ct_out)
+    lift = lambda w: int(w) - (1 << 37) if int(w) >= (1 << 36) else int(w)
+    nI, nJ, nK = ref.tile_counts(tile, 32, 64, 8)
+    maxw = max(abs(lift(w)) for w in W.reshape(-1))
+    bound = 2 * 64 * maxw * (P.r_t + 41)
+    assert bound < P.delta // 2
+    for I in range(nI):
+        acc = [0] * P.N
+        for J in range(nJ):
+            A = [[lift(W[J * r + j, I * m + i]) for j in range(r)] for i in range(m)]
+            B = [[int(X[k, J * r + j]) for k in range(n)] for j in range(r)]
+            prod = ref.negacyclic_mul_int(ref.encode_A(A, P.N, r), ref.encode_B(B, P.N, m), P.N)
+            acc = [u + v for u, v in zip(acc, prod)]
+        assert pts[I * nK] == [v % P.t for v in acc]
+        assert max(abs(v) for v in noise[I * nK]) < bound
+
+
+def test_he_matmul_schoolbook_equals_oracle_ntt(P4096):
+    P, tile = P4096, (16, 8, 32)
+    Nb, R, Ma = 40, 24, 40          # ragged: nI=3, nJ=3, nK=2, partial tiles everywhere
+    ct_in = synth.uniform_below(31, (3, 2, 2, P.L, P.N), P.primes)
+    W = synth.weights(32, R, Ma)
+    sb = ref.he_matmul(P, tile, W, ct_in, Nb)
+    tiles = [(I, K) for I in range(3) for K in range(2)]
+    nt = ref.he_matmul_ntt_tiles(P, tile, W, ct_in, Nb, tiles)
+    for o, (I, K) in enumerate(tiles):
+        assert np.array_equal(sb[I, K], nt[o])
+
+
+# ------------------------------------------------------------------------------ end to end (Alg. 1; O7-O11)
+@pytest.mark.parametrize("shape,tile,compress", [
+    ((8, 64, 64), (16, 32, 8), True),      # config c0
+    ((8, 64, 64), (16, 32, 8), False),
+    ((5, 37, 19), (4, 8, 4), True),        # ragged in every dimension
+    ((3, 1, 2), (1, 1, 1), True),          # degenerate 1x1x1 tile
+])
+def test_protocol_reconstructs_XW_mod_t(P4096, shape, tile, compress):
+    Nb, R, Ma = shape
+    X = synth.activations(41, Nb, R)
+    W = synth.weights(42, R, Ma)
+    out = ref.matmul_protocol(P4096, tile, X, W, 43, 44, 45, compress)
+    got = (out["share_client"] + out["share_server"]) & np.uint64((1 << 37) - 1)
+    assert np.array_equal(got, ref.matmul_mod_t(X, W))
+
+
+def test_compressed_decrypt_equals_full_and_size(P4096):
+    P, tile = P4096, (16, 32, 8)
+    m, r, n = tile
+    X = synth.activations(51, 8, 64)
+    W = synth.weights(52, 64, 64)
+    sk = ref.keygen(P, 53)
+    ct_out = ref.he_matmul(P, tile, W, ref.encrypt(P, tile, sk, X, 54), 8)
+    mc, sc = ref.mask_and_share(P, tile, ct_out, 64, 8, 55, True)
+    mf, sf = ref.mask_and_share(P, tile, ct_out, 64, 8, 55, False)
+    assert np.array_equal(sc, sf)
+    assert np.array_equal(ref.decrypt_share(P, tile, sk, mc, 64, 8, True),
+                          ref.decrypt_share(P, tile, sk, mf, 64, 8, False))
+    # response size ratio (N + m*n) / 2N exactly ("roughly reduces half")
+    assert mc.shape[-1] * 2 * P.N == mf.shape[-1] * (P.N + m * n)
+
+
+def test_mask_uniform_chi_squared(P4096):
+    """The server share is the mask at the decoded positions: uniform on Z_{2^37}."""
+    P, tile = P4096, (16, 8, 32)
+    ct = synth.uniform_below(61, (4, 4, 2, P.L, P.N), P.primes)
+    _, share = ref.mask_and_share(P, tile, ct, 64, 128, 62, True)
+    top = (share >> np.uint64(33)).astype(np.int64).reshape(-1)     # 16 buckets of the top 4 bits
+    counts = np.bincount(top, minlength=16)
+    exp = len(top) / 16
+    chi2 = ((counts - exp) ** 2 / exp).sum()
+    assert chi2 < 37.7        # chi^2_{15} at p = 0.001
