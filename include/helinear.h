@@ -1,0 +1,190 @@
+/*
+ * helinear.h -- C ABI of the B200-native server-side homomorphic linear layer of
+ * arxiv 2305.18396 ("Privacy-Computing-Friendly Transformer Inference"), Algorithm 1
+ * (Pi_MatMul), with the response compression of §3.1.3
+ * and the GPU cipher-plain multiply of PAPER.md:155-156.
+ *
+ * Roles (reading C1 of DESIGN.md §3): the server holds W (R x Ma), the
+ * client holds its share X (Nb x R).  Alg. 1 is run on A = W^T (server, left operand) and
+ * B = X^T (client, right operand); shares of C = A.B = (X.W)^T are emitted in the layout
+ * of X.W, i.e. [Nb][Ma] (the transposition trick of PAPER.md:115, footnote).
+ *
+ * Ring and parameters (§2.2): BFV-RNS over R_q = Z_q[X]/(X^N+1),
+ * q = p_0 ... p_{L-1}, plaintext modulus t = 2^log2_t, Delta = floor(q/t).
+ *
+ * Tiles (reading C2): an explicit (m, r, n) with m*r*n <= N.  Counts
+ *   nI = ceil(Ma/m), nJ = ceil(R/r), nK = ceil(Nb/n); partial tiles are zero-padded.
+ * Encodings (Alg. 1 step 1):
+ *   pi_A: a_IJ[i*r + r-1-j] = lift(W[J*r+j][I*m+i]),  lift = centered [-t/2, t/2) (reading C6)
+ *   pi_B: b_JK[k*m*r + j]   = X[K*n+k][J*r+j]
+ * Decoding (Alg. 1 step 4): C[i][k] = c[pos(i,k)], pos(i,k) = k*m*r + i*r + r-1.
+ *
+ * Memory layouts (uint64 words; residues canonical in [0, p_l); little-endian hosts):
+ *   X          [Nb][R]                      values < 2^log2_t
+ *   W          [R][Ma]                      values < 2^log2_t (two's complement of the lift)
+ *   sk         int8 [N]                     ternary {-1, 0, 1}
+ *   ct_in      [nJ][nK][2][L][N]            (c0, c1) of Enc(pi_B(X^T tile JK)), coefficient form
+ *   ct_out     [nI_s][nK][2][L][N]          Enc(c_IK) = sum_J a_IJ * ct_in[J][K], coefficient form
+ *   ct_masked  compressed: [nI_s][nK][ L*m*n (c0 at pos(i,k), index k*m+i) | L*N (c1) ]
+ *              full:       [nI_s][nK][2][L][N]
+ *   share      [Nb][Ma]                     (server share; a shard writes only its columns)
+ *   wcache     opaque device bytes          NTT-domain pi_A polynomials of a shard of I tiles
+ *   workspace  opaque device bytes          NTT-domain copy of ct_in
+ * where a shard is the I-tile range [i_begin, i_end) (i_end = -1 means nI) and nI_s = i_end - i_begin.
+ *
+ * Randomness (reading C10): a ChaCha20 PRF (RFC 8439 block function), key = LE64(seed) || 0^24,
+ * nonce = LE32(domain) || LE64(stream), block counter from 0; u64 word i = LE64(keystream[8i, 8i+8)).
+ * Domains: 1 secret key (stream 0), 2 uniform a (stream g*L + l), 3 error (stream g),
+ * 4 mask (stream I*nK + K, I global).  g = J*nK + K.
+ *
+ * Ownership: the caller allocates and owns every buffer (host or device as stated per call).
+ * The library owns only the context: parameters, per-prime constants and twiddle tables
+ * (uploaded once to `device` at create) plus a few bytes of device scratch for status flags.
+ * The library performs no device allocation after hl_ctx_create.
+ *
+ * Errors: every call returns HL_OK (0) or a negative code; hl_last_error() returns a
+ * thread-local message describing the last failure on the calling thread.  Device calls
+ * are enqueued on `stream` (a cudaStream_t passed as void*; NULL = legacy default stream)
+ * and return after launch: asynchronous faults surface at the next synchronisation.
+ * Contexts are immutable after creation and may be used concurrently from several threads
+ * on different streams.
+ */
+#ifndef HELINEAR_H_
+#define HELINEAR_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum {
+  HL_OK = 0,
+  HL_EINVAL = -1,   /* null pointer, bad shard range, shape mismatch          */
+  HL_EDIM = -2,     /* m*r*n > N or a non-positive tile dimension ("dims too large")        */
+  HL_ERANGE = -3,   /* an input value >= 2^log2_t, or a secret key not ternary             */
+  HL_ENOISE = -4,   /* static worst-case noise bound 2R*max|w|*(r_t + 41) >= Delta/2       */
+  HL_ECUDA = -5,    /* a CUDA runtime error; the message carries cudaGetErrorString         */
+  HL_ENOTSUP = -6   /* (N, L, log2_t) outside the built kernels: N in {4096, 8192},
+                       1 <= L <= 3, primes in (2^49, 2^50), 1 <= log2_t <= 62              */
+};
+
+typedef struct hl_ctx hl_ctx;
+
+typedef struct { int32_t m, r, n; } hl_tile;
+
+typedef struct {
+  int64_t nI, nJ, nK;         /* tile counts of the full problem                              */
+  int64_t nI_shard;           /* i_end - i_begin                                              */
+  int64_t ct_in_words;        /* nJ*nK*2*L*N                                                  */
+  int64_t ct_out_words;       /* nI_shard*nK*2*L*N                                            */
+  int64_t ct_masked_words;    /* compressed: nI_shard*nK*L*(m*n + N)                          */
+  int64_t ct_full_words;      /* uncompressed masked: nI_shard*nK*2*L*N                       */
+  int64_t share_words;        /* Nb*Ma                                                        */
+  int64_t wcache_bytes;       /* nI_shard*nJ*L*N*8                                            */
+  int64_t workspace_bytes;    /* nJ*nK*2*L*N*8                                                */
+} hl_layout;
+
+/* ---- context ---------------------------------------------------------------------------- */
+
+/* Thread-local description of the last error on this thread ("" if none). */
+const char *hl_last_error(void);
+
+/* Create a context for N, L primes, t = 2^log2_t on CUDA device `device`.
+ * primes == NULL selects the L largest primes below 2^50 with p = 1 (mod 2N), descending
+ * (reading C4); otherwise primes[0..L) must be distinct primes in (2^49, 2^50), p = 1 mod 2N.
+ * device < 0 creates a host-only context: the client calls (keygen, encrypt, decrypt_share)
+ * and the queries work, the device calls fail with HL_EINVAL. */
+int hl_ctx_create(uint32_t N, uint32_t L, uint32_t log2_t, const uint64_t *primes, int device,
+                  hl_ctx **out);
+int hl_ctx_destroy(hl_ctx *ctx);
+
+/* Copy the primes and Delta mod p_l (Delta = floor(q/t), reading C5) into caller arrays of L. */
+int hl_ctx_params(const hl_ctx *ctx, uint64_t *primes_out, uint64_t *delta_mod_out);
+
+/* Sizes of every buffer of one matmul (Ma x R weights, Nb tokens) for I-tile shard [i_begin, i_end). */
+int hl_layout_query(const hl_ctx *ctx, hl_tile tile, int64_t Ma, int64_t R, int64_t Nb,
+                    int64_t i_begin, int64_t i_end, hl_layout *out);
+
+/* ---- client side (host memory; the boundary of the server path) ------------------------- */
+
+/* Secret key s_i = (u64_SK[i] mod 3) - 1 (reading C7).  sk: host int8[N]. */
+int hl_keygen(const hl_ctx *ctx, uint64_t seed, int8_t *sk);
+
+/* Alg. 1 step 2: encode every tile with pi_B and encrypt with the secret key:
+ *   c1 = a_l, c0 = -a_l*s + e + Delta_l*b (mod p_l), a uniform, e discrete Gaussian sigma=3.2
+ *   (CDT, reading C8).  X: host [Nb][R]; ct_in: host [nJ][nK][2][L][N] (layout.ct_in_words).
+ * Errors: HL_ERANGE if some X >= 2^log2_t or sk is not ternary. */
+int hl_encrypt(const hl_ctx *ctx, const int8_t *sk, hl_tile tile, const uint64_t *X, int64_t Nb,
+               int64_t R, uint64_t seed, uint64_t *ct_in);
+
+/* Alg. 1 step 4 on the client: m = c0 + c1*s, x = CRT(m) in [0, q),
+ * y = floor((t*x + floor(q/2)) / q) mod t at pos(i,k); share_client[K*n+k][I*m+i] = y.
+ * ct_masked: host, whole problem (shard [0, nI)); share_client: host [Nb][Ma]. */
+int hl_decrypt_share(const hl_ctx *ctx, const int8_t *sk, hl_tile tile, const uint64_t *ct_masked,
+                     int compress, int64_t Ma, int64_t Nb, uint64_t *share_client);
+
+/* ---- server side (device memory, stream-ordered) ----------------------------------------- */
+
+/* Alg. 1 step 1 for the server + the NTT of PAPER.md:156 fn: pi_A of every
+ * (I, J) tile with I in [i_begin, i_end), lifted (C6), reduced mod p_l, forward-NTT'd into
+ * `wcache` (layout.wcache_bytes, device).  W: device [R][Ma].  Synchronises `stream` once to
+ * check the input range and the static noise bound (offline call).
+ * Errors: HL_ERANGE (W >= 2^log2_t), HL_ENOISE (worst-case noise >= Delta/2). */
+int hl_encode_weights(const hl_ctx *ctx, hl_tile tile, const uint64_t *W, int64_t R, int64_t Ma,
+                      int64_t i_begin, int64_t i_end, void *wcache, void *stream);
+
+/* Alg. 1 step 3, homomorphic part: for every I in the shard and every K,
+ *   ct_out[I][K][c] = sum_J a_IJ * ct_in[J][K][c]  mod (X^N + 1, p_l),  c in {0, 1}
+ * computed as forward NTT of ct_in -> pointwise multiply-accumulate over J against the cached
+ * NTT-domain weights -> inverse NTT.  ct_in: device [nJ][nK][2][L][N]; workspace: device,
+ * layout.workspace_bytes; ct_out: device [nI_s][nK][2][L][N], canonical residues. */
+int hl_he_matmul(const hl_ctx *ctx, hl_tile tile, const void *wcache, int64_t Ma, int64_t R,
+                 int64_t Nb, int64_t i_begin, int64_t i_end, const uint64_t *ct_in,
+                 void *workspace, uint64_t *ct_out, void *stream);
+
+/* Alg. 1 step 3, masking + §3.1.3 compression:
+ *   sigma = u64_MASK(stream I*nK+K)[0..N) & (t-1);  c0 <- c0 - Delta_l*sigma (mod p_l);
+ *   compress != 0: keep c1 and c0 at pos(i,k) only;  share_server[K*n+k][I*m+i] = sigma[pos(i,k)].
+ * ct_out: device [nI_s][nK][2][L][N]; ct_masked: device (layout.ct_masked_words or
+ * ct_full_words); share_server: device [Nb][Ma], only the shard's columns are written. */
+int hl_mask_and_share(const hl_ctx *ctx, hl_tile tile, int64_t Ma, int64_t Nb, int64_t i_begin,
+                      int64_t i_end, const uint64_t *ct_out, uint64_t seed, int compress,
+                      uint64_t *ct_masked, uint64_t *share_server, void *stream);
+
+/* he_matmul followed by mask_and_share in one call: the inverse NTT and the masking /
+ * compression / share extraction run as one fused kernel, so the coefficient-form ct_out is
+ * never written.  Results are bit-identical to the two calls.  ct_out_ntt: device scratch of
+ * layout.ct_out_words (holds the NTT-domain accumulators). */
+int hl_he_matmul_share(const hl_ctx *ctx, hl_tile tile, const void *wcache, int64_t Ma, int64_t R,
+                       int64_t Nb, int64_t i_begin, int64_t i_end, const uint64_t *ct_in,
+                       void *workspace, uint64_t *ct_out_ntt, uint64_t seed, int compress,
+                       uint64_t *ct_masked, uint64_t *share_server, void *stream);
+
+/* End-to-end server call on HOST buffers (the e2e path of bench.py): copies ct_in_host
+ * (pinned host, [nJ][nK][2][L][N]) to dev_ct_in, runs hl_he_matmul_share, and copies the
+ * masked response and the server share back to ct_masked_host / share_host (pinned host).
+ * All device buffers are caller-owned; the call is stream-ordered (synchronise before reading). */
+int hl_he_linear_host(const hl_ctx *ctx, hl_tile tile, const void *wcache, int64_t Ma, int64_t R,
+                      int64_t Nb, const uint64_t *ct_in_host, uint64_t seed, int compress,
+                      uint64_t *ct_masked_host, uint64_t *share_host, uint64_t *dev_ct_in,
+                      void *workspace, uint64_t *dev_ct_out_ntt, uint64_t *dev_ct_masked,
+                      uint64_t *dev_share, void *stream);
+
+/* ---- diagnostics (used by the parity tests and the NTT microbenchmark) -------------------- */
+
+/* out[p] = a[p] * b[p] in Z_{p_l}[X]/(X^N+1) for p < npoly, through the device NTT/INTT
+ * kernels.  a, b, out: device [npoly][L][N] canonical residues; out may alias a or b.
+ * scratch: device, npoly*L*N*8*2 bytes. */
+int hl_poly_mul(const hl_ctx *ctx, const uint64_t *a, const uint64_t *b, uint64_t *out,
+                int64_t npoly, void *scratch, void *stream);
+
+/* Forward NTT then inverse NTT of x in place (identity on canonical residues): exercises the
+ * two transforms alone.  x: device [npoly][L][N]; scratch: device npoly*L*N*8 bytes. */
+int hl_ntt_roundtrip(const hl_ctx *ctx, uint64_t *x, int64_t npoly, void *scratch, void *stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* HELINEAR_H_ */

@@ -338,48 +338,72 @@ void or_he_matmul_ntt_tiles(uint32_t N, uint32_t L, const uint64_t *primes, cons
   }
 }
 
-/* Alg. 1 step 3 + §3.1.3 (O7-O9; readings C3, C10-C12):
+/* Alg. 1 step 3 + §3.1.3 (O7-O9; readings C3, C10-C12) for ONE output ciphertext (I, K):
  *   sigma[i] = u64_MASK(stream I*nK+K)[i] & (2^t_bits - 1)
  *   c0 <- c0 - Delta_l * sigma (mod p_l);  keep c1, keep c0 at pos(i,k) = k*m*r + i*r + r-1
- *   S[K*n+k][I*m+i] = sigma[pos(i,k)]                                                   */
+ * Writes the masked ciphertext to dst and sigma at the kept positions (index k*m+i) to kept. */
+static void mask_one(uint32_t N, uint32_t L, const uint64_t *primes, const uint64_t *delta_mod,
+                     uint32_t t_bits, uint32_t m, uint32_t r, uint32_t n, uint64_t stream,
+                     const uint64_t *src, uint64_t seed, int compress, uint64_t *dst, uint64_t *kept) {
+  uint64_t tmask = (t_bits == 64) ? ~0ull : ((1ull << t_bits) - 1);
+  uint64_t *sigma = (uint64_t *)malloc(8ull * N);
+  or_prf_u64(seed, DOM_MASK, stream, 0, N, sigma);
+  for (uint32_t i = 0; i < N; i++) sigma[i] &= tmask;
+  for (uint32_t l = 0; l < L; l++) {
+    uint64_t p = primes[l];
+    const uint64_t *c0 = src + (uint64_t)l * N, *c1 = src + (uint64_t)(L + l) * N;
+    if (compress) {
+      for (uint32_t k = 0; k < n; k++)
+        for (uint32_t i = 0; i < m; i++) {
+          uint32_t pos = k * m * r + i * r + r - 1;
+          dst[(uint64_t)l * m * n + k * m + i] = submod(c0[pos], mulmod(delta_mod[l], sigma[pos] % p, p), p);
+        }
+      memcpy(dst + (uint64_t)L * m * n + (uint64_t)l * N, c1, 8ull * N);
+    } else {
+      for (uint32_t s = 0; s < N; s++)
+        dst[(uint64_t)l * N + s] = submod(c0[s], mulmod(delta_mod[l], sigma[s] % p, p), p);
+      memcpy(dst + (uint64_t)(L + l) * N, c1, 8ull * N);
+    }
+  }
+  for (uint32_t k = 0; k < n; k++)
+    for (uint32_t i = 0; i < m; i++) kept[k * m + i] = sigma[k * m * r + i * r + r - 1];
+  free(sigma);
+}
+
+/* Whole problem: every (I, K); server share S[K*n+k][I*m+i] = sigma[pos(i,k)] in range. */
 void or_mask_and_share(uint32_t N, uint32_t L, const uint64_t *primes, const uint64_t *delta_mod,
                        uint32_t t_bits, uint32_t m, uint32_t r, uint32_t n, int64_t Ma, int64_t Nb,
                        const uint64_t *ct_out, uint64_t seed, int compress, uint64_t *ct_masked,
                        uint64_t *share) {
   int64_t nI = (Ma + m - 1) / m, nK = (Nb + n - 1) / n;
-  uint64_t tmask = (t_bits == 64) ? ~0ull : ((1ull << t_bits) - 1);
   uint64_t per_ct = compress ? (uint64_t)L * (m * n + N) : 2ull * L * N;
 #pragma omp parallel for schedule(dynamic)
   for (int64_t o = 0; o < nI * nK; o++) {
     int64_t I = o / nK, K = o % nK;
-    uint64_t *sigma = (uint64_t *)malloc(8ull * N);
-    or_prf_u64(seed, DOM_MASK, (uint64_t)o, 0, N, sigma);
-    for (uint32_t i = 0; i < N; i++) sigma[i] &= tmask;
-    const uint64_t *src = ct_out + (uint64_t)o * 2 * L * N;
-    uint64_t *dst = ct_masked + (uint64_t)o * per_ct;
-    for (uint32_t l = 0; l < L; l++) {
-      uint64_t p = primes[l];
-      const uint64_t *c0 = src + (uint64_t)l * N, *c1 = src + (uint64_t)(L + l) * N;
-      if (compress) {
-        for (uint32_t k = 0; k < n; k++)
-          for (uint32_t i = 0; i < m; i++) {
-            uint32_t pos = k * m * r + i * r + r - 1;
-            dst[(uint64_t)l * m * n + k * m + i] = submod(c0[pos], mulmod(delta_mod[l], sigma[pos] % p, p), p);
-          }
-        memcpy(dst + (uint64_t)L * m * n + (uint64_t)l * N, c1, 8ull * N);
-      } else {
-        for (uint32_t s = 0; s < N; s++)
-          dst[(uint64_t)l * N + s] = submod(c0[s], mulmod(delta_mod[l], sigma[s] % p, p), p);
-        memcpy(dst + (uint64_t)(L + l) * N, c1, 8ull * N);
-      }
-    }
+    uint64_t *kept = (uint64_t *)malloc(8ull * m * n);
+    mask_one(N, L, primes, delta_mod, t_bits, m, r, n, (uint64_t)o, ct_out + (uint64_t)o * 2 * L * N,
+             seed, compress, ct_masked + (uint64_t)o * per_ct, kept);
     for (uint32_t k = 0; k < n; k++)
       for (uint32_t i = 0; i < m; i++) {
         int64_t row = K * n + k, col = I * (int64_t)m + i;
-        if (row < Nb && col < Ma) share[row * Ma + col] = sigma[k * m * r + i * r + r - 1];
+        if (row < Nb && col < Ma) share[row * Ma + col] = kept[k * m + i];
       }
-    free(sigma);
+    free(kept);
   }
+}
+
+/* Selected output tiles only (for sampled parity at full size): tiles = pairs (I, K) with
+ * global I; ct [ntiles][2][L][N] -> masked [ntiles][per_ct], kept sigma [ntiles][m*n].       */
+void or_mask_tiles(uint32_t N, uint32_t L, const uint64_t *primes, const uint64_t *delta_mod,
+                   uint32_t t_bits, uint32_t m, uint32_t r, uint32_t n, int64_t nK,
+                   const uint64_t *ct, const int64_t *tiles, int64_t ntiles, uint64_t seed,
+                   int compress, uint64_t *masked, uint64_t *kept) {
+  uint64_t per_ct = compress ? (uint64_t)L * (m * n + N) : 2ull * L * N;
+#pragma omp parallel for schedule(dynamic)
+  for (int64_t o = 0; o < ntiles; o++)
+    mask_one(N, L, primes, delta_mod, t_bits, m, r, n, (uint64_t)(tiles[2 * o] * nK + tiles[2 * o + 1]),
+             ct + (uint64_t)o * 2 * L * N, seed, compress, masked + (uint64_t)o * per_ct,
+             kept + (uint64_t)o * m * n);
 }
 
 /* Decryption core ("m = s*c1 + c0"), per prime, at the decoded positions

@@ -347,6 +347,22 @@ def mask_and_share(P: Params, tile, ct_out: np.ndarray, Ma: int, Nb: int, seed: 
     return masked, share
 
 
+def mask_tiles(P: Params, tile, ct: np.ndarray, nK: int, tiles, seed: int, compress: bool = True):
+    """O7-O9 for selected output tiles [(I, K), ...] (global I): ct [ntiles][2][L][N] ->
+    (masked [ntiles][per_ct], sigma at the kept positions [ntiles][m*n], index k*m+i)."""
+    m, r, n = tile
+    tl = np.ascontiguousarray(np.array(tiles, dtype=np.int64).reshape(-1, 2))
+    per = P.L * (m * n + P.N) if compress else 2 * P.L * P.N
+    masked = np.zeros((len(tl), per), dtype=np.uint64)
+    kept = np.zeros((len(tl), m * n), dtype=np.uint64)
+    lib().or_mask_tiles(ctypes.c_uint32(P.N), ctypes.c_uint32(P.L), _p(_u64arr(P.primes)),
+                        _p(_u64arr(P.delta_mod)), ctypes.c_uint32(P.t_bits), ctypes.c_uint32(m),
+                        ctypes.c_uint32(r), ctypes.c_uint32(n), ctypes.c_int64(nK),
+                        _p(np.ascontiguousarray(ct)), _p(tl, ctypes.c_int64), ctypes.c_int64(len(tl)),
+                        ctypes.c_uint64(seed), ctypes.c_int(int(compress)), _p(masked), _p(kept))
+    return masked, kept
+
+
 def crt_round(P: Params, residues) -> int:
     """O10: x = CRT(residues) in [0, q); y = floor((t*x + floor(q/2)) / q) mod t."""
     q = P.q

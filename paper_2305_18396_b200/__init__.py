@@ -1,0 +1,295 @@
+"""paper_2305_18396_b200 -- B200-native homomorphic linear layer of arxiv 2305.18396 (Alg. 1).
+
+Thin Python binding of libhelinear (C ABI declared in include/helinear.h): argument
+marshalling only.  Every step of the server path (encode_weights, he_matmul,
+mask_and_share) runs in the sm_100a kernels of csrc/kernels.cu; the client calls
+(keygen, encrypt, decrypt_share) run in the library's host C++.  PyTorch supplies device
+memory and streams.  There is no CPU fallback: if libhelinear.so is missing or no CUDA
+device is present, the device calls raise.
+
+Arrays are uint64 bit patterns.  Host arguments are numpy uint64 arrays; device arguments
+are torch CUDA tensors of dtype int64 or uint64 (same bits) -- see include/helinear.h for
+every layout.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from dataclasses import dataclass
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "lib", "libhelinear.so")
+
+HL_OK, HL_EINVAL, HL_EDIM, HL_ERANGE, HL_ENOISE, HL_ECUDA, HL_ENOTSUP = 0, -1, -2, -3, -4, -5, -6
+_CODES = {HL_EINVAL: "HL_EINVAL", HL_EDIM: "HL_EDIM", HL_ERANGE: "HL_ERANGE", HL_ENOISE: "HL_ENOISE",
+          HL_ECUDA: "HL_ECUDA", HL_ENOTSUP: "HL_ENOTSUP"}
+
+# every symbol include/helinear.h declares (checked by tests/test_abi.py)
+EXPORTS = ("hl_last_error", "hl_ctx_create", "hl_ctx_destroy", "hl_ctx_params", "hl_layout_query",
+           "hl_keygen", "hl_encrypt", "hl_decrypt_share", "hl_encode_weights", "hl_he_matmul",
+           "hl_mask_and_share", "hl_he_matmul_share", "hl_he_linear_host", "hl_poly_mul",
+           "hl_ntt_roundtrip")
+
+
+class HLError(RuntimeError):
+    def __init__(self, code: int, msg: str):
+        super().__init__(f"{_CODES.get(code, code)}: {msg}")
+        self.code = code
+
+
+class Tile(ctypes.Structure):
+    _fields_ = [("m", ctypes.c_int32), ("r", ctypes.c_int32), ("n", ctypes.c_int32)]
+
+    def __repr__(self):
+        return f"Tile({self.m}, {self.r}, {self.n})"
+
+
+class _Layout(ctypes.Structure):
+    _fields_ = [(f, ctypes.c_int64) for f in (
+        "nI", "nJ", "nK", "nI_shard", "ct_in_words", "ct_out_words", "ct_masked_words",
+        "ct_full_words", "share_words", "wcache_bytes", "workspace_bytes")]
+
+
+@dataclass(frozen=True)
+class Layout:
+    nI: int
+    nJ: int
+    nK: int
+    nI_shard: int
+    ct_in_words: int
+    ct_out_words: int
+    ct_masked_words: int
+    ct_full_words: int
+    share_words: int
+    wcache_bytes: int
+    workspace_bytes: int
+
+
+_lib = None
+
+
+def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
+    """Load libhelinear.so (built by `python -m paper_2305_18396_b200.build`); raises if absent."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(path):
+        raise ImportError(f"libhelinear.so not built at {path}: run `python -m paper_2305_18396_b200.build`")
+    L = ctypes.CDLL(path)
+    vp, i64, u64, i32 = ctypes.c_void_p, ctypes.c_int64, ctypes.c_uint64, ctypes.c_int
+    L.hl_last_error.restype = ctypes.c_char_p
+    L.hl_last_error.argtypes = []
+    sig = {
+        "hl_ctx_create": [ctypes.c_uint32, ctypes.c_uint32, ctypes.c_uint32, vp, i32, ctypes.POINTER(vp)],
+        "hl_ctx_destroy": [vp],
+        "hl_ctx_params": [vp, vp, vp],
+        "hl_layout_query": [vp, Tile, i64, i64, i64, i64, i64, ctypes.POINTER(_Layout)],
+        "hl_keygen": [vp, u64, vp],
+        "hl_encrypt": [vp, vp, Tile, vp, i64, i64, u64, vp],
+        "hl_decrypt_share": [vp, vp, Tile, vp, i32, i64, i64, vp],
+        "hl_encode_weights": [vp, Tile, vp, i64, i64, i64, i64, vp, vp],
+        "hl_he_matmul": [vp, Tile, vp, i64, i64, i64, i64, i64, vp, vp, vp, vp],
+        "hl_mask_and_share": [vp, Tile, i64, i64, i64, i64, vp, u64, i32, vp, vp, vp],
+        "hl_he_matmul_share": [vp, Tile, vp, i64, i64, i64, i64, i64, vp, vp, vp, u64, i32, vp, vp, vp],
+        "hl_he_linear_host": [vp, Tile, vp, i64, i64, i64, vp, u64, i32, vp, vp, vp, vp, vp, vp, vp, vp],
+        "hl_poly_mul": [vp, vp, vp, vp, i64, vp, vp],
+        "hl_ntt_roundtrip": [vp, vp, i64, vp, vp],
+    }
+    for name, args in sig.items():
+        f = getattr(L, name)
+        f.argtypes = args
+        f.restype = ctypes.c_int
+    _lib = L
+    return L
+
+
+def _check(rc: int):
+    if rc != HL_OK:
+        raise HLError(rc, _lib.hl_last_error().decode())
+
+
+def _tile(t) -> Tile:
+    return t if isinstance(t, Tile) else Tile(*[int(v) for v in t])
+
+
+def _hptr(a: np.ndarray, dtype) -> int:
+    assert isinstance(a, np.ndarray) and a.dtype == dtype and a.flags["C_CONTIGUOUS"], (a.dtype, dtype)
+    return a.ctypes.data
+
+
+def _dptr(t) -> int:
+    import torch
+    if not (isinstance(t, torch.Tensor) and t.is_cuda and t.is_contiguous()):
+        raise HLError(HL_EINVAL, "expected a contiguous CUDA tensor")
+    return t.data_ptr()
+
+
+def _stream(stream) -> int:
+    import torch
+    if stream is None:
+        return torch.cuda.current_stream().cuda_stream
+    return stream.cuda_stream if hasattr(stream, "cuda_stream") else int(stream)
+
+
+def _dev_empty(nwords: int, device):
+    import torch
+    return torch.empty(int(nwords), dtype=torch.int64, device=device)
+
+
+class Context:
+    """A BFV-RNS parameter set {N, t = 2^t_bits, q = p_0..p_{L-1}} bound to one CUDA device."""
+
+    def __init__(self, N: int = 4096, L: int = 2, t_bits: int = 37, primes=None, device: int = 0):
+        lib = load_library()
+        self.N, self.L, self.t_bits, self.device = int(N), int(L), int(t_bits), int(device)
+        h = ctypes.c_void_p()
+        pr = None
+        if primes is not None:
+            pr = np.ascontiguousarray(np.array(primes, dtype=np.uint64))
+        _check(lib.hl_ctx_create(self.N, self.L, self.t_bits, pr.ctypes.data if pr is not None else None,
+                                 self.device, ctypes.byref(h)))
+        self._h = h
+        p = np.zeros(self.L, np.uint64)
+        d = np.zeros(self.L, np.uint64)
+        _check(lib.hl_ctx_params(h, p.ctypes.data, d.ctypes.data))
+        self.primes = tuple(int(v) for v in p)
+        self.delta_mod = tuple(int(v) for v in d)
+
+    def close(self):
+        if getattr(self, "_h", None):
+            _lib.hl_ctx_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    @property
+    def device_str(self) -> str:
+        return f"cuda:{self.device}"
+
+    def layout(self, tile, Ma: int, R: int, Nb: int, i_begin: int = 0, i_end: int = -1) -> Layout:
+        out = _Layout()
+        _check(_lib.hl_layout_query(self._h, _tile(tile), Ma, R, Nb, i_begin, i_end, ctypes.byref(out)))
+        return Layout(*[getattr(out, f) for f, _ in _Layout._fields_])
+
+    # ---------------------------------------------------------------- client (host memory)
+    def keygen(self, seed: int) -> np.ndarray:
+        sk = np.zeros(self.N, dtype=np.int8)
+        _check(_lib.hl_keygen(self._h, seed, sk.ctypes.data))
+        return sk
+
+    def encrypt(self, sk: np.ndarray, tile, X: np.ndarray, seed: int) -> np.ndarray:
+        X = np.ascontiguousarray(X, dtype=np.uint64)
+        Nb, R = X.shape
+        lay = self.layout(tile, 1, R, Nb)
+        ct = np.zeros((lay.nJ, lay.nK, 2, self.L, self.N), dtype=np.uint64)
+        _check(_lib.hl_encrypt(self._h, _hptr(np.ascontiguousarray(sk), np.int8), _tile(tile), X.ctypes.data,
+                               Nb, R, seed, ct.ctypes.data))
+        return ct
+
+    def decrypt_share(self, sk: np.ndarray, tile, ct_masked: np.ndarray, Ma: int, Nb: int,
+                      compress: bool = True) -> np.ndarray:
+        ct_masked = np.ascontiguousarray(ct_masked, dtype=np.uint64)
+        lay = self.layout(tile, Ma, 1, Nb)
+        need = lay.ct_masked_words if compress else lay.ct_full_words
+        if ct_masked.size != need:
+            raise HLError(HL_EINVAL, f"ct_masked has {ct_masked.size} words, expected {need}")
+        out = np.zeros((Nb, Ma), dtype=np.uint64)
+        _check(_lib.hl_decrypt_share(self._h, _hptr(np.ascontiguousarray(sk), np.int8), _tile(tile),
+                                     ct_masked.ctypes.data, int(bool(compress)), Ma, Nb, out.ctypes.data))
+        return out
+
+    # ---------------------------------------------------------------- server (device memory)
+    def encode_weights(self, tile, W, i_begin: int = 0, i_end: int = -1, wcache=None, stream=None):
+        """W: CUDA tensor [R][Ma] (int64/uint64 bits).  Returns the opaque NTT-domain cache."""
+        R, Ma = W.shape
+        lay = self.layout(tile, Ma, R, 1, i_begin, i_end)
+        if wcache is None:
+            wcache = _dev_empty(lay.wcache_bytes // 8, W.device)
+        _check(_lib.hl_encode_weights(self._h, _tile(tile), _dptr(W), R, Ma, i_begin, i_end, _dptr(wcache),
+                                      _stream(stream)))
+        return wcache
+
+    def he_matmul(self, tile, wcache, Ma: int, R: int, Nb: int, ct_in, i_begin: int = 0, i_end: int = -1,
+                  workspace=None, ct_out=None, stream=None):
+        lay = self.layout(tile, Ma, R, Nb, i_begin, i_end)
+        if workspace is None:
+            workspace = _dev_empty(lay.workspace_bytes // 8, ct_in.device)
+        if ct_out is None:
+            ct_out = _dev_empty(lay.ct_out_words, ct_in.device)
+        _check(_lib.hl_he_matmul(self._h, _tile(tile), _dptr(wcache), Ma, R, Nb, i_begin, i_end, _dptr(ct_in),
+                                 _dptr(workspace), _dptr(ct_out), _stream(stream)))
+        return ct_out
+
+    def mask_and_share(self, tile, Ma: int, Nb: int, ct_out, seed: int, compress: bool = True,
+                       i_begin: int = 0, i_end: int = -1, ct_masked=None, share=None, stream=None):
+        lay = self.layout(tile, Ma, 1, Nb, i_begin, i_end)
+        if ct_masked is None:
+            ct_masked = _dev_empty(lay.ct_masked_words if compress else lay.ct_full_words, ct_out.device)
+        if share is None:
+            import torch
+            share = torch.zeros(Nb * Ma, dtype=torch.int64, device=ct_out.device)
+        _check(_lib.hl_mask_and_share(self._h, _tile(tile), Ma, Nb, i_begin, i_end, _dptr(ct_out), seed,
+                                      int(bool(compress)), _dptr(ct_masked), _dptr(share), _stream(stream)))
+        return ct_masked, share
+
+    def he_matmul_share(self, tile, wcache, Ma: int, R: int, Nb: int, ct_in, seed: int, compress: bool = True,
+                        i_begin: int = 0, i_end: int = -1, workspace=None, ct_out_ntt=None, ct_masked=None,
+                        share=None, stream=None):
+        lay = self.layout(tile, Ma, R, Nb, i_begin, i_end)
+        dev = ct_in.device
+        if workspace is None:
+            workspace = _dev_empty(lay.workspace_bytes // 8, dev)
+        if ct_out_ntt is None:
+            ct_out_ntt = _dev_empty(lay.ct_out_words, dev)
+        if ct_masked is None:
+            ct_masked = _dev_empty(lay.ct_masked_words if compress else lay.ct_full_words, dev)
+        if share is None:
+            import torch
+            share = torch.zeros(Nb * Ma, dtype=torch.int64, device=dev)
+        _check(_lib.hl_he_matmul_share(self._h, _tile(tile), _dptr(wcache), Ma, R, Nb, i_begin, i_end,
+                                       _dptr(ct_in), _dptr(workspace), _dptr(ct_out_ntt), seed,
+                                       int(bool(compress)), _dptr(ct_masked), _dptr(share), _stream(stream)))
+        return ct_masked, share
+
+    def he_linear_host(self, tile, wcache, Ma: int, R: int, Nb: int, ct_in_host, seed: int, ct_masked_host,
+                       share_host, dev_ct_in, workspace, dev_ct_out_ntt, dev_ct_masked, dev_share,
+                       compress: bool = True, stream=None):
+        """End-to-end server call on pinned host buffers (torch CPU tensors, pin_memory=True)."""
+        _check(_lib.hl_he_linear_host(self._h, _tile(tile), _dptr(wcache), Ma, R, Nb, ct_in_host.data_ptr(), seed,
+                                      int(bool(compress)), ct_masked_host.data_ptr(), share_host.data_ptr(),
+                                      _dptr(dev_ct_in), _dptr(workspace), _dptr(dev_ct_out_ntt),
+                                      _dptr(dev_ct_masked), _dptr(dev_share), _stream(stream)))
+
+    # ---------------------------------------------------------------- diagnostics
+    def poly_mul(self, a, b, out=None, scratch=None, stream=None):
+        npoly = a.numel() // (self.L * self.N)
+        if out is None:
+            out = _dev_empty(a.numel(), a.device)
+        if scratch is None:
+            scratch = _dev_empty(2 * a.numel(), a.device)
+        _check(_lib.hl_poly_mul(self._h, _dptr(a), _dptr(b), _dptr(out), npoly, _dptr(scratch), _stream(stream)))
+        return out
+
+    def ntt_roundtrip(self, x, scratch=None, stream=None):
+        npoly = x.numel() // (self.L * self.N)
+        if scratch is None:
+            scratch = _dev_empty(x.numel(), x.device)
+        _check(_lib.hl_ntt_roundtrip(self._h, _dptr(x), npoly, _dptr(scratch), _stream(stream)))
+        return x
+
+
+def to_device(a: np.ndarray, device="cuda"):
+    """numpy uint64 -> CUDA int64 tensor with the same bits."""
+    import torch
+    return torch.from_numpy(np.ascontiguousarray(a, dtype=np.uint64).view(np.int64)).to(device)
+
+
+def to_host(t) -> np.ndarray:
+    """CUDA/CPU int64 tensor -> numpy uint64 with the same bits."""
+    return t.detach().cpu().numpy().view(np.uint64)

@@ -1,0 +1,314 @@
+// ctx.cpp -- context, parameters, twiddle tables, layouts and error reporting of libhelinear.
+//
+// Parameters follow PAPER.md:65 (§2.2: BFV-RNS with {N, t, q}, t = 2^l) with the readings of
+// primes = the L largest p < 2^50 with p = 1 mod 2N (C4), Delta = floor(q/t) (C5),
+// discrete Gaussian sigma = 3.2 by a CDT table (C8).  Independent of oracle/.
+#include <cuda_runtime.h>
+#include <quadmath.h>
+
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+
+#include "hl_internal.h"
+
+// ---------------------------------------------------------------------------------------
+// errors
+// ---------------------------------------------------------------------------------------
+static thread_local std::string g_last_error;
+
+void hl_set_error(const std::string &msg) { g_last_error = msg; }
+int hl_fail(int code, const std::string &msg) { g_last_error = msg; return code; }
+int hl_cuda_check(const char *what) {
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return hl_fail(HL_ECUDA, std::string(what) + ": " + cudaGetErrorString(e));
+  return HL_OK;
+}
+
+extern "C" const char *hl_last_error(void) { return g_last_error.c_str(); }
+
+// ---------------------------------------------------------------------------------------
+// primes (reading C4) and roots
+// ---------------------------------------------------------------------------------------
+static bool is_prime_u64(uint64_t n) {
+  if (n < 2) return false;
+  static const uint64_t bases[] = {2, 3, 5, 7, 11, 13, 17, 19, 23, 29, 31, 37};
+  for (uint64_t b : bases) if (n % b == 0) return n == b;
+  uint64_t d = n - 1; int s = 0;
+  while (!(d & 1)) { d >>= 1; s++; }
+  for (uint64_t a : bases) {      // deterministic for n < 3.3e24 with these 12 bases
+    uint64_t x = h_powmod(a, d, n);
+    if (x == 1 || x == n - 1) continue;
+    bool comp = true;
+    for (int i = 1; i < s; i++) { x = h_mulmod(x, x, n); if (x == n - 1) { comp = false; break; } }
+    if (comp) return false;
+  }
+  return true;
+}
+
+// psi with psi^N = -1 (a primitive 2N-th root of unity since 2N is a power of two)
+static uint64_t find_psi(uint64_t p, uint32_t N) {
+  for (uint64_t x = 2; x < 1000000; x++) {
+    uint64_t psi = h_powmod(x, (p - 1) / (2ull * N), p);
+    if (h_powmod(psi, N, p) == p - 1) return psi;
+  }
+  return 0;
+}
+
+static uint32_t bitrev(uint32_t x, int bits) {
+  uint32_t r = 0;
+  for (int i = 0; i < bits; i++) { r = (r << 1) | (x & 1); x >>= 1; }
+  return r;
+}
+
+// ---------------------------------------------------------------------------------------
+// small unsigned big integers (4 x u64, little endian) for q, q/p_l
+// ---------------------------------------------------------------------------------------
+static void big_mul_u64(uint64_t *a, uint64_t m) {   // a *= m (a has 4 limbs, no overflow)
+  hl_u128 c = 0;
+  for (int i = 0; i < 4; i++) { c += (hl_u128)a[i] * m; a[i] = (uint64_t)c; c >>= 64; }
+}
+static uint64_t big_mod_u64(const uint64_t *a, uint64_t m) {
+  hl_u128 r = 0;
+  for (int i = 3; i >= 0; i--) r = ((r << 64) | a[i]) % m;
+  return (uint64_t)r;
+}
+static void big_div_u64(const uint64_t *a, uint64_t m, uint64_t *q) {
+  hl_u128 r = 0;
+  for (int i = 3; i >= 0; i--) { hl_u128 cur = (r << 64) | a[i]; q[i] = (uint64_t)(cur / m); r = cur % m; }
+}
+static void big_shr(const uint64_t *a, int s, uint64_t *out) {  // s < 64
+  for (int i = 0; i < 4; i++) {
+    uint64_t hi = (i + 1 < 4) ? a[i + 1] : 0;
+    out[i] = s ? ((a[i] >> s) | (hi << (64 - s))) : a[i];
+  }
+}
+static double big_log2(const uint64_t *a) {
+  double v = 0;
+  for (int i = 3; i >= 0; i--) v = v * 18446744073709551616.0 + (double)a[i];
+  return log2(v);
+}
+
+// ---------------------------------------------------------------------------------------
+// discrete Gaussian CDT (reading C8): T[k] = floor(2^63 * P(|E| <= k)), sigma = 3.2, |E| <= 41
+// ---------------------------------------------------------------------------------------
+static void build_cdt(std::vector<uint64_t> &T) {
+  const int tail = 41;
+  __float128 sigma = strtoflt128("3.2", nullptr), two_s2 = 2 * sigma * sigma;
+  __float128 rho[tail + 1], Z = 0;
+  for (int k = 0; k <= tail; k++) { rho[k] = expq(-(__float128)(k * k) / two_s2); Z += (k ? 2 : 1) * rho[k]; }
+  T.assign(tail + 1, 0);
+  __float128 acc = 0, two63 = ldexpq((__float128)1, 63);
+  for (int k = 0; k <= tail; k++) {
+    acc += (k ? 2 : 1) * rho[k];
+    T[k] = (uint64_t)floorq(two63 * acc / Z);
+  }
+  T[tail] = 1ull << 63;
+}
+
+// ---------------------------------------------------------------------------------------
+// context
+// ---------------------------------------------------------------------------------------
+extern "C" int hl_ctx_create(uint32_t N, uint32_t L, uint32_t log2_t, const uint64_t *primes,
+                             int device, hl_ctx **out) {
+  if (!out) return hl_fail(HL_EINVAL, "hl_ctx_create: out is NULL");
+  *out = nullptr;
+  if (N != 4096 && N != 8192) return hl_fail(HL_ENOTSUP, "hl_ctx_create: N must be 4096 or 8192");
+  if (L < 1 || L > HL_MAX_L) return hl_fail(HL_ENOTSUP, "hl_ctx_create: 1 <= L <= 3 required");
+  if (log2_t < 1 || log2_t > 62) return hl_fail(HL_ENOTSUP, "hl_ctx_create: 1 <= log2_t <= 62 required");
+  hl_ctx *c = new hl_ctx();
+  c->N = N; c->L = L; c->log2_t = log2_t; c->device = device;
+  int logN = 0; while ((1u << logN) < N) logN++;
+  if (primes) {
+    for (uint32_t l = 0; l < L; l++) {
+      uint64_t p = primes[l];
+      if (p <= (1ull << 49) || p >= (1ull << 50) || (p - 1) % (2ull * N) != 0 || !is_prime_u64(p)) {
+        delete c;
+        return hl_fail(HL_ENOTSUP, "hl_ctx_create: primes must be primes in (2^49, 2^50) with p = 1 mod 2N");
+      }
+      for (uint32_t k = 0; k < l; k++)
+        if (primes[k] == p) { delete c; return hl_fail(HL_EINVAL, "hl_ctx_create: primes must be distinct"); }
+      c->primes.push_back(p);
+    }
+  } else {
+    uint64_t step = 2ull * N, p = ((1ull << 50) - 1) / step * step + 1;
+    while (c->primes.size() < L) { if (is_prime_u64(p)) c->primes.push_back(p); p -= step; }
+  }
+  // q, Delta = floor(q / t), Delta mod p_l, q / p_l, (q / p_l)^-1 mod p_l, r_t = q mod t
+  uint64_t q[4] = {1, 0, 0, 0};
+  for (uint64_t p : c->primes) big_mul_u64(q, p);
+  memcpy(c->q_limbs, q, sizeof(q));
+  big_shr(q, 1, c->half_q_limbs);
+  uint64_t delta[4];
+  {
+    // Delta = q >> log2_t
+    uint64_t tmp[4];
+    int s = (int)log2_t;
+    memcpy(tmp, q, sizeof(tmp));
+    while (s >= 63) { big_shr(tmp, 63, delta); memcpy(tmp, delta, sizeof(tmp)); s -= 63; }
+    big_shr(tmp, s, delta);
+  }
+  c->r_t = q[0] & ((1ull << log2_t) - 1);
+  c->log2_delta = big_log2(delta);
+  for (uint32_t l = 0; l < L; l++) {
+    uint64_t p = c->primes[l];
+    c->delta_mod.push_back(big_mod_u64(delta, p));
+    big_div_u64(q, p, c->Ml_limbs[l]);
+    c->Ml_inv[l] = h_powmod(big_mod_u64(c->Ml_limbs[l], p), p - 2, p);
+  }
+  // roots and twiddles: tw_fwd[i] = psi^bitrev(i), tw_inv[i] = psi^-bitrev(i)
+  c->h_tw_fwd.resize((size_t)L * N); c->h_tw_fwd_sh.resize((size_t)L * N);
+  c->h_tw_inv.resize((size_t)L * N); c->h_tw_inv_sh.resize((size_t)L * N);
+  std::vector<ulonglong2> tw((size_t)2 * L * N);
+  DevParams &dp = c->dp;
+  dp.N = (int)N; dp.logN = logN; dp.L = (int)L; dp.t_bits = (int)log2_t;
+  for (uint32_t l = 0; l < L; l++) {
+    uint64_t p = c->primes[l];
+    uint64_t psi = find_psi(p, N);
+    if (!psi) { delete c; return hl_fail(HL_ENOTSUP, "hl_ctx_create: no 2N-th root of unity"); }
+    c->psi.push_back(psi);
+    uint64_t psi_inv = h_powmod(psi, p - 2, p);
+    for (uint32_t i = 0; i < N; i++) {
+      uint32_t br = bitrev(i, logN);
+      uint64_t wf = h_powmod(psi, br, p), wi = h_powmod(psi_inv, br, p);
+      size_t o = (size_t)l * N + i;
+      c->h_tw_fwd[o] = wf; c->h_tw_fwd_sh[o] = h_shoup(wf, p);
+      c->h_tw_inv[o] = wi; c->h_tw_inv_sh[o] = h_shoup(wi, p);
+      tw[o] = make_ulonglong2(wf, c->h_tw_fwd_sh[o]);
+      tw[(size_t)L * N + o] = make_ulonglong2(wi, c->h_tw_inv_sh[o]);
+    }
+    PrimeConsts &pc = dp.pc[l];
+    pc.p = p; pc.two_p = 2 * p;
+    pc.mu = (uint64_t)((~(hl_u128)0 >> 64) / p);                 // floor((2^64 - 1) / p) = floor(2^64/p)
+    pc.r64 = (uint64_t)(((hl_u128)1 << 64) % p);
+    pc.r64_sh = h_shoup(pc.r64, p);
+    pc.delta = c->delta_mod[l]; pc.delta_sh = h_shoup(pc.delta, p);
+    pc.ninv = h_powmod(N, p - 2, p); pc.ninv_sh = h_shoup(pc.ninv, p);
+    pc.ninv_w1 = h_mulmod(pc.ninv, c->h_tw_inv[(size_t)l * N + 1], p);
+    pc.ninv_w1_sh = h_shoup(pc.ninv_w1, p);
+  }
+  build_cdt(c->cdt);
+  // device tables (device < 0: host-only context for the client calls; no CUDA needed)
+  if (device < 0) {
+    dp.tw_fwd = dp.tw_inv = nullptr;
+    *out = c;
+    return HL_OK;
+  }
+  if (cudaSetDevice(device) != cudaSuccess) { delete c; return hl_cuda_check("hl_ctx_create: cudaSetDevice"); }
+  size_t bytes = tw.size() * sizeof(ulonglong2);
+  if (cudaMalloc(&c->d_tw, bytes) != cudaSuccess ||
+      cudaMemcpy(c->d_tw, tw.data(), bytes, cudaMemcpyHostToDevice) != cudaSuccess ||
+      cudaMalloc((void **)&c->d_flags, 64) != cudaSuccess) {
+    int rc = hl_cuda_check("hl_ctx_create: device tables");
+    if (c->d_tw) cudaFree(c->d_tw);
+    delete c;
+    return rc ? rc : hl_fail(HL_ECUDA, "hl_ctx_create: device allocation failed");
+  }
+  dp.tw_fwd = (const ulonglong2 *)c->d_tw;
+  dp.tw_inv = (const ulonglong2 *)c->d_tw + (size_t)L * N;
+  *out = c;
+  return HL_OK;
+}
+
+extern "C" int hl_ctx_destroy(hl_ctx *c) {
+  if (!c) return HL_OK;
+  if (c->d_tw) cudaFree(c->d_tw);
+  if (c->d_flags) cudaFree(c->d_flags);
+  delete c;
+  return HL_OK;
+}
+
+extern "C" int hl_ctx_params(const hl_ctx *c, uint64_t *primes_out, uint64_t *delta_mod_out) {
+  if (!c) return hl_fail(HL_EINVAL, "hl_ctx_params: ctx is NULL");
+  for (uint32_t l = 0; l < c->L; l++) {
+    if (primes_out) primes_out[l] = c->primes[l];
+    if (delta_mod_out) delta_mod_out[l] = c->delta_mod[l];
+  }
+  return HL_OK;
+}
+
+int hl_geometry(const hl_ctx *c, hl_tile tile, int64_t Ma, int64_t R, int64_t Nb, int64_t i_begin,
+                int64_t i_end, Geo *g) {
+  if (!c) return hl_fail(HL_EINVAL, "ctx is NULL");
+  if (tile.m <= 0 || tile.r <= 0 || tile.n <= 0 ||
+      (int64_t)tile.m * tile.r * tile.n > (int64_t)c->N)
+    return hl_fail(HL_EDIM, "tile (m, r, n) must be positive with m*r*n <= N");
+  if (Ma <= 0 || R <= 0 || Nb <= 0) return hl_fail(HL_EINVAL, "Ma, R, Nb must be positive");
+  g->m = tile.m; g->r = tile.r; g->n = tile.n;
+  g->nI = (Ma + tile.m - 1) / tile.m;
+  g->nJ = (R + tile.r - 1) / tile.r;
+  g->nK = (Nb + tile.n - 1) / tile.n;
+  if (i_end < 0) i_end = g->nI;
+  if (i_begin < 0 || i_begin >= i_end || i_end > g->nI)
+    return hl_fail(HL_EINVAL, "shard [i_begin, i_end) must be a non-empty sub-range of [0, nI)");
+  g->i_begin = i_begin; g->i_end = i_end; g->nIs = i_end - i_begin;
+  return HL_OK;
+}
+
+extern "C" int hl_layout_query(const hl_ctx *c, hl_tile tile, int64_t Ma, int64_t R, int64_t Nb,
+                               int64_t i_begin, int64_t i_end, hl_layout *out) {
+  Geo g;
+  int rc = hl_geometry(c, tile, Ma, R, Nb, i_begin, i_end, &g);
+  if (rc) return rc;
+  if (!out) return hl_fail(HL_EINVAL, "hl_layout_query: out is NULL");
+  int64_t LN = (int64_t)c->L * c->N;
+  out->nI = g.nI; out->nJ = g.nJ; out->nK = g.nK; out->nI_shard = g.nIs;
+  out->ct_in_words = g.nJ * g.nK * 2 * LN;
+  out->ct_out_words = g.nIs * g.nK * 2 * LN;
+  out->ct_masked_words = g.nIs * g.nK * (int64_t)c->L * ((int64_t)g.m * g.n + c->N);
+  out->ct_full_words = g.nIs * g.nK * 2 * LN;
+  out->share_words = Nb * Ma;
+  out->wcache_bytes = g.nIs * g.nJ * LN * 8;
+  out->workspace_bytes = g.nJ * g.nK * 2 * LN * 8;
+  return HL_OK;
+}
+
+// ---------------------------------------------------------------------------------------
+// host NTT (client side).  Same transform as the device kernels: merged-psi Cooley-Tukey
+// forward (natural -> bit-reversed), Gentleman-Sande inverse (bit-reversed -> natural).
+// ---------------------------------------------------------------------------------------
+static inline uint64_t h_shoup_mul(uint64_t x, uint64_t w, uint64_t wsh, uint64_t p) {
+  uint64_t qq = (uint64_t)(((hl_u128)x * wsh) >> 64);
+  return x * w - qq * p;   // [0, 2p)
+}
+
+void hl_host_ntt_fwd(const hl_ctx *c, int l, uint64_t *a) {
+  const uint32_t N = c->N;
+  const uint64_t p = c->primes[l], p2 = 2 * p;
+  const uint64_t *w = &c->h_tw_fwd[(size_t)l * N], *ws = &c->h_tw_fwd_sh[(size_t)l * N];
+  for (uint32_t m = 1, t = N / 2; m < N; m <<= 1, t >>= 1)
+    for (uint32_t i = 0; i < m; i++) {
+      uint32_t j1 = 2 * i * t;
+      for (uint32_t j = j1; j < j1 + t; j++) {
+        uint64_t X = a[j]; if (X >= p2) X -= p2;
+        uint64_t T = h_shoup_mul(a[j + t], w[m + i], ws[m + i], p);
+        a[j] = X + T; a[j + t] = X - T + p2;
+      }
+    }
+  for (uint32_t j = 0; j < N; j++) { uint64_t x = a[j]; if (x >= p2) x -= p2; if (x >= p) x -= p; a[j] = x; }
+}
+
+void hl_host_ntt_inv(const hl_ctx *c, int l, uint64_t *a) {
+  const uint32_t N = c->N;
+  const uint64_t p = c->primes[l], p2 = 2 * p;
+  const uint64_t *w = &c->h_tw_inv[(size_t)l * N], *ws = &c->h_tw_inv_sh[(size_t)l * N];
+  for (uint32_t m = N, t = 1; m > 1; m >>= 1, t <<= 1) {
+    uint32_t h = m / 2;
+    for (uint32_t i = 0; i < h; i++) {
+      uint32_t j1 = 2 * i * t;
+      for (uint32_t j = j1; j < j1 + t; j++) {
+        uint64_t X = a[j], Y = a[j + t];
+        uint64_t S = X + Y; if (S >= p2) S -= p2;
+        a[j] = S;
+        a[j + t] = h_shoup_mul(X - Y + p2, w[h + i], ws[h + i], p);
+      }
+    }
+  }
+  const PrimeConsts &pc = c->dp.pc[l];
+  for (uint32_t j = 0; j < N; j++) {
+    uint64_t x = h_shoup_mul(a[j], pc.ninv, pc.ninv_sh, p);
+    if (x >= p) x -= p;
+    a[j] = x;
+  }
+}

@@ -1,0 +1,84 @@
+// hl_internal.h -- private declarations of libhelinear (the CUDA path).
+// Nothing here is shared with oracle/ (the CPU oracle is an independent implementation).
+#pragma once
+
+#include <cstdint>
+#include <string>
+#include <vector>
+
+#include <vector_types.h>   // ulonglong2 (CUDA vector type; host-side include only)
+
+#include "../../include/helinear.h"
+
+#define HL_MAX_L 3
+
+typedef unsigned __int128 hl_u128;
+
+// Per-prime constants used by the device kernels (passed by value as kernel parameters).
+struct PrimeConsts {
+  uint64_t p;         // prime, 2^49 < p < 2^50, p = 1 mod 2N
+  uint64_t two_p;     // 2p
+  uint64_t mu;        // floor(2^64 / p)              (Barrett for 64-bit inputs)
+  uint64_t r64;       // 2^64 mod p
+  uint64_t r64_sh;    // floor(r64 * 2^64 / p)        (Shoup companion)
+  uint64_t delta;     // Delta mod p, Delta = floor(q / t)
+  uint64_t delta_sh;  // Shoup companion of delta
+  uint64_t ninv;      // N^-1 mod p
+  uint64_t ninv_sh;
+  uint64_t ninv_w1;   // N^-1 * psi^-bitrev(1) mod p (last inverse stage, folded)
+  uint64_t ninv_w1_sh;
+};
+
+struct DevParams {
+  int N, logN, L, t_bits;
+  PrimeConsts pc[HL_MAX_L];
+  const ulonglong2 *tw_fwd;   // [L][N] {w, w'}: psi^bitrev(i) with Shoup companion
+  const ulonglong2 *tw_inv;   // [L][N] {w, w'}: psi^-bitrev(i)
+};
+
+struct hl_ctx {
+  uint32_t N, L, log2_t;
+  int device;
+  std::vector<uint64_t> primes;
+  std::vector<uint64_t> psi;          // primitive 2N-th roots
+  std::vector<uint64_t> delta_mod;    // Delta mod p_l
+  // big-integer constants for host decryption (little-endian u64 limbs, 4 limbs)
+  uint64_t q_limbs[4];
+  uint64_t half_q_limbs[4];
+  uint64_t Ml_limbs[HL_MAX_L][4];     // q / p_l
+  uint64_t Ml_inv[HL_MAX_L];          // (q / p_l)^-1 mod p_l
+  uint64_t r_t;                       // q mod t  (noise-bound check)
+  double log2_delta;
+  // host twiddles (same tables as the device copy)
+  std::vector<uint64_t> h_tw_fwd, h_tw_fwd_sh, h_tw_inv, h_tw_inv_sh;
+  std::vector<uint64_t> cdt;          // 42 entries, floor(2^63 * P(|E| <= k))
+  DevParams dp;
+  void *d_tw = nullptr;               // device allocation holding tw_fwd + tw_inv
+  uint32_t *d_flags = nullptr;        // device scratch: [0] range flag, [1] max |w| (as u32 bits)
+};
+
+// ---- error handling ------------------------------------------------------------------
+void hl_set_error(const std::string &msg);
+int hl_fail(int code, const std::string &msg);
+int hl_cuda_check(const char *what);
+
+// ---- host modular helpers --------------------------------------------------------------
+static inline uint64_t h_mulmod(uint64_t a, uint64_t b, uint64_t p) { return (uint64_t)(((hl_u128)a * b) % p); }
+static inline uint64_t h_powmod(uint64_t b, uint64_t e, uint64_t p) {
+  uint64_t r = 1 % p; b %= p;
+  while (e) { if (e & 1) r = h_mulmod(r, b, p); b = h_mulmod(b, b, p); e >>= 1; }
+  return r;
+}
+static inline uint64_t h_shoup(uint64_t w, uint64_t p) { return (uint64_t)(((hl_u128)w << 64) / p); }
+
+// tile geometry
+struct Geo {
+  int64_t nI, nJ, nK, nIs, i_begin, i_end;
+  int m, r, n;
+};
+int hl_geometry(const hl_ctx *ctx, hl_tile tile, int64_t Ma, int64_t R, int64_t Nb, int64_t i_begin,
+                int64_t i_end, Geo *g);
+
+// host NTT (client side): natural-order in, bit-reversed out / inverse, canonical outputs
+void hl_host_ntt_fwd(const hl_ctx *ctx, int l, uint64_t *a);
+void hl_host_ntt_inv(const hl_ctx *ctx, int l, uint64_t *a);

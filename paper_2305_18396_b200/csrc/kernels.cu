@@ -1,0 +1,799 @@
+// kernels.cu -- sm_100a kernels and device entry points of libhelinear.
+//
+// The server path of Alg. 1 with the GPU cipher-plain multiply of
+// PAPER.md:155-156 ("Multiplication of polynomials is done by NTT and elementwise
+// multiplication"), redesigned for B200 integer pipes:
+//
+//   encode_weights : pi_A scatter + centered lift + forward NTT  -> wcache (25-bit limb pairs)
+//   he_matmul      : forward NTT of ct_in -> slot-parallel modular MAC over J -> inverse NTT
+//   mask_and_share : ChaCha20 mask, c0 -= Delta*sigma, drop unused c0, shares
+//   he_matmul_share: the inverse NTT fused with the masking/compression epilogue
+//
+// NTT: negacyclic, merged-psi Cooley-Tukey forward / Gentleman-Sande inverse (Harvey lazy
+// butterflies, values in [0, 4p) / [0, 2p), 64-bit Shoup twiddle products).  One CTA per
+// polynomial, N/16 threads holding 16 coefficients each; radix-16 rounds in registers with
+// padded shared-memory transposes between rounds.  NTT-domain slot order is internal:
+// slot P(idx) = (idx & 15) * (N/16) + (idx >> 4) of the bit-reversed CT output index, which
+// makes both the last forward round and the first inverse round fully coalesced.
+//
+// MAC: per (prime, slot) a small GEMM out[I][col] = sum_J W[I][J] * X[J][col] mod p.
+// Operands are stored as 25-bit limb pairs (x = x0 + 2^25 x1); each modular MAC costs three
+// IMAD.WIDE.U32 (Karatsuba: x0*y0, x1*y1, (x0+x1)(y0+y1)) into three exact 64-bit lazy
+// accumulators; one 128-bit reduction per output.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdio>
+#include <initializer_list>
+#include <string>
+
+#include "chacha.h"
+#include "hl_internal.h"
+
+namespace {
+
+constexpr uint32_t kLimbBits = 25;
+constexpr uint32_t kLimbMask = (1u << kLimbBits) - 1;
+constexpr int kMacJChunk = 4096;   // (2^26)^2 * 4096 = 2^64: exact 64-bit lazy accumulation bound
+
+// ---------------------------------------------------------------------------------------
+// modular helpers
+// ---------------------------------------------------------------------------------------
+__device__ __forceinline__ uint64_t shoup_mul(uint64_t x, uint64_t w, uint64_t wsh, uint64_t p) {
+  const uint64_t q = __umul64hi(x, wsh);
+  return x * w - q * p;   // in [0, 2p) for any x < 2^64
+}
+
+__device__ __forceinline__ void ct_bfly(uint64_t &X, uint64_t &Y, ulonglong2 w, uint64_t p, uint64_t p2) {
+  uint64_t x = X >= p2 ? X - p2 : X;          // [0, 2p)
+  uint64_t t = shoup_mul(Y, w.x, w.y, p);     // [0, 2p)
+  X = x + t;                                  // [0, 4p)
+  Y = x - t + p2;                             // (0, 4p)
+}
+
+__device__ __forceinline__ void gs_bfly(uint64_t &X, uint64_t &Y, ulonglong2 w, uint64_t p, uint64_t p2) {
+  uint64_t s = X + Y;
+  s = s >= p2 ? s - p2 : s;                   // [0, 2p)
+  Y = shoup_mul(X - Y + p2, w.x, w.y, p);     // [0, 2p)
+  X = s;
+}
+
+__device__ __forceinline__ uint64_t canon4(uint64_t x, uint64_t p, uint64_t p2) {   // [0,4p) -> [0,p)
+  x = x >= p2 ? x - p2 : x;
+  return x >= p ? x - p : x;
+}
+
+__device__ __forceinline__ PrimeConsts pick(const DevParams &P, int l) {
+  PrimeConsts c = P.pc[0];
+  if (l == 1) c = P.pc[1];
+  if (l == 2) c = P.pc[2];
+  return c;
+}
+
+// ---------------------------------------------------------------------------------------
+// NTT round geometry.  Rounds cover the stages [S0, S0+K) of the log2(N) CT stages; round 0
+// is the short one when log2(N) is not a multiple of 4.  A thread holds G = 16 >> K groups of
+// 2^K coefficients; the coefficient (g, u) of thread t has bit-reversed-order index idx.
+// ---------------------------------------------------------------------------------------
+template <int LOGN>
+struct Geom {
+  static constexpr int N = 1 << LOGN;
+  static constexpr int NT = N / 16;
+  static constexpr int K0 = (LOGN % 4) ? (LOGN % 4) : 4;
+  static constexpr int NR = (LOGN - K0) / 4 + 1;
+  static constexpr int SMEM_WORDS = N + N / 16;
+  __host__ __device__ static constexpr int s0(int r) { return r == 0 ? 0 : K0 + 4 * (r - 1); }
+  __host__ __device__ static constexpr int k(int r) { return r == 0 ? K0 : 4; }
+  __host__ __device__ static constexpr int lo(int r) { return LOGN - s0(r) - k(r); }
+};
+
+template <int LOGN, int R>
+__device__ __forceinline__ int elem_idx(int t, int g, int u) {
+  using Gm = Geom<LOGN>;
+  constexpr int K = Gm::k(R), LO = Gm::lo(R);
+  const int gid = t + g * Gm::NT;
+  return ((gid >> LO) << (LO + K)) | (u << LO) | (gid & ((1 << LO) - 1));
+}
+
+__device__ __forceinline__ int pad_idx(int idx) { return idx + (idx >> 4); }
+
+template <int LOGN, int R>
+__device__ __forceinline__ void to_smem(const uint64_t (&a)[16], uint64_t *sm, int t) {
+  constexpr int K = Geom<LOGN>::k(R), G = 16 >> K;
+#pragma unroll
+  for (int g = 0; g < G; g++)
+#pragma unroll
+    for (int u = 0; u < (1 << K); u++) sm[pad_idx(elem_idx<LOGN, R>(t, g, u))] = a[g * (1 << K) + u];
+}
+
+template <int LOGN, int R>
+__device__ __forceinline__ void from_smem(uint64_t (&a)[16], const uint64_t *sm, int t) {
+  constexpr int K = Geom<LOGN>::k(R), G = 16 >> K;
+#pragma unroll
+  for (int g = 0; g < G; g++)
+#pragma unroll
+    for (int u = 0; u < (1 << K); u++) a[g * (1 << K) + u] = sm[pad_idx(elem_idx<LOGN, R>(t, g, u))];
+}
+
+// Forward CT stages of round R.  Twiddle of a pair whose lower index is idx at stage st:
+// psi^bitrev((1<<st) + (idx >> (LOGN - st))); within a round that is
+// (1<<st) + (gid_high << ls) + (u >> (K - ls)).
+template <int LOGN, int R>
+__device__ __forceinline__ void fwd_round(uint64_t (&a)[16], int t, const ulonglong2 *tw, uint64_t p, uint64_t p2) {
+  using Gm = Geom<LOGN>;
+  constexpr int S0 = Gm::s0(R), K = Gm::k(R), LO = Gm::lo(R), G = 16 >> K;
+#pragma unroll
+  for (int ls = 0; ls < K; ls++) {
+    const int st = S0 + ls;
+    const int half = 1 << (K - 1 - ls);
+#pragma unroll
+    for (int g = 0; g < G; g++) {
+      const int gid_high = (t + g * Gm::NT) >> LO;
+#pragma unroll
+      for (int u = 0; u < (1 << K); u++) {
+        if (u & half) continue;
+        const ulonglong2 w = __ldg(&tw[(1 << st) + (gid_high << ls) + (u >> (K - ls))]);
+        ct_bfly(a[g * (1 << K) + u], a[g * (1 << K) + u + half], w, p, p2);
+      }
+    }
+  }
+}
+
+// Inverse GS stages of round R (stages descending); N^-1 is folded into stage 0.
+template <int LOGN, int R>
+__device__ __forceinline__ void inv_round(uint64_t (&a)[16], int t, const ulonglong2 *tw, const PrimeConsts &pc) {
+  using Gm = Geom<LOGN>;
+  constexpr int S0 = Gm::s0(R), K = Gm::k(R), LO = Gm::lo(R), G = 16 >> K;
+  const uint64_t p = pc.p, p2 = pc.two_p;
+#pragma unroll
+  for (int ls = K - 1; ls >= 0; ls--) {
+    const int st = S0 + ls;
+    const int half = 1 << (K - 1 - ls);
+#pragma unroll
+    for (int g = 0; g < G; g++) {
+      const int gid_high = (t + g * Gm::NT) >> LO;
+#pragma unroll
+      for (int u = 0; u < (1 << K); u++) {
+        if (u & half) continue;
+        uint64_t &X = a[g * (1 << K) + u], &Y = a[g * (1 << K) + u + half];
+        if (st == 0) {
+          // last stage: (X, Y) -> ((X+Y) N^-1, (X-Y) psi^-bitrev(1) N^-1)
+          const uint64_t s = X + Y, d = X - Y + p2;
+          X = shoup_mul(s, pc.ninv, pc.ninv_sh, p);
+          Y = shoup_mul(d, pc.ninv_w1, pc.ninv_w1_sh, p);
+        } else {
+          const ulonglong2 w = __ldg(&tw[(1 << st) + (gid_high << ls) + (u >> (K - ls))]);
+          gs_bfly(X, Y, w, p, p2);
+        }
+      }
+    }
+  }
+}
+
+template <int LOGN, int R>
+__device__ __forceinline__ void fwd_rounds_from(uint64_t (&a)[16], uint64_t *sm, int t, const ulonglong2 *tw,
+                                                uint64_t p, uint64_t p2) {
+  if constexpr (R < Geom<LOGN>::NR) {
+    if constexpr (R > 0) {
+      to_smem<LOGN, R - 1>(a, sm, t);
+      __syncthreads();
+      from_smem<LOGN, R>(a, sm, t);
+      __syncthreads();
+    }
+    fwd_round<LOGN, R>(a, t, tw, p, p2);
+    fwd_rounds_from<LOGN, R + 1>(a, sm, t, tw, p, p2);
+  }
+}
+
+template <int LOGN, int R>
+__device__ __forceinline__ void inv_rounds_from(uint64_t (&a)[16], uint64_t *sm, int t, const ulonglong2 *tw,
+                                                const PrimeConsts &pc) {
+  if constexpr (R >= 0) {
+    if constexpr (R < Geom<LOGN>::NR - 1) {
+      to_smem<LOGN, R + 1>(a, sm, t);
+      __syncthreads();
+      from_smem<LOGN, R>(a, sm, t);
+      __syncthreads();
+    }
+    inv_round<LOGN, R>(a, t, tw, pc);
+    inv_rounds_from<LOGN, R - 1>(a, sm, t, tw, pc);
+  }
+}
+
+// slot position of the bit-reversed CT index held by the last forward round (lo = 0, K = 4)
+template <int LOGN>
+__device__ __forceinline__ int slot_of(int t, int u) { return u * Geom<LOGN>::NT + t; }
+
+// ---------------------------------------------------------------------------------------
+// Forward NTT kernels
+// ---------------------------------------------------------------------------------------
+// (a) ciphertext polynomials: in [npoly][L][N] coefficient form -> out uint2 limbs [npoly][L][N]
+template <int LOGN, bool SPLIT>
+__global__ void __launch_bounds__(Geom<LOGN>::NT)
+k_ntt_fwd(const uint64_t *__restrict__ in, void *__restrict__ out, DevParams P) {
+  using Gm = Geom<LOGN>;
+  extern __shared__ uint64_t sm[];
+  const int t = threadIdx.x, l = blockIdx.y;
+  const size_t base = ((size_t)blockIdx.x * P.L + l) * Gm::N;
+  const PrimeConsts pc = pick(P, l);
+  const ulonglong2 *tw = P.tw_fwd + (size_t)l * Gm::N;
+  uint64_t a[16];
+  constexpr int K = Gm::k(0), G = 16 >> K;
+#pragma unroll
+  for (int g = 0; g < G; g++)
+#pragma unroll
+    for (int u = 0; u < (1 << K); u++) a[g * (1 << K) + u] = __ldcs(in + base + elem_idx<LOGN, 0>(t, g, u));
+  fwd_rounds_from<LOGN, 0>(a, sm, t, tw, pc.p, pc.two_p);
+#pragma unroll
+  for (int u = 0; u < 16; u++) {
+    const uint64_t x = canon4(a[u], pc.p, pc.two_p);
+    if constexpr (SPLIT) {
+      reinterpret_cast<uint2 *>(out)[base + slot_of<LOGN>(t, u)] =
+          make_uint2((uint32_t)x & kLimbMask, (uint32_t)(x >> kLimbBits));
+    } else {
+      reinterpret_cast<uint64_t *>(out)[base + slot_of<LOGN>(t, u)] = x;
+    }
+  }
+}
+
+// (b) weights: pi_A of tile (I, J), centered lift (reading C6), mod p_l, NTT.
+//     poly index = I_loc * nJ + J; wcache uint2 [nIs][nJ][L][N].
+struct EncodeArgs {
+  const uint64_t *W;
+  int64_t R, Ma, nJ, i_begin;
+  int m, r;
+};
+
+template <int LOGN>
+__global__ void __launch_bounds__(Geom<LOGN>::NT)
+k_encode_weights(EncodeArgs A, uint2 *__restrict__ wcache, DevParams P, uint32_t *flags) {
+  using Gm = Geom<LOGN>;
+  extern __shared__ uint64_t sm[];
+  const int t = threadIdx.x, l = blockIdx.y;
+  const int64_t poly = blockIdx.x, Iloc = poly / A.nJ, J = poly % A.nJ, I = A.i_begin + Iloc;
+  const PrimeConsts pc = pick(P, l);
+  const ulonglong2 *tw = P.tw_fwd + (size_t)l * Gm::N;
+  const uint64_t tmask = (P.t_bits >= 64) ? ~0ull : ((1ull << P.t_bits) - 1);
+  const uint64_t half = 1ull << (P.t_bits - 1);
+  const int mr = A.m * A.r;
+  uint64_t a[16];
+  uint32_t maxabs = 0, bad = 0;
+  constexpr int K = Gm::k(0), G = 16 >> K;
+#pragma unroll
+  for (int g = 0; g < G; g++)
+#pragma unroll
+    for (int u = 0; u < (1 << K); u++) {
+      const int e = elem_idx<LOGN, 0>(t, g, u);
+      uint64_t v = 0;
+      if (e < mr) {
+        const int i = e / A.r, j = A.r - 1 - e % A.r;
+        const int64_t row = J * A.r + j, col = I * A.m + i;
+        if (row < A.R && col < A.Ma) {
+          const uint64_t w = A.W[row * A.Ma + col];
+          bad |= (w & ~tmask) != 0;
+          const uint64_t wm = w & tmask;
+          if (wm < half) {                      // lift(w) = w
+            v = wm % pc.p;
+            maxabs = max(maxabs, (uint32_t)min(wm, (uint64_t)0xffffffffu));
+          } else {                              // lift(w) = w - t  (negative)
+            const uint64_t mag = (tmask - wm) + 1;
+            const uint64_t mm = mag % pc.p;
+            v = mm ? pc.p - mm : 0;
+            maxabs = max(maxabs, (uint32_t)min(mag, (uint64_t)0xffffffffu));
+          }
+        }
+      }
+      a[g * (1 << K) + u] = v;
+    }
+  if (l == 0) {
+    if (bad) atomicOr(&flags[0], 1u);
+    if (maxabs) atomicMax(&flags[1], maxabs);
+  }
+  fwd_rounds_from<LOGN, 0>(a, sm, t, tw, pc.p, pc.two_p);
+  const size_t base = ((size_t)poly * P.L + l) * Gm::N;
+#pragma unroll
+  for (int u = 0; u < 16; u++) {
+    const uint64_t x = canon4(a[u], pc.p, pc.two_p);
+    wcache[base + slot_of<LOGN>(t, u)] = make_uint2((uint32_t)x & kLimbMask, (uint32_t)(x >> kLimbBits));
+  }
+}
+
+// ---------------------------------------------------------------------------------------
+// Inverse NTT kernel: in u64 [npoly][L][N] (NTT domain, slot order) -> out [npoly][L][N]
+// coefficient form, canonical.  in may alias out.
+// ---------------------------------------------------------------------------------------
+template <int LOGN>
+__device__ __forceinline__ void load_ntt_domain(uint64_t (&a)[16], const uint64_t *src, int t) {
+#pragma unroll
+  for (int u = 0; u < 16; u++) a[u] = __ldcs(src + slot_of<LOGN>(t, u));
+}
+
+template <int LOGN>
+__global__ void __launch_bounds__(Geom<LOGN>::NT)
+k_ntt_inv(const uint64_t *in, uint64_t *out, DevParams P) {
+  using Gm = Geom<LOGN>;
+  extern __shared__ uint64_t sm[];
+  const int t = threadIdx.x, l = blockIdx.y;
+  const size_t base = ((size_t)blockIdx.x * P.L + l) * Gm::N;
+  const PrimeConsts pc = pick(P, l);
+  const ulonglong2 *tw = P.tw_inv + (size_t)l * Gm::N;
+  uint64_t a[16];
+  load_ntt_domain<LOGN>(a, in + base, t);
+  inv_rounds_from<LOGN, Gm::NR - 1>(a, sm, t, tw, pc);
+  constexpr int K = Gm::k(0), G = 16 >> K;
+#pragma unroll
+  for (int g = 0; g < G; g++)
+#pragma unroll
+    for (int u = 0; u < (1 << K); u++) {
+      uint64_t x = a[g * (1 << K) + u];
+      x = x >= pc.p ? x - pc.p : x;
+      out[base + elem_idx<LOGN, 0>(t, g, u)] = x;
+    }
+}
+
+// ---------------------------------------------------------------------------------------
+// Fused inverse NTT + mask + compression + server share (compressed mode only).
+// One CTA per (output ct o = I_loc*nK + K, component c); loops over the L primes.
+//   c = 1: c1 copied to the compressed response
+//   c = 0: sigma at the kept positions (ChaCha20, once for all primes), c0 - Delta_l*sigma
+//          written at index k*m+i; share_server[K*n+k][I*m+i] = sigma (in-range only).
+// ---------------------------------------------------------------------------------------
+struct MaskArgs {
+  int64_t Ma, Nb, nK, i_begin;
+  int m, r, n;
+  uint64_t seed;
+};
+
+template <int LOGN>
+__global__ void __launch_bounds__(Geom<LOGN>::NT)
+k_ntt_inv_mask(const uint64_t *__restrict__ ct_ntt, uint64_t *__restrict__ masked, uint64_t *__restrict__ share,
+               MaskArgs M, DevParams P) {
+  using Gm = Geom<LOGN>;
+  extern __shared__ uint64_t sm[];
+  uint64_t *sig_sm = sm + Gm::SMEM_WORDS;   // sigma at kept positions (index k*m + i)
+  const int t = threadIdx.x;
+  const int c = blockIdx.x & 1;
+  const int64_t o = blockIdx.x >> 1;                  // I_loc * nK + K
+  const int64_t Iloc = o / M.nK, K = o % M.nK, I = M.i_begin + Iloc;
+  const int mn = M.m * M.n, mr = M.m * M.r;
+  const int L = P.L;
+  const uint64_t tmask = (P.t_bits >= 64) ? ~0ull : ((1ull << P.t_bits) - 1);
+  const size_t per = (size_t)L * (mn + Gm::N);
+  uint64_t *dst = masked + (size_t)o * per;
+  if (c == 0) {
+    const uint64_t stream = (uint64_t)(I * M.nK + K);
+    for (int kk = t; kk < mn; kk += Gm::NT) {
+      const int k = kk / M.m, i = kk % M.m;
+      const int pos = k * mr + i * M.r + M.r - 1;
+      const uint64_t s = hl::prf_u64(M.seed, hl::kDomMask, stream, (uint64_t)pos) & tmask;
+      sig_sm[kk] = s;
+      const int64_t row = K * M.n + k, col = I * M.m + i;
+      if (row < M.Nb && col < M.Ma) share[row * M.Ma + col] = s;
+    }
+    __syncthreads();
+  }
+  for (int l = 0; l < L; l++) {
+    const PrimeConsts pc = pick(P, l);
+    const ulonglong2 *tw = P.tw_inv + (size_t)l * Gm::N;
+    uint64_t a[16];
+    load_ntt_domain<LOGN>(a, ct_ntt + (((size_t)o * 2 + c) * L + l) * Gm::N, t);
+    inv_rounds_from<LOGN, Gm::NR - 1>(a, sm, t, tw, pc);
+    constexpr int K0 = Gm::k(0), G = 16 >> K0;
+#pragma unroll
+    for (int g = 0; g < G; g++)
+#pragma unroll
+      for (int u = 0; u < (1 << K0); u++) {
+        uint64_t x = a[g * (1 << K0) + u];
+        x = x >= pc.p ? x - pc.p : x;
+        const int idx = elem_idx<LOGN, 0>(t, g, u);
+        if (c == 1) {
+          dst[(size_t)L * mn + (size_t)l * Gm::N + idx] = x;
+        } else if (idx < mr * M.n && (idx % M.r) == M.r - 1) {
+          const int k = idx / mr, i = (idx % mr) / M.r;
+          const int kk = k * M.m + i;
+          uint64_t d = shoup_mul(sig_sm[kk], pc.delta, pc.delta_sh, pc.p);
+          d = d >= pc.p ? d - pc.p : d;
+          dst[(size_t)l * mn + kk] = x >= d ? x - d : x + pc.p - d;
+        }
+      }
+    __syncthreads();   // smem reuse by the next prime
+  }
+}
+
+// ---------------------------------------------------------------------------------------
+// Unfused mask_and_share: CTA per output ct, one thread per ChaCha block (8 positions).
+// ---------------------------------------------------------------------------------------
+__global__ void k_mask(const uint64_t *__restrict__ ct_out, uint64_t *__restrict__ masked,
+                       uint64_t *__restrict__ share, MaskArgs M, DevParams P, int compress) {
+  const int N = P.N, L = P.L;
+  const int64_t o = blockIdx.y;
+  const int64_t Iloc = o / M.nK, K = o % M.nK, I = M.i_begin + Iloc;
+  const int b = blockIdx.x * blockDim.x + threadIdx.x;      // ChaCha block: positions 8b .. 8b+7
+  if (b >= N / 8) return;
+  const int mn = M.m * M.n, mr = M.m * M.r;
+  const uint64_t tmask = (P.t_bits >= 64) ? ~0ull : ((1ull << P.t_bits) - 1);
+  const size_t per = compress ? (size_t)L * (mn + N) : (size_t)2 * L * N;
+  const uint64_t *src = ct_out + (size_t)o * 2 * L * N;
+  uint64_t *dst = masked + (size_t)o * per;
+  bool any_kept = false;
+#pragma unroll
+  for (int q = 0; q < 8; q++) {
+    const int pos = 8 * b + q;
+    any_kept |= pos < mr * M.n && (pos % M.r) == M.r - 1;
+  }
+  uint64_t sig[8];
+  if (!compress || any_kept) {
+    hl::chacha_block_u64(M.seed, hl::kDomMask, (uint64_t)(I * M.nK + K), (uint32_t)b, sig);
+#pragma unroll
+    for (int q = 0; q < 8; q++) sig[q] &= tmask;
+  }
+  for (int l = 0; l < L; l++) {
+    const PrimeConsts pc = pick(P, l);
+    const uint64_t *c0 = src + (size_t)l * N, *c1 = src + (size_t)(L + l) * N;
+#pragma unroll
+    for (int q = 0; q < 8; q++) {
+      const int pos = 8 * b + q;
+      const bool kept = pos < mr * M.n && (pos % M.r) == M.r - 1;
+      if (!compress || kept) {
+        uint64_t d = shoup_mul(sig[q], pc.delta, pc.delta_sh, pc.p);
+        d = d >= pc.p ? d - pc.p : d;
+        const uint64_t x = c0[pos];
+        const uint64_t y = x >= d ? x - d : x + pc.p - d;
+        if (compress) {
+          const int k = pos / mr, i = (pos % mr) / M.r;
+          dst[(size_t)l * mn + k * M.m + i] = y;
+        } else {
+          dst[(size_t)l * N + pos] = y;
+        }
+      }
+      const uint64_t v1 = c1[pos];
+      if (compress) dst[(size_t)L * mn + (size_t)l * N + pos] = v1;
+      else dst[(size_t)(L + l) * N + pos] = v1;
+    }
+  }
+  if (any_kept) {
+#pragma unroll
+    for (int q = 0; q < 8; q++) {
+      const int pos = 8 * b + q;
+      if (pos < mr * M.n && (pos % M.r) == M.r - 1) {
+        const int k = pos / mr, i = (pos % mr) / M.r;
+        const int64_t row = K * M.n + k, col = I * M.m + i;
+        if (row < M.Nb && col < M.Ma) share[row * M.Ma + col] = sig[q];
+      }
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------------------
+// Slot-parallel modular MAC (the dominant kernel).
+//   W   uint2 [nIs][nJ][LN]     X uint2 [nJ][nC][LN]     out u64 [nIs][nC][LN]
+//   out[I][col][s] (+)= sum_{J in [j0, j1)} W[I][J][s] * X[J][col][s]  mod p_{s / N}
+// Warp = 32 consecutive slots; each thread owns a TI x TC register tile of outputs.  The 8
+// warps of a CTA share the slots (X re-use through L1) and step over (I-tile, C-tile) pairs
+// with the I tile fastest.  W is streamed once (evict-first loads).
+// ---------------------------------------------------------------------------------------
+struct MacArgs {
+  const uint2 *W;
+  const uint2 *X;
+  uint64_t *out;
+  int nI, nJ, nC, j0, j1, LN, N;
+  int accumulate;
+};
+
+__device__ __forceinline__ uint2 ld_stream(const uint2 *p) {
+  uint2 v;
+  asm volatile("ld.global.nc.L1::no_allocate.v2.u32 {%0, %1}, [%2];"
+               : "=r"(v.x), "=r"(v.y) : "l"(p));
+  return v;
+}
+
+template <int TI, int TC>
+__global__ void __launch_bounds__(256)
+k_mac(MacArgs A, DevParams P) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int s = blockIdx.y * 32 + lane;
+  const int nIt = (A.nI + TI - 1) / TI, nCt = (A.nC + TC - 1) / TC;
+  const int tile = blockIdx.x * 8 + warp;
+  if (tile >= nIt * nCt) return;
+  const int I0 = (tile % nIt) * TI, C0 = (tile / nIt) * TC;
+  const size_t LN = (size_t)A.LN;
+
+  uint64_t lo[TI][TC], hi[TI][TC], md[TI][TC];
+#pragma unroll
+  for (int a = 0; a < TI; a++)
+#pragma unroll
+    for (int b = 0; b < TC; b++) lo[a][b] = hi[a][b] = md[a][b] = 0;
+
+  const uint2 *Wp[TI];
+#pragma unroll
+  for (int a = 0; a < TI; a++) {
+    const int I = min(I0 + a, A.nI - 1);       // clamped rows are computed but not stored
+    Wp[a] = A.W + ((size_t)I * A.nJ) * LN + s;
+  }
+  const uint2 *Xp[TC];
+#pragma unroll
+  for (int b = 0; b < TC; b++) {
+    const int C = min(C0 + b, A.nC - 1);
+    Xp[b] = A.X + (size_t)C * LN + s;
+  }
+  const size_t xstride = (size_t)A.nC * LN;
+
+#pragma unroll 2
+  for (int J = A.j0; J < A.j1; J++) {
+    uint2 w[TI], x[TC];
+#pragma unroll
+    for (int a = 0; a < TI; a++) w[a] = ld_stream(Wp[a] + (size_t)J * LN);
+#pragma unroll
+    for (int b = 0; b < TC; b++) x[b] = __ldg(Xp[b] + (size_t)J * xstride);
+    uint32_t xs[TC];
+#pragma unroll
+    for (int b = 0; b < TC; b++) xs[b] = x[b].x + x[b].y;
+#pragma unroll
+    for (int a = 0; a < TI; a++) {
+      const uint32_t ws = w[a].x + w[a].y;
+#pragma unroll
+      for (int b = 0; b < TC; b++) {
+        lo[a][b] += (uint64_t)w[a].x * x[b].x;
+        hi[a][b] += (uint64_t)w[a].y * x[b].y;
+        md[a][b] += (uint64_t)ws * xs[b];
+      }
+    }
+  }
+
+  const int l = s / A.N;
+  const PrimeConsts pc = pick(P, l);
+#pragma unroll
+  for (int a = 0; a < TI; a++) {
+    if (I0 + a >= A.nI) continue;
+#pragma unroll
+    for (int b = 0; b < TC; b++) {
+      if (C0 + b >= A.nC) continue;
+      const uint64_t mid = md[a][b] - lo[a][b] - hi[a][b];     // exact: x0 y1 + x1 y0
+      // V = hi 2^50 + mid 2^25 + lo  (< 2^113)
+      const hl_u128 V = ((hl_u128)hi[a][b] << (2 * kLimbBits)) + ((hl_u128)mid << kLimbBits) + lo[a][b];
+      const uint64_t vh = (uint64_t)(V >> 64), vl = (uint64_t)V;
+      const uint64_t r1 = shoup_mul(vh, pc.r64, pc.r64_sh, pc.p);           // vh 2^64 mod p, [0, 2p)
+      const uint64_t r2 = vl - __umul64hi(vl, pc.mu) * pc.p;                // vl mod p, [0, 2p)
+      uint64_t r = r1 + r2;
+      r = r >= pc.two_p ? r - pc.two_p : r;
+      r = r >= pc.p ? r - pc.p : r;
+      uint64_t *dst = A.out + ((size_t)(I0 + a) * A.nC + C0 + b) * LN + s;
+      if (A.accumulate) {
+        r += *dst;
+        r = r >= pc.p ? r - pc.p : r;
+      }
+      *dst = r;
+    }
+  }
+}
+
+// pointwise product in the NTT domain (diagnostics only)
+__global__ void k_pointwise(const uint64_t *a, const uint64_t *b, uint64_t *out, int64_t n, DevParams P) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const int l = (int)((i / P.N) % P.L);
+  const uint64_t p = pick(P, l).p;
+  out[i] = (uint64_t)(((hl_u128)a[i] * b[i]) % p);
+}
+
+// ---------------------------------------------------------------------------------------
+// launch helpers
+// ---------------------------------------------------------------------------------------
+template <typename Kern>
+void set_smem(Kern k, size_t bytes) {
+  cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+}
+
+template <int LOGN>
+constexpr size_t ntt_smem() { return (size_t)Geom<LOGN>::SMEM_WORDS * 8; }
+
+template <int LOGN, bool SPLIT>
+void launch_fwd(const hl_ctx *c, const uint64_t *in, void *out, int64_t npoly, cudaStream_t st) {
+  static bool init = false;
+  if (!init) { set_smem(k_ntt_fwd<LOGN, SPLIT>, ntt_smem<LOGN>()); init = true; }
+  dim3 grid((unsigned)npoly, c->L);
+  k_ntt_fwd<LOGN, SPLIT><<<grid, Geom<LOGN>::NT, ntt_smem<LOGN>(), st>>>(in, out, c->dp);
+}
+
+template <int LOGN>
+void launch_inv(const hl_ctx *c, const uint64_t *in, uint64_t *out, int64_t npoly, cudaStream_t st) {
+  static bool init = false;
+  if (!init) { set_smem(k_ntt_inv<LOGN>, ntt_smem<LOGN>()); init = true; }
+  dim3 grid((unsigned)npoly, c->L);
+  k_ntt_inv<LOGN><<<grid, Geom<LOGN>::NT, ntt_smem<LOGN>(), st>>>(in, out, c->dp);
+}
+
+void fwd_ntt(const hl_ctx *c, const uint64_t *in, void *out, int64_t npoly, bool split, cudaStream_t st) {
+  if (c->N == 4096) { if (split) launch_fwd<12, true>(c, in, out, npoly, st); else launch_fwd<12, false>(c, in, out, npoly, st); }
+  else { if (split) launch_fwd<13, true>(c, in, out, npoly, st); else launch_fwd<13, false>(c, in, out, npoly, st); }
+}
+
+void inv_ntt(const hl_ctx *c, const uint64_t *in, uint64_t *out, int64_t npoly, cudaStream_t st) {
+  if (c->N == 4096) launch_inv<12>(c, in, out, npoly, st); else launch_inv<13>(c, in, out, npoly, st);
+}
+
+template <int TI, int TC>
+void launch_mac_t(const hl_ctx *c, MacArgs A, cudaStream_t st) {
+  const int nIt = (A.nI + TI - 1) / TI, nCt = (A.nC + TC - 1) / TC;
+  dim3 grid((unsigned)((nIt * nCt + 7) / 8), (unsigned)(A.LN / 32));
+  k_mac<TI, TC><<<grid, 256, 0, st>>>(A, c->dp);
+}
+
+void launch_mac(const hl_ctx *c, const uint2 *W, const uint2 *X, uint64_t *out, int64_t nIs, int64_t nJ,
+                int64_t nC, cudaStream_t st) {
+  MacArgs A;
+  A.W = W; A.X = X; A.out = out;
+  A.nI = (int)nIs; A.nJ = (int)nJ; A.nC = (int)nC;
+  A.LN = (int)(c->L * c->N); A.N = (int)c->N;
+  for (int64_t j0 = 0; j0 < nJ; j0 += kMacJChunk) {
+    A.j0 = (int)j0; A.j1 = (int)std::min<int64_t>(nJ, j0 + kMacJChunk);
+    A.accumulate = j0 > 0;
+    if (nC >= 8) launch_mac_t<2, 8>(c, A, st);
+    else if (nC >= 4) launch_mac_t<4, 4>(c, A, st);
+    else if (nC >= 2) launch_mac_t<8, 2>(c, A, st);
+    else launch_mac_t<8, 1>(c, A, st);
+  }
+}
+
+template <int LOGN>
+void launch_inv_mask(const hl_ctx *c, const uint64_t *ct_ntt, uint64_t *masked, uint64_t *share, MaskArgs M,
+                     int64_t nout, cudaStream_t st) {
+  static bool init = false;
+  if (!init) { set_smem(k_ntt_inv_mask<LOGN>, ntt_smem<LOGN>() + (size_t)Geom<LOGN>::N * 8); init = true; }
+  const size_t smem = ntt_smem<LOGN>() + (size_t)M.m * M.n * 8;
+  k_ntt_inv_mask<LOGN><<<(unsigned)(nout * 2), Geom<LOGN>::NT, smem, st>>>(ct_ntt, masked, share, M, c->dp);
+}
+
+}  // namespace
+
+// =========================================================================================
+// entry points
+// =========================================================================================
+static int check_ptrs(std::initializer_list<const void *> ps, const char *who) {
+  for (const void *p : ps)
+    if (!p) return hl_fail(HL_EINVAL, std::string(who) + ": NULL argument");
+  const hl_ctx *c = (const hl_ctx *)*ps.begin();
+  if (c->device < 0) return hl_fail(HL_EINVAL, std::string(who) + ": host-only context (device < 0)");
+  return HL_OK;
+}
+
+extern "C" int hl_encode_weights(const hl_ctx *c, hl_tile tile, const uint64_t *W, int64_t R, int64_t Ma,
+                                 int64_t i_begin, int64_t i_end, void *wcache, void *stream) {
+  int rc;
+  if ((rc = check_ptrs({c, W, wcache}, "hl_encode_weights"))) return rc;
+  Geo g;
+  if ((rc = hl_geometry(c, tile, Ma, R, 1, i_begin, i_end, &g))) return rc;
+  cudaStream_t st = (cudaStream_t)stream;
+  cudaSetDevice(c->device);
+  cudaMemsetAsync(c->d_flags, 0, 8, st);
+  EncodeArgs A{W, R, Ma, g.nJ, g.i_begin, g.m, g.r};
+  dim3 grid((unsigned)(g.nIs * g.nJ), c->L);
+  if (c->N == 4096) {
+    static bool init = false;
+    if (!init) { set_smem(k_encode_weights<12>, ntt_smem<12>()); init = true; }
+    k_encode_weights<12><<<grid, Geom<12>::NT, ntt_smem<12>(), st>>>(A, (uint2 *)wcache, c->dp, c->d_flags);
+  } else {
+    static bool init = false;
+    if (!init) { set_smem(k_encode_weights<13>, ntt_smem<13>()); init = true; }
+    k_encode_weights<13><<<grid, Geom<13>::NT, ntt_smem<13>(), st>>>(A, (uint2 *)wcache, c->dp, c->d_flags);
+  }
+  if ((rc = hl_cuda_check("hl_encode_weights: launch"))) return rc;
+  uint32_t flags[2];
+  if (cudaMemcpyAsync(flags, c->d_flags, 8, cudaMemcpyDeviceToHost, st) != cudaSuccess ||
+      cudaStreamSynchronize(st) != cudaSuccess)
+    return hl_cuda_check("hl_encode_weights: status readback");
+  if (flags[0]) return hl_fail(HL_ERANGE, "hl_encode_weights: W value >= 2^log2_t");
+  // Appendix C of SURVEY.md: |noise| <= 2R max|w| (r_t + e_max) must stay below Delta/2
+  const double bound = log2(2.0 * (double)R) + log2((double)flags[1] + 1.0) + log2((double)c->r_t + 41.0);
+  if (bound >= c->log2_delta - 1.0)
+    return hl_fail(HL_ENOISE, "hl_encode_weights: worst-case noise bound 2R*max|w|*(r_t+41) >= Delta/2");
+  return HL_OK;
+}
+
+extern "C" int hl_he_matmul(const hl_ctx *c, hl_tile tile, const void *wcache, int64_t Ma, int64_t R, int64_t Nb,
+                            int64_t i_begin, int64_t i_end, const uint64_t *ct_in, void *workspace,
+                            uint64_t *ct_out, void *stream) {
+  int rc;
+  if ((rc = check_ptrs({c, wcache, ct_in, workspace, ct_out}, "hl_he_matmul"))) return rc;
+  Geo g;
+  if ((rc = hl_geometry(c, tile, Ma, R, Nb, i_begin, i_end, &g))) return rc;
+  cudaStream_t st = (cudaStream_t)stream;
+  const int64_t nC = 2 * g.nK;
+  fwd_ntt(c, ct_in, workspace, g.nJ * nC, true, st);
+  launch_mac(c, (const uint2 *)wcache, (const uint2 *)workspace, ct_out, g.nIs, g.nJ, nC, st);
+  inv_ntt(c, ct_out, ct_out, g.nIs * nC, st);
+  return hl_cuda_check("hl_he_matmul: launch");
+}
+
+static MaskArgs mask_args(const Geo &g, int64_t Ma, int64_t Nb, uint64_t seed) {
+  MaskArgs M;
+  M.Ma = Ma; M.Nb = Nb; M.nK = g.nK; M.i_begin = g.i_begin;
+  M.m = g.m; M.r = g.r; M.n = g.n; M.seed = seed;
+  return M;
+}
+
+extern "C" int hl_mask_and_share(const hl_ctx *c, hl_tile tile, int64_t Ma, int64_t Nb, int64_t i_begin,
+                                 int64_t i_end, const uint64_t *ct_out, uint64_t seed, int compress,
+                                 uint64_t *ct_masked, uint64_t *share, void *stream) {
+  int rc;
+  if ((rc = check_ptrs({c, ct_out, ct_masked, share}, "hl_mask_and_share"))) return rc;
+  Geo g;
+  if ((rc = hl_geometry(c, tile, Ma, 1, Nb, i_begin, i_end, &g))) return rc;
+  cudaStream_t st = (cudaStream_t)stream;
+  dim3 grid((unsigned)((c->N / 8 + 127) / 128), (unsigned)(g.nIs * g.nK));
+  k_mask<<<grid, 128, 0, st>>>(ct_out, ct_masked, share, mask_args(g, Ma, Nb, seed), c->dp, compress ? 1 : 0);
+  return hl_cuda_check("hl_mask_and_share: launch");
+}
+
+extern "C" int hl_he_matmul_share(const hl_ctx *c, hl_tile tile, const void *wcache, int64_t Ma, int64_t R,
+                                  int64_t Nb, int64_t i_begin, int64_t i_end, const uint64_t *ct_in,
+                                  void *workspace, uint64_t *ct_out_ntt, uint64_t seed, int compress,
+                                  uint64_t *ct_masked, uint64_t *share, void *stream) {
+  int rc;
+  if ((rc = check_ptrs({c, wcache, ct_in, workspace, ct_out_ntt, ct_masked, share}, "hl_he_matmul_share")))
+    return rc;
+  Geo g;
+  if ((rc = hl_geometry(c, tile, Ma, R, Nb, i_begin, i_end, &g))) return rc;
+  if (!compress) {   // full responses: the unfused pair (the mask needs every coefficient)
+    if ((rc = hl_he_matmul(c, tile, wcache, Ma, R, Nb, i_begin, i_end, ct_in, workspace, ct_out_ntt, stream)))
+      return rc;
+    return hl_mask_and_share(c, tile, Ma, Nb, i_begin, i_end, ct_out_ntt, seed, 0, ct_masked, share, stream);
+  }
+  cudaStream_t st = (cudaStream_t)stream;
+  const int64_t nC = 2 * g.nK;
+  fwd_ntt(c, ct_in, workspace, g.nJ * nC, true, st);
+  launch_mac(c, (const uint2 *)wcache, (const uint2 *)workspace, ct_out_ntt, g.nIs, g.nJ, nC, st);
+  MaskArgs M = mask_args(g, Ma, Nb, seed);
+  if (c->N == 4096) launch_inv_mask<12>(c, ct_out_ntt, ct_masked, share, M, g.nIs * g.nK, st);
+  else launch_inv_mask<13>(c, ct_out_ntt, ct_masked, share, M, g.nIs * g.nK, st);
+  return hl_cuda_check("hl_he_matmul_share: launch");
+}
+
+extern "C" int hl_he_linear_host(const hl_ctx *c, hl_tile tile, const void *wcache, int64_t Ma, int64_t R,
+                                 int64_t Nb, const uint64_t *ct_in_host, uint64_t seed, int compress,
+                                 uint64_t *ct_masked_host, uint64_t *share_host, uint64_t *dev_ct_in,
+                                 void *workspace, uint64_t *dev_ct_out_ntt, uint64_t *dev_ct_masked,
+                                 uint64_t *dev_share, void *stream) {
+  int rc;
+  if ((rc = check_ptrs({c, wcache, ct_in_host, ct_masked_host, share_host, dev_ct_in, workspace,
+                        dev_ct_out_ntt, dev_ct_masked, dev_share}, "hl_he_linear_host")))
+    return rc;
+  hl_layout lay;
+  if ((rc = hl_layout_query(c, tile, Ma, R, Nb, 0, -1, &lay))) return rc;
+  cudaStream_t st = (cudaStream_t)stream;
+  if (cudaMemcpyAsync(dev_ct_in, ct_in_host, (size_t)lay.ct_in_words * 8, cudaMemcpyHostToDevice, st) != cudaSuccess)
+    return hl_cuda_check("hl_he_linear_host: H2D");
+  if ((rc = hl_he_matmul_share(c, tile, wcache, Ma, R, Nb, 0, -1, dev_ct_in, workspace, dev_ct_out_ntt, seed,
+                               compress, dev_ct_masked, dev_share, stream)))
+    return rc;
+  const size_t mw = compress ? (size_t)lay.ct_masked_words : (size_t)lay.ct_full_words;
+  if (cudaMemcpyAsync(ct_masked_host, dev_ct_masked, mw * 8, cudaMemcpyDeviceToHost, st) != cudaSuccess ||
+      cudaMemcpyAsync(share_host, dev_share, (size_t)lay.share_words * 8, cudaMemcpyDeviceToHost, st) != cudaSuccess)
+    return hl_cuda_check("hl_he_linear_host: D2H");
+  return HL_OK;
+}
+
+extern "C" int hl_poly_mul(const hl_ctx *c, const uint64_t *a, const uint64_t *b, uint64_t *out, int64_t npoly,
+                           void *scratch, void *stream) {
+  int rc;
+  if ((rc = check_ptrs({c, a, b, out, scratch}, "hl_poly_mul"))) return rc;
+  if (npoly <= 0) return hl_fail(HL_EINVAL, "hl_poly_mul: npoly must be positive");
+  cudaStream_t st = (cudaStream_t)stream;
+  const int64_t n = npoly * c->L * c->N;
+  uint64_t *s1 = (uint64_t *)scratch, *s2 = s1 + n;
+  fwd_ntt(c, a, s1, npoly, false, st);
+  fwd_ntt(c, b, s2, npoly, false, st);
+  k_pointwise<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(s1, s2, s1, n, c->dp);
+  inv_ntt(c, s1, out, npoly, st);
+  return hl_cuda_check("hl_poly_mul: launch");
+}
+
+extern "C" int hl_ntt_roundtrip(const hl_ctx *c, uint64_t *x, int64_t npoly, void *scratch, void *stream) {
+  int rc;
+  if ((rc = check_ptrs({c, x, scratch}, "hl_ntt_roundtrip"))) return rc;
+  if (npoly <= 0) return hl_fail(HL_EINVAL, "hl_ntt_roundtrip: npoly must be positive");
+  cudaStream_t st = (cudaStream_t)stream;
+  fwd_ntt(c, x, scratch, npoly, false, st);
+  inv_ntt(c, (uint64_t *)scratch, x, npoly, st);
+  return hl_cuda_check("hl_ntt_roundtrip: launch");
+}

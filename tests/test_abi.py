@@ -1,0 +1,130 @@
+"""C-ABI library checks that need no GPU (-m "not gpu").
+
+* libhelinear.so loads and exports every function include/helinear.h declares;
+* the library's host-side client (keygen, encrypt, decrypt_share) is bit-exact against the
+  oracle on the same seeds (host-only context, device = -1);
+* parameter derivation, layouts and error codes.
+"""
+import ctypes
+import os
+import re
+
+import numpy as np
+import pytest
+
+import synth
+from oracle import ref
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+@pytest.fixture(scope="module")
+def hl():
+    from paper_2305_18396_b200 import build
+    build.build()
+    import paper_2305_18396_b200 as hl
+    hl.load_library()
+    return hl
+
+
+def _declared_functions():
+    src = open(os.path.join(ROOT, "include", "helinear.h")).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"\b(hl_[a-z_0-9]+)\s*\(", src)))
+
+
+def test_exports_every_declared_symbol(hl):
+    declared = _declared_functions()
+    assert len(declared) >= 14
+    lib = ctypes.CDLL(hl.LIB_PATH)
+    for name in declared:
+        assert hasattr(lib, name), name
+    assert sorted(hl.EXPORTS) == declared
+
+
+@pytest.mark.parametrize("N,L", [(4096, 2), (8192, 3)])
+def test_params_match_oracle(hl, N, L):
+    ctx = hl.Context(N, L, 37, device=-1)
+    P = ref.bfv_params(N, L, 37)
+    assert ctx.primes == P.primes
+    assert ctx.delta_mod == tuple(P.delta_mod)
+
+
+def test_explicit_primes_and_errors(hl):
+    P = ref.bfv_params(4096, 2, 37)
+    ctx = hl.Context(4096, 2, 37, primes=P.primes[::-1], device=-1)
+    assert ctx.primes == P.primes[::-1]
+    with pytest.raises(hl.HLError) as e:
+        hl.Context(2048, 2, 37, device=-1)
+    assert e.value.code == hl.HL_ENOTSUP
+    with pytest.raises(hl.HLError) as e:
+        hl.Context(4096, 2, 37, primes=[P.primes[0] + 2, P.primes[1]], device=-1)
+    assert e.value.code == hl.HL_ENOTSUP
+    with pytest.raises(hl.HLError) as e:
+        hl.Context(4096, 4, 37, device=-1)
+    assert e.value.code == hl.HL_ENOTSUP
+
+
+def test_layout_and_dims(hl):
+    ctx = hl.Context(4096, 2, 37, device=-1)
+    lay = ctx.layout((16, 8, 32), 2304, 768, 128)
+    assert (lay.nI, lay.nJ, lay.nK) == (144, 96, 4)
+    assert lay.ct_in_words == 96 * 4 * 2 * 2 * 4096
+    assert lay.ct_masked_words == 144 * 4 * 2 * (16 * 32 + 4096)
+    assert lay.wcache_bytes == 144 * 96 * 2 * 4096 * 8
+    sh = ctx.layout((16, 8, 32), 2304, 768, 128, 10, 20)
+    assert sh.nI_shard == 10 and sh.wcache_bytes == 10 * 96 * 2 * 4096 * 8
+    with pytest.raises(hl.HLError) as e:
+        ctx.layout((16, 16, 32), 64, 64, 64)          # m*r*n = 8192 > N
+    assert e.value.code == hl.HL_EDIM
+    with pytest.raises(hl.HLError) as e:
+        ctx.layout((16, 8, 32), 64, 64, 64, 3, 9)     # shard beyond nI = 4
+    assert e.value.code == hl.HL_EINVAL
+
+
+def test_keygen_matches_oracle(hl):
+    ctx = hl.Context(4096, 2, 37, device=-1)
+    P = ref.bfv_params(4096, 2, 37)
+    for seed in (0, 7, 2**63 + 5):
+        assert np.array_equal(ctx.keygen(seed), ref.keygen(P, seed))
+
+
+@pytest.mark.parametrize("N,L,shape,tile", [
+    (4096, 2, (8, 64), (16, 32, 8)),
+    (4096, 2, (37, 21), (4, 8, 16)),           # ragged
+    (8192, 3, (16, 40), (32, 16, 16)),
+])
+def test_encrypt_bit_exact_vs_oracle(hl, N, L, shape, tile):
+    ctx = hl.Context(N, L, 37, device=-1)
+    P = ref.bfv_params(N, L, 37)
+    X = synth.activations(101, *shape)
+    sk = ref.keygen(P, 102)
+    assert np.array_equal(ctx.encrypt(sk, tile, X, 103), ref.encrypt(P, tile, sk, X, 103))
+
+
+@pytest.mark.parametrize("compress", [True, False])
+def test_decrypt_share_matches_oracle(hl, compress):
+    ctx = hl.Context(4096, 2, 37, device=-1)
+    P = ref.bfv_params(4096, 2, 37)
+    tile, Nb, R, Ma = (8, 16, 16), 20, 40, 24
+    X, W = synth.activations(111, Nb, R), synth.weights(112, R, Ma)
+    out = ref.matmul_protocol(P, tile, X, W, 113, 114, 115, compress)
+    got = ctx.decrypt_share(out["sk"], tile, out["masked"], Ma, Nb, compress)
+    assert np.array_equal(got, out["share_client"])
+
+
+def test_client_errors(hl):
+    ctx = hl.Context(4096, 2, 37, device=-1)
+    sk = ctx.keygen(1)
+    bad = sk.copy(); bad[5] = 2
+    X = synth.activations(1, 8, 64)
+    with pytest.raises(hl.HLError) as e:
+        ctx.encrypt(bad, (16, 32, 8), X, 1)
+    assert e.value.code == hl.HL_ERANGE
+    X2 = X.copy(); X2[0, 0] = 1 << 37
+    with pytest.raises(hl.HLError) as e:
+        ctx.encrypt(sk, (16, 32, 8), X2, 1)
+    assert e.value.code == hl.HL_ERANGE
+    with pytest.raises(hl.HLError) as e:
+        ctx.encrypt(sk, (16, 32, 16), X, 1)
+    assert e.value.code == hl.HL_EDIM

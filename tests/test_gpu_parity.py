@@ -1,0 +1,241 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle, bit for bit (-m gpu).
+
+Every expected value comes from oracle/ (or from brute-force numpy matmul for the
+reconstruction property); inputs come from synth/ (seeded) or the oracle's encrypt.
+Integer work, so the bar is bit-exact equality everywhere.
+"""
+import numpy as np
+import pytest
+
+import synth
+from oracle import ref
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def hl():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.fail("CUDA device required for -m gpu tests")
+    import paper_2305_18396_b200 as hl
+    hl.load_library()
+    return hl
+
+
+@pytest.fixture(scope="module")
+def ctx4096(hl):
+    return hl.Context(4096, 2, 37, device=0)
+
+
+@pytest.fixture(scope="module")
+def ctx8192(hl):
+    return hl.Context(8192, 3, 37, device=0)
+
+
+def _P(ctx):
+    return ref.bfv_params(ctx.N, ctx.L, ctx.t_bits)
+
+
+def _sync():
+    import torch
+    torch.cuda.synchronize()
+
+
+# ------------------------------------------------------------------------- NTT kernels
+@pytest.mark.parametrize("which", ["4096", "8192"])
+def test_ntt_roundtrip_identity(hl, ctx4096, ctx8192, which):
+    ctx = ctx4096 if which == "4096" else ctx8192
+    P = _P(ctx)
+    x = synth.uniform_below(1, (7, ctx.L, ctx.N), P.primes)
+    # extreme residues: 0 and p-1 everywhere in one polynomial
+    x[0, :, :] = 0
+    for l, p in enumerate(P.primes):
+        x[1, l, :] = p - 1
+    d = hl.to_device(x)
+    ctx.ntt_roundtrip(d)
+    _sync()
+    assert np.array_equal(hl.to_host(d).reshape(x.shape), x)
+
+
+@pytest.mark.parametrize("which", ["4096", "8192"])
+def test_poly_mul_vs_oracle_schoolbook(hl, ctx4096, ctx8192, which):
+    ctx = ctx4096 if which == "4096" else ctx8192
+    P = _P(ctx)
+    a = synth.uniform_below(2, (3, ctx.L, ctx.N), P.primes)
+    b = synth.uniform_below(3, (3, ctx.L, ctx.N), P.primes)
+    # special case x^(N-1) * x = -1 in polynomial 0
+    a[0] = 0; a[0, :, ctx.N - 1] = 1
+    b[0] = 0; b[0, :, 1] = 1
+    out = hl.to_host(ctx.poly_mul(hl.to_device(a), hl.to_device(b))).reshape(a.shape)
+    for i in range(3):
+        for l, p in enumerate(P.primes):
+            assert np.array_equal(out[i, l], ref.negacyclic_mul(ctx.N, p, a[i, l], b[i, l])), (i, l)
+    assert all(out[0, l, 0] == p - 1 for l, p in enumerate(P.primes)) and not out[0, :, 1:].any()
+
+
+# ------------------------------------------------------------------------- he_matmul / mask
+CASES = [
+    # (N, shape (Nb, R, Ma), tile)                          what it covers
+    (4096, (8, 64, 64), (16, 32, 8)),      # config c0
+    (4096, (40, 24, 40), (16, 8, 32)),     # ragged in every dimension, several tiles
+    (4096, (64, 48, 100), (4, 8, 16)),     # nC = 8, ragged I tail (nI = 25)
+    (4096, (3, 5, 7), (1, 1, 1)),          # degenerate 1x1x1 tile, nC = 6
+    (8192, (32, 48, 40), (32, 16, 16)),    # c4 parameters (N=8192, L=3) at small size
+]
+
+
+def _case_inputs(ctx, shape, tile, seed):
+    P = _P(ctx)
+    Nb, R, Ma = shape
+    nI, nJ, nK = ref.tile_counts(tile, Ma, R, Nb)
+    ct_in = synth.uniform_below(seed, (nJ, nK, 2, ctx.L, ctx.N), P.primes)
+    W = synth.weights(seed + 1, R, Ma)
+    return P, ct_in, W
+
+
+@pytest.mark.parametrize("N,shape,tile", CASES)
+def test_he_matmul_bit_exact(hl, ctx4096, ctx8192, N, shape, tile):
+    ctx = ctx4096 if N == 4096 else ctx8192
+    Nb, R, Ma = shape
+    P, ct_in, W = _case_inputs(ctx, shape, tile, 200 + N + Ma)
+    wc = ctx.encode_weights(tile, hl.to_device(W))
+    out = ctx.he_matmul(tile, wc, Ma, R, Nb, hl.to_device(ct_in))
+    got = hl.to_host(out).reshape(-1, 2, ctx.L, ctx.N)
+    exp = ref.he_matmul(P, tile, W, ct_in, Nb).reshape(-1, 2, ctx.L, ctx.N)
+    assert np.array_equal(got, exp)
+
+
+@pytest.mark.parametrize("N,shape,tile", CASES)
+@pytest.mark.parametrize("compress", [True, False])
+def test_mask_and_share_bit_exact(hl, ctx4096, ctx8192, N, shape, tile, compress):
+    ctx = ctx4096 if N == 4096 else ctx8192
+    Nb, R, Ma = shape
+    P = _P(ctx)
+    nI, _, nK = ref.tile_counts(tile, Ma, R, Nb)
+    ct_out = synth.uniform_below(300 + N, (nI, nK, 2, ctx.L, ctx.N), P.primes)
+    masked, share = ctx.mask_and_share(tile, Ma, Nb, hl.to_device(ct_out), seed=77, compress=compress)
+    em, es = ref.mask_and_share(P, tile, ct_out, Ma, Nb, 77, compress)
+    assert np.array_equal(hl.to_host(masked).reshape(em.shape), em)
+    assert np.array_equal(hl.to_host(share).reshape(es.shape), es)
+
+
+@pytest.mark.parametrize("N,shape,tile", CASES)
+def test_fused_he_matmul_share_bit_exact(hl, ctx4096, ctx8192, N, shape, tile):
+    ctx = ctx4096 if N == 4096 else ctx8192
+    Nb, R, Ma = shape
+    P, ct_in, W = _case_inputs(ctx, shape, tile, 400 + N + Ma)
+    wc = ctx.encode_weights(tile, hl.to_device(W))
+    masked, share = ctx.he_matmul_share(tile, wc, Ma, R, Nb, hl.to_device(ct_in), seed=91)
+    exp_ct = ref.he_matmul(P, tile, W, ct_in, Nb)
+    em, es = ref.mask_and_share(P, tile, exp_ct, Ma, Nb, 91, True)
+    assert np.array_equal(hl.to_host(masked).reshape(em.shape), em)
+    assert np.array_equal(hl.to_host(share).reshape(es.shape), es)
+
+
+def test_sharded_outputs_equal_slices(hl, ctx4096):
+    """I-tile shards [i0, i1) produce exactly the slice of the unsharded result (mask streams
+    are indexed by the global tile), so any GPU count gives identical outputs."""
+    ctx = ctx4096
+    tile, (Nb, R, Ma) = (16, 8, 32), (64, 32, 160)
+    P, ct_in, W = _case_inputs(ctx, (Nb, R, Ma), tile, 501)
+    dW, dct = hl.to_device(W), hl.to_device(ct_in)
+    full_m, full_s = ctx.he_matmul_share(tile, ctx.encode_weights(tile, dW), Ma, R, Nb, dct, seed=5)
+    full_m = hl.to_host(full_m).reshape(10, 2, -1)
+    full_s = hl.to_host(full_s).reshape(Nb, Ma)
+    for i0, i1 in [(0, 3), (3, 4), (4, 10)]:
+        wc = ctx.encode_weights(tile, dW, i0, i1)
+        m, s = ctx.he_matmul_share(tile, wc, Ma, R, Nb, dct, seed=5, i_begin=i0, i_end=i1)
+        assert np.array_equal(hl.to_host(m).reshape(i1 - i0, 2, -1), full_m[i0:i1])
+        s = hl.to_host(s).reshape(Nb, Ma)
+        cols = slice(i0 * 16, i1 * 16)
+        assert np.array_equal(s[:, cols], full_s[:, cols])
+
+
+# ------------------------------------------------------------------------- end to end (Alg. 1)
+@pytest.mark.parametrize("N,shape,tile", [
+    (4096, (8, 64, 64), (16, 32, 8)),
+    (4096, (37, 50, 45), (8, 8, 32)),
+    (8192, (16, 40, 24), (32, 16, 16)),
+])
+def test_end_to_end_reconstructs_XW(hl, ctx4096, ctx8192, N, shape, tile):
+    """Oracle client (keygen, encrypt, decrypt) around the GPU server: shares sum to X.W mod 2^37,
+    and the GPU's response equals the oracle server's response."""
+    ctx = ctx4096 if N == 4096 else ctx8192
+    P = _P(ctx)
+    Nb, R, Ma = shape
+    X, W = synth.activations(601, Nb, R), synth.weights(602, R, Ma)
+    sk = ref.keygen(P, 603)
+    ct_in = ref.encrypt(P, tile, sk, X, 604)
+    wc = ctx.encode_weights(tile, hl.to_device(W))
+    masked, share_s = ctx.he_matmul_share(tile, wc, Ma, R, Nb, hl.to_device(ct_in), seed=605)
+    masked = hl.to_host(masked).reshape(-1, P.L * (tile[0] * tile[2] + P.N))
+    share_s = hl.to_host(share_s).reshape(Nb, Ma)
+    share_c = ref.decrypt_share(P, tile, sk, masked, Ma, Nb, True)
+    got = (share_c + share_s) & np.uint64((1 << 37) - 1)
+    assert np.array_equal(got, ref.matmul_mod_t(X, W))
+    em, es = ref.mask_and_share(P, tile, ref.he_matmul(P, tile, W, ct_in, Nb), Ma, Nb, 605, True)
+    assert np.array_equal(masked.reshape(em.shape), em) and np.array_equal(share_s, es)
+
+
+def test_bert_tiny_block_c1(hl, ctx4096):
+    """Config c1 (BERT-Tiny block, the four matmuls) end to end against the oracle server."""
+    ctx = ctx4096
+    cfg = synth.CONFIGS["c1"]
+    P = _P(ctx)
+    for mi, mm in enumerate(cfg.matmuls):
+        X = synth.activations(synth.seed_for(0, mi, "x"), mm.Nb, mm.R)
+        W = synth.weights(synth.seed_for(0, mi, "w"), mm.R, mm.Ma)
+        nI, nJ, nK = ref.tile_counts(cfg.tile, mm.Ma, mm.R, mm.Nb)
+        ct_in = synth.uniform_below(synth.seed_for(0, mi, "enc"), (nJ, nK, 2, P.L, P.N), P.primes)
+        wc = ctx.encode_weights(cfg.tile, hl.to_device(W))
+        seed = synth.seed_for(0, mi, "mask")
+        m, s = ctx.he_matmul_share(cfg.tile, wc, mm.Ma, mm.R, mm.Nb, hl.to_device(ct_in), seed=seed)
+        em, es = ref.mask_and_share(P, cfg.tile, ref.he_matmul(P, cfg.tile, W, ct_in, mm.Nb), mm.Ma, mm.Nb, seed)
+        assert np.array_equal(hl.to_host(m).reshape(em.shape), em), mm.name
+        assert np.array_equal(hl.to_host(s).reshape(es.shape), es), mm.name
+
+
+def test_bert_base_full_size_sampled(hl, ctx4096):
+    """Config c2 at full size in the bench's launch configuration (fused call, default tile):
+    sampled output tiles bit-exact against the oracle (its own scalar NTT), and for the whole
+    matmul the reconstruction property (library decrypt + brute-force X.W mod 2^37)."""
+    ctx = ctx4096
+    cfg = synth.CONFIGS["c2"]
+    P = _P(ctx)
+    tile = cfg.tile
+    mm = cfg.matmuls[3]                     # FF2: R = 3072, the longest J reduction
+    X = synth.activations(synth.seed_for(0, 3, "x"), mm.Nb, mm.R)
+    W = synth.weights(synth.seed_for(0, 3, "w"), mm.R, mm.Ma)
+    sk = ctx.keygen(synth.seed_for(0, 3, "key"))
+    ct_in = ctx.encrypt(sk, tile, X, synth.seed_for(0, 3, "enc"))
+    assert np.array_equal(ct_in[:1, :1], ref.encrypt(P, tile, sk, X[:tile[2], :tile[1]],
+                                                     synth.seed_for(0, 3, "enc")))
+    wc = ctx.encode_weights(tile, hl.to_device(W))
+    seed = synth.seed_for(0, 3, "mask")
+    masked, share = ctx.he_matmul_share(tile, wc, mm.Ma, mm.R, mm.Nb, hl.to_device(ct_in), seed=seed)
+    nI, nJ, nK = ref.tile_counts(tile, mm.Ma, mm.R, mm.Nb)
+    masked = hl.to_host(masked).reshape(nI, nK, -1)
+    share = hl.to_host(share).reshape(mm.Nb, mm.Ma)
+    tiles = [(0, 0), (nI - 1, nK - 1), (17, 2)]
+    exp_ct = ref.he_matmul_ntt_tiles(P, tile, W, ct_in, mm.Nb, tiles)
+    em, kept = ref.mask_tiles(P, tile, exp_ct, nK, tiles, seed, True)
+    for o, (I, K) in enumerate(tiles):
+        assert np.array_equal(masked[I, K], em[o]), (I, K)
+    share_c = ctx.decrypt_share(sk, tile, masked, mm.Ma, mm.Nb, True)
+    got = (share_c + share) & np.uint64((1 << 37) - 1)
+    assert np.array_equal(got, ref.matmul_mod_t(X, W))
+
+
+# ------------------------------------------------------------------------- errors
+def test_encode_weights_errors(hl, ctx4096):
+    ctx = ctx4096
+    W = synth.weights(1, 64, 64)
+    W[3, 5] = 1 << 37
+    with pytest.raises(hl.HLError) as e:
+        ctx.encode_weights((16, 32, 8), hl.to_device(W))
+    assert e.value.code == hl.HL_ERANGE
+    Wbig = synth.stressed_weights(2, 64, 64, bound=1 << 30)     # 2R max|w| r_t >> Delta/2
+    with pytest.raises(hl.HLError) as e:
+        ctx.encode_weights((16, 32, 8), hl.to_device(Wbig))
+    assert e.value.code == hl.HL_ENOISE
