@@ -1,0 +1,399 @@
+"""bench.py -- the server's homomorphic linear layers of one BERT-base encoder block (config c2).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config c2]
+    python -m torch.distributed.run --nproc-per-node N --master-addr 127.0.0.1 bench.py --gpus N ...
+
+A step is one pass of the whole hot path over one BERT-base
+block: for each of the four encrypted products X.W_qkv, X.W_o, X.W_1, H.W_2 -- forward NTT
+of the client's ciphertexts, modular MAC against the cached NTT-domain weights, inverse NTT,
+mask + compression + server share (hl_he_matmul_share).  Weights are encoded once before
+timing (offline, reported separately); input ciphertexts are resident in HBM.  Multi-GPU:
+weak scaling -- every rank runs its own block (independently seeded), no data-path collective.
+
+Prints ONE JSON line (rank 0).  `--impl reference` times the CPU oracle (oracle/) on a
+bounded sample of the same workload instead (the reference arm of this tier).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import synth  # noqa: E402
+
+METRIC = "ms per BERT-base encoder block's encrypted matmuls"
+UNIT = "ms"
+
+
+def _peaks():
+    try:
+        return json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except Exception:
+        return {}
+
+
+# ----------------------------------------------------------------------------- algorithmic counts
+def counts(cfg, lay_by_mm):
+    """Per-matmul algorithmic work: MACs, butterflies, bytes of each kernel."""
+    N, L = cfg.N, cfg.L
+    m, r, n = cfg.tile
+    out = []
+    logN = N.bit_length() - 1
+    for mm, lay in zip(cfg.matmuls, lay_by_mm):
+        nI, nJ, nK = lay.nI, lay.nJ, lay.nK
+        nC = 2 * nK
+        P = nI * nJ * nK
+        out.append(dict(
+            name=mm.name, products=P,
+            mac=P * 2 * L * N,                                   # modular MACs
+            bfly_fwd=nJ * nC * L * (N // 2) * logN,
+            bfly_inv=nI * nC * L * (N // 2) * logN,
+            # MAC kernel bytes: weight cache + NTT-domain ct_in (read once) + NTT-domain output
+            mac_bytes=8 * (nI * nJ * L * N + nJ * nC * L * N + nI * nC * L * N),
+            fwd_bytes=8 * 2 * nJ * nC * L * N,                   # coefficient ct_in in, limb pairs out
+            inv_bytes=8 * (nI * nC * L * N + nI * nK * L * (m * n + N) + mm.Nb * mm.Ma),
+            # whole-path algorithmic bytes (SURVEY.md §8(d) "Bytes")
+            path_bytes=8 * (nJ * nK * 2 * L * N + nI * nJ * L * N + nI * nK * L * (N + m * n) + mm.Nb * mm.Ma),
+        ))
+    return out
+
+
+# ----------------------------------------------------------------------------- clocks sampler
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region (B200_PROFILING.md)."""
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index, self.proc, self.lines = index, None, []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                 "-lms", "50"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+            time.sleep(0.15)
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.1)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=2)
+        except Exception:
+            self.proc.kill()
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 6:
+                continue
+            try:
+                sm.append(float(f[0]))
+                mx = float(f[1])
+            except ValueError:
+                continue
+            for nm, v in zip(names, f[2:6]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# ----------------------------------------------------------------------------- our arm
+def run_ours(args, rank, world, local_rank):
+    import torch
+    import paper_2305_18396_b200 as hl
+
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    cfg = synth.CONFIGS[args.config]
+    tile = tuple(args.tile) if args.tile else cfg.tile
+    ctx = hl.Context(cfg.N, cfg.L, synth.T_BITS, device=local_rank)
+    block = rank                      # weak scaling: every rank owns one independently seeded block
+    stream = torch.cuda.current_stream()
+
+    # ---------------- setup (untimed): client encryption on the host, weight encoding on device
+    mats = []
+    t_enc = 0.0
+    for mi, mm in enumerate(cfg.matmuls):
+        lay = ctx.layout(tile, mm.Ma, mm.R, mm.Nb)
+        X = synth.activations(synth.seed_for(block, mi, "x"), mm.Nb, mm.R)
+        W = synth.weights(synth.seed_for(block, mi, "w"), mm.R, mm.Ma)
+        sk = ctx.keygen(synth.seed_for(block, mi, "key"))
+        ct_host = ctx.encrypt(sk, tile, X, synth.seed_for(block, mi, "enc"))
+        dW = hl.to_device(W, dev)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        wc = ctx.encode_weights(tile, dW)
+        torch.cuda.synchronize()
+        t_enc += time.perf_counter() - t0
+        del dW
+        mats.append(dict(mm=mm, lay=lay, wc=wc, ct=hl.to_device(ct_host, dev),
+                         ct_host=torch.from_numpy(ct_host.view(np.int64).reshape(-1)).pin_memory(),
+                         seed=synth.seed_for(block, mi, "mask")))
+    ws_words = max(m["lay"].workspace_bytes // 8 for m in mats)
+    out_words = max(m["lay"].ct_out_words for m in mats)
+    workspace = torch.empty(ws_words, dtype=torch.int64, device=dev)
+    ct_out_ntt = torch.empty(out_words, dtype=torch.int64, device=dev)
+    for m in mats:
+        m["masked"] = torch.empty(m["lay"].ct_masked_words, dtype=torch.int64, device=dev)
+        m["share"] = torch.zeros(m["lay"].share_words, dtype=torch.int64, device=dev)
+
+    def step():
+        for m in mats:
+            mm = m["mm"]
+            ctx.he_matmul_share(tile, m["wc"], mm.Ma, mm.R, mm.Nb, m["ct"], m["seed"], True,
+                                workspace=workspace, ct_out_ntt=ct_out_ntt, ct_masked=m["masked"],
+                                share=m["share"], stream=stream)
+
+    def barrier():
+        if world > 1:
+            import torch.distributed as dist
+            dist.barrier()
+
+    def max_over_ranks(x: float) -> float:
+        if world > 1:
+            import torch.distributed as dist
+            t = torch.tensor([x], dtype=torch.float64, device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            return float(t.item())
+        return x
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+
+    # ---------------- timed region (device events on the launching stream)
+    clocks = ClockSampler(local_rank) if rank == 0 else None
+    if clocks:
+        clocks.start()
+    ctx.timing_enable(True)
+    barrier()
+    torch.cuda.synchronize()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ev0.record(stream)
+    for _ in range(args.steps):
+        step()
+    ev1.record(stream)
+    torch.cuda.synchronize()
+    barrier()
+    ctx.timing_enable(False)
+    elapsed = max_over_ranks(ev0.elapsed_time(ev1))
+    ktimes = ctx.timing_read()
+    clk = clocks.stop() if clocks else None
+
+    # ---------------- end to end through the public API on pinned host buffers
+    host_masked = [torch.empty(m["lay"].ct_masked_words, dtype=torch.int64).pin_memory() for m in mats]
+    host_share = [torch.empty(m["lay"].share_words, dtype=torch.int64).pin_memory() for m in mats]
+    dev_ct_in = torch.empty(max(m["lay"].ct_in_words for m in mats), dtype=torch.int64, device=dev)
+
+    def e2e_step():
+        for m, hm, hs in zip(mats, host_masked, host_share):
+            mm = m["mm"]
+            ctx.he_linear_host(tile, m["wc"], mm.Ma, mm.R, mm.Nb, m["ct_host"], m["seed"], hm, hs, dev_ct_in,
+                               workspace, ct_out_ntt, m["masked"], m["share"], compress=True, stream=stream)
+
+    e2e_steps = max(3, min(args.steps, 20))
+    for _ in range(2):
+        e2e_step()
+    torch.cuda.synchronize()
+    barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(e2e_steps):
+        e2e_step()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    barrier()
+    e2e_ms = max_over_ranks(e0.elapsed_time(e1)) / e2e_steps
+    h2d = sum(m["lay"].ct_in_words * 8 for m in mats)
+    d2h = sum((m["lay"].ct_masked_words + m["lay"].share_words) * 8 for m in mats)
+
+    if rank != 0:
+        return None
+
+    # ---------------- numbers
+    ms_step = elapsed / args.steps
+    value = elapsed / (args.steps * world)            # ms per block over all ranks' blocks
+    cnt = counts(cfg, [m["lay"] for m in mats])
+    products = sum(c["products"] for c in cnt)
+    peaks = _peaks()
+    hbm = peaks.get("hbm_gbs")
+    hbm_src = "measured (MEASURED_PEAKS.json hbm_gbs)" if hbm else "fallback 6650 GB/s (B200_PROFILING.md)"
+    hbm = hbm or 6650.0
+    sm_max = (peaks.get("sm_max_mhz") or 1965.0)
+    # integer-pipe peak: 64 IMAD/clk/SM (B300_MICROARCH.md: IMAD on the fma pipe,
+    # rt_SMSP = 2 -> 16 lanes/clk per SMSP x 4 SMSPs) x 148 SMs x max SM clock.
+    imad_peak = 64 * 148 * sm_max * 1e6                           # IMAD/s
+    mac_ms, mac_n = ktimes["mac"]
+    mac_avg_s = mac_ms / max(mac_n, 1) * 1e-3
+    per_launch_mac = sum(c["mac"] for c in cnt) / len(cnt)
+    per_launch_bytes = sum(c["mac_bytes"] for c in cnt) / len(cnt)
+    # bound of the MAC kernel: the slower of ALU (3 IMAD.WIDE per modular MAC) and HBM
+    t_alu = 3 * per_launch_mac / imad_peak
+    t_hbm = per_launch_bytes / (hbm * 1e9)
+    if t_alu >= t_hbm:
+        roof = {"bound": "alu", "achieved": 3 * per_launch_mac / mac_avg_s / 1e12, "peak": imad_peak / 1e12,
+                "unit": "T IMAD.WIDE/s (3 per modular MAC)"}
+    else:
+        roof = {"bound": "hbm", "achieved": per_launch_bytes / mac_avg_s / 1e9, "peak": hbm, "unit": "GB/s"}
+    roof["frac"] = roof["achieved"] / roof["peak"]
+    roof["traffic"] = None
+    roof["kernel"] = "k_mac (slot-parallel modular MAC)"
+    roof["peak_source"] = ("guide unit counts x sm_max_mhz (DESIGN.md §6)" if roof["bound"] == "alu" else hbm_src)
+    roof["hbm_frac_same_kernel"] = per_launch_bytes / mac_avg_s / 1e9 / hbm
+    total_k = sum(v[0] for v in ktimes.values())
+    kernel_share = {k: {"ms_per_step": v[0] / args.steps, "launches_per_step": v[1] / args.steps,
+                        "share": v[0] / total_k if total_k else None} for k, v in ktimes.items() if v[1]}
+    launches = sum(v[1] for v in ktimes.values())
+    path_bytes = sum(c["path_bytes"] for c in cnt)
+
+    line = {
+        "metric": METRIC, "value": round(value, 4), "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": round(ms_step, 4), "higher_is_better": False, "scaling": "weak",
+        "vs_baseline": None, "dtype": "u64", "data": "synthetic",
+        "config": {"workload": f"{cfg.name}: {cfg.note}", "N": cfg.N, "L": cfg.L, "t_bits": synth.T_BITS,
+                   "tile": list(tile), "matmuls": [[mm.Nb, mm.R, mm.Ma] for mm in cfg.matmuls],
+                   "blocks_per_step_per_rank": 1, "compress": True,
+                   "l2": "inputs larger than L2: 3.6 GB NTT-domain weight cache + 352 MB ct_in per block",
+                   "parallelism": f"weak x{world} (one block per rank)"},
+        "poly_products_per_s": products * args.steps * world / (elapsed * 1e-3),
+        "path_bytes_per_block": path_bytes,
+        "path_hbm_frac": path_bytes / (value * 1e-3) / (hbm * 1e9),
+        "roofline": roof,
+        "kernels": kernel_share,
+        "gpu_launches": launches,
+        "encode_weights_ms": round(t_enc * 1e3, 3),
+        "e2e": {"value": round(e2e_ms, 4), "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
+        "clocks": clk,
+    }
+    if world == 1 and not args.no_cpu_baseline:
+        line["cpu_baseline"] = oracle_baseline(cfg, tile, args.cpu_itiles)
+    return line
+
+
+# ----------------------------------------------------------------------------- the oracle arm
+def oracle_baseline(cfg, tile, itiles: int, ktiles: int = 0):
+    """The CPU oracle as it stands (sparse schoolbook he_matmul + mask; OpenMP over output
+    ciphertext x component x prime) on a bounded sample: the first `itiles` I tiles and the first
+    `ktiles` K tiles (0 = all) of each matmul, all J, extrapolated linearly to the whole block
+    (oracle work is exactly linear in the number of output ciphertexts)."""
+    from oracle import ref
+    P = ref.bfv_params(cfg.N, cfg.L, synth.T_BITS)
+    m, r, n = tile
+    total_s = 0.0
+    sampled = total = 0
+    for mi, mm in enumerate(cfg.matmuls):
+        nI, nJ, nK = ref.tile_counts(tile, mm.Ma, mm.R, mm.Nb)
+        s = min(itiles, nI)
+        kk = nK if ktiles <= 0 else min(ktiles, nK)
+        Nb = min(mm.Nb, kk * n)
+        W = synth.weights(synth.seed_for(0, mi, "w"), mm.R, mm.Ma)[:, : s * m].copy()
+        ct_in = synth.uniform_below(synth.seed_for(0, mi, "enc"), (nJ, kk, 2, P.L, P.N), P.primes)
+        t0 = time.perf_counter()
+        ct_out = ref.he_matmul(P, tile, W, ct_in, Nb)
+        ref.mask_and_share(P, tile, ct_out, W.shape[1], Nb, 1, True)
+        dt = time.perf_counter() - t0
+        total_s += dt * (nI * nK) / (s * kk)
+        sampled += s * kk
+        total += nI * nK
+    cores = len(os.sched_getaffinity(0))
+    return {"value": round(total_s * 1e3, 1), "unit": UNIT, "cores": cores, "kind": "oracle",
+            "sample": f"{sampled} of {total} output ciphertexts (first {itiles} I-tile(s) x "
+                      f"{'all' if ktiles <= 0 else ktiles} K-tile(s) of each of the 4 matmuls, all J), "
+                      f"extrapolated linearly to the block",
+            "cpu": _cpu_model()}
+
+
+def _cpu_model():
+    try:
+        for ln in open("/proc/cpuinfo"):
+            if ln.startswith("model name"):
+                return ln.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return None
+
+
+def run_reference(args, rank, world):
+    if rank != 0:
+        return None
+    cfg = synth.CONFIGS[args.config]
+    tile = tuple(args.tile) if args.tile else cfg.tile
+    vals = []
+    for _ in range(min(args.warmup, 1)):
+        oracle_baseline(cfg, tile, 1, 1)
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        vals.append(oracle_baseline(cfg, tile, 1, 1)["value"])
+    wall = time.perf_counter() - t0
+    v = float(np.mean(vals))
+    base = oracle_baseline.__doc__
+    cores = len(os.sched_getaffinity(0))
+    return {"metric": METRIC, "value": round(v, 1), "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": round(v, 1), "higher_is_better": False, "scaling": "weak",
+            "vs_baseline": None, "dtype": "u64", "data": "synthetic", "impl": "reference",
+            "config": {"workload": f"{cfg.name}: {cfg.note}", "N": cfg.N, "L": cfg.L, "t_bits": synth.T_BITS,
+                       "tile": list(tile), "parallelism": "CPU oracle, OpenMP over output tiles"},
+            "cpu_baseline": {"value": round(v, 1), "unit": UNIT, "cores": cores, "kind": "oracle",
+                             "sample": "per step: output ciphertext (I=0, K=0) of each of the 4 matmuls "
+                                       "(4 of 1728), extrapolated linearly to the block", "cpu": _cpu_model(),
+                             "wall_s": round(wall, 2)},
+            "e2e": {"value": round(v, 1), "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+            "gpu_launches": 0, "note": base.split("\n")[0] if base else ""}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--config", default="c2", choices=sorted(synth.CONFIGS))
+    ap.add_argument("--tile", type=int, nargs=3, default=None)
+    ap.add_argument("--cpu-itiles", type=int, default=2)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3 and args.impl == "ours":
+        args.warmup = 3
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1 and args.impl == "ours":
+        import torch
+        import torch.distributed as dist
+        torch.cuda.set_device(local_rank)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    if args.impl == "reference":
+        line = run_reference(args, rank, world)
+    else:
+        line = run_ours(args, rank, world, local_rank)
+    if rank == 0 and line is not None:
+        print(json.dumps(line), flush=True)
+    if world > 1 and args.impl == "ours":
+        import torch.distributed as dist
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -81,8 +81,8 @@ typedef struct {
   int64_t ct_masked_words;    /* compressed: nI_shard*nK*L*(m*n + N)                          */
   int64_t ct_full_words;      /* uncompressed masked: nI_shard*nK*2*L*N                       */
   int64_t share_words;        /* Nb*Ma                                                        */
-  int64_t wcache_bytes;       /* nI_shard*nJ*L*N*8                                            */
-  int64_t workspace_bytes;    /* nJ*nK*2*L*N*8                                                */
+  int64_t wcache_bytes;       /* ceil(nI_shard/16)*16*nJ*L*N*8 (rows padded to 16)            */
+  int64_t workspace_bytes;    /* nJ*nK*2*L*N*12                                               */
 } hl_layout;
 
 /* ---- context ---------------------------------------------------------------------------- */
@@ -182,6 +182,28 @@ int hl_poly_mul(const hl_ctx *ctx, const uint64_t *a, const uint64_t *b, uint64_
 /* Forward NTT then inverse NTT of x in place (identity on canonical residues): exercises the
  * two transforms alone.  x: device [npoly][L][N]; scratch: device npoly*L*N*8 bytes. */
 int hl_ntt_roundtrip(const hl_ctx *ctx, uint64_t *x, int64_t npoly, void *scratch, void *stream);
+
+/* ---- per-kernel timing (bench.py's roofline evidence) ------------------------------------- */
+
+enum {
+  HL_K_NTT_FWD = 0,     /* forward NTT of ct_in (he_matmul step 1)                              */
+  HL_K_MAC = 1,         /* slot-parallel modular multiply-accumulate over J (step 2)             */
+  HL_K_INTT_MASK = 2,   /* fused inverse NTT + mask + compression + share (he_matmul_share)      */
+  HL_K_INTT = 3,        /* inverse NTT (he_matmul step 3)                                        */
+  HL_K_MASK = 4,        /* mask_and_share                                                        */
+  HL_K_ENCODE = 5,      /* encode_weights (pi_A + forward NTT)                                   */
+  HL_K_OTHER = 6,       /* diagnostics                                                           */
+  HL_K_COUNT = 7
+};
+
+/* on != 0: record a CUDA event pair on the launching stream around every kernel launch made
+ * through ctx (adds ~2 event records per launch); on == 0: stop recording.  Mutates the
+ * context's timing record: do not enable while other threads use the context. */
+int hl_timing_enable(hl_ctx *ctx, int on);
+
+/* Wait for the recorded events, ADD the summed durations (ms) and launch counts per kernel
+ * class into ms[HL_K_COUNT] and count[HL_K_COUNT], then clear the record. */
+int hl_timing_read(hl_ctx *ctx, double *ms, int64_t *count);
 
 #ifdef __cplusplus
 }

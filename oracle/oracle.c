@@ -270,33 +270,32 @@ void or_he_matmul(uint32_t N, uint32_t L, const uint64_t *primes, uint32_t m, ui
                   uint32_t n, uint32_t t_bits, const uint64_t *W, int64_t R, int64_t Ma,
                   int64_t Nb, const uint64_t *ct_in, uint64_t *ct_out) {
   int64_t nI = (Ma + m - 1) / m, nJ = (R + r - 1) / r, nK = (Nb + n - 1) / n;
+  /* independent work items: (output tile (I, K), component c, prime l) */
 #pragma omp parallel for schedule(dynamic)
-  for (int64_t o = 0; o < nI * nK; o++) {
-    int64_t I = o / nK, K = o % nK;
-    u128 *pos = (u128 *)malloc(sizeof(u128) * N), *neg = (u128 *)malloc(sizeof(u128) * N);
-    for (int c = 0; c < 2; c++)
-      for (uint32_t l = 0; l < L; l++) {
-        uint64_t p = primes[l];
-        memset(pos, 0, sizeof(u128) * N); memset(neg, 0, sizeof(u128) * N);
-        for (int64_t J = 0; J < nJ; J++) {
-          const uint64_t *x = ct_in + ((uint64_t)(J * nK + K) * 2 + c) * L * N + (uint64_t)l * N;
-          for (uint32_t i = 0; i < m; i++)
-            for (uint32_t j = 0; j < r; j++) {
-              int64_t row = J * (int64_t)r + j, col = I * (int64_t)m + i;
-              if (row >= R || col >= Ma) continue;
-              uint64_t val = signed_mod(lift(W[row * Ma + col], t_bits), p);
-              if (val == 0) continue;
-              uint32_t e = i * r + r - 1 - j;          /* exponent of a_ij in pi_A */
-              for (uint32_t s = 0; s < N; s++) {
-                u128 prod = (u128)val * x[s];
-                if (s + e < N) pos[s + e] += prod; else neg[s + e - N] += prod;
-              }
-            }
+  for (int64_t w = 0; w < nI * nK * 2 * (int64_t)L; w++) {
+    int64_t o = w / (2 * L), I = o / nK, K = o % nK;
+    int c = (int)((w / L) % 2);
+    uint32_t l = (uint32_t)(w % L);
+    uint64_t p = primes[l];
+    u128 *pos = (u128 *)calloc(N, sizeof(u128)), *neg = (u128 *)calloc(N, sizeof(u128));
+    for (int64_t J = 0; J < nJ; J++) {
+      const uint64_t *x = ct_in + ((uint64_t)(J * nK + K) * 2 + c) * L * N + (uint64_t)l * N;
+      for (uint32_t i = 0; i < m; i++)
+        for (uint32_t j = 0; j < r; j++) {
+          int64_t row = J * (int64_t)r + j, col = I * (int64_t)m + i;
+          if (row >= R || col >= Ma) continue;
+          uint64_t val = signed_mod(lift(W[row * Ma + col], t_bits), p);
+          if (val == 0) continue;
+          uint32_t e = i * r + r - 1 - j;          /* exponent of a_ij in pi_A */
+          for (uint32_t s = 0; s < N; s++) {
+            u128 prod = (u128)val * x[s];
+            if (s + e < N) pos[s + e] += prod; else neg[s + e - N] += prod;
+          }
         }
-        uint64_t *y = ct_out + ((uint64_t)(I * nK + K) * 2 + c) * L * N + (uint64_t)l * N;
-        for (uint32_t k = 0; k < N; k++)
-          y[k] = submod((uint64_t)(pos[k] % p), (uint64_t)(neg[k] % p), p);
-      }
+    }
+    uint64_t *y = ct_out + ((uint64_t)(I * nK + K) * 2 + c) * L * N + (uint64_t)l * N;
+    for (uint32_t k = 0; k < N; k++)
+      y[k] = submod((uint64_t)(pos[k] % p), (uint64_t)(neg[k] % p), p);
     free(pos); free(neg);
   }
 }

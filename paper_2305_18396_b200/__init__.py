@@ -30,7 +30,8 @@ _CODES = {HL_EINVAL: "HL_EINVAL", HL_EDIM: "HL_EDIM", HL_ERANGE: "HL_ERANGE", HL
 EXPORTS = ("hl_last_error", "hl_ctx_create", "hl_ctx_destroy", "hl_ctx_params", "hl_layout_query",
            "hl_keygen", "hl_encrypt", "hl_decrypt_share", "hl_encode_weights", "hl_he_matmul",
            "hl_mask_and_share", "hl_he_matmul_share", "hl_he_linear_host", "hl_poly_mul",
-           "hl_ntt_roundtrip")
+           "hl_ntt_roundtrip", "hl_timing_enable", "hl_timing_read")
+KERNELS = ("ntt_fwd", "mac", "intt_mask", "intt", "mask", "encode", "other")   # HL_K_* order
 
 
 class HLError(RuntimeError):
@@ -96,6 +97,8 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
         "hl_he_linear_host": [vp, Tile, vp, i64, i64, i64, vp, u64, i32, vp, vp, vp, vp, vp, vp, vp, vp],
         "hl_poly_mul": [vp, vp, vp, vp, i64, vp, vp],
         "hl_ntt_roundtrip": [vp, vp, i64, vp, vp],
+        "hl_timing_enable": [vp, i32],
+        "hl_timing_read": [vp, vp, vp],
     }
     for name, args in sig.items():
         f = getattr(L, name)
@@ -265,6 +268,17 @@ class Context:
                                       int(bool(compress)), ct_masked_host.data_ptr(), share_host.data_ptr(),
                                       _dptr(dev_ct_in), _dptr(workspace), _dptr(dev_ct_out_ntt),
                                       _dptr(dev_ct_masked), _dptr(dev_share), _stream(stream)))
+
+    # ---------------------------------------------------------------- timing
+    def timing_enable(self, on: bool = True):
+        _check(_lib.hl_timing_enable(self._h, int(bool(on))))
+
+    def timing_read(self) -> dict:
+        """{kernel: (total_ms, launches)} since the last read (synchronises the recorded events)."""
+        ms = np.zeros(len(KERNELS), np.float64)
+        cnt = np.zeros(len(KERNELS), np.int64)
+        _check(_lib.hl_timing_read(self._h, ms.ctypes.data, cnt.ctypes.data))
+        return {k: (float(ms[i]), int(cnt[i])) for i, k in enumerate(KERNELS)}
 
     # ---------------------------------------------------------------- diagnostics
     def poly_mul(self, a, b, out=None, scratch=None, stream=None):

@@ -205,14 +205,65 @@ extern "C" int hl_ctx_create(uint32_t N, uint32_t L, uint32_t log2_t, const uint
     delete c;
     return rc ? rc : hl_fail(HL_ECUDA, "hl_ctx_create: device allocation failed");
   }
+  cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, device);
   dp.tw_fwd = (const ulonglong2 *)c->d_tw;
   dp.tw_inv = (const ulonglong2 *)c->d_tw + (size_t)L * N;
   *out = c;
   return HL_OK;
 }
 
+// ---------------------------------------------------------------------------------------
+// kernel timing
+// ---------------------------------------------------------------------------------------
+static void *take_event(TimingState *ts) {
+  if (!ts->pool.empty()) { void *e = ts->pool.back(); ts->pool.pop_back(); return e; }
+  cudaEvent_t e;
+  if (cudaEventCreate(&e) != cudaSuccess) return nullptr;
+  return (void *)e;
+}
+
+KTimer::KTimer(const hl_ctx *c_, int kid_, void *stream_) : c(c_), kid(kid_), stream(stream_) {
+  if (!c->timing || !c->timing->on) return;
+  ev0 = take_event(c->timing); ev1 = take_event(c->timing);
+  if (ev0) cudaEventRecord((cudaEvent_t)ev0, (cudaStream_t)stream);
+}
+
+KTimer::~KTimer() {
+  if (!ev0 || !ev1) return;
+  cudaEventRecord((cudaEvent_t)ev1, (cudaStream_t)stream);
+  c->timing->rec.push_back({kid, {ev0, ev1}});
+}
+
+extern "C" int hl_timing_enable(hl_ctx *c, int on) {
+  if (!c) return hl_fail(HL_EINVAL, "hl_timing_enable: ctx is NULL");
+  if (!c->timing) c->timing = new TimingState();
+  c->timing->on = on != 0;
+  return HL_OK;
+}
+
+extern "C" int hl_timing_read(hl_ctx *c, double *ms, int64_t *count) {
+  if (!c || !ms || !count) return hl_fail(HL_EINVAL, "hl_timing_read: NULL argument");
+  if (!c->timing) return HL_OK;
+  for (auto &r : c->timing->rec) {
+    float t = 0;
+    if (cudaEventSynchronize((cudaEvent_t)r.second.second) != cudaSuccess ||
+        cudaEventElapsedTime(&t, (cudaEvent_t)r.second.first, (cudaEvent_t)r.second.second) != cudaSuccess)
+      return hl_cuda_check("hl_timing_read");
+    if (r.first >= 0 && r.first < HL_K_COUNT) { ms[r.first] += t; count[r.first] += 1; }
+    c->timing->pool.push_back(r.second.first);
+    c->timing->pool.push_back(r.second.second);
+  }
+  c->timing->rec.clear();
+  return HL_OK;
+}
+
 extern "C" int hl_ctx_destroy(hl_ctx *c) {
   if (!c) return HL_OK;
+  if (c->timing) {
+    for (void *e : c->timing->pool) cudaEventDestroy((cudaEvent_t)e);
+    for (auto &r : c->timing->rec) { cudaEventDestroy((cudaEvent_t)r.second.first); cudaEventDestroy((cudaEvent_t)r.second.second); }
+    delete c->timing;
+  }
   if (c->d_tw) cudaFree(c->d_tw);
   if (c->d_flags) cudaFree(c->d_flags);
   delete c;
@@ -259,8 +310,8 @@ extern "C" int hl_layout_query(const hl_ctx *c, hl_tile tile, int64_t Ma, int64_
   out->ct_masked_words = g.nIs * g.nK * (int64_t)c->L * ((int64_t)g.m * g.n + c->N);
   out->ct_full_words = g.nIs * g.nK * 2 * LN;
   out->share_words = Nb * Ma;
-  out->wcache_bytes = g.nIs * g.nJ * LN * 8;
-  out->workspace_bytes = g.nJ * g.nK * 2 * LN * 8;
+  out->wcache_bytes = (g.nIs + 15) / 16 * 16 * g.nJ * LN * 8;   // I rows padded to 16 (MAC tiles)
+  out->workspace_bytes = g.nJ * g.nK * 2 * LN * 12;   // limb pairs + limb sums (MAC operand X)
   return HL_OK;
 }
 

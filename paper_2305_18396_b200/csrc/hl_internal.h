@@ -36,9 +36,17 @@ struct DevParams {
   const ulonglong2 *tw_inv;   // [L][N] {w, w'}: psi^-bitrev(i)
 };
 
+// CUDA-event timing of kernel launches (hl_timing_enable / hl_timing_read)
+struct TimingState {
+  bool on = false;
+  std::vector<void *> pool;                        // free cudaEvent_t
+  std::vector<std::pair<int, std::pair<void *, void *>>> rec;   // (kernel class, (start, stop))
+};
+
 struct hl_ctx {
   uint32_t N, L, log2_t;
   int device;
+  int num_sms = 148;
   std::vector<uint64_t> primes;
   std::vector<uint64_t> psi;          // primitive 2N-th roots
   std::vector<uint64_t> delta_mod;    // Delta mod p_l
@@ -55,6 +63,14 @@ struct hl_ctx {
   DevParams dp;
   void *d_tw = nullptr;               // device allocation holding tw_fwd + tw_inv
   uint32_t *d_flags = nullptr;        // device scratch: [0] range flag, [1] max |w| (as u32 bits)
+  TimingState *timing = nullptr;      // owned; mutable through const hl_ctx*
+};
+
+// RAII event pair around one kernel launch when timing is on
+struct KTimer {
+  const hl_ctx *c; int kid; void *stream; void *ev0 = nullptr, *ev1 = nullptr;
+  KTimer(const hl_ctx *c_, int kid_, void *stream_);
+  ~KTimer();
 };
 
 // ---- error handling ------------------------------------------------------------------

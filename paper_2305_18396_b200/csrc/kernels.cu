@@ -205,12 +205,47 @@ template <int LOGN>
 __device__ __forceinline__ int slot_of(int t, int u) { return u * Geom<LOGN>::NT + t; }
 
 // ---------------------------------------------------------------------------------------
+// MAC operand layouts in HBM (NTT domain, 25-bit limb pairs).  Both are blocked
+// so that the operands of one (tile, J) step of the MAC kernel are ONE contiguous chunk each,
+// fetched by a single bulk (TMA) copy:
+//   W cache   [nIb][nSb][nJ][32 slots][16 rows] uint2            nIb = ceil(nIs/16), nSb = L*N/32
+//   X (ct_in) [nSb][nCg][nJ]{ [32 slots][CW cols] uint2 limb pairs, [32 slots][CW cols] u32 x0+x1 }
+//             CW in {8,4,2} divides nC, nCg = nC/CW; the limb sums of X (Karatsuba middle term)
+//             are stored so that the MAC's integer-multiply pipe only multiplies.
+// slot s = l*N + P(idx) (prime-major), rows = I tiles of the shard, cols = K*2 + c.
+// ---------------------------------------------------------------------------------------
+struct MacGeom {
+  int nIs, nIb, nJ, nC, CW, nCg, nSb, LN;
+};
+
+__host__ __device__ __forceinline__ size_t w_index(const MacGeom &g, int iloc, int J, int s) {
+  return ((((size_t)(iloc >> 4) * g.nSb + (s >> 5)) * g.nJ + J) * 32 + (s & 31)) * 16 + (iloc & 15);
+}
+
+// u32-word offset of the X chunk of (J, column group cg, slot block sb): 96*CW words (3 KB at CW=8)
+__host__ __device__ __forceinline__ size_t x_chunk(const MacGeom &g, int J, int cg, int sb) {
+  return (((size_t)sb * g.nCg + cg) * g.nJ + J) * (size_t)(96 * g.CW);
+}
+
+MacGeom mac_geom(const hl_ctx *c, int64_t nIs, int64_t nJ, int64_t nC) {
+  MacGeom g;
+  g.nIs = (int)nIs; g.nIb = (int)((nIs + 15) / 16); g.nJ = (int)nJ; g.nC = (int)nC;
+  g.CW = (nC % 8 == 0) ? 8 : ((nC % 4 == 0) ? 4 : 2);
+  g.nCg = (int)(nC / g.CW);
+  g.LN = (int)(c->L * c->N);
+  g.nSb = g.LN / 32;
+  return g;
+}
+
+// ---------------------------------------------------------------------------------------
 // Forward NTT kernels
 // ---------------------------------------------------------------------------------------
-// (a) ciphertext polynomials: in [npoly][L][N] coefficient form -> out uint2 limbs [npoly][L][N]
-template <int LOGN, bool SPLIT>
+// (a) ciphertext polynomials: in [npoly][L][N] coefficient form ->
+//     MODE 0: u64 [npoly][L][N] in slot order (diagnostics)
+//     MODE 1: limb pairs in the blocked X layout (poly = J*nC + col), the MAC operand
+template <int LOGN, int MODE>
 __global__ void __launch_bounds__(Geom<LOGN>::NT)
-k_ntt_fwd(const uint64_t *__restrict__ in, void *__restrict__ out, DevParams P) {
+k_ntt_fwd(const uint64_t *__restrict__ in, void *__restrict__ out, DevParams P, MacGeom mg) {
   using Gm = Geom<LOGN>;
   extern __shared__ uint64_t sm[];
   const int t = threadIdx.x, l = blockIdx.y;
@@ -224,12 +259,17 @@ k_ntt_fwd(const uint64_t *__restrict__ in, void *__restrict__ out, DevParams P) 
 #pragma unroll
     for (int u = 0; u < (1 << K); u++) a[g * (1 << K) + u] = __ldcs(in + base + elem_idx<LOGN, 0>(t, g, u));
   fwd_rounds_from<LOGN, 0>(a, sm, t, tw, pc.p, pc.two_p);
+  const int J = (int)(blockIdx.x / (unsigned)max(mg.nC, 1)), col = (int)(blockIdx.x % (unsigned)max(mg.nC, 1));
 #pragma unroll
   for (int u = 0; u < 16; u++) {
     const uint64_t x = canon4(a[u], pc.p, pc.two_p);
-    if constexpr (SPLIT) {
-      reinterpret_cast<uint2 *>(out)[base + slot_of<LOGN>(t, u)] =
-          make_uint2((uint32_t)x & kLimbMask, (uint32_t)(x >> kLimbBits));
+    if constexpr (MODE == 1) {
+      const int s = l * Gm::N + slot_of<LOGN>(t, u);
+      uint32_t *ch = reinterpret_cast<uint32_t *>(out) + x_chunk(mg, J, col / mg.CW, s >> 5);
+      const int e = (s & 31) * mg.CW + col % mg.CW;
+      const uint32_t x0 = (uint32_t)x & kLimbMask, x1 = (uint32_t)(x >> kLimbBits);
+      reinterpret_cast<uint2 *>(ch)[e] = make_uint2(x0, x1);
+      ch[64 * mg.CW + e] = x0 + x1;
     } else {
       reinterpret_cast<uint64_t *>(out)[base + slot_of<LOGN>(t, u)] = x;
     }
@@ -237,11 +277,12 @@ k_ntt_fwd(const uint64_t *__restrict__ in, void *__restrict__ out, DevParams P) 
 }
 
 // (b) weights: pi_A of tile (I, J), centered lift (reading C6), mod p_l, NTT.
-//     poly index = I_loc * nJ + J; wcache uint2 [nIs][nJ][L][N].
+//     poly index = I_loc * nJ + J over the 16-padded shard; wcache in the blocked W layout.
 struct EncodeArgs {
   const uint64_t *W;
-  int64_t R, Ma, nJ, i_begin;
+  int64_t R, Ma, nJ, nIs, i_begin;
   int m, r;
+  MacGeom mg;
 };
 
 template <int LOGN>
@@ -265,7 +306,7 @@ k_encode_weights(EncodeArgs A, uint2 *__restrict__ wcache, DevParams P, uint32_t
     for (int u = 0; u < (1 << K); u++) {
       const int e = elem_idx<LOGN, 0>(t, g, u);
       uint64_t v = 0;
-      if (e < mr) {
+      if (e < mr && Iloc < A.nIs) {          // rows padded up to 16 are zero polynomials
         const int i = e / A.r, j = A.r - 1 - e % A.r;
         const int64_t row = J * A.r + j, col = I * A.m + i;
         if (row < A.R && col < A.Ma) {
@@ -290,11 +331,11 @@ k_encode_weights(EncodeArgs A, uint2 *__restrict__ wcache, DevParams P, uint32_t
     if (maxabs) atomicMax(&flags[1], maxabs);
   }
   fwd_rounds_from<LOGN, 0>(a, sm, t, tw, pc.p, pc.two_p);
-  const size_t base = ((size_t)poly * P.L + l) * Gm::N;
 #pragma unroll
   for (int u = 0; u < 16; u++) {
     const uint64_t x = canon4(a[u], pc.p, pc.two_p);
-    wcache[base + slot_of<LOGN>(t, u)] = make_uint2((uint32_t)x & kLimbMask, (uint32_t)(x >> kLimbBits));
+    const int s = l * Gm::N + slot_of<LOGN>(t, u);
+    wcache[w_index(A.mg, (int)Iloc, (int)J, s)] = make_uint2((uint32_t)x & kLimbMask, (uint32_t)(x >> kLimbBits));
   }
 }
 
@@ -465,104 +506,194 @@ __global__ void k_mask(const uint64_t *__restrict__ ct_out, uint64_t *__restrict
 }
 
 // ---------------------------------------------------------------------------------------
-// Slot-parallel modular MAC (the dominant kernel).
-//   W   uint2 [nIs][nJ][LN]     X uint2 [nJ][nC][LN]     out u64 [nIs][nC][LN]
+// Slot-parallel modular MAC (the dominant kernel), persistent and warp-specialised.
 //   out[I][col][s] (+)= sum_{J in [j0, j1)} W[I][J][s] * X[J][col][s]  mod p_{s / N}
-// Warp = 32 consecutive slots; each thread owns a TI x TC register tile of outputs.  The 8
-// warps of a CTA share the slots (X re-use through L1) and step over (I-tile, C-tile) pairs
-// with the I tile fastest.  W is streamed once (evict-first loads).
+// A tile is 16 rows (I) x 32 slots x CW columns.  Warp 8 (producer) streams, for every J, the
+// tile's W chunk (4 KB) and X chunk (256*CW B) into a NST-deep shared-memory ring with
+// cp.async.bulk (TMA bulk copies completing on mbarriers).  Warps 0-7 (consumers) each own 4
+// slots: lane = (row = lane & 15, slot pair half = lane >> 4), 2 slots x CW columns per thread,
+// three IMAD.WIDE.U32 per modular MAC (Karatsuba on 25-bit limbs) into exact 64-bit lazy
+// accumulators.  The epilogue reduces mod p (one 128-bit reduction per output), transposes
+// through shared memory and stores 256-B rows of out[I][col][LN] (the inverse NTT's input).
 // ---------------------------------------------------------------------------------------
 struct MacArgs {
   const uint2 *W;
-  const uint2 *X;
+  const uint32_t *X;
   uint64_t *out;
-  int nI, nJ, nC, j0, j1, LN, N;
-  int accumulate;
+  MacGeom g;
+  int N, j0, j1, accumulate;
 };
 
-__device__ __forceinline__ uint2 ld_stream(const uint2 *p) {
-  uint2 v;
-  asm volatile("ld.global.nc.L1::no_allocate.v2.u32 {%0, %1}, [%2];"
-               : "=r"(v.x), "=r"(v.y) : "l"(p));
-  return v;
+__device__ __forceinline__ uint32_t smem_u32(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+__device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
 }
 
-template <int TI, int TC>
-__global__ void __launch_bounds__(256)
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra WAIT_%=;\n}" ::"r"(smem_u32(bar)), "r"(parity) : "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
+__device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+
+__device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t bytes, uint64_t *bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+               ::"r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar)) : "memory");
+}
+
+template <int CW>
+struct MacSmem {
+  static constexpr int W_BYTES = 32 * 16 * 8;
+  static constexpr int X_BYTES = 32 * CW * 12;
+  static constexpr int STAGE = W_BYTES + X_BYTES;
+  static constexpr int E_STRIDE = CW * 32 + 1;               // odd row stride: conflict-free transpose
+  static constexpr int E_BYTES = 16 * E_STRIDE * 8;
+};
+
+constexpr int kMacStages = 8;
+constexpr int kMacThreads = 9 * 32;
+
+template <int CW, int LN, int NST>
+__global__ void __launch_bounds__(kMacThreads, 1)
 k_mac(MacArgs A, DevParams P) {
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int s = blockIdx.y * 32 + lane;
-  const int nIt = (A.nI + TI - 1) / TI, nCt = (A.nC + TC - 1) / TC;
-  const int tile = blockIdx.x * 8 + warp;
-  if (tile >= nIt * nCt) return;
-  const int I0 = (tile % nIt) * TI, C0 = (tile / nIt) * TC;
-  const size_t LN = (size_t)A.LN;
+  using S = MacSmem<CW>;
+  extern __shared__ __align__(128) unsigned char smem[];
+  uint64_t *full = reinterpret_cast<uint64_t *>(smem + NST * S::STAGE + S::E_BYTES);
+  uint64_t *empty = full + NST;
+  uint64_t *ebuf = reinterpret_cast<uint64_t *>(smem + NST * S::STAGE);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const MacGeom &g = A.g;
+  const int ntiles = g.nIb * g.nCg * g.nSb;
+  const int nj = A.j1 - A.j0;
 
-  uint64_t lo[TI][TC], hi[TI][TC], md[TI][TC];
-#pragma unroll
-  for (int a = 0; a < TI; a++)
-#pragma unroll
-    for (int b = 0; b < TC; b++) lo[a][b] = hi[a][b] = md[a][b] = 0;
-
-  const uint2 *Wp[TI];
-#pragma unroll
-  for (int a = 0; a < TI; a++) {
-    const int I = min(I0 + a, A.nI - 1);       // clamped rows are computed but not stored
-    Wp[a] = A.W + ((size_t)I * A.nJ) * LN + s;
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < NST; i++) { mbar_init(&full[i], 1); mbar_init(&empty[i], 8); }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  const uint2 *Xp[TC];
-#pragma unroll
-  for (int b = 0; b < TC; b++) {
-    const int C = min(C0 + b, A.nC - 1);
-    Xp[b] = A.X + (size_t)C * LN + s;
-  }
-  const size_t xstride = (size_t)A.nC * LN;
+  __syncthreads();
 
-#pragma unroll 2
-  for (int J = A.j0; J < A.j1; J++) {
-    uint2 w[TI], x[TC];
-#pragma unroll
-    for (int a = 0; a < TI; a++) w[a] = ld_stream(Wp[a] + (size_t)J * LN);
-#pragma unroll
-    for (int b = 0; b < TC; b++) x[b] = __ldg(Xp[b] + (size_t)J * xstride);
-    uint32_t xs[TC];
-#pragma unroll
-    for (int b = 0; b < TC; b++) xs[b] = x[b].x + x[b].y;
-#pragma unroll
-    for (int a = 0; a < TI; a++) {
-      const uint32_t ws = w[a].x + w[a].y;
-#pragma unroll
-      for (int b = 0; b < TC; b++) {
-        lo[a][b] += (uint64_t)w[a].x * x[b].x;
-        hi[a][b] += (uint64_t)w[a].y * x[b].y;
-        md[a][b] += (uint64_t)ws * xs[b];
+  if (warp == 8) {
+    // ------------------------------------------------------------------ producer
+    if (lane == 0) {
+      uint32_t it = 0;
+      for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+        const int ib = tile % g.nIb, cg = (tile / g.nIb) % g.nCg, sb = tile / (g.nIb * g.nCg);
+        const uint2 *wsrc = A.W + (((size_t)ib * g.nSb + sb) * g.nJ + A.j0) * 512;
+        const uint32_t *xsrc = A.X + x_chunk(g, A.j0, cg, sb);
+        for (int j = 0; j < nj; j++, it++) {
+          const int st = it % NST;
+          mbar_wait(&empty[st], ((it / NST) & 1) ^ 1);
+          unsigned char *dst = smem + st * S::STAGE;
+          mbar_expect_tx(&full[st], S::STAGE);
+          bulk_g2s(dst, wsrc + (size_t)j * 512, S::W_BYTES, &full[st]);
+          bulk_g2s(dst + S::W_BYTES, xsrc + (size_t)j * 96 * CW, S::X_BYTES, &full[st]);
+        }
       }
     }
+    return;
   }
 
-  const int l = s / A.N;
-  const PrimeConsts pc = pick(P, l);
+  // -------------------------------------------------------------------- consumers
+  const int row = lane & 15;
+  const int sl0 = 4 * warp + (lane >> 4), sl1 = sl0 + 2;      // the two slots of this thread
+  uint32_t it = 0;
+  for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    const int ib = tile % g.nIb, cg = (tile / g.nIb) % g.nCg, sb = tile / (g.nIb * g.nCg);
+    uint64_t lo[2][CW], hi[2][CW], md[2][CW];
 #pragma unroll
-  for (int a = 0; a < TI; a++) {
-    if (I0 + a >= A.nI) continue;
+    for (int p = 0; p < 2; p++)
 #pragma unroll
-    for (int b = 0; b < TC; b++) {
-      if (C0 + b >= A.nC) continue;
-      const uint64_t mid = md[a][b] - lo[a][b] - hi[a][b];     // exact: x0 y1 + x1 y0
-      // V = hi 2^50 + mid 2^25 + lo  (< 2^113)
-      const hl_u128 V = ((hl_u128)hi[a][b] << (2 * kLimbBits)) + ((hl_u128)mid << kLimbBits) + lo[a][b];
-      const uint64_t vh = (uint64_t)(V >> 64), vl = (uint64_t)V;
-      const uint64_t r1 = shoup_mul(vh, pc.r64, pc.r64_sh, pc.p);           // vh 2^64 mod p, [0, 2p)
-      const uint64_t r2 = vl - __umul64hi(vl, pc.mu) * pc.p;                // vl mod p, [0, 2p)
-      uint64_t r = r1 + r2;
-      r = r >= pc.two_p ? r - pc.two_p : r;
-      r = r >= pc.p ? r - pc.p : r;
-      uint64_t *dst = A.out + ((size_t)(I0 + a) * A.nC + C0 + b) * LN + s;
-      if (A.accumulate) {
-        r += *dst;
-        r = r >= pc.p ? r - pc.p : r;
+      for (int b = 0; b < CW; b++) lo[p][b] = hi[p][b] = md[p][b] = 0;
+
+    for (int j = 0; j < nj; j++, it++) {
+      const int st = it % NST;
+      mbar_wait(&full[st], (it / NST) & 1);
+      const uint2 *sW = reinterpret_cast<const uint2 *>(smem + st * S::STAGE);
+      const uint2 *sX = reinterpret_cast<const uint2 *>(smem + st * S::STAGE + S::W_BYTES);
+      const uint32_t *sXs = reinterpret_cast<const uint32_t *>(smem + st * S::STAGE + S::W_BYTES + 32 * CW * 8);
+      uint2 w[2];
+      uint2 x[2][CW];
+      uint32_t xsum[2][CW];
+      w[0] = sW[sl0 * 16 + row];
+      w[1] = sW[sl1 * 16 + row];
+#pragma unroll
+      for (int q = 0; q < CW / 2; q++) {
+        const uint4 v0 = *reinterpret_cast<const uint4 *>(&sX[sl0 * CW + 2 * q]);
+        const uint4 v1 = *reinterpret_cast<const uint4 *>(&sX[sl1 * CW + 2 * q]);
+        x[0][2 * q] = make_uint2(v0.x, v0.y); x[0][2 * q + 1] = make_uint2(v0.z, v0.w);
+        x[1][2 * q] = make_uint2(v1.x, v1.y); x[1][2 * q + 1] = make_uint2(v1.z, v1.w);
       }
-      *dst = r;
+#pragma unroll
+      for (int p = 0; p < 2; p++) {
+        const int sl = p ? sl1 : sl0;
+        if constexpr (CW >= 4) {
+#pragma unroll
+          for (int q = 0; q < CW / 4; q++) {
+            const uint4 v = *reinterpret_cast<const uint4 *>(&sXs[sl * CW + 4 * q]);
+            xsum[p][4 * q] = v.x; xsum[p][4 * q + 1] = v.y; xsum[p][4 * q + 2] = v.z; xsum[p][4 * q + 3] = v.w;
+          }
+        } else {
+          const uint2 v = *reinterpret_cast<const uint2 *>(&sXs[sl * CW]);
+          xsum[p][0] = v.x; xsum[p][1] = v.y;
+        }
+      }
+#pragma unroll
+      for (int p = 0; p < 2; p++) {
+        const uint32_t ws = w[p].x + w[p].y;
+#pragma unroll
+        for (int b = 0; b < CW; b++) {
+          const uint32_t xs = xsum[p][b];
+          lo[p][b] += (uint64_t)w[p].x * x[p][b].x;
+          hi[p][b] += (uint64_t)w[p].y * x[p][b].y;
+          md[p][b] += (uint64_t)ws * xs;
+        }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[st]);
+    }
+
+    // ---------------- epilogue: reduce, transpose through smem, coalesced stores
+    const int l = (sb * 32) / A.N;
+    const PrimeConsts pc = pick(P, l);
+    asm volatile("bar.sync 1, 256;" ::: "memory");       // previous tile's ebuf reads are done
+#pragma unroll
+    for (int p = 0; p < 2; p++) {
+      const int sl = p ? sl1 : sl0;
+#pragma unroll
+      for (int b = 0; b < CW; b++) {
+        const uint64_t mid = md[p][b] - lo[p][b] - hi[p][b];          // exact: x0 y1 + x1 y0
+        const hl_u128 V = ((hl_u128)hi[p][b] << (2 * kLimbBits)) + ((hl_u128)mid << kLimbBits) + lo[p][b];
+        const uint64_t vh = (uint64_t)(V >> 64), vl = (uint64_t)V;
+        const uint64_t r1 = shoup_mul(vh, pc.r64, pc.r64_sh, pc.p);   // vh * 2^64 mod p, [0, 2p)
+        const uint64_t r2 = vl - __umul64hi(vl, pc.mu) * pc.p;        // vl mod p, [0, 2p)
+        uint64_t r = r1 + r2;
+        r = r >= pc.two_p ? r - pc.two_p : r;
+        r = r >= pc.p ? r - pc.p : r;
+        ebuf[row * S::E_STRIDE + b * 32 + sl] = r;
+      }
+    }
+    asm volatile("bar.sync 1, 256;" ::: "memory");
+    const int I0 = ib * 16;
+    for (int e = threadIdx.x; e < 16 * CW * 32; e += 256) {
+      const int rr = e / (CW * 32), b = (e / 32) % CW, sl = e % 32;
+      if (I0 + rr >= g.nIs) continue;
+      uint64_t v = ebuf[rr * S::E_STRIDE + b * 32 + sl];
+      uint64_t *dst = A.out + ((size_t)(I0 + rr) * g.nC + cg * CW + b) * LN + sb * 32 + sl;
+      if (A.accumulate) {
+        v += *dst;
+        v = v >= pc.p ? v - pc.p : v;
+      }
+      *dst = v;
     }
   }
 }
@@ -587,12 +718,13 @@ void set_smem(Kern k, size_t bytes) {
 template <int LOGN>
 constexpr size_t ntt_smem() { return (size_t)Geom<LOGN>::SMEM_WORDS * 8; }
 
-template <int LOGN, bool SPLIT>
-void launch_fwd(const hl_ctx *c, const uint64_t *in, void *out, int64_t npoly, cudaStream_t st) {
+template <int LOGN, int MODE>
+void launch_fwd(const hl_ctx *c, const uint64_t *in, void *out, int64_t npoly, const MacGeom &mg, cudaStream_t st) {
   static bool init = false;
-  if (!init) { set_smem(k_ntt_fwd<LOGN, SPLIT>, ntt_smem<LOGN>()); init = true; }
+  if (!init) { set_smem(k_ntt_fwd<LOGN, MODE>, ntt_smem<LOGN>()); init = true; }
   dim3 grid((unsigned)npoly, c->L);
-  k_ntt_fwd<LOGN, SPLIT><<<grid, Geom<LOGN>::NT, ntt_smem<LOGN>(), st>>>(in, out, c->dp);
+  KTimer kt(c, MODE ? HL_K_NTT_FWD : HL_K_OTHER, st);
+  k_ntt_fwd<LOGN, MODE><<<grid, Geom<LOGN>::NT, ntt_smem<LOGN>(), st>>>(in, out, c->dp, mg);
 }
 
 template <int LOGN>
@@ -600,38 +732,54 @@ void launch_inv(const hl_ctx *c, const uint64_t *in, uint64_t *out, int64_t npol
   static bool init = false;
   if (!init) { set_smem(k_ntt_inv<LOGN>, ntt_smem<LOGN>()); init = true; }
   dim3 grid((unsigned)npoly, c->L);
+  KTimer kt(c, HL_K_INTT, st);
   k_ntt_inv<LOGN><<<grid, Geom<LOGN>::NT, ntt_smem<LOGN>(), st>>>(in, out, c->dp);
 }
 
-void fwd_ntt(const hl_ctx *c, const uint64_t *in, void *out, int64_t npoly, bool split, cudaStream_t st) {
-  if (c->N == 4096) { if (split) launch_fwd<12, true>(c, in, out, npoly, st); else launch_fwd<12, false>(c, in, out, npoly, st); }
-  else { if (split) launch_fwd<13, true>(c, in, out, npoly, st); else launch_fwd<13, false>(c, in, out, npoly, st); }
+// MODE 0 (u64, slot order) when mg == nullptr, else MODE 1 (blocked X limbs)
+void fwd_ntt(const hl_ctx *c, const uint64_t *in, void *out, int64_t npoly, const MacGeom *mg, cudaStream_t st) {
+  MacGeom z{};
+  if (c->N == 4096) { if (mg) launch_fwd<12, 1>(c, in, out, npoly, *mg, st); else launch_fwd<12, 0>(c, in, out, npoly, z, st); }
+  else { if (mg) launch_fwd<13, 1>(c, in, out, npoly, *mg, st); else launch_fwd<13, 0>(c, in, out, npoly, z, st); }
 }
 
 void inv_ntt(const hl_ctx *c, const uint64_t *in, uint64_t *out, int64_t npoly, cudaStream_t st) {
   if (c->N == 4096) launch_inv<12>(c, in, out, npoly, st); else launch_inv<13>(c, in, out, npoly, st);
 }
 
-template <int TI, int TC>
-void launch_mac_t(const hl_ctx *c, MacArgs A, cudaStream_t st) {
-  const int nIt = (A.nI + TI - 1) / TI, nCt = (A.nC + TC - 1) / TC;
-  dim3 grid((unsigned)((nIt * nCt + 7) / 8), (unsigned)(A.LN / 32));
-  k_mac<TI, TC><<<grid, 256, 0, st>>>(A, c->dp);
+template <int CW, int LN>
+void launch_mac_t(const hl_ctx *c, const MacArgs &A, cudaStream_t st) {
+  using S = MacSmem<CW>;
+  constexpr size_t smem = (size_t)kMacStages * S::STAGE + S::E_BYTES + 2 * kMacStages * 8;
+  static bool init = false;
+  if (!init) { set_smem(k_mac<CW, LN, kMacStages>, smem); init = true; }
+  const int ntiles = A.g.nIb * A.g.nCg * A.g.nSb;
+  const int grid = std::min(ntiles, c->num_sms);
+  KTimer kt(c, HL_K_MAC, st);
+  k_mac<CW, LN, kMacStages><<<grid, kMacThreads, smem, st>>>(A, c->dp);
 }
 
-void launch_mac(const hl_ctx *c, const uint2 *W, const uint2 *X, uint64_t *out, int64_t nIs, int64_t nJ,
-                int64_t nC, cudaStream_t st) {
+template <int LN>
+void launch_mac_ln(const hl_ctx *c, const MacArgs &A, cudaStream_t st) {
+  if (A.g.CW == 8) launch_mac_t<8, LN>(c, A, st);
+  else if (A.g.CW == 4) launch_mac_t<4, LN>(c, A, st);
+  else launch_mac_t<2, LN>(c, A, st);
+}
+
+void launch_mac(const hl_ctx *c, const uint2 *W, const uint32_t *X, uint64_t *out, const MacGeom &g, cudaStream_t st) {
   MacArgs A;
-  A.W = W; A.X = X; A.out = out;
-  A.nI = (int)nIs; A.nJ = (int)nJ; A.nC = (int)nC;
-  A.LN = (int)(c->L * c->N); A.N = (int)c->N;
-  for (int64_t j0 = 0; j0 < nJ; j0 += kMacJChunk) {
-    A.j0 = (int)j0; A.j1 = (int)std::min<int64_t>(nJ, j0 + kMacJChunk);
+  A.W = W; A.X = X; A.out = out; A.g = g; A.N = (int)c->N;
+  for (int64_t j0 = 0; j0 < g.nJ; j0 += kMacJChunk) {
+    A.j0 = (int)j0; A.j1 = (int)std::min<int64_t>(g.nJ, j0 + kMacJChunk);
     A.accumulate = j0 > 0;
-    if (nC >= 8) launch_mac_t<2, 8>(c, A, st);
-    else if (nC >= 4) launch_mac_t<4, 4>(c, A, st);
-    else if (nC >= 2) launch_mac_t<8, 2>(c, A, st);
-    else launch_mac_t<8, 1>(c, A, st);
+    switch (g.LN) {
+      case 4096: launch_mac_ln<4096>(c, A, st); break;
+      case 8192: launch_mac_ln<8192>(c, A, st); break;
+      case 12288: launch_mac_ln<12288>(c, A, st); break;
+      case 16384: launch_mac_ln<16384>(c, A, st); break;
+      case 24576: launch_mac_ln<24576>(c, A, st); break;
+      default: break;
+    }
   }
 }
 
@@ -641,6 +789,7 @@ void launch_inv_mask(const hl_ctx *c, const uint64_t *ct_ntt, uint64_t *masked, 
   static bool init = false;
   if (!init) { set_smem(k_ntt_inv_mask<LOGN>, ntt_smem<LOGN>() + (size_t)Geom<LOGN>::N * 8); init = true; }
   const size_t smem = ntt_smem<LOGN>() + (size_t)M.m * M.n * 8;
+  KTimer kt(c, HL_K_INTT_MASK, st);
   k_ntt_inv_mask<LOGN><<<(unsigned)(nout * 2), Geom<LOGN>::NT, smem, st>>>(ct_ntt, masked, share, M, c->dp);
 }
 
@@ -666,8 +815,11 @@ extern "C" int hl_encode_weights(const hl_ctx *c, hl_tile tile, const uint64_t *
   cudaStream_t st = (cudaStream_t)stream;
   cudaSetDevice(c->device);
   cudaMemsetAsync(c->d_flags, 0, 8, st);
-  EncodeArgs A{W, R, Ma, g.nJ, g.i_begin, g.m, g.r};
-  dim3 grid((unsigned)(g.nIs * g.nJ), c->L);
+  const MacGeom mg = mac_geom(c, g.nIs, g.nJ, 2 * g.nK);
+  EncodeArgs A{W, R, Ma, g.nJ, g.nIs, g.i_begin, g.m, g.r, mg};
+  dim3 grid((unsigned)((int64_t)mg.nIb * 16 * g.nJ), c->L);
+  {
+  KTimer kt(c, HL_K_ENCODE, st);
   if (c->N == 4096) {
     static bool init = false;
     if (!init) { set_smem(k_encode_weights<12>, ntt_smem<12>()); init = true; }
@@ -676,6 +828,7 @@ extern "C" int hl_encode_weights(const hl_ctx *c, hl_tile tile, const uint64_t *
     static bool init = false;
     if (!init) { set_smem(k_encode_weights<13>, ntt_smem<13>()); init = true; }
     k_encode_weights<13><<<grid, Geom<13>::NT, ntt_smem<13>(), st>>>(A, (uint2 *)wcache, c->dp, c->d_flags);
+  }
   }
   if ((rc = hl_cuda_check("hl_encode_weights: launch"))) return rc;
   uint32_t flags[2];
@@ -699,8 +852,9 @@ extern "C" int hl_he_matmul(const hl_ctx *c, hl_tile tile, const void *wcache, i
   if ((rc = hl_geometry(c, tile, Ma, R, Nb, i_begin, i_end, &g))) return rc;
   cudaStream_t st = (cudaStream_t)stream;
   const int64_t nC = 2 * g.nK;
-  fwd_ntt(c, ct_in, workspace, g.nJ * nC, true, st);
-  launch_mac(c, (const uint2 *)wcache, (const uint2 *)workspace, ct_out, g.nIs, g.nJ, nC, st);
+  const MacGeom mg = mac_geom(c, g.nIs, g.nJ, nC);
+  fwd_ntt(c, ct_in, workspace, g.nJ * nC, &mg, st);
+  launch_mac(c, (const uint2 *)wcache, (const uint32_t *)workspace, ct_out, mg, st);
   inv_ntt(c, ct_out, ct_out, g.nIs * nC, st);
   return hl_cuda_check("hl_he_matmul: launch");
 }
@@ -721,6 +875,7 @@ extern "C" int hl_mask_and_share(const hl_ctx *c, hl_tile tile, int64_t Ma, int6
   if ((rc = hl_geometry(c, tile, Ma, 1, Nb, i_begin, i_end, &g))) return rc;
   cudaStream_t st = (cudaStream_t)stream;
   dim3 grid((unsigned)((c->N / 8 + 127) / 128), (unsigned)(g.nIs * g.nK));
+  KTimer kt(c, HL_K_MASK, st);
   k_mask<<<grid, 128, 0, st>>>(ct_out, ct_masked, share, mask_args(g, Ma, Nb, seed), c->dp, compress ? 1 : 0);
   return hl_cuda_check("hl_mask_and_share: launch");
 }
@@ -741,8 +896,9 @@ extern "C" int hl_he_matmul_share(const hl_ctx *c, hl_tile tile, const void *wca
   }
   cudaStream_t st = (cudaStream_t)stream;
   const int64_t nC = 2 * g.nK;
-  fwd_ntt(c, ct_in, workspace, g.nJ * nC, true, st);
-  launch_mac(c, (const uint2 *)wcache, (const uint2 *)workspace, ct_out_ntt, g.nIs, g.nJ, nC, st);
+  const MacGeom mg = mac_geom(c, g.nIs, g.nJ, nC);
+  fwd_ntt(c, ct_in, workspace, g.nJ * nC, &mg, st);
+  launch_mac(c, (const uint2 *)wcache, (const uint32_t *)workspace, ct_out_ntt, mg, st);
   MaskArgs M = mask_args(g, Ma, Nb, seed);
   if (c->N == 4096) launch_inv_mask<12>(c, ct_out_ntt, ct_masked, share, M, g.nIs * g.nK, st);
   else launch_inv_mask<13>(c, ct_out_ntt, ct_masked, share, M, g.nIs * g.nK, st);
@@ -781,9 +937,10 @@ extern "C" int hl_poly_mul(const hl_ctx *c, const uint64_t *a, const uint64_t *b
   cudaStream_t st = (cudaStream_t)stream;
   const int64_t n = npoly * c->L * c->N;
   uint64_t *s1 = (uint64_t *)scratch, *s2 = s1 + n;
-  fwd_ntt(c, a, s1, npoly, false, st);
-  fwd_ntt(c, b, s2, npoly, false, st);
-  k_pointwise<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(s1, s2, s1, n, c->dp);
+  fwd_ntt(c, a, s1, npoly, nullptr, st);
+  fwd_ntt(c, b, s2, npoly, nullptr, st);
+  { KTimer kt(c, HL_K_OTHER, st);
+  k_pointwise<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(s1, s2, s1, n, c->dp); }
   inv_ntt(c, s1, out, npoly, st);
   return hl_cuda_check("hl_poly_mul: launch");
 }
@@ -793,7 +950,7 @@ extern "C" int hl_ntt_roundtrip(const hl_ctx *c, uint64_t *x, int64_t npoly, voi
   if ((rc = check_ptrs({c, x, scratch}, "hl_ntt_roundtrip"))) return rc;
   if (npoly <= 0) return hl_fail(HL_EINVAL, "hl_ntt_roundtrip: npoly must be positive");
   cudaStream_t st = (cudaStream_t)stream;
-  fwd_ntt(c, x, scratch, npoly, false, st);
+  fwd_ntt(c, x, scratch, npoly, nullptr, st);
   inv_ntt(c, (uint64_t *)scratch, x, npoly, st);
   return hl_cuda_check("hl_ntt_roundtrip: launch");
 }

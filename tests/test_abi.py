@@ -73,7 +73,7 @@ def test_layout_and_dims(hl):
     assert lay.ct_masked_words == 144 * 4 * 2 * (16 * 32 + 4096)
     assert lay.wcache_bytes == 144 * 96 * 2 * 4096 * 8
     sh = ctx.layout((16, 8, 32), 2304, 768, 128, 10, 20)
-    assert sh.nI_shard == 10 and sh.wcache_bytes == 10 * 96 * 2 * 4096 * 8
+    assert sh.nI_shard == 10 and sh.wcache_bytes == 16 * 96 * 2 * 4096 * 8   # rows padded to 16
     with pytest.raises(hl.HLError) as e:
         ctx.layout((16, 16, 32), 64, 64, 64)          # m*r*n = 8192 > N
     assert e.value.code == hl.HL_EDIM
