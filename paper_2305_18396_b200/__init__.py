@@ -27,7 +27,8 @@ _CODES = {HL_EINVAL: "HL_EINVAL", HL_EDIM: "HL_EDIM", HL_ERANGE: "HL_ERANGE", HL
           HL_ECUDA: "HL_ECUDA", HL_ENOTSUP: "HL_ENOTSUP"}
 
 # every symbol include/helinear.h declares (checked by tests/test_abi.py)
-EXPORTS = ("hl_last_error", "hl_ctx_create", "hl_ctx_destroy", "hl_ctx_params", "hl_layout_query",
+EXPORTS = ("hl_last_error", "hl_ctx_create", "hl_ctx_destroy", "hl_ctx_params", "hl_ctx_set_mac_engine",
+           "hl_layout_query",
            "hl_keygen", "hl_encrypt", "hl_decrypt_share", "hl_encode_weights", "hl_he_matmul",
            "hl_mask_and_share", "hl_he_matmul_share", "hl_he_linear_host", "hl_poly_mul",
            "hl_ntt_roundtrip", "hl_timing_enable", "hl_timing_read")
@@ -86,6 +87,7 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
         "hl_ctx_create": [ctypes.c_uint32, ctypes.c_uint32, ctypes.c_uint32, vp, i32, ctypes.POINTER(vp)],
         "hl_ctx_destroy": [vp],
         "hl_ctx_params": [vp, vp, vp],
+        "hl_ctx_set_mac_engine": [vp, i32],
         "hl_layout_query": [vp, Tile, i64, i64, i64, i64, i64, ctypes.POINTER(_Layout)],
         "hl_keygen": [vp, u64, vp],
         "hl_encrypt": [vp, vp, Tile, vp, i64, i64, u64, vp],
@@ -159,6 +161,12 @@ class Context:
         _check(lib.hl_ctx_params(h, p.ctypes.data, d.ctypes.data))
         self.primes = tuple(int(v) for v in p)
         self.delta_mod = tuple(int(v) for v in d)
+
+    MAC_IMAD, MAC_F64 = 0, 1
+
+    def set_mac_engine(self, engine: int):
+        """0 = IMAD.WIDE limbs, 1 = exact FP64 products (default).  Re-encode weights after."""
+        _check(_lib.hl_ctx_set_mac_engine(self._h, int(engine)))
 
     def close(self):
         if getattr(self, "_h", None):

@@ -7,6 +7,7 @@
 #include <quadmath.h>
 
 #include <cmath>
+#include <cstdlib>
 #include <cstdio>
 #include <cstring>
 #include <string>
@@ -189,6 +190,7 @@ extern "C" int hl_ctx_create(uint32_t N, uint32_t L, uint32_t log2_t, const uint
     pc.ninv_w1_sh = h_shoup(pc.ninv_w1, p);
   }
   build_cdt(c->cdt);
+  if (const char *e = getenv("HELINEAR_MAC_ENGINE")) c->mac_engine = (strcmp(e, "imad") == 0) ? 0 : 1;
   // device tables (device < 0: host-only context for the client calls; no CUDA needed)
   if (device < 0) {
     dp.tw_fwd = dp.tw_inv = nullptr;
@@ -267,6 +269,13 @@ extern "C" int hl_ctx_destroy(hl_ctx *c) {
   if (c->d_tw) cudaFree(c->d_tw);
   if (c->d_flags) cudaFree(c->d_flags);
   delete c;
+  return HL_OK;
+}
+
+extern "C" int hl_ctx_set_mac_engine(hl_ctx *c, int engine) {
+  if (!c) return hl_fail(HL_EINVAL, "hl_ctx_set_mac_engine: ctx is NULL");
+  if (engine != 0 && engine != 1) return hl_fail(HL_EINVAL, "hl_ctx_set_mac_engine: engine must be 0 or 1");
+  c->mac_engine = engine;
   return HL_OK;
 }
 

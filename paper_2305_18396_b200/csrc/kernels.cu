@@ -216,15 +216,19 @@ __device__ __forceinline__ int slot_of(int t, int u) { return u * Geom<LOGN>::NT
 // ---------------------------------------------------------------------------------------
 struct MacGeom {
   int nIs, nIb, nJ, nC, CW, nCg, nSb, LN;
+  int f64;       // MAC engine: 0 = IMAD.WIDE on 25-bit limbs, 1 = exact FP64 (DFMA) products
 };
 
 __host__ __device__ __forceinline__ size_t w_index(const MacGeom &g, int iloc, int J, int s) {
   return ((((size_t)(iloc >> 4) * g.nSb + (s >> 5)) * g.nJ + J) * 32 + (s & 31)) * 16 + (iloc & 15);
 }
 
-// u32-word offset of the X chunk of (J, column group cg, slot block sb): 96*CW words (3 KB at CW=8)
+// u32-word offset of the X chunk of (J, column group cg, slot block sb):
+//   IMAD engine: 96*CW words ([32][CW] limb pairs + [32][CW] limb sums, 3 KB at CW = 8)
+//   FP64 engine: 64*CW words ([32][CW] doubles, 2 KB at CW = 8)
+__host__ __device__ __forceinline__ int x_chunk_words(const MacGeom &g) { return (g.f64 ? 64 : 96) * g.CW; }
 __host__ __device__ __forceinline__ size_t x_chunk(const MacGeom &g, int J, int cg, int sb) {
-  return (((size_t)sb * g.nCg + cg) * g.nJ + J) * (size_t)(96 * g.CW);
+  return (((size_t)sb * g.nCg + cg) * g.nJ + J) * (size_t)x_chunk_words(g);
 }
 
 MacGeom mac_geom(const hl_ctx *c, int64_t nIs, int64_t nJ, int64_t nC) {
@@ -234,6 +238,7 @@ MacGeom mac_geom(const hl_ctx *c, int64_t nIs, int64_t nJ, int64_t nC) {
   g.nCg = (int)(nC / g.CW);
   g.LN = (int)(c->L * c->N);
   g.nSb = g.LN / 32;
+  g.f64 = c->mac_engine == 1;
   return g;
 }
 
@@ -267,9 +272,13 @@ k_ntt_fwd(const uint64_t *__restrict__ in, void *__restrict__ out, DevParams P, 
       const int s = l * Gm::N + slot_of<LOGN>(t, u);
       uint32_t *ch = reinterpret_cast<uint32_t *>(out) + x_chunk(mg, J, col / mg.CW, s >> 5);
       const int e = (s & 31) * mg.CW + col % mg.CW;
-      const uint32_t x0 = (uint32_t)x & kLimbMask, x1 = (uint32_t)(x >> kLimbBits);
-      reinterpret_cast<uint2 *>(ch)[e] = make_uint2(x0, x1);
-      ch[64 * mg.CW + e] = x0 + x1;
+      if (mg.f64) {
+        reinterpret_cast<double *>(ch)[e] = (double)x;              // exact: x < 2^50
+      } else {
+        const uint32_t x0 = (uint32_t)x & kLimbMask, x1 = (uint32_t)(x >> kLimbBits);
+        reinterpret_cast<uint2 *>(ch)[e] = make_uint2(x0, x1);
+        ch[64 * mg.CW + e] = x0 + x1;
+      }
     } else {
       reinterpret_cast<uint64_t *>(out)[base + slot_of<LOGN>(t, u)] = x;
     }
@@ -335,7 +344,10 @@ k_encode_weights(EncodeArgs A, uint2 *__restrict__ wcache, DevParams P, uint32_t
   for (int u = 0; u < 16; u++) {
     const uint64_t x = canon4(a[u], pc.p, pc.two_p);
     const int s = l * Gm::N + slot_of<LOGN>(t, u);
-    wcache[w_index(A.mg, (int)Iloc, (int)J, s)] = make_uint2((uint32_t)x & kLimbMask, (uint32_t)(x >> kLimbBits));
+    if (A.mg.f64)
+      reinterpret_cast<double *>(wcache)[w_index(A.mg, (int)Iloc, (int)J, s)] = (double)x;   // exact
+    else
+      wcache[w_index(A.mg, (int)Iloc, (int)J, s)] = make_uint2((uint32_t)x & kLimbMask, (uint32_t)(x >> kLimbBits));
   }
 }
 
@@ -560,8 +572,9 @@ struct MacSmem {
   static constexpr int E_BYTES = 16 * E_STRIDE * 8;
 };
 
-constexpr int kMacStages = 8;
-constexpr int kMacThreads = 9 * 32;
+constexpr int kMacStages = 16;                     // IMAD engine ring depth (16 x 7 KB in flight per SM)
+constexpr int kMacConsumerWarps = 16;                      // one slot per thread, 2 slots per warp
+constexpr int kMacThreads = (kMacConsumerWarps + 1) * 32;  // + 1 producer warp
 
 template <int CW, int LN, int NST>
 __global__ void __launch_bounds__(kMacThreads, 1)
@@ -577,26 +590,27 @@ k_mac(MacArgs A, DevParams P) {
   const int nj = A.j1 - A.j0;
 
   if (threadIdx.x == 0) {
-    for (int i = 0; i < NST; i++) { mbar_init(&full[i], 1); mbar_init(&empty[i], 8); }
+    for (int i = 0; i < NST; i++) { mbar_init(&full[i], 1); mbar_init(&empty[i], kMacConsumerWarps); }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
 
-  if (warp == 8) {
+  if (warp == kMacConsumerWarps) {
     // ------------------------------------------------------------------ producer
     if (lane == 0) {
-      uint32_t it = 0;
+      int st = 0;
+      uint32_t phase = 1;                 // a fresh empty barrier completes "phase -1" (parity 1)
       for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
         const int ib = tile % g.nIb, cg = (tile / g.nIb) % g.nCg, sb = tile / (g.nIb * g.nCg);
         const uint2 *wsrc = A.W + (((size_t)ib * g.nSb + sb) * g.nJ + A.j0) * 512;
         const uint32_t *xsrc = A.X + x_chunk(g, A.j0, cg, sb);
-        for (int j = 0; j < nj; j++, it++) {
-          const int st = it % NST;
-          mbar_wait(&empty[st], ((it / NST) & 1) ^ 1);
+        for (int j = 0; j < nj; j++) {
+          mbar_wait(&empty[st], phase);
           unsigned char *dst = smem + st * S::STAGE;
           mbar_expect_tx(&full[st], S::STAGE);
           bulk_g2s(dst, wsrc + (size_t)j * 512, S::W_BYTES, &full[st]);
           bulk_g2s(dst + S::W_BYTES, xsrc + (size_t)j * 96 * CW, S::X_BYTES, &full[st]);
+          if (++st == NST) { st = 0; phase ^= 1; }
         }
       }
     }
@@ -605,90 +619,242 @@ k_mac(MacArgs A, DevParams P) {
 
   // -------------------------------------------------------------------- consumers
   const int row = lane & 15;
-  const int sl0 = 4 * warp + (lane >> 4), sl1 = sl0 + 2;      // the two slots of this thread
-  uint32_t it = 0;
+  const int sl = 2 * warp + (lane >> 4);            // this thread's slot within the 32-slot block
+  constexpr int NCT = kMacConsumerWarps * 32;
+  int st = 0;
+  uint32_t phase = 0;
+  const int woff = (sl * 16 + row) * 8, xoff = S::W_BYTES + sl * CW * 8, soff = S::W_BYTES + 32 * CW * 8 + sl * CW * 4;
   for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
     const int ib = tile % g.nIb, cg = (tile / g.nIb) % g.nCg, sb = tile / (g.nIb * g.nCg);
-    uint64_t lo[2][CW], hi[2][CW], md[2][CW];
+    uint64_t lo[CW], hi[CW], md[CW];
 #pragma unroll
-    for (int p = 0; p < 2; p++)
-#pragma unroll
-      for (int b = 0; b < CW; b++) lo[p][b] = hi[p][b] = md[p][b] = 0;
+    for (int b = 0; b < CW; b++) lo[b] = hi[b] = md[b] = 0;
 
-    for (int j = 0; j < nj; j++, it++) {
-      const int st = it % NST;
-      mbar_wait(&full[st], (it / NST) & 1);
-      const uint2 *sW = reinterpret_cast<const uint2 *>(smem + st * S::STAGE);
-      const uint2 *sX = reinterpret_cast<const uint2 *>(smem + st * S::STAGE + S::W_BYTES);
-      const uint32_t *sXs = reinterpret_cast<const uint32_t *>(smem + st * S::STAGE + S::W_BYTES + 32 * CW * 8);
-      uint2 w[2];
-      uint2 x[2][CW];
-      uint32_t xsum[2][CW];
-      w[0] = sW[sl0 * 16 + row];
-      w[1] = sW[sl1 * 16 + row];
+#pragma unroll 1
+    for (int j = 0; j < nj; j++) {
+      mbar_wait(&full[st], phase);
+      const unsigned char *stage = smem + st * S::STAGE;
+      const uint2 w = *reinterpret_cast<const uint2 *>(stage + woff);
+      uint2 x[CW];
+      uint32_t xs[CW];
 #pragma unroll
       for (int q = 0; q < CW / 2; q++) {
-        const uint4 v0 = *reinterpret_cast<const uint4 *>(&sX[sl0 * CW + 2 * q]);
-        const uint4 v1 = *reinterpret_cast<const uint4 *>(&sX[sl1 * CW + 2 * q]);
-        x[0][2 * q] = make_uint2(v0.x, v0.y); x[0][2 * q + 1] = make_uint2(v0.z, v0.w);
-        x[1][2 * q] = make_uint2(v1.x, v1.y); x[1][2 * q + 1] = make_uint2(v1.z, v1.w);
+        const uint4 v = *reinterpret_cast<const uint4 *>(stage + xoff + 16 * q);
+        x[2 * q] = make_uint2(v.x, v.y); x[2 * q + 1] = make_uint2(v.z, v.w);
       }
+      if constexpr (CW >= 4) {
 #pragma unroll
-      for (int p = 0; p < 2; p++) {
-        const int sl = p ? sl1 : sl0;
-        if constexpr (CW >= 4) {
-#pragma unroll
-          for (int q = 0; q < CW / 4; q++) {
-            const uint4 v = *reinterpret_cast<const uint4 *>(&sXs[sl * CW + 4 * q]);
-            xsum[p][4 * q] = v.x; xsum[p][4 * q + 1] = v.y; xsum[p][4 * q + 2] = v.z; xsum[p][4 * q + 3] = v.w;
-          }
-        } else {
-          const uint2 v = *reinterpret_cast<const uint2 *>(&sXs[sl * CW]);
-          xsum[p][0] = v.x; xsum[p][1] = v.y;
+        for (int q = 0; q < CW / 4; q++) {
+          const uint4 v = *reinterpret_cast<const uint4 *>(stage + soff + 16 * q);
+          xs[4 * q] = v.x; xs[4 * q + 1] = v.y; xs[4 * q + 2] = v.z; xs[4 * q + 3] = v.w;
         }
-      }
-#pragma unroll
-      for (int p = 0; p < 2; p++) {
-        const uint32_t ws = w[p].x + w[p].y;
-#pragma unroll
-        for (int b = 0; b < CW; b++) {
-          const uint32_t xs = xsum[p][b];
-          lo[p][b] += (uint64_t)w[p].x * x[p][b].x;
-          hi[p][b] += (uint64_t)w[p].y * x[p][b].y;
-          md[p][b] += (uint64_t)ws * xs;
-        }
+      } else {
+        const uint2 v = *reinterpret_cast<const uint2 *>(stage + soff);
+        xs[0] = v.x; xs[1] = v.y;
       }
       __syncwarp();
-      if (lane == 0) mbar_arrive(&empty[st]);
+      if (lane == 0) mbar_arrive(&empty[st]);       // operands are in registers: release the stage
+      if (++st == NST) { st = 0; phase ^= 1; }
+      const uint32_t ws = w.x + w.y;
+#pragma unroll
+      for (int b = 0; b < CW; b++) {
+        lo[b] += (uint64_t)w.x * x[b].x;
+        hi[b] += (uint64_t)w.y * x[b].y;
+        md[b] += (uint64_t)ws * xs[b];
+      }
     }
 
     // ---------------- epilogue: reduce, transpose through smem, coalesced stores
     const int l = (sb * 32) / A.N;
     const PrimeConsts pc = pick(P, l);
-    asm volatile("bar.sync 1, 256;" ::: "memory");       // previous tile's ebuf reads are done
+    asm volatile("bar.sync 1, %0;" ::"r"(NCT) : "memory");     // previous tile's ebuf reads are done
 #pragma unroll
-    for (int p = 0; p < 2; p++) {
-      const int sl = p ? sl1 : sl0;
-#pragma unroll
-      for (int b = 0; b < CW; b++) {
-        const uint64_t mid = md[p][b] - lo[p][b] - hi[p][b];          // exact: x0 y1 + x1 y0
-        const hl_u128 V = ((hl_u128)hi[p][b] << (2 * kLimbBits)) + ((hl_u128)mid << kLimbBits) + lo[p][b];
-        const uint64_t vh = (uint64_t)(V >> 64), vl = (uint64_t)V;
-        const uint64_t r1 = shoup_mul(vh, pc.r64, pc.r64_sh, pc.p);   // vh * 2^64 mod p, [0, 2p)
-        const uint64_t r2 = vl - __umul64hi(vl, pc.mu) * pc.p;        // vl mod p, [0, 2p)
-        uint64_t r = r1 + r2;
-        r = r >= pc.two_p ? r - pc.two_p : r;
-        r = r >= pc.p ? r - pc.p : r;
-        ebuf[row * S::E_STRIDE + b * 32 + sl] = r;
+    for (int b = 0; b < CW; b++) {
+      const uint64_t mid = md[b] - lo[b] - hi[b];                      // exact: x0 y1 + x1 y0
+      const hl_u128 V = ((hl_u128)hi[b] << (2 * kLimbBits)) + ((hl_u128)mid << kLimbBits) + lo[b];
+      const uint64_t vh = (uint64_t)(V >> 64), vl = (uint64_t)V;
+      const uint64_t r1 = shoup_mul(vh, pc.r64, pc.r64_sh, pc.p);    // vh * 2^64 mod p, [0, 2p)
+      const uint64_t r2 = vl - __umul64hi(vl, pc.mu) * pc.p;         // vl mod p, [0, 2p)
+      uint64_t r = r1 + r2;
+      r = r >= pc.two_p ? r - pc.two_p : r;
+      r = r >= pc.p ? r - pc.p : r;
+      ebuf[row * S::E_STRIDE + b * 32 + sl] = r;
+    }
+    asm volatile("bar.sync 1, %0;" ::"r"(NCT) : "memory");
+    const int I0 = ib * 16;
+    for (int e = threadIdx.x; e < 16 * CW * 32; e += NCT) {
+      const int rr = e / (CW * 32), b = (e / 32) % CW, s2 = e % 32;
+      if (I0 + rr >= g.nIs) continue;
+      uint64_t v = ebuf[rr * S::E_STRIDE + b * 32 + s2];
+      uint64_t *dst = A.out + ((size_t)(I0 + rr) * g.nC + cg * CW + b) * LN + sb * 32 + s2;
+      if (A.accumulate) {
+        v += *dst;
+        v = v >= pc.p ? v - pc.p : v;
+      }
+      *dst = v;
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------------------
+// FP64 MAC engine (default).  Same tiling, ring and epilogue as k_mac; the exact product of
+// two residues a = W, b = X < 2^50 (held as doubles, exact) is formed with error-free FP64
+// transformations on the DFMA pipe (57 /clk/SM vs 24 for IMAD.WIDE, profiles/r01):
+//   t  = fma(a * 2^-49, b, C)            C = 1.5 * 2^52:  t = C + hi, hi = round(a b / 2^49) < 2^51
+//   c  = fma(t, -2^49, C * 2^49)         = -hi * 2^49   (exact: 51 significant bits)
+//   r  = fma(a, b, c)                    = a b - hi 2^49, |r| <= 2^48, exact
+//   H += bits(t)  (u64; subtract nj*bits(C) at the end)     R += r  (exact for 32 terms)
+// R is flushed to an int64 every 32 J.  sum_J a b = (H - nj bits(C)) * 2^49 + R_total exactly.
+// ---------------------------------------------------------------------------------------
+template <int CW, int JPS>
+struct MacSmemF64 {
+  static constexpr int W_BYTES = 32 * 16 * 8;             // per J
+  static constexpr int X_BYTES = 32 * CW * 8;             // per J
+  static constexpr int STAGE = JPS * (W_BYTES + X_BYTES); // JPS consecutive J per stage
+  static constexpr int E_STRIDE = CW * 32 + 1;
+  static constexpr int E_BYTES = 16 * E_STRIDE * 8;
+};
+
+template <int CW, int LN, int NST, int JPS>
+__global__ void __launch_bounds__(kMacThreads, 1)
+k_mac_f64(MacArgs A, DevParams P) {
+  using S = MacSmemF64<CW, JPS>;
+  extern __shared__ __align__(128) unsigned char smem[];
+  uint64_t *full = reinterpret_cast<uint64_t *>(smem + NST * S::STAGE + S::E_BYTES);
+  uint64_t *empty = full + NST;
+  uint64_t *ebuf = reinterpret_cast<uint64_t *>(smem + NST * S::STAGE);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const MacGeom &g = A.g;
+  const int ntiles = g.nIb * g.nCg * g.nSb;
+  const int nj = A.j1 - A.j0;
+  const int nstage = (nj + JPS - 1) / JPS;                // stages per tile
+
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < NST; i++) { mbar_init(&full[i], 1); mbar_init(&empty[i], kMacConsumerWarps); }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+
+  if (warp == kMacConsumerWarps) {
+    if (lane == 0) {
+      int st = 0;
+      uint32_t phase = 1;
+      for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+        const int ib = tile % g.nIb, cg = (tile / g.nIb) % g.nCg, sb = tile / (g.nIb * g.nCg);
+        const double *wsrc = reinterpret_cast<const double *>(A.W) + (((size_t)ib * g.nSb + sb) * g.nJ + A.j0) * 512;
+        const uint32_t *xsrc = A.X + x_chunk(g, A.j0, cg, sb);
+        for (int k = 0; k < nstage; k++) {
+          const int jn = min(JPS, nj - k * JPS);
+          mbar_wait(&empty[st], phase);
+          unsigned char *dst = smem + st * S::STAGE;
+          mbar_expect_tx(&full[st], jn * (S::W_BYTES + S::X_BYTES));
+          bulk_g2s(dst, wsrc + (size_t)k * JPS * 512, jn * S::W_BYTES, &full[st]);
+          bulk_g2s(dst + JPS * S::W_BYTES, xsrc + (size_t)k * JPS * 64 * CW, jn * S::X_BYTES, &full[st]);
+          if (++st == NST) { st = 0; phase ^= 1; }
+        }
       }
     }
-    asm volatile("bar.sync 1, 256;" ::: "memory");
+    return;
+  }
+
+  const int row = lane & 15;
+  const int sl = 2 * warp + (lane >> 4);
+  constexpr int NCT = kMacConsumerWarps * 32;
+  constexpr double kC = 6755399441055744.0;                          // 1.5 * 2^52
+  constexpr double kC49 = 6755399441055744.0 * 562949953421312.0;   // C * 2^49
+  constexpr double kM49 = -562949953421312.0;                       // -2^49
+  constexpr double kS49 = 1.7763568394002505e-15;                   // 2^-49
+  const uint64_t kCbits = 0x4338000000000000ull;                    // bit pattern of C
+  int st = 0;
+  uint32_t phase = 0;
+  const int woff = (sl * 16 + row) * 8, xoff = JPS * S::W_BYTES + sl * CW * 8;
+
+  // one J step: t = C + round(w x / 2^49) -> H; r = w x - (t - C) 2^49 -> R  (all exact)
+  auto mac_step = [&](const unsigned char *wp, const unsigned char *xp, uint64_t (&H)[CW], double (&R)[CW]) {
+    const double w = *reinterpret_cast<const double *>(wp);
+    double x[CW];
+#pragma unroll
+    for (int q = 0; q < CW / 2; q++) {
+      const double2 v = *reinterpret_cast<const double2 *>(xp + 16 * q);
+      x[2 * q] = v.x; x[2 * q + 1] = v.y;
+    }
+    const double ws = w * kS49;                                       // exact
+    double t[CW];
+#pragma unroll
+    for (int b = 0; b < CW; b++) t[b] = __fma_rn(ws, x[b], kC);
+#pragma unroll
+    for (int b = 0; b < CW; b++) H[b] += (uint64_t)__double_as_longlong(t[b]);
+#pragma unroll
+    for (int b = 0; b < CW; b++) t[b] = __fma_rn(t[b], kM49, kC49);    // -hi * 2^49
+#pragma unroll
+    for (int b = 0; b < CW; b++) t[b] = __fma_rn(w, x[b], t[b]);       // w x - hi 2^49
+#pragma unroll
+    for (int b = 0; b < CW; b++) R[b] = __dadd_rn(R[b], t[b]);
+  };
+  // |R| <= 32 * 2^48: move round(R / 2^49) into H (same magic), keep the exact remainder in R
+  auto flush = [&](uint64_t (&H)[CW], double (&R)[CW]) {
+#pragma unroll
+    for (int b = 0; b < CW; b++) {
+      const double t2 = __fma_rn(R[b], kS49, kC);
+      H[b] += (uint64_t)__double_as_longlong(t2);
+      R[b] = __dadd_rn(R[b], __fma_rn(t2, kM49, kC49));
+    }
+  };
+
+  for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    const int ib = tile % g.nIb, cg = (tile / g.nIb) % g.nCg, sb = tile / (g.nIb * g.nCg);
+    uint64_t H[CW];
+    double R[CW];
+#pragma unroll
+    for (int b = 0; b < CW; b++) { H[b] = 0; R[b] = 0.0; }
+    int nmagic = 0;                                   // number of C offsets added into H
+
+#pragma unroll 1
+    for (int k = 0; k < nstage; k++) {
+      const int jn = min(JPS, nj - k * JPS);
+      mbar_wait(&full[st], phase);
+      const unsigned char *stage = smem + st * S::STAGE;
+      if (jn == JPS) {
+#pragma unroll
+        for (int jj = 0; jj < JPS; jj++)
+          mac_step(stage + jj * S::W_BYTES + woff, stage + xoff + jj * S::X_BYTES, H, R);
+      } else {
+#pragma unroll 1
+        for (int jj = 0; jj < jn; jj++)
+          mac_step(stage + jj * S::W_BYTES + woff, stage + xoff + jj * S::X_BYTES, H, R);
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[st]);
+      if (++st == NST) { st = 0; phase ^= 1; }
+      nmagic += jn;
+      if (((k + 1) * JPS) % 32 == 0) { flush(H, R); nmagic++; }
+    }
+    flush(H, R);                                      // |R| <= 2^48 afterwards
+    nmagic++;
+
+    const int l = (sb * 32) / A.N;
+    const PrimeConsts pc = pick(P, l);
+    asm volatile("bar.sync 1, %0;" ::"r"(NCT) : "memory");
+#pragma unroll
+    for (int b = 0; b < CW; b++) {
+      const uint64_t hi = H[b] - (uint64_t)nmagic * kCbits;            // sum of the rounded 2^49 parts
+      const int64_t lo = __double2ll_rn(R[b]);                         // exact remainder, |lo| <= 2^48
+      const hl_u128 V = ((hl_u128)hi << 49) + (hl_u128)(__int128)lo;  // exact sum_J a b >= 0
+      const uint64_t vh = (uint64_t)(V >> 64), vl = (uint64_t)V;
+      const uint64_t r1 = shoup_mul(vh, pc.r64, pc.r64_sh, pc.p);
+      const uint64_t r2 = vl - __umul64hi(vl, pc.mu) * pc.p;
+      uint64_t r = r1 + r2;
+      r = r >= pc.two_p ? r - pc.two_p : r;
+      r = r >= pc.p ? r - pc.p : r;
+      ebuf[row * S::E_STRIDE + b * 32 + sl] = r;
+    }
+    asm volatile("bar.sync 1, %0;" ::"r"(NCT) : "memory");
     const int I0 = ib * 16;
-    for (int e = threadIdx.x; e < 16 * CW * 32; e += 256) {
-      const int rr = e / (CW * 32), b = (e / 32) % CW, sl = e % 32;
+    for (int e = threadIdx.x; e < 16 * CW * 32; e += NCT) {
+      const int rr = e / (CW * 32), b = (e / 32) % CW, s2 = e % 32;
       if (I0 + rr >= g.nIs) continue;
-      uint64_t v = ebuf[rr * S::E_STRIDE + b * 32 + sl];
-      uint64_t *dst = A.out + ((size_t)(I0 + rr) * g.nC + cg * CW + b) * LN + sb * 32 + sl;
+      uint64_t v = ebuf[rr * S::E_STRIDE + b * 32 + s2];
+      uint64_t *dst = A.out + ((size_t)(I0 + rr) * g.nC + cg * CW + b) * LN + sb * 32 + s2;
       if (A.accumulate) {
         v += *dst;
         v = v >= pc.p ? v - pc.p : v;
@@ -759,11 +925,32 @@ void launch_mac_t(const hl_ctx *c, const MacArgs &A, cudaStream_t st) {
   k_mac<CW, LN, kMacStages><<<grid, kMacThreads, smem, st>>>(A, c->dp);
 }
 
+constexpr int kMacF64Jps = 4;                    // J steps per ring stage (one bulk copy pair)
+constexpr int kMacF64Stages = 6;                 // 6 x 4 x 6 KB = 144 KB in flight per SM at CW = 8
+
+template <int CW, int LN>
+void launch_mac_f64_t(const hl_ctx *c, const MacArgs &A, cudaStream_t st) {
+  using S = MacSmemF64<CW, kMacF64Jps>;
+  constexpr size_t smem = (size_t)kMacF64Stages * S::STAGE + S::E_BYTES + 2 * kMacF64Stages * 8;
+  static bool init = false;
+  if (!init) { set_smem(k_mac_f64<CW, LN, kMacF64Stages, kMacF64Jps>, smem); init = true; }
+  const int ntiles = A.g.nIb * A.g.nCg * A.g.nSb;
+  const int grid = std::min(ntiles, c->num_sms);
+  KTimer kt(c, HL_K_MAC, st);
+  k_mac_f64<CW, LN, kMacF64Stages, kMacF64Jps><<<grid, kMacThreads, smem, st>>>(A, c->dp);
+}
+
 template <int LN>
 void launch_mac_ln(const hl_ctx *c, const MacArgs &A, cudaStream_t st) {
-  if (A.g.CW == 8) launch_mac_t<8, LN>(c, A, st);
-  else if (A.g.CW == 4) launch_mac_t<4, LN>(c, A, st);
-  else launch_mac_t<2, LN>(c, A, st);
+  if (A.g.f64) {
+    if (A.g.CW == 8) launch_mac_f64_t<8, LN>(c, A, st);
+    else if (A.g.CW == 4) launch_mac_f64_t<4, LN>(c, A, st);
+    else launch_mac_f64_t<2, LN>(c, A, st);
+  } else {
+    if (A.g.CW == 8) launch_mac_t<8, LN>(c, A, st);
+    else if (A.g.CW == 4) launch_mac_t<4, LN>(c, A, st);
+    else launch_mac_t<2, LN>(c, A, st);
+  }
 }
 
 void launch_mac(const hl_ctx *c, const uint2 *W, const uint32_t *X, uint64_t *out, const MacGeom &g, cudaStream_t st) {

@@ -239,3 +239,50 @@ def test_encode_weights_errors(hl, ctx4096):
     with pytest.raises(hl.HLError) as e:
         ctx.encode_weights((16, 32, 8), hl.to_device(Wbig))
     assert e.value.code == hl.HL_ENOISE
+
+
+# ------------------------------------------------------------------------- both MAC engines
+@pytest.mark.parametrize("engine", [0, 1])
+@pytest.mark.parametrize("N,shape,tile", [
+    (4096, (40, 24, 40), (16, 8, 32)),
+    (4096, (64, 48, 100), (4, 8, 16)),
+    (4096, (3, 5, 7), (1, 1, 1)),
+    (8192, (32, 48, 40), (32, 16, 16)),
+])
+def test_mac_engines_bit_exact(hl, ctx4096, ctx8192, engine, N, shape, tile):
+    """IMAD.WIDE (engine 0) and exact-FP64 (engine 1) MACs both equal the oracle."""
+    ctx = ctx4096 if N == 4096 else ctx8192
+    Nb, R, Ma = shape
+    P, ct_in, W = _case_inputs(ctx, shape, tile, 700 + N + Ma + engine)
+    ctx.set_mac_engine(engine)
+    try:
+        wc = ctx.encode_weights(tile, hl.to_device(W))
+        out = ctx.he_matmul(tile, wc, Ma, R, Nb, hl.to_device(ct_in))
+        got = hl.to_host(out).reshape(-1, 2, ctx.L, ctx.N)
+    finally:
+        ctx.set_mac_engine(1)
+    exp = ref.he_matmul(P, tile, W, ct_in, Nb).reshape(-1, 2, ctx.L, ctx.N)
+    assert np.array_equal(got, exp)
+
+
+@pytest.mark.parametrize("engine", [0, 1])
+def test_mac_extreme_residues(hl, ctx4096, engine):
+    """All weights and ciphertext residues = p - 1 (the largest products and sums) over a long
+    J reduction (R = 3072 -> nJ = 384), both engines."""
+    ctx = ctx4096
+    P = _P(ctx)
+    tile, (Nb, R, Ma) = (16, 8, 32), (32, 3072, 16)
+    nI, nJ, nK = ref.tile_counts(tile, Ma, R, Nb)
+    ct_in = np.empty((nJ, nK, 2, P.L, P.N), dtype=np.uint64)
+    for l, p in enumerate(P.primes):
+        ct_in[:, :, :, l, :] = p - 1
+    W = synth.weights(801, R, Ma)
+    ctx.set_mac_engine(engine)
+    try:
+        wc = ctx.encode_weights(tile, hl.to_device(W))
+        out = ctx.he_matmul(tile, wc, Ma, R, Nb, hl.to_device(ct_in))
+        got = hl.to_host(out).reshape(-1, 2, ctx.L, ctx.N)
+    finally:
+        ctx.set_mac_engine(1)
+    exp = ref.he_matmul(P, tile, W, ct_in, Nb).reshape(-1, 2, ctx.L, ctx.N)
+    assert np.array_equal(got, exp)
