@@ -32,6 +32,8 @@ import synth  # noqa: E402
 
 METRIC = "ms per BERT-base encoder block's encrypted matmuls"
 IMAD_WIDE_PER_CLK_SM = 24.4      # measured peak, profiles/r01/microbench_intpipe3.log
+DFMA_PER_CLK_SM = 57.3           # measured peak (same run): the FP64 pipe of the default MAC engine
+FP64_OPS_PER_MAC = 4.125         # 3 DFMA + 1 DADD per modular MAC + 1 DMUL per 8 (k_mac_f64)
 UNIT = "ms"
 
 
@@ -59,7 +61,7 @@ def counts(cfg, lay_by_mm):
             bfly_fwd=nJ * nC * L * (N // 2) * logN,
             bfly_inv=nI * nC * L * (N // 2) * logN,
             # MAC kernel bytes: weight cache + NTT-domain ct_in (read once) + NTT-domain output
-            mac_bytes=8 * (nI * nJ * L * N + nJ * nC * L * N + nI * nC * L * N),
+            mac_bytes=8 * (-(-nI // 16) * 16 * nJ * L * N + nJ * nC * L * N + nI * nC * L * N),
             fwd_bytes=8 * 2 * nJ * nC * L * N,                   # coefficient ct_in in, limb pairs out
             inv_bytes=8 * (nI * nC * L * N + nI * nK * L * (m * n + N) + mm.Nb * mm.Ma),
             # whole-path algorithmic bytes (SURVEY.md §8(d) "Bytes")
@@ -242,28 +244,32 @@ def run_ours(args, rank, world, local_rank):
     hbm_src = "measured (MEASURED_PEAKS.json hbm_gbs)" if hbm else "fallback 6650 GB/s (B200_PROFILING.md)"
     hbm = hbm or 6650.0
     sm_max = (peaks.get("sm_max_mhz") or 1965.0)
-    # integer-pipe peak: IMAD.WIDE.U32 (32x32->64 multiply-add, the MAC's only
-    # multiply) issues at 24.4 /clk/SM on B200 (tools/microbench/intpipe3.cu, profiles/r01/
-    # microbench_intpipe3.log; the guide's 64/clk/SM holds for the 32-bit IMAD only) x 148 SMs
-    # x max SM clock.
-    imad_peak = IMAD_WIDE_PER_CLK_SM * 148 * sm_max * 1e6          # IMAD.WIDE/s
+    # ALU peaks, measured on this B200 by tools/microbench/intpipe3.cu
+    # (profiles/r01/microbench_intpipe3.log): IMAD.WIDE.U32 24.4 /clk/SM (the IMAD engine's
+    # multiply), DFMA 57.3 /clk/SM (the default FP64 engine); x 148 SMs x max SM clock.
+    engine = os.environ.get("HELINEAR_MAC_ENGINE", "f64")
+    if engine == "imad":
+        ops_per_mac, alu_peak, alu_unit = 3.0, IMAD_WIDE_PER_CLK_SM * 148 * sm_max * 1e6, "T IMAD.WIDE/s (3 per modular MAC)"
+    else:
+        ops_per_mac, alu_peak, alu_unit = FP64_OPS_PER_MAC, DFMA_PER_CLK_SM * 148 * sm_max * 1e6, \
+            "T FP64 op/s (4.125 per modular MAC)"
     mac_ms, mac_n = ktimes["mac"]
     mac_avg_s = mac_ms / max(mac_n, 1) * 1e-3
     per_launch_mac = sum(c["mac"] for c in cnt) / len(cnt)
     per_launch_bytes = sum(c["mac_bytes"] for c in cnt) / len(cnt)
-    # bound of the MAC kernel: the slower of ALU (3 IMAD.WIDE per modular MAC) and HBM
-    t_alu = 3 * per_launch_mac / imad_peak
+    # bound of the MAC kernel: the slower of the ALU pipe and HBM
+    t_alu = ops_per_mac * per_launch_mac / alu_peak
     t_hbm = per_launch_bytes / (hbm * 1e9)
     if t_alu >= t_hbm:
-        roof = {"bound": "alu", "achieved": 3 * per_launch_mac / mac_avg_s / 1e12, "peak": imad_peak / 1e12,
-                "unit": "T IMAD.WIDE/s (3 per modular MAC)"}
+        roof = {"bound": "alu", "achieved": ops_per_mac * per_launch_mac / mac_avg_s / 1e12, "peak": alu_peak / 1e12,
+                "unit": alu_unit}
     else:
         roof = {"bound": "hbm", "achieved": per_launch_bytes / mac_avg_s / 1e9, "peak": hbm, "unit": "GB/s"}
     roof["frac"] = roof["achieved"] / roof["peak"]
     roof["traffic"] = None
-    roof["kernel"] = "k_mac (slot-parallel modular MAC)"
-    roof["peak_source"] = ("measured IMAD.WIDE 24.4/clk/SM x 148 SMs x sm_max_mhz (DESIGN.md §6)"
-                           if roof["bound"] == "alu" else hbm_src)
+    roof["kernel"] = ("k_mac_f64" if engine != "imad" else "k_mac") + " (slot-parallel modular MAC)"
+    roof["peak_source"] = (("measured DFMA 57.3" if engine != "imad" else "measured IMAD.WIDE 24.4") +
+                           "/clk/SM x 148 SMs x sm_max_mhz (DESIGN.md §6)" if roof["bound"] == "alu" else hbm_src)
     roof["hbm_frac_same_kernel"] = per_launch_bytes / mac_avg_s / 1e9 / hbm
     total_k = sum(v[0] for v in ktimes.values())
     kernel_share = {k: {"ms_per_step": v[0] / args.steps, "launches_per_step": v[1] / args.steps,

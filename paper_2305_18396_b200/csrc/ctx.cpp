@@ -161,7 +161,7 @@ extern "C" int hl_ctx_create(uint32_t N, uint32_t L, uint32_t log2_t, const uint
   // roots and twiddles: tw_fwd[i] = psi^bitrev(i), tw_inv[i] = psi^-bitrev(i)
   c->h_tw_fwd.resize((size_t)L * N); c->h_tw_fwd_sh.resize((size_t)L * N);
   c->h_tw_inv.resize((size_t)L * N); c->h_tw_inv_sh.resize((size_t)L * N);
-  std::vector<ulonglong2> tw((size_t)2 * L * N);
+  std::vector<double> tw((size_t)2 * L * N);
   DevParams &dp = c->dp;
   dp.N = (int)N; dp.logN = logN; dp.L = (int)L; dp.t_bits = (int)log2_t;
   for (uint32_t l = 0; l < L; l++) {
@@ -176,8 +176,8 @@ extern "C" int hl_ctx_create(uint32_t N, uint32_t L, uint32_t log2_t, const uint
       size_t o = (size_t)l * N + i;
       c->h_tw_fwd[o] = wf; c->h_tw_fwd_sh[o] = h_shoup(wf, p);
       c->h_tw_inv[o] = wi; c->h_tw_inv_sh[o] = h_shoup(wi, p);
-      tw[o] = make_ulonglong2(wf, c->h_tw_fwd_sh[o]);
-      tw[(size_t)L * N + o] = make_ulonglong2(wi, c->h_tw_inv_sh[o]);
+      tw[o] = (double)wf;                       // exact: w < 2^50
+      tw[(size_t)L * N + o] = (double)wi;
     }
     PrimeConsts &pc = dp.pc[l];
     pc.p = p; pc.two_p = 2 * p;
@@ -188,17 +188,19 @@ extern "C" int hl_ctx_create(uint32_t N, uint32_t L, uint32_t log2_t, const uint
     pc.ninv = h_powmod(N, p - 2, p); pc.ninv_sh = h_shoup(pc.ninv, p);
     pc.ninv_w1 = h_mulmod(pc.ninv, c->h_tw_inv[(size_t)l * N + 1], p);
     pc.ninv_w1_sh = h_shoup(pc.ninv_w1, p);
+    pc.pd = (double)p; pc.pinv = 1.0 / (double)p;
+    pc.ninv_d = (double)pc.ninv; pc.ninv_w1_d = (double)pc.ninv_w1;
   }
   build_cdt(c->cdt);
   if (const char *e = getenv("HELINEAR_MAC_ENGINE")) c->mac_engine = (strcmp(e, "imad") == 0) ? 0 : 1;
   // device tables (device < 0: host-only context for the client calls; no CUDA needed)
   if (device < 0) {
-    dp.tw_fwd = dp.tw_inv = nullptr;
+    dp.twd_fwd = dp.twd_inv = nullptr;
     *out = c;
     return HL_OK;
   }
   if (cudaSetDevice(device) != cudaSuccess) { delete c; return hl_cuda_check("hl_ctx_create: cudaSetDevice"); }
-  size_t bytes = tw.size() * sizeof(ulonglong2);
+  size_t bytes = tw.size() * sizeof(double);
   if (cudaMalloc(&c->d_tw, bytes) != cudaSuccess ||
       cudaMemcpy(c->d_tw, tw.data(), bytes, cudaMemcpyHostToDevice) != cudaSuccess ||
       cudaMalloc((void **)&c->d_flags, 64) != cudaSuccess) {
@@ -208,8 +210,8 @@ extern "C" int hl_ctx_create(uint32_t N, uint32_t L, uint32_t log2_t, const uint
     return rc ? rc : hl_fail(HL_ECUDA, "hl_ctx_create: device allocation failed");
   }
   cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, device);
-  dp.tw_fwd = (const ulonglong2 *)c->d_tw;
-  dp.tw_inv = (const ulonglong2 *)c->d_tw + (size_t)L * N;
+  dp.twd_fwd = (const double *)c->d_tw;
+  dp.twd_inv = (const double *)c->d_tw + (size_t)L * N;
   *out = c;
   return HL_OK;
 }

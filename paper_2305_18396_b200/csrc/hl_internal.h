@@ -27,13 +27,15 @@ struct PrimeConsts {
   uint64_t ninv_sh;
   uint64_t ninv_w1;   // N^-1 * psi^-bitrev(1) mod p (last inverse stage, folded)
   uint64_t ninv_w1_sh;
+  // FP64 NTT constants (exact integer-valued doubles; pinv = 1/p rounded to nearest)
+  double pd, pinv, ninv_d, ninv_w1_d;
 };
 
 struct DevParams {
   int N, logN, L, t_bits;
   PrimeConsts pc[HL_MAX_L];
-  const ulonglong2 *tw_fwd;   // [L][N] {w, w'}: psi^bitrev(i) with Shoup companion
-  const ulonglong2 *tw_inv;   // [L][N] {w, w'}: psi^-bitrev(i)
+  const double *twd_fwd;      // [L][N] psi^bitrev(i) as exact doubles
+  const double *twd_inv;      // [L][N] psi^-bitrev(i)
 };
 
 // CUDA-event timing of kernel launches (hl_timing_enable / hl_timing_read)

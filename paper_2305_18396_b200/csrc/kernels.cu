@@ -9,8 +9,9 @@
 //   mask_and_share : ChaCha20 mask, c0 -= Delta*sigma, drop unused c0, shares
 //   he_matmul_share: the inverse NTT fused with the masking/compression epilogue
 //
-// NTT: negacyclic, merged-psi Cooley-Tukey forward / Gentleman-Sande inverse (Harvey lazy
-// butterflies, values in [0, 4p) / [0, 2p), 64-bit Shoup twiddle products).  One CTA per
+// NTT: negacyclic, merged-psi Cooley-Tukey forward / Gentleman-Sande inverse on the FP64
+// pipe (exact modular products by error-free DFMA transformations, signed lazy residues,
+// reductions every second stage; see mm_d / red_d).  One CTA per
 // polynomial, N/16 threads holding 16 coefficients each; radix-16 rounds in registers with
 // padded shared-memory transposes between rounds.  NTT-domain slot order is internal:
 // slot P(idx) = (idx & 15) * (N/16) + (idx >> 4) of the bit-reversed CT output index, which
@@ -44,23 +45,42 @@ __device__ __forceinline__ uint64_t shoup_mul(uint64_t x, uint64_t w, uint64_t w
   return x * w - q * p;   // in [0, 2p) for any x < 2^64
 }
 
-__device__ __forceinline__ void ct_bfly(uint64_t &X, uint64_t &Y, ulonglong2 w, uint64_t p, uint64_t p2) {
-  uint64_t x = X >= p2 ? X - p2 : X;          // [0, 2p)
-  uint64_t t = shoup_mul(Y, w.x, w.y, p);     // [0, 2p)
-  X = x + t;                                  // [0, 4p)
-  Y = x - t + p2;                             // (0, 4p)
+// ---------------------------------------------------------------------------------------
+// Exact modular arithmetic on the FP64 pipe (DFMA 57 /clk/SM vs 24 for the
+// IMAD.WIDE a 64-bit Shoup product needs).  Residues are integer-valued doubles, signed and
+// lazily reduced; every intermediate below is an integer of magnitude < 2^53, hence exact.
+//   mm_d(y, w):  h = y w (rounded), l = fma(y, w, -h) (exact: y w = h + l),
+//                q = rint(h / p) via the 1.5*2^52 magic, r = fma(-q, p, h) (exact), return r + l.
+//                Requires |y| < 2^51 and 0 <= w < p; |h/p - q| <= 0.75 so |result| < p.
+//   red_d(v):    v - p * rint(v / p), |result| <= p/2 (+ tiny) for |v| < 2^51.
+// ---------------------------------------------------------------------------------------
+constexpr double kMagic = 6755399441055744.0;            // 1.5 * 2^52
+constexpr double kTwo52 = 4503599627370496.0;            // 2^52
+
+__device__ __forceinline__ double mm_d(double y, double w, double p, double pinv) {
+  const double h = __dmul_rn(y, w);
+  const double l = __fma_rn(y, w, -h);
+  const double q = __dsub_rn(__fma_rn(h, pinv, kMagic), kMagic);
+  const double r = __fma_rn(-q, p, h);
+  return __dadd_rn(r, l);
 }
 
-__device__ __forceinline__ void gs_bfly(uint64_t &X, uint64_t &Y, ulonglong2 w, uint64_t p, uint64_t p2) {
-  uint64_t s = X + Y;
-  s = s >= p2 ? s - p2 : s;                   // [0, 2p)
-  Y = shoup_mul(X - Y + p2, w.x, w.y, p);     // [0, 2p)
-  X = s;
+__device__ __forceinline__ double red_d(double v, double p, double pinv) {
+  const double q = __dsub_rn(__fma_rn(v, pinv, kMagic), kMagic);
+  return __fma_rn(-q, p, v);
 }
 
-__device__ __forceinline__ uint64_t canon4(uint64_t x, uint64_t p, uint64_t p2) {   // [0,4p) -> [0,p)
-  x = x >= p2 ? x - p2 : x;
-  return x >= p ? x - p : x;
+// [0, 2^52) integer <-> double without the conversion unit
+__device__ __forceinline__ double u2d(uint64_t x) {
+  return __dsub_rn(__longlong_as_double((long long)(x | 0x4330000000000000ull)), kTwo52);
+}
+__device__ __forceinline__ uint64_t d2u(double v) {      // v integer-valued in [0, 2^52)
+  return (uint64_t)__double_as_longlong(__dadd_rn(v, kTwo52)) - 0x4330000000000000ull;
+}
+// canonical residue in [0, p) as an integer-valued double, from |v| < 2^51
+__device__ __forceinline__ double canon_d(double v, double p, double pinv) {
+  const double r = red_d(v, p, pinv);
+  return r < 0.0 ? __dadd_rn(r, p) : r;
 }
 
 __device__ __forceinline__ PrimeConsts pick(const DevParams &P, int l) {
@@ -98,7 +118,7 @@ __device__ __forceinline__ int elem_idx(int t, int g, int u) {
 __device__ __forceinline__ int pad_idx(int idx) { return idx + (idx >> 4); }
 
 template <int LOGN, int R>
-__device__ __forceinline__ void to_smem(const uint64_t (&a)[16], uint64_t *sm, int t) {
+__device__ __forceinline__ void to_smem(const double (&a)[16], double *sm, int t) {
   constexpr int K = Geom<LOGN>::k(R), G = 16 >> K;
 #pragma unroll
   for (int g = 0; g < G; g++)
@@ -107,7 +127,7 @@ __device__ __forceinline__ void to_smem(const uint64_t (&a)[16], uint64_t *sm, i
 }
 
 template <int LOGN, int R>
-__device__ __forceinline__ void from_smem(uint64_t (&a)[16], const uint64_t *sm, int t) {
+__device__ __forceinline__ void from_smem(double (&a)[16], const double *sm, int t) {
   constexpr int K = Geom<LOGN>::k(R), G = 16 >> K;
 #pragma unroll
   for (int g = 0; g < G; g++)
@@ -118,8 +138,11 @@ __device__ __forceinline__ void from_smem(uint64_t (&a)[16], const uint64_t *sm,
 // Forward CT stages of round R.  Twiddle of a pair whose lower index is idx at stage st:
 // psi^bitrev((1<<st) + (idx >> (LOGN - st))); within a round that is
 // (1<<st) + (gid_high << ls) + (u >> (K - ls)).
+// Values: |v| <= p at entry of stage 0 (canonical input) or <= p/2 after a reduction; a CT
+// stage adds < p, so every value is reduced (red_d) after each odd stage: multiplicands stay
+// below 2p < 2^51 as mm_d requires.
 template <int LOGN, int R>
-__device__ __forceinline__ void fwd_round(uint64_t (&a)[16], int t, const ulonglong2 *tw, uint64_t p, uint64_t p2) {
+__device__ __forceinline__ void fwd_round(double (&a)[16], int t, const double *tw, double p, double pinv) {
   using Gm = Geom<LOGN>;
   constexpr int S0 = Gm::s0(R), K = Gm::k(R), LO = Gm::lo(R), G = 16 >> K;
 #pragma unroll
@@ -132,19 +155,28 @@ __device__ __forceinline__ void fwd_round(uint64_t (&a)[16], int t, const ulongl
 #pragma unroll
       for (int u = 0; u < (1 << K); u++) {
         if (u & half) continue;
-        const ulonglong2 w = __ldg(&tw[(1 << st) + (gid_high << ls) + (u >> (K - ls))]);
-        ct_bfly(a[g * (1 << K) + u], a[g * (1 << K) + u + half], w, p, p2);
+        const double w = __ldg(&tw[(1 << st) + (gid_high << ls) + (u >> (K - ls))]);
+        double &X = a[g * (1 << K) + u], &Y = a[g * (1 << K) + u + half];
+        const double T = mm_d(Y, w, p, pinv);
+        Y = __dsub_rn(X, T);
+        X = __dadd_rn(X, T);
       }
+    }
+    if (st & 1) {
+#pragma unroll
+      for (int i = 0; i < 16; i++) a[i] = red_d(a[i], p, pinv);
     }
   }
 }
 
-// Inverse GS stages of round R (stages descending); N^-1 is folded into stage 0.
+// Inverse GS stages of round R (stages descending); N^-1 is folded into stage 0.  Inputs must
+// satisfy |v| <= p/2; a GS stage keeps |Y'| < p and |X'| <= 2 max|v|, so values are reduced
+// after every second stage (counted from the top, stage LOGN-1) -- differences stay < 2p.
 template <int LOGN, int R>
-__device__ __forceinline__ void inv_round(uint64_t (&a)[16], int t, const ulonglong2 *tw, const PrimeConsts &pc) {
+__device__ __forceinline__ void inv_round(double (&a)[16], int t, const double *tw, const PrimeConsts &pc) {
   using Gm = Geom<LOGN>;
   constexpr int S0 = Gm::s0(R), K = Gm::k(R), LO = Gm::lo(R), G = 16 >> K;
-  const uint64_t p = pc.p, p2 = pc.two_p;
+  const double p = pc.pd, pinv = pc.pinv;
 #pragma unroll
   for (int ls = K - 1; ls >= 0; ls--) {
     const int st = S0 + ls;
@@ -155,24 +187,29 @@ __device__ __forceinline__ void inv_round(uint64_t (&a)[16], int t, const ulongl
 #pragma unroll
       for (int u = 0; u < (1 << K); u++) {
         if (u & half) continue;
-        uint64_t &X = a[g * (1 << K) + u], &Y = a[g * (1 << K) + u + half];
+        double &X = a[g * (1 << K) + u], &Y = a[g * (1 << K) + u + half];
+        const double s = __dadd_rn(X, Y), d = __dsub_rn(X, Y);
         if (st == 0) {
           // last stage: (X, Y) -> ((X+Y) N^-1, (X-Y) psi^-bitrev(1) N^-1)
-          const uint64_t s = X + Y, d = X - Y + p2;
-          X = shoup_mul(s, pc.ninv, pc.ninv_sh, p);
-          Y = shoup_mul(d, pc.ninv_w1, pc.ninv_w1_sh, p);
+          X = mm_d(s, pc.ninv_d, p, pinv);
+          Y = mm_d(d, pc.ninv_w1_d, p, pinv);
         } else {
-          const ulonglong2 w = __ldg(&tw[(1 << st) + (gid_high << ls) + (u >> (K - ls))]);
-          gs_bfly(X, Y, w, p, p2);
+          const double w = __ldg(&tw[(1 << st) + (gid_high << ls) + (u >> (K - ls))]);
+          X = s;
+          Y = mm_d(d, w, p, pinv);
         }
       }
+    }
+    if (st > 0 && ((LOGN - 1 - st) & 1)) {
+#pragma unroll
+      for (int i = 0; i < 16; i++) a[i] = red_d(a[i], p, pinv);
     }
   }
 }
 
 template <int LOGN, int R>
-__device__ __forceinline__ void fwd_rounds_from(uint64_t (&a)[16], uint64_t *sm, int t, const ulonglong2 *tw,
-                                                uint64_t p, uint64_t p2) {
+__device__ __forceinline__ void fwd_rounds_from(double (&a)[16], double *sm, int t, const double *tw,
+                                                double p, double pinv) {
   if constexpr (R < Geom<LOGN>::NR) {
     if constexpr (R > 0) {
       to_smem<LOGN, R - 1>(a, sm, t);
@@ -180,13 +217,13 @@ __device__ __forceinline__ void fwd_rounds_from(uint64_t (&a)[16], uint64_t *sm,
       from_smem<LOGN, R>(a, sm, t);
       __syncthreads();
     }
-    fwd_round<LOGN, R>(a, t, tw, p, p2);
-    fwd_rounds_from<LOGN, R + 1>(a, sm, t, tw, p, p2);
+    fwd_round<LOGN, R>(a, t, tw, p, pinv);
+    fwd_rounds_from<LOGN, R + 1>(a, sm, t, tw, p, pinv);
   }
 }
 
 template <int LOGN, int R>
-__device__ __forceinline__ void inv_rounds_from(uint64_t (&a)[16], uint64_t *sm, int t, const ulonglong2 *tw,
+__device__ __forceinline__ void inv_rounds_from(double (&a)[16], double *sm, int t, const double *tw,
                                                 const PrimeConsts &pc) {
   if constexpr (R >= 0) {
     if constexpr (R < Geom<LOGN>::NR - 1) {
@@ -252,35 +289,36 @@ template <int LOGN, int MODE>
 __global__ void __launch_bounds__(Geom<LOGN>::NT)
 k_ntt_fwd(const uint64_t *__restrict__ in, void *__restrict__ out, DevParams P, MacGeom mg) {
   using Gm = Geom<LOGN>;
-  extern __shared__ uint64_t sm[];
+  extern __shared__ double sm[];
   const int t = threadIdx.x, l = blockIdx.y;
   const size_t base = ((size_t)blockIdx.x * P.L + l) * Gm::N;
   const PrimeConsts pc = pick(P, l);
-  const ulonglong2 *tw = P.tw_fwd + (size_t)l * Gm::N;
-  uint64_t a[16];
+  const double *tw = P.twd_fwd + (size_t)l * Gm::N;
+  double a[16];
   constexpr int K = Gm::k(0), G = 16 >> K;
 #pragma unroll
   for (int g = 0; g < G; g++)
 #pragma unroll
-    for (int u = 0; u < (1 << K); u++) a[g * (1 << K) + u] = __ldcs(in + base + elem_idx<LOGN, 0>(t, g, u));
-  fwd_rounds_from<LOGN, 0>(a, sm, t, tw, pc.p, pc.two_p);
+    for (int u = 0; u < (1 << K); u++) a[g * (1 << K) + u] = u2d(__ldcs(in + base + elem_idx<LOGN, 0>(t, g, u)));
+  fwd_rounds_from<LOGN, 0>(a, sm, t, tw, pc.pd, pc.pinv);
   const int J = (int)(blockIdx.x / (unsigned)max(mg.nC, 1)), col = (int)(blockIdx.x % (unsigned)max(mg.nC, 1));
 #pragma unroll
   for (int u = 0; u < 16; u++) {
-    const uint64_t x = canon4(a[u], pc.p, pc.two_p);
+    const double xd = canon_d(a[u], pc.pd, pc.pinv);
     if constexpr (MODE == 1) {
       const int s = l * Gm::N + slot_of<LOGN>(t, u);
       uint32_t *ch = reinterpret_cast<uint32_t *>(out) + x_chunk(mg, J, col / mg.CW, s >> 5);
       const int e = (s & 31) * mg.CW + col % mg.CW;
       if (mg.f64) {
-        reinterpret_cast<double *>(ch)[e] = (double)x;              // exact: x < 2^50
+        reinterpret_cast<double *>(ch)[e] = xd;
       } else {
+        const uint64_t x = d2u(xd);
         const uint32_t x0 = (uint32_t)x & kLimbMask, x1 = (uint32_t)(x >> kLimbBits);
         reinterpret_cast<uint2 *>(ch)[e] = make_uint2(x0, x1);
         ch[64 * mg.CW + e] = x0 + x1;
       }
     } else {
-      reinterpret_cast<uint64_t *>(out)[base + slot_of<LOGN>(t, u)] = x;
+      reinterpret_cast<uint64_t *>(out)[base + slot_of<LOGN>(t, u)] = d2u(xd);
     }
   }
 }
@@ -298,15 +336,15 @@ template <int LOGN>
 __global__ void __launch_bounds__(Geom<LOGN>::NT)
 k_encode_weights(EncodeArgs A, uint2 *__restrict__ wcache, DevParams P, uint32_t *flags) {
   using Gm = Geom<LOGN>;
-  extern __shared__ uint64_t sm[];
+  extern __shared__ double sm[];
   const int t = threadIdx.x, l = blockIdx.y;
   const int64_t poly = blockIdx.x, Iloc = poly / A.nJ, J = poly % A.nJ, I = A.i_begin + Iloc;
   const PrimeConsts pc = pick(P, l);
-  const ulonglong2 *tw = P.tw_fwd + (size_t)l * Gm::N;
+  const double *tw = P.twd_fwd + (size_t)l * Gm::N;
   const uint64_t tmask = (P.t_bits >= 64) ? ~0ull : ((1ull << P.t_bits) - 1);
   const uint64_t half = 1ull << (P.t_bits - 1);
   const int mr = A.m * A.r;
-  uint64_t a[16];
+  double a[16];
   uint32_t maxabs = 0, bad = 0;
   constexpr int K = Gm::k(0), G = 16 >> K;
 #pragma unroll
@@ -333,19 +371,20 @@ k_encode_weights(EncodeArgs A, uint2 *__restrict__ wcache, DevParams P, uint32_t
           }
         }
       }
-      a[g * (1 << K) + u] = v;
+      a[g * (1 << K) + u] = u2d(v);
     }
   if (l == 0) {
     if (bad) atomicOr(&flags[0], 1u);
     if (maxabs) atomicMax(&flags[1], maxabs);
   }
-  fwd_rounds_from<LOGN, 0>(a, sm, t, tw, pc.p, pc.two_p);
+  fwd_rounds_from<LOGN, 0>(a, sm, t, tw, pc.pd, pc.pinv);
 #pragma unroll
   for (int u = 0; u < 16; u++) {
-    const uint64_t x = canon4(a[u], pc.p, pc.two_p);
+    const double xd = canon_d(a[u], pc.pd, pc.pinv);
+    const uint64_t x = d2u(xd);
     const int s = l * Gm::N + slot_of<LOGN>(t, u);
     if (A.mg.f64)
-      reinterpret_cast<double *>(wcache)[w_index(A.mg, (int)Iloc, (int)J, s)] = (double)x;   // exact
+      reinterpret_cast<double *>(wcache)[w_index(A.mg, (int)Iloc, (int)J, s)] = xd;
     else
       wcache[w_index(A.mg, (int)Iloc, (int)J, s)] = make_uint2((uint32_t)x & kLimbMask, (uint32_t)(x >> kLimbBits));
   }
@@ -355,33 +394,31 @@ k_encode_weights(EncodeArgs A, uint2 *__restrict__ wcache, DevParams P, uint32_t
 // Inverse NTT kernel: in u64 [npoly][L][N] (NTT domain, slot order) -> out [npoly][L][N]
 // coefficient form, canonical.  in may alias out.
 // ---------------------------------------------------------------------------------------
+// canonical residues in, reduced to |v| <= p/2 (the inverse rounds' entry bound)
 template <int LOGN>
-__device__ __forceinline__ void load_ntt_domain(uint64_t (&a)[16], const uint64_t *src, int t) {
+__device__ __forceinline__ void load_ntt_domain(double (&a)[16], const uint64_t *src, int t, const PrimeConsts &pc) {
 #pragma unroll
-  for (int u = 0; u < 16; u++) a[u] = __ldcs(src + slot_of<LOGN>(t, u));
+  for (int u = 0; u < 16; u++) a[u] = red_d(u2d(__ldcs(src + slot_of<LOGN>(t, u))), pc.pd, pc.pinv);
 }
 
 template <int LOGN>
 __global__ void __launch_bounds__(Geom<LOGN>::NT)
 k_ntt_inv(const uint64_t *in, uint64_t *out, DevParams P) {
   using Gm = Geom<LOGN>;
-  extern __shared__ uint64_t sm[];
+  extern __shared__ double sm[];
   const int t = threadIdx.x, l = blockIdx.y;
   const size_t base = ((size_t)blockIdx.x * P.L + l) * Gm::N;
   const PrimeConsts pc = pick(P, l);
-  const ulonglong2 *tw = P.tw_inv + (size_t)l * Gm::N;
-  uint64_t a[16];
-  load_ntt_domain<LOGN>(a, in + base, t);
+  const double *tw = P.twd_inv + (size_t)l * Gm::N;
+  double a[16];
+  load_ntt_domain<LOGN>(a, in + base, t, pc);
   inv_rounds_from<LOGN, Gm::NR - 1>(a, sm, t, tw, pc);
   constexpr int K = Gm::k(0), G = 16 >> K;
 #pragma unroll
   for (int g = 0; g < G; g++)
 #pragma unroll
-    for (int u = 0; u < (1 << K); u++) {
-      uint64_t x = a[g * (1 << K) + u];
-      x = x >= pc.p ? x - pc.p : x;
-      out[base + elem_idx<LOGN, 0>(t, g, u)] = x;
-    }
+    for (int u = 0; u < (1 << K); u++)
+      out[base + elem_idx<LOGN, 0>(t, g, u)] = d2u(canon_d(a[g * (1 << K) + u], pc.pd, pc.pinv));
 }
 
 // ---------------------------------------------------------------------------------------
@@ -402,8 +439,8 @@ __global__ void __launch_bounds__(Geom<LOGN>::NT)
 k_ntt_inv_mask(const uint64_t *__restrict__ ct_ntt, uint64_t *__restrict__ masked, uint64_t *__restrict__ share,
                MaskArgs M, DevParams P) {
   using Gm = Geom<LOGN>;
-  extern __shared__ uint64_t sm[];
-  uint64_t *sig_sm = sm + Gm::SMEM_WORDS;   // sigma at kept positions (index k*m + i)
+  extern __shared__ double sm[];
+  uint64_t *sig_sm = reinterpret_cast<uint64_t *>(sm + Gm::SMEM_WORDS);   // sigma at kept positions
   const int t = threadIdx.x;
   const int c = blockIdx.x & 1;
   const int64_t o = blockIdx.x >> 1;                  // I_loc * nK + K
@@ -427,17 +464,16 @@ k_ntt_inv_mask(const uint64_t *__restrict__ ct_ntt, uint64_t *__restrict__ maske
   }
   for (int l = 0; l < L; l++) {
     const PrimeConsts pc = pick(P, l);
-    const ulonglong2 *tw = P.tw_inv + (size_t)l * Gm::N;
-    uint64_t a[16];
-    load_ntt_domain<LOGN>(a, ct_ntt + (((size_t)o * 2 + c) * L + l) * Gm::N, t);
+    const double *tw = P.twd_inv + (size_t)l * Gm::N;
+    double a[16];
+    load_ntt_domain<LOGN>(a, ct_ntt + (((size_t)o * 2 + c) * L + l) * Gm::N, t, pc);
     inv_rounds_from<LOGN, Gm::NR - 1>(a, sm, t, tw, pc);
     constexpr int K0 = Gm::k(0), G = 16 >> K0;
 #pragma unroll
     for (int g = 0; g < G; g++)
 #pragma unroll
       for (int u = 0; u < (1 << K0); u++) {
-        uint64_t x = a[g * (1 << K0) + u];
-        x = x >= pc.p ? x - pc.p : x;
+        const uint64_t x = d2u(canon_d(a[g * (1 << K0) + u], pc.pd, pc.pinv));
         const int idx = elem_idx<LOGN, 0>(t, g, u);
         if (c == 1) {
           dst[(size_t)L * mn + (size_t)l * Gm::N + idx] = x;
