@@ -62,6 +62,9 @@ def counts(cfg, lay_by_mm):
             bfly_inv=nI * nC * L * (N // 2) * logN,
             # MAC kernel bytes: weight cache + NTT-domain ct_in (read once) + NTT-domain output
             mac_bytes=8 * (-(-nI // 16) * 16 * nJ * L * N + nJ * nC * L * N + nI * nC * L * N),
+            # tensor-core engine: weight residues as 7 byte limbs (the least whole bytes of a
+            # 50-bit residue), ct_in residues and outputs as u64, each read/written once
+            mac_bytes_tc=(7 * nI * nJ + 8 * nJ * nC + 8 * nI * nC) * L * N,
             fwd_bytes=8 * 2 * nJ * nC * L * N,                   # coefficient ct_in in, limb pairs out
             inv_bytes=8 * (nI * nC * L * N + nI * nK * L * (m * n + N) + mm.Nb * mm.Ma),
             # whole-path algorithmic bytes (SURVEY.md §8(d) "Bytes")
@@ -247,8 +250,10 @@ def run_ours(args, rank, world, local_rank):
     # ALU peaks, measured on this B200 by tools/microbench/intpipe3.cu
     # (profiles/r01/microbench_intpipe3.log): IMAD.WIDE.U32 24.4 /clk/SM (the IMAD engine's
     # multiply), DFMA 57.3 /clk/SM (the default FP64 engine); x 148 SMs x max SM clock.
-    engine = os.environ.get("HELINEAR_MAC_ENGINE", "f64")
-    if engine == "imad":
+    engine = os.environ.get("HELINEAR_MAC_ENGINE", "tc")
+    if engine == "tc":
+        ops_per_mac, alu_peak, alu_unit = 0.0, 1.0, ""
+    elif engine == "imad":
         ops_per_mac, alu_peak, alu_unit = 3.0, IMAD_WIDE_PER_CLK_SM * 148 * sm_max * 1e6, "T IMAD.WIDE/s (3 per modular MAC)"
     else:
         ops_per_mac, alu_peak, alu_unit = FP64_OPS_PER_MAC, DFMA_PER_CLK_SM * 148 * sm_max * 1e6, \
@@ -256,8 +261,9 @@ def run_ours(args, rank, world, local_rank):
     mac_ms, mac_n = ktimes["mac"]
     mac_avg_s = mac_ms / max(mac_n, 1) * 1e-3
     per_launch_mac = sum(c["mac"] for c in cnt) / len(cnt)
-    per_launch_bytes = sum(c["mac_bytes"] for c in cnt) / len(cnt)
-    # bound of the MAC kernel: the slower of the ALU pipe and HBM
+    per_launch_bytes = sum(c["mac_bytes_tc" if engine == "tc" else "mac_bytes"] for c in cnt) / len(cnt)
+    # bound of the MAC kernel: the slower of the ALU pipe and HBM (the tensor-core engine's int8
+    # MMA time is < 1/3 of its HBM time at these shapes: HBM-bound)
     t_alu = ops_per_mac * per_launch_mac / alu_peak
     t_hbm = per_launch_bytes / (hbm * 1e9)
     if t_alu >= t_hbm:
@@ -267,9 +273,10 @@ def run_ours(args, rank, world, local_rank):
         roof = {"bound": "hbm", "achieved": per_launch_bytes / mac_avg_s / 1e9, "peak": hbm, "unit": "GB/s"}
     roof["frac"] = roof["achieved"] / roof["peak"]
     roof["traffic"] = None
-    roof["kernel"] = ("k_mac_f64" if engine != "imad" else "k_mac") + " (slot-parallel modular MAC)"
+    roof["kernel"] = {"tc": "k_mac_tc", "f64": "k_mac_f64", "imad": "k_mac"}[engine] + " (slot-parallel modular MAC)"
     roof["peak_source"] = (("measured DFMA 57.3" if engine != "imad" else "measured IMAD.WIDE 24.4") +
                            "/clk/SM x 148 SMs x sm_max_mhz (DESIGN.md §6)" if roof["bound"] == "alu" else hbm_src)
+    roof["engine"] = engine
     roof["hbm_frac_same_kernel"] = per_launch_bytes / mac_avg_s / 1e9 / hbm
     total_k = sum(v[0] for v in ktimes.values())
     kernel_share = {k: {"ms_per_step": v[0] / args.steps, "launches_per_step": v[1] / args.steps,

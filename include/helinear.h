@@ -100,10 +100,12 @@ int hl_ctx_create(uint32_t N, uint32_t L, uint32_t log2_t, const uint64_t *prime
 int hl_ctx_destroy(hl_ctx *ctx);
 
 /* Select the MAC engine of he_matmul: 0 = IMAD.WIDE.U32 on 25-bit limbs,
- * 1 = exact FP64 products (error-free DFMA transformations; default).  Results are
- * bit-identical; the NTT-domain weight cache and workspace formats differ, so a cache must be
- * encoded and used under the same engine.  The environment variable HELINEAR_MAC_ENGINE=imad
- * selects engine 0 at context creation.  Not thread-safe against concurrent calls on ctx. */
+ * 1 = exact FP64 products (error-free DFMA transformations), 2 = exact products on the int8
+ * tensor cores (tcgen05.mma kind::i8, 7 byte limbs, TMEM accumulators; default).  Results are
+ * bit-identical; the NTT-domain weight cache and workspace formats (and sizes, see
+ * hl_layout_query) differ, so a cache must be encoded and used under the same engine.  The
+ * environment variable HELINEAR_MAC_ENGINE=imad|f64|tc selects the engine at context creation.
+ * Not thread-safe against concurrent calls on ctx. */
 int hl_ctx_set_mac_engine(hl_ctx *ctx, int engine);
 
 /* Copy the primes and Delta mod p_l (Delta = floor(q/t), reading C5) into caller arrays of L. */

@@ -162,10 +162,11 @@ class Context:
         self.primes = tuple(int(v) for v in p)
         self.delta_mod = tuple(int(v) for v in d)
 
-    MAC_IMAD, MAC_F64 = 0, 1
+    MAC_IMAD, MAC_F64, MAC_TC = 0, 1, 2
 
     def set_mac_engine(self, engine: int):
-        """0 = IMAD.WIDE limbs, 1 = exact FP64 products (default).  Re-encode weights after."""
+        """0 = IMAD.WIDE limbs, 1 = exact FP64 products, 2 = int8 tensor cores (default).
+        Re-encode weights after (cache formats differ)."""
         _check(_lib.hl_ctx_set_mac_engine(self._h, int(engine)))
 
     def close(self):

@@ -29,7 +29,7 @@ CXX_FLAGS = ["-O2", "-std=c++17", "-fPIC", "-fopenmp", "-Wall", "-Wno-unknown-pr
 
 CU_SOURCES = ["kernels.cu"]
 CXX_SOURCES = ["ctx.cpp", "client.cpp"]
-HEADERS = ["hl_internal.h", "chacha.h"]
+HEADERS = ["hl_internal.h", "chacha.h", "mac_tc.cuh"]
 
 
 def _newer(src_list, target) -> bool:

@@ -192,7 +192,8 @@ extern "C" int hl_ctx_create(uint32_t N, uint32_t L, uint32_t log2_t, const uint
     pc.ninv_d = (double)pc.ninv; pc.ninv_w1_d = (double)pc.ninv_w1;
   }
   build_cdt(c->cdt);
-  if (const char *e = getenv("HELINEAR_MAC_ENGINE")) c->mac_engine = (strcmp(e, "imad") == 0) ? 0 : 1;
+  if (const char *e = getenv("HELINEAR_MAC_ENGINE"))
+    c->mac_engine = (strcmp(e, "imad") == 0) ? 0 : ((strcmp(e, "f64") == 0) ? 1 : 2);
   // device tables (device < 0: host-only context for the client calls; no CUDA needed)
   if (device < 0) {
     dp.twd_fwd = dp.twd_inv = nullptr;
@@ -276,7 +277,7 @@ extern "C" int hl_ctx_destroy(hl_ctx *c) {
 
 extern "C" int hl_ctx_set_mac_engine(hl_ctx *c, int engine) {
   if (!c) return hl_fail(HL_EINVAL, "hl_ctx_set_mac_engine: ctx is NULL");
-  if (engine != 0 && engine != 1) return hl_fail(HL_EINVAL, "hl_ctx_set_mac_engine: engine must be 0 or 1");
+  if (engine < 0 || engine > 2) return hl_fail(HL_EINVAL, "hl_ctx_set_mac_engine: engine must be 0, 1 or 2");
   c->mac_engine = engine;
   return HL_OK;
 }
@@ -321,8 +322,15 @@ extern "C" int hl_layout_query(const hl_ctx *c, hl_tile tile, int64_t Ma, int64_
   out->ct_masked_words = g.nIs * g.nK * (int64_t)c->L * ((int64_t)g.m * g.n + c->N);
   out->ct_full_words = g.nIs * g.nK * 2 * LN;
   out->share_words = Nb * Ma;
-  out->wcache_bytes = (g.nIs + 15) / 16 * 16 * g.nJ * LN * 8;   // I rows padded to 16 (MAC tiles)
-  out->workspace_bytes = g.nJ * g.nK * 2 * LN * 12;   // limb pairs + limb sums (MAC operand X)
+  const int64_t nIp = (g.nIs + 15) / 16 * 16;                     // I rows padded to 16 (MAC tiles)
+  if (c->mac_engine == 2) {            // int8 tensor cores: 7 byte planes per residue, J padded to 32
+    const int64_t nJp = (g.nJ + 31) / 32 * 32;
+    out->wcache_bytes = nIp * nJp * LN * 7;
+    out->workspace_bytes = nJp * g.nK * 2 * LN * 8;                // canonical residues [cg][LN][nJp][CW]
+  } else {
+    out->wcache_bytes = nIp * g.nJ * LN * 8;
+    out->workspace_bytes = g.nJ * g.nK * 2 * LN * 12;              // limb pairs + limb sums (MAC operand X)
+  }
   return HL_OK;
 }
 

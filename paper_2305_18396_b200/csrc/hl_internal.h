@@ -49,7 +49,7 @@ struct hl_ctx {
   uint32_t N, L, log2_t;
   int device;
   int num_sms = 148;
-  int mac_engine = 1;                 // 0 = IMAD.WIDE limbs, 1 = exact FP64 products (default)
+  int mac_engine = 2;                 // 0 = IMAD.WIDE limbs, 1 = exact FP64 products, 2 = int8 tensor cores (default)
   std::vector<uint64_t> primes;
   std::vector<uint64_t> psi;          // primitive 2N-th roots
   std::vector<uint64_t> delta_mod;    // Delta mod p_l

@@ -254,6 +254,8 @@ __device__ __forceinline__ int slot_of(int t, int u) { return u * Geom<LOGN>::NT
 struct MacGeom {
   int nIs, nIb, nJ, nC, CW, nCg, nSb, LN;
   int f64;       // MAC engine: 0 = IMAD.WIDE on 25-bit limbs, 1 = exact FP64 (DFMA) products
+  int engine;    // 0 IMAD, 1 FP64, 2 int8 tensor cores (mac_tc.cuh)
+  int nIp, nIt, nJp, nJc;   // engine 2: rows padded to 16, I tiles of 128, J padded to 32, 32-J steps
 };
 
 __host__ __device__ __forceinline__ size_t w_index(const MacGeom &g, int iloc, int J, int s) {
@@ -271,11 +273,19 @@ __host__ __device__ __forceinline__ size_t x_chunk(const MacGeom &g, int J, int 
 MacGeom mac_geom(const hl_ctx *c, int64_t nIs, int64_t nJ, int64_t nC) {
   MacGeom g;
   g.nIs = (int)nIs; g.nIb = (int)((nIs + 15) / 16); g.nJ = (int)nJ; g.nC = (int)nC;
-  g.CW = (nC % 8 == 0) ? 8 : ((nC % 4 == 0) ? 4 : 2);
+  g.engine = c->mac_engine;
+  if (g.engine == 2)
+    g.CW = (nC % 16 == 0) ? 16 : ((nC % 8 == 0) ? 8 : ((nC % 4 == 0) ? 4 : 2));
+  else
+    g.CW = (nC % 8 == 0) ? 8 : ((nC % 4 == 0) ? 4 : 2);
   g.nCg = (int)(nC / g.CW);
   g.LN = (int)(c->L * c->N);
   g.nSb = g.LN / 32;
   g.f64 = c->mac_engine == 1;
+  g.nIp = g.nIb * 16;
+  g.nIt = (g.nIp + 127) / 128;
+  g.nJp = (int)((nJ + 31) / 32 * 32);
+  g.nJc = g.nJp / 32;
   return g;
 }
 
@@ -309,7 +319,10 @@ k_ntt_fwd(const uint64_t *__restrict__ in, void *__restrict__ out, DevParams P, 
       const int s = l * Gm::N + slot_of<LOGN>(t, u);
       uint32_t *ch = reinterpret_cast<uint32_t *>(out) + x_chunk(mg, J, col / mg.CW, s >> 5);
       const int e = (s & 31) * mg.CW + col % mg.CW;
-      if (mg.f64) {
+      if (mg.engine == 2) {
+        const int cg = col / mg.CW, c = col % mg.CW;
+        reinterpret_cast<uint64_t *>(out)[(((size_t)cg * mg.LN + s) * mg.nJp + J) * mg.CW + c] = d2u(xd);
+      } else if (mg.f64) {
         reinterpret_cast<double *>(ch)[e] = xd;
       } else {
         const uint64_t x = d2u(xd);
@@ -383,7 +396,15 @@ k_encode_weights(EncodeArgs A, uint2 *__restrict__ wcache, DevParams P, uint32_t
     const double xd = canon_d(a[u], pc.pd, pc.pinv);
     const uint64_t x = d2u(xd);
     const int s = l * Gm::N + slot_of<LOGN>(t, u);
-    if (A.mg.f64)
+    if (A.mg.engine == 2) {
+      // 7 byte planes, UMMA canonical K-major: [I tile][slot][32-J step][plane][K half][row][16 B]
+      const int tt = (int)(Iloc >> 7), row = (int)(Iloc & 127);
+      const int rows = min(128, A.mg.nIp - 128 * tt);
+      uint8_t *wb = reinterpret_cast<uint8_t *>(wcache) + (size_t)tt * 128 * A.mg.LN * A.mg.nJp * 7 +
+                    ((size_t)s * A.mg.nJc + (J >> 5)) * 224 * rows + ((J >> 4) & 1) * rows * 16 + row * 16 + (J & 15);
+#pragma unroll
+      for (int a = 0; a < 7; a++) wb[a * 32 * rows] = (uint8_t)(x >> (8 * a));
+    } else if (A.mg.f64)
       reinterpret_cast<double *>(wcache)[w_index(A.mg, (int)Iloc, (int)J, s)] = xd;
     else
       wcache[w_index(A.mg, (int)Iloc, (int)J, s)] = make_uint2((uint32_t)x & kLimbMask, (uint32_t)(x >> kLimbBits));
@@ -900,6 +921,8 @@ k_mac_f64(MacArgs A, DevParams P) {
   }
 }
 
+#include "mac_tc.cuh"
+
 // pointwise product in the NTT domain (diagnostics only)
 __global__ void k_pointwise(const uint64_t *a, const uint64_t *b, uint64_t *out, int64_t n, DevParams P) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -989,7 +1012,33 @@ void launch_mac_ln(const hl_ctx *c, const MacArgs &A, cudaStream_t st) {
   }
 }
 
+template <int CW>
+void launch_mac_tc_t(const hl_ctx *c, const MacTcArgs &A, cudaStream_t st) {
+  using T = TcGeom<CW>;
+  static bool init = false;
+  if (!init) { set_smem(k_mac_tc<CW>, T::SMEM); init = true; }
+  KTimer kt(c, HL_K_MAC, st);
+  k_mac_tc<CW><<<c->num_sms, 256, T::SMEM, st>>>(A, c->dp);
+}
+
+void launch_mac_tc(const hl_ctx *c, const void *W, const void *X, uint64_t *out, const MacGeom &g, cudaStream_t st) {
+  MacTcArgs A;
+  A.W = (const uint8_t *)W; A.X = (const uint64_t *)X; A.out = out; A.g = g; A.N = (int)c->N;
+  for (int64_t j0 = 0; j0 < g.nJp; j0 += kMacJChunk) {     // S_d < 7 * 4096 * 255^2 < 2^31 per launch
+    A.jc0 = (int)(j0 / 32);
+    A.njc = (int)((std::min<int64_t>(g.nJp, j0 + kMacJChunk) - j0) / 32);
+    A.accumulate = j0 > 0;
+    switch (g.CW) {
+      case 16: launch_mac_tc_t<16>(c, A, st); break;
+      case 8: launch_mac_tc_t<8>(c, A, st); break;
+      case 4: launch_mac_tc_t<4>(c, A, st); break;
+      default: launch_mac_tc_t<2>(c, A, st); break;
+    }
+  }
+}
+
 void launch_mac(const hl_ctx *c, const uint2 *W, const uint32_t *X, uint64_t *out, const MacGeom &g, cudaStream_t st) {
+  if (g.engine == 2) { launch_mac_tc(c, W, X, out, g, st); return; }
   MacArgs A;
   A.W = W; A.X = X; A.out = out; A.g = g; A.N = (int)c->N;
   for (int64_t j0 = 0; j0 < g.nJ; j0 += kMacJChunk) {
@@ -1039,6 +1088,8 @@ extern "C" int hl_encode_weights(const hl_ctx *c, hl_tile tile, const uint64_t *
   cudaSetDevice(c->device);
   cudaMemsetAsync(c->d_flags, 0, 8, st);
   const MacGeom mg = mac_geom(c, g.nIs, g.nJ, 2 * g.nK);
+  if (mg.engine == 2 && mg.nJp != mg.nJ)      // J padded to the 32-J MMA step: zero weight planes
+    cudaMemsetAsync(wcache, 0, (size_t)mg.nIp * mg.LN * mg.nJp * 7, st);
   EncodeArgs A{W, R, Ma, g.nJ, g.nIs, g.i_begin, g.m, g.r, mg};
   dim3 grid((unsigned)((int64_t)mg.nIb * 16 * g.nJ), c->L);
   {

@@ -1,0 +1,318 @@
+// mac_tc.cuh -- the slot-parallel modular MAC on the 5th-generation tensor cores (tcgen05,
+// kind::i8, accumulators in TMEM).  Included by kernels.cu inside its anonymous namespace.
+//
+// What it computes (the "elementwise multiplication" of PAPER.md:156 fn
+// accumulated over the shared dimension, reading C3): for every prime l and NTT slot s,
+//     out[I][col][s] = sum_J W[I][J][s] * X[J][col][s]  mod p_l          (W, X < p_l < 2^50)
+// i.e. one small GEMM (nI x nJ) . (nJ x nC) per slot.  Exact integer products on int8 tensor
+// cores: residues are split into 7 unsigned bytes, W = sum_a w_a 2^(8a), X = sum_b x_b 2^(8b),
+//     sum_J W X = sum_{d=0..12} 2^(8d) S_d,   S_d = sum_{a+b=d} sum_J w_a x_b   (S_d < 2^31 for nJ <= 4096)
+// and the tensor core forms every S_d directly: for limb plane a, MMA a multiplies A_a = w_a
+// [128 I rows x 32 J] by a B operand whose row (d*CW + c) holds x_{d-a}[c] -- a window into ONE
+// Toeplitz image Z of the X limbs (rows (b+6)*CW + c hold x_b[c], all other rows zero), selected
+// by shifting the B descriptor's start address by (6-a)*CW rows.  7 MMAs per 32-J step
+// accumulate S_d[I][c] in TMEM column d*CW + c; the epilogue forms sum_d S_d 2^(8d) (< 2^124)
+// and reduces it mod p_l once per output.
+//
+// Kernel roles (256 threads, one persistent CTA per SM):
+//   warp 0      TMA producer: per (slot, 32-J step) one cp.async.bulk of the 7 weight planes
+//               (224 B per I row, pre-laid-out by encode_weights in UMMA canonical K-major
+//               no-swizzle form) and one of the X residues (u64, written by the forward NTT)
+//   warp 1      TMEM allocator + single-thread MMA issuer (tcgen05.mma, tcgen05.commit)
+//   warps 2-3   converters: u64 residues -> byte rows of the Toeplitz image Z (generic stores,
+//               fence.proxy.async before release to the tensor core)
+//   warps 4-7   epilogue: tcgen05.ld of S_d, 128-bit recombination, mod p, staging of 4 slots,
+//               full 32-B sector stores of out[I][col][s..s+3]
+// Work item = (I tile of 128 rows, column group of CW, 4 consecutive slots); TMEM holds two
+// accumulators so the epilogue of slot s overlaps the MMAs of slot s+1.
+#pragma once
+
+template <int CW>
+struct TcGeom {
+  static constexpr int N = ((13 * CW + 15) / 16) * 16;   // MMA N: columns d*CW + c, d < 13
+  static constexpr int ZR = N + 6 * CW;                  // rows of the Toeplitz B image
+  static constexpr int A_BYTES = 7 * 2 * 128 * 16;       // 7 planes x (2 K-halves x 128 rows x 16 B)
+  static constexpr int RAW_BYTES = 32 * CW * 8;          // X residues of one 32-J step
+  static constexpr int Z_BYTES = 2 * ZR * 16;
+  static constexpr int STAGE = A_BYTES + RAW_BYTES + Z_BYTES;
+  static constexpr int NST = CW >= 16 ? 3 : 4;           // ring depth
+  static constexpr int SPI = 4;                          // slots per work item (32-B output sectors)
+  static constexpr int STG_STRIDE = CW * SPI + 1;        // u64 per staged row (+1: bank spread)
+  static constexpr int STG_BYTES = 128 * STG_STRIDE * 8;
+  static constexpr int TCOLS = 2 * N <= 64 ? 64 : (2 * N <= 128 ? 128 : (2 * N <= 256 ? 256 : 512));
+  static constexpr int BAR_BYTES = 256;
+  static constexpr int SMEM = NST * STAGE + STG_BYTES + BAR_BYTES;
+  static_assert(STAGE % 128 == 0, "stage alignment");
+};
+
+struct MacTcArgs {
+  const uint8_t *W;       // weight planes (encode_weights, engine 2 layout)
+  const uint64_t *X;      // NTT-domain ct_in residues [nCg][LN][nJp][CW]
+  uint64_t *out;          // [nIs][nC][LN] canonical residues
+  MacGeom g;
+  int N, jc0, njc, accumulate;
+};
+
+// UMMA shared-memory descriptor: K-major, no swizzle; core matrix = 8 rows x 16 B contiguous.
+// lbo = byte distance between the two 16-B K halves, sbo = between 8-row groups; version 1 (sm_100).
+__device__ __forceinline__ uint64_t umma_sdesc(uint32_t addr, uint32_t lbo, uint32_t sbo) {
+  return (uint64_t)((addr >> 4) & 0x3fff) | ((uint64_t)((lbo >> 4) & 0x3fff) << 16) |
+         ((uint64_t)((sbo >> 4) & 0x3fff) << 32) | (1ull << 46);
+}
+// instruction descriptor kind::i8: A, B unsigned 8-bit K-major, D s32, M x N
+__host__ __device__ constexpr uint32_t umma_idesc_u8(int M, int N) {
+  return (2u << 4) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
+}
+
+__device__ __forceinline__ void umma_i8(uint32_t d_tmem, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
+  asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+               "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t}"
+               ::"r"(d_tmem), "l"(a), "l"(b), "r"(idesc), "r"(acc));
+}
+__device__ __forceinline__ void umma_commit(uint64_t *bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];"
+               ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+
+template <int CW>
+__device__ __forceinline__ void tmem_ld_cw(uint32_t addr, uint32_t (&v)[CW]) {
+  if constexpr (CW == 2) {
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x2.b32 {%0,%1}, [%2];" : "=r"(v[0]), "=r"(v[1]) : "r"(addr));
+  } else if constexpr (CW == 4) {
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]) : "r"(addr));
+  } else if constexpr (CW == 8) {
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                 : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7])
+                 : "r"(addr));
+  } else {
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+                 : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+                   "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
+                 : "r"(addr));
+  }
+}
+
+// Work schedule shared by every role: round k covers, for one (I tile, column group) "kind",
+// the slot quads blockIdx.x + G*(k / kinds); kinds alternate per round so every CTA sees the same
+// mix of full and partial I tiles.
+struct TcItem { int t, cg, sq; };
+__device__ __forceinline__ bool tc_item(const MacGeom &g, int k, TcItem &it) {
+  const int kinds = g.nIt * g.nCg;
+  const int kind = k % kinds;
+  it.sq = (k / kinds) * (int)gridDim.x + (int)blockIdx.x;
+  it.t = kind / g.nCg;
+  it.cg = kind % g.nCg;
+  return it.sq < g.LN / 4;
+}
+__device__ __forceinline__ int tc_rounds(const MacGeom &g) {
+  return g.nIt * g.nCg * ((g.LN / 4 + (int)gridDim.x - 1) / (int)gridDim.x);
+}
+
+template <int CW>
+__global__ void __launch_bounds__(256, 1)
+k_mac_tc(MacTcArgs A, DevParams P) {
+  using T = TcGeom<CW>;
+  constexpr int NST = T::NST;
+  extern __shared__ __align__(128) unsigned char smem[];
+  uint64_t *stg = reinterpret_cast<uint64_t *>(smem + NST * T::STAGE);
+  uint64_t *full = reinterpret_cast<uint64_t *>(smem + NST * T::STAGE + T::STG_BYTES);
+  uint64_t *zfull = full + NST, *empty = zfull + NST, *tfull = empty + NST, *tempty = tfull + 2;
+  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(tempty + 2);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const MacGeom &g = A.g;
+  const int nrounds = tc_rounds(g);
+
+  // ---- setup: zero the Toeplitz images (only data rows are rewritten), barriers, TMEM
+  for (int st = 0; st < NST; st++) {
+    uint4 *z = reinterpret_cast<uint4 *>(smem + st * T::STAGE + T::A_BYTES + T::RAW_BYTES);
+    for (int i = threadIdx.x; i < T::Z_BYTES / 16; i += blockDim.x) z[i] = make_uint4(0, 0, 0, 0);
+  }
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < NST; i++) { mbar_init(&full[i], 1); mbar_init(&zfull[i], 64); mbar_init(&empty[i], 1); }
+    for (int i = 0; i < 2; i++) { mbar_init(&tfull[i], 1); mbar_init(&tempty[i], 4); }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;"
+                 ::"r"(smem_u32(tmem_slot)), "n"(T::TCOLS));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    // ------------------------------------------------------------------ TMA producer
+    if (lane == 0) {
+      int st = 0;
+      uint32_t ph = 1;
+      for (int k = 0; k < nrounds; k++) {
+        TcItem it;
+        if (!tc_item(g, k, it)) continue;
+        const int rows = min(128, g.nIp - 128 * it.t);
+        const uint32_t abytes = 224u * rows;
+        const uint8_t *wt = A.W + (size_t)it.t * 128 * g.LN * g.nJp * 7;
+        for (int si = 0; si < T::SPI; si++) {
+          const int s = it.sq * T::SPI + si;
+          for (int kk = 0; kk < A.njc; kk++) {
+            const int jc = A.jc0 + kk;
+            mbar_wait(&empty[st], ph);
+            unsigned char *dst = smem + st * T::STAGE;
+            mbar_expect_tx(&full[st], abytes + T::RAW_BYTES);
+            bulk_g2s(dst, wt + ((size_t)s * g.nJc + jc) * abytes, abytes, &full[st]);
+            bulk_g2s(dst + T::A_BYTES, A.X + (((size_t)it.cg * g.LN + s) * g.nJp + (size_t)jc * 32) * CW,
+                     T::RAW_BYTES, &full[st]);
+            if (++st == NST) { st = 0; ph ^= 1; }
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ------------------------------------------------------------------ MMA issuer
+    if (lane == 0) {
+      const uint32_t idesc = umma_idesc_u8(128, T::N);
+      int st = 0;
+      uint32_t ph = 0;
+      uint32_t tile_no = 0;
+      for (int k = 0; k < nrounds; k++) {
+        TcItem it;
+        if (!tc_item(g, k, it)) continue;
+        const int rows = min(128, g.nIp - 128 * it.t);
+        for (int si = 0; si < T::SPI; si++, tile_no++) {
+          const uint32_t buf = tile_no & 1, tph = (tile_no >> 1) & 1;
+          mbar_wait(&tempty[buf], tph ^ 1);
+          tc_fence_after();
+          const uint32_t dcol = tmem + buf * T::N;
+          for (int kk = 0; kk < A.njc; kk++) {
+            mbar_wait(&full[st], ph);
+            mbar_wait(&zfull[st], ph);
+            tc_fence_after();
+            const uint32_t a0 = smem_u32(smem + st * T::STAGE);
+            const uint32_t z0 = a0 + T::A_BYTES + T::RAW_BYTES;
+#pragma unroll
+            for (int a = 0; a < 7; a++) {
+              const uint64_t ad = umma_sdesc(a0 + a * 32 * rows, rows * 16, 128);
+              const uint64_t bd = umma_sdesc(z0 + (6 - a) * CW * 16, T::ZR * 16, 128);
+              umma_i8(dcol, ad, bd, idesc, (kk | a) ? 1u : 0u);
+            }
+            umma_commit(&empty[st]);
+            if (++st == NST) { st = 0; ph ^= 1; }
+          }
+          umma_commit(&tfull[buf]);
+        }
+      }
+    }
+  } else if (warp < 4) {
+    // ------------------------------------------------------------------ converters
+    const int ct = threadIdx.x - 64;
+    int st = 0;
+    uint32_t ph = 0;
+    for (int k = 0; k < nrounds; k++) {
+      TcItem it;
+      if (!tc_item(g, k, it)) continue;
+      for (int si = 0; si < T::SPI; si++) {
+        for (int kk = 0; kk < A.njc; kk++) {
+          mbar_wait(&full[st], ph);
+          const uint64_t *raw = reinterpret_cast<const uint64_t *>(smem + st * T::STAGE + T::A_BYTES);
+          unsigned char *z = smem + st * T::STAGE + T::A_BYTES + T::RAW_BYTES;
+          for (int q = ct; q < CW * 8; q += 64) {
+            const int c = q >> 3, h = (q >> 2) & 1, gq = q & 3;
+            const int j0 = h * 16 + gq * 4;
+            uint32_t lo[4], hi[4];
+#pragma unroll
+            for (int j = 0; j < 4; j++) {
+              const uint64_t x = raw[(j0 + j) * CW + c];
+              lo[j] = (uint32_t)x; hi[j] = (uint32_t)(x >> 32);
+            }
+            uint32_t *zrow = reinterpret_cast<uint32_t *>(z + ((size_t)h * T::ZR + 6 * CW + c) * 16) + gq;
+#pragma unroll
+            for (int b = 0; b < 7; b++) {
+              const uint32_t *src = b < 4 ? lo : hi;
+              const uint32_t bb = b & 3;
+              const uint32_t sel = bb | ((bb + 4) << 4);
+              const uint32_t t01 = __byte_perm(src[0], src[1], sel);
+              const uint32_t t23 = __byte_perm(src[2], src[3], sel);
+              zrow[b * CW * 4] = __byte_perm(t01, t23, 0x5410);   // row (b+6)*CW + c
+            }
+          }
+          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+          mbar_arrive(&zfull[st]);
+          if (++st == NST) { st = 0; ph ^= 1; }
+        }
+      }
+    }
+  } else {
+    // ------------------------------------------------------------------ epilogue
+    const int q = warp - 4;                          // TMEM lane quadrant of this warp
+    const int row = 32 * q + lane;
+    const int et = threadIdx.x - 128;
+    uint32_t tile_no = 0;
+    for (int k = 0; k < nrounds; k++) {
+      TcItem it;
+      if (!tc_item(g, k, it)) continue;
+      const int l = (it.sq * T::SPI) / A.N;
+      const PrimeConsts pc = pick(P, l);
+      for (int si = 0; si < T::SPI; si++, tile_no++) {
+        const uint32_t buf = tile_no & 1, tph = (tile_no >> 1) & 1;
+        mbar_wait(&tfull[buf], tph);
+        tc_fence_after();
+        hl_u128 acc[CW];
+#pragma unroll
+        for (int c = 0; c < CW; c++) acc[c] = 0;
+        const uint32_t base = tmem + ((uint32_t)(32 * q) << 16) + buf * T::N;
+#pragma unroll
+        for (int d = 0; d < 13; d++) {
+          uint32_t v[CW];
+          tmem_ld_cw<CW>(base + d * CW, v);
+          asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+          for (int c = 0; c < CW; c++) acc[c] += (hl_u128)v[c] << (8 * d);
+        }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&tempty[buf]);
+#pragma unroll
+        for (int c = 0; c < CW; c++) {
+          const uint64_t vh = (uint64_t)(acc[c] >> 64), vl = (uint64_t)acc[c];
+          const uint64_t r1 = shoup_mul(vh, pc.r64, pc.r64_sh, pc.p);   // vh 2^64 mod p, [0, 2p)
+          const uint64_t r2 = vl - __umul64hi(vl, pc.mu) * pc.p;        // vl mod p, [0, 2p)
+          uint64_t r = r1 + r2;
+          r = r >= pc.two_p ? r - pc.two_p : r;
+          r = r >= pc.p ? r - pc.p : r;
+          stg[row * T::STG_STRIDE + c * T::SPI + si] = r;
+        }
+      }
+      // 4 slots staged: full 32-B sector stores of out[I][col][s0 .. s0+3]
+      asm volatile("bar.sync 2, 128;" ::: "memory");
+      const int rows_valid = min(128, g.nIs - 128 * it.t);
+      const size_t s0 = (size_t)it.sq * T::SPI;
+      for (int e = et; e < rows_valid * CW; e += 128) {
+        const int rr = e / CW, c = e % CW;
+        const uint64_t *sv = stg + rr * T::STG_STRIDE + c * T::SPI;
+        uint64_t v0 = sv[0], v1 = sv[1], v2 = sv[2], v3 = sv[3];
+        ulonglong2 *dst = reinterpret_cast<ulonglong2 *>(
+            A.out + ((size_t)(128 * it.t + rr) * g.nC + it.cg * CW + c) * g.LN + s0);
+        if (A.accumulate) {
+          const ulonglong2 o0 = dst[0], o1 = dst[1];
+          v0 += o0.x; v1 += o0.y; v2 += o1.x; v3 += o1.y;
+          v0 = v0 >= pc.p ? v0 - pc.p : v0; v1 = v1 >= pc.p ? v1 - pc.p : v1;
+          v2 = v2 >= pc.p ? v2 - pc.p : v2; v3 = v3 >= pc.p ? v3 - pc.p : v3;
+        }
+        dst[0] = make_ulonglong2(v0, v1);
+        dst[1] = make_ulonglong2(v2, v3);
+      }
+      asm volatile("bar.sync 2, 128;" ::: "memory");
+    }
+  }
+
+  // ---- teardown
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(T::TCOLS));
+}

@@ -242,7 +242,7 @@ def test_encode_weights_errors(hl, ctx4096):
 
 
 # ------------------------------------------------------------------------- both MAC engines
-@pytest.mark.parametrize("engine", [0, 1])
+@pytest.mark.parametrize("engine", [0, 1, 2])
 @pytest.mark.parametrize("N,shape,tile", [
     (4096, (40, 24, 40), (16, 8, 32)),
     (4096, (64, 48, 100), (4, 8, 16)),
@@ -250,7 +250,8 @@ def test_encode_weights_errors(hl, ctx4096):
     (8192, (32, 48, 40), (32, 16, 16)),
 ])
 def test_mac_engines_bit_exact(hl, ctx4096, ctx8192, engine, N, shape, tile):
-    """IMAD.WIDE (engine 0) and exact-FP64 (engine 1) MACs both equal the oracle."""
+    """IMAD.WIDE (engine 0), exact-FP64 (engine 1) and int8 tensor-core (engine 2, the default)
+    MACs all equal the oracle."""
     ctx = ctx4096 if N == 4096 else ctx8192
     Nb, R, Ma = shape
     P, ct_in, W = _case_inputs(ctx, shape, tile, 700 + N + Ma + engine)
@@ -260,15 +261,15 @@ def test_mac_engines_bit_exact(hl, ctx4096, ctx8192, engine, N, shape, tile):
         out = ctx.he_matmul(tile, wc, Ma, R, Nb, hl.to_device(ct_in))
         got = hl.to_host(out).reshape(-1, 2, ctx.L, ctx.N)
     finally:
-        ctx.set_mac_engine(1)
+        ctx.set_mac_engine(2)
     exp = ref.he_matmul(P, tile, W, ct_in, Nb).reshape(-1, 2, ctx.L, ctx.N)
     assert np.array_equal(got, exp)
 
 
-@pytest.mark.parametrize("engine", [0, 1])
+@pytest.mark.parametrize("engine", [0, 1, 2])
 def test_mac_extreme_residues(hl, ctx4096, engine):
     """All weights and ciphertext residues = p - 1 (the largest products and sums) over a long
-    J reduction (R = 3072 -> nJ = 384), both engines."""
+    J reduction (R = 3072 -> nJ = 384), every engine."""
     ctx = ctx4096
     P = _P(ctx)
     tile, (Nb, R, Ma) = (16, 8, 32), (32, 3072, 16)
@@ -283,6 +284,25 @@ def test_mac_extreme_residues(hl, ctx4096, engine):
         out = ctx.he_matmul(tile, wc, Ma, R, Nb, hl.to_device(ct_in))
         got = hl.to_host(out).reshape(-1, 2, ctx.L, ctx.N)
     finally:
-        ctx.set_mac_engine(1)
+        ctx.set_mac_engine(2)
+    exp = ref.he_matmul(P, tile, W, ct_in, Nb).reshape(-1, 2, ctx.L, ctx.N)
+    assert np.array_equal(got, exp)
+
+
+@pytest.mark.parametrize("engine", [1, 2])
+def test_mac_long_j_chunked(hl, ctx4096, engine):
+    """nJ = 4100 > 4096: the MAC splits J into launches of <= 4096 (the exact-accumulation bound
+    of every engine) and adds the partial results mod p; the 4-J ragged tail also exercises the
+    tensor-core engine's zero padding of J up to its 32-J MMA step."""
+    ctx = ctx4096
+    tile, (Nb, R, Ma) = (1, 2, 1), (1, 8200, 2)
+    P, ct_in, W = _case_inputs(ctx, (Nb, R, Ma), tile, 900 + engine)
+    ctx.set_mac_engine(engine)
+    try:
+        wc = ctx.encode_weights(tile, hl.to_device(W))
+        out = ctx.he_matmul(tile, wc, Ma, R, Nb, hl.to_device(ct_in))
+        got = hl.to_host(out).reshape(-1, 2, ctx.L, ctx.N)
+    finally:
+        ctx.set_mac_engine(2)
     exp = ref.he_matmul(P, tile, W, ct_in, Nb).reshape(-1, 2, ctx.L, ctx.N)
     assert np.array_equal(got, exp)
