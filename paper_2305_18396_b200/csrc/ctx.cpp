@@ -184,6 +184,8 @@ extern "C" int hl_ctx_create(uint32_t N, uint32_t L, uint32_t log2_t, const uint
     pc.mu = (uint64_t)((~(hl_u128)0 >> 64) / p);                 // floor((2^64 - 1) / p) = floor(2^64/p)
     pc.r64 = (uint64_t)(((hl_u128)1 << 64) % p);
     pc.r64_sh = h_shoup(pc.r64, p);
+    pc.c40 = h_powmod(2, 40, p); pc.c40_sh = h_shoup(pc.c40, p);
+    pc.c72 = h_powmod(2, 72, p); pc.c72_sh = h_shoup(pc.c72, p);
     pc.delta = c->delta_mod[l]; pc.delta_sh = h_shoup(pc.delta, p);
     pc.ninv = h_powmod(N, p - 2, p); pc.ninv_sh = h_shoup(pc.ninv, p);
     pc.ninv_w1 = h_mulmod(pc.ninv, c->h_tw_inv[(size_t)l * N + 1], p);

@@ -21,6 +21,7 @@ struct PrimeConsts {
   uint64_t mu;        // floor(2^64 / p)              (Barrett for 64-bit inputs)
   uint64_t r64;       // 2^64 mod p
   uint64_t r64_sh;    // floor(r64 * 2^64 / p)        (Shoup companion)
+  uint64_t c40, c40_sh, c72, c72_sh;   // 2^40, 2^72 mod p (tensor-core MAC recombination) + Shoup
   uint64_t delta;     // Delta mod p, Delta = floor(q / t)
   uint64_t delta_sh;  // Shoup companion of delta
   uint64_t ninv;      // N^-1 mod p

@@ -25,6 +25,7 @@
 
 #include <algorithm>
 #include <cstdio>
+#include <cstdlib>
 #include <initializer_list>
 #include <string>
 
@@ -255,7 +256,7 @@ struct MacGeom {
   int nIs, nIb, nJ, nC, CW, nCg, nSb, LN;
   int f64;       // MAC engine: 0 = IMAD.WIDE on 25-bit limbs, 1 = exact FP64 (DFMA) products
   int engine;    // 0 IMAD, 1 FP64, 2 int8 tensor cores (mac_tc.cuh)
-  int nIp, nIt, nJp, nJc;   // engine 2: rows padded to 16, I tiles of 128, J padded to 32, 32-J steps
+  int nIp, nIt, RT, nJp, nJc;   // engine 2: rows padded to 16, nIt balanced I tiles of RT rows, J padded to 32, 32-J steps
 };
 
 __host__ __device__ __forceinline__ size_t w_index(const MacGeom &g, int iloc, int J, int s) {
@@ -284,6 +285,8 @@ MacGeom mac_geom(const hl_ctx *c, int64_t nIs, int64_t nJ, int64_t nC) {
   g.f64 = c->mac_engine == 1;
   g.nIp = g.nIb * 16;
   g.nIt = (g.nIp + 127) / 128;
+  g.RT = ((g.nIp + g.nIt - 1) / g.nIt + 7) / 8 * 8;      // balanced tiles, multiple of 8 (UMMA core rows)
+  if ((int64_t)g.RT * (g.nIt - 1) >= nIs) g.RT = 128;   // never an empty last tile
   g.nJp = (int)((nJ + 31) / 32 * 32);
   g.nJc = g.nJp / 32;
   return g;
@@ -332,6 +335,50 @@ k_ntt_fwd(const uint64_t *__restrict__ in, void *__restrict__ out, DevParams P, 
       }
     } else {
       reinterpret_cast<uint64_t *>(out)[base + slot_of<LOGN>(t, u)] = d2u(xd);
+    }
+  }
+}
+
+// (a') ciphertext polynomials for the tensor-core MAC (engine 2): G consecutive polynomials
+//      (same J, columns col0 .. col0+G-1 of one CW group) per CTA, canonical residues staged in
+//      shared memory as [slot][G] so that every (slot, J) store is G consecutive u64 of the X
+//      layout [cg][LN][nJp][CW] (a 16-B half sector for G = 2, a full 32-B sector for G = 4).
+template <int LOGN, int G>
+__global__ void __launch_bounds__(Geom<LOGN>::NT * G)
+k_ntt_fwd_x(const uint64_t *__restrict__ in, uint64_t *__restrict__ out, DevParams P, MacGeom mg) {
+  using Gm = Geom<LOGN>;
+  extern __shared__ double sm[];
+  const int sub = threadIdx.x / Gm::NT, t = threadIdx.x % Gm::NT, l = blockIdx.y;
+  const int64_t poly0 = (int64_t)blockIdx.x * G;
+  const size_t base = ((size_t)(poly0 + sub) * P.L + l) * Gm::N;
+  const PrimeConsts pc = pick(P, l);
+  const double *tw = P.twd_fwd + (size_t)l * Gm::N;
+  double a[16];
+  constexpr int K = Gm::k(0), GG = 16 >> K;
+#pragma unroll
+  for (int g = 0; g < GG; g++)
+#pragma unroll
+    for (int u = 0; u < (1 << K); u++) a[g * (1 << K) + u] = u2d(__ldcs(in + base + elem_idx<LOGN, 0>(t, g, u)));
+  fwd_rounds_from<LOGN, 0>(a, sm + sub * Gm::SMEM_WORDS, t, tw, pc.pd, pc.pinv);
+  __syncthreads();                                     // every sub-NTT is done with its smem
+  uint64_t *xs = reinterpret_cast<uint64_t *>(sm);     // [N][G] canonical residues
+#pragma unroll
+  for (int u = 0; u < 16; u++) xs[slot_of<LOGN>(t, u) * G + sub] = d2u(canon_d(a[u], pc.pd, pc.pinv));
+  __syncthreads();
+  const int J = (int)(poly0 / mg.nC), col0 = (int)(poly0 % mg.nC);
+  const int cg = col0 / mg.CW, c0 = col0 % mg.CW;
+  uint64_t *dst0 = out + ((size_t)cg * mg.LN + (size_t)l * Gm::N) * mg.nJp * mg.CW + (size_t)J * mg.CW + c0;
+  for (int sl = threadIdx.x; sl < Gm::N; sl += Gm::NT * G) {
+    uint64_t *dst = dst0 + (size_t)sl * mg.nJp * mg.CW;
+    if constexpr (G == 4) {
+      const ulonglong2 v0 = *reinterpret_cast<const ulonglong2 *>(xs + sl * 4);
+      const ulonglong2 v1 = *reinterpret_cast<const ulonglong2 *>(xs + sl * 4 + 2);
+      reinterpret_cast<ulonglong2 *>(dst)[0] = v0;
+      reinterpret_cast<ulonglong2 *>(dst)[1] = v1;
+    } else if constexpr (G == 2) {
+      *reinterpret_cast<ulonglong2 *>(dst) = *reinterpret_cast<const ulonglong2 *>(xs + sl * 2);
+    } else {
+      *dst = xs[sl];
     }
   }
 }
@@ -398,9 +445,9 @@ k_encode_weights(EncodeArgs A, uint2 *__restrict__ wcache, DevParams P, uint32_t
     const int s = l * Gm::N + slot_of<LOGN>(t, u);
     if (A.mg.engine == 2) {
       // 7 byte planes, UMMA canonical K-major: [I tile][slot][32-J step][plane][K half][row][16 B]
-      const int tt = (int)(Iloc >> 7), row = (int)(Iloc & 127);
-      const int rows = min(128, A.mg.nIp - 128 * tt);
-      uint8_t *wb = reinterpret_cast<uint8_t *>(wcache) + (size_t)tt * 128 * A.mg.LN * A.mg.nJp * 7 +
+      const int tt = (int)(Iloc / A.mg.RT), row = (int)(Iloc % A.mg.RT);
+      const int rows = min(A.mg.RT, A.mg.nIp - A.mg.RT * tt);
+      uint8_t *wb = reinterpret_cast<uint8_t *>(wcache) + (size_t)tt * A.mg.RT * A.mg.LN * A.mg.nJp * 7 +
                     ((size_t)s * A.mg.nJc + (J >> 5)) * 224 * rows + ((J >> 4) & 1) * rows * 16 + row * 16 + (J & 15);
 #pragma unroll
       for (int a = 0; a < 7; a++) wb[a * 32 * rows] = (uint8_t)(x >> (8 * a));
@@ -961,8 +1008,36 @@ void launch_inv(const hl_ctx *c, const uint64_t *in, uint64_t *out, int64_t npol
   k_ntt_inv<LOGN><<<grid, Geom<LOGN>::NT, ntt_smem<LOGN>(), st>>>(in, out, c->dp);
 }
 
-// MODE 0 (u64, slot order) when mg == nullptr, else MODE 1 (blocked X limbs)
+template <int LOGN, int G>
+void launch_fwd_x(const hl_ctx *c, const uint64_t *in, void *out, int64_t npoly, const MacGeom &mg, cudaStream_t st) {
+  constexpr size_t smem = ntt_smem<LOGN>() * G;
+  static bool init = false;
+  if (!init) { set_smem(k_ntt_fwd_x<LOGN, G>, smem); init = true; }
+  dim3 grid((unsigned)(npoly / G), c->L);
+  KTimer kt(c, HL_K_NTT_FWD, st);
+  k_ntt_fwd_x<LOGN, G><<<grid, Geom<LOGN>::NT * G, smem, st>>>(in, (uint64_t *)out, c->dp, mg);
+}
+
+static int ntt_group() {
+  static int g = [] { const char *e = getenv("HELINEAR_NTT_G"); return e ? atoi(e) : 2; }();
+  return g;
+}
+
+// MODE 0 (u64, slot order) when mg == nullptr, else MODE 1 (the MAC engine's X layout)
 void fwd_ntt(const hl_ctx *c, const uint64_t *in, void *out, int64_t npoly, const MacGeom *mg, cudaStream_t st) {
+  if (mg && mg->engine == 2) {
+    // G consecutive polynomials share J and a column group (G divides CW)
+    const int G = (mg->CW % 4 == 0 && ntt_group() >= 4 && c->N == 4096) ? 4 : (ntt_group() >= 2 ? 2 : 1);
+    if (c->N == 4096) {
+      if (G == 4) launch_fwd_x<12, 4>(c, in, out, npoly, *mg, st);
+      else if (G == 2) launch_fwd_x<12, 2>(c, in, out, npoly, *mg, st);
+      else launch_fwd_x<12, 1>(c, in, out, npoly, *mg, st);
+    } else {
+      if (G >= 2) launch_fwd_x<13, 2>(c, in, out, npoly, *mg, st);
+      else launch_fwd_x<13, 1>(c, in, out, npoly, *mg, st);
+    }
+    return;
+  }
   MacGeom z{};
   if (c->N == 4096) { if (mg) launch_fwd<12, 1>(c, in, out, npoly, *mg, st); else launch_fwd<12, 0>(c, in, out, npoly, z, st); }
   else { if (mg) launch_fwd<13, 1>(c, in, out, npoly, *mg, st); else launch_fwd<13, 0>(c, in, out, npoly, z, st); }
@@ -1013,12 +1088,13 @@ void launch_mac_ln(const hl_ctx *c, const MacArgs &A, cudaStream_t st) {
 }
 
 template <int CW>
-void launch_mac_tc_t(const hl_ctx *c, const MacTcArgs &A, cudaStream_t st) {
+void launch_mac_tc_t(const hl_ctx *c, MacTcArgs A, cudaStream_t st) {
   using T = TcGeom<CW>;
   static bool init = false;
-  if (!init) { set_smem(k_mac_tc<CW>, T::SMEM); init = true; }
+  if (!init) { set_smem(k_mac_tc<CW>, T::SMEM_MAX); init = true; }
+  A.ring = tc_ring<CW>(A.g.RT);
   KTimer kt(c, HL_K_MAC, st);
-  k_mac_tc<CW><<<c->num_sms, 256, T::SMEM, st>>>(A, c->dp);
+  k_mac_tc<CW><<<c->num_sms, T::THREADS, A.ring.smem, st>>>(A, c->dp);
 }
 
 void launch_mac_tc(const hl_ctx *c, const void *W, const void *X, uint64_t *out, const MacGeom &g, cudaStream_t st) {

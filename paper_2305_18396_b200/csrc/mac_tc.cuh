@@ -14,42 +14,62 @@
 // accumulate S_d[I][c] in TMEM column d*CW + c; the epilogue forms sum_d S_d 2^(8d) (< 2^124)
 // and reduces it mod p_l once per output.
 //
-// Kernel roles (256 threads, one persistent CTA per SM):
+// Kernel roles (384 threads, one persistent CTA per SM):
 //   warp 0      TMA producer: per (slot, 32-J step) one cp.async.bulk of the 7 weight planes
 //               (224 B per I row, pre-laid-out by encode_weights in UMMA canonical K-major
 //               no-swizzle form) and one of the X residues (u64, written by the forward NTT)
 //   warp 1      TMEM allocator + single-thread MMA issuer (tcgen05.mma, tcgen05.commit)
 //   warps 2-3   converters: u64 residues -> byte rows of the Toeplitz image Z (generic stores,
 //               fence.proxy.async before release to the tensor core)
-//   warps 4-7   epilogue: tcgen05.ld of S_d, 128-bit recombination, mod p, staging of 4 slots,
-//               full 32-B sector stores of out[I][col][s..s+3]
-// Work item = (I tile of 128 rows, column group of CW, 4 consecutive slots); TMEM holds two
-// accumulators so the epilogue of slot s overlaps the MMAs of slot s+1.
+//   warps 4-11  epilogue (2 warps per TMEM lane quadrant, each half of the columns): tcgen05.ld
+//               of S_d, recombination sum_d S_d 2^(8d) mod p, staging of 4 slots, full 32-B
+//               sector stores of out[I][col][s..s+3]
+// Work item = (I tile of RT <= 128 rows, column group of CW, 4 consecutive slots); the nI rows are
+// split into balanced tiles (e.g. 144 = 2 x 72) and the ring depth is sized to the tile (more
+// stages for short tiles, so that enough bytes stay in flight).  TMEM holds two accumulators so the
+// epilogue of slot s overlaps the MMAs of slot s+1.
 #pragma once
 
 template <int CW>
 struct TcGeom {
   static constexpr int N = ((13 * CW + 15) / 16) * 16;   // MMA N: columns d*CW + c, d < 13
   static constexpr int ZR = N + 6 * CW;                  // rows of the Toeplitz B image
-  static constexpr int A_BYTES = 7 * 2 * 128 * 16;       // 7 planes x (2 K-halves x 128 rows x 16 B)
+  static constexpr int Z_BYTES = 2 * ZR * 16;            // stage layout: [Z][RAW][A (224 B per I row)]
   static constexpr int RAW_BYTES = 32 * CW * 8;          // X residues of one 32-J step
-  static constexpr int Z_BYTES = 2 * ZR * 16;
-  static constexpr int STAGE = A_BYTES + RAW_BYTES + Z_BYTES;
-  static constexpr int NST = CW >= 16 ? 3 : 4;           // ring depth
+  static constexpr int A_OFF = Z_BYTES + RAW_BYTES;
   static constexpr int SPI = 4;                          // slots per work item (32-B output sectors)
   static constexpr int STG_STRIDE = CW * SPI + 1;        // u64 per staged row (+1: bank spread)
-  static constexpr int STG_BYTES = 128 * STG_STRIDE * 8;
   static constexpr int TCOLS = 2 * N <= 64 ? 64 : (2 * N <= 128 ? 128 : (2 * N <= 256 ? 256 : 512));
-  static constexpr int BAR_BYTES = 256;
-  static constexpr int SMEM = NST * STAGE + STG_BYTES + BAR_BYTES;
-  static_assert(STAGE % 128 == 0, "stage alignment");
+  static constexpr int MAX_NST = 16;
+  static constexpr int BAR_BYTES = (3 * MAX_NST + 4) * 8 + 16;
+  static constexpr int THREADS = 384;                    // 4 role warps + 8 epilogue warps
+  static constexpr int SMEM_MAX = 232448;                // 227 KB opt-in per CTA
+  static_assert(A_OFF % 16 == 0, "stage alignment");
 };
+
+// ring geometry for a launch: rt rows per I tile (balanced tiles, multiple of 8)
+struct TcRing { int nst, sbytes, stg_off, bar_off, smem; };
+template <int CW>
+TcRing tc_ring(int rt) {
+  using T = TcGeom<CW>;
+  TcRing r;
+  // the M = 128 MMA reads 128 rows of every plane (rows >= rt are don't-care): plane 6 starts at
+  // 192 rt, row 127 of its second K half ends 2048 + 16 rt later -> 208 rt + 2048 >= 224 rt bytes
+  r.sbytes = (T::A_OFF + 208 * rt + 2048 + 127) / 128 * 128;
+  const int stg = (rt * T::STG_STRIDE * 8 + 127) / 128 * 128;
+  r.nst = std::min(T::MAX_NST, (T::SMEM_MAX - stg - T::BAR_BYTES) / r.sbytes);
+  r.stg_off = r.nst * r.sbytes;
+  r.bar_off = r.stg_off + stg;
+  r.smem = r.bar_off + T::BAR_BYTES;
+  return r;
+}
 
 struct MacTcArgs {
   const uint8_t *W;       // weight planes (encode_weights, engine 2 layout)
   const uint64_t *X;      // NTT-domain ct_in residues [nCg][LN][nJp][CW]
   uint64_t *out;          // [nIs][nC][LN] canonical residues
   MacGeom g;
+  TcRing ring;
   int N, jc0, njc, accumulate;
 };
 
@@ -78,7 +98,9 @@ __device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence:
 
 template <int CW>
 __device__ __forceinline__ void tmem_ld_cw(uint32_t addr, uint32_t (&v)[CW]) {
-  if constexpr (CW == 2) {
+  if constexpr (CW == 1) {
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x1.b32 {%0}, [%1];" : "=r"(v[0]) : "r"(addr));
+  } else if constexpr (CW == 2) {
     asm volatile("tcgen05.ld.sync.aligned.32x32b.x2.b32 {%0,%1}, [%2];" : "=r"(v[0]), "=r"(v[1]) : "r"(addr));
   } else if constexpr (CW == 4) {
     asm volatile("tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0,%1,%2,%3}, [%4];"
@@ -95,13 +117,13 @@ __device__ __forceinline__ void tmem_ld_cw(uint32_t addr, uint32_t (&v)[CW]) {
   }
 }
 
-// Work schedule shared by every role: round k covers, for one (I tile, column group) "kind",
-// the slot quads blockIdx.x + G*(k / kinds); kinds alternate per round so every CTA sees the same
-// mix of full and partial I tiles.
+// Work schedule shared by every role: in rounds k = kinds*r .. kinds*r + kinds-1 CTA b covers every
+// (I tile, column group) "kind" of slot quad r*G + b (the X residues of the quad are re-read from L2),
+// starting at kind b mod kinds so that concurrently running CTAs spread over the kinds.
 struct TcItem { int t, cg, sq; };
 __device__ __forceinline__ bool tc_item(const MacGeom &g, int k, TcItem &it) {
   const int kinds = g.nIt * g.nCg;
-  const int kind = k % kinds;
+  const int kind = (k + (int)blockIdx.x) % kinds;       // neighbouring CTAs work on different kinds
   it.sq = (k / kinds) * (int)gridDim.x + (int)blockIdx.x;
   it.t = kind / g.nCg;
   it.cg = kind % g.nCg;
@@ -112,13 +134,13 @@ __device__ __forceinline__ int tc_rounds(const MacGeom &g) {
 }
 
 template <int CW>
-__global__ void __launch_bounds__(256, 1)
+__global__ void __launch_bounds__(TcGeom<CW>::THREADS, 1)
 k_mac_tc(MacTcArgs A, DevParams P) {
   using T = TcGeom<CW>;
-  constexpr int NST = T::NST;
+  const int NST = A.ring.nst, SB = A.ring.sbytes;
   extern __shared__ __align__(128) unsigned char smem[];
-  uint64_t *stg = reinterpret_cast<uint64_t *>(smem + NST * T::STAGE);
-  uint64_t *full = reinterpret_cast<uint64_t *>(smem + NST * T::STAGE + T::STG_BYTES);
+  uint64_t *stg = reinterpret_cast<uint64_t *>(smem + A.ring.stg_off);
+  uint64_t *full = reinterpret_cast<uint64_t *>(smem + A.ring.bar_off);
   uint64_t *zfull = full + NST, *empty = zfull + NST, *tfull = empty + NST, *tempty = tfull + 2;
   uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(tempty + 2);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -127,13 +149,13 @@ k_mac_tc(MacTcArgs A, DevParams P) {
 
   // ---- setup: zero the Toeplitz images (only data rows are rewritten), barriers, TMEM
   for (int st = 0; st < NST; st++) {
-    uint4 *z = reinterpret_cast<uint4 *>(smem + st * T::STAGE + T::A_BYTES + T::RAW_BYTES);
+    uint4 *z = reinterpret_cast<uint4 *>(smem + st * SB);
     for (int i = threadIdx.x; i < T::Z_BYTES / 16; i += blockDim.x) z[i] = make_uint4(0, 0, 0, 0);
   }
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
   if (threadIdx.x == 0) {
     for (int i = 0; i < NST; i++) { mbar_init(&full[i], 1); mbar_init(&zfull[i], 64); mbar_init(&empty[i], 1); }
-    for (int i = 0; i < 2; i++) { mbar_init(&tfull[i], 1); mbar_init(&tempty[i], 4); }
+    for (int i = 0; i < 2; i++) { mbar_init(&tfull[i], 1); mbar_init(&tempty[i], 8); }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 1) {
@@ -154,18 +176,18 @@ k_mac_tc(MacTcArgs A, DevParams P) {
       for (int k = 0; k < nrounds; k++) {
         TcItem it;
         if (!tc_item(g, k, it)) continue;
-        const int rows = min(128, g.nIp - 128 * it.t);
+        const int rows = min(g.RT, g.nIp - g.RT * it.t);
         const uint32_t abytes = 224u * rows;
-        const uint8_t *wt = A.W + (size_t)it.t * 128 * g.LN * g.nJp * 7;
+        const uint8_t *wt = A.W + (size_t)it.t * g.RT * g.LN * g.nJp * 7;
         for (int si = 0; si < T::SPI; si++) {
           const int s = it.sq * T::SPI + si;
           for (int kk = 0; kk < A.njc; kk++) {
             const int jc = A.jc0 + kk;
             mbar_wait(&empty[st], ph);
-            unsigned char *dst = smem + st * T::STAGE;
+            unsigned char *dst = smem + st * SB;
             mbar_expect_tx(&full[st], abytes + T::RAW_BYTES);
-            bulk_g2s(dst, wt + ((size_t)s * g.nJc + jc) * abytes, abytes, &full[st]);
-            bulk_g2s(dst + T::A_BYTES, A.X + (((size_t)it.cg * g.LN + s) * g.nJp + (size_t)jc * 32) * CW,
+            bulk_g2s(dst + T::A_OFF, wt + ((size_t)s * g.nJc + jc) * abytes, abytes, &full[st]);
+            bulk_g2s(dst + T::Z_BYTES, A.X + (((size_t)it.cg * g.LN + s) * g.nJp + (size_t)jc * 32) * CW,
                      T::RAW_BYTES, &full[st]);
             if (++st == NST) { st = 0; ph ^= 1; }
           }
@@ -182,7 +204,7 @@ k_mac_tc(MacTcArgs A, DevParams P) {
       for (int k = 0; k < nrounds; k++) {
         TcItem it;
         if (!tc_item(g, k, it)) continue;
-        const int rows = min(128, g.nIp - 128 * it.t);
+        const int rows = min(g.RT, g.nIp - g.RT * it.t);
         for (int si = 0; si < T::SPI; si++, tile_no++) {
           const uint32_t buf = tile_no & 1, tph = (tile_no >> 1) & 1;
           mbar_wait(&tempty[buf], tph ^ 1);
@@ -192,8 +214,8 @@ k_mac_tc(MacTcArgs A, DevParams P) {
             mbar_wait(&full[st], ph);
             mbar_wait(&zfull[st], ph);
             tc_fence_after();
-            const uint32_t a0 = smem_u32(smem + st * T::STAGE);
-            const uint32_t z0 = a0 + T::A_BYTES + T::RAW_BYTES;
+            const uint32_t z0 = smem_u32(smem + st * SB);
+            const uint32_t a0 = z0 + T::A_OFF;
 #pragma unroll
             for (int a = 0; a < 7; a++) {
               const uint64_t ad = umma_sdesc(a0 + a * 32 * rows, rows * 16, 128);
@@ -218,8 +240,8 @@ k_mac_tc(MacTcArgs A, DevParams P) {
       for (int si = 0; si < T::SPI; si++) {
         for (int kk = 0; kk < A.njc; kk++) {
           mbar_wait(&full[st], ph);
-          const uint64_t *raw = reinterpret_cast<const uint64_t *>(smem + st * T::STAGE + T::A_BYTES);
-          unsigned char *z = smem + st * T::STAGE + T::A_BYTES + T::RAW_BYTES;
+          const uint64_t *raw = reinterpret_cast<const uint64_t *>(smem + st * SB + T::Z_BYTES);
+          unsigned char *z = smem + st * SB;
           for (int q = ct; q < CW * 8; q += 64) {
             const int c = q >> 3, h = (q >> 2) & 1, gq = q & 3;
             const int j0 = h * 16 + gq * 4;
@@ -248,7 +270,12 @@ k_mac_tc(MacTcArgs A, DevParams P) {
     }
   } else {
     // ------------------------------------------------------------------ epilogue
-    const int q = warp - 4;                          // TMEM lane quadrant of this warp
+    // warp w (4..11): TMEM lanes 32*(w&3).. (the hardware quadrant of w), columns c in half hh.
+    // Recombination: L = sum_{d<5} S_d 2^(8d) < 2^64, M = sum_{d=5..8} S_d 2^(8(d-5)) < 2^56,
+    // H = sum_{d=9..12} S_d 2^(8(d-9)) < 2^56 (S_d < 2^31), sum_J W X = L + M 2^40 + H 2^72,
+    // reduced as Barrett(L) + Shoup(M, 2^40 mod p) + Shoup(H, 2^72 mod p), each in [0, 2p).
+    constexpr int CH = CW / 2;
+    const int q = warp & 3, hh = (warp - 4) >> 2;
     const int row = 32 * q + lane;
     const int et = threadIdx.x - 128;
     uint32_t tile_no = 0;
@@ -257,46 +284,52 @@ k_mac_tc(MacTcArgs A, DevParams P) {
       if (!tc_item(g, k, it)) continue;
       const int l = (it.sq * T::SPI) / A.N;
       const PrimeConsts pc = pick(P, l);
+      const int rows_valid = min(g.RT, g.nIs - g.RT * it.t);
+      const bool active = 32 * q < rows_valid;           // warp-uniform: this quadrant holds outputs
       for (int si = 0; si < T::SPI; si++, tile_no++) {
         const uint32_t buf = tile_no & 1, tph = (tile_no >> 1) & 1;
         mbar_wait(&tfull[buf], tph);
         tc_fence_after();
-        hl_u128 acc[CW];
+        uint32_t v[13][CH];
+        if (active) {
+          const uint32_t base = tmem + ((uint32_t)(32 * q) << 16) + buf * T::N + hh * CH;
 #pragma unroll
-        for (int c = 0; c < CW; c++) acc[c] = 0;
-        const uint32_t base = tmem + ((uint32_t)(32 * q) << 16) + buf * T::N;
-#pragma unroll
-        for (int d = 0; d < 13; d++) {
-          uint32_t v[CW];
-          tmem_ld_cw<CW>(base + d * CW, v);
+          for (int d = 0; d < 13; d++) tmem_ld_cw<CH>(base + d * CW, v[d]);
           asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-#pragma unroll
-          for (int c = 0; c < CW; c++) acc[c] += (hl_u128)v[c] << (8 * d);
         }
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(&tempty[buf]);
+        if (active) {
 #pragma unroll
-        for (int c = 0; c < CW; c++) {
-          const uint64_t vh = (uint64_t)(acc[c] >> 64), vl = (uint64_t)acc[c];
-          const uint64_t r1 = shoup_mul(vh, pc.r64, pc.r64_sh, pc.p);   // vh 2^64 mod p, [0, 2p)
-          const uint64_t r2 = vl - __umul64hi(vl, pc.mu) * pc.p;        // vl mod p, [0, 2p)
-          uint64_t r = r1 + r2;
-          r = r >= pc.two_p ? r - pc.two_p : r;
-          r = r >= pc.p ? r - pc.p : r;
-          stg[row * T::STG_STRIDE + c * T::SPI + si] = r;
+          for (int c = 0; c < CH; c++) {
+            uint64_t L = v[0][c], M = v[5][c], H = v[9][c];
+#pragma unroll
+            for (int d = 1; d < 4; d++) {
+              L += (uint64_t)v[d][c] << (8 * d);
+              M += (uint64_t)v[5 + d][c] << (8 * d);
+              H += (uint64_t)v[9 + d][c] << (8 * d);
+            }
+            L += (uint64_t)v[4][c] << 32;
+            const uint64_t rl = L - __umul64hi(L, pc.mu) * pc.p;
+            const uint64_t rm = shoup_mul(M, pc.c40, pc.c40_sh, pc.p);
+            const uint64_t rh = shoup_mul(H, pc.c72, pc.c72_sh, pc.p);
+            uint64_t r = rl + rm + rh;                                   // < 6p < 2^53
+            r -= __umul64hi(r, pc.mu) * pc.p;                            // [0, 2p)
+            r = r >= pc.p ? r - pc.p : r;
+            if (row < rows_valid) stg[row * T::STG_STRIDE + (hh * CH + c) * T::SPI + si] = r;
+          }
         }
       }
       // 4 slots staged: full 32-B sector stores of out[I][col][s0 .. s0+3]
-      asm volatile("bar.sync 2, 128;" ::: "memory");
-      const int rows_valid = min(128, g.nIs - 128 * it.t);
+      asm volatile("bar.sync 2, 256;" ::: "memory");
       const size_t s0 = (size_t)it.sq * T::SPI;
-      for (int e = et; e < rows_valid * CW; e += 128) {
+      for (int e = et; e < rows_valid * CW; e += 256) {
         const int rr = e / CW, c = e % CW;
         const uint64_t *sv = stg + rr * T::STG_STRIDE + c * T::SPI;
         uint64_t v0 = sv[0], v1 = sv[1], v2 = sv[2], v3 = sv[3];
         ulonglong2 *dst = reinterpret_cast<ulonglong2 *>(
-            A.out + ((size_t)(128 * it.t + rr) * g.nC + it.cg * CW + c) * g.LN + s0);
+            A.out + ((size_t)(g.RT * it.t + rr) * g.nC + it.cg * CW + c) * g.LN + s0);
         if (A.accumulate) {
           const ulonglong2 o0 = dst[0], o1 = dst[1];
           v0 += o0.x; v1 += o0.y; v2 += o1.x; v3 += o1.y;
@@ -306,7 +339,7 @@ k_mac_tc(MacTcArgs A, DevParams P) {
         dst[0] = make_ulonglong2(v0, v1);
         dst[1] = make_ulonglong2(v2, v3);
       }
-      asm volatile("bar.sync 2, 128;" ::: "memory");
+      asm volatile("bar.sync 2, 256;" ::: "memory");
     }
   }
 

@@ -47,7 +47,7 @@ __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
                ::"r"(smem_u32(bar)), "r"(parity) : "memory");
 }
 
-template <int CW>
+template <int CW, int M = 128>
 __global__ void k_test(const uint8_t *A, const uint8_t *Z, int32_t *D, int reps, long long *clk) {
   using g = G<CW>;
   extern __shared__ __align__(1024) uint8_t sm[];
@@ -72,7 +72,7 @@ __global__ void k_test(const uint8_t *A, const uint8_t *Z, int32_t *D, int reps,
   const uint32_t tm = tbase;
   long long t0 = 0, t1 = 0;
   if (threadIdx.x == 0) {
-    const uint32_t id = idesc_i8(128, g::N);
+    const uint32_t id = idesc_i8(M, g::N);
     t0 = clock64();
     for (int r = 0; r < reps; r++) {
 #pragma unroll
@@ -105,7 +105,7 @@ __global__ void k_test(const uint8_t *A, const uint8_t *Z, int32_t *D, int reps,
   if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tm), "n"(g::TCOLS));
 }
 
-template <int CW>
+template <int CW, int M = 128>
 int run(int reps, int nblk) {
   using g = G<CW>;
   std::vector<uint8_t> A(g::A_BYTES), Z(g::Z_BYTES, 0);
@@ -124,13 +124,22 @@ int run(int reps, int nblk) {
   CK(cudaMemcpy(dA, A.data(), A.size(), cudaMemcpyHostToDevice));
   CK(cudaMemcpy(dZ, Z.data(), Z.size(), cudaMemcpyHostToDevice));
   const int smem = g::A_BYTES + g::Z_BYTES;
-  CK(cudaFuncSetAttribute(k_test<CW>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-  k_test<CW><<<1, 128, smem>>>(dA, dZ, dD, 1, dclk);
+  CK(cudaFuncSetAttribute(k_test<CW, M>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+  k_test<CW, M><<<1, 128, smem>>>(dA, dZ, dD, 1, dclk);
   CK(cudaGetLastError()); CK(cudaDeviceSynchronize());
   std::vector<int32_t> D(128 * g::N);
   CK(cudaMemcpy(D.data(), dD, D.size() * 4, cudaMemcpyDeviceToHost));
   int bad = 0;
-  for (int i = 0; i < 128; i++)
+  if (M == 64) {   // locate where row i landed: print lane of first match for a few rows
+    for (int i = 0; i < 64; i += 1) {
+      long long e0 = 0;
+      for (int k = 0; k < 32; k++) e0 += (long long)w[0][i][k] * x[0][0][k];   // d=0,c=0 column
+      int found = -1, nf = 0;
+      for (int ln = 0; ln < 128; ln++) if (D[ln * g::N + 0] == e0) { if (found < 0) found = ln; nf++; }
+      if (i < 20 || i % 16 == 15) printf("M=64 row %d -> lane %d (%d matches)\n", i, found, nf);
+    }
+  }
+  for (int i = 0; i < (M == 64 ? 0 : 128); i++)
     for (int d = 0; d < 13; d++)
       for (int c = 0; c < CW; c++) {
         long long e = 0;
@@ -142,18 +151,18 @@ int run(int reps, int nblk) {
         const long long got = D[i * g::N + d * CW + c];
         if (got != e && bad++ < 5) printf("CW=%d mismatch i=%d d=%d c=%d got %lld exp %lld\n", CW, i, d, c, got, e);
       }
-  printf("CW=%d N=%d correctness: %s (%d bad)\n", CW, g::N, bad ? "FAIL" : "ok", bad);
+  printf("M=%d CW=%d N=%d correctness: %s (%d bad)\n", M, CW, g::N, bad ? "FAIL" : "ok", bad);
   // throughput: every SM, reps x 7 MMAs
   cudaEvent_t e0, e1; cudaEventCreate(&e0); cudaEventCreate(&e1);
-  k_test<CW><<<nblk, 128, smem>>>(dA, dZ, dD, reps, dclk);
+  k_test<CW, M><<<nblk, 128, smem>>>(dA, dZ, dD, reps, dclk);
   cudaEventRecord(e0);
-  k_test<CW><<<nblk, 128, smem>>>(dA, dZ, dD, reps, dclk);
+  k_test<CW, M><<<nblk, 128, smem>>>(dA, dZ, dD, reps, dclk);
   cudaEventRecord(e1);
   CK(cudaDeviceSynchronize());
   float ms; cudaEventElapsedTime(&ms, e0, e1);
   std::vector<long long> clk(nblk);
   CK(cudaMemcpy(clk.data(), dclk, nblk * 8, cudaMemcpyDeviceToHost));
-  double macs = (double)nblk * reps * 7 * 128.0 * g::N * 32;
+  double macs = (double)nblk * reps * 7 * (double)M * g::N * 32;
   printf("CW=%d N=%d: %d CTAs x %d x 7 MMAs: %.3f ms, %.1f T MAC/s, %.0f MAC/clk/SM (clk64 %lld)\n", CW, g::N, nblk,
          reps, ms, macs / ms / 1e9, macs / nblk / (double)clk[0], clk[0]);
   cudaFree(dA); cudaFree(dZ); cudaFree(dD); cudaFree(dclk);
@@ -166,6 +175,8 @@ int main() {
   bad += run<4>(2000, 148);
   bad += run<8>(2000, 148);
   bad += run<16>(2000, 148);
+  bad += run<8, 64>(2000, 148);
+  bad += run<16, 64>(2000, 148);
   printf(bad ? "FAILED\n" : "ALL OK\n");
   return bad != 0;
 }
