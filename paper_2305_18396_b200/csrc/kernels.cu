@@ -1093,8 +1093,24 @@ void launch_mac_tc_t(const hl_ctx *c, MacTcArgs A, cudaStream_t st) {
   static bool init = false;
   if (!init) { set_smem(k_mac_tc<CW>, T::SMEM_MAX); init = true; }
   A.ring = tc_ring<CW>(A.g.RT);
+  static const bool prof = getenv("HELINEAR_MAC_PROF") != nullptr;
+  A.prof = nullptr;
+  if (prof) cudaMalloc(&A.prof, 8 * sizeof(unsigned long long)), cudaMemsetAsync(A.prof, 0, 64, st);
+  {
   KTimer kt(c, HL_K_MAC, st);
   k_mac_tc<CW><<<c->num_sms, T::THREADS, A.ring.smem, st>>>(A, c->dp);
+  }
+  if (prof) {   // diagnostics: average cycles per CTA waiting, by role
+    unsigned long long h[8];
+    cudaMemcpyAsync(h, A.prof, 64, cudaMemcpyDeviceToHost, st);
+    cudaStreamSynchronize(st);
+    const double n = c->num_sms;
+    fprintf(stderr, "[mac_tc CW=%d nIs=%d nJ=%d RT=%d nst=%d sb=%d] total %.0f | prod.empty %.0f | mma.tempty %.0f "
+            "mma.full %.0f mma.zfull %.0f mma.issue %.0f | conv.full %.0f | epi.tfull %.0f (cycles/CTA)\n", CW, A.g.nIs,
+            A.g.nJ, A.g.RT, A.ring.nst, A.ring.sbytes, h[7] / n, h[0] / n, h[1] / n, h[2] / n, h[3] / n, h[6] / n,
+            h[4] / n, h[5] / n);
+    cudaFree(A.prof);
+  }
 }
 
 void launch_mac_tc(const hl_ctx *c, const void *W, const void *X, uint64_t *out, const MacGeom &g, cudaStream_t st) {

@@ -71,6 +71,7 @@ struct MacTcArgs {
   MacGeom g;
   TcRing ring;
   int N, jc0, njc, accumulate;
+  unsigned long long *prof;   // diagnostics (HELINEAR_MAC_PROF): per-CTA cycles spent waiting, by role
 };
 
 // UMMA shared-memory descriptor: K-major, no swizzle; core matrix = 8 rows x 16 B contiguous.
@@ -92,6 +93,21 @@ __device__ __forceinline__ void umma_i8(uint32_t d_tmem, uint64_t a, uint64_t b,
 __device__ __forceinline__ void umma_commit(uint64_t *bar) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];"
                ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ bool elect_one() {
+  uint32_t pred;
+  asm volatile("{\n\t.reg .pred P;\n\telect.sync _|P, 0xffffffff;\n\tselp.b32 %0, 1, 0, P;\n\t}" : "=r"(pred));
+  return pred != 0;
+}
+// mbarrier wait that, when profiling, adds the cycles spent waiting to *acc
+__device__ __forceinline__ void mbar_wait_p(uint64_t *bar, uint32_t parity, unsigned long long *acc) {
+  if (acc) {
+    const long long t0 = clock64();
+    mbar_wait(bar, parity);
+    *acc += (unsigned long long)(clock64() - t0);
+  } else {
+    mbar_wait(bar, parity);
+  }
 }
 __device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
@@ -167,6 +183,8 @@ k_mac_tc(MacTcArgs A, DevParams P) {
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  unsigned long long pw[8] = {0, 0, 0, 0, 0, 0, 0, 0};   // profiling accumulators (registers)
+  const long long t_start = clock64();
 
   if (warp == 0) {
     // ------------------------------------------------------------------ TMA producer
@@ -183,7 +201,7 @@ k_mac_tc(MacTcArgs A, DevParams P) {
           const int s = it.sq * T::SPI + si;
           for (int kk = 0; kk < A.njc; kk++) {
             const int jc = A.jc0 + kk;
-            mbar_wait(&empty[st], ph);
+            mbar_wait_p(&empty[st], ph, A.prof ? &pw[0] : nullptr);
             unsigned char *dst = smem + st * SB;
             mbar_expect_tx(&full[st], abytes + T::RAW_BYTES);
             bulk_g2s(dst + T::A_OFF, wt + ((size_t)s * g.nJc + jc) * abytes, abytes, &full[st]);
@@ -196,37 +214,45 @@ k_mac_tc(MacTcArgs A, DevParams P) {
     }
   } else if (warp == 1) {
     // ------------------------------------------------------------------ MMA issuer
-    if (lane == 0) {
-      const uint32_t idesc = umma_idesc_u8(128, T::N);
-      int st = 0;
-      uint32_t ph = 0;
-      uint32_t tile_no = 0;
-      for (int k = 0; k < nrounds; k++) {
-        TcItem it;
-        if (!tc_item(g, k, it)) continue;
-        const int rows = min(g.RT, g.nIp - g.RT * it.t);
-        for (int si = 0; si < T::SPI; si++, tile_no++) {
-          const uint32_t buf = tile_no & 1, tph = (tile_no >> 1) & 1;
-          mbar_wait(&tempty[buf], tph ^ 1);
+    // The whole warp runs the loop (every value is warp-uniform, so descriptors live in uniform
+    // registers) and one elected lane issues: a per-MMA register->uniform conversion in a
+    // single-lane branch costs more than the MMA itself (profiles/r01/microbench_umma_i8_cost.log).
+    const uint32_t idesc = umma_idesc_u8(128, T::N);
+    int st = 0;
+    uint32_t ph = 0;
+    uint32_t tile_no = 0;
+    for (int k = 0; k < nrounds; k++) {
+      TcItem it;
+      if (!tc_item(g, k, it)) continue;
+      const int rows = min(g.RT, g.nIp - g.RT * it.t);
+      const uint32_t plane = 32u * rows, lbo_a = 16u * rows;
+      for (int si = 0; si < T::SPI; si++, tile_no++) {
+        const uint32_t buf = tile_no & 1, tph = (tile_no >> 1) & 1;
+        mbar_wait_p(&tempty[buf], tph ^ 1, (A.prof && lane == 0) ? &pw[1] : nullptr);
+        tc_fence_after();
+        const uint32_t dcol = tmem + buf * T::N;
+        for (int kk = 0; kk < A.njc; kk++) {
+          mbar_wait_p(&full[st], ph, (A.prof && lane == 0) ? &pw[2] : nullptr);
+          mbar_wait_p(&zfull[st], ph, (A.prof && lane == 0) ? &pw[3] : nullptr);
           tc_fence_after();
-          const uint32_t dcol = tmem + buf * T::N;
-          for (int kk = 0; kk < A.njc; kk++) {
-            mbar_wait(&full[st], ph);
-            mbar_wait(&zfull[st], ph);
-            tc_fence_after();
-            const uint32_t z0 = smem_u32(smem + st * SB);
-            const uint32_t a0 = z0 + T::A_OFF;
+          const long long ti0 = A.prof ? clock64() : 0;
+          const uint32_t z0 = smem_u32(smem + st * SB);
+          const uint32_t a0 = z0 + T::A_OFF;
+          if (elect_one()) {
 #pragma unroll
             for (int a = 0; a < 7; a++) {
-              const uint64_t ad = umma_sdesc(a0 + a * 32 * rows, rows * 16, 128);
+              const uint64_t ad = umma_sdesc(a0 + a * plane, lbo_a, 128);
               const uint64_t bd = umma_sdesc(z0 + (6 - a) * CW * 16, T::ZR * 16, 128);
               umma_i8(dcol, ad, bd, idesc, (kk | a) ? 1u : 0u);
             }
             umma_commit(&empty[st]);
-            if (++st == NST) { st = 0; ph ^= 1; }
           }
-          umma_commit(&tfull[buf]);
+          __syncwarp();
+          if (A.prof && lane == 0) pw[6] += (unsigned long long)(clock64() - ti0);
+          if (++st == NST) { st = 0; ph ^= 1; }
         }
+        if (elect_one()) umma_commit(&tfull[buf]);
+        __syncwarp();
       }
     }
   } else if (warp < 4) {
@@ -239,7 +265,7 @@ k_mac_tc(MacTcArgs A, DevParams P) {
       if (!tc_item(g, k, it)) continue;
       for (int si = 0; si < T::SPI; si++) {
         for (int kk = 0; kk < A.njc; kk++) {
-          mbar_wait(&full[st], ph);
+          mbar_wait_p(&full[st], ph, (A.prof && ct == 0) ? &pw[4] : nullptr);
           const uint64_t *raw = reinterpret_cast<const uint64_t *>(smem + st * SB + T::Z_BYTES);
           unsigned char *z = smem + st * SB;
           for (int q = ct; q < CW * 8; q += 64) {
@@ -288,7 +314,7 @@ k_mac_tc(MacTcArgs A, DevParams P) {
       const bool active = 32 * q < rows_valid;           // warp-uniform: this quadrant holds outputs
       for (int si = 0; si < T::SPI; si++, tile_no++) {
         const uint32_t buf = tile_no & 1, tph = (tile_no >> 1) & 1;
-        mbar_wait(&tfull[buf], tph);
+        mbar_wait_p(&tfull[buf], tph, (A.prof && et == 0) ? &pw[5] : nullptr);
         tc_fence_after();
         uint32_t v[13][CH];
         if (active) {
@@ -344,6 +370,13 @@ k_mac_tc(MacTcArgs A, DevParams P) {
   }
 
   // ---- teardown
+  if (A.prof) {
+    const unsigned long long tot = (unsigned long long)(clock64() - t_start);
+    if (threadIdx.x == 0) { atomicAdd(&A.prof[0], pw[0]); atomicAdd(&A.prof[7], tot); }
+    if (threadIdx.x == 32) { atomicAdd(&A.prof[1], pw[1]); atomicAdd(&A.prof[2], pw[2]); atomicAdd(&A.prof[3], pw[3]); atomicAdd(&A.prof[6], pw[6]); }
+    if (threadIdx.x == 64) atomicAdd(&A.prof[4], pw[4]);
+    if (threadIdx.x == 128) atomicAdd(&A.prof[5], pw[5]);
+  }
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
