@@ -164,12 +164,22 @@ def run_ours(args, rank, world, local_rank):
         m["masked"] = torch.empty(m["lay"].ct_masked_words, dtype=torch.int64, device=dev)
         m["share"] = torch.zeros(m["lay"].share_words, dtype=torch.int64, device=dev)
 
+    # every product gets its own scratch: the batch call pipelines them over two streams
+    for m in mats:
+        m["ws"] = torch.empty(m["lay"].workspace_bytes // 8, dtype=torch.int64, device=dev)
+        m["co"] = torch.empty(m["lay"].ct_out_words, dtype=torch.int64, device=dev)
+    entries = [dict(wcache=m["wc"], Ma=m["mm"].Ma, R=m["mm"].R, Nb=m["mm"].Nb, ct_in=m["ct"], seed=m["seed"],
+                    workspace=m["ws"], ct_out_ntt=m["co"], ct_masked=m["masked"], share=m["share"]) for m in mats]
+
     def step():
-        for m in mats:
-            mm = m["mm"]
-            ctx.he_matmul_share(tile, m["wc"], mm.Ma, mm.R, mm.Nb, m["ct"], m["seed"], True,
-                                workspace=workspace, ct_out_ntt=ct_out_ntt, ct_masked=m["masked"],
-                                share=m["share"], stream=stream)
+        if args.sequential:
+            for m in mats:
+                mm = m["mm"]
+                ctx.he_matmul_share(tile, m["wc"], mm.Ma, mm.R, mm.Nb, m["ct"], m["seed"], True,
+                                    workspace=workspace, ct_out_ntt=ct_out_ntt, ct_masked=m["masked"],
+                                    share=m["share"], stream=stream)
+        else:
+            ctx.he_linear_batch(tile, entries, stream=stream)
 
     def barrier():
         if world > 1:
@@ -389,6 +399,7 @@ def main():
     ap.add_argument("--tile", type=int, nargs=3, default=None)
     ap.add_argument("--cpu-itiles", type=int, default=2)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--sequential", action="store_true", help="one he_matmul_share per product (no 2-stream pipeline)")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "ours":
         args.warmup = 3

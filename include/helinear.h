@@ -81,8 +81,9 @@ typedef struct {
   int64_t ct_masked_words;    /* compressed: nI_shard*nK*L*(m*n + N)                          */
   int64_t ct_full_words;      /* uncompressed masked: nI_shard*nK*2*L*N                       */
   int64_t share_words;        /* Nb*Ma                                                        */
-  int64_t wcache_bytes;       /* ceil(nI_shard/16)*16*nJ*L*N*8 (rows padded to 16)            */
-  int64_t workspace_bytes;    /* nJ*nK*2*L*N*12                                               */
+  int64_t wcache_bytes;       /* engine 2 (default): ceil(nI_shard/16)*16 * ceil(nJ/32)*32 * L*N*7
+                                 engines 0/1: ceil(nI_shard/16)*16 * nJ * L*N*8               */
+  int64_t workspace_bytes;    /* engine 2: ceil(nJ/32)*32 * nK*2*L*N*8 + 256; engines 0/1: nJ*nK*2*L*N*12 */
 } hl_layout;
 
 /* ---- context ---------------------------------------------------------------------------- */
@@ -169,6 +170,26 @@ int hl_he_matmul_share(const hl_ctx *ctx, hl_tile tile, const void *wcache, int6
                        int64_t Nb, int64_t i_begin, int64_t i_end, const uint64_t *ct_in,
                        void *workspace, uint64_t *ct_out_ntt, uint64_t seed, int compress,
                        uint64_t *ct_masked, uint64_t *share_server, void *stream);
+
+/* One entry of hl_he_linear_batch: a whole product (shard [0, nI)), compressed responses. */
+typedef struct {
+  const void *wcache;         /* hl_encode_weights output for this (Ma, R), device                */
+  int64_t Ma, R, Nb;
+  const uint64_t *ct_in;      /* device [nJ][nK][2][L][N]                                          */
+  void *workspace;            /* device, layout.workspace_bytes -- distinct for every entry        */
+  uint64_t *ct_out_ntt;       /* device, layout.ct_out_words    -- distinct for every entry        */
+  uint64_t seed;              /* mask seed (as hl_mask_and_share)                                  */
+  uint64_t *ct_masked;        /* device, layout.ct_masked_words (compressed response)              */
+  uint64_t *share;            /* device [Nb][Ma] server share                                      */
+} hl_linear_desc;
+
+/* n compressed hl_he_matmul_share calls, e.g. the four products of an encoder block; results are
+ * bit-identical to the calls made one after the other on `stream`.  The calls are pipelined: the
+ * MAC of entry i (HBM-bound) runs on `stream` while the forward NTT of entry i+1 and the inverse
+ * NTT + mask of entry i-1 (FP64-pipe-bound) run on the context's auxiliary stream; `stream`
+ * waits for all of it before later work.  Uses the context's auxiliary stream: do not run two
+ * batches on one context concurrently. */
+int hl_he_linear_batch(const hl_ctx *ctx, hl_tile tile, int n, const hl_linear_desc *descs, void *stream);
 
 /* End-to-end server call on HOST buffers (the e2e path of bench.py): copies ct_in_host
  * (pinned host, [nJ][nK][2][L][N]) to dev_ct_in, runs hl_he_matmul_share, and copies the

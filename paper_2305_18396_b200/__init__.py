@@ -30,7 +30,7 @@ _CODES = {HL_EINVAL: "HL_EINVAL", HL_EDIM: "HL_EDIM", HL_ERANGE: "HL_ERANGE", HL
 EXPORTS = ("hl_last_error", "hl_ctx_create", "hl_ctx_destroy", "hl_ctx_params", "hl_ctx_set_mac_engine",
            "hl_layout_query",
            "hl_keygen", "hl_encrypt", "hl_decrypt_share", "hl_encode_weights", "hl_he_matmul",
-           "hl_mask_and_share", "hl_he_matmul_share", "hl_he_linear_host", "hl_poly_mul",
+           "hl_mask_and_share", "hl_he_matmul_share", "hl_he_linear_batch", "hl_he_linear_host", "hl_poly_mul",
            "hl_ntt_roundtrip", "hl_timing_enable", "hl_timing_read")
 KERNELS = ("ntt_fwd", "mac", "intt_mask", "intt", "mask", "encode", "other")   # HL_K_* order
 
@@ -52,6 +52,13 @@ class _Layout(ctypes.Structure):
     _fields_ = [(f, ctypes.c_int64) for f in (
         "nI", "nJ", "nK", "nI_shard", "ct_in_words", "ct_out_words", "ct_masked_words",
         "ct_full_words", "share_words", "wcache_bytes", "workspace_bytes")]
+
+
+class LinearDesc(ctypes.Structure):
+    """hl_linear_desc: one product of hl_he_linear_batch (device pointers)."""
+    _fields_ = [("wcache", ctypes.c_void_p), ("Ma", ctypes.c_int64), ("R", ctypes.c_int64), ("Nb", ctypes.c_int64),
+                ("ct_in", ctypes.c_void_p), ("workspace", ctypes.c_void_p), ("ct_out_ntt", ctypes.c_void_p),
+                ("seed", ctypes.c_uint64), ("ct_masked", ctypes.c_void_p), ("share", ctypes.c_void_p)]
 
 
 @dataclass(frozen=True)
@@ -96,6 +103,7 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
         "hl_he_matmul": [vp, Tile, vp, i64, i64, i64, i64, i64, vp, vp, vp, vp],
         "hl_mask_and_share": [vp, Tile, i64, i64, i64, i64, vp, u64, i32, vp, vp, vp],
         "hl_he_matmul_share": [vp, Tile, vp, i64, i64, i64, i64, i64, vp, vp, vp, u64, i32, vp, vp, vp],
+        "hl_he_linear_batch": [vp, Tile, i32, ctypes.POINTER(LinearDesc), vp],
         "hl_he_linear_host": [vp, Tile, vp, i64, i64, i64, vp, u64, i32, vp, vp, vp, vp, vp, vp, vp, vp],
         "hl_poly_mul": [vp, vp, vp, vp, i64, vp, vp],
         "hl_ntt_roundtrip": [vp, vp, i64, vp, vp],
@@ -268,6 +276,31 @@ class Context:
                                        _dptr(ct_in), _dptr(workspace), _dptr(ct_out_ntt), seed,
                                        int(bool(compress)), _dptr(ct_masked), _dptr(share), _stream(stream)))
         return ct_masked, share
+
+    def he_linear_batch(self, tile, entries, stream=None):
+        """Pipelined compressed he_matmul_share over several products (hl_he_linear_batch).
+        entries: dicts with wcache, Ma, R, Nb, ct_in, seed and optionally workspace, ct_out_ntt,
+        ct_masked, share (allocated here if absent; every entry gets its own buffers).
+        Returns [(ct_masked, share), ...]."""
+        import torch
+        descs = (LinearDesc * len(entries))()
+        keep, outs = [], []
+        for d, e in zip(descs, entries):
+            Ma, R, Nb = int(e["Ma"]), int(e["R"]), int(e["Nb"])
+            lay = self.layout(tile, Ma, R, Nb)
+            dev = e["ct_in"].device
+            ws = e.get("workspace") if e.get("workspace") is not None else _dev_empty(lay.workspace_bytes // 8, dev)
+            co = e.get("ct_out_ntt") if e.get("ct_out_ntt") is not None else _dev_empty(lay.ct_out_words, dev)
+            cm = e.get("ct_masked") if e.get("ct_masked") is not None else _dev_empty(lay.ct_masked_words, dev)
+            sh = e.get("share") if e.get("share") is not None else torch.zeros(Nb * Ma, dtype=torch.int64, device=dev)
+            d.wcache, d.Ma, d.R, d.Nb = _dptr(e["wcache"]), Ma, R, Nb
+            d.ct_in, d.workspace, d.ct_out_ntt = _dptr(e["ct_in"]), _dptr(ws), _dptr(co)
+            d.seed, d.ct_masked, d.share = int(e["seed"]), _dptr(cm), _dptr(sh)
+            keep += [ws, co]
+            outs.append((cm, sh))
+        _check(_lib.hl_he_linear_batch(self._h, _tile(tile), len(entries), descs, _stream(stream)))
+        self._batch_keep = keep        # scratch stays alive until the next batch call
+        return outs
 
     def he_linear_host(self, tile, wcache, Ma: int, R: int, Nb: int, ct_in_host, seed: int, ct_masked_host,
                        share_host, dev_ct_in, workspace, dev_ct_out_ntt, dev_ct_masked, dev_share,

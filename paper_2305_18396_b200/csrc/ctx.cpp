@@ -213,6 +213,20 @@ extern "C" int hl_ctx_create(uint32_t N, uint32_t L, uint32_t log2_t, const uint
     return rc ? rc : hl_fail(HL_ECUDA, "hl_ctx_create: device allocation failed");
   }
   cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, device);
+  {
+    // the batch pipeline's streams: MACs at the highest priority so that their persistent CTAs
+    // are placed before queued NTT blocks of the concurrent low-priority stream
+    int lo = 0, hi = 0;
+    cudaDeviceGetStreamPriorityRange(&lo, &hi);
+    cudaStream_t aux, mac;
+    if (cudaStreamCreateWithPriority(&aux, cudaStreamNonBlocking, lo) != cudaSuccess ||
+        cudaStreamCreateWithPriority(&mac, cudaStreamNonBlocking, hi) != cudaSuccess) {
+      cudaFree(c->d_tw); cudaFree(c->d_flags); delete c;
+      return hl_cuda_check("hl_ctx_create: pipeline streams");
+    }
+    c->aux_stream = (void *)aux;
+    c->mac_stream = (void *)mac;
+  }
   dp.twd_fwd = (const double *)c->d_tw;
   dp.twd_inv = (const double *)c->d_tw + (size_t)L * N;
   *out = c;
@@ -271,6 +285,8 @@ extern "C" int hl_ctx_destroy(hl_ctx *c) {
     for (auto &r : c->timing->rec) { cudaEventDestroy((cudaEvent_t)r.second.first); cudaEventDestroy((cudaEvent_t)r.second.second); }
     delete c->timing;
   }
+  if (c->aux_stream) cudaStreamDestroy((cudaStream_t)c->aux_stream);
+  if (c->mac_stream) cudaStreamDestroy((cudaStream_t)c->mac_stream);
   if (c->d_tw) cudaFree(c->d_tw);
   if (c->d_flags) cudaFree(c->d_flags);
   delete c;
@@ -328,7 +344,7 @@ extern "C" int hl_layout_query(const hl_ctx *c, hl_tile tile, int64_t Ma, int64_
   if (c->mac_engine == 2) {            // int8 tensor cores: 7 byte planes per residue, J padded to 32
     const int64_t nJp = (g.nJ + 31) / 32 * 32;
     out->wcache_bytes = nIp * nJp * LN * 7;
-    out->workspace_bytes = nJp * g.nK * 2 * LN * 8;                // canonical residues [cg][LN][nJp][CW]
+    out->workspace_bytes = nJp * g.nK * 2 * LN * 8 + 256;          // residues [cg][LN][nJp][CW] + MAC scheduler
   } else {
     out->wcache_bytes = nIp * g.nJ * LN * 8;
     out->workspace_bytes = g.nJ * g.nK * 2 * LN * 12;              // limb pairs + limb sums (MAC operand X)

@@ -67,6 +67,8 @@ struct hl_ctx {
   DevParams dp;
   void *d_tw = nullptr;               // device allocation holding tw_fwd + tw_inv
   uint32_t *d_flags = nullptr;        // device scratch: [0] range flag, [1] max |w| (as u32 bits)
+  void *aux_stream = nullptr;         // cudaStream_t (non-blocking, lowest priority): hl_he_linear_batch's NTT stages
+  void *mac_stream = nullptr;         // cudaStream_t (non-blocking, highest priority): hl_he_linear_batch's MACs
   TimingState *timing = nullptr;      // owned; mutable through const hl_ctx*
 };
 

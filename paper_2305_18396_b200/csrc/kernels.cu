@@ -28,6 +28,7 @@
 #include <cstdlib>
 #include <initializer_list>
 #include <string>
+#include <vector>
 
 #include "chacha.h"
 #include "hl_internal.h"
@@ -1088,11 +1089,11 @@ void launch_mac_ln(const hl_ctx *c, const MacArgs &A, cudaStream_t st) {
 }
 
 template <int CW>
-void launch_mac_tc_t(const hl_ctx *c, MacTcArgs A, cudaStream_t st) {
+void launch_mac_tc_t(const hl_ctx *c, MacTcArgs A, int smem_budget, cudaStream_t st) {
   using T = TcGeom<CW>;
   static bool init = false;
   if (!init) { set_smem(k_mac_tc<CW>, T::SMEM_MAX); init = true; }
-  A.ring = tc_ring<CW>(A.g.RT);
+  A.ring = tc_ring<CW>(A.g.RT, smem_budget);
   static const bool prof = getenv("HELINEAR_MAC_PROF") != nullptr;
   A.prof = nullptr;
   if (prof) cudaMalloc(&A.prof, 8 * sizeof(unsigned long long)), cudaMemsetAsync(A.prof, 0, 64, st);
@@ -1113,24 +1114,36 @@ void launch_mac_tc_t(const hl_ctx *c, MacTcArgs A, cudaStream_t st) {
   }
 }
 
-void launch_mac_tc(const hl_ctx *c, const void *W, const void *X, uint64_t *out, const MacGeom &g, cudaStream_t st) {
+// the tensor-core engine's workspace = X residues [nCg][LN][nJp][CW] u64 + 256 B of scheduler state
+inline size_t tc_sched_offset(const MacGeom &g) { return (size_t)g.nJp * g.nC * g.LN * 8; }
+
+void launch_mac_tc(const hl_ctx *c, const void *W, const void *X, uint64_t *out, const MacGeom &g, int smem_budget,
+                   cudaStream_t st) {
   MacTcArgs A;
   A.W = (const uint8_t *)W; A.X = (const uint64_t *)X; A.out = out; A.g = g; A.N = (int)c->N;
+  A.sched = (int *)((char *)X + tc_sched_offset(g));
+  static const int ko = [] { const char *e = getenv("HELINEAR_MAC_KO"); return e ? atoi(e) : 0; }();
+  A.ko = ko;
   for (int64_t j0 = 0; j0 < g.nJp; j0 += kMacJChunk) {     // S_d < 7 * 4096 * 255^2 < 2^31 per launch
     A.jc0 = (int)(j0 / 32);
     A.njc = (int)((std::min<int64_t>(g.nJp, j0 + kMacJChunk) - j0) / 32);
     A.accumulate = j0 > 0;
+    cudaMemsetAsync(A.sched, 0, sizeof(int), st);
     switch (g.CW) {
-      case 16: launch_mac_tc_t<16>(c, A, st); break;
-      case 8: launch_mac_tc_t<8>(c, A, st); break;
-      case 4: launch_mac_tc_t<4>(c, A, st); break;
-      default: launch_mac_tc_t<2>(c, A, st); break;
+      case 16: launch_mac_tc_t<16>(c, A, smem_budget, st); break;
+      case 8: launch_mac_tc_t<8>(c, A, smem_budget, st); break;
+      case 4: launch_mac_tc_t<4>(c, A, smem_budget, st); break;
+      default: launch_mac_tc_t<2>(c, A, smem_budget, st); break;
     }
   }
 }
 
-void launch_mac(const hl_ctx *c, const uint2 *W, const uint32_t *X, uint64_t *out, const MacGeom &g, cudaStream_t st) {
-  if (g.engine == 2) { launch_mac_tc(c, W, X, out, g, st); return; }
+constexpr int kMacSmemAlone = 232448;        // the MAC alone on the SM: the deepest ring that fits
+constexpr int kMacSmemShared = 150 * 1024;   // leaves ~77 KB for NTT CTAs running concurrently
+
+void launch_mac(const hl_ctx *c, const uint2 *W, const uint32_t *X, uint64_t *out, const MacGeom &g, cudaStream_t st,
+                int smem_budget = kMacSmemAlone) {
+  if (g.engine == 2) { launch_mac_tc(c, W, X, out, g, smem_budget, st); return; }
   MacArgs A;
   A.W = W; A.X = X; A.out = out; A.g = g; A.N = (int)c->N;
   for (int64_t j0 = 0; j0 < g.nJ; j0 += kMacJChunk) {
@@ -1269,6 +1282,60 @@ extern "C" int hl_he_matmul_share(const hl_ctx *c, hl_tile tile, const void *wca
   if (c->N == 4096) launch_inv_mask<12>(c, ct_out_ntt, ct_masked, share, M, g.nIs * g.nK, st);
   else launch_inv_mask<13>(c, ct_out_ntt, ct_masked, share, M, g.nIs * g.nK, st);
   return hl_cuda_check("hl_he_matmul_share: launch");
+}
+
+// ---------------------------------------------------------------------------------------
+// Pipelined batch of compressed he_matmul_share calls (e.g. the four products of an encoder
+// block).  The MAC is HBM-bound (weight cache) while the NTT kernels are bound by the FP64 pipe
+// and latency, so they share SMs well: MAC(i) runs on the context's high-priority stream while
+// the forward NTT of entry i+1 and the inverse NTT + mask of entry i-1 run on its low-priority
+// stream; `stream` is joined to both at the start and at the end.
+// ---------------------------------------------------------------------------------------
+extern "C" int hl_he_linear_batch(const hl_ctx *c, hl_tile tile, int n, const hl_linear_desc *d, void *stream) {
+  int rc;
+  if ((rc = check_ptrs({c, d}, "hl_he_linear_batch"))) return rc;
+  if (n <= 0) return hl_fail(HL_EINVAL, "hl_he_linear_batch: n must be positive");
+  struct Entry { Geo g; MacGeom mg; MaskArgs M; };
+  std::vector<Entry> E(n);
+  for (int i = 0; i < n; i++) {
+    if ((rc = check_ptrs({c, d[i].wcache, d[i].ct_in, d[i].workspace, d[i].ct_out_ntt, d[i].ct_masked, d[i].share},
+                         "hl_he_linear_batch")))
+      return rc;
+    if ((rc = hl_geometry(c, tile, d[i].Ma, d[i].R, d[i].Nb, 0, -1, &E[i].g))) return rc;
+    E[i].mg = mac_geom(c, E[i].g.nIs, E[i].g.nJ, 2 * E[i].g.nK);
+    E[i].M = mask_args(E[i].g, d[i].Ma, d[i].Nb, d[i].seed);
+  }
+  cudaStream_t sc = (cudaStream_t)stream, s0 = (cudaStream_t)c->mac_stream, s1 = (cudaStream_t)c->aux_stream;
+  std::vector<cudaEvent_t> ev(2 * n + 3);
+  for (auto &e : ev)
+    if (cudaEventCreateWithFlags(&e, cudaEventDisableTiming) != cudaSuccess) return hl_cuda_check("hl_he_linear_batch: events");
+  cudaEvent_t *e_fwd = ev.data(), *e_mac = ev.data() + n, e_in = ev[2 * n], e_done = ev[2 * n + 1];
+  cudaEvent_t e_macs = ev[2 * n + 2];
+  auto fwd = [&](int i) { fwd_ntt(c, d[i].ct_in, d[i].workspace, E[i].g.nJ * 2 * E[i].g.nK, &E[i].mg, s1); };
+  auto inv = [&](int i) {
+    if (c->N == 4096) launch_inv_mask<12>(c, d[i].ct_out_ntt, d[i].ct_masked, d[i].share, E[i].M, E[i].g.nIs * E[i].g.nK, s1);
+    else launch_inv_mask<13>(c, d[i].ct_out_ntt, d[i].ct_masked, d[i].share, E[i].M, E[i].g.nIs * E[i].g.nK, s1);
+  };
+  cudaEventRecord(e_in, sc);                      // inputs written on `stream` are visible to both streams
+  cudaStreamWaitEvent(s0, e_in, 0);
+  cudaStreamWaitEvent(s1, e_in, 0);
+  fwd(0);
+  cudaEventRecord(e_fwd[0], s1);
+  for (int i = 0; i < n; i++) {
+    cudaStreamWaitEvent(s0, e_fwd[i], 0);
+    launch_mac(c, (const uint2 *)d[i].wcache, (const uint32_t *)d[i].workspace, d[i].ct_out_ntt, E[i].mg, s0,
+               kMacSmemShared);
+    cudaEventRecord(e_mac[i], s0);
+    if (i + 1 < n) { fwd(i + 1); cudaEventRecord(e_fwd[i + 1], s1); }     // overlaps MAC(i)
+    cudaStreamWaitEvent(s1, e_mac[i], 0);
+    inv(i);                                                               // overlaps MAC(i+1)
+  }
+  cudaEventRecord(e_done, s1);
+  cudaEventRecord(e_macs, s0);
+  cudaStreamWaitEvent(sc, e_done, 0);
+  cudaStreamWaitEvent(sc, e_macs, 0);
+  for (auto &e : ev) cudaEventDestroy(e);         // released once the recorded work completes
+  return hl_cuda_check("hl_he_linear_batch: launch");
 }
 
 extern "C" int hl_he_linear_host(const hl_ctx *c, hl_tile tile, const void *wcache, int64_t Ma, int64_t R,

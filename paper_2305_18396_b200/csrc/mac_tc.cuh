@@ -34,31 +34,35 @@ template <int CW>
 struct TcGeom {
   static constexpr int N = ((13 * CW + 15) / 16) * 16;   // MMA N: columns d*CW + c, d < 13
   static constexpr int ZR = N + 6 * CW;                  // rows of the Toeplitz B image
-  static constexpr int Z_BYTES = 2 * ZR * 16;            // stage layout: [Z][RAW][A (224 B per I row)]
+  static constexpr int Z_BYTES = 2 * ZR * 16;            // one Toeplitz image (Z ring entry)
+  static constexpr int NZ = 4;                           // Z ring depth (decoupled from the TMA ring)
   static constexpr int RAW_BYTES = 32 * CW * 8;          // X residues of one 32-J step
-  static constexpr int A_OFF = Z_BYTES + RAW_BYTES;
+  static constexpr int A_OFF = RAW_BYTES;                // TMA stage layout: [RAW][A (224 B per I row)]
   static constexpr int SPI = 4;                          // slots per work item (32-B output sectors)
   static constexpr int STG_STRIDE = CW * SPI + 1;        // u64 per staged row (+1: bank spread)
-  static constexpr int TCOLS = 2 * N <= 64 ? 64 : (2 * N <= 128 ? 128 : (2 * N <= 256 ? 256 : 512));
-  static constexpr int MAX_NST = 16;
-  static constexpr int BAR_BYTES = (3 * MAX_NST + 4) * 8 + 16;
+  static constexpr int NBUF = 4 * N <= 512 ? 4 : 2;      // TMEM accumulators in flight (MMA runs ahead of the epilogue)
+  static constexpr int TCOLS = NBUF * N <= 64 ? 64 : (NBUF * N <= 128 ? 128 : (NBUF * N <= 256 ? 256 : 512));
+  static constexpr int MAX_NST = 24;
+  static constexpr int BAR_BYTES = (2 * MAX_NST + 2 * NZ + 2 * NBUF + 2 * 4) * 8 + 4 * 4 + 16;
   static constexpr int THREADS = 384;                    // 4 role warps + 8 epilogue warps
   static constexpr int SMEM_MAX = 232448;                // 227 KB opt-in per CTA
-  static_assert(A_OFF % 16 == 0, "stage alignment");
+  static_assert(A_OFF % 16 == 0 && Z_BYTES % 128 == 0, "alignment");
 };
 
 // ring geometry for a launch: rt rows per I tile (balanced tiles, multiple of 8)
-struct TcRing { int nst, sbytes, stg_off, bar_off, smem; };
+struct TcRing { int nst, sbytes, z_off, stg_off, bar_off, smem; };
 template <int CW>
-TcRing tc_ring(int rt) {
+TcRing tc_ring(int rt, int smem_budget) {
   using T = TcGeom<CW>;
   TcRing r;
   // the M = 128 MMA reads 128 rows of every plane (rows >= rt are don't-care): plane 6 starts at
   // 192 rt, row 127 of its second K half ends 2048 + 16 rt later -> 208 rt + 2048 >= 224 rt bytes
   r.sbytes = (T::A_OFF + 208 * rt + 2048 + 127) / 128 * 128;
   const int stg = (rt * T::STG_STRIDE * 8 + 127) / 128 * 128;
-  r.nst = std::min(T::MAX_NST, (T::SMEM_MAX - stg - T::BAR_BYTES) / r.sbytes);
-  r.stg_off = r.nst * r.sbytes;
+  const int fixed = T::NZ * T::Z_BYTES + stg + T::BAR_BYTES;
+  r.nst = std::max(2, std::min(T::MAX_NST, (std::min(smem_budget, T::SMEM_MAX) - fixed) / r.sbytes));
+  r.z_off = r.nst * r.sbytes;
+  r.stg_off = r.z_off + T::NZ * T::Z_BYTES;
   r.bar_off = r.stg_off + stg;
   r.smem = r.bar_off + T::BAR_BYTES;
   return r;
@@ -72,6 +76,8 @@ struct MacTcArgs {
   TcRing ring;
   int N, jc0, njc, accumulate;
   unsigned long long *prof;   // diagnostics (HELINEAR_MAC_PROF): per-CTA cycles spent waiting, by role
+  int *sched;                 // work counter (zeroed before the launch; in the caller's workspace)
+  int ko;                     // diagnostics (HELINEAR_MAC_KO bitmask): 1 skip MMAs, 2 skip conversion, 4 skip epilogue math
 };
 
 // UMMA shared-memory descriptor: K-major, no swizzle; core matrix = 8 rows x 16 B contiguous.
@@ -93,6 +99,10 @@ __device__ __forceinline__ void umma_i8(uint32_t d_tmem, uint64_t a, uint64_t b,
 __device__ __forceinline__ void umma_commit(uint64_t *bar) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];"
                ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void bulk_g2s_hint(void *dst, const void *src, uint32_t bytes, uint64_t *bar, uint64_t pol) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;"
+               ::"r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(pol) : "memory");
 }
 __device__ __forceinline__ bool elect_one() {
   uint32_t pred;
@@ -133,45 +143,61 @@ __device__ __forceinline__ void tmem_ld_cw(uint32_t addr, uint32_t (&v)[CW]) {
   }
 }
 
-// Work schedule shared by every role: in rounds k = kinds*r .. kinds*r + kinds-1 CTA b covers every
-// (I tile, column group) "kind" of slot quad r*G + b (the X residues of the quad are re-read from L2),
-// starting at kind b mod kinds so that concurrently running CTAs spread over the kinds.
+// Dynamic work schedule: the producer takes the next item from a global counter (in the caller's
+// workspace, zeroed before the launch) and hands it to the other roles through a 4-deep ring in
+// shared memory, so CTAs that start late (e.g. behind NTT blocks of a concurrent kernel) simply
+// take fewer items.  Consecutive items share a slot quad (kind fastest): the X residues of the
+// quad are re-read from L2 by the CTAs working on its other (I tile, column group) kinds.
 struct TcItem { int t, cg, sq; };
-__device__ __forceinline__ bool tc_item(const MacGeom &g, int k, TcItem &it) {
-  const int kinds = g.nIt * g.nCg;
-  const int kind = (k + (int)blockIdx.x) % kinds;       // neighbouring CTAs work on different kinds
-  it.sq = (k / kinds) * (int)gridDim.x + (int)blockIdx.x;
+__device__ __forceinline__ TcItem tc_decode(const MacGeom &g, int item) {
+  const int kinds = g.nIt * g.nCg, kind = item % kinds;
+  TcItem it;
+  it.sq = item / kinds;
   it.t = kind / g.nCg;
   it.cg = kind % g.nCg;
-  return it.sq < g.LN / 4;
+  return it;
 }
-__device__ __forceinline__ int tc_rounds(const MacGeom &g) {
-  return g.nIt * g.nCg * ((g.LN / 4 + (int)gridDim.x - 1) / (int)gridDim.x);
+constexpr int kItemRing = 4;
+constexpr int kItemConsumers = 11;    // MMA warp + 2 converter warps + 8 epilogue warps (lane 0 each)
+// consumer side: wait for item number `seq`, read it, release the ring slot; returns -1 at the end
+__device__ __forceinline__ int tc_next_item(uint64_t *ifull, uint64_t *iempty, const volatile int *itm, uint32_t seq) {
+  const int slot = seq % kItemRing;
+  mbar_wait(&ifull[slot], (seq / kItemRing) & 1);
+  const int item = itm[slot];
+  __syncwarp();
+  if ((threadIdx.x & 31) == 0) mbar_arrive(&iempty[slot]);
+  return item;
 }
 
 template <int CW>
-__global__ void __launch_bounds__(TcGeom<CW>::THREADS, 1)
+// <= 80 registers for CW <= 8 (minBlocks 2): leaves room for NTT CTAs on the same SM when the
+// MAC of one matmul runs concurrently with the NTTs of its neighbours (hl_he_linear_batch)
+__global__ void __launch_bounds__(TcGeom<CW>::THREADS, (CW <= 8 ? 2 : 1))
 k_mac_tc(MacTcArgs A, DevParams P) {
   using T = TcGeom<CW>;
   const int NST = A.ring.nst, SB = A.ring.sbytes;
   extern __shared__ __align__(128) unsigned char smem[];
   uint64_t *stg = reinterpret_cast<uint64_t *>(smem + A.ring.stg_off);
+  unsigned char *zring = smem + A.ring.z_off;
   uint64_t *full = reinterpret_cast<uint64_t *>(smem + A.ring.bar_off);
-  uint64_t *zfull = full + NST, *empty = zfull + NST, *tfull = empty + NST, *tempty = tfull + 2;
-  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(tempty + 2);
+  uint64_t *empty = full + NST, *zfull = empty + NST, *zempty = zfull + T::NZ;
+  uint64_t *tfull = zempty + T::NZ, *tempty = tfull + T::NBUF;
+  uint64_t *ifull = tempty + T::NBUF, *iempty = ifull + kItemRing;
+  int *itm = reinterpret_cast<int *>(iempty + kItemRing);
+  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(itm + kItemRing);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const MacGeom &g = A.g;
-  const int nrounds = tc_rounds(g);
+  const int total_items = g.nIt * g.nCg * (g.LN / 4);
 
   // ---- setup: zero the Toeplitz images (only data rows are rewritten), barriers, TMEM
-  for (int st = 0; st < NST; st++) {
-    uint4 *z = reinterpret_cast<uint4 *>(smem + st * SB);
-    for (int i = threadIdx.x; i < T::Z_BYTES / 16; i += blockDim.x) z[i] = make_uint4(0, 0, 0, 0);
-  }
+  for (int i = threadIdx.x; i < T::NZ * T::Z_BYTES / 16; i += blockDim.x)
+    reinterpret_cast<uint4 *>(zring)[i] = make_uint4(0, 0, 0, 0);
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
   if (threadIdx.x == 0) {
-    for (int i = 0; i < NST; i++) { mbar_init(&full[i], 1); mbar_init(&zfull[i], 64); mbar_init(&empty[i], 1); }
-    for (int i = 0; i < 2; i++) { mbar_init(&tfull[i], 1); mbar_init(&tempty[i], 8); }
+    for (int i = 0; i < NST; i++) { mbar_init(&full[i], 1); mbar_init(&empty[i], 1); }
+    for (int i = 0; i < T::NZ; i++) { mbar_init(&zfull[i], 64); mbar_init(&zempty[i], 1); }
+    for (int i = 0; i < T::NBUF; i++) { mbar_init(&tfull[i], 1); mbar_init(&tempty[i], 8); }
+    for (int i = 0; i < kItemRing; i++) { mbar_init(&ifull[i], 1); mbar_init(&iempty[i], kItemConsumers); }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 1) {
@@ -191,9 +217,16 @@ k_mac_tc(MacTcArgs A, DevParams P) {
     if (lane == 0) {
       int st = 0;
       uint32_t ph = 1;
-      for (int k = 0; k < nrounds; k++) {
-        TcItem it;
-        if (!tc_item(g, k, it)) continue;
+      uint64_t pol_w;                     // the weight cache is streamed once: evict it from L2 first
+      asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol_w));
+      for (uint32_t seq = 0;; seq++) {
+        const int slot = seq % kItemRing;
+        mbar_wait(&iempty[slot], ((seq / kItemRing) & 1) ^ 1);
+        const int item = atomicAdd(A.sched, 1);
+        itm[slot] = item < total_items ? item : -1;
+        mbar_arrive(&ifull[slot]);
+        if (item >= total_items) break;
+        const TcItem it = tc_decode(g, item);
         const int rows = min(g.RT, g.nIp - g.RT * it.t);
         const uint32_t abytes = 224u * rows;
         const uint8_t *wt = A.W + (size_t)it.t * g.RT * g.LN * g.nJp * 7;
@@ -204,8 +237,8 @@ k_mac_tc(MacTcArgs A, DevParams P) {
             mbar_wait_p(&empty[st], ph, A.prof ? &pw[0] : nullptr);
             unsigned char *dst = smem + st * SB;
             mbar_expect_tx(&full[st], abytes + T::RAW_BYTES);
-            bulk_g2s(dst + T::A_OFF, wt + ((size_t)s * g.nJc + jc) * abytes, abytes, &full[st]);
-            bulk_g2s(dst + T::Z_BYTES, A.X + (((size_t)it.cg * g.LN + s) * g.nJp + (size_t)jc * 32) * CW,
+            bulk_g2s_hint(dst + T::A_OFF, wt + ((size_t)s * g.nJc + jc) * abytes, abytes, &full[st], pol_w);
+            bulk_g2s(dst, A.X + (((size_t)it.cg * g.LN + s) * g.nJp + (size_t)jc * 32) * CW,
                      T::RAW_BYTES, &full[st]);
             if (++st == NST) { st = 0; ph ^= 1; }
           }
@@ -217,35 +250,41 @@ k_mac_tc(MacTcArgs A, DevParams P) {
     // The whole warp runs the loop (every value is warp-uniform, so descriptors live in uniform
     // registers) and one elected lane issues: a per-MMA register->uniform conversion in a
     // single-lane branch costs more than the MMA itself (profiles/r01/microbench_umma_i8_cost.log).
-    const uint32_t idesc = umma_idesc_u8(128, T::N);
+    // tiles of <= 64 rows use M = 64 (half the A-operand shared-memory reads per MMA); the
+    // accumulator rows then sit in lanes 32(r/16) + r%16 (profiles/r01/microbench_umma_i8.log)
+    const uint32_t idesc = umma_idesc_u8(g.RT <= 64 ? 64 : 128, T::N);
     int st = 0;
     uint32_t ph = 0;
-    uint32_t tile_no = 0;
-    for (int k = 0; k < nrounds; k++) {
-      TcItem it;
-      if (!tc_item(g, k, it)) continue;
+    uint32_t tile_no = 0, zseq = 0;
+    for (uint32_t seq = 0;; seq++) {
+      const int item = tc_next_item(ifull, iempty, itm, seq);
+      if (item < 0) break;
+      const TcItem it = tc_decode(g, item);
       const int rows = min(g.RT, g.nIp - g.RT * it.t);
       const uint32_t plane = 32u * rows, lbo_a = 16u * rows;
       for (int si = 0; si < T::SPI; si++, tile_no++) {
-        const uint32_t buf = tile_no & 1, tph = (tile_no >> 1) & 1;
+        const uint32_t buf = tile_no % T::NBUF, tph = (tile_no / T::NBUF) & 1;
         mbar_wait_p(&tempty[buf], tph ^ 1, (A.prof && lane == 0) ? &pw[1] : nullptr);
         tc_fence_after();
         const uint32_t dcol = tmem + buf * T::N;
-        for (int kk = 0; kk < A.njc; kk++) {
+        for (int kk = 0; kk < A.njc; kk++, zseq++) {
+          const uint32_t zi = zseq % T::NZ, zph = (zseq / T::NZ) & 1;
           mbar_wait_p(&full[st], ph, (A.prof && lane == 0) ? &pw[2] : nullptr);
-          mbar_wait_p(&zfull[st], ph, (A.prof && lane == 0) ? &pw[3] : nullptr);
+          mbar_wait_p(&zfull[zi], zph, (A.prof && lane == 0) ? &pw[3] : nullptr);
           tc_fence_after();
           const long long ti0 = A.prof ? clock64() : 0;
-          const uint32_t z0 = smem_u32(smem + st * SB);
-          const uint32_t a0 = z0 + T::A_OFF;
+          const uint32_t a0 = smem_u32(smem + st * SB) + T::A_OFF;
+          const uint32_t z0 = smem_u32(zring + zi * T::Z_BYTES);
           if (elect_one()) {
 #pragma unroll
             for (int a = 0; a < 7; a++) {
+              if (A.ko & 1) break;
               const uint64_t ad = umma_sdesc(a0 + a * plane, lbo_a, 128);
               const uint64_t bd = umma_sdesc(z0 + (6 - a) * CW * 16, T::ZR * 16, 128);
               umma_i8(dcol, ad, bd, idesc, (kk | a) ? 1u : 0u);
             }
             umma_commit(&empty[st]);
+            umma_commit(&zempty[zi]);
           }
           __syncwarp();
           if (A.prof && lane == 0) pw[6] += (unsigned long long)(clock64() - ti0);
@@ -259,16 +298,18 @@ k_mac_tc(MacTcArgs A, DevParams P) {
     // ------------------------------------------------------------------ converters
     const int ct = threadIdx.x - 64;
     int st = 0;
-    uint32_t ph = 0;
-    for (int k = 0; k < nrounds; k++) {
-      TcItem it;
-      if (!tc_item(g, k, it)) continue;
+    uint32_t ph = 0, zseq = 0;
+    for (uint32_t seq = 0;; seq++) {
+      const int item = tc_next_item(ifull, iempty, itm, seq);
+      if (item < 0) break;
       for (int si = 0; si < T::SPI; si++) {
-        for (int kk = 0; kk < A.njc; kk++) {
+        for (int kk = 0; kk < A.njc; kk++, zseq++) {
+          const uint32_t zi = zseq % T::NZ, zph = (zseq / T::NZ) & 1;
           mbar_wait_p(&full[st], ph, (A.prof && ct == 0) ? &pw[4] : nullptr);
-          const uint64_t *raw = reinterpret_cast<const uint64_t *>(smem + st * SB + T::Z_BYTES);
-          unsigned char *z = smem + st * SB;
-          for (int q = ct; q < CW * 8; q += 64) {
+          mbar_wait(&zempty[zi], zph ^ 1);
+          const uint64_t *raw = reinterpret_cast<const uint64_t *>(smem + st * SB);
+          unsigned char *z = zring + zi * T::Z_BYTES;
+          for (int q = ct; q < ((A.ko & 2) ? 0 : CW * 8); q += 64) {
             const int c = q >> 3, h = (q >> 2) & 1, gq = q & 3;
             const int j0 = h * 16 + gq * 4;
             uint32_t lo[4], hi[4];
@@ -289,7 +330,7 @@ k_mac_tc(MacTcArgs A, DevParams P) {
             }
           }
           asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-          mbar_arrive(&zfull[st]);
+          mbar_arrive(&zfull[zi]);
           if (++st == NST) { st = 0; ph ^= 1; }
         }
       }
@@ -302,44 +343,65 @@ k_mac_tc(MacTcArgs A, DevParams P) {
     // reduced as Barrett(L) + Shoup(M, 2^40 mod p) + Shoup(H, 2^72 mod p), each in [0, 2p).
     constexpr int CH = CW / 2;
     const int q = warp & 3, hh = (warp - 4) >> 2;
-    const int row = 32 * q + lane;
+    const bool m64 = g.RT <= 64;
+    const int row = m64 ? (lane < 16 ? 16 * q + lane : 1 << 20) : 32 * q + lane;   // tile row held by this lane
     const int et = threadIdx.x - 128;
     uint32_t tile_no = 0;
-    for (int k = 0; k < nrounds; k++) {
-      TcItem it;
-      if (!tc_item(g, k, it)) continue;
+    for (uint32_t seq = 0;; seq++) {
+      const int item = tc_next_item(ifull, iempty, itm, seq);
+      if (item < 0) break;
+      const TcItem it = tc_decode(g, item);
       const int l = (it.sq * T::SPI) / A.N;
       const PrimeConsts pc = pick(P, l);
       const int rows_valid = min(g.RT, g.nIs - g.RT * it.t);
-      const bool active = 32 * q < rows_valid;           // warp-uniform: this quadrant holds outputs
+      const bool active = (m64 ? 16 : 32) * q < rows_valid;   // warp-uniform: this quadrant holds outputs
       for (int si = 0; si < T::SPI; si++, tile_no++) {
-        const uint32_t buf = tile_no & 1, tph = (tile_no >> 1) & 1;
+        const uint32_t buf = tile_no % T::NBUF, tph = (tile_no / T::NBUF) & 1;
         mbar_wait_p(&tfull[buf], tph, (A.prof && et == 0) ? &pw[5] : nullptr);
         tc_fence_after();
-        uint32_t v[13][CH];
-        if (active) {
+        // three column groups (d < 5 -> L, 5..8 -> M, 9..12 -> H) loaded and folded one at a time
+        uint64_t L[CH], M[CH], H[CH];
+        if (active && !(A.ko & 4)) {
           const uint32_t base = tmem + ((uint32_t)(32 * q) << 16) + buf * T::N + hh * CH;
+          uint32_t v[5][CH];
 #pragma unroll
-          for (int d = 0; d < 13; d++) tmem_ld_cw<CH>(base + d * CW, v[d]);
+          for (int d = 0; d < 5; d++) tmem_ld_cw<CH>(base + d * CW, v[d]);
           asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+          for (int c = 0; c < CH; c++) {
+            L[c] = v[0][c];
+#pragma unroll
+            for (int d = 1; d < 4; d++) L[c] += (uint64_t)v[d][c] << (8 * d);
+            L[c] += (uint64_t)v[4][c] << 32;
+          }
+#pragma unroll
+          for (int d = 0; d < 4; d++) tmem_ld_cw<CH>(base + (5 + d) * CW, v[d]);
+          asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+          for (int c = 0; c < CH; c++) {
+            M[c] = v[0][c];
+#pragma unroll
+            for (int d = 1; d < 4; d++) M[c] += (uint64_t)v[d][c] << (8 * d);
+          }
+#pragma unroll
+          for (int d = 0; d < 4; d++) tmem_ld_cw<CH>(base + (9 + d) * CW, v[d]);
+          asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+          for (int c = 0; c < CH; c++) {
+            H[c] = v[0][c];
+#pragma unroll
+            for (int d = 1; d < 4; d++) H[c] += (uint64_t)v[d][c] << (8 * d);
+          }
         }
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(&tempty[buf]);
-        if (active) {
+        if (active && !(A.ko & 4)) {
 #pragma unroll
           for (int c = 0; c < CH; c++) {
-            uint64_t L = v[0][c], M = v[5][c], H = v[9][c];
-#pragma unroll
-            for (int d = 1; d < 4; d++) {
-              L += (uint64_t)v[d][c] << (8 * d);
-              M += (uint64_t)v[5 + d][c] << (8 * d);
-              H += (uint64_t)v[9 + d][c] << (8 * d);
-            }
-            L += (uint64_t)v[4][c] << 32;
-            const uint64_t rl = L - __umul64hi(L, pc.mu) * pc.p;
-            const uint64_t rm = shoup_mul(M, pc.c40, pc.c40_sh, pc.p);
-            const uint64_t rh = shoup_mul(H, pc.c72, pc.c72_sh, pc.p);
+            const uint64_t rl = L[c] - __umul64hi(L[c], pc.mu) * pc.p;
+            const uint64_t rm = shoup_mul(M[c], pc.c40, pc.c40_sh, pc.p);
+            const uint64_t rh = shoup_mul(H[c], pc.c72, pc.c72_sh, pc.p);
             uint64_t r = rl + rm + rh;                                   // < 6p < 2^53
             r -= __umul64hi(r, pc.mu) * pc.p;                            // [0, 2p)
             r = r >= pc.p ? r - pc.p : r;

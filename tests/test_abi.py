@@ -73,11 +73,11 @@ def test_layout_and_dims(hl):
     assert lay.ct_masked_words == 144 * 4 * 2 * (16 * 32 + 4096)
     # default engine 2 (int8 tensor cores): 7 byte limbs per NTT-domain weight residue
     assert lay.wcache_bytes == 144 * 96 * 2 * 4096 * 7
-    assert lay.workspace_bytes == 96 * 4 * 2 * 2 * 4096 * 8
+    assert lay.workspace_bytes == 96 * 4 * 2 * 2 * 4096 * 8 + 256
     sh = ctx.layout((16, 8, 32), 2304, 768, 128, 10, 20)
     assert sh.nI_shard == 10 and sh.wcache_bytes == 16 * 96 * 2 * 4096 * 7   # rows padded to 16
     odd = ctx.layout((16, 8, 32), 64, 40, 64)                    # nJ = 5 padded to the 32-J MMA step
-    assert odd.wcache_bytes == 16 * 32 * 2 * 4096 * 7 and odd.workspace_bytes == 32 * 2 * 2 * 2 * 4096 * 8
+    assert odd.wcache_bytes == 16 * 32 * 2 * 4096 * 7 and odd.workspace_bytes == 32 * 2 * 2 * 2 * 4096 * 8 + 256
     ctx.set_mac_engine(1)                                        # FP64 engine: one double per residue
     assert ctx.layout((16, 8, 32), 2304, 768, 128).wcache_bytes == 144 * 96 * 2 * 4096 * 8
     with pytest.raises(hl.HLError) as e:

@@ -196,6 +196,55 @@ def test_bert_tiny_block_c1(hl, ctx4096):
         assert np.array_equal(hl.to_host(s).reshape(es.shape), es), mm.name
 
 
+def _block_inputs(ctx, cfg, block=0):
+    P = _P(ctx)
+    out = []
+    for mi, mm in enumerate(cfg.matmuls):
+        W = synth.weights(synth.seed_for(block, mi, "w"), mm.R, mm.Ma)
+        nI, nJ, nK = ref.tile_counts(cfg.tile, mm.Ma, mm.R, mm.Nb)
+        ct_in = synth.uniform_below(synth.seed_for(block, mi, "enc"), (nJ, nK, 2, P.L, P.N), P.primes)
+        out.append((mm, W, ct_in, synth.seed_for(block, mi, "mask")))
+    return out
+
+
+def test_linear_batch_c1_vs_oracle(hl, ctx4096):
+    """hl_he_linear_batch (the bench's call: the four products pipelined over two streams) on
+    config c1, bit-exact against the oracle server for every product."""
+    ctx = ctx4096
+    cfg = synth.CONFIGS["c1"]
+    P = _P(ctx)
+    ins = _block_inputs(ctx, cfg)
+    entries = [dict(wcache=ctx.encode_weights(cfg.tile, hl.to_device(W)), Ma=mm.Ma, R=mm.R, Nb=mm.Nb,
+                    ct_in=hl.to_device(ct_in), seed=seed) for mm, W, ct_in, seed in ins]
+    outs = ctx.he_linear_batch(cfg.tile, entries)
+    _sync()
+    for (mm, W, ct_in, seed), (m, sh) in zip(ins, outs):
+        em, es = ref.mask_and_share(P, cfg.tile, ref.he_matmul(P, cfg.tile, W, ct_in, mm.Nb), mm.Ma, mm.Nb, seed)
+        assert np.array_equal(hl.to_host(m).reshape(em.shape), em), mm.name
+        assert np.array_equal(hl.to_host(sh).reshape(es.shape), es), mm.name
+
+
+def test_linear_batch_c2_equals_single_calls(hl, ctx4096):
+    """Config c2 at full size in the bench's launch configuration (batch of the four products):
+    bit-identical to four he_matmul_share calls (each of which is checked against the oracle by
+    test_bert_base_full_size_sampled), repeated twice to catch cross-stream races."""
+    ctx = ctx4096
+    cfg = synth.CONFIGS["c2"]
+    ins = _block_inputs(ctx, cfg)
+    entries = [dict(wcache=ctx.encode_weights(cfg.tile, hl.to_device(W)), Ma=mm.Ma, R=mm.R, Nb=mm.Nb,
+                    ct_in=hl.to_device(ct_in), seed=seed) for mm, W, ct_in, seed in ins]
+    single = []
+    for e in entries:
+        m, sh = ctx.he_matmul_share(cfg.tile, e["wcache"], e["Ma"], e["R"], e["Nb"], e["ct_in"], seed=e["seed"])
+        single.append((hl.to_host(m), hl.to_host(sh)))
+    for _ in range(2):
+        outs = ctx.he_linear_batch(cfg.tile, entries)
+        _sync()
+        for (mm, *_), (m, sh), (em, es) in zip(ins, outs, single):
+            assert np.array_equal(hl.to_host(m), em), mm.name
+            assert np.array_equal(hl.to_host(sh), es), mm.name
+
+
 def test_bert_base_full_size_sampled(hl, ctx4096):
     """Config c2 at full size in the bench's launch configuration (fused call, default tile):
     sampled output tiles bit-exact against the oracle (its own scalar NTT), and for the whole
