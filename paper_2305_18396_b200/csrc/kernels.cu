@@ -157,7 +157,11 @@ __device__ __forceinline__ void fwd_round(double (&a)[16], int t, const double *
 #pragma unroll
       for (int u = 0; u < (1 << K); u++) {
         if (u & half) continue;
+#ifdef HL_NTT_KO_TW
+        const double w = __ldg(&tw[(1 << st)]);         // timing experiment only: wrong twiddles
+#else
         const double w = __ldg(&tw[(1 << st) + (gid_high << ls) + (u >> (K - ls))]);
+#endif
         double &X = a[g * (1 << K) + u], &Y = a[g * (1 << K) + u + half];
         const double T = mm_d(Y, w, p, pinv);
         Y = __dsub_rn(X, T);
@@ -196,7 +200,11 @@ __device__ __forceinline__ void inv_round(double (&a)[16], int t, const double *
           X = mm_d(s, pc.ninv_d, p, pinv);
           Y = mm_d(d, pc.ninv_w1_d, p, pinv);
         } else {
+#ifdef HL_NTT_KO_TW
+          const double w = __ldg(&tw[(1 << st)]);
+#else
           const double w = __ldg(&tw[(1 << st) + (gid_high << ls) + (u >> (K - ls))]);
+#endif
           X = s;
           Y = mm_d(d, w, p, pinv);
         }
