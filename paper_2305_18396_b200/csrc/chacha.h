@@ -36,8 +36,8 @@ HL_HD void chacha_block_u64(uint64_t seed, uint32_t domain, uint64_t stream, uin
   uint32_t x0 = 0x61707865u, x1 = 0x3320646eu, x2 = 0x79622d32u, x3 = 0x6b206574u;
   uint32_t x4 = k0, x5 = k1, x6 = 0, x7 = 0, x8 = 0, x9 = 0, x10 = 0, x11 = 0;
   uint32_t x12 = ctr, x13 = n0, x14 = n1, x15 = n2;
-#pragma unroll
-  for (int i = 0; i < 10; i++) {
+#pragma unroll 1
+  for (int i = 0; i < 10; i++) {   // not unrolled: keeps the fused INTT+mask kernel within the I-cache
     HL_QR(x0, x4, x8, x12) HL_QR(x1, x5, x9, x13) HL_QR(x2, x6, x10, x14) HL_QR(x3, x7, x11, x15)
     HL_QR(x0, x5, x10, x15) HL_QR(x1, x6, x11, x12) HL_QR(x2, x7, x8, x13) HL_QR(x3, x4, x9, x14)
   }

@@ -315,6 +315,8 @@ int hl_geometry(const hl_ctx *c, hl_tile tile, int64_t Ma, int64_t R, int64_t Nb
   if (tile.m <= 0 || tile.r <= 0 || tile.n <= 0 ||
       (int64_t)tile.m * tile.r * tile.n > (int64_t)c->N)
     return hl_fail(HL_EDIM, "tile (m, r, n) must be positive with m*r*n <= N");
+  if ((tile.m & (tile.m - 1)) || (tile.r & (tile.r - 1)) || (tile.n & (tile.n - 1)))
+    return hl_fail(HL_EDIM, "tile (m, r, n) must be powers of two (reading C2)");
   if (Ma <= 0 || R <= 0 || Nb <= 0) return hl_fail(HL_EINVAL, "Ma, R, Nb must be positive");
   g->m = tile.m; g->r = tile.r; g->n = tile.n;
   g->nI = (Ma + tile.m - 1) / tile.m;

@@ -508,6 +508,7 @@ k_ntt_inv(const uint64_t *in, uint64_t *out, DevParams P) {
 struct MaskArgs {
   int64_t Ma, Nb, nK, i_begin;
   int m, r, n;
+  int lm, lr;          // log2 m, log2 r (tiles are powers of two: divisions become shifts)
   uint64_t seed;
 };
 
@@ -529,9 +530,10 @@ k_ntt_inv_mask(const uint64_t *__restrict__ ct_ntt, uint64_t *__restrict__ maske
   uint64_t *dst = masked + (size_t)o * per;
   if (c == 0) {
     const uint64_t stream = (uint64_t)(I * M.nK + K);
+#pragma unroll 1
     for (int kk = t; kk < mn; kk += Gm::NT) {
-      const int k = kk / M.m, i = kk % M.m;
-      const int pos = k * mr + i * M.r + M.r - 1;
+      const int k = kk >> M.lm, i = kk & (M.m - 1);
+      const int pos = ((k * M.m + i) << M.lr) + M.r - 1;
       const uint64_t s = hl::prf_u64(M.seed, hl::kDomMask, stream, (uint64_t)pos) & tmask;
       sig_sm[kk] = s;
       const int64_t row = K * M.n + k, col = I * M.m + i;
@@ -554,9 +556,8 @@ k_ntt_inv_mask(const uint64_t *__restrict__ ct_ntt, uint64_t *__restrict__ maske
         const int idx = elem_idx<LOGN, 0>(t, g, u);
         if (c == 1) {
           dst[(size_t)L * mn + (size_t)l * Gm::N + idx] = x;
-        } else if (idx < mr * M.n && (idx % M.r) == M.r - 1) {
-          const int k = idx / mr, i = (idx % mr) / M.r;
-          const int kk = k * M.m + i;
+        } else if (idx < mr * M.n && (idx & (M.r - 1)) == M.r - 1) {
+          const int kk = idx >> M.lr;               // = k*m + i for pos(i, k) = (k m + i) r + r - 1
           uint64_t d = shoup_mul(sig_sm[kk], pc.delta, pc.delta_sh, pc.p);
           d = d >= pc.p ? d - pc.p : d;
           dst[(size_t)l * mn + kk] = x >= d ? x - d : x + pc.p - d;
@@ -1250,6 +1251,7 @@ static MaskArgs mask_args(const Geo &g, int64_t Ma, int64_t Nb, uint64_t seed) {
   MaskArgs M;
   M.Ma = Ma; M.Nb = Nb; M.nK = g.nK; M.i_begin = g.i_begin;
   M.m = g.m; M.r = g.r; M.n = g.n; M.seed = seed;
+  M.lm = __builtin_ctz((unsigned)g.m); M.lr = __builtin_ctz((unsigned)g.r);
   return M;
 }
 

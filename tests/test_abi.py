@@ -84,6 +84,9 @@ def test_layout_and_dims(hl):
         ctx.layout((16, 16, 32), 64, 64, 64)          # m*r*n = 8192 > N
     assert e.value.code == hl.HL_EDIM
     with pytest.raises(hl.HLError) as e:
+        ctx.layout((3, 8, 32), 64, 64, 64)            # tiles are powers of two (reading C2)
+    assert e.value.code == hl.HL_EDIM
+    with pytest.raises(hl.HLError) as e:
         ctx.layout((16, 8, 32), 64, 64, 64, 3, 9)     # shard beyond nI = 4
     assert e.value.code == hl.HL_EINVAL
 
