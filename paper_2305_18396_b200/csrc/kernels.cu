@@ -515,13 +515,13 @@ struct MaskArgs {
 template <int LOGN>
 __global__ void __launch_bounds__(Geom<LOGN>::NT)
 k_ntt_inv_mask(const uint64_t *__restrict__ ct_ntt, uint64_t *__restrict__ masked, uint64_t *__restrict__ share,
-               MaskArgs M, DevParams P) {
+               MaskArgs M, DevParams P, int c1_only) {
   using Gm = Geom<LOGN>;
   extern __shared__ double sm[];
   uint64_t *sig_sm = reinterpret_cast<uint64_t *>(sm + Gm::SMEM_WORDS);   // sigma at kept positions
   const int t = threadIdx.x;
-  const int c = blockIdx.x & 1;
-  const int64_t o = blockIdx.x >> 1;                  // I_loc * nK + K
+  const int c = c1_only ? 1 : (blockIdx.x & 1);
+  const int64_t o = c1_only ? blockIdx.x : (blockIdx.x >> 1);   // I_loc * nK + K
   const int64_t Iloc = o / M.nK, K = o % M.nK, I = M.i_begin + Iloc;
   const int mn = M.m * M.n, mr = M.m * M.r;
   const int L = P.L;
@@ -565,6 +565,92 @@ k_ntt_inv_mask(const uint64_t *__restrict__ ct_ntt, uint64_t *__restrict__ maske
       }
     __syncthreads();   // smem reuse by the next prime
   }
+}
+
+// ---------------------------------------------------------------------------------------
+// c0 of the compressed response, pruned (k_ntt_inv_mask computes c1).  Only the coefficients
+// pos(i,k) = (k m + i) r + r - 1, the residue class r-1 mod r, are kept.  The
+// first inverse round (distances 1..8) mixes every class; every later stage pairs indices >= 16
+// apart, i.e. within a class when r <= 16.  Phase A: all threads run the first round of every
+// prime and park the values in shared memory.  Phase B: per prime, NT/r threads -- the live
+// "virtual threads" tv = 16 h + (r j + r - 1) of the remaining rounds -- finish the transform on
+// their own warps, all primes concurrently: 1/r of the remaining butterflies.
+// ---------------------------------------------------------------------------------------
+template <int LOGN, int R>
+__device__ __forceinline__ void inv_rounds_live(double (&a)[16], double *sm, int tv, bool act, int bar, int nbar,
+                                                const double *tw, const PrimeConsts &pc) {
+  if constexpr (R >= 0) {
+    if (act) to_smem<LOGN, R + 1>(a, sm, tv);
+    asm volatile("bar.sync %0, %1;" ::"r"(bar), "r"(nbar) : "memory");
+    if (act) from_smem<LOGN, R>(a, sm, tv);
+    asm volatile("bar.sync %0, %1;" ::"r"(bar), "r"(nbar) : "memory");
+    if (act) inv_round<LOGN, R>(a, tv, tw, pc);
+    inv_rounds_live<LOGN, R - 1>(a, sm, tv, act, bar, nbar, tw, pc);
+  }
+}
+
+template <int LOGN>
+__global__ void __launch_bounds__(Geom<LOGN>::NT)
+k_intt_c0_pruned(const uint64_t *__restrict__ ct_ntt, uint64_t *__restrict__ masked, uint64_t *__restrict__ share,
+                 MaskArgs M, DevParams P) {
+  using Gm = Geom<LOGN>;
+  extern __shared__ double sm[];
+  const int L = P.L;
+  uint64_t *sig_sm = reinterpret_cast<uint64_t *>(sm + (size_t)L * Gm::SMEM_WORDS);
+  const int t = threadIdx.x, warp = t >> 5;
+  const int64_t o = blockIdx.x;                        // I_loc * nK + K
+  const int64_t Iloc = o / M.nK, K = o % M.nK, I = M.i_begin + Iloc;
+  const int mn = M.m * M.n, mr = M.m * M.r;
+  const uint64_t tmask = (P.t_bits >= 64) ? ~0ull : ((1ull << P.t_bits) - 1);
+  uint64_t *dst = masked + (size_t)o * L * (mn + Gm::N);
+  const uint64_t stream = (uint64_t)(I * M.nK + K);
+#pragma unroll 1
+  for (int kk = t; kk < mn; kk += Gm::NT) {
+    const int k = kk >> M.lm, i = kk & (M.m - 1);
+    const uint64_t s = hl::prf_u64(M.seed, hl::kDomMask, stream, (uint64_t)(((k * M.m + i) << M.lr) + M.r - 1)) & tmask;
+    sig_sm[kk] = s;
+    const int64_t row = K * M.n + k, col = I * M.m + i;
+    if (row < M.Nb && col < M.Ma) share[row * M.Ma + col] = s;
+  }
+  // phase A: first inverse round of every prime (all threads)
+  for (int l = 0; l < L; l++) {
+    const PrimeConsts pc = pick(P, l);
+    double a[16];
+    load_ntt_domain<LOGN>(a, ct_ntt + (((size_t)o * 2) * L + l) * Gm::N, t, pc);
+    inv_round<LOGN, Gm::NR - 1>(a, t, P.twd_inv + (size_t)l * Gm::N, pc);
+    to_smem<LOGN, Gm::NR - 1>(a, sm + (size_t)l * Gm::SMEM_WORDS, t);
+  }
+  __syncthreads();
+  // phase B: prime l on warps [l*wpp, (l+1)*wpp)
+  const int nlive = 16 / M.r, nact = Gm::NT / M.r, wpp = (nact + 31) / 32;
+  if (warp >= L * wpp) return;
+  const int l = warp / wpp, p = (warp % wpp) * 32 + (t & 31);
+  const bool act = p < nact;
+  const int tv = ((p / nlive) << 4) | (M.r * (p % nlive) + M.r - 1);
+  const PrimeConsts pc = pick(P, l);
+  const double *tw = P.twd_inv + (size_t)l * Gm::N;
+  double *sml = sm + (size_t)l * Gm::SMEM_WORDS;
+  double a[16];
+  if (act) {
+    from_smem<LOGN, Gm::NR - 2>(a, sml, tv);
+    inv_round<LOGN, Gm::NR - 2>(a, tv, tw, pc);
+  }
+  inv_rounds_live<LOGN, Gm::NR - 3>(a, sml, tv, act, 1 + l, wpp * 32, tw, pc);
+  if (!act) return;
+  constexpr int K0 = Gm::k(0), G = 16 >> K0;
+#pragma unroll
+  for (int g = 0; g < G; g++)
+#pragma unroll
+    for (int u = 0; u < (1 << K0); u++) {
+      const int idx = elem_idx<LOGN, 0>(tv, g, u);
+      if (idx < mr * M.n) {                            // idx = r-1 mod r by construction
+        const uint64_t x = d2u(canon_d(a[g * (1 << K0) + u], pc.pd, pc.pinv));
+        const int kk = idx >> M.lr;
+        uint64_t d = shoup_mul(sig_sm[kk], pc.delta, pc.delta_sh, pc.p);
+        d = d >= pc.p ? d - pc.p : d;
+        dst[(size_t)l * mn + kk] = x >= d ? x - d : x + pc.p - d;
+      }
+    }
 }
 
 // ---------------------------------------------------------------------------------------
@@ -1172,11 +1258,27 @@ void launch_mac(const hl_ctx *c, const uint2 *W, const uint32_t *X, uint64_t *ou
 template <int LOGN>
 void launch_inv_mask(const hl_ctx *c, const uint64_t *ct_ntt, uint64_t *masked, uint64_t *share, MaskArgs M,
                      int64_t nout, cudaStream_t st) {
+  using Gm = Geom<LOGN>;
   static bool init = false;
-  if (!init) { set_smem(k_ntt_inv_mask<LOGN>, ntt_smem<LOGN>() + (size_t)Geom<LOGN>::N * 8); init = true; }
+  if (!init) {
+    set_smem(k_ntt_inv_mask<LOGN>, ntt_smem<LOGN>() + (size_t)Gm::N * 8);
+    set_smem(k_intt_c0_pruned<LOGN>, 232448);
+    init = true;
+  }
+  // the pruned c0 transform needs r in {2..16} and one warp group per prime within the CTA
+  static const bool no_prune = getenv("HELINEAR_NO_PRUNE") != nullptr;
+  const int wpp = (Gm::NT / std::max(M.r, 1) + 31) / 32;
+  const size_t smem_c0 = ntt_smem<LOGN>() * c->L + (size_t)M.m * M.n * 8;
+  const bool prune = !no_prune && M.r >= 2 && M.r <= 16 && (int)c->L * wpp <= Gm::NT / 32 && smem_c0 <= 232448;
   const size_t smem = ntt_smem<LOGN>() + (size_t)M.m * M.n * 8;
   KTimer kt(c, HL_K_INTT_MASK, st);
-  k_ntt_inv_mask<LOGN><<<(unsigned)(nout * 2), Geom<LOGN>::NT, smem, st>>>(ct_ntt, masked, share, M, c->dp);
+  if (prune) {
+    k_intt_c0_pruned<LOGN><<<(unsigned)nout, Gm::NT, smem_c0, st>>>(
+        ct_ntt, masked, share, M, c->dp);
+    k_ntt_inv_mask<LOGN><<<(unsigned)nout, Gm::NT, smem, st>>>(ct_ntt, masked, share, M, c->dp, 1);
+  } else {
+    k_ntt_inv_mask<LOGN><<<(unsigned)(nout * 2), Gm::NT, smem, st>>>(ct_ntt, masked, share, M, c->dp, 0);
+  }
 }
 
 }  // namespace
