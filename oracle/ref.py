@@ -449,3 +449,30 @@ def matmul_mod_t(X: np.ndarray, W: np.ndarray, t_bits: int = 37) -> np.ndarray:
         for j in range(X.shape[1]):
             acc += np.outer(X[:, j].astype(np.uint64), W[j, :].astype(np.uint64))
     return acc & np.uint64((1 << t_bits) - 1)
+
+
+# ----------------------------------------------------------------------------------------
+# FC layer (§3.1.1 "fully connected layer"): with the input shared as
+# x = <x>_0 + <x>_1 (client, server), the client's share of y = W x + b is the decrypted
+# Pi_MatMul output <W<x>_0>_0 and the server's is <y>_1 = <W<x>_0>_1 + W<x>_1 + b.  In the
+# layout of X.W (reading C1): Y = X W + b, server share = share_server + X1.W + b mod 2^t.
+# ----------------------------------------------------------------------------------------
+def fc_server_share(share_server: np.ndarray, X1: np.ndarray, W: np.ndarray, bias, t_bits: int = 37) -> np.ndarray:
+    """<y>_1 = <W<x>_0>_1 + W<x>_1 + b, all mod 2^t_bits; bias per output
+    column (broadcast over the Nb rows) or None."""
+    out = share_server.astype(np.uint64) + matmul_mod_t(X1, W, 64 if t_bits >= 64 else t_bits)
+    if bias is not None:
+        with np.errstate(over="ignore"):
+            out = out + np.asarray(bias, dtype=np.uint64)[None, :]
+    return out & np.uint64((1 << t_bits) - 1)
+
+
+def fc_protocol(P: Params, tile, X: np.ndarray, X1: np.ndarray, W: np.ndarray, bias, key_seed: int,
+                enc_seed: int, mask_seed: int):
+    """The FC protocol of PAPER.md:106-111 on the oracle: X = X0 + X1 mod 2^t with X0 the
+    client's share; returns (client share, server share) of X.W + b."""
+    tmask = np.uint64((1 << P.t_bits) - 1)
+    with np.errstate(over="ignore"):
+        X0 = (X.astype(np.uint64) - X1.astype(np.uint64)) & tmask
+    r = matmul_protocol(P, tile, X0, W, key_seed, enc_seed, mask_seed, True)
+    return r["share_client"], fc_server_share(r["share_server"], X1, W, bias, P.t_bits)

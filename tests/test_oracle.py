@@ -316,3 +316,39 @@ def test_mask_uniform_chi_squared(P4096):
     exp = len(top) / 16
     chi2 = ((counts - exp) ** 2 / exp).sum()
     assert chi2 < 37.7        # chi^2_{15} at p = 0.001
+
+
+# ----------------------------------------------------------------------------- FC layer (row f1)
+@pytest.mark.parametrize("shape,tile", [((8, 64, 64), (16, 32, 8)), ((5, 24, 40), (16, 8, 32))])
+def test_fc_protocol_reconstructs_XW_plus_b(P4096, shape, tile):
+    """with x = <x>_0 + <x>_1, the client's decrypted Pi_MatMul share of
+    W<x>_0 plus the server's <W<x>_0>_1 + W<x>_1 + b reconstruct W x + b (mod 2^l) -- checked
+    against brute force with Python integers (no numpy wrapping)."""
+    import synth
+    Nb, R, Ma = shape
+    X = synth.activations(71, Nb, R)
+    X1 = synth.activations(72, Nb, R)           # the server's share: uniform, independent of X
+    W = synth.weights(73, R, Ma)
+    b = synth.activations(74, 1, Ma)[0]
+    sc, ss = ref.fc_protocol(P4096, tile, X, X1, W, b, 75, 76, 77)
+    t = 1 << 37
+    for i in range(Nb):
+        for j in range(Ma):
+            want = (sum(int(X[i, k]) * int(W[k, j]) for k in range(R)) + int(b[j])) % t
+            assert (int(sc[i, j]) + int(ss[i, j])) % t == want
+
+
+def test_fc_server_share_special_cases(P4096):
+    """X1 = 0 and b = 0 leave the HE share unchanged; the local term is X1.W mod 2^37 (Python
+    integers) and the bias is added per output column."""
+    import synth
+    S = synth.activations(81, 4, 6)
+    X1 = synth.activations(82, 4, 3)
+    W = synth.weights(83, 3, 6)
+    b = synth.activations(84, 1, 6)[0]
+    assert np.array_equal(ref.fc_server_share(S, np.zeros_like(X1), W, None), S)
+    got = ref.fc_server_share(S, X1, W, b)
+    for i in range(4):
+        for j in range(6):
+            want = (int(S[i, j]) + sum(int(X1[i, k]) * int(W[k, j]) for k in range(3)) + int(b[j])) % (1 << 37)
+            assert int(got[i, j]) == want
