@@ -234,6 +234,38 @@ def run_ours(args, rank, world, local_rank):
     ktimes = ctx.timing_read()
     clk = clocks.stop() if clocks else None
 
+    # ---------------- row f1: the server's FC share assembly, share += X1.W + b,
+    # timed separately (it is not part of the Pi_MatMul metric): device-resident inputs, events
+    fc_info = None
+    if not shard:
+        fc_in = []
+        for mi, m in enumerate(mats):
+            mm = m["mm"]
+            W = synth.weights(synth.seed_for(block, mi, "w"), mm.R, mm.Ma)
+            fc_in.append(dict(X1=hl.to_device(synth.activations(synth.seed_for(block, mi, "x") + 7, mm.Nb, mm.R), dev),
+                              wp=ctx.fc_encode_weights(hl.to_device(W, dev)),
+                              b=hl.to_device(synth.activations(synth.seed_for(block, mi, "x") + 8, 1, mm.Ma)[0], dev),
+                              mm=mm, share=m["share"]))
+
+        def fc_step():
+            for f in fc_in:
+                ctx.fc_local_share(f["X1"], f["wp"], f["mm"].Ma, f["share"], bias=f["b"], stream=stream)
+        for _ in range(3):
+            fc_step()
+        torch.cuda.synchronize()
+        f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        f0.record(stream)
+        for _ in range(args.steps):
+            fc_step()
+        f1.record(stream)
+        torch.cuda.synchronize()
+        fc_ms = f0.elapsed_time(f1) / args.steps
+        fc_macs = sum(f["mm"].Nb * f["mm"].R * f["mm"].Ma for f in fc_in)
+        fc_info = {"what": "server FC share assembly share += X1.W + b mod 2^37 (row f1, PAPER.md:106-111), "
+                           "4 products of the block, int8 tensor cores (15 limb MMAs per 32-K step)",
+                   "ms_per_block": round(fc_ms, 4), "plaintext_macs": fc_macs,
+                   "gmacs_per_s": round(fc_macs / (fc_ms * 1e-3) / 1e9, 1)}
+
     # ---------------- end to end through the public API on pinned host buffers
     host_masked = [torch.empty(m["lay"].ct_masked_words, dtype=torch.int64).pin_memory() for m in mats]
     host_share = [torch.empty(m["lay"].share_words, dtype=torch.int64).pin_memory() for m in mats]
@@ -341,6 +373,8 @@ def run_ours(args, rank, world, local_rank):
         "e2e": {"value": round(e2e_ms, 4), "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
         "clocks": clk,
     }
+    if fc_info:
+        line["fc_local_share"] = fc_info
     if world == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = oracle_baseline(cfg, tile, args.cpu_itiles)
     return line

@@ -201,6 +201,29 @@ int hl_he_linear_host(const hl_ctx *ctx, hl_tile tile, const void *wcache, int64
                       void *workspace, uint64_t *dev_ct_out_ntt, uint64_t *dev_ct_masked,
                       uint64_t *dev_share, void *stream);
 
+/* ---- FC layer, server side --------------------- */
+
+/* With the layer input shared as x = <x>_0 + <x>_1 (client, server), the server's share of
+ * y = W x + b is <y>_1 = <W<x>_0>_1 + W<x>_1 + b (mod 2^l), <W<x>_0>_1 being its share from
+ * hl_mask_and_share / hl_he_matmul_share.  In the layout of X.W (reading C1):
+ *   share[Nb][Ma] <- share + X1 . W + b   (mod 2^log2_t; b per output column)
+ * computed exactly on the int8 tensor cores (5 byte limbs, only limb pairs a+b <= 4 survive
+ * mod 2^37).  Supports log2_t <= 40 and R <= 6400 (HL_ENOTSUP otherwise). */
+
+/* Buffer sizes: wplanes_bytes (hl_fc_encode_weights output), workspace_bytes (per call scratch). */
+int hl_fc_layout(const hl_ctx *ctx, int64_t Nb, int64_t R, int64_t Ma, int64_t *wplanes_bytes,
+                 int64_t *workspace_bytes);
+
+/* Offline: W device [R][Ma] (< 2^log2_t, HL_ERANGE otherwise; synchronises `stream` once) ->
+ * wplanes (device, opaque byte planes). */
+int hl_fc_encode_weights(const hl_ctx *ctx, const uint64_t *W, int64_t R, int64_t Ma, void *wplanes,
+                         void *stream);
+
+/* Online: X1 device [Nb][R] (the server's share of the input, taken mod 2^log2_t), bias device [Ma]
+ * or NULL, share device [Nb][Ma] (in/out), workspace device (hl_fc_layout). Stream-ordered. */
+int hl_fc_local_share(const hl_ctx *ctx, const uint64_t *X1, const void *wplanes, const uint64_t *bias,
+                      int64_t Nb, int64_t R, int64_t Ma, void *workspace, uint64_t *share, void *stream);
+
 /* ---- diagnostics (used by the parity tests and the NTT microbenchmark) -------------------- */
 
 /* out[p] = a[p] * b[p] in Z_{p_l}[X]/(X^N+1) for p < npoly, through the device NTT/INTT
@@ -223,7 +246,8 @@ enum {
   HL_K_MASK = 4,        /* mask_and_share                                                        */
   HL_K_ENCODE = 5,      /* encode_weights (pi_A + forward NTT)                                   */
   HL_K_OTHER = 6,       /* diagnostics                                                           */
-  HL_K_COUNT = 7
+  HL_K_FC = 7,          /* FC local share (hl_fc_local_share)                                    */
+  HL_K_COUNT = 8
 };
 
 /* on != 0: record a CUDA event pair on the launching stream around every kernel launch made

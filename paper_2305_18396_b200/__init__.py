@@ -31,8 +31,9 @@ EXPORTS = ("hl_last_error", "hl_ctx_create", "hl_ctx_destroy", "hl_ctx_params", 
            "hl_layout_query",
            "hl_keygen", "hl_encrypt", "hl_decrypt_share", "hl_encode_weights", "hl_he_matmul",
            "hl_mask_and_share", "hl_he_matmul_share", "hl_he_linear_batch", "hl_he_linear_host", "hl_poly_mul",
-           "hl_ntt_roundtrip", "hl_timing_enable", "hl_timing_read")
-KERNELS = ("ntt_fwd", "mac", "intt_mask", "intt", "mask", "encode", "other")   # HL_K_* order
+           "hl_ntt_roundtrip", "hl_timing_enable", "hl_timing_read", "hl_fc_layout", "hl_fc_encode_weights",
+           "hl_fc_local_share")
+KERNELS = ("ntt_fwd", "mac", "intt_mask", "intt", "mask", "encode", "other", "fc")   # HL_K_* order
 
 
 class HLError(RuntimeError):
@@ -108,6 +109,9 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
         "hl_poly_mul": [vp, vp, vp, vp, i64, vp, vp],
         "hl_ntt_roundtrip": [vp, vp, i64, vp, vp],
         "hl_timing_enable": [vp, i32],
+        "hl_fc_layout": [vp, i64, i64, i64, ctypes.POINTER(i64), ctypes.POINTER(i64)],
+        "hl_fc_encode_weights": [vp, vp, i64, i64, vp, vp],
+        "hl_fc_local_share": [vp, vp, vp, vp, i64, i64, i64, vp, vp, vp],
         "hl_timing_read": [vp, vp, vp],
     }
     for name, args in sig.items():
@@ -310,6 +314,30 @@ class Context:
                                       int(bool(compress)), ct_masked_host.data_ptr(), share_host.data_ptr(),
                                       _dptr(dev_ct_in), _dptr(workspace), _dptr(dev_ct_out_ntt),
                                       _dptr(dev_ct_masked), _dptr(dev_share), _stream(stream)))
+
+    # ---------------------------------------------------------------- FC layer (row f1)
+    def fc_layout(self, Nb: int, R: int, Ma: int):
+        wb, ws = ctypes.c_int64(), ctypes.c_int64()
+        _check(_lib.hl_fc_layout(self._h, Nb, R, Ma, ctypes.byref(wb), ctypes.byref(ws)))
+        return wb.value, ws.value
+
+    def fc_encode_weights(self, W, stream=None):
+        """W: CUDA tensor [R][Ma] (< 2^t).  Returns the opaque byte-plane form."""
+        R, Ma = W.shape
+        wb, _ = self.fc_layout(1, R, Ma)
+        wp = _dev_empty(-(-wb // 8), W.device)
+        _check(_lib.hl_fc_encode_weights(self._h, _dptr(W), R, Ma, _dptr(wp), _stream(stream)))
+        return wp
+
+    def fc_local_share(self, X1, wplanes, Ma: int, share, bias=None, workspace=None, stream=None):
+        """share[Nb][Ma] += X1.W + bias (mod 2^t), in place."""
+        Nb, R = X1.shape
+        _, ws = self.fc_layout(Nb, R, Ma)
+        if workspace is None:
+            workspace = _dev_empty(-(-ws // 8), X1.device)
+        _check(_lib.hl_fc_local_share(self._h, _dptr(X1), _dptr(wplanes), _dptr(bias) if bias is not None else None,
+                                      Nb, R, Ma, _dptr(workspace), _dptr(share), _stream(stream)))
+        return share
 
     # ---------------------------------------------------------------- timing
     def timing_enable(self, on: bool = True):

@@ -1065,6 +1065,7 @@ k_mac_f64(MacArgs A, DevParams P) {
 }
 
 #include "mac_tc.cuh"
+#include "fc.cuh"
 
 // pointwise product in the NTT domain (diagnostics only)
 __global__ void k_pointwise(const uint64_t *a, const uint64_t *b, uint64_t *out, int64_t n, DevParams P) {
@@ -1435,8 +1436,12 @@ extern "C" int hl_he_linear_batch(const hl_ctx *c, hl_tile tile, int n, const hl
   cudaEventRecord(e_fwd[0], s1);
   for (int i = 0; i < n; i++) {
     cudaStreamWaitEvent(s0, e_fwd[i], 0);
+    static const int mac_smem = [] {
+      const char *e = getenv("HELINEAR_BATCH_MAC_SMEM_KB");
+      return e ? atoi(e) * 1024 : kMacSmemShared;
+    }();
     launch_mac(c, (const uint2 *)d[i].wcache, (const uint32_t *)d[i].workspace, d[i].ct_out_ntt, E[i].mg, s0,
-               kMacSmemShared);
+               mac_smem);
     cudaEventRecord(e_mac[i], s0);
     if (i + 1 < n) { fwd(i + 1); cudaEventRecord(e_fwd[i + 1], s1); }     // overlaps MAC(i)
     cudaStreamWaitEvent(s1, e_mac[i], 0);
@@ -1448,6 +1453,77 @@ extern "C" int hl_he_linear_batch(const hl_ctx *c, hl_tile tile, int n, const hl
   cudaStreamWaitEvent(sc, e_macs, 0);
   for (auto &e : ev) cudaEventDestroy(e);         // released once the recorded work completes
   return hl_cuda_check("hl_he_linear_batch: launch");
+}
+
+// ---------------------------------------------------------------------------------------
+// FC-layer share assembly, fc.cuh
+// ---------------------------------------------------------------------------------------
+static int fc_geom(const hl_ctx *c, int64_t Nb, int64_t R, int64_t Ma, FcGeom *g) {
+  if (!c) return hl_fail(HL_EINVAL, "ctx is NULL");
+  if (Nb <= 0 || R <= 0 || Ma <= 0) return hl_fail(HL_EINVAL, "Nb, R, Ma must be positive");
+  if (R > 6400) return hl_fail(HL_ENOTSUP, "FC local share: R > 6400 (s32 limb accumulators)");
+  if (c->log2_t > 40) return hl_fail(HL_ENOTSUP, "FC local share: log2_t > 40 (5 byte limbs)");
+  g->Nb = Nb; g->R = R; g->Ma = Ma;
+  g->nMt = (int)((Nb + kFcMT - 1) / kFcMT);
+  g->nNt = (int)((Ma + kFcNT - 1) / kFcNT);
+  g->nKc = (int)((R + 31) / 32);
+  // split K so that the grid covers ~2 CTAs per SM (partial sums meet by wrapping atomic adds)
+  const int tiles = g->nMt * g->nNt;
+  const int splits = std::max(1, std::min(g->nKc, (2 * c->num_sms + tiles - 1) / tiles));
+  g->kps = (g->nKc + splits - 1) / splits;
+  g->tmask = (1ull << c->log2_t) - 1;
+  return HL_OK;
+}
+
+extern "C" int hl_fc_layout(const hl_ctx *c, int64_t Nb, int64_t R, int64_t Ma, int64_t *wplanes_bytes,
+                            int64_t *workspace_bytes) {
+  FcGeom g;
+  int rc;
+  if ((rc = fc_geom(c, Nb, R, Ma, &g))) return rc;
+  if (wplanes_bytes) *wplanes_bytes = (int64_t)g.nNt * g.nKc * kFcBStage;
+  if (workspace_bytes) *workspace_bytes = (int64_t)g.nMt * g.nKc * kFcAStage;
+  return HL_OK;
+}
+
+extern "C" int hl_fc_encode_weights(const hl_ctx *c, const uint64_t *W, int64_t R, int64_t Ma, void *wplanes,
+                                    void *stream) {
+  int rc;
+  if ((rc = check_ptrs({c, W, wplanes}, "hl_fc_encode_weights"))) return rc;
+  FcGeom g;
+  if ((rc = fc_geom(c, 1, R, Ma, &g))) return rc;
+  cudaStream_t st = (cudaStream_t)stream;
+  cudaMemsetAsync(c->d_flags, 0, 8, st);
+  const int64_t n = (int64_t)g.nNt * kFcNT * g.nKc * 32;
+  {
+    KTimer kt(c, HL_K_ENCODE, st);
+    k_fc_w_planes<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(W, (uint8_t *)wplanes, g, c->d_flags);
+  }
+  if ((rc = hl_cuda_check("hl_fc_encode_weights: launch"))) return rc;
+  uint32_t flags[2];
+  if (cudaMemcpyAsync(flags, c->d_flags, 8, cudaMemcpyDeviceToHost, st) != cudaSuccess ||
+      cudaStreamSynchronize(st) != cudaSuccess)
+    return hl_cuda_check("hl_fc_encode_weights: status readback");
+  if (flags[0]) return hl_fail(HL_ERANGE, "hl_fc_encode_weights: W value >= 2^log2_t");
+  return HL_OK;
+}
+
+extern "C" int hl_fc_local_share(const hl_ctx *c, const uint64_t *X1, const void *wplanes, const uint64_t *bias,
+                                 int64_t Nb, int64_t R, int64_t Ma, void *workspace, uint64_t *share, void *stream) {
+  int rc;
+  if ((rc = check_ptrs({c, X1, wplanes, workspace, share}, "hl_fc_local_share"))) return rc;
+  FcGeom g;
+  if ((rc = fc_geom(c, Nb, R, Ma, &g))) return rc;
+  cudaStream_t st = (cudaStream_t)stream;
+  static bool init = false;
+  if (!init) { set_smem(k_fc_gemm, kFcSmem); init = true; }
+  KTimer kt(c, HL_K_FC, st);
+  const int64_t n = (int64_t)g.nMt * kFcMT * g.nKc * 8;
+  k_fc_x_planes<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(X1, (uint8_t *)workspace, g);
+  const unsigned nsplit = (unsigned)((g.nKc + g.kps - 1) / g.kps);
+  k_fc_gemm<<<dim3(g.nNt, g.nMt, nsplit), 256, kFcSmem, st>>>((const uint8_t *)workspace, (const uint8_t *)wplanes,
+                                                              bias, share, g);
+  k_fc_mask<<<(unsigned)((Nb * Ma + 255) / 256), 256, 0, st>>>(share, Nb * Ma, g.tmask);
+  return hl_cuda_check("hl_fc_local_share: launch");
 }
 
 extern "C" int hl_he_linear_host(const hl_ctx *c, hl_tile tile, const void *wcache, int64_t Ma, int64_t R,

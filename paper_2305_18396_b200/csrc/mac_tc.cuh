@@ -252,7 +252,7 @@ k_mac_tc(MacTcArgs A, DevParams P) {
     // single-lane branch costs more than the MMA itself (profiles/r01/microbench_umma_i8_cost.log).
     // tiles of <= 64 rows use M = 64 (half the A-operand shared-memory reads per MMA); the
     // accumulator rows then sit in lanes 32(r/16) + r%16 (profiles/r01/microbench_umma_i8.log)
-    const uint32_t idesc = umma_idesc_u8(g.RT <= 64 ? 64 : 128, T::N);
+    const uint32_t idesc = umma_idesc_u8(g.RT <= 64 ? 64 : 128, (A.ko & 8) ? 16 : T::N);   // ko 8: timing only
     int st = 0;
     uint32_t ph = 0;
     uint32_t tile_no = 0, zseq = 0;

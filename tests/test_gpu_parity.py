@@ -355,3 +355,47 @@ def test_mac_long_j_chunked(hl, ctx4096, engine):
         ctx.set_mac_engine(2)
     exp = ref.he_matmul(P, tile, W, ct_in, Nb).reshape(-1, 2, ctx.L, ctx.N)
     assert np.array_equal(got, exp)
+
+
+# ------------------------------------------------------------------------- FC layer (row f1)
+@pytest.mark.parametrize("Nb,R,Ma", [(128, 768, 768), (5, 40, 50), (200, 100, 97), (1, 1, 1), (128, 3072, 96)])
+def test_fc_local_share_vs_oracle(hl, ctx4096, Nb, R, Ma):
+    """hl_fc_local_share (int8 tensor cores, 5 byte limbs) == oracle <W<x>_0>_1 + W<x>_1 + b mod 2^37:
+    several M/N/K tiles with ragged tails (Nb > 128, Ma not a multiple of 48, R not of 32), the
+    degenerate 1x1x1 product, and extreme limbs (all-ones 37-bit values)."""
+    ctx = ctx4096
+    S = synth.activations(901 + Nb, Nb, Ma)
+    X1 = synth.activations(902 + R, Nb, R)
+    W = synth.weights(903 + Ma, R, Ma)
+    b = synth.activations(904, 1, Ma)[0]
+    if Nb == 200:
+        X1[:] = (1 << 37) - 1
+        W[:7] = (1 << 37) - 1
+    wp = ctx.fc_encode_weights(hl.to_device(W))
+    share = hl.to_device(S)
+    ctx.fc_local_share(hl.to_device(X1), wp, Ma, share, bias=hl.to_device(b))
+    _sync()
+    assert np.array_equal(hl.to_host(share).reshape(Nb, Ma), ref.fc_server_share(S, X1, W, b))
+
+
+def test_fc_protocol_end_to_end(hl, ctx4096):
+    """The FC protocol of PAPER.md:106-111 with the GPU server: the client encrypts its share X0,
+    the server runs he_matmul_share and adds W X1 + b; client + server shares = X.W + b mod 2^37."""
+    ctx = ctx4096
+    P = _P(ctx)
+    tile, (Nb, R, Ma) = (16, 8, 32), (40, 48, 72)
+    X = synth.activations(911, Nb, R)
+    X1 = synth.activations(912, Nb, R)
+    X0 = (X - X1) & np.uint64((1 << 37) - 1)
+    W = synth.weights(913, R, Ma)
+    b = synth.activations(914, 1, Ma)[0]
+    sk = ctx.keygen(915)
+    ct_in = ctx.encrypt(sk, tile, X0, 916)
+    wc = ctx.encode_weights(tile, hl.to_device(W))
+    masked, share = ctx.he_matmul_share(tile, wc, Ma, R, Nb, hl.to_device(ct_in), seed=917)
+    ctx.fc_local_share(hl.to_device(X1), ctx.fc_encode_weights(hl.to_device(W)), Ma, share, bias=hl.to_device(b))
+    _sync()
+    share_c = ctx.decrypt_share(sk, tile, hl.to_host(masked), Ma, Nb, True)
+    got = (share_c + hl.to_host(share).reshape(Nb, Ma)) & np.uint64((1 << 37) - 1)
+    want = (ref.matmul_mod_t(X, W) + b[None, :]) & np.uint64((1 << 37) - 1)
+    assert np.array_equal(got, want)
