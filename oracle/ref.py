@@ -476,3 +476,24 @@ def fc_protocol(P: Params, tile, X: np.ndarray, X1: np.ndarray, W: np.ndarray, b
         X0 = (X.astype(np.uint64) - X1.astype(np.uint64)) & tmask
     r = matmul_protocol(P, tile, X0, W, key_seed, enc_seed, mask_seed, True)
     return r["share_client"], fc_server_share(r["share_server"], X1, W, bias, P.t_bits)
+
+
+# ----------------------------------------------------------------------------------------
+# Attention cross terms (Eq. 2): Z = X Y with both inputs shared,
+# X = X0 + X1, Y = Y0 + Y1 (client 0, server 1).  Two Pi_MatMul invocations give shares of
+# the cross terms X1 Y0 + X0 Y1 -- in the form of footnote 3 so that the client
+# always encrypts: Pi_MatMul(Y0^T -> client, X1^T -> server) yields shares of (X1 Y0)^T, which
+# both parties transpose -- and each party adds its local product (client X0 Y0, server X1 Y1).
+# ----------------------------------------------------------------------------------------
+def attention_protocol(P: Params, tile, X0: np.ndarray, X1: np.ndarray, Y0: np.ndarray, Y1: np.ndarray,
+                       seeds=(1, 2, 3, 4, 5, 6)):
+    """Returns (client share Z0, server share Z1) of Z = (X0+X1)(Y0+Y1) mod 2^t."""
+    tmask = np.uint64((1 << P.t_bits) - 1)
+    # term 1: X1 Y0 = (Y0^T X1^T)^T -- client operand Y0^T, server operand X1^T
+    t1 = matmul_protocol(P, tile, np.ascontiguousarray(Y0.T), np.ascontiguousarray(X1.T), *seeds[0:3])
+    # term 2: X0 Y1 -- client operand X0, server operand Y1
+    t2 = matmul_protocol(P, tile, X0, Y1, *seeds[3:6])
+    with np.errstate(over="ignore"):
+        Z0 = (t1["share_client"].T + t2["share_client"] + matmul_mod_t(X0, Y0, P.t_bits)) & tmask
+        Z1 = (t1["share_server"].T + t2["share_server"] + matmul_mod_t(X1, Y1, P.t_bits)) & tmask
+    return Z0, Z1

@@ -352,3 +352,36 @@ def test_fc_server_share_special_cases(P4096):
         for j in range(6):
             want = (int(S[i, j]) + sum(int(X1[i, k]) * int(W[k, j]) for k in range(3)) + int(b[j])) % (1 << 37)
             assert int(got[i, j]) == want
+
+
+# ----------------------------------------------------------------------------- attention (row f2)
+def test_attention_cross_terms_reconstruct_XY(P8192):
+    """PAPER.md:113-118 (Eq. 2): with X and Y both shared, two Pi_MatMul invocations on the cross
+    terms plus each party's local product give shares of X.Y mod 2^l -- checked against brute
+    force with Python integers.  Shares are uniform in Z_(2^37), so the server operand is not
+    small: the N=8192, L=3 set (q ~ 2^150) keeps the noise below Delta/2."""
+    import synth
+    tile = (32, 16, 16)
+    n, d = 24, 20                                   # Q K^T shape: (n x d) . (d x n)
+    X0, X1 = synth.activations(61, n, d), synth.activations(62, n, d)
+    Y0, Y1 = synth.activations(63, d, n), synth.activations(64, d, n)
+    Z0, Z1 = ref.attention_protocol(P8192, tile, X0, X1, Y0, Y1)
+    t = 1 << 37
+    X = [[(int(X0[i, k]) + int(X1[i, k])) % t for k in range(d)] for i in range(n)]
+    Y = [[(int(Y0[k, j]) + int(Y1[k, j])) % t for j in range(n)] for k in range(d)]
+    for i in range(n):
+        for j in range(n):
+            assert (int(Z0[i, j]) + int(Z1[i, j])) % t == sum(X[i][k] * Y[k][j] for k in range(d)) % t
+
+
+def test_attention_noise_needs_the_large_modulus(P4096):
+    """At N=4096, L=2 (q ~ 2^100) a uniform 37-bit server operand breaks decryption (the
+    r_t * K term of SURVEY Appendix C, ~2^75, exceeds Delta/2 ~ 2^62): the reconstruction fails,
+    which is why row f2 uses the q ~ 2^150 parameter set."""
+    import synth
+    tile = (16, 8, 32)
+    X0, X1 = synth.activations(65, 8, 24), synth.activations(66, 8, 24)
+    Y0, Y1 = synth.activations(67, 24, 8), synth.activations(68, 24, 8)
+    Z0, Z1 = ref.attention_protocol(P4096, tile, X0, X1, Y0, Y1)
+    want = ref.matmul_mod_t((X0 + X1) & np.uint64((1 << 37) - 1), (Y0 + Y1) & np.uint64((1 << 37) - 1))
+    assert not np.array_equal((Z0 + Z1) & np.uint64((1 << 37) - 1), want)
