@@ -266,6 +266,44 @@ def run_ours(args, rank, world, local_rank):
                    "ms_per_block": round(fc_ms, 4), "plaintext_macs": fc_macs,
                    "gmacs_per_s": round(fc_macs / (fc_ms * 1e-3) / 1e9, 1)}
 
+    # ---------------- row f2: the server side of one BERT-base block's attention
+    # cross terms, 12 heads x (Q K^T: 128x64 . 64x128, A V: 128x128 . 128x64), both inputs shared;
+    # N=8192, L=3 (uniform shares as server operands need q ~ 2^150), tile (32, 16, 16).
+    att_info = None
+    if not shard and not args.no_attention:
+        from paper_2305_18396_b200 import attention
+        actx = hl.Context(8192, 3, synth.T_BITS, device=local_rank)
+        atile = (32, 16, 16)
+        heads = []
+        for h in range(12):
+            for (n, d, n2) in ((128, 64, 128), (128, 128, 64)):
+                sd = synth.seed_for(block, 50 + h, "x") + 10 * d
+                X0, X1 = synth.activations(sd, n, d), synth.activations(sd + 1, n, d)
+                Y0, Y1 = synth.activations(sd + 2, d, n2), synth.activations(sd + 3, d, n2)
+                sk1, sk2 = actx.keygen(sd + 4), actx.keygen(sd + 5)
+                heads.append(dict(X1=hl.to_device(X1, dev), Y1=hl.to_device(Y1, dev),
+                                  ct1=hl.to_device(actx.encrypt(sk1, atile, np.ascontiguousarray(Y0.T), sd + 6), dev),
+                                  ct2=hl.to_device(actx.encrypt(sk2, atile, X0, sd + 7), dev), seeds=(sd + 8, sd + 9)))
+
+        def att_step():
+            for hd_ in heads:
+                attention.server_cross_product(actx, atile, hd_["X1"], hd_["Y1"], hd_["ct1"], hd_["ct2"],
+                                               hd_["seeds"], stream=stream)
+        att_step()
+        torch.cuda.synchronize()
+        nrep = max(2, min(args.steps, 5))
+        a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a0.record(stream)
+        for _ in range(nrep):
+            att_step()
+        a1.record(stream)
+        torch.cuda.synchronize()
+        att_info = {"what": "server side of the attention cross terms of one BERT-base block (row f2, "
+                            "PAPER.md:113-118): 12 heads x (QK^T, AV), 2 Pi_MatMul + local product each, online "
+                            "pi_A encoding of the server's shares, N=8192 L=3, tile (32,16,16)",
+                    "ms_per_block": round(a0.elapsed_time(a1) / nrep, 3), "cross_products": len(heads)}
+        del actx
+
     # ---------------- end to end through the public API on pinned host buffers
     host_masked = [torch.empty(m["lay"].ct_masked_words, dtype=torch.int64).pin_memory() for m in mats]
     host_share = [torch.empty(m["lay"].share_words, dtype=torch.int64).pin_memory() for m in mats]
@@ -375,6 +413,8 @@ def run_ours(args, rank, world, local_rank):
     }
     if fc_info:
         line["fc_local_share"] = fc_info
+    if att_info:
+        line["attention_cross_terms"] = att_info
     if world == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = oracle_baseline(cfg, tile, args.cpu_itiles)
     return line
@@ -465,6 +505,7 @@ def main():
     ap.add_argument("--cpu-itiles", type=int, default=2)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--sequential", action="store_true", help="one he_matmul_share per product (no 2-stream pipeline)")
+    ap.add_argument("--no-attention", action="store_true", help="skip the row-f2 attention measurement")
     ap.add_argument("--mode", choices=["weak", "shard"], default="weak",
                     help="weak: one block per rank; shard: one block split by I tiles + gather to rank 0")
     args = ap.parse_args()

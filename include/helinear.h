@@ -144,6 +144,13 @@ int hl_decrypt_share(const hl_ctx *ctx, const int8_t *sk, hl_tile tile, const ui
 int hl_encode_weights(const hl_ctx *ctx, hl_tile tile, const uint64_t *W, int64_t R, int64_t Ma,
                       int64_t i_begin, int64_t i_end, void *wcache, void *stream);
 
+/* hl_encode_weights for a strided W: element (row k, column j) at W[k*ld_row + j*ld_col], e.g.
+ * ld_row = 1, ld_col = R encodes the transpose of a row-major [Ma][R] matrix (the server operand
+ * X1^T of the attention cross term X1 Y0, PAPER.md:115 footnote). */
+int hl_encode_weights_strided(const hl_ctx *ctx, hl_tile tile, const uint64_t *W, int64_t R, int64_t Ma,
+                              int64_t ld_row, int64_t ld_col, int64_t i_begin, int64_t i_end, void *wcache,
+                              void *stream);
+
 /* Alg. 1 step 3, homomorphic part: for every I in the shard and every K,
  *   ct_out[I][K][c] = sum_J a_IJ * ct_in[J][K][c]  mod (X^N + 1, p_l),  c in {0, 1}
  * computed as forward NTT of ct_in -> pointwise multiply-accumulate over J against the cached
@@ -223,6 +230,13 @@ int hl_fc_encode_weights(const hl_ctx *ctx, const uint64_t *W, int64_t R, int64_
  * or NULL, share device [Nb][Ma] (in/out), workspace device (hl_fc_layout). Stream-ordered. */
 int hl_fc_local_share(const hl_ctx *ctx, const uint64_t *X1, const void *wplanes, const uint64_t *bias,
                       int64_t Nb, int64_t R, int64_t Ma, void *workspace, uint64_t *share, void *stream);
+
+/* Share arithmetic (attention cross terms):
+ * dst[rows][cols] <- dst + src (mod 2^log2_t), or dst + src^T when transpose != 0 (src then
+ * [cols][rows]: the shares of (X1 Y0)^T returned by Pi_MatMul in the footnote-3 form).
+ * Device buffers, stream-ordered. */
+int hl_share_accumulate(const hl_ctx *ctx, uint64_t *dst, const uint64_t *src, int64_t rows, int64_t cols,
+                        int transpose, void *stream);
 
 /* ---- diagnostics (used by the parity tests and the NTT microbenchmark) -------------------- */
 

@@ -32,7 +32,7 @@ EXPORTS = ("hl_last_error", "hl_ctx_create", "hl_ctx_destroy", "hl_ctx_params", 
            "hl_keygen", "hl_encrypt", "hl_decrypt_share", "hl_encode_weights", "hl_he_matmul",
            "hl_mask_and_share", "hl_he_matmul_share", "hl_he_linear_batch", "hl_he_linear_host", "hl_poly_mul",
            "hl_ntt_roundtrip", "hl_timing_enable", "hl_timing_read", "hl_fc_layout", "hl_fc_encode_weights",
-           "hl_fc_local_share")
+           "hl_fc_local_share", "hl_encode_weights_strided", "hl_share_accumulate")
 KERNELS = ("ntt_fwd", "mac", "intt_mask", "intt", "mask", "encode", "other", "fc")   # HL_K_* order
 
 
@@ -110,6 +110,8 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
         "hl_ntt_roundtrip": [vp, vp, i64, vp, vp],
         "hl_timing_enable": [vp, i32],
         "hl_fc_layout": [vp, i64, i64, i64, ctypes.POINTER(i64), ctypes.POINTER(i64)],
+        "hl_encode_weights_strided": [vp, Tile, vp, i64, i64, i64, i64, i64, i64, vp, vp],
+        "hl_share_accumulate": [vp, vp, vp, i64, i64, i32, vp],
         "hl_fc_encode_weights": [vp, vp, i64, i64, vp, vp],
         "hl_fc_local_share": [vp, vp, vp, vp, i64, i64, i64, vp, vp, vp],
         "hl_timing_read": [vp, vp, vp],
@@ -238,6 +240,22 @@ class Context:
         _check(_lib.hl_encode_weights(self._h, _tile(tile), _dptr(W), R, Ma, i_begin, i_end, _dptr(wcache),
                                       _stream(stream)))
         return wcache
+
+    def encode_weights_T(self, tile, M, i_begin: int = 0, i_end: int = -1, wcache=None, stream=None):
+        """Encode W = M^T for a CUDA tensor M [Ma][R] without materialising the transpose."""
+        Ma, R = M.shape
+        lay = self.layout(tile, Ma, R, 1, i_begin, i_end)
+        if wcache is None:
+            wcache = _dev_empty(lay.wcache_bytes // 8, M.device)
+        _check(_lib.hl_encode_weights_strided(self._h, _tile(tile), _dptr(M), R, Ma, 1, R, i_begin, i_end,
+                                              _dptr(wcache), _stream(stream)))
+        return wcache
+
+    def share_accumulate(self, dst, src, rows: int, cols: int, transpose: bool = False, stream=None):
+        """dst[rows][cols] += src (or src^T) mod 2^t, in place."""
+        _check(_lib.hl_share_accumulate(self._h, _dptr(dst), _dptr(src), rows, cols, int(bool(transpose)),
+                                        _stream(stream)))
+        return dst
 
     def he_matmul(self, tile, wcache, Ma: int, R: int, Nb: int, ct_in, i_begin: int = 0, i_end: int = -1,
                   workspace=None, ct_out=None, stream=None):

@@ -399,6 +399,7 @@ struct EncodeArgs {
   int64_t R, Ma, nJ, nIs, i_begin;
   int m, r;
   MacGeom mg;
+  int64_t ld_r, ld_c;      // element (row, col) of W at W[row * ld_r + col * ld_c]
 };
 
 template <int LOGN>
@@ -426,7 +427,7 @@ k_encode_weights(EncodeArgs A, uint2 *__restrict__ wcache, DevParams P, uint32_t
         const int i = e / A.r, j = A.r - 1 - e % A.r;
         const int64_t row = J * A.r + j, col = I * A.m + i;
         if (row < A.R && col < A.Ma) {
-          const uint64_t w = A.W[row * A.Ma + col];
+          const uint64_t w = A.W[row * A.ld_r + col * A.ld_c];
           bad |= (w & ~tmask) != 0;
           const uint64_t wm = w & tmask;
           if (wm < half) {                      // lift(w) = w
@@ -1295,8 +1296,22 @@ static int check_ptrs(std::initializer_list<const void *> ps, const char *who) {
   return HL_OK;
 }
 
+static int encode_weights_impl(const hl_ctx *c, hl_tile tile, const uint64_t *W, int64_t R, int64_t Ma, int64_t ld_r,
+                               int64_t ld_c, int64_t i_begin, int64_t i_end, void *wcache, void *stream);
+
 extern "C" int hl_encode_weights(const hl_ctx *c, hl_tile tile, const uint64_t *W, int64_t R, int64_t Ma,
                                  int64_t i_begin, int64_t i_end, void *wcache, void *stream) {
+  return encode_weights_impl(c, tile, W, R, Ma, Ma, 1, i_begin, i_end, wcache, stream);
+}
+
+extern "C" int hl_encode_weights_strided(const hl_ctx *c, hl_tile tile, const uint64_t *W, int64_t R, int64_t Ma,
+                                         int64_t ld_row, int64_t ld_col, int64_t i_begin, int64_t i_end, void *wcache,
+                                         void *stream) {
+  return encode_weights_impl(c, tile, W, R, Ma, ld_row, ld_col, i_begin, i_end, wcache, stream);
+}
+
+static int encode_weights_impl(const hl_ctx *c, hl_tile tile, const uint64_t *W, int64_t R, int64_t Ma, int64_t ld_r,
+                               int64_t ld_c, int64_t i_begin, int64_t i_end, void *wcache, void *stream) {
   int rc;
   if ((rc = check_ptrs({c, W, wcache}, "hl_encode_weights"))) return rc;
   Geo g;
@@ -1307,7 +1322,7 @@ extern "C" int hl_encode_weights(const hl_ctx *c, hl_tile tile, const uint64_t *
   const MacGeom mg = mac_geom(c, g.nIs, g.nJ, 2 * g.nK);
   if (mg.engine == 2 && mg.nJp != mg.nJ)      // J padded to the 32-J MMA step: zero weight planes
     cudaMemsetAsync(wcache, 0, (size_t)mg.nIp * mg.LN * mg.nJp * 7, st);
-  EncodeArgs A{W, R, Ma, g.nJ, g.nIs, g.i_begin, g.m, g.r, mg};
+  EncodeArgs A{W, R, Ma, g.nJ, g.nIs, g.i_begin, g.m, g.r, mg, ld_r, ld_c};
   dim3 grid((unsigned)((int64_t)mg.nIb * 16 * g.nJ), c->L);
   {
   KTimer kt(c, HL_K_ENCODE, st);
@@ -1453,6 +1468,44 @@ extern "C" int hl_he_linear_batch(const hl_ctx *c, hl_tile tile, int n, const hl
   cudaStreamWaitEvent(sc, e_macs, 0);
   for (auto &e : ev) cudaEventDestroy(e);         // released once the recorded work completes
   return hl_cuda_check("hl_he_linear_batch: launch");
+}
+
+// ---------------------------------------------------------------------------------------
+// Share arithmetic: dst[rows][cols] += src (or src^T, src being [cols][rows]) mod 2^t.  The
+// attention cross terms add shares of (X1 Y0)^T after the transposition of
+// footnote 3.  32x32 tiles through shared memory (coalesced both ways).
+// ---------------------------------------------------------------------------------------
+__global__ void k_share_acc(uint64_t *__restrict__ dst, const uint64_t *__restrict__ src, int64_t rows, int64_t cols,
+                            int transpose, uint64_t tmask) {
+  __shared__ uint64_t tl[32][33];
+  const int64_t r0 = (int64_t)blockIdx.y * 32, c0 = (int64_t)blockIdx.x * 32;
+  const int tx = threadIdx.x, ty = threadIdx.y;           // 32 x 8
+  if (transpose) {
+    for (int k = ty; k < 32; k += 8) {                     // src row = c0 + k (a dst column), src col = r0 + tx
+      const int64_t sr = c0 + k, sc = r0 + tx;
+      tl[k][tx] = (sr < cols && sc < rows) ? src[sr * rows + sc] : 0;
+    }
+    __syncthreads();
+  }
+  for (int k = ty; k < 32; k += 8) {
+    const int64_t r = r0 + k, cc = c0 + tx;
+    if (r < rows && cc < cols) {
+      const uint64_t v = transpose ? tl[tx][k] : src[r * cols + cc];
+      dst[r * cols + cc] = (dst[r * cols + cc] + v) & tmask;
+    }
+  }
+}
+
+extern "C" int hl_share_accumulate(const hl_ctx *c, uint64_t *dst, const uint64_t *src, int64_t rows, int64_t cols,
+                                   int transpose, void *stream) {
+  int rc;
+  if ((rc = check_ptrs({c, dst, src}, "hl_share_accumulate"))) return rc;
+  if (rows <= 0 || cols <= 0) return hl_fail(HL_EINVAL, "hl_share_accumulate: rows, cols must be positive");
+  const uint64_t tmask = c->log2_t >= 64 ? ~0ull : ((1ull << c->log2_t) - 1);
+  KTimer kt(c, HL_K_OTHER, (cudaStream_t)stream);
+  k_share_acc<<<dim3((unsigned)((cols + 31) / 32), (unsigned)((rows + 31) / 32)), dim3(32, 8), 0,
+                (cudaStream_t)stream>>>(dst, src, rows, cols, transpose ? 1 : 0, tmask);
+  return hl_cuda_check("hl_share_accumulate: launch");
 }
 
 // ---------------------------------------------------------------------------------------

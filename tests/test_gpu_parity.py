@@ -399,3 +399,46 @@ def test_fc_protocol_end_to_end(hl, ctx4096):
     got = (share_c + hl.to_host(share).reshape(Nb, Ma)) & np.uint64((1 << 37) - 1)
     want = (ref.matmul_mod_t(X, W) + b[None, :]) & np.uint64((1 << 37) - 1)
     assert np.array_equal(got, want)
+
+
+# ------------------------------------------------------------------------- attention (row f2)
+@pytest.mark.parametrize("n,d,n2", [(24, 20, 24), (128, 64, 128)])
+def test_attention_cross_terms_vs_oracle(hl, ctx8192, n, d, n2):
+    """Server side of Z = X.Y with both inputs shared: the responses and the
+    server share equal the oracle's bit for bit, and with the client's decryptions plus its local
+    product X0.Y0 the shares reconstruct X.Y mod 2^37 (N=8192, L=3; (128, 64, 128) = one BERT
+    head's Q K^T)."""
+    from paper_2305_18396_b200 import attention
+    ctx = ctx8192
+    P = _P(ctx)
+    tile = (32, 16, 16)
+    X0, X1 = synth.activations(921, n, d), synth.activations(922, n, d)
+    Y0, Y1 = synth.activations(923, d, n2), synth.activations(924, d, n2)
+    seeds = (931, 932, 933, 934, 935, 936)          # (key, enc, mask) of term 1, then of term 2
+    sk1, sk2 = ref.keygen(P, seeds[0]), ref.keygen(P, seeds[3])
+    ct1 = ref.encrypt(P, tile, sk1, np.ascontiguousarray(Y0.T), seeds[1])
+    ct2 = ref.encrypt(P, tile, sk2, X0, seeds[4])
+    m1, m2, z1 = attention.server_cross_product(ctx, tile, hl.to_device(X1), hl.to_device(Y1), hl.to_device(ct1),
+                                                hl.to_device(ct2), (seeds[2], seeds[5]))
+    _sync()
+    Z0, Z1 = ref.attention_protocol(P, tile, X0, X1, Y0, Y1, seeds)
+    assert np.array_equal(hl.to_host(z1).reshape(n, n2), Z1)
+    c1 = ctx.decrypt_share(sk1, tile, hl.to_host(m1), n, n2, True)        # [n2][n]
+    c2 = ctx.decrypt_share(sk2, tile, hl.to_host(m2), n2, n, True)        # [n][n2]
+    tm = np.uint64((1 << 37) - 1)
+    z0 = (c1.T + c2 + ref.matmul_mod_t(X0, Y0)) & tm
+    assert np.array_equal(z0, Z0)
+    assert np.array_equal((z0 + hl.to_host(z1).reshape(n, n2)) & tm, ref.matmul_mod_t((X0 + X1) & tm, (Y0 + Y1) & tm))
+
+
+def test_share_accumulate_transpose(hl, ctx4096):
+    """hl_share_accumulate: dst += src^T (and src) mod 2^37 on ragged 32x32 tiles."""
+    ctx = ctx4096
+    a = synth.activations(941, 45, 70)
+    b = synth.activations(942, 70, 45)
+    c = synth.activations(943, 45, 70)
+    d = hl.to_device(a)
+    ctx.share_accumulate(d, hl.to_device(b), 45, 70, transpose=True)
+    ctx.share_accumulate(d, hl.to_device(c), 45, 70)
+    _sync()
+    assert np.array_equal(hl.to_host(d).reshape(45, 70), (a + b.T + c) & np.uint64((1 << 37) - 1))
