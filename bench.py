@@ -152,7 +152,10 @@ def run_ours(args, rank, world, local_rank):
         X = synth.activations(synth.seed_for(block, mi, "x"), mm.Nb, mm.R)
         W = synth.weights(synth.seed_for(block, mi, "w"), mm.R, mm.Ma)
         sk = ctx.keygen(synth.seed_for(block, mi, "key"))
-        ct_host = ctx.encrypt(sk, tile, X, synth.seed_for(block, mi, "enc"))
+        s_hat = ctx.sk_prepare(sk, dev)
+        dX = hl.to_device(X, dev)
+        ct_dev = ctx.encrypt_device(s_hat, tile, dX, synth.seed_for(block, mi, "enc"))   # row f3, == encrypt()
+        ct_host = hl.to_host(ct_dev)
         dW = hl.to_device(W, dev)
         torch.cuda.synchronize()
         t0 = time.perf_counter()
@@ -160,7 +163,7 @@ def run_ours(args, rank, world, local_rank):
         torch.cuda.synchronize()
         t_enc += time.perf_counter() - t0
         del dW
-        mats.append(dict(mm=mm, lay=lay, wc=wc, ct=hl.to_device(ct_host, dev), i0=i0, i1=i1, nI_full=nI_full,
+        mats.append(dict(mm=mm, lay=lay, wc=wc, ct=ct_dev, i0=i0, i1=i1, nI_full=nI_full, s_hat=s_hat, dX=dX,
                          ct_host=torch.from_numpy(ct_host.view(np.int64).reshape(-1)).pin_memory(),
                          seed=synth.seed_for(block, mi, "mask")))
     ws_words = max(m["lay"].workspace_bytes // 8 for m in mats)
@@ -265,6 +268,40 @@ def run_ours(args, rank, world, local_rank):
                            "4 products of the block, int8 tensor cores (15 limb MMAs per 32-K step)",
                    "ms_per_block": round(fc_ms, 4), "plaintext_macs": fc_macs,
                    "gmacs_per_s": round(fc_macs / (fc_ms * 1e-3) / 1e9, 1)}
+
+    # ---------------- row f3: the client side of the block on the GPU -- encryption of the four
+    # inputs (pi_B + secret-key BFV) and decryption of the four compressed responses
+    # (PAPER.md:101, 154); CUDA events, device-resident buffers
+    cli_info = None
+    if not shard:
+        cts = [torch.empty_like(m["ct"]) for m in mats]
+        shc = [torch.empty(m["lay"].share_words, dtype=torch.int64, device=dev) for m in mats]
+
+        def enc_step():
+            for m, ct in zip(mats, cts):
+                ctx.encrypt_device(m["s_hat"], tile, m["dX"], synth.seed_for(block, 0, "enc") + 99, ct_in=ct,
+                                   stream=stream)
+
+        def dec_step():
+            for m, sh in zip(mats, shc):
+                ctx.decrypt_share_device(m["s_hat"], tile, m["masked"], m["mm"].Ma, m["mm"].Nb, share=sh,
+                                         stream=stream)
+        enc_step(); dec_step()
+        torch.cuda.synchronize()
+        nrep = max(2, min(args.steps, 10))
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
+        ev[0].record(stream)
+        for _ in range(nrep):
+            enc_step()
+        ev[1].record(stream)
+        for _ in range(nrep):
+            dec_step()
+        ev[2].record(stream)
+        torch.cuda.synchronize()
+        cli_info = {"what": "client side of the block on the GPU (row f3): encrypt the 4 inputs (2688 ciphertexts), "
+                            "decrypt the 4 compressed responses (1728), bit-identical to the host client / oracle",
+                    "encrypt_ms_per_block": round(ev[0].elapsed_time(ev[1]) / nrep, 3),
+                    "decrypt_ms_per_block": round(ev[1].elapsed_time(ev[2]) / nrep, 3)}
 
     # ---------------- row f2: the server side of one BERT-base block's attention
     # cross terms, 12 heads x (Q K^T: 128x64 . 64x128, A V: 128x128 . 128x64), both inputs shared;
@@ -415,6 +452,8 @@ def run_ours(args, rank, world, local_rank):
         line["fc_local_share"] = fc_info
     if att_info:
         line["attention_cross_terms"] = att_info
+    if cli_info:
+        line["client_gpu"] = cli_info
     if world == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = oracle_baseline(cfg, tile, args.cpu_itiles)
     return line

@@ -134,6 +134,22 @@ int hl_encrypt(const hl_ctx *ctx, const int8_t *sk, hl_tile tile, const uint64_t
 int hl_decrypt_share(const hl_ctx *ctx, const int8_t *sk, hl_tile tile, const uint64_t *ct_masked,
                      int compress, int64_t Ma, int64_t Nb, uint64_t *share_client);
 
+/* ---- client side on the GPU (device memory) ------------------------ */
+
+/* NTT(s) per prime (slot order, device [L][N]) of the ternary secret sk (host int8[N]); the
+ * device client calls take it instead of sk.  Synchronises `stream`.  HL_ERANGE if not ternary. */
+int hl_sk_prepare(const hl_ctx *ctx, const int8_t *sk, uint64_t *s_hat, void *stream);
+
+/* hl_encrypt on the GPU, bit-identical: X device [Nb][R] (< 2^log2_t, HL_ERANGE otherwise; the
+ * check synchronises `stream`), ct_in device [nJ][nK][2][L][N]. */
+int hl_encrypt_device(const hl_ctx *ctx, const uint64_t *s_hat, hl_tile tile, const uint64_t *X, int64_t Nb,
+                      int64_t R, uint64_t seed, uint64_t *ct_in, void *stream);
+
+/* hl_decrypt_share of a COMPRESSED response on the GPU, bit-identical (RNS rounding, see
+ * client_dev.cuh): ct_masked device (whole problem), share_client device [Nb][Ma]. */
+int hl_decrypt_share_device(const hl_ctx *ctx, const uint64_t *s_hat, hl_tile tile, const uint64_t *ct_masked,
+                            int64_t Ma, int64_t Nb, uint64_t *share_client, void *stream);
+
 /* ---- server side (device memory, stream-ordered) ----------------------------------------- */
 
 /* Alg. 1 step 1 for the server + the NTT of PAPER.md:156 fn: pi_A of every

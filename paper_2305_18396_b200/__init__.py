@@ -32,7 +32,8 @@ EXPORTS = ("hl_last_error", "hl_ctx_create", "hl_ctx_destroy", "hl_ctx_params", 
            "hl_keygen", "hl_encrypt", "hl_decrypt_share", "hl_encode_weights", "hl_he_matmul",
            "hl_mask_and_share", "hl_he_matmul_share", "hl_he_linear_batch", "hl_he_linear_host", "hl_poly_mul",
            "hl_ntt_roundtrip", "hl_timing_enable", "hl_timing_read", "hl_fc_layout", "hl_fc_encode_weights",
-           "hl_fc_local_share", "hl_encode_weights_strided", "hl_share_accumulate")
+           "hl_fc_local_share", "hl_encode_weights_strided", "hl_share_accumulate", "hl_sk_prepare",
+           "hl_encrypt_device", "hl_decrypt_share_device")
 KERNELS = ("ntt_fwd", "mac", "intt_mask", "intt", "mask", "encode", "other", "fc")   # HL_K_* order
 
 
@@ -112,6 +113,9 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
         "hl_fc_layout": [vp, i64, i64, i64, ctypes.POINTER(i64), ctypes.POINTER(i64)],
         "hl_encode_weights_strided": [vp, Tile, vp, i64, i64, i64, i64, i64, i64, vp, vp],
         "hl_share_accumulate": [vp, vp, vp, i64, i64, i32, vp],
+        "hl_sk_prepare": [vp, vp, vp, vp],
+        "hl_encrypt_device": [vp, vp, Tile, vp, i64, i64, u64, vp, vp],
+        "hl_decrypt_share_device": [vp, vp, Tile, vp, i64, i64, vp, vp],
         "hl_fc_encode_weights": [vp, vp, i64, i64, vp, vp],
         "hl_fc_local_share": [vp, vp, vp, vp, i64, i64, i64, vp, vp, vp],
         "hl_timing_read": [vp, vp, vp],
@@ -229,6 +233,33 @@ class Context:
         _check(_lib.hl_decrypt_share(self._h, _hptr(np.ascontiguousarray(sk), np.int8), _tile(tile),
                                      ct_masked.ctypes.data, int(bool(compress)), Ma, Nb, out.ctypes.data))
         return out
+
+    # ---------------------------------------------------------------- client on the GPU (row f3)
+    def sk_prepare(self, sk: np.ndarray, device=None, stream=None):
+        """NTT(s) per prime on the device (the device client's key form)."""
+        import torch
+        dev = device if device is not None else torch.device("cuda", self.device)
+        s_hat = _dev_empty(self.L * self.N, dev)
+        _check(_lib.hl_sk_prepare(self._h, _hptr(np.ascontiguousarray(sk), np.int8), _dptr(s_hat), _stream(stream)))
+        return s_hat
+
+    def encrypt_device(self, s_hat, tile, X, seed: int, ct_in=None, stream=None):
+        """X: CUDA tensor [Nb][R] (< 2^t) -> ct_in CUDA tensor [nJ][nK][2][L][N] (== encrypt())."""
+        Nb, R = X.shape
+        lay = self.layout(tile, 1, R, Nb)
+        if ct_in is None:
+            ct_in = _dev_empty(lay.ct_in_words, X.device)
+        _check(_lib.hl_encrypt_device(self._h, _dptr(s_hat), _tile(tile), _dptr(X), Nb, R, seed, _dptr(ct_in),
+                                      _stream(stream)))
+        return ct_in
+
+    def decrypt_share_device(self, s_hat, tile, ct_masked, Ma: int, Nb: int, share=None, stream=None):
+        """Compressed response (CUDA tensor) -> client share [Nb][Ma] (== decrypt_share())."""
+        if share is None:
+            share = _dev_empty(Nb * Ma, ct_masked.device)
+        _check(_lib.hl_decrypt_share_device(self._h, _dptr(s_hat), _tile(tile), _dptr(ct_masked), Ma, Nb,
+                                            _dptr(share), _stream(stream)))
+        return share
 
     # ---------------------------------------------------------------- server (device memory)
     def encode_weights(self, tile, W, i_begin: int = 0, i_end: int = -1, wcache=None, stream=None):

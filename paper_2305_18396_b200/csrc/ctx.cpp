@@ -185,6 +185,11 @@ extern "C" int hl_ctx_create(uint32_t N, uint32_t L, uint32_t log2_t, const uint
     pc.r64 = (uint64_t)(((hl_u128)1 << 64) % p);
     pc.r64_sh = h_shoup(pc.r64, p);
     pc.c40 = h_powmod(2, 40, p); pc.c40_sh = h_shoup(pc.c40, p);
+    {   // RNS decryption constants: theta_l = t * inv_l / p_l = I + F / 2^64  (inv_l = (q/p_l)^-1 mod p_l)
+      const hl_u128 ti = ((hl_u128)1 << log2_t) * c->Ml_inv[l];
+      pc.dec_I = (uint64_t)(ti / p);
+      pc.dec_F = (uint64_t)((((hl_u128)(uint64_t)(ti % p)) << 64) / p);
+    }
     pc.c72 = h_powmod(2, 72, p); pc.c72_sh = h_shoup(pc.c72, p);
     pc.delta = c->delta_mod[l]; pc.delta_sh = h_shoup(pc.delta, p);
     pc.ninv = h_powmod(N, p - 2, p); pc.ninv_sh = h_shoup(pc.ninv, p);
@@ -213,6 +218,11 @@ extern "C" int hl_ctx_create(uint32_t N, uint32_t L, uint32_t log2_t, const uint
     return rc ? rc : hl_fail(HL_ECUDA, "hl_ctx_create: device allocation failed");
   }
   cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, device);
+  if (cudaMalloc((void **)&c->d_cdt, c->cdt.size() * 8) != cudaSuccess ||
+      cudaMemcpy(c->d_cdt, c->cdt.data(), c->cdt.size() * 8, cudaMemcpyHostToDevice) != cudaSuccess) {
+    cudaFree(c->d_tw); cudaFree(c->d_flags); delete c;
+    return hl_cuda_check("hl_ctx_create: CDT table");
+  }
   {
     // the batch pipeline's streams: MACs at the highest priority so that their persistent CTAs
     // are placed before queued NTT blocks of the concurrent low-priority stream
@@ -289,6 +299,7 @@ extern "C" int hl_ctx_destroy(hl_ctx *c) {
   if (c->mac_stream) cudaStreamDestroy((cudaStream_t)c->mac_stream);
   if (c->d_tw) cudaFree(c->d_tw);
   if (c->d_flags) cudaFree(c->d_flags);
+  if (c->d_cdt) cudaFree(c->d_cdt);
   delete c;
   return HL_OK;
 }

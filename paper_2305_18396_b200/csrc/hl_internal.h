@@ -22,6 +22,7 @@ struct PrimeConsts {
   uint64_t r64;       // 2^64 mod p
   uint64_t r64_sh;    // floor(r64 * 2^64 / p)        (Shoup companion)
   uint64_t c40, c40_sh, c72, c72_sh;   // 2^40, 2^72 mod p (tensor-core MAC recombination) + Shoup
+  uint64_t dec_I, dec_F;   // theta_l = t ((q/p)^-1 mod p) / p = dec_I + dec_F 2^-64 (RNS decryption, row f3)
   uint64_t delta;     // Delta mod p, Delta = floor(q / t)
   uint64_t delta_sh;  // Shoup companion of delta
   uint64_t ninv;      // N^-1 mod p
@@ -67,6 +68,7 @@ struct hl_ctx {
   DevParams dp;
   void *d_tw = nullptr;               // device allocation holding tw_fwd + tw_inv
   uint32_t *d_flags = nullptr;        // device scratch: [0] range flag, [1] max |w| (as u32 bits)
+  uint64_t *d_cdt = nullptr;          // device copy of the CDT table (device encryption, row f3)
   void *aux_stream = nullptr;         // cudaStream_t (non-blocking, lowest priority): hl_he_linear_batch's NTT stages
   void *mac_stream = nullptr;         // cudaStream_t (non-blocking, highest priority): hl_he_linear_batch's MACs
   TimingState *timing = nullptr;      // owned; mutable through const hl_ctx*

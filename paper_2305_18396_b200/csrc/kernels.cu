@@ -1067,6 +1067,7 @@ k_mac_f64(MacArgs A, DevParams P) {
 
 #include "mac_tc.cuh"
 #include "fc.cuh"
+#include "client_dev.cuh"
 
 // pointwise product in the NTT domain (diagnostics only)
 __global__ void k_pointwise(const uint64_t *a, const uint64_t *b, uint64_t *out, int64_t n, DevParams P) {
@@ -1468,6 +1469,84 @@ extern "C" int hl_he_linear_batch(const hl_ctx *c, hl_tile tile, int n, const hl
   cudaStreamWaitEvent(sc, e_macs, 0);
   for (auto &e : ev) cudaEventDestroy(e);         // released once the recorded work completes
   return hl_cuda_check("hl_he_linear_batch: launch");
+}
+
+// ---------------------------------------------------------------------------------------
+// the client side on the GPU (client_dev.cuh)
+// ---------------------------------------------------------------------------------------
+extern "C" int hl_sk_prepare(const hl_ctx *c, const int8_t *sk, uint64_t *s_hat, void *stream) {
+  int rc;
+  if ((rc = check_ptrs({c, sk, s_hat}, "hl_sk_prepare"))) return rc;
+  std::vector<uint64_t> res((size_t)c->L * c->N);
+  for (uint32_t i = 0; i < c->N; i++)
+    if (sk[i] < -1 || sk[i] > 1) return hl_fail(HL_ERANGE, "hl_sk_prepare: secret key must be ternary");
+  for (uint32_t l = 0; l < c->L; l++)
+    for (uint32_t i = 0; i < c->N; i++)
+      res[(size_t)l * c->N + i] = sk[i] > 0 ? 1 : (sk[i] < 0 ? c->primes[l] - 1 : 0);
+  cudaStream_t st = (cudaStream_t)stream;
+  if (cudaMemcpyAsync(s_hat, res.data(), res.size() * 8, cudaMemcpyHostToDevice, st) != cudaSuccess)
+    return hl_cuda_check("hl_sk_prepare: upload");
+  fwd_ntt(c, s_hat, s_hat, 1, nullptr, st);            // in place: NTT(s) per prime, slot order
+  if (cudaStreamSynchronize(st) != cudaSuccess) return hl_cuda_check("hl_sk_prepare: sync");
+  return hl_cuda_check("hl_sk_prepare: launch");
+}
+
+extern "C" int hl_encrypt_device(const hl_ctx *c, const uint64_t *s_hat, hl_tile tile, const uint64_t *X, int64_t Nb,
+                                 int64_t R, uint64_t seed, uint64_t *ct_in, void *stream) {
+  int rc;
+  if ((rc = check_ptrs({c, s_hat, X, ct_in}, "hl_encrypt_device"))) return rc;
+  Geo g;
+  if ((rc = hl_geometry(c, tile, 1, R, Nb, 0, -1, &g))) return rc;
+  cudaStream_t st = (cudaStream_t)stream;
+  cudaMemsetAsync(c->d_flags, 0, 8, st);
+  EncArgs E{X, Nb, R, g.nK, g.m, g.r, g.n, __builtin_ctz((unsigned)g.m), __builtin_ctz((unsigned)g.r), seed, s_hat};
+  const unsigned nct = (unsigned)(g.nJ * g.nK);
+  {
+    KTimer kt(c, HL_K_OTHER, st);
+    if (c->N == 4096) {
+      constexpr size_t sm = ntt_smem<12>() + 4096;
+      static bool init = false;
+      if (!init) { set_smem(k_encrypt<12>, sm); init = true; }
+      k_encrypt<12><<<nct, Geom<12>::NT, sm, st>>>(E, ct_in, c->dp, c->d_cdt, c->d_flags);
+    } else {
+      constexpr size_t sm = ntt_smem<13>() + 8192;
+      static bool init = false;
+      if (!init) { set_smem(k_encrypt<13>, sm); init = true; }
+      k_encrypt<13><<<nct, Geom<13>::NT, sm, st>>>(E, ct_in, c->dp, c->d_cdt, c->d_flags);
+    }
+  }
+  if ((rc = hl_cuda_check("hl_encrypt_device: launch"))) return rc;
+  uint32_t flags[2];
+  if (cudaMemcpyAsync(flags, c->d_flags, 8, cudaMemcpyDeviceToHost, st) != cudaSuccess ||
+      cudaStreamSynchronize(st) != cudaSuccess)
+    return hl_cuda_check("hl_encrypt_device: status readback");
+  if (flags[0]) return hl_fail(HL_ERANGE, "hl_encrypt_device: X value >= 2^log2_t");
+  return HL_OK;
+}
+
+extern "C" int hl_decrypt_share_device(const hl_ctx *c, const uint64_t *s_hat, hl_tile tile, const uint64_t *ct_masked,
+                                       int64_t Ma, int64_t Nb, uint64_t *share_client, void *stream) {
+  int rc;
+  if ((rc = check_ptrs({c, s_hat, ct_masked, share_client}, "hl_decrypt_share_device"))) return rc;
+  Geo g;
+  if ((rc = hl_geometry(c, tile, Ma, 1, Nb, 0, -1, &g))) return rc;
+  cudaStream_t st = (cudaStream_t)stream;
+  DecArgs D{Ma, Nb, g.nK, g.m, g.r, g.n, __builtin_ctz((unsigned)g.m), __builtin_ctz((unsigned)g.r), s_hat};
+  const size_t res = (size_t)c->L * g.m * g.n * 8;
+  const unsigned nout = (unsigned)(g.nI * g.nK);
+  KTimer kt(c, HL_K_OTHER, st);
+  if (c->N == 4096) {
+    const size_t sm = ntt_smem<12>() + res;
+    static bool init = false;
+    if (!init) { set_smem(k_decrypt<12>, 232448); init = true; }
+    k_decrypt<12><<<nout, Geom<12>::NT, sm, st>>>(ct_masked, share_client, D, c->dp);
+  } else {
+    const size_t sm = ntt_smem<13>() + res;
+    static bool init = false;
+    if (!init) { set_smem(k_decrypt<13>, 232448); init = true; }
+    k_decrypt<13><<<nout, Geom<13>::NT, sm, st>>>(ct_masked, share_client, D, c->dp);
+  }
+  return hl_cuda_check("hl_decrypt_share_device: launch");
 }
 
 // ---------------------------------------------------------------------------------------

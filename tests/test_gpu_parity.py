@@ -442,3 +442,30 @@ def test_share_accumulate_transpose(hl, ctx4096):
     ctx.share_accumulate(d, hl.to_device(c), 45, 70)
     _sync()
     assert np.array_equal(hl.to_host(d).reshape(45, 70), (a + b.T + c) & np.uint64((1 << 37) - 1))
+
+
+# ------------------------------------------------------------------------- client on the GPU (row f3)
+@pytest.mark.parametrize("N,shape,tile", [(4096, (8, 64, 64), (16, 32, 8)), (4096, (40, 24, 40), (16, 8, 32)),
+                                          (8192, (32, 48, 40), (32, 16, 16)), (4096, (3, 5, 7), (1, 1, 1))])
+def test_device_client_encrypt_decrypt(hl, ctx4096, ctx8192, N, shape, tile):
+    """hl_encrypt_device == the oracle's encrypt (and the host client), bit for bit; the GPU server
+    then runs, and hl_decrypt_share_device (RNS rounding) == the oracle's decrypt (exact CRT)."""
+    ctx = ctx4096 if N == 4096 else ctx8192
+    P = _P(ctx)
+    Nb, R, Ma = shape
+    X = synth.activations(951 + N, Nb, R)
+    W = synth.weights(952 + N, R, Ma)
+    sk = ref.keygen(P, 953)
+    s_hat = ctx.sk_prepare(sk)
+    ct_dev = ctx.encrypt_device(s_hat, tile, hl.to_device(X), 954)
+    _sync()
+    exp = ref.encrypt(P, tile, sk, X, 954)
+    assert np.array_equal(hl.to_host(ct_dev).reshape(exp.shape), exp)
+    wc = ctx.encode_weights(tile, hl.to_device(W))
+    masked, share_s = ctx.he_matmul_share(tile, wc, Ma, R, Nb, ct_dev, seed=955)
+    share_c = ctx.decrypt_share_device(s_hat, tile, masked, Ma, Nb)
+    _sync()
+    exp_c = ref.decrypt_share(P, tile, sk, hl.to_host(masked), Ma, Nb, True)
+    assert np.array_equal(hl.to_host(share_c).reshape(Nb, Ma), exp_c)
+    assert np.array_equal((exp_c + hl.to_host(share_s).reshape(Nb, Ma)) & np.uint64((1 << 37) - 1),
+                          ref.matmul_mod_t(X, W))
