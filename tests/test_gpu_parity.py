@@ -82,6 +82,9 @@ CASES = [
     (4096, (64, 48, 100), (4, 8, 16)),     # nC = 8, ragged I tail (nI = 25)
     (4096, (3, 5, 7), (1, 1, 1)),          # degenerate 1x1x1 tile, nC = 6
     (8192, (32, 48, 40), (32, 16, 16)),    # c4 parameters (N=8192, L=3) at small size
+    (4096, (256, 40, 50), (16, 8, 32)),    # nC = 16: the MAC's 16-column groups (CW = 16)
+    (4096, (520, 24, 40), (16, 8, 32)),    # nC = 34 -> CW = 2, 17 column groups, ragged K tail
+    (8192, (288, 48, 40), (32, 16, 16)),   # c4 tile, nC = 36 (CW = 4, 9 groups), N=8192 L=3
 ]
 
 
@@ -469,3 +472,65 @@ def test_device_client_encrypt_decrypt(hl, ctx4096, ctx8192, N, shape, tile):
     assert np.array_equal(hl.to_host(share_c).reshape(Nb, Ma), exp_c)
     assert np.array_equal((exp_c + hl.to_host(share_s).reshape(Nb, Ma)) & np.uint64((1 << 37) - 1),
                           ref.matmul_mod_t(X, W))
+
+
+
+def test_bert_base_c3_shape_sampled(hl, ctx4096):
+    """Config c3's product shape (8 sequences: Nb = 1024 -> nC = 64, four 16-column groups) for
+    W_o (768 x 768) at full size in the bench's launch configuration: sampled output ciphertexts
+    bit-exact vs the oracle's scalar NTT path, and the whole product's reconstruction vs X.W."""
+    ctx = ctx4096
+    cfg = synth.CONFIGS["c3"]
+    P = _P(ctx)
+    tile = cfg.tile
+    mm = cfg.matmuls[1]
+    assert (mm.Nb, mm.R, mm.Ma) == (1024, 768, 768)
+    X = synth.activations(961, mm.Nb, mm.R)
+    W = synth.weights(962, mm.R, mm.Ma)
+    sk = ctx.keygen(963)
+    s_hat = ctx.sk_prepare(sk)
+    ct_in = ctx.encrypt_device(s_hat, tile, hl.to_device(X), 964)
+    wc = ctx.encode_weights(tile, hl.to_device(W))
+    masked, share = ctx.he_linear_batch(tile, [dict(wcache=wc, Ma=mm.Ma, R=mm.R, Nb=mm.Nb, ct_in=ct_in, seed=965)])[0]
+    share_c = ctx.decrypt_share_device(s_hat, tile, masked, mm.Ma, mm.Nb)
+    _sync()
+    nI, nJ, nK = ref.tile_counts(tile, mm.Ma, mm.R, mm.Nb)
+    mh = hl.to_host(masked).reshape(nI, nK, -1)
+    tiles = [(0, 0), (nI - 1, nK - 1), (13, 17), (47, 31)]
+    exp_ct = ref.he_matmul_ntt_tiles(P, tile, W, hl.to_host(ct_in).reshape(nJ, nK, 2, P.L, P.N), mm.Nb, tiles)
+    em, _ = ref.mask_tiles(P, tile, exp_ct, nK, tiles, 965, True)
+    for o, (I, K) in enumerate(tiles):
+        assert np.array_equal(mh[I, K], em[o]), (I, K)
+    got = (hl.to_host(share_c).reshape(mm.Nb, mm.Ma) + hl.to_host(share).reshape(mm.Nb, mm.Ma)) & np.uint64((1 << 37) - 1)
+    assert np.array_equal(got, ref.matmul_mod_t(X, W))
+
+
+def test_bert_large_c4_shape_sampled(hl, ctx8192):
+    """Config c4's parameters and product shape (N=8192, L=3, tile (32,16,16); 4 sequences of 512:
+    Nb = 2048 -> nC = 256, sixteen 16-column groups) for W_o (1024 x 1024) at full size: sampled
+    output ciphertexts bit-exact vs the oracle's scalar NTT path, whole-product reconstruction."""
+    ctx = ctx8192
+    cfg = synth.CONFIGS["c4"]
+    P = _P(ctx)
+    tile = cfg.tile
+    mm = cfg.matmuls[1]
+    assert (mm.Nb, mm.R, mm.Ma) == (2048, 1024, 1024) and tile == (32, 16, 16)
+    X = synth.activations(971, mm.Nb, mm.R)
+    W = synth.weights(972, mm.R, mm.Ma)
+    sk = ctx.keygen(973)
+    s_hat = ctx.sk_prepare(sk)
+    ct_in = ctx.encrypt_device(s_hat, tile, hl.to_device(X), 974)
+    wc = ctx.encode_weights(tile, hl.to_device(W))
+    masked, share = ctx.he_linear_batch(tile, [dict(wcache=wc, Ma=mm.Ma, R=mm.R, Nb=mm.Nb, ct_in=ct_in, seed=975)])[0]
+    share_c = ctx.decrypt_share_device(s_hat, tile, masked, mm.Ma, mm.Nb)
+    _sync()
+    nI, nJ, nK = ref.tile_counts(tile, mm.Ma, mm.R, mm.Nb)
+    mh = hl.to_host(masked).reshape(nI, nK, -1)
+    tiles = [(0, 0), (nI - 1, nK - 1), (17, 100)]
+    ct_h = hl.to_host(ct_in).reshape(nJ, nK, 2, P.L, P.N)
+    exp_ct = ref.he_matmul_ntt_tiles(P, tile, W, ct_h, mm.Nb, tiles)
+    em, _ = ref.mask_tiles(P, tile, exp_ct, nK, tiles, 975, True)
+    for o, (I, K) in enumerate(tiles):
+        assert np.array_equal(mh[I, K], em[o]), (I, K)
+    got = (hl.to_host(share_c).reshape(mm.Nb, mm.Ma) + hl.to_host(share).reshape(mm.Nb, mm.Ma)) & np.uint64((1 << 37) - 1)
+    assert np.array_equal(got, ref.matmul_mod_t(X, W))
