@@ -497,3 +497,74 @@ def attention_protocol(P: Params, tile, X0: np.ndarray, X1: np.ndarray, Y0: np.n
         Z0 = (t1["share_client"].T + t2["share_client"] + matmul_mod_t(X0, Y0, P.t_bits)) & tmask
         Z1 = (t1["share_server"].T + t2["share_server"] + matmul_mod_t(X1, Y1, P.t_bits)) & tmask
     return Z0, Z1
+
+
+# ----------------------------------------------------------------------------------------
+# Response re-randomisation (reading C22 of DESIGN.md).  The paper is
+# silent (C13); without it the client, who knows its own c1 = a_J, learns sum_J pi_A(W_IJ) * a_J
+# from the response's c1 and so W (linear algebra).  Standard fix: add a fresh public-key
+# encryption of zero, c' = c + (pk0 u + e1 + F, pk1 u + e2), with u ternary, e1, e2 discrete
+# Gaussian and F a uniform "flooding" term of flood_bits bits (|F| <= 2^(flood_bits-1)) that hides
+# the W-dependent noise as far as the noise budget allows.
+#   pk  = (pk0, pk1) = (-a s + e, a): a from PRF domain 5 (stream l), e from domain 6 (stream 0)
+#   u   = (u64_RR_U[i] mod 3) - 1          domain 7, stream I*nK + K
+#   e1, e2 = CDT(u64_RR_E)                  domain 8, streams 2(I*nK+K) and 2(I*nK+K)+1
+#   F[i] = (u64_RR_F[i] mod 2^fb) - 2^(fb-1)  domain 9, stream I*nK + K  (F = 0 when fb = 0)
+# ----------------------------------------------------------------------------------------
+DOM_PK_A, DOM_PK_E, DOM_RR_U, DOM_RR_E, DOM_RR_F = 5, 6, 7, 8, 9
+
+
+def _cdt_sample(words: np.ndarray) -> np.ndarray:
+    """Reading C8 on given PRF words: sign = u>>63, |e| = min{k : (u & (2^63-1)) < T[k]}."""
+    T = np.array(cdt_table(), dtype=np.uint64)
+    v = words & np.uint64((1 << 63) - 1)
+    mag = np.searchsorted(T, v, side="right").astype(np.int64)
+    return np.where((words >> np.uint64(63)) != 0, -mag, mag)
+
+
+def _to_mod(v: np.ndarray, p: int) -> np.ndarray:
+    return np.array([int(x) % p for x in v], dtype=np.uint64)
+
+
+def pk_gen(P: Params, sk: np.ndarray, seed: int) -> np.ndarray:
+    """Public key pk [2][L][N]: pk1 = a, pk0 = -a*s + e (mod p_l)."""
+    N = P.N
+    e = _cdt_sample(prf_u64(seed, DOM_PK_E, 0, N))
+    pk = np.zeros((2, P.L, N), dtype=np.uint64)
+    for l, p in enumerate(P.primes):
+        u = prf_u64(seed, DOM_PK_A, l, 2 * N)
+        a = np.array([(int(u[2 * i]) + (int(u[2 * i + 1]) << 64)) % p for i in range(N)], dtype=np.uint64)
+        s_l = _to_mod(sk.astype(np.int64), p)
+        as_ = negacyclic_mul(N, p, a, s_l)
+        e_l = _to_mod(e, p)
+        pk[0, l] = np.array([(p - int(x) + int(y)) % p for x, y in zip(as_, e_l)], dtype=np.uint64)
+        pk[1, l] = a
+    return pk
+
+
+def rerandomize(P: Params, tile, pk: np.ndarray, ct_out: np.ndarray, nK: int, seed: int, flood_bits: int,
+                i_begin: int = 0) -> np.ndarray:
+    """c' = c + Enc_pk(0) + (F, 0) for every output ciphertext of ct_out [nI][nK][2][L][N]
+    (coefficient form; global tile index (i_begin + I) nK + K)."""
+    N = P.N
+    out = ct_out.copy()
+    for I in range(ct_out.shape[0]):
+        for K in range(nK):
+            st = (i_begin + I) * nK + K
+            u = (prf_u64(seed, DOM_RR_U, st, N) % np.uint64(3)).astype(np.int64) - 1
+            e1 = _cdt_sample(prf_u64(seed, DOM_RR_E, 2 * st, N))
+            e2 = _cdt_sample(prf_u64(seed, DOM_RR_E, 2 * st + 1, N))
+            if flood_bits > 0:
+                w = prf_u64(seed, DOM_RR_F, st, N) & np.uint64((1 << flood_bits) - 1)
+                F = w.astype(np.int64) - (1 << (flood_bits - 1))
+            else:
+                F = np.zeros(N, dtype=np.int64)
+            for l, p in enumerate(P.primes):
+                u_l = _to_mod(u, p)
+                a0 = negacyclic_mul(N, p, pk[0, l], u_l)
+                a1 = negacyclic_mul(N, p, pk[1, l], u_l)
+                add0 = _to_mod(e1 + F, p)
+                add1 = _to_mod(e2, p)
+                out[I, K, 0, l] = [(int(c) + int(x) + int(y)) % p for c, x, y in zip(out[I, K, 0, l], a0, add0)]
+                out[I, K, 1, l] = [(int(c) + int(x) + int(y)) % p for c, x, y in zip(out[I, K, 1, l], a1, add1)]
+    return out

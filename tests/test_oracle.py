@@ -385,3 +385,51 @@ def test_attention_noise_needs_the_large_modulus(P4096):
     Z0, Z1 = ref.attention_protocol(P4096, tile, X0, X1, Y0, Y1)
     want = ref.matmul_mod_t((X0 + X1) & np.uint64((1 << 37) - 1), (Y0 + Y1) & np.uint64((1 << 37) - 1))
     assert not np.array_equal((Z0 + Z1) & np.uint64((1 << 37) - 1), want)
+
+
+# ----------------------------------------------------------------------------- re-randomisation (row f4)
+def test_rerandomized_response_reconstructs_and_floods(P4096):
+    """Row f4 (reading C22): a fresh public-key encryption of zero plus a flooding term of
+    fb = log2(Delta) - 3 bits keeps decryption exact (shares reconstruct X.W mod 2^37), and the
+    decryption noise of the response is then dominated by the flood (|noise| ~ 2^(fb-1))."""
+    import synth
+    tile, (Nb, R, Ma) = (16, 8, 32), (24, 16, 40)
+    X, W = synth.activations(101, Nb, R), synth.weights(102, R, Ma)
+    sk = ref.keygen(P4096, 103)
+    pk = ref.pk_gen(P4096, sk, 104)
+    ct_in = ref.encrypt(P4096, tile, sk, X, 105)
+    nI, nJ, nK = ref.tile_counts(tile, Ma, R, Nb)
+    fb = int(np.floor(np.log2(float(P4096.delta)))) - 3
+    ct = ref.rerandomize(P4096, tile, pk, ref.he_matmul(P4096, tile, W, ct_in, Nb), nK, 106, fb)
+    masked, share_s = ref.mask_and_share(P4096, tile, ct, Ma, Nb, 106, True)
+    share_c = ref.decrypt_share(P4096, tile, sk, masked, Ma, Nb, True)
+    assert np.array_equal((share_c + share_s) & np.uint64((1 << 37) - 1), ref.matmul_mod_t(X, W))
+    pts, noise = ref.decrypt_full(P4096, sk, ct[0, 0])
+    assert max(abs(int(v)) for v in noise[0]) > 1 << (fb - 3)    # flood-sized, not HE-noise-sized
+
+
+def test_rerandomization_defeats_weight_recovery(P4096):
+    """Without re-randomisation (the paper's Alg. 1 as stated, reading C13) the client recovers W
+    from the response: with nJ = 1, c1_out = pi_A(W) * a in R_q, so NTT(pi_A(W)) = NTT(c1_out)/NTT(a)
+    coefficient-wise.  After re-randomisation the same computation no longer yields pi_A(W)."""
+    import synth
+    tile, (Nb, R, Ma) = (16, 8, 32), (32, 8, 16)          # nI = nJ = nK = 1
+    X, W = synth.activations(111, Nb, R), synth.weights(112, R, Ma)
+    sk = ref.keygen(P4096, 113)
+    ct_in = ref.encrypt(P4096, tile, sk, X, 114)
+    ct_out = ref.he_matmul(P4096, tile, W, ct_in, Nb)
+    pk = ref.pk_gen(P4096, sk, 115)
+    ct_rr = ref.rerandomize(P4096, tile, pk, ct_out, 1, 116, 0)
+    p, psi, N = P4096.primes[0], P4096.psis[0], P4096.N
+    a = ct_in[0, 0, 1, 0]
+    a_hat = ref.ntt(N, p, psi, a)
+    inv = np.array([pow(int(v), p - 2, p) for v in a_hat], dtype=object)
+
+    def recover(c1):
+        c_hat = ref.ntt(N, p, psi, c1)
+        return ref.intt(N, p, psi, np.array([(int(x) * int(y)) % p for x, y in zip(c_hat, inv)], dtype=np.uint64))
+
+    wpoly = ref.encode_A([[int(W[j, i]) for j in range(R)] for i in range(Ma)], N, tile[1])
+    lift = np.array([(int(v) - (1 << 37)) % p if int(v) >= (1 << 36) else int(v) for v in wpoly], dtype=np.uint64)
+    assert np.array_equal(recover(ct_out[0, 0, 1, 0]), lift)            # the leak: pi_A(W) mod p, centered lift
+    assert not np.array_equal(recover(ct_rr[0, 0, 1, 0]), lift)         # closed
