@@ -303,6 +303,29 @@ def run_ours(args, rank, world, local_rank):
                     "encrypt_ms_per_block": round(ev[0].elapsed_time(ev[1]) / nrep, 3),
                     "decrypt_ms_per_block": round(ev[1].elapsed_time(ev[2]) / nrep, 3)}
 
+    # ---------------- row f4 (reading C22): the block with re-randomised, flooded responses
+    # (fresh pk-encryption of zero + 2^57 flood per response), sequential calls
+    rr_info = None
+    if not shard:
+        sk_rr = ctx.keygen(synth.seed_for(block, 0, "key") + 11)
+        pk_hat = ctx.pk_prepare(ctx.pk_gen(sk_rr, synth.seed_for(block, 0, "key") + 12))
+
+        def rr_step():
+            for m in mats:
+                mm = m["mm"]
+                ctx.he_matmul_share_rr(tile, m["wc"], mm.Ma, mm.R, mm.Nb, m["ct"], m["seed"], pk_hat, 58, stream=stream)
+        rr_step()
+        torch.cuda.synchronize()
+        nrep = max(2, min(args.steps, 10))
+        r0, r1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        r0.record(stream)
+        for _ in range(nrep):
+            rr_step()
+        r1.record(stream)
+        torch.cuda.synchronize()
+        rr_info = {"what": "the block's 4 products with re-randomised responses (row f4: + Enc_pk(0), 58-bit flood), "
+                           "sequential hl_he_matmul_share_rr", "ms_per_block": round(r0.elapsed_time(r1) / nrep, 4)}
+
     # ---------------- row f2: the server side of one BERT-base block's attention
     # cross terms, 12 heads x (Q K^T: 128x64 . 64x128, A V: 128x128 . 128x64), both inputs shared;
     # N=8192, L=3 (uniform shares as server operands need q ~ 2^150), tile (32, 16, 16).
@@ -454,6 +477,8 @@ def run_ours(args, rank, world, local_rank):
         line["attention_cross_terms"] = att_info
     if cli_info:
         line["client_gpu"] = cli_info
+    if rr_info:
+        line["rerandomized"] = rr_info
     if world == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = oracle_baseline(cfg, tile, args.cpu_itiles)
     return line

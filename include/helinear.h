@@ -150,6 +150,29 @@ int hl_encrypt_device(const hl_ctx *ctx, const uint64_t *s_hat, hl_tile tile, co
 int hl_decrypt_share_device(const hl_ctx *ctx, const uint64_t *s_hat, hl_tile tile, const uint64_t *ct_masked,
                             int64_t Ma, int64_t Nb, uint64_t *share_client, void *stream);
 
+/* ---- re-randomised responses (reading C22 of DESIGN.md) ---------- */
+
+/* Client: public key pk = (pk0, pk1) = (-a s + e, a), host [2][L][N] coefficient form; a from
+ * PRF domain 5 (stream l), e from domain 6 (stream 0). */
+int hl_pk_gen(const hl_ctx *ctx, const int8_t *sk, uint64_t seed, uint64_t *pk);
+
+/* Server: NTT(pk) per prime (device [2][L][N], slot order) from the host pk.  Synchronises. */
+int hl_pk_prepare(const hl_ctx *ctx, const uint64_t *pk, uint64_t *pk_hat, void *stream);
+
+/* hl_he_matmul_share (compressed) with every output ciphertext re-randomised before masking:
+ *   c0 += pk0*u + e1 + F,  c1 += pk1*u + e2
+ * u ternary (domain 7, stream I*nK+K), e1, e2 CDT (domain 8, streams 2(I*nK+K) and +1),
+ * F[i] = (u64_RR_F[i] mod 2^flood_bits) - 2^(flood_bits-1) (domain 9; none for flood_bits = 0),
+ * all from `seed` (the mask seed).  Closes the weight leak of reading C13 (the client no longer
+ * sees sum_J pi_A(W) * a_J in c1); flooding hides the W-dependent noise up to the budget.  The
+ * caller keeps the HE noise + 2^(flood_bits-1) below Delta/2 (HL_ERANGE unless
+ * 0 <= flood_bits <= min(62, log2(Delta) - 1): F comes from one PRF word per coefficient).
+ * rr_ws: device scratch of nI_shard*nK*L*N words. */
+int hl_he_matmul_share_rr(const hl_ctx *ctx, hl_tile tile, const void *wcache, int64_t Ma, int64_t R,
+                          int64_t Nb, int64_t i_begin, int64_t i_end, const uint64_t *ct_in, void *workspace,
+                          uint64_t *ct_out_ntt, const uint64_t *pk_hat, int flood_bits, uint64_t *rr_ws,
+                          uint64_t seed, uint64_t *ct_masked, uint64_t *share_server, void *stream);
+
 /* ---- server side (device memory, stream-ordered) ----------------------------------------- */
 
 /* Alg. 1 step 1 for the server + the NTT of PAPER.md:156 fn: pi_A of every

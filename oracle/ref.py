@@ -509,7 +509,7 @@ def attention_protocol(P: Params, tile, X0: np.ndarray, X1: np.ndarray, Y0: np.n
 #   pk  = (pk0, pk1) = (-a s + e, a): a from PRF domain 5 (stream l), e from domain 6 (stream 0)
 #   u   = (u64_RR_U[i] mod 3) - 1          domain 7, stream I*nK + K
 #   e1, e2 = CDT(u64_RR_E)                  domain 8, streams 2(I*nK+K) and 2(I*nK+K)+1
-#   F[i] = (u64_RR_F[i] mod 2^fb) - 2^(fb-1)  domain 9, stream I*nK + K  (F = 0 when fb = 0)
+#   F[i] = (u64_RR_F[i] mod 2^fb) - 2^(fb-1)  domain 9, stream I*nK + K  (F = 0 when fb = 0; fb <= 62)
 # ----------------------------------------------------------------------------------------
 DOM_PK_A, DOM_PK_E, DOM_RR_U, DOM_RR_E, DOM_RR_F = 5, 6, 7, 8, 9
 

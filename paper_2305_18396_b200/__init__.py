@@ -33,7 +33,7 @@ EXPORTS = ("hl_last_error", "hl_ctx_create", "hl_ctx_destroy", "hl_ctx_params", 
            "hl_mask_and_share", "hl_he_matmul_share", "hl_he_linear_batch", "hl_he_linear_host", "hl_poly_mul",
            "hl_ntt_roundtrip", "hl_timing_enable", "hl_timing_read", "hl_fc_layout", "hl_fc_encode_weights",
            "hl_fc_local_share", "hl_encode_weights_strided", "hl_share_accumulate", "hl_sk_prepare",
-           "hl_encrypt_device", "hl_decrypt_share_device")
+           "hl_encrypt_device", "hl_decrypt_share_device", "hl_pk_gen", "hl_pk_prepare", "hl_he_matmul_share_rr")
 KERNELS = ("ntt_fwd", "mac", "intt_mask", "intt", "mask", "encode", "other", "fc")   # HL_K_* order
 
 
@@ -116,6 +116,9 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
         "hl_sk_prepare": [vp, vp, vp, vp],
         "hl_encrypt_device": [vp, vp, Tile, vp, i64, i64, u64, vp, vp],
         "hl_decrypt_share_device": [vp, vp, Tile, vp, i64, i64, vp, vp],
+        "hl_pk_gen": [vp, vp, u64, vp],
+        "hl_pk_prepare": [vp, vp, vp, vp],
+        "hl_he_matmul_share_rr": [vp, Tile, vp, i64, i64, i64, i64, i64, vp, vp, vp, vp, i32, vp, u64, vp, vp, vp],
         "hl_fc_encode_weights": [vp, vp, i64, i64, vp, vp],
         "hl_fc_local_share": [vp, vp, vp, vp, i64, i64, i64, vp, vp, vp],
         "hl_timing_read": [vp, vp, vp],
@@ -260,6 +263,37 @@ class Context:
         _check(_lib.hl_decrypt_share_device(self._h, _dptr(s_hat), _tile(tile), _dptr(ct_masked), Ma, Nb,
                                             _dptr(share), _stream(stream)))
         return share
+
+    # ---------------------------------------------------------------- re-randomisation (row f4)
+    def pk_gen(self, sk: np.ndarray, seed: int) -> np.ndarray:
+        pk = np.zeros((2, self.L, self.N), dtype=np.uint64)
+        _check(_lib.hl_pk_gen(self._h, _hptr(np.ascontiguousarray(sk), np.int8), seed, pk.ctypes.data))
+        return pk
+
+    def pk_prepare(self, pk: np.ndarray, device=None, stream=None):
+        import torch
+        dev = device if device is not None else torch.device("cuda", self.device)
+        pk_hat = _dev_empty(2 * self.L * self.N, dev)
+        _check(_lib.hl_pk_prepare(self._h, _hptr(np.ascontiguousarray(pk, dtype=np.uint64), np.uint64),
+                                  _dptr(pk_hat), _stream(stream)))
+        return pk_hat
+
+    def he_matmul_share_rr(self, tile, wcache, Ma: int, R: int, Nb: int, ct_in, seed: int, pk_hat, flood_bits: int,
+                           i_begin: int = 0, i_end: int = -1, stream=None):
+        """Compressed he_matmul_share with re-randomised responses (hl_he_matmul_share_rr)."""
+        import torch
+        lay = self.layout(tile, Ma, R, Nb, i_begin, i_end)
+        dev = ct_in.device
+        ws = _dev_empty(lay.workspace_bytes // 8, dev)
+        co = _dev_empty(lay.ct_out_words, dev)
+        rr = _dev_empty(lay.nI_shard * lay.nK * self.L * self.N, dev)
+        cm = _dev_empty(lay.ct_masked_words, dev)
+        sh = torch.zeros(Nb * Ma, dtype=torch.int64, device=dev)
+        _check(_lib.hl_he_matmul_share_rr(self._h, _tile(tile), _dptr(wcache), Ma, R, Nb, i_begin, i_end, _dptr(ct_in),
+                                          _dptr(ws), _dptr(co), _dptr(pk_hat), int(flood_bits), _dptr(rr), seed,
+                                          _dptr(cm), _dptr(sh), _stream(stream)))
+        self._rr_keep = (ws, co, rr)
+        return cm, sh
 
     # ---------------------------------------------------------------- server (device memory)
     def encode_weights(self, tile, W, i_begin: int = 0, i_end: int = -1, wcache=None, stream=None):

@@ -11,7 +11,8 @@
 
 namespace hl {
 
-enum : uint32_t { kDomSK = 1, kDomA = 2, kDomE = 3, kDomMask = 4 };
+enum : uint32_t { kDomSK = 1, kDomA = 2, kDomE = 3, kDomMask = 4,
+                  kDomPkA = 5, kDomPkE = 6, kDomRrU = 7, kDomRrE = 8, kDomRrF = 9 };   // 5-9: row f4 (reading C22)
 
 HL_HD uint32_t rotl(uint32_t x, int n) {
 #ifdef __CUDA_ARCH__

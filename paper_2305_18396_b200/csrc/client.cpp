@@ -111,6 +111,49 @@ extern "C" int hl_encrypt(const hl_ctx *c, const int8_t *sk, hl_tile tile, const
   return HL_OK;
 }
 
+// Public key (row f4, reading C22): pk1 = a (domain 5, stream l), pk0 = -a*s + e (e: domain 6,
+// stream 0), layout [2][L][N], coefficient form.
+extern "C" int hl_pk_gen(const hl_ctx *c, const int8_t *sk, uint64_t seed, uint64_t *pk) {
+  if (!c || !sk || !pk) return hl_fail(HL_EINVAL, "hl_pk_gen: NULL argument");
+  int rc;
+  if ((rc = check_sk(c, sk))) return rc;
+  const uint32_t N = c->N, L = c->L;
+  std::vector<uint64_t> shat;
+  sk_ntt(c, sk, shat);
+  std::vector<int64_t> e(N);
+  for (uint32_t blk = 0; blk < N / 8; blk++) {
+    uint64_t w[8];
+    hl::chacha_block_u64(seed, hl::kDomPkE, 0, blk, w);
+    for (int i = 0; i < 8; i++) {
+      uint64_t v = w[i] & 0x7fffffffffffffffull;
+      int k = 0;
+      while (k < 41 && v >= c->cdt[k]) k++;
+      e[8 * blk + i] = (w[i] >> 63) ? -(int64_t)k : (int64_t)k;
+    }
+  }
+  std::vector<uint64_t> a(N), as(N);
+  for (uint32_t l = 0; l < L; l++) {
+    const uint64_t p = c->primes[l];
+    for (uint32_t blk = 0; blk < N / 4; blk++) {
+      uint64_t w[8];
+      hl::chacha_block_u64(seed, hl::kDomPkA, l, blk, w);
+      for (int i = 0; i < 4; i++) a[4 * blk + i] = (uint64_t)((((hl_u128)w[2 * i + 1] << 64) | w[2 * i]) % p);
+    }
+    memcpy(as.data(), a.data(), 8ull * N);
+    hl_host_ntt_fwd(c, (int)l, as.data());
+    for (uint32_t i = 0; i < N; i++) as[i] = h_mulmod(as[i], shat[(size_t)l * N + i], p);
+    hl_host_ntt_inv(c, (int)l, as.data());
+    for (uint32_t i = 0; i < N; i++) {
+      uint64_t v = as[i] ? p - as[i] : 0;
+      uint64_t ev = e[i] >= 0 ? (uint64_t)e[i] : p - (uint64_t)(-e[i]);
+      v += ev; if (v >= p) v -= p;
+      pk[(size_t)l * N + i] = v;
+      pk[(size_t)(L + l) * N + i] = a[i];
+    }
+  }
+  return HL_OK;
+}
+
 // --- 256-bit helpers for the CRT and the rounding of decryption ---------------------------
 struct U256 { uint64_t w[4]; };
 

@@ -511,9 +511,83 @@ struct MaskArgs {
   int m, r, n;
   int lm, lr;          // log2 m, log2 r (tiles are powers of two: divisions become shifts)
   uint64_t seed;
+  // row f4 (reading C22): re-randomisation c += Enc_pk(0) + (F, 0); pk_hat == nullptr: off
+  const uint64_t *pk_hat;   // [2][L][N] NTT(pk) in slot order
+  const uint64_t *u_hat;    // [nout][L][N] NTT(u) in slot order (k_rr_u)
+  const uint64_t *cdt;      // device CDT table
+  int flood_bits;
 };
 
+// e (reading C8) from one PRF word
+__device__ __forceinline__ int cdt_sample(uint64_t w, const uint64_t *cdt) {
+  const uint64_t v = w & 0x7fffffffffffffffull;
+  int k = 0;
+  while (k < 41 && v >= __ldg(&cdt[k])) k++;
+  return (w >> 63) ? -k : k;
+}
+// signed value mod p (|v| < 2^63)
+__device__ __forceinline__ uint64_t smod(int64_t v, const PrimeConsts &pc) {
+  if (v >= 0) return (uint64_t)v % pc.p;
+  const uint64_t m = (uint64_t)(-v) % pc.p;
+  return m ? pc.p - m : 0;
+}
+// c0 extra of re-randomisation at position pos: e1[pos] + F[pos] (domains 8 and 9)
+__device__ __forceinline__ int64_t rr_c0_extra(const MaskArgs &M, uint64_t stream, int pos) {
+  int64_t ext = cdt_sample(hl::prf_u64(M.seed, hl::kDomRrE, 2 * stream, (uint64_t)pos), M.cdt);
+  if (M.flood_bits > 0)
+    ext += (int64_t)(hl::prf_u64(M.seed, hl::kDomRrF, stream, (uint64_t)pos) & ((1ull << M.flood_bits) - 1)) -
+           (1ll << (M.flood_bits - 1));
+  return ext;
+}
+// re-randomisation of a loaded NTT-domain polynomial: a += pk_hat[c] * u_hat  (slot order)
 template <int LOGN>
+__device__ __forceinline__ void rr_add_ntt(double (&a)[16], const MaskArgs &M, int64_t o, int c, int l, int L, int t,
+                                           const PrimeConsts &pc) {
+  const uint64_t *pk = M.pk_hat + ((size_t)c * L + l) * Geom<LOGN>::N;
+  const uint64_t *uh = M.u_hat + ((size_t)o * L + l) * Geom<LOGN>::N;
+#pragma unroll
+  for (int u = 0; u < 16; u++) {
+    const int sl = slot_of<LOGN>(t, u);
+    a[u] = red_d(__dadd_rn(a[u], mm_d(u2d(__ldg(&uh[sl])), u2d(__ldg(&pk[sl])), pc.pd, pc.pinv)), pc.pd, pc.pinv);
+  }
+}
+
+// u_hat[o][l] = NTT(u) (slot order) of the ternary u of every output ciphertext (domain 7,
+// stream (i_begin + I) nK + K)
+template <int LOGN>
+__global__ void __launch_bounds__(Geom<LOGN>::NT)
+k_rr_u(uint64_t *__restrict__ u_hat, MaskArgs M, DevParams P) {
+  using Gm = Geom<LOGN>;
+  extern __shared__ double sm[];
+  int8_t *u_sm = reinterpret_cast<int8_t *>(sm + Gm::SMEM_WORDS);
+  const int t = threadIdx.x, L = P.L;
+  const int64_t o = blockIdx.x, I = M.i_begin + o / M.nK, K = o % M.nK;
+#pragma unroll 1
+  for (int blk = t; blk < Gm::N / 8; blk += Gm::NT) {
+    uint64_t w[8];
+    hl::chacha_block_u64(M.seed, hl::kDomRrU, (uint64_t)(I * M.nK + K), (uint32_t)blk, w);
+#pragma unroll
+    for (int i = 0; i < 8; i++) u_sm[8 * blk + i] = (int8_t)((int)(w[i] % 3) - 1);
+  }
+  __syncthreads();
+  constexpr int K0 = Gm::k(0), G = 16 >> K0;
+  for (int l = 0; l < L; l++) {
+    const PrimeConsts pc = pick(P, l);
+    double a[16];
+#pragma unroll
+    for (int g = 0; g < G; g++)
+#pragma unroll
+      for (int u = 0; u < (1 << K0); u++) a[g * (1 << K0) + u] = (double)u_sm[elem_idx<LOGN, 0>(t, g, u)];
+    fwd_rounds_from<LOGN, 0>(a, sm, t, P.twd_fwd + (size_t)l * Gm::N, pc.pd, pc.pinv);
+    uint64_t *dst = u_hat + ((size_t)o * L + l) * Gm::N;
+#pragma unroll
+    for (int u = 0; u < 16; u++) dst[slot_of<LOGN>(t, u)] = d2u(canon_d(a[u], pc.pd, pc.pinv));
+    __syncthreads();
+  }
+}
+
+
+template <int LOGN, bool RR>
 __global__ void __launch_bounds__(Geom<LOGN>::NT)
 k_ntt_inv_mask(const uint64_t *__restrict__ ct_ntt, uint64_t *__restrict__ masked, uint64_t *__restrict__ share,
                MaskArgs M, DevParams P, int c1_only) {
@@ -529,8 +603,11 @@ k_ntt_inv_mask(const uint64_t *__restrict__ ct_ntt, uint64_t *__restrict__ maske
   const uint64_t tmask = (P.t_bits >= 64) ? ~0ull : ((1ull << P.t_bits) - 1);
   const size_t per = (size_t)L * (mn + Gm::N);
   uint64_t *dst = masked + (size_t)o * per;
+  constexpr bool rr = RR;                                         // row f4 (compile-time: lean plain kernel)
+  int64_t *ext_sm = reinterpret_cast<int64_t *>(sig_sm + mn);    // c0: e1 + F at the kept positions
+  int8_t *e2_sm = reinterpret_cast<int8_t *>(sig_sm);             // c1: e2 at every position
+  const uint64_t stream = (uint64_t)(I * M.nK + K);
   if (c == 0) {
-    const uint64_t stream = (uint64_t)(I * M.nK + K);
 #pragma unroll 1
     for (int kk = t; kk < mn; kk += Gm::NT) {
       const int k = kk >> M.lm, i = kk & (M.m - 1);
@@ -539,6 +616,16 @@ k_ntt_inv_mask(const uint64_t *__restrict__ ct_ntt, uint64_t *__restrict__ maske
       sig_sm[kk] = s;
       const int64_t row = K * M.n + k, col = I * M.m + i;
       if (row < M.Nb && col < M.Ma) share[row * M.Ma + col] = s;
+      if (rr) ext_sm[kk] = rr_c0_extra(M, stream, pos);
+    }
+    __syncthreads();
+  } else if (rr) {
+#pragma unroll 1
+    for (int blk = t; blk < Gm::N / 8; blk += Gm::NT) {
+      uint64_t w[8];
+      hl::chacha_block_u64(M.seed, hl::kDomRrE, 2 * stream + 1, (uint32_t)blk, w);
+#pragma unroll
+      for (int i = 0; i < 8; i++) e2_sm[8 * blk + i] = (int8_t)cdt_sample(w[i], M.cdt);
     }
     __syncthreads();
   }
@@ -547,18 +634,21 @@ k_ntt_inv_mask(const uint64_t *__restrict__ ct_ntt, uint64_t *__restrict__ maske
     const double *tw = P.twd_inv + (size_t)l * Gm::N;
     double a[16];
     load_ntt_domain<LOGN>(a, ct_ntt + (((size_t)o * 2 + c) * L + l) * Gm::N, t, pc);
+    if (rr) rr_add_ntt<LOGN>(a, M, o, c, l, L, t, pc);
     inv_rounds_from<LOGN, Gm::NR - 1>(a, sm, t, tw, pc);
     constexpr int K0 = Gm::k(0), G = 16 >> K0;
 #pragma unroll
     for (int g = 0; g < G; g++)
 #pragma unroll
       for (int u = 0; u < (1 << K0); u++) {
-        const uint64_t x = d2u(canon_d(a[g * (1 << K0) + u], pc.pd, pc.pinv));
+        uint64_t x = d2u(canon_d(a[g * (1 << K0) + u], pc.pd, pc.pinv));
         const int idx = elem_idx<LOGN, 0>(t, g, u);
         if (c == 1) {
+          if (rr) { x += smod(e2_sm[idx], pc); x = x >= pc.p ? x - pc.p : x; }
           dst[(size_t)L * mn + (size_t)l * Gm::N + idx] = x;
         } else if (idx < mr * M.n && (idx & (M.r - 1)) == M.r - 1) {
           const int kk = idx >> M.lr;               // = k*m + i for pos(i, k) = (k m + i) r + r - 1
+          if (rr) { x += smod(ext_sm[kk], pc); x = x >= pc.p ? x - pc.p : x; }
           uint64_t d = shoup_mul(sig_sm[kk], pc.delta, pc.delta_sh, pc.p);
           d = d >= pc.p ? d - pc.p : d;
           dst[(size_t)l * mn + kk] = x >= d ? x - d : x + pc.p - d;
@@ -590,7 +680,7 @@ __device__ __forceinline__ void inv_rounds_live(double (&a)[16], double *sm, int
   }
 }
 
-template <int LOGN>
+template <int LOGN, bool RR>
 __global__ void __launch_bounds__(Geom<LOGN>::NT)
 k_intt_c0_pruned(const uint64_t *__restrict__ ct_ntt, uint64_t *__restrict__ masked, uint64_t *__restrict__ share,
                  MaskArgs M, DevParams P) {
@@ -598,6 +688,7 @@ k_intt_c0_pruned(const uint64_t *__restrict__ ct_ntt, uint64_t *__restrict__ mas
   extern __shared__ double sm[];
   const int L = P.L;
   uint64_t *sig_sm = reinterpret_cast<uint64_t *>(sm + (size_t)L * Gm::SMEM_WORDS);
+  int64_t *ext_sm = reinterpret_cast<int64_t *>(sig_sm + M.m * M.n);   // row f4: e1 + F at the kept positions
   const int t = threadIdx.x, warp = t >> 5;
   const int64_t o = blockIdx.x;                        // I_loc * nK + K
   const int64_t Iloc = o / M.nK, K = o % M.nK, I = M.i_begin + Iloc;
@@ -612,12 +703,14 @@ k_intt_c0_pruned(const uint64_t *__restrict__ ct_ntt, uint64_t *__restrict__ mas
     sig_sm[kk] = s;
     const int64_t row = K * M.n + k, col = I * M.m + i;
     if (row < M.Nb && col < M.Ma) share[row * M.Ma + col] = s;
+    if constexpr (RR) ext_sm[kk] = rr_c0_extra(M, stream, ((k * M.m + i) << M.lr) + M.r - 1);
   }
   // phase A: first inverse round of every prime (all threads)
   for (int l = 0; l < L; l++) {
     const PrimeConsts pc = pick(P, l);
     double a[16];
     load_ntt_domain<LOGN>(a, ct_ntt + (((size_t)o * 2) * L + l) * Gm::N, t, pc);
+    if constexpr (RR) rr_add_ntt<LOGN>(a, M, o, 0, l, L, t, pc);
     inv_round<LOGN, Gm::NR - 1>(a, t, P.twd_inv + (size_t)l * Gm::N, pc);
     to_smem<LOGN, Gm::NR - 1>(a, sm + (size_t)l * Gm::SMEM_WORDS, t);
   }
@@ -645,8 +738,9 @@ k_intt_c0_pruned(const uint64_t *__restrict__ ct_ntt, uint64_t *__restrict__ mas
     for (int u = 0; u < (1 << K0); u++) {
       const int idx = elem_idx<LOGN, 0>(tv, g, u);
       if (idx < mr * M.n) {                            // idx = r-1 mod r by construction
-        const uint64_t x = d2u(canon_d(a[g * (1 << K0) + u], pc.pd, pc.pinv));
+        uint64_t x = d2u(canon_d(a[g * (1 << K0) + u], pc.pd, pc.pinv));
         const int kk = idx >> M.lr;
+        if constexpr (RR) { x += smod(ext_sm[kk], pc); x = x >= pc.p ? x - pc.p : x; }
         uint64_t d = shoup_mul(sig_sm[kk], pc.delta, pc.delta_sh, pc.p);
         d = d >= pc.p ? d - pc.p : d;
         dst[(size_t)l * mn + kk] = x >= d ? x - d : x + pc.p - d;
@@ -1258,30 +1352,37 @@ void launch_mac(const hl_ctx *c, const uint2 *W, const uint32_t *X, uint64_t *ou
   }
 }
 
-template <int LOGN>
-void launch_inv_mask(const hl_ctx *c, const uint64_t *ct_ntt, uint64_t *masked, uint64_t *share, MaskArgs M,
-                     int64_t nout, cudaStream_t st) {
+template <int LOGN, bool RR>
+void launch_inv_mask_t(const hl_ctx *c, const uint64_t *ct_ntt, uint64_t *masked, uint64_t *share, MaskArgs M,
+                       int64_t nout, cudaStream_t st) {
   using Gm = Geom<LOGN>;
   static bool init = false;
   if (!init) {
-    set_smem(k_ntt_inv_mask<LOGN>, ntt_smem<LOGN>() + (size_t)Gm::N * 8);
-    set_smem(k_intt_c0_pruned<LOGN>, 232448);
+    set_smem(k_ntt_inv_mask<LOGN, RR>, ntt_smem<LOGN>() + (size_t)Gm::N * 16);
+    set_smem(k_intt_c0_pruned<LOGN, RR>, 232448);
     init = true;
   }
   // the pruned c0 transform needs r in {2..16} and one warp group per prime within the CTA
   static const bool no_prune = getenv("HELINEAR_NO_PRUNE") != nullptr;
   const int wpp = (Gm::NT / std::max(M.r, 1) + 31) / 32;
-  const size_t smem_c0 = ntt_smem<LOGN>() * c->L + (size_t)M.m * M.n * 8;
+  const size_t ext = RR ? 16 : 8;                      // sigma (+ row f4: e1 + F) per kept position
+  const size_t smem_c0 = ntt_smem<LOGN>() * c->L + (size_t)M.m * M.n * ext;
   const bool prune = !no_prune && M.r >= 2 && M.r <= 16 && (int)c->L * wpp <= Gm::NT / 32 && smem_c0 <= 232448;
-  const size_t smem = ntt_smem<LOGN>() + (size_t)M.m * M.n * 8;
+  const size_t smem = ntt_smem<LOGN>() + (RR ? std::max((size_t)M.m * M.n * 16, (size_t)Gm::N) : (size_t)M.m * M.n * 8);
   KTimer kt(c, HL_K_INTT_MASK, st);
   if (prune) {
-    k_intt_c0_pruned<LOGN><<<(unsigned)nout, Gm::NT, smem_c0, st>>>(
-        ct_ntt, masked, share, M, c->dp);
-    k_ntt_inv_mask<LOGN><<<(unsigned)nout, Gm::NT, smem, st>>>(ct_ntt, masked, share, M, c->dp, 1);
+    k_intt_c0_pruned<LOGN, RR><<<(unsigned)nout, Gm::NT, smem_c0, st>>>(ct_ntt, masked, share, M, c->dp);
+    k_ntt_inv_mask<LOGN, RR><<<(unsigned)nout, Gm::NT, smem, st>>>(ct_ntt, masked, share, M, c->dp, 1);
   } else {
-    k_ntt_inv_mask<LOGN><<<(unsigned)(nout * 2), Gm::NT, smem, st>>>(ct_ntt, masked, share, M, c->dp, 0);
+    k_ntt_inv_mask<LOGN, RR><<<(unsigned)(nout * 2), Gm::NT, smem, st>>>(ct_ntt, masked, share, M, c->dp, 0);
   }
+}
+
+template <int LOGN>
+void launch_inv_mask(const hl_ctx *c, const uint64_t *ct_ntt, uint64_t *masked, uint64_t *share, MaskArgs M,
+                     int64_t nout, cudaStream_t st) {
+  if (M.pk_hat) launch_inv_mask_t<LOGN, true>(c, ct_ntt, masked, share, M, nout, st);
+  else launch_inv_mask_t<LOGN, false>(c, ct_ntt, masked, share, M, nout, st);
 }
 
 }  // namespace
@@ -1371,6 +1472,7 @@ static MaskArgs mask_args(const Geo &g, int64_t Ma, int64_t Nb, uint64_t seed) {
   M.Ma = Ma; M.Nb = Nb; M.nK = g.nK; M.i_begin = g.i_begin;
   M.m = g.m; M.r = g.r; M.n = g.n; M.seed = seed;
   M.lm = __builtin_ctz((unsigned)g.m); M.lr = __builtin_ctz((unsigned)g.r);
+  M.pk_hat = nullptr; M.u_hat = nullptr; M.cdt = nullptr; M.flood_bits = 0;
   return M;
 }
 
@@ -1656,6 +1758,57 @@ extern "C" int hl_fc_local_share(const hl_ctx *c, const uint64_t *X1, const void
                                                               bias, share, g);
   k_fc_mask<<<(unsigned)((Nb * Ma + 255) / 256), 256, 0, st>>>(share, Nb * Ma, g.tmask);
   return hl_cuda_check("hl_fc_local_share: launch");
+}
+
+// ---------------------------------------------------------------------------------------
+// re-randomised responses (reading C22)
+// ---------------------------------------------------------------------------------------
+extern "C" int hl_pk_prepare(const hl_ctx *c, const uint64_t *pk, uint64_t *pk_hat, void *stream) {
+  int rc;
+  if ((rc = check_ptrs({c, pk, pk_hat}, "hl_pk_prepare"))) return rc;
+  cudaStream_t st = (cudaStream_t)stream;
+  if (cudaMemcpyAsync(pk_hat, pk, (size_t)2 * c->L * c->N * 8, cudaMemcpyHostToDevice, st) != cudaSuccess)
+    return hl_cuda_check("hl_pk_prepare: upload");
+  fwd_ntt(c, pk_hat, pk_hat, 2, nullptr, st);          // NTT(pk0), NTT(pk1) per prime, slot order
+  if (cudaStreamSynchronize(st) != cudaSuccess) return hl_cuda_check("hl_pk_prepare: sync");
+  return hl_cuda_check("hl_pk_prepare: launch");
+}
+
+extern "C" int hl_he_matmul_share_rr(const hl_ctx *c, hl_tile tile, const void *wcache, int64_t Ma, int64_t R,
+                                     int64_t Nb, int64_t i_begin, int64_t i_end, const uint64_t *ct_in,
+                                     void *workspace, uint64_t *ct_out_ntt, const uint64_t *pk_hat, int flood_bits,
+                                     uint64_t *rr_ws, uint64_t seed, uint64_t *ct_masked, uint64_t *share,
+                                     void *stream) {
+  int rc;
+  if ((rc = check_ptrs({c, wcache, ct_in, workspace, ct_out_ntt, pk_hat, rr_ws, ct_masked, share},
+                       "hl_he_matmul_share_rr")))
+    return rc;
+  Geo g;
+  if ((rc = hl_geometry(c, tile, Ma, R, Nb, i_begin, i_end, &g))) return rc;
+  if (flood_bits < 0 || flood_bits > std::min(62, (int)c->log2_delta - 1))
+    return hl_fail(HL_ERANGE, "hl_he_matmul_share_rr: flood_bits must be in [0, min(62, log2(Delta) - 1)]");
+  cudaStream_t st = (cudaStream_t)stream;
+  const int64_t nC = 2 * g.nK, nout = g.nIs * g.nK;
+  const MacGeom mg = mac_geom(c, g.nIs, g.nJ, nC);
+  fwd_ntt(c, ct_in, workspace, g.nJ * nC, &mg, st);
+  launch_mac(c, (const uint2 *)wcache, (const uint32_t *)workspace, ct_out_ntt, mg, st);
+  MaskArgs M = mask_args(g, Ma, Nb, seed);
+  M.pk_hat = pk_hat; M.u_hat = rr_ws; M.cdt = c->d_cdt; M.flood_bits = flood_bits;
+  {
+    KTimer kt(c, HL_K_INTT_MASK, st);
+    if (c->N == 4096) {
+      static bool init = false;
+      if (!init) { set_smem(k_rr_u<12>, ntt_smem<12>() + 4096); init = true; }
+      k_rr_u<12><<<(unsigned)nout, Geom<12>::NT, ntt_smem<12>() + 4096, st>>>(rr_ws, M, c->dp);
+    } else {
+      static bool init = false;
+      if (!init) { set_smem(k_rr_u<13>, ntt_smem<13>() + 8192); init = true; }
+      k_rr_u<13><<<(unsigned)nout, Geom<13>::NT, ntt_smem<13>() + 8192, st>>>(rr_ws, M, c->dp);
+    }
+  }
+  if (c->N == 4096) launch_inv_mask<12>(c, ct_out_ntt, ct_masked, share, M, nout, st);
+  else launch_inv_mask<13>(c, ct_out_ntt, ct_masked, share, M, nout, st);
+  return hl_cuda_check("hl_he_matmul_share_rr: launch");
 }
 
 extern "C" int hl_he_linear_host(const hl_ctx *c, hl_tile tile, const void *wcache, int64_t Ma, int64_t R,

@@ -98,6 +98,15 @@ def test_keygen_matches_oracle(hl):
         assert np.array_equal(ctx.keygen(seed), ref.keygen(P, seed))
 
 
+@pytest.mark.parametrize("N,L", [(4096, 2), (8192, 3)])
+def test_pk_gen_matches_oracle(hl, N, L):
+    """Row f4: the library's public key (host client) equals the oracle's, bit for bit."""
+    ctx = hl.Context(N, L, 37, device=-1)
+    P = ref.bfv_params(N, L, 37)
+    sk = ref.keygen(P, 41)
+    assert np.array_equal(ctx.pk_gen(sk, 42), ref.pk_gen(P, sk, 42))
+
+
 @pytest.mark.parametrize("N,L,shape,tile", [
     (4096, 2, (8, 64), (16, 32, 8)),
     (4096, 2, (37, 21), (4, 8, 16)),           # ragged

@@ -534,3 +534,32 @@ def test_bert_large_c4_shape_sampled(hl, ctx8192):
         assert np.array_equal(mh[I, K], em[o]), (I, K)
     got = (hl.to_host(share_c).reshape(mm.Nb, mm.Ma) + hl.to_host(share).reshape(mm.Nb, mm.Ma)) & np.uint64((1 << 37) - 1)
     assert np.array_equal(got, ref.matmul_mod_t(X, W))
+
+
+# ------------------------------------------------------------------------- re-randomisation (row f4)
+@pytest.mark.parametrize("N,shape,tile,fb", [
+    (4096, (24, 16, 40), (16, 8, 32), 0),          # pruned c0 path (r = 8), no flooding
+    (4096, (24, 16, 40), (16, 8, 32), 58),         # with flooding
+    (4096, (8, 64, 64), (16, 32, 8), 40),          # r = 32: unpruned c0 path
+    (8192, (32, 48, 40), (32, 16, 16), 62),        # N=8192, L=3, the largest flood (one PRF word)
+])
+def test_rerandomized_response_vs_oracle(hl, ctx4096, ctx8192, N, shape, tile, fb):
+    """hl_he_matmul_share_rr == oracle rerandomize + mask_and_share bit for bit; the client's
+    decryption of the re-randomised (and flooded) response still reconstructs X.W mod 2^37."""
+    ctx = ctx4096 if N == 4096 else ctx8192
+    P = _P(ctx)
+    Nb, R, Ma = shape
+    X, W = synth.activations(981 + fb, Nb, R), synth.weights(982, R, Ma)
+    sk = ref.keygen(P, 983)
+    pk = ref.pk_gen(P, sk, 984)
+    ct_in = ref.encrypt(P, tile, sk, X, 985)
+    wc = ctx.encode_weights(tile, hl.to_device(W))
+    masked, share = ctx.he_matmul_share_rr(tile, wc, Ma, R, Nb, hl.to_device(ct_in), 986, ctx.pk_prepare(pk), fb)
+    _sync()
+    nI, nJ, nK = ref.tile_counts(tile, Ma, R, Nb)
+    ct_rr = ref.rerandomize(P, tile, pk, ref.he_matmul(P, tile, W, ct_in, Nb), nK, 986, fb)
+    em, es = ref.mask_and_share(P, tile, ct_rr, Ma, Nb, 986, True)
+    assert np.array_equal(hl.to_host(masked).reshape(em.shape), em)
+    assert np.array_equal(hl.to_host(share).reshape(es.shape), es)
+    share_c = ctx.decrypt_share(sk, tile, hl.to_host(masked), Ma, Nb, True)
+    assert np.array_equal((share_c + es) & np.uint64((1 << 37) - 1), ref.matmul_mod_t(X, W))
