@@ -51,8 +51,9 @@ def launches(path):
     hdr = rows[0]
     ik, iv, iu = hdr.index("Kernel Name"), hdr.index("Metric Value"), hdr.index("Metric Unit")
     tot, cnt = defaultdict(float), defaultdict(int)
+    im = hdr.index("Metric Name")
     for r in rows[1:]:
-        if len(r) != len(hdr):
+        if len(r) != len(hdr) or r[im] != "gpu__time_duration.sum":
             continue
         v = float(r[iv].replace(",", ""))
         v *= {"ns": 1e-3, "nsecond": 1e-3, "us": 1.0, "usecond": 1.0, "ms": 1e3, "msecond": 1e3}.get(r[iu], 1.0)
