@@ -8,11 +8,11 @@
 // cores: residues are split into 7 unsigned bytes, W = sum_a w_a 2^(8a), X = sum_b x_b 2^(8b),
 //     sum_J W X = sum_{d=0..12} 2^(8d) S_d,   S_d = sum_{a+b=d} sum_J w_a x_b   (S_d < 2^31 for nJ <= 4096)
 // and the tensor core forms every S_d directly: for limb plane a, MMA a multiplies A_a = w_a
-// [128 I rows x 32 J] by a B operand whose row (d*CW + c) holds x_{d-a}[c] -- a window into ONE
-// Toeplitz image Z of the X limbs (rows (b+6)*CW + c hold x_b[c], all other rows zero), selected
-// by shifting the B descriptor's start address by (6-a)*CW rows.  7 MMAs per 32-J step
-// accumulate S_d[I][c] in TMEM column d*CW + c; the epilogue forms sum_d S_d 2^(8d) (< 2^124)
-// and reduces it mod p_l once per output.
+// [128 I rows x 32 J] by the X limbs (B operand, row b*CW + c = x_b[c], N = 7 CW) and
+// accumulates into the TMEM column window starting at a*CW, so column (a+b)*CW + c = d*CW + c
+// collects S_d -- the Toeplitz structure lives in the accumulator address, not in a zero-padded
+// B image (half the B operand, the MMA at its issue floor).  7 MMAs per 32-J step; the epilogue
+// forms sum_d S_d 2^(8d) (< 2^124) and reduces it mod p_l once per output.
 //
 // Kernel roles (384 threads, one persistent CTA per SM):
 //   warp 0      TMA producer: per (slot, 32-J step) one cp.async.bulk of the 7 weight planes
@@ -32,9 +32,10 @@
 
 template <int CW>
 struct TcGeom {
-  static constexpr int N = ((13 * CW + 15) / 16) * 16;   // MMA N: columns d*CW + c, d < 13
-  static constexpr int ZR = N + 6 * CW;                  // rows of the Toeplitz B image
-  static constexpr int Z_BYTES = 2 * ZR * 16;            // one Toeplitz image (Z ring entry)
+  static constexpr int NM = ((7 * CW + 15) / 16) * 16;   // MMA N: the 7 limbs x CW columns of X (+ zero pad)
+  static constexpr int N = 6 * CW + NM;                  // accumulator width: columns d*CW + c, d < 13 (+ pad)
+  static constexpr int ZR = NM;                          // rows of the X-limb B image: row b*CW + c = x_b[c]
+  static constexpr int Z_BYTES = 2 * ZR * 16;            // one B image (Z ring entry)
   static constexpr int NZ = 4;                           // Z ring depth (decoupled from the TMA ring)
   static constexpr int RAW_BYTES = 32 * CW * 8;          // X residues of one 32-J step
   static constexpr int A_OFF = RAW_BYTES;                // TMA stage layout: [RAW][A (224 B per I row)]
@@ -209,6 +210,19 @@ k_mac_tc(MacTcArgs A, DevParams P) {
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  // The limb-plane MMA a accumulates into the column window [a*CW, a*CW + NM) of its buffer (the
+  // Toeplitz shift lives in the accumulator address): columns [NM, N) must start at zero.  The
+  // epilogue re-zeroes them after draining a buffer; here every buffer is zeroed once.
+  if (warp >= 4) {
+    const uint32_t lanes = (uint32_t)(32 * (warp & 3)) << 16;
+    for (int b = 0; b < T::NBUF; b++)
+      for (int col = T::NM + ((warp - 4) >> 2); col < T::N; col += 2)
+        asm volatile("tcgen05.st.sync.aligned.32x32b.x1.b32 [%0], {%1};" ::"r"(tmem + lanes + b * T::N + col), "r"(0u));
+    asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
   unsigned long long pw[8] = {0, 0, 0, 0, 0, 0, 0, 0};   // profiling accumulators (registers)
   const long long t_start = clock64();
 
@@ -252,7 +266,7 @@ k_mac_tc(MacTcArgs A, DevParams P) {
     // single-lane branch costs more than the MMA itself (profiles/r01/microbench_umma_i8_cost.log).
     // tiles of <= 64 rows use M = 64 (half the A-operand shared-memory reads per MMA); the
     // accumulator rows then sit in lanes 32(r/16) + r%16 (profiles/r01/microbench_umma_i8.log)
-    const uint32_t idesc = umma_idesc_u8(g.RT <= 64 ? 64 : 128, (A.ko & 8) ? 16 : T::N);   // ko 8: timing only
+    const uint32_t idesc = umma_idesc_u8(g.RT <= 64 ? 64 : 128, (A.ko & 8) ? 16 : T::NM);   // ko 8: timing only
     int st = 0;
     uint32_t ph = 0;
     uint32_t tile_no = 0, zseq = 0;
@@ -280,8 +294,8 @@ k_mac_tc(MacTcArgs A, DevParams P) {
             for (int a = 0; a < 7; a++) {
               if (A.ko & 1) break;
               const uint64_t ad = umma_sdesc(a0 + a * plane, lbo_a, 128);
-              const uint64_t bd = umma_sdesc(z0 + (6 - a) * CW * 16, T::ZR * 16, 128);
-              umma_i8(dcol, ad, bd, idesc, (kk | a) ? 1u : 0u);
+              const uint64_t bd = umma_sdesc(z0, T::ZR * 16, 128);
+              umma_i8(dcol + a * CW, ad, bd, idesc, (kk | a) ? 1u : 0u);   // D window shifted by a*CW
             }
             umma_commit(&empty[st]);
             umma_commit(&zempty[zi]);
@@ -318,7 +332,7 @@ k_mac_tc(MacTcArgs A, DevParams P) {
               const uint64_t x = raw[(j0 + j) * CW + c];
               lo[j] = (uint32_t)x; hi[j] = (uint32_t)(x >> 32);
             }
-            uint32_t *zrow = reinterpret_cast<uint32_t *>(z + ((size_t)h * T::ZR + 6 * CW + c) * 16) + gq;
+            uint32_t *zrow = reinterpret_cast<uint32_t *>(z + ((size_t)h * T::ZR + c) * 16) + gq;
 #pragma unroll
             for (int b = 0; b < 7; b++) {
               const uint32_t *src = b < 4 ? lo : hi;
@@ -326,7 +340,7 @@ k_mac_tc(MacTcArgs A, DevParams P) {
               const uint32_t sel = bb | ((bb + 4) << 4);
               const uint32_t t01 = __byte_perm(src[0], src[1], sel);
               const uint32_t t23 = __byte_perm(src[2], src[3], sel);
-              zrow[b * CW * 4] = __byte_perm(t01, t23, 0x5410);   // row (b+6)*CW + c
+              zrow[b * CW * 4] = __byte_perm(t01, t23, 0x5410);   // row b*CW + c
             }
           }
           asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -392,6 +406,14 @@ k_mac_tc(MacTcArgs A, DevParams P) {
 #pragma unroll
             for (int d = 1; d < 4; d++) H[c] += (uint64_t)v[d][c] << (8 * d);
           }
+        }
+        {   // re-zero the columns no a = 0 MMA initialises (see the setup) -- only columns of this
+            // warp's own half (c / CH == hh): the other warp of the quadrant may still be reading its half
+          const uint32_t zb = tmem + ((uint32_t)(32 * q) << 16) + buf * T::N;
+          for (int col = T::NM; col < T::N; col++)
+            if ((col % CW) / CH == hh)
+              asm volatile("tcgen05.st.sync.aligned.32x32b.x1.b32 [%0], {%1};" ::"r"(zb + col), "r"(0u));
+          asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
         }
         tc_fence_before();
         __syncwarp();
