@@ -23,6 +23,7 @@ struct PrimeConsts {
   uint64_t r64_sh;    // floor(r64 * 2^64 / p)        (Shoup companion)
   uint64_t c40, c40_sh, c72, c72_sh;   // 2^40, 2^72 mod p (tensor-core MAC recombination) + Shoup
   uint64_t dec_I, dec_F;   // theta_l = t ((q/p)^-1 mod p) / p = dec_I + dec_F 2^-64 (RNS decryption, row f3)
+  uint64_t mc;             // 2^50 - p if < 2^32 (pseudo-Mersenne fold 2^50 = mc mod p), else 0
   uint64_t delta;     // Delta mod p, Delta = floor(q / t)
   uint64_t delta_sh;  // Shoup companion of delta
   uint64_t ninv;      // N^-1 mod p

@@ -472,7 +472,7 @@ k_encode_weights(EncodeArgs A, uint2 *__restrict__ wcache, DevParams P, uint32_t
 // Inverse NTT kernel: in u64 [npoly][L][N] (NTT domain, slot order) -> out [npoly][L][N]
 // coefficient form, canonical.  in may alias out.
 // ---------------------------------------------------------------------------------------
-// canonical residues in, reduced to |v| <= p/2 (the inverse rounds' entry bound)
+// residues in [0, 2^52) (canonical, or the MAC's lazy outputs < 4p), reduced to |v| <= p/2 (the inverse rounds' entry bound)
 template <int LOGN>
 __device__ __forceinline__ void load_ntt_domain(double (&a)[16], const uint64_t *src, int t, const PrimeConsts &pc) {
 #pragma unroll
@@ -1320,6 +1320,7 @@ void launch_mac_tc(const hl_ctx *c, const void *W, const void *X, uint64_t *out,
     A.jc0 = (int)(j0 / 32);
     A.njc = (int)((std::min<int64_t>(g.nJp, j0 + kMacJChunk) - j0) / 32);
     A.accumulate = j0 > 0;
+    A.lazy_out = g.nJp <= kMacJChunk;                       // single launch: nobody adds to the outputs
     cudaMemsetAsync(A.sched, 0, sizeof(int), st);
     switch (g.CW) {
       case 16: launch_mac_tc_t<16>(c, A, smem_budget, st); break;

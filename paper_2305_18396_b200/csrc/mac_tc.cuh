@@ -79,6 +79,7 @@ struct MacTcArgs {
   unsigned long long *prof;   // diagnostics (HELINEAR_MAC_PROF): per-CTA cycles spent waiting, by role
   int *sched;                 // work counter (zeroed before the launch; in the caller's workspace)
   int ko;                     // diagnostics (HELINEAR_MAC_KO bitmask): 1 skip MMAs, 2 skip conversion, 4 skip epilogue math
+  int lazy_out;               // 1: outputs only < 2^52 (= residue + k p, k < 4): fine for the inverse NTT's input
 };
 
 // UMMA shared-memory descriptor: K-major, no swizzle; core matrix = 8 rows x 16 B contiguous.
@@ -141,6 +142,20 @@ __device__ __forceinline__ void tmem_ld_cw(uint32_t addr, uint32_t (&v)[CW]) {
                  : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
                    "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
                  : "r"(addr));
+  }
+}
+
+// zero CH consecutive accumulator columns of the warp's 32 lanes
+template <int CH>
+__device__ __forceinline__ void tmem_zero_cw(uint32_t addr) {
+  if constexpr (CH == 1) {
+    asm volatile("tcgen05.st.sync.aligned.32x32b.x1.b32 [%0], {%1};" ::"r"(addr), "r"(0u));
+  } else if constexpr (CH == 2) {
+    asm volatile("tcgen05.st.sync.aligned.32x32b.x2.b32 [%0], {%1,%1};" ::"r"(addr), "r"(0u));
+  } else if constexpr (CH == 4) {
+    asm volatile("tcgen05.st.sync.aligned.32x32b.x4.b32 [%0], {%1,%1,%1,%1};" ::"r"(addr), "r"(0u));
+  } else {
+    asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%1,%1,%1,%1,%1,%1,%1};" ::"r"(addr), "r"(0u));
   }
 }
 
@@ -409,10 +424,9 @@ k_mac_tc(MacTcArgs A, DevParams P) {
         }
         {   // re-zero the columns no a = 0 MMA initialises (see the setup) -- only columns of this
             // warp's own half (c / CH == hh): the other warp of the quadrant may still be reading its half
-          const uint32_t zb = tmem + ((uint32_t)(32 * q) << 16) + buf * T::N;
-          for (int col = T::NM; col < T::N; col++)
-            if ((col % CW) / CH == hh)
-              asm volatile("tcgen05.st.sync.aligned.32x32b.x1.b32 [%0], {%1};" ::"r"(zb + col), "r"(0u));
+          const uint32_t zb = tmem + ((uint32_t)(32 * q) << 16) + buf * T::N + hh * CH;
+#pragma unroll
+          for (int d = T::NM / CW; d < T::N / CW; d++) tmem_zero_cw<CH>(zb + d * CW);
           asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
         }
         tc_fence_before();
@@ -421,12 +435,20 @@ k_mac_tc(MacTcArgs A, DevParams P) {
         if (active && !(A.ko & 4)) {
 #pragma unroll
           for (int c = 0; c < CH; c++) {
-            const uint64_t rl = L[c] - __umul64hi(L[c], pc.mu) * pc.p;
-            const uint64_t rm = shoup_mul(M[c], pc.c40, pc.c40_sh, pc.p);
-            const uint64_t rh = shoup_mul(H[c], pc.c72, pc.c72_sh, pc.p);
-            uint64_t r = rl + rm + rh;                                   // < 6p < 2^53
-            r -= __umul64hi(r, pc.mu) * pc.p;                            // [0, 2p)
-            r = r >= pc.p ? r - pc.p : r;
+            // V = L + M 2^40 + H 2^72 < 2^124 exactly; V mod p = Shoup(V_hi, 2^64 mod p) + (V_lo mod p)
+            const hl_u128 V = (hl_u128)L[c] + ((hl_u128)M[c] << 40) + ((hl_u128)H[c] << 72);
+            const uint64_t vh = (uint64_t)(V >> 64), vl = (uint64_t)V;
+            uint64_t r = shoup_mul(vh, pc.r64, pc.r64_sh, pc.p);           // [0, 2p)
+            if (pc.mc) {
+              // pseudo-Mersenne fold, 2^50 = mc (mod p): vl = a 2^50 + b -> b + a mc < 2^50 + 2^46 < 2p
+              r += (vl & ((1ull << 50) - 1)) + (vl >> 50) * pc.mc;
+            } else {
+              r += vl - __umul64hi(vl, pc.mu) * pc.p;                      // [0, 2p)
+            }                                                              // r in [0, 4p) < 2^52
+            if (!A.lazy_out) {
+              r = r >= pc.two_p ? r - pc.two_p : r;
+              r = r >= pc.p ? r - pc.p : r;
+            }
             if (row < rows_valid) stg[row * T::STG_STRIDE + (hh * CH + c) * T::SPI + si] = r;
           }
         }
