@@ -137,6 +137,23 @@ __device__ __forceinline__ void from_smem(double (&a)[16], const double *sm, int
     for (int u = 0; u < (1 << K); u++) a[g * (1 << K) + u] = sm[pad_idx(elem_idx<LOGN, R>(t, g, u))];
 }
 
+// All twiddles of round R for thread t, loaded up front (issued before the round's smem exchange
+// so that their L1/L2 latency overlaps it): wv[g (2^K - 1) + 2^ls - 1 + (u >> (K - ls))].
+template <int LOGN, int R>
+__device__ __forceinline__ void load_round_tw(double (&wv)[15], int t, const double *tw) {
+  using Gm = Geom<LOGN>;
+  constexpr int S0 = Gm::s0(R), K = Gm::k(R), LO = Gm::lo(R), G = 16 >> K;
+#pragma unroll
+  for (int g = 0; g < G; g++) {
+    const int gid_high = (t + g * Gm::NT) >> LO;
+#pragma unroll
+    for (int ls = 0; ls < K; ls++)
+#pragma unroll
+      for (int j = 0; j < (1 << ls); j++)
+        wv[g * ((1 << K) - 1) + (1 << ls) - 1 + j] = __ldg(&tw[(1 << (S0 + ls)) + (gid_high << ls) + j]);
+  }
+}
+
 // Forward CT stages of round R.  Twiddle of a pair whose lower index is idx at stage st:
 // psi^bitrev((1<<st) + (idx >> (LOGN - st))); within a round that is
 // (1<<st) + (gid_high << ls) + (u >> (K - ls)).
@@ -144,24 +161,19 @@ __device__ __forceinline__ void from_smem(double (&a)[16], const double *sm, int
 // stage adds < p, so every value is reduced (red_d) after each odd stage: multiplicands stay
 // below 2p < 2^51 as mm_d requires.
 template <int LOGN, int R>
-__device__ __forceinline__ void fwd_round(double (&a)[16], int t, const double *tw, double p, double pinv) {
+__device__ __forceinline__ void fwd_round(double (&a)[16], const double (&wv)[15], double p, double pinv) {
   using Gm = Geom<LOGN>;
-  constexpr int S0 = Gm::s0(R), K = Gm::k(R), LO = Gm::lo(R), G = 16 >> K;
+  constexpr int S0 = Gm::s0(R), K = Gm::k(R), G = 16 >> K;
 #pragma unroll
   for (int ls = 0; ls < K; ls++) {
     const int st = S0 + ls;
     const int half = 1 << (K - 1 - ls);
 #pragma unroll
     for (int g = 0; g < G; g++) {
-      const int gid_high = (t + g * Gm::NT) >> LO;
 #pragma unroll
       for (int u = 0; u < (1 << K); u++) {
         if (u & half) continue;
-#ifdef HL_NTT_KO_TW
-        const double w = __ldg(&tw[(1 << st)]);         // timing experiment only: wrong twiddles
-#else
-        const double w = __ldg(&tw[(1 << st) + (gid_high << ls) + (u >> (K - ls))]);
-#endif
+        const double w = wv[g * ((1 << K) - 1) + (1 << ls) - 1 + (u >> (K - ls))];
         double &X = a[g * (1 << K) + u], &Y = a[g * (1 << K) + u + half];
         const double T = mm_d(Y, w, p, pinv);
         Y = __dsub_rn(X, T);
@@ -179,9 +191,9 @@ __device__ __forceinline__ void fwd_round(double (&a)[16], int t, const double *
 // satisfy |v| <= p/2; a GS stage keeps |Y'| < p and |X'| <= 2 max|v|, so values are reduced
 // after every second stage (counted from the top, stage LOGN-1) -- differences stay < 2p.
 template <int LOGN, int R>
-__device__ __forceinline__ void inv_round(double (&a)[16], int t, const double *tw, const PrimeConsts &pc) {
+__device__ __forceinline__ void inv_round(double (&a)[16], const double (&wv)[15], const PrimeConsts &pc) {
   using Gm = Geom<LOGN>;
-  constexpr int S0 = Gm::s0(R), K = Gm::k(R), LO = Gm::lo(R), G = 16 >> K;
+  constexpr int S0 = Gm::s0(R), K = Gm::k(R), G = 16 >> K;
   const double p = pc.pd, pinv = pc.pinv;
 #pragma unroll
   for (int ls = K - 1; ls >= 0; ls--) {
@@ -189,7 +201,6 @@ __device__ __forceinline__ void inv_round(double (&a)[16], int t, const double *
     const int half = 1 << (K - 1 - ls);
 #pragma unroll
     for (int g = 0; g < G; g++) {
-      const int gid_high = (t + g * Gm::NT) >> LO;
 #pragma unroll
       for (int u = 0; u < (1 << K); u++) {
         if (u & half) continue;
@@ -200,11 +211,7 @@ __device__ __forceinline__ void inv_round(double (&a)[16], int t, const double *
           X = mm_d(s, pc.ninv_d, p, pinv);
           Y = mm_d(d, pc.ninv_w1_d, p, pinv);
         } else {
-#ifdef HL_NTT_KO_TW
-          const double w = __ldg(&tw[(1 << st)]);
-#else
-          const double w = __ldg(&tw[(1 << st) + (gid_high << ls) + (u >> (K - ls))]);
-#endif
+          const double w = wv[g * ((1 << K) - 1) + (1 << ls) - 1 + (u >> (K - ls))];
           X = s;
           Y = mm_d(d, w, p, pinv);
         }
@@ -221,13 +228,15 @@ template <int LOGN, int R>
 __device__ __forceinline__ void fwd_rounds_from(double (&a)[16], double *sm, int t, const double *tw,
                                                 double p, double pinv) {
   if constexpr (R < Geom<LOGN>::NR) {
+    double wv[15];
+    load_round_tw<LOGN, R>(wv, t, tw);               // in flight during the smem exchange
     if constexpr (R > 0) {
       to_smem<LOGN, R - 1>(a, sm, t);
       __syncthreads();
       from_smem<LOGN, R>(a, sm, t);
       __syncthreads();
     }
-    fwd_round<LOGN, R>(a, t, tw, p, pinv);
+    fwd_round<LOGN, R>(a, wv, p, pinv);
     fwd_rounds_from<LOGN, R + 1>(a, sm, t, tw, p, pinv);
   }
 }
@@ -236,13 +245,15 @@ template <int LOGN, int R>
 __device__ __forceinline__ void inv_rounds_from(double (&a)[16], double *sm, int t, const double *tw,
                                                 const PrimeConsts &pc) {
   if constexpr (R >= 0) {
+    double wv[15];
+    load_round_tw<LOGN, R>(wv, t, tw);
     if constexpr (R < Geom<LOGN>::NR - 1) {
       to_smem<LOGN, R + 1>(a, sm, t);
       __syncthreads();
       from_smem<LOGN, R>(a, sm, t);
       __syncthreads();
     }
-    inv_round<LOGN, R>(a, t, tw, pc);
+    inv_round<LOGN, R>(a, wv, pc);
     inv_rounds_from<LOGN, R - 1>(a, sm, t, tw, pc);
   }
 }
@@ -588,7 +599,7 @@ k_rr_u(uint64_t *__restrict__ u_hat, MaskArgs M, DevParams P) {
 
 
 template <int LOGN, bool RR>
-__global__ void __launch_bounds__(Geom<LOGN>::NT)
+__global__ void __launch_bounds__(Geom<LOGN>::NT, 2)
 k_ntt_inv_mask(const uint64_t *__restrict__ ct_ntt, uint64_t *__restrict__ masked, uint64_t *__restrict__ share,
                MaskArgs M, DevParams P, int c1_only) {
   using Gm = Geom<LOGN>;
@@ -671,11 +682,13 @@ template <int LOGN, int R>
 __device__ __forceinline__ void inv_rounds_live(double (&a)[16], double *sm, int tv, bool act, int bar, int nbar,
                                                 const double *tw, const PrimeConsts &pc) {
   if constexpr (R >= 0) {
+    double wv[15];
+    if (act) load_round_tw<LOGN, R>(wv, tv, tw);
     if (act) to_smem<LOGN, R + 1>(a, sm, tv);
     asm volatile("bar.sync %0, %1;" ::"r"(bar), "r"(nbar) : "memory");
     if (act) from_smem<LOGN, R>(a, sm, tv);
     asm volatile("bar.sync %0, %1;" ::"r"(bar), "r"(nbar) : "memory");
-    if (act) inv_round<LOGN, R>(a, tv, tw, pc);
+    if (act) inv_round<LOGN, R>(a, wv, pc);
     inv_rounds_live<LOGN, R - 1>(a, sm, tv, act, bar, nbar, tw, pc);
   }
 }
@@ -711,7 +724,7 @@ k_intt_c0_pruned(const uint64_t *__restrict__ ct_ntt, uint64_t *__restrict__ mas
     double a[16];
     load_ntt_domain<LOGN>(a, ct_ntt + (((size_t)o * 2) * L + l) * Gm::N, t, pc);
     if constexpr (RR) rr_add_ntt<LOGN>(a, M, o, 0, l, L, t, pc);
-    inv_round<LOGN, Gm::NR - 1>(a, t, P.twd_inv + (size_t)l * Gm::N, pc);
+    { double wv[15]; load_round_tw<LOGN, Gm::NR - 1>(wv, t, P.twd_inv + (size_t)l * Gm::N); inv_round<LOGN, Gm::NR - 1>(a, wv, pc); }
     to_smem<LOGN, Gm::NR - 1>(a, sm + (size_t)l * Gm::SMEM_WORDS, t);
   }
   __syncthreads();
@@ -726,8 +739,10 @@ k_intt_c0_pruned(const uint64_t *__restrict__ ct_ntt, uint64_t *__restrict__ mas
   double *sml = sm + (size_t)l * Gm::SMEM_WORDS;
   double a[16];
   if (act) {
+    double wv[15];
+    load_round_tw<LOGN, Gm::NR - 2>(wv, tv, tw);
     from_smem<LOGN, Gm::NR - 2>(a, sml, tv);
-    inv_round<LOGN, Gm::NR - 2>(a, tv, tw, pc);
+    inv_round<LOGN, Gm::NR - 2>(a, wv, pc);
   }
   inv_rounds_live<LOGN, Gm::NR - 3>(a, sml, tv, act, 1 + l, wpp * 32, tw, pc);
   if (!act) return;
