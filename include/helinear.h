@@ -247,6 +247,37 @@ int hl_he_linear_host(const hl_ctx *ctx, hl_tile tile, const void *wcache, int64
                       void *workspace, uint64_t *dev_ct_out_ntt, uint64_t *dev_ct_masked,
                       uint64_t *dev_share, void *stream);
 
+/* ---- Seeded ciphertext upload ------------------------------------ */
+
+/* The c1 half of every input ciphertext is a = PRF(enc_seed, A, g*L + l) reduced mod p_l (reading
+ * C10; the same stream hl_encrypt / hl_encrypt_device draw), i.e. public randomness the client
+ * need not send: it uploads the c0 halves and the seed, and the server regenerates c1.
+ * hl_expand_seeded writes the c1 halves of ct_in (device [nJ][nK][2][L][N] for (R, Nb)),
+ * leaving the c0 halves untouched; the result is bit-identical to the client's ciphertext.
+ * Stream-ordered; errors: HL_EINVAL (bad tile / sizes / null). */
+int hl_expand_seeded(const hl_ctx *ctx, hl_tile tile, int64_t R, int64_t Nb, uint64_t enc_seed,
+                     uint64_t *ct_in, void *stream);
+
+/* One entry of hl_he_linear_batch_host: the device buffers of a hl_he_linear_batch entry
+ * (dev.ct_in is the upload target) plus pinned host buffers. */
+typedef struct {
+  hl_linear_desc dev;
+  const uint64_t *c0_host;    /* pinned host [nJ][nK][L][N]: the c0 halves of the input ciphertexts */
+  uint64_t enc_seed;          /* the client's encryption seed (c1 regenerated on the device)       */
+  uint64_t *ct_masked_host;   /* pinned host, layout.ct_masked_words (compressed response)         */
+  uint64_t *share_host;       /* pinned host [Nb][Ma] server share                                 */
+} hl_linear_host_desc;
+
+/* The end-to-end form of hl_he_linear_batch (bench.py's e2e leg): for every entry, the c0 halves
+ * are copied host->device (strided into dev.ct_in) and c1 is expanded from enc_seed, the product
+ * runs as in hl_he_linear_batch, and the compressed response + share are copied back to the host
+ * buffers.  Entry i+1 uploads and entry i-1 downloads while entry i computes (the context's upload
+ * / download streams).  Stream-ordered on `stream`: synchronise it before reading the host
+ * outputs.  Results are bit-identical to hl_he_matmul_share on the client's full ciphertexts.
+ * Do not run two batches on one context concurrently. */
+int hl_he_linear_batch_host(const hl_ctx *ctx, hl_tile tile, int n, const hl_linear_host_desc *descs,
+                            void *stream);
+
 /* ---- FC layer, server side --------------------- */
 
 /* With the layer input shared as x = <x>_0 + <x>_1 (client, server), the server's share of

@@ -33,7 +33,8 @@ EXPORTS = ("hl_last_error", "hl_ctx_create", "hl_ctx_destroy", "hl_ctx_params", 
            "hl_mask_and_share", "hl_he_matmul_share", "hl_he_linear_batch", "hl_he_linear_host", "hl_poly_mul",
            "hl_ntt_roundtrip", "hl_timing_enable", "hl_timing_read", "hl_fc_layout", "hl_fc_encode_weights",
            "hl_fc_local_share", "hl_encode_weights_strided", "hl_share_accumulate", "hl_sk_prepare",
-           "hl_encrypt_device", "hl_decrypt_share_device", "hl_pk_gen", "hl_pk_prepare", "hl_he_matmul_share_rr")
+           "hl_encrypt_device", "hl_decrypt_share_device", "hl_pk_gen", "hl_pk_prepare", "hl_he_matmul_share_rr",
+           "hl_expand_seeded", "hl_he_linear_batch_host")
 KERNELS = ("ntt_fwd", "mac", "intt_mask", "intt", "mask", "encode", "other", "fc")   # HL_K_* order
 
 
@@ -61,6 +62,12 @@ class LinearDesc(ctypes.Structure):
     _fields_ = [("wcache", ctypes.c_void_p), ("Ma", ctypes.c_int64), ("R", ctypes.c_int64), ("Nb", ctypes.c_int64),
                 ("ct_in", ctypes.c_void_p), ("workspace", ctypes.c_void_p), ("ct_out_ntt", ctypes.c_void_p),
                 ("seed", ctypes.c_uint64), ("ct_masked", ctypes.c_void_p), ("share", ctypes.c_void_p)]
+
+
+class LinearHostDesc(ctypes.Structure):
+    """hl_linear_host_desc: one product of hl_he_linear_batch_host (device + pinned host pointers)."""
+    _fields_ = [("dev", LinearDesc), ("c0_host", ctypes.c_void_p), ("enc_seed", ctypes.c_uint64),
+                ("ct_masked_host", ctypes.c_void_p), ("share_host", ctypes.c_void_p)]
 
 
 @dataclass(frozen=True)
@@ -122,7 +129,12 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
         "hl_fc_encode_weights": [vp, vp, i64, i64, vp, vp],
         "hl_fc_local_share": [vp, vp, vp, vp, i64, i64, i64, vp, vp, vp],
         "hl_timing_read": [vp, vp, vp],
+        "hl_expand_seeded": [vp, Tile, i64, i64, u64, vp, vp],
+        "hl_he_linear_batch_host": [vp, Tile, i32, ctypes.POINTER(LinearHostDesc), vp],
     }
+    missing = set(EXPORTS) - set(sig) - {"hl_last_error"}
+    if missing:     # an entry point without a prototype would be called with C-int arguments
+        raise ImportError(f"libhelinear binding: no signature for {sorted(missing)}")
     for name, args in sig.items():
         f = getattr(L, name)
         f.argtypes = args
@@ -369,25 +381,55 @@ class Context:
         entries: dicts with wcache, Ma, R, Nb, ct_in, seed and optionally workspace, ct_out_ntt,
         ct_masked, share (allocated here if absent; every entry gets its own buffers).
         Returns [(ct_masked, share), ...]."""
-        import torch
         descs = (LinearDesc * len(entries))()
         keep, outs = [], []
         for d, e in zip(descs, entries):
-            Ma, R, Nb = int(e["Ma"]), int(e["R"]), int(e["Nb"])
-            lay = self.layout(tile, Ma, R, Nb)
-            dev = e["ct_in"].device
-            ws = e.get("workspace") if e.get("workspace") is not None else _dev_empty(lay.workspace_bytes // 8, dev)
-            co = e.get("ct_out_ntt") if e.get("ct_out_ntt") is not None else _dev_empty(lay.ct_out_words, dev)
-            cm = e.get("ct_masked") if e.get("ct_masked") is not None else _dev_empty(lay.ct_masked_words, dev)
-            sh = e.get("share") if e.get("share") is not None else torch.zeros(Nb * Ma, dtype=torch.int64, device=dev)
-            d.wcache, d.Ma, d.R, d.Nb = _dptr(e["wcache"]), Ma, R, Nb
-            d.ct_in, d.workspace, d.ct_out_ntt = _dptr(e["ct_in"]), _dptr(ws), _dptr(co)
-            d.seed, d.ct_masked, d.share = int(e["seed"]), _dptr(cm), _dptr(sh)
-            keep += [ws, co]
-            outs.append((cm, sh))
+            self._fill_desc(tile, d, e, keep, outs)
         _check(_lib.hl_he_linear_batch(self._h, _tile(tile), len(entries), descs, _stream(stream)))
         self._batch_keep = keep        # scratch stays alive until the next batch call
         return outs
+
+    def _fill_desc(self, tile, d, e, keep, outs):
+        import torch
+        Ma, R, Nb = int(e["Ma"]), int(e["R"]), int(e["Nb"])
+        lay = self.layout(tile, Ma, R, Nb)
+        dev = e["ct_in"].device
+        ws = e.get("workspace") if e.get("workspace") is not None else _dev_empty(lay.workspace_bytes // 8, dev)
+        co = e.get("ct_out_ntt") if e.get("ct_out_ntt") is not None else _dev_empty(lay.ct_out_words, dev)
+        cm = e.get("ct_masked") if e.get("ct_masked") is not None else _dev_empty(lay.ct_masked_words, dev)
+        sh = e.get("share") if e.get("share") is not None else torch.zeros(Nb * Ma, dtype=torch.int64, device=dev)
+        d.wcache, d.Ma, d.R, d.Nb = _dptr(e["wcache"]), Ma, R, Nb
+        d.ct_in, d.workspace, d.ct_out_ntt = _dptr(e["ct_in"]), _dptr(ws), _dptr(co)
+        d.seed, d.ct_masked, d.share = int(e["seed"]), _dptr(cm), _dptr(sh)
+        keep += [ws, co]
+        outs.append((cm, sh))
+
+    def expand_seeded(self, tile, R: int, Nb: int, enc_seed: int, ct_in, stream=None):
+        """hl_expand_seeded: regenerate the c1 = a halves of ct_in (CUDA int64 [nJ][nK][2][L][N])
+        from the client's encryption seed."""
+        _check(_lib.hl_expand_seeded(self._h, _tile(tile), R, Nb, enc_seed, _dptr(ct_in), _stream(stream)))
+        return ct_in
+
+    def he_linear_batch_host(self, tile, entries, stream=None):
+        """End-to-end pipelined batch on pinned host buffers (hl_he_linear_batch_host).  entries:
+        the he_linear_batch dicts (ct_in = the device upload buffer, distinct per entry) plus
+        c0_host (pinned CPU int64 [nJ][nK][L][N], see c0_halves), enc_seed, masked_host and
+        share_host (pinned CPU int64).  Stream-ordered: synchronise before reading the host outputs."""
+        descs = (LinearHostDesc * len(entries))()
+        keep, outs = [], []
+        for d, e in zip(descs, entries):
+            self._fill_desc(tile, d.dev, e, keep, outs)
+            d.c0_host, d.enc_seed = e["c0_host"].data_ptr(), int(e["enc_seed"])
+            d.ct_masked_host, d.share_host = e["masked_host"].data_ptr(), e["share_host"].data_ptr()
+            keep += [e["c0_host"], e["masked_host"], e["share_host"]] + [o for o in outs[-1]]
+        _check(_lib.hl_he_linear_batch_host(self._h, _tile(tile), len(entries), descs, _stream(stream)))
+        self._batch_keep = keep
+
+    @staticmethod
+    def c0_halves(ct):
+        """The c0 halves of input ciphertexts [nJ][nK][2][L][N] (what a seeded upload sends):
+        a contiguous [nJ][nK][L][N] array."""
+        return np.ascontiguousarray(np.asarray(ct)[:, :, 0])
 
     def he_linear_host(self, tile, wcache, Ma: int, R: int, Nb: int, ct_in_host, seed: int, ct_masked_host,
                        share_host, dev_ct_in, workspace, dev_ct_out_ntt, dev_ct_masked, dev_share,

@@ -176,3 +176,25 @@ k_decrypt(const uint64_t *__restrict__ masked, uint64_t *__restrict__ share, Dec
     share[row * D.Ma + col] = s & tmask;
   }
 }
+
+// Seeded ciphertext upload (hl_expand_seeded): c1 = a_l of every input ciphertext regenerated from
+// the client's encryption seed -- the same PRF stream (A, g*L + l) and the same reduction as
+// k_encrypt / the host client / the oracle (reading C10), so the expanded ciphertext is
+// bit-identical to the one the client encrypted.  One thread per ChaCha block (4 coefficients).
+__global__ void k_expand_a(uint64_t *__restrict__ ct, int64_t nct, int logn, uint64_t seed, DevParams P) {
+  const int L = P.L, N = 1 << logn;
+  const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t per = (int64_t)L * (N / 4);
+  if (tid >= nct * per) return;
+  const int64_t gi = tid / per;
+  const int l = (int)((tid % per) / (N / 4)), blk = (int)(tid % (N / 4));
+  const PrimeConsts pc = pick(P, l);
+  uint64_t w[8];
+  hl::chacha_block_u64(seed, hl::kDomA, (uint64_t)gi * L + l, (uint32_t)blk, w);
+  uint64_t a[4];
+#pragma unroll
+  for (int i = 0; i < 4; i++) a[i] = mod_u128(w[2 * i + 1], w[2 * i], pc);
+  ulonglong2 *dst = reinterpret_cast<ulonglong2 *>(ct + ((size_t)gi * 2 * L + L + l) * N + 4 * blk);
+  dst[0] = make_ulonglong2(a[0], a[1]);
+  dst[1] = make_ulonglong2(a[2], a[3]);
+}

@@ -229,14 +229,20 @@ extern "C" int hl_ctx_create(uint32_t N, uint32_t L, uint32_t log2_t, const uint
     // are placed before queued NTT blocks of the concurrent low-priority stream
     int lo = 0, hi = 0;
     cudaDeviceGetStreamPriorityRange(&lo, &hi);
-    cudaStream_t aux, mac;
+    cudaStream_t aux, mac, up, down, fwd;
     if (cudaStreamCreateWithPriority(&aux, cudaStreamNonBlocking, lo) != cudaSuccess ||
-        cudaStreamCreateWithPriority(&mac, cudaStreamNonBlocking, hi) != cudaSuccess) {
+        cudaStreamCreateWithPriority(&fwd, cudaStreamNonBlocking, lo) != cudaSuccess ||
+        cudaStreamCreateWithPriority(&mac, cudaStreamNonBlocking, hi) != cudaSuccess ||
+        cudaStreamCreateWithFlags(&up, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaStreamCreateWithFlags(&down, cudaStreamNonBlocking) != cudaSuccess) {
       cudaFree(c->d_tw); cudaFree(c->d_flags); delete c;
       return hl_cuda_check("hl_ctx_create: pipeline streams");
     }
     c->aux_stream = (void *)aux;
     c->mac_stream = (void *)mac;
+    c->up_stream = (void *)up;
+    c->fwd_stream = (void *)fwd;
+    c->down_stream = (void *)down;
   }
   dp.twd_fwd = (const double *)c->d_tw;
   dp.twd_inv = (const double *)c->d_tw + (size_t)L * N;
@@ -298,6 +304,9 @@ extern "C" int hl_ctx_destroy(hl_ctx *c) {
   }
   if (c->aux_stream) cudaStreamDestroy((cudaStream_t)c->aux_stream);
   if (c->mac_stream) cudaStreamDestroy((cudaStream_t)c->mac_stream);
+  if (c->up_stream) cudaStreamDestroy((cudaStream_t)c->up_stream);
+  if (c->fwd_stream) cudaStreamDestroy((cudaStream_t)c->fwd_stream);
+  if (c->down_stream) cudaStreamDestroy((cudaStream_t)c->down_stream);
   if (c->d_tw) cudaFree(c->d_tw);
   if (c->d_flags) cudaFree(c->d_flags);
   if (c->d_cdt) cudaFree(c->d_cdt);

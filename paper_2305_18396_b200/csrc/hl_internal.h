@@ -72,6 +72,9 @@ struct hl_ctx {
   uint64_t *d_cdt = nullptr;          // device copy of the CDT table (device encryption, row f3)
   void *aux_stream = nullptr;         // cudaStream_t (non-blocking, lowest priority): hl_he_linear_batch's NTT stages
   void *mac_stream = nullptr;         // cudaStream_t (non-blocking, highest priority): hl_he_linear_batch's MACs
+  void *fwd_stream = nullptr;         // cudaStream_t (non-blocking, lowest priority): hl_he_linear_batch_host's forward NTTs
+  void *up_stream = nullptr;          // cudaStream_t (non-blocking): hl_he_linear_batch_host's uploads
+  void *down_stream = nullptr;        // cudaStream_t (non-blocking): hl_he_linear_batch_host's downloads
   TimingState *timing = nullptr;      // owned; mutable through const hl_ctx*
 };
 

@@ -1538,10 +1538,15 @@ extern "C" int hl_he_matmul_share(const hl_ctx *c, hl_tile tile, const void *wca
 // the forward NTT of entry i+1 and the inverse NTT + mask of entry i-1 run on its low-priority
 // stream; `stream` is joined to both at the start and at the end.
 // ---------------------------------------------------------------------------------------
-extern "C" int hl_he_linear_batch(const hl_ctx *c, hl_tile tile, int n, const hl_linear_desc *d, void *stream) {
+// ready[i] (optional): event the forward NTT of entry i waits for (its input upload);
+// done[i] (optional): recorded on the auxiliary stream once entry i's results are written.
+// expand_seed (optional, with ready): per entry, the c1 halves are regenerated from this seed on the
+// forward stream before the forward NTT, and every forward NTT is issued up front on the context's
+// upload-side NTT stream so that no entry's inverse NTT queues behind a later entry's upload.
+static void expand_seeded(const hl_ctx *c, int64_t nct, uint64_t enc_seed, uint64_t *ct_in, cudaStream_t st);
+static int linear_batch_run(const hl_ctx *c, hl_tile tile, int n, const hl_linear_desc *d, void *stream,
+                            const cudaEvent_t *ready, const cudaEvent_t *done, const uint64_t *expand_seed) {
   int rc;
-  if ((rc = check_ptrs({c, d}, "hl_he_linear_batch"))) return rc;
-  if (n <= 0) return hl_fail(HL_EINVAL, "hl_he_linear_batch: n must be positive");
   struct Entry { Geo g; MacGeom mg; MaskArgs M; };
   std::vector<Entry> E(n);
   for (int i = 0; i < n; i++) {
@@ -1558,7 +1563,15 @@ extern "C" int hl_he_linear_batch(const hl_ctx *c, hl_tile tile, int n, const hl
     if (cudaEventCreateWithFlags(&e, cudaEventDisableTiming) != cudaSuccess) return hl_cuda_check("hl_he_linear_batch: events");
   cudaEvent_t *e_fwd = ev.data(), *e_mac = ev.data() + n, e_in = ev[2 * n], e_done = ev[2 * n + 1];
   cudaEvent_t e_macs = ev[2 * n + 2];
-  auto fwd = [&](int i) { fwd_ntt(c, d[i].ct_in, d[i].workspace, E[i].g.nJ * 2 * E[i].g.nK, &E[i].mg, s1); };
+  const bool split = ready != nullptr;
+  cudaStream_t sf = split ? (cudaStream_t)c->fwd_stream : s1;
+  auto fwd = [&](int i) {
+    if (ready) cudaStreamWaitEvent(sf, ready[i], 0);
+    if (expand_seed)
+      expand_seeded(c, E[i].g.nJ * E[i].g.nK, expand_seed[i], const_cast<uint64_t *>(d[i].ct_in), sf);
+    fwd_ntt(c, d[i].ct_in, d[i].workspace, E[i].g.nJ * 2 * E[i].g.nK, &E[i].mg, sf);
+    cudaEventRecord(e_fwd[i], sf);
+  };
   auto inv = [&](int i) {
     if (c->N == 4096) launch_inv_mask<12>(c, d[i].ct_out_ntt, d[i].ct_masked, d[i].share, E[i].M, E[i].g.nIs * E[i].g.nK, s1);
     else launch_inv_mask<13>(c, d[i].ct_out_ntt, d[i].ct_masked, d[i].share, E[i].M, E[i].g.nIs * E[i].g.nK, s1);
@@ -1566,8 +1579,12 @@ extern "C" int hl_he_linear_batch(const hl_ctx *c, hl_tile tile, int n, const hl
   cudaEventRecord(e_in, sc);                      // inputs written on `stream` are visible to both streams
   cudaStreamWaitEvent(s0, e_in, 0);
   cudaStreamWaitEvent(s1, e_in, 0);
-  fwd(0);
-  cudaEventRecord(e_fwd[0], s1);
+  if (split) {
+    cudaStreamWaitEvent(sf, e_in, 0);
+    for (int i = 0; i < n; i++) fwd(i);
+  } else {
+    fwd(0);
+  }
   for (int i = 0; i < n; i++) {
     cudaStreamWaitEvent(s0, e_fwd[i], 0);
     static const int mac_smem = [] {
@@ -1577,16 +1594,96 @@ extern "C" int hl_he_linear_batch(const hl_ctx *c, hl_tile tile, int n, const hl
     launch_mac(c, (const uint2 *)d[i].wcache, (const uint32_t *)d[i].workspace, d[i].ct_out_ntt, E[i].mg, s0,
                mac_smem);
     cudaEventRecord(e_mac[i], s0);
-    if (i + 1 < n) { fwd(i + 1); cudaEventRecord(e_fwd[i + 1], s1); }     // overlaps MAC(i)
+    if (!split && i + 1 < n) fwd(i + 1);                                 // overlaps MAC(i)
     cudaStreamWaitEvent(s1, e_mac[i], 0);
     inv(i);                                                               // overlaps MAC(i+1)
+    if (done) cudaEventRecord(done[i], s1);
   }
   cudaEventRecord(e_done, s1);
   cudaEventRecord(e_macs, s0);
   cudaStreamWaitEvent(sc, e_done, 0);
   cudaStreamWaitEvent(sc, e_macs, 0);
+  // (split: every forward NTT precedes a MAC, so sf is joined through s0)
   for (auto &e : ev) cudaEventDestroy(e);         // released once the recorded work completes
   return hl_cuda_check("hl_he_linear_batch: launch");
+}
+
+extern "C" int hl_he_linear_batch(const hl_ctx *c, hl_tile tile, int n, const hl_linear_desc *d, void *stream) {
+  int rc;
+  if ((rc = check_ptrs({c, d}, "hl_he_linear_batch"))) return rc;
+  if (n <= 0) return hl_fail(HL_EINVAL, "hl_he_linear_batch: n must be positive");
+  return linear_batch_run(c, tile, n, d, stream, nullptr, nullptr, nullptr);
+}
+
+// ---------------------------------------------------------------------------------------
+// Seeded ciphertext upload: c1 = a is PRF output of the client's
+// encryption seed (reading C10), so only c0 crosses PCIe and the device regenerates c1.
+// ---------------------------------------------------------------------------------------
+static void expand_seeded(const hl_ctx *c, int64_t nct, uint64_t enc_seed, uint64_t *ct_in, cudaStream_t st) {
+  const int64_t nth = nct * c->L * (c->N / 4);
+  KTimer kt(c, HL_K_OTHER, st);
+  k_expand_a<<<(unsigned)((nth + 255) / 256), 256, 0, st>>>(ct_in, nct, __builtin_ctz((unsigned)c->N), enc_seed, c->dp);
+}
+
+extern "C" int hl_expand_seeded(const hl_ctx *c, hl_tile tile, int64_t R, int64_t Nb, uint64_t enc_seed,
+                                uint64_t *ct_in, void *stream) {
+  int rc;
+  if ((rc = check_ptrs({c, ct_in}, "hl_expand_seeded"))) return rc;
+  Geo g;
+  if ((rc = hl_geometry(c, tile, 1, R, Nb, 0, -1, &g))) return rc;
+  expand_seeded(c, g.nJ * g.nK, enc_seed, ct_in, (cudaStream_t)stream);
+  return hl_cuda_check("hl_expand_seeded: launch");
+}
+
+// End-to-end batch on host buffers: a three-stage pipeline over the entries -- upload of entry
+// i+1 (c0 halves, strided H2D on the context's upload stream, then the c1 expansion) while entry
+// i computes (hl_he_linear_batch's streams) while entry i-1's results download (download stream).
+extern "C" int hl_he_linear_batch_host(const hl_ctx *c, hl_tile tile, int n, const hl_linear_host_desc *h,
+                                       void *stream) {
+  int rc;
+  if ((rc = check_ptrs({c, h}, "hl_he_linear_batch_host"))) return rc;
+  if (n <= 0) return hl_fail(HL_EINVAL, "hl_he_linear_batch_host: n must be positive");
+  std::vector<hl_linear_desc> d(n);
+  std::vector<hl_layout> lay(n);
+  for (int i = 0; i < n; i++) {
+    if ((rc = check_ptrs({h[i].c0_host, h[i].ct_masked_host, h[i].share_host, h[i].dev.ct_in},
+                         "hl_he_linear_batch_host")))
+      return rc;
+    if ((rc = hl_layout_query(c, tile, h[i].dev.Ma, h[i].dev.R, h[i].dev.Nb, 0, -1, &lay[i]))) return rc;
+    d[i] = h[i].dev;
+  }
+  cudaStream_t sc = (cudaStream_t)stream, su = (cudaStream_t)c->up_stream, sd = (cudaStream_t)c->down_stream;
+  std::vector<cudaEvent_t> ev(2 * n + 2);
+  for (auto &e : ev)
+    if (cudaEventCreateWithFlags(&e, cudaEventDisableTiming) != cudaSuccess)
+      return hl_cuda_check("hl_he_linear_batch_host: events");
+  cudaEvent_t *e_up = ev.data(), *e_res = ev.data() + n, e_in = ev[2 * n], e_down = ev[2 * n + 1];
+  cudaEventRecord(e_in, sc);                      // the buffers are free once earlier work on `stream` is done
+  cudaStreamWaitEvent(su, e_in, 0);
+  cudaStreamWaitEvent(sd, e_in, 0);
+  const size_t half = (size_t)c->L * c->N * 8;
+  std::vector<uint64_t> seeds(n);
+  for (int i = 0; i < n; i++) {
+    const int64_t nct = lay[i].ct_in_words / (2 * c->L * c->N);
+    if (cudaMemcpy2DAsync(const_cast<uint64_t *>(d[i].ct_in), 2 * half, h[i].c0_host, half, half, (size_t)nct, cudaMemcpyHostToDevice,
+                          su) != cudaSuccess)
+      return hl_cuda_check("hl_he_linear_batch_host: H2D");
+    cudaEventRecord(e_up[i], su);
+    seeds[i] = h[i].enc_seed;
+  }
+  if ((rc = linear_batch_run(c, tile, n, d.data(), stream, e_up, e_res, seeds.data()))) return rc;
+  for (int i = 0; i < n; i++) {
+    cudaStreamWaitEvent(sd, e_res[i], 0);
+    if (cudaMemcpyAsync(h[i].ct_masked_host, d[i].ct_masked, (size_t)lay[i].ct_masked_words * 8,
+                        cudaMemcpyDeviceToHost, sd) != cudaSuccess ||
+        cudaMemcpyAsync(h[i].share_host, d[i].share, (size_t)lay[i].share_words * 8, cudaMemcpyDeviceToHost,
+                        sd) != cudaSuccess)
+      return hl_cuda_check("hl_he_linear_batch_host: D2H");
+  }
+  cudaEventRecord(e_down, sd);
+  cudaStreamWaitEvent(sc, e_down, 0);
+  for (auto &e : ev) cudaEventDestroy(e);
+  return hl_cuda_check("hl_he_linear_batch_host: launch");
 }
 
 // ---------------------------------------------------------------------------------------

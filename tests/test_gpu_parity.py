@@ -250,6 +250,61 @@ def test_linear_batch_c2_equals_single_calls(hl, ctx4096):
             assert np.array_equal(hl.to_host(sh), es), mm.name
 
 
+@pytest.mark.parametrize("N", [4096, 8192])
+def test_expand_seeded_vs_oracle_encrypt(hl, ctx4096, ctx8192, N):
+    """Seeded upload: c1 regenerated on the device from the encryption seed equals the oracle
+    client's c1 = a bit for bit (both PRF streams, reading C10); c0 halves are left untouched."""
+    import torch
+    ctx = ctx4096 if N == 4096 else ctx8192
+    P = _P(ctx)
+    tile = (16, 8, 32) if N == 4096 else (32, 16, 16)
+    Nb, R, seed = 40, 72, 4242 + N
+    X = synth.activations(seed, Nb, R)
+    sk = ref.keygen(P, seed + 1)
+    ct = ref.encrypt(P, tile, sk, X, seed + 2)
+    up = ct.copy()
+    up[:, :, 1] = 0x5a5a5a5a                       # garbage where c1 will be regenerated
+    dev = hl.to_device(up)
+    ctx.expand_seeded(tile, R, Nb, seed + 2, dev)
+    _sync()
+    assert np.array_equal(hl.to_host(dev).reshape(ct.shape), ct)
+
+
+def test_linear_batch_host_seeded_c1_vs_oracle(hl, ctx4096):
+    """hl_he_linear_batch_host (bench.py's e2e call): only the c0 halves + the encryption seed go
+    host->device, results come back to pinned host buffers; every product's compressed response
+    and share bit-exact against the oracle client + server, repeated to catch stream races."""
+    import torch
+    ctx = ctx4096
+    cfg = synth.CONFIGS["c1"]
+    P = _P(ctx)
+    entries, exp = [], []
+    for mi, mm in enumerate(cfg.matmuls):
+        X = synth.activations(synth.seed_for(0, mi, "x"), mm.Nb, mm.R)
+        W = synth.weights(synth.seed_for(0, mi, "w"), mm.R, mm.Ma)
+        sk = ref.keygen(P, synth.seed_for(0, mi, "key"))
+        es = synth.seed_for(0, mi, "enc")
+        ct = ref.encrypt(P, cfg.tile, sk, X, es)
+        seed = synth.seed_for(0, mi, "mask")
+        lay = ctx.layout(cfg.tile, mm.Ma, mm.R, mm.Nb)
+        c0 = torch.from_numpy(hl.Context.c0_halves(ct).view(np.int64).reshape(-1)).pin_memory()
+        entries.append(dict(wcache=ctx.encode_weights(cfg.tile, hl.to_device(W)), Ma=mm.Ma, R=mm.R, Nb=mm.Nb,
+                            ct_in=torch.full((lay.ct_in_words,), 7, dtype=torch.int64, device="cuda"),
+                            seed=seed, c0_host=c0, enc_seed=es,
+                            masked_host=torch.zeros(lay.ct_masked_words, dtype=torch.int64).pin_memory(),
+                            share_host=torch.zeros(lay.share_words, dtype=torch.int64).pin_memory()))
+        exp.append(ref.mask_and_share(P, cfg.tile, ref.he_matmul(P, cfg.tile, W, ct, mm.Nb), mm.Ma, mm.Nb, seed))
+    for rep in range(3):
+        for e in entries:
+            e["masked_host"].zero_()
+            e["share_host"].zero_()
+        ctx.he_linear_batch_host(cfg.tile, entries)
+        _sync()
+        for mm, e, (em, es_) in zip(cfg.matmuls, entries, exp):
+            assert np.array_equal(e["masked_host"].numpy().view(np.uint64).reshape(em.shape), em), (rep, mm.name)
+            assert np.array_equal(e["share_host"].numpy().view(np.uint64).reshape(es_.shape), es_), (rep, mm.name)
+
+
 def test_bert_base_full_size_sampled(hl, ctx4096):
     """Config c2 at full size in the bench's launch configuration (fused call, default tile):
     sampled output tiles bit-exact against the oracle (its own scalar NTT), and for the whole
