@@ -246,13 +246,13 @@ __device__ __forceinline__ void inv_rounds_from(double (&a)[16], double *sm, int
                                                 const PrimeConsts &pc) {
   if constexpr (R >= 0) {
     double wv[15];
-    load_round_tw<LOGN, R>(wv, t, tw);
     if constexpr (R < Geom<LOGN>::NR - 1) {
       to_smem<LOGN, R + 1>(a, sm, t);
       __syncthreads();
       from_smem<LOGN, R>(a, sm, t);
       __syncthreads();
     }
+    load_round_tw<LOGN, R>(wv, t, tw);
     inv_round<LOGN, R>(a, wv, pc);
     inv_rounds_from<LOGN, R - 1>(a, sm, t, tw, pc);
   }
@@ -599,7 +599,7 @@ k_rr_u(uint64_t *__restrict__ u_hat, MaskArgs M, DevParams P) {
 
 
 template <int LOGN, bool RR>
-__global__ void __launch_bounds__(Geom<LOGN>::NT, 2)
+__global__ void __launch_bounds__(Geom<LOGN>::NT, LOGN == 12 ? 2 : 1)
 k_ntt_inv_mask(const uint64_t *__restrict__ ct_ntt, uint64_t *__restrict__ masked, uint64_t *__restrict__ share,
                MaskArgs M, DevParams P, int c1_only) {
   using Gm = Geom<LOGN>;
@@ -683,11 +683,11 @@ __device__ __forceinline__ void inv_rounds_live(double (&a)[16], double *sm, int
                                                 const double *tw, const PrimeConsts &pc) {
   if constexpr (R >= 0) {
     double wv[15];
-    if (act) load_round_tw<LOGN, R>(wv, tv, tw);
     if (act) to_smem<LOGN, R + 1>(a, sm, tv);
     asm volatile("bar.sync %0, %1;" ::"r"(bar), "r"(nbar) : "memory");
     if (act) from_smem<LOGN, R>(a, sm, tv);
     asm volatile("bar.sync %0, %1;" ::"r"(bar), "r"(nbar) : "memory");
+    if (act) load_round_tw<LOGN, R>(wv, tv, tw);
     if (act) inv_round<LOGN, R>(a, wv, pc);
     inv_rounds_live<LOGN, R - 1>(a, sm, tv, act, bar, nbar, tw, pc);
   }
