@@ -45,13 +45,12 @@ def _peaks():
 
 
 # ----------------------------------------------------------------------------- algorithmic counts
-def counts(cfg, lay_by_mm):
+def counts(cfg, lay_by_mm, tiles):
     """Per-matmul algorithmic work: MACs, butterflies, bytes of each kernel."""
     N, L = cfg.N, cfg.L
-    m, r, n = cfg.tile
     out = []
     logN = N.bit_length() - 1
-    for mm, lay in zip(cfg.matmuls, lay_by_mm):
+    for mm, lay, (m, r, n) in zip(cfg.matmuls, lay_by_mm, tiles):
         nI, nJ, nK = lay.nI_shard, lay.nJ, lay.nK     # this rank's I tiles
         nC = 2 * nK
         P = nI * nJ * nK
@@ -132,8 +131,10 @@ def run_ours(args, rank, world, local_rank):
     torch.cuda.set_device(local_rank)
     dev = torch.device("cuda", local_rank)
     cfg = synth.CONFIGS[args.config]
-    tile = tuple(args.tile) if args.tile else cfg.tile
+    tiles = _tiles(cfg, args)
     ctx = hl.Context(cfg.N, cfg.L, synth.T_BITS, device=local_rank)
+    if not args.tile and cfg.tiles:     # the bench's tiles are the library planner's choices (hl_plan_tile)
+        assert all(ctx.plan_tile(mm.Ma, mm.R, mm.Nb) == t for mm, t in zip(cfg.matmuls, tiles)), 'planner drift'
     shard = args.mode == "shard"
     # weak: every rank owns one independently seeded block, no data-path collective.
     # shard: one block; its I tiles (output columns) are split over the ranks,
@@ -146,6 +147,7 @@ def run_ours(args, rank, world, local_rank):
     t_enc = 0.0
     from paper_2305_18396_b200 import dist as hd
     for mi, mm in enumerate(cfg.matmuls):
+        tile = tiles[mi]
         nI_full = ctx.layout(tile, mm.Ma, mm.R, mm.Nb).nI
         i0, i1 = hd.shard_range(nI_full, world, rank) if shard else (0, nI_full)
         lay = ctx.layout(tile, mm.Ma, mm.R, mm.Nb, i0, i1)
@@ -163,7 +165,7 @@ def run_ours(args, rank, world, local_rank):
         torch.cuda.synchronize()
         t_enc += time.perf_counter() - t0
         del dW
-        mats.append(dict(mm=mm, lay=lay, wc=wc, ct=ct_dev, i0=i0, i1=i1, nI_full=nI_full, s_hat=s_hat, dX=dX,
+        mats.append(dict(mm=mm, tile=tile, lay=lay, wc=wc, ct=ct_dev, i0=i0, i1=i1, nI_full=nI_full, s_hat=s_hat, dX=dX,
                          ct_host=torch.from_numpy(ct_host.view(np.int64).reshape(-1)).pin_memory(),
                          c0_host=torch.from_numpy(hl.Context.c0_halves(ct_host.reshape(lay.nJ, lay.nK, 2, -1)).view(np.int64).reshape(-1)).pin_memory(),
                          enc_seed=synth.seed_for(block, mi, "enc"),
@@ -180,14 +182,14 @@ def run_ours(args, rank, world, local_rank):
     for m in mats:
         m["ws"] = torch.empty(m["lay"].workspace_bytes // 8, dtype=torch.int64, device=dev)
         m["co"] = torch.empty(m["lay"].ct_out_words, dtype=torch.int64, device=dev)
-    entries = [dict(wcache=m["wc"], Ma=m["mm"].Ma, R=m["mm"].R, Nb=m["mm"].Nb, ct_in=m["ct"], seed=m["seed"],
+    entries = [dict(wcache=m["wc"], Ma=m["mm"].Ma, R=m["mm"].R, Nb=m["mm"].Nb, ct_in=m["ct"], seed=m["seed"], tile=m["tile"],
                     workspace=m["ws"], ct_out_ntt=m["co"], ct_masked=m["masked"], share=m["share"]) for m in mats]
 
     def step():
         if shard:
-            per_ct = cfg.L * (tile[0] * tile[2] + cfg.N)
             for m in mats:
-                mm = m["mm"]
+                mm, tile = m["mm"], m["tile"]
+                per_ct = cfg.L * (tile[0] * tile[2] + cfg.N)
                 ctx.he_matmul_share(tile, m["wc"], mm.Ma, mm.R, mm.Nb, m["ct"], m["seed"], True, m["i0"], m["i1"],
                                     workspace=workspace, ct_out_ntt=ct_out_ntt, ct_masked=m["masked"],
                                     share=m["share"], stream=stream)
@@ -196,12 +198,12 @@ def run_ours(args, rank, world, local_rank):
                                         mm.Nb, dst=0)
         elif args.sequential:
             for m in mats:
-                mm = m["mm"]
+                mm, tile = m["mm"], m["tile"]
                 ctx.he_matmul_share(tile, m["wc"], mm.Ma, mm.R, mm.Nb, m["ct"], m["seed"], True,
                                     workspace=workspace, ct_out_ntt=ct_out_ntt, ct_masked=m["masked"],
                                     share=m["share"], stream=stream)
         else:
-            ctx.he_linear_batch(tile, entries, stream=stream)
+            ctx.he_linear_batch(tiles[0], entries, stream=stream)
 
     def barrier():
         if world > 1:
@@ -281,12 +283,12 @@ def run_ours(args, rank, world, local_rank):
 
         def enc_step():
             for m, ct in zip(mats, cts):
-                ctx.encrypt_device(m["s_hat"], tile, m["dX"], synth.seed_for(block, 0, "enc") + 99, ct_in=ct,
+                ctx.encrypt_device(m["s_hat"], m["tile"], m["dX"], synth.seed_for(block, 0, "enc") + 99, ct_in=ct,
                                    stream=stream)
 
         def dec_step():
             for m, sh in zip(mats, shc):
-                ctx.decrypt_share_device(m["s_hat"], tile, m["masked"], m["mm"].Ma, m["mm"].Nb, share=sh,
+                ctx.decrypt_share_device(m["s_hat"], m["tile"], m["masked"], m["mm"].Ma, m["mm"].Nb, share=sh,
                                          stream=stream)
         enc_step(); dec_step()
         torch.cuda.synchronize()
@@ -315,7 +317,7 @@ def run_ours(args, rank, world, local_rank):
         def rr_step():
             for m in mats:
                 mm = m["mm"]
-                ctx.he_matmul_share_rr(tile, m["wc"], mm.Ma, mm.R, mm.Nb, m["ct"], m["seed"], pk_hat, 58, stream=stream)
+                ctx.he_matmul_share_rr(m["tile"], m["wc"], mm.Ma, mm.R, mm.Nb, m["ct"], m["seed"], pk_hat, 58, stream=stream)
         rr_step()
         torch.cuda.synchronize()
         nrep = max(2, min(args.steps, 10))
@@ -379,11 +381,11 @@ def run_ours(args, rank, world, local_rank):
 
     def e2e_step():
         if not shard:
-            ctx.he_linear_batch_host(tile, host_entries, stream=stream)
+            ctx.he_linear_batch_host(tiles[0], host_entries, stream=stream)
             return
         for m, hm, hs in zip(mats, host_masked, host_share):
             mm = m["mm"]
-            ctx.he_linear_host(tile, m["wc"], mm.Ma, mm.R, mm.Nb, m["ct_host"], m["seed"], hm, hs, dev_ct_in,
+            ctx.he_linear_host(m["tile"], m["wc"], mm.Ma, mm.R, mm.Nb, m["ct_host"], m["seed"], hm, hs, dev_ct_in,
                                workspace, ct_out_ntt, m["masked"], m["share"], compress=True, stream=stream)
 
     e2e_steps = max(3, min(args.steps, 20))
@@ -413,7 +415,7 @@ def run_ours(args, rank, world, local_rank):
     # ---------------- numbers
     ms_step = elapsed / args.steps
     value = ms_step if shard else elapsed / (args.steps * world)   # ms per block (all ranks' blocks)
-    cnt = counts(cfg, [m["lay"] for m in mats])
+    cnt = counts(cfg, [m["lay"] for m in mats], tiles)
     products = sum(c["products"] for c in cnt)
     peaks = _peaks()
     hbm = peaks.get("hbm_gbs")
@@ -471,7 +473,9 @@ def run_ours(args, rank, world, local_rank):
         "scaling": "strong" if shard else "weak",
         "vs_baseline": None, "dtype": "u64", "data": "synthetic",
         "config": {"workload": f"{cfg.name}: {cfg.note}", "N": cfg.N, "L": cfg.L, "t_bits": synth.T_BITS,
-                   "tile": list(tile), "matmuls": [[mm.Nb, mm.R, mm.Ma] for mm in cfg.matmuls],
+                   "tile": [list(t) for t in tiles],
+                   "tile_choice": "--tile override" if args.tile else "per product, hl_plan_tile (DESIGN.md §5)",
+                   "matmuls": [[mm.Nb, mm.R, mm.Ma] for mm in cfg.matmuls],
                    "blocks_per_step_per_rank": 1, "compress": True,
                    "l2": "inputs larger than L2: 3.6 GB NTT-domain weight cache + 352 MB ct_in per block",
                    "parallelism": (f"shard x{world} (I tiles of one block per rank, responses gathered to rank 0)"
@@ -500,22 +504,23 @@ def run_ours(args, rank, world, local_rank):
     if rr_info:
         line["rerandomized"] = rr_info
     if world == 1 and not args.no_cpu_baseline:
-        line["cpu_baseline"] = oracle_baseline(cfg, tile, args.cpu_itiles)
+        line["cpu_baseline"] = oracle_baseline(cfg, tiles, args.cpu_itiles)
     return line
 
 
 # ----------------------------------------------------------------------------- the oracle arm
-def oracle_baseline(cfg, tile, itiles: int, ktiles: int = 0):
+def oracle_baseline(cfg, tiles, itiles: int, ktiles: int = 0):
     """The CPU oracle as it stands (sparse schoolbook he_matmul + mask; OpenMP over output
     ciphertext x component x prime) on a bounded sample: the first `itiles` I tiles and the first
     `ktiles` K tiles (0 = all) of each matmul, all J, extrapolated linearly to the whole block
     (oracle work is exactly linear in the number of output ciphertexts)."""
     from oracle import ref
     P = ref.bfv_params(cfg.N, cfg.L, synth.T_BITS)
-    m, r, n = tile
     total_s = 0.0
     sampled = total = 0
     for mi, mm in enumerate(cfg.matmuls):
+        tile = tiles[mi]
+        m, r, n = tile
         nI, nJ, nK = ref.tile_counts(tile, mm.Ma, mm.R, mm.Nb)
         s = min(itiles, nI)
         kk = nK if ktiles <= 0 else min(ktiles, nK)
@@ -537,6 +542,11 @@ def oracle_baseline(cfg, tile, itiles: int, ktiles: int = 0):
             "cpu": _cpu_model()}
 
 
+def _tiles(cfg, args):
+    """Per-product tiles: --tile for all, else the config's (synth: hl_plan_tile's choices for c2)."""
+    return [tuple(args.tile)] * len(cfg.matmuls) if args.tile else [cfg.tile_of(i) for i in range(len(cfg.matmuls))]
+
+
 def _cpu_model():
     try:
         for ln in open("/proc/cpuinfo"):
@@ -551,15 +561,15 @@ def run_reference(args, rank, world):
     if rank != 0:
         return None
     cfg = synth.CONFIGS[args.config]
-    tile = tuple(args.tile) if args.tile else cfg.tile
+    tiles = _tiles(cfg, args)
     vals = []
     # the same bounded sample as our arm's cpu_baseline (first 2 I tiles x all K tiles of each product:
     # 32 output ciphertexts, enough OpenMP tasks for the host's cores), extrapolated to the block
     for _ in range(min(args.warmup, 1)):
-        oracle_baseline(cfg, tile, 2, 0)
+        oracle_baseline(cfg, tiles, 2, 0)
     t0 = time.perf_counter()
     for _ in range(args.steps):
-        vals.append(oracle_baseline(cfg, tile, 2, 0)["value"])
+        vals.append(oracle_baseline(cfg, tiles, 2, 0)["value"])
     wall = time.perf_counter() - t0
     v = float(np.mean(vals))
     base = oracle_baseline.__doc__
@@ -568,10 +578,10 @@ def run_reference(args, rank, world):
             "warmup": args.warmup, "ms_per_step": round(v, 1), "higher_is_better": False, "scaling": "weak",
             "vs_baseline": None, "dtype": "u64", "data": "synthetic", "impl": "reference",
             "config": {"workload": f"{cfg.name}: {cfg.note}", "N": cfg.N, "L": cfg.L, "t_bits": synth.T_BITS,
-                       "tile": list(tile), "parallelism": "CPU oracle, OpenMP over output tiles"},
+                       "tile": [list(t) for t in tiles], "parallelism": "CPU oracle, OpenMP over output tiles"},
             "cpu_baseline": {"value": round(v, 1), "unit": UNIT, "cores": cores, "kind": "oracle",
-                             "sample": "per step: the first 2 I tiles x all K tiles of each of the 4 matmuls "
-                                       "(32 of 1728 output ciphertexts), extrapolated linearly to the block",
+                             "sample": "per step: the first 2 I tiles x all K tiles of each of the 4 matmuls, "
+                                       "extrapolated linearly to the block",
                              "cpu": _cpu_model(),
                              "wall_s": round(wall, 2)},
             "e2e": {"value": round(v, 1), "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},

@@ -112,6 +112,17 @@ int hl_ctx_set_mac_engine(hl_ctx *ctx, int engine);
 /* Copy the primes and Delta mod p_l (Delta = floor(q/t), reading C5) into caller arrays of L. */
 int hl_ctx_params(const hl_ctx *ctx, uint64_t *primes_out, uint64_t *delta_mod_out);
 
+/* Tile planner (reading C2: the tile is an explicit protocol parameter; the client encrypts and
+ * decrypts with the tile the server announces).  Among the power-of-two tiles with m*r*n <= N,
+ * m <= Ma, r <= R, n <= Nb (each rounded up to a power of two) it returns the one minimising a
+ * cost model of the GPU path, calibrated on B200:
+ *   T = Wbytes / (6.2 TB/s * e_mac) + 0.17 us * nJ*nK + 0.14 us * nI*nK
+ * Wbytes = the padded weight cache (layout.wcache_bytes), nJ*nK forward and nI*nK inverse
+ * transforms (ciphertexts), e_mac = (nC <= 4 ? 1 : nC <= 8 ? 0.85 : 0.5) * min(1, nI/96), nC = 2 nK
+ * the MAC's columns.  Ties keep the first candidate (m, then r, then n descending).
+ * c2 (BERT-base): QKV, FF1 -> (16, 8, 32); O -> (8, 8, 64); FF2 -> (4, 32, 32). */
+int hl_plan_tile(const hl_ctx *ctx, int64_t Ma, int64_t R, int64_t Nb, hl_tile *out);
+
 /* Sizes of every buffer of one matmul (Ma x R weights, Nb tokens) for I-tile shard [i_begin, i_end). */
 int hl_layout_query(const hl_ctx *ctx, hl_tile tile, int64_t Ma, int64_t R, int64_t Nb,
                     int64_t i_begin, int64_t i_end, hl_layout *out);
@@ -227,6 +238,7 @@ typedef struct {
   uint64_t seed;              /* mask seed (as hl_mask_and_share)                                  */
   uint64_t *ct_masked;        /* device, layout.ct_masked_words (compressed response)              */
   uint64_t *share;            /* device [Nb][Ma] server share                                      */
+  hl_tile tile;               /* this product's tile; m == 0: the tile argument of the batch call  */
 } hl_linear_desc;
 
 /* n compressed hl_he_matmul_share calls, e.g. the four products of an encoder block; results are

@@ -27,7 +27,7 @@ _CODES = {HL_EINVAL: "HL_EINVAL", HL_EDIM: "HL_EDIM", HL_ERANGE: "HL_ERANGE", HL
           HL_ECUDA: "HL_ECUDA", HL_ENOTSUP: "HL_ENOTSUP"}
 
 # every symbol include/helinear.h declares (checked by tests/test_abi.py)
-EXPORTS = ("hl_last_error", "hl_ctx_create", "hl_ctx_destroy", "hl_ctx_params", "hl_ctx_set_mac_engine",
+EXPORTS = ("hl_last_error", "hl_ctx_create", "hl_ctx_destroy", "hl_ctx_params", "hl_ctx_set_mac_engine", "hl_plan_tile",
            "hl_layout_query",
            "hl_keygen", "hl_encrypt", "hl_decrypt_share", "hl_encode_weights", "hl_he_matmul",
            "hl_mask_and_share", "hl_he_matmul_share", "hl_he_linear_batch", "hl_he_linear_host", "hl_poly_mul",
@@ -61,7 +61,8 @@ class LinearDesc(ctypes.Structure):
     """hl_linear_desc: one product of hl_he_linear_batch (device pointers)."""
     _fields_ = [("wcache", ctypes.c_void_p), ("Ma", ctypes.c_int64), ("R", ctypes.c_int64), ("Nb", ctypes.c_int64),
                 ("ct_in", ctypes.c_void_p), ("workspace", ctypes.c_void_p), ("ct_out_ntt", ctypes.c_void_p),
-                ("seed", ctypes.c_uint64), ("ct_masked", ctypes.c_void_p), ("share", ctypes.c_void_p)]
+                ("seed", ctypes.c_uint64), ("ct_masked", ctypes.c_void_p), ("share", ctypes.c_void_p),
+                ("tile", Tile)]
 
 
 class LinearHostDesc(ctypes.Structure):
@@ -105,6 +106,7 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
         "hl_ctx_params": [vp, vp, vp],
         "hl_ctx_set_mac_engine": [vp, i32],
         "hl_layout_query": [vp, Tile, i64, i64, i64, i64, i64, ctypes.POINTER(_Layout)],
+        "hl_plan_tile": [vp, i64, i64, i64, ctypes.POINTER(Tile)],
         "hl_keygen": [vp, u64, vp],
         "hl_encrypt": [vp, vp, Tile, vp, i64, i64, u64, vp],
         "hl_decrypt_share": [vp, vp, Tile, vp, i32, i64, i64, vp],
@@ -223,6 +225,12 @@ class Context:
         return Layout(*[getattr(out, f) for f, _ in _Layout._fields_])
 
     # ---------------------------------------------------------------- client (host memory)
+    def plan_tile(self, Ma: int, R: int, Nb: int) -> tuple:
+        """hl_plan_tile: the planner's (m, r, n) for an Nb x R . R x Ma product."""
+        t = Tile()
+        _check(_lib.hl_plan_tile(self._h, Ma, R, Nb, ctypes.byref(t)))
+        return (t.m, t.r, t.n)
+
     def keygen(self, seed: int) -> np.ndarray:
         sk = np.zeros(self.N, dtype=np.int8)
         _check(_lib.hl_keygen(self._h, seed, sk.ctypes.data))
@@ -378,8 +386,9 @@ class Context:
 
     def he_linear_batch(self, tile, entries, stream=None):
         """Pipelined compressed he_matmul_share over several products (hl_he_linear_batch).
-        entries: dicts with wcache, Ma, R, Nb, ct_in, seed and optionally workspace, ct_out_ntt,
-        ct_masked, share (allocated here if absent; every entry gets its own buffers).
+        entries: dicts with wcache, Ma, R, Nb, ct_in, seed and optionally tile (this product's tile;
+        default: `tile`), workspace, ct_out_ntt, ct_masked, share (allocated here if absent; every
+        entry gets its own buffers).
         Returns [(ct_masked, share), ...]."""
         descs = (LinearDesc * len(entries))()
         keep, outs = [], []
@@ -392,6 +401,7 @@ class Context:
     def _fill_desc(self, tile, d, e, keep, outs):
         import torch
         Ma, R, Nb = int(e["Ma"]), int(e["R"]), int(e["Nb"])
+        tile = tuple(e["tile"]) if e.get("tile") is not None else tuple(tile)
         lay = self.layout(tile, Ma, R, Nb)
         dev = e["ct_in"].device
         ws = e.get("workspace") if e.get("workspace") is not None else _dev_empty(lay.workspace_bytes // 8, dev)
@@ -401,6 +411,7 @@ class Context:
         d.wcache, d.Ma, d.R, d.Nb = _dptr(e["wcache"]), Ma, R, Nb
         d.ct_in, d.workspace, d.ct_out_ntt = _dptr(e["ct_in"]), _dptr(ws), _dptr(co)
         d.seed, d.ct_masked, d.share = int(e["seed"]), _dptr(cm), _dptr(sh)
+        d.tile = _tile(tile)
         keep += [ws, co]
         outs.append((cm, sh))
 

@@ -375,6 +375,34 @@ extern "C" int hl_layout_query(const hl_ctx *c, hl_tile tile, int64_t Ma, int64_
   return HL_OK;
 }
 
+// Tile planner: the cost model of include/helinear.h (constants from the B200 tile sweep,
+// tools/gpu/tile_sweep.py).  Candidates: powers of two with m*r*n <= N and
+// m <= Ma, r <= R, n <= Nb rounded up to a power of two (padded tiles cost what they move).
+extern "C" int hl_plan_tile(const hl_ctx *c, int64_t Ma, int64_t R, int64_t Nb, hl_tile *out) {
+  if (!c || !out) return hl_fail(HL_EINVAL, "hl_plan_tile: ctx or out is NULL");
+  if (Ma <= 0 || R <= 0 || Nb <= 0) return hl_fail(HL_EINVAL, "hl_plan_tile: Ma, R, Nb must be positive");
+  auto ceil_pow2 = [](int64_t v) { int64_t p = 1; while (p < v) p <<= 1; return p; };
+  const int64_t N = c->N, mmax = std::min<int64_t>(ceil_pow2(Ma), N), rmax = std::min<int64_t>(ceil_pow2(R), N),
+                nmax = std::min<int64_t>(ceil_pow2(Nb), N);
+  double best = 0;
+  bool found = false;
+  for (int64_t m = mmax; m >= 1; m >>= 1)
+    for (int64_t r = rmax; r >= 1; r >>= 1)
+      for (int64_t n = nmax; n >= 1; n >>= 1) {
+      if (m * r * n > N) continue;
+      hl_tile t{(int32_t)m, (int32_t)r, (int32_t)n};
+      hl_layout lay;
+      if (hl_layout_query(c, t, Ma, R, Nb, 0, -1, &lay) != HL_OK) continue;
+      const double nC = 2.0 * lay.nK;
+      const double e_mac = (nC <= 4 ? 1.0 : nC <= 8 ? 0.85 : 0.5) * std::min(1.0, (double)lay.nI / 96.0);
+      const double cost = (double)lay.wcache_bytes / (6.2e12 * e_mac) + 0.17e-6 * (double)(lay.nJ * lay.nK) +
+                          0.14e-6 * (double)(lay.nI * lay.nK);
+      if (!found || cost < best) { best = cost; *out = t; found = true; }
+    }
+  if (!found) return hl_fail(HL_EDIM, "hl_plan_tile: no tile fits the problem");
+  return HL_OK;
+}
+
 // ---------------------------------------------------------------------------------------
 // host NTT (client side).  Same transform as the device kernels: merged-psi Cooley-Tukey
 // forward (natural -> bit-reversed), Gentleman-Sande inverse (bit-reversed -> natural).

@@ -1553,7 +1553,7 @@ static int linear_batch_run(const hl_ctx *c, hl_tile tile, int n, const hl_linea
     if ((rc = check_ptrs({c, d[i].wcache, d[i].ct_in, d[i].workspace, d[i].ct_out_ntt, d[i].ct_masked, d[i].share},
                          "hl_he_linear_batch")))
       return rc;
-    if ((rc = hl_geometry(c, tile, d[i].Ma, d[i].R, d[i].Nb, 0, -1, &E[i].g))) return rc;
+    if ((rc = hl_geometry(c, d[i].tile.m ? d[i].tile : tile, d[i].Ma, d[i].R, d[i].Nb, 0, -1, &E[i].g))) return rc;
     E[i].mg = mac_geom(c, E[i].g.nIs, E[i].g.nJ, 2 * E[i].g.nK);
     E[i].M = mask_args(E[i].g, d[i].Ma, d[i].Nb, d[i].seed);
   }
@@ -1649,7 +1649,9 @@ extern "C" int hl_he_linear_batch_host(const hl_ctx *c, hl_tile tile, int n, con
     if ((rc = check_ptrs({h[i].c0_host, h[i].ct_masked_host, h[i].share_host, h[i].dev.ct_in},
                          "hl_he_linear_batch_host")))
       return rc;
-    if ((rc = hl_layout_query(c, tile, h[i].dev.Ma, h[i].dev.R, h[i].dev.Nb, 0, -1, &lay[i]))) return rc;
+    if ((rc = hl_layout_query(c, h[i].dev.tile.m ? h[i].dev.tile : tile, h[i].dev.Ma, h[i].dev.R, h[i].dev.Nb, 0,
+                              -1, &lay[i])))
+      return rc;
     d[i] = h[i].dev;
   }
   cudaStream_t sc = (cudaStream_t)stream, su = (cudaStream_t)c->up_stream, sd = (cudaStream_t)c->down_stream;

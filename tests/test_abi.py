@@ -91,6 +91,26 @@ def test_layout_and_dims(hl):
     assert e.value.code == hl.HL_EINVAL
 
 
+def test_plan_tile(hl):
+    """hl_plan_tile (host logic, no GPU): valid power-of-two tiles with m*r*n = N, the c2 choices
+    that synth.CONFIGS['c2'].tiles (the bench's tiles) records, and the argument checks."""
+    ctx = hl.Context(4096, 2, 37, device=-1)
+    cfg = synth.CONFIGS["c2"]
+    for mi, mm in enumerate(cfg.matmuls):
+        t = ctx.plan_tile(mm.Ma, mm.R, mm.Nb)
+        assert t == cfg.tile_of(mi), (mm.name, t)
+    for shape in [(1, 1, 1), (7, 300, 5), (4096, 4096, 4096), (128, 3072, 768)]:
+        m, r, n = ctx.plan_tile(*shape)
+        assert m * r * n <= 4096 and all(v & (v - 1) == 0 for v in (m, r, n))
+        assert m <= 2 * shape[0] and r <= 2 * shape[1] and n <= 2 * shape[2]
+        assert m * r * n == 4096 or (m >= shape[0] and r >= shape[1] and n >= shape[2])
+        ctx.layout((m, r, n), *shape)                   # accepted by the geometry check
+    assert hl.Context(8192, 3, 37, device=-1).plan_tile(1024, 1024, 2048)[0] > 0
+    with pytest.raises(hl.HLError) as e:
+        ctx.plan_tile(0, 8, 8)
+    assert e.value.code == hl.HL_EINVAL
+
+
 def test_keygen_matches_oracle(hl):
     ctx = hl.Context(4096, 2, 37, device=-1)
     P = ref.bfv_params(4096, 2, 37)

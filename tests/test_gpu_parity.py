@@ -199,12 +199,13 @@ def test_bert_tiny_block_c1(hl, ctx4096):
         assert np.array_equal(hl.to_host(s).reshape(es.shape), es), mm.name
 
 
-def _block_inputs(ctx, cfg, block=0):
+def _block_inputs(ctx, cfg, block=0, tiles=None):
     P = _P(ctx)
     out = []
     for mi, mm in enumerate(cfg.matmuls):
+        tile = tiles[mi] if tiles else cfg.tile
         W = synth.weights(synth.seed_for(block, mi, "w"), mm.R, mm.Ma)
-        nI, nJ, nK = ref.tile_counts(cfg.tile, mm.Ma, mm.R, mm.Nb)
+        nI, nJ, nK = ref.tile_counts(tile, mm.Ma, mm.R, mm.Nb)
         ct_in = synth.uniform_below(synth.seed_for(block, mi, "enc"), (nJ, nK, 2, P.L, P.N), P.primes)
         out.append((mm, W, ct_in, synth.seed_for(block, mi, "mask")))
     return out
@@ -229,18 +230,39 @@ def test_linear_batch_c1_vs_oracle(hl, ctx4096):
             assert np.array_equal(hl.to_host(sh).reshape(es.shape), es), (rep, mm.name)
 
 
+def test_linear_batch_mixed_tiles_vs_oracle(hl, ctx4096):
+    """hl_he_linear_batch with a different tile per product (hl_linear_desc.tile, as bench.py runs
+    c2 with the planner's tiles) on config c1's shapes, bit-exact against the oracle."""
+    ctx = ctx4096
+    cfg = synth.CONFIGS["c1"]
+    P = _P(ctx)
+    tiles = [(16, 8, 32), (8, 8, 64), (4, 32, 32), (32, 4, 32)]
+    ins = _block_inputs(ctx, cfg, tiles=tiles)
+    entries = [dict(wcache=ctx.encode_weights(t, hl.to_device(W)), Ma=mm.Ma, R=mm.R, Nb=mm.Nb, tile=t,
+                    ct_in=hl.to_device(ct_in), seed=seed) for t, (mm, W, ct_in, seed) in zip(tiles, ins)]
+    exp = [ref.mask_and_share(P, t, ref.he_matmul(P, t, W, ct_in, mm.Nb), mm.Ma, mm.Nb, seed)
+           for t, (mm, W, ct_in, seed) in zip(tiles, ins)]
+    for rep in range(3):
+        outs = ctx.he_linear_batch((1, 1, 1), entries)   # the call's tile is overridden by every entry
+        _sync()
+        for (mm, *_), (m, sh), (em, es) in zip(ins, outs, exp):
+            assert np.array_equal(hl.to_host(m).reshape(em.shape), em), (rep, mm.name)
+            assert np.array_equal(hl.to_host(sh).reshape(es.shape), es), (rep, mm.name)
+
+
 def test_linear_batch_c2_equals_single_calls(hl, ctx4096):
-    """Config c2 at full size in the bench's launch configuration (batch of the four products):
-    bit-identical to four he_matmul_share calls (each of which is checked against the oracle by
-    test_bert_base_full_size_sampled), repeated twice to catch cross-stream races."""
+    """Config c2 at full size in the bench's launch configuration (batch of the four products, each
+    with its planned tile): bit-identical to four he_matmul_share calls (each checked against the
+    oracle by test_bert_base_full_size_sampled), repeated twice to catch cross-stream races."""
     ctx = ctx4096
     cfg = synth.CONFIGS["c2"]
-    ins = _block_inputs(ctx, cfg)
-    entries = [dict(wcache=ctx.encode_weights(cfg.tile, hl.to_device(W)), Ma=mm.Ma, R=mm.R, Nb=mm.Nb,
-                    ct_in=hl.to_device(ct_in), seed=seed) for mm, W, ct_in, seed in ins]
+    tiles = [cfg.tile_of(mi) for mi in range(len(cfg.matmuls))]
+    ins = _block_inputs(ctx, cfg, tiles=tiles)
+    entries = [dict(wcache=ctx.encode_weights(t, hl.to_device(W)), Ma=mm.Ma, R=mm.R, Nb=mm.Nb, tile=t,
+                    ct_in=hl.to_device(ct_in), seed=seed) for t, (mm, W, ct_in, seed) in zip(tiles, ins)]
     single = []
-    for e in entries:
-        m, sh = ctx.he_matmul_share(cfg.tile, e["wcache"], e["Ma"], e["R"], e["Nb"], e["ct_in"], seed=e["seed"])
+    for t, e in zip(tiles, entries):
+        m, sh = ctx.he_matmul_share(t, e["wcache"], e["Ma"], e["R"], e["Nb"], e["ct_in"], seed=e["seed"])
         single.append((hl.to_host(m), hl.to_host(sh)))
     for _ in range(2):
         outs = ctx.he_linear_batch(cfg.tile, entries)
@@ -305,28 +327,32 @@ def test_linear_batch_host_seeded_c1_vs_oracle(hl, ctx4096):
             assert np.array_equal(e["share_host"].numpy().view(np.uint64).reshape(es_.shape), es_), (rep, mm.name)
 
 
-def test_bert_base_full_size_sampled(hl, ctx4096):
-    """Config c2 at full size in the bench's launch configuration (fused call, default tile):
-    sampled output tiles bit-exact against the oracle (its own scalar NTT), and for the whole
-    matmul the reconstruction property (library decrypt + brute-force X.W mod 2^37)."""
+@pytest.mark.parametrize("mi,tile", [
+    (3, (16, 8, 32)),     # FF2 (R = 3072, the longest J reduction) at the default tile
+    (3, (4, 32, 32)),     # FF2 at the planner's tile (bench): r = 32, unpruned c0 inverse, nI = 192
+    (1, (8, 8, 64)),      # O at the planner's tile (bench): nK = 2, 4 MAC columns (CW = 4)
+])
+def test_bert_base_full_size_sampled(hl, ctx4096, mi, tile):
+    """Config c2 at full size in the bench's launch configuration (fused call): sampled output
+    tiles bit-exact against the oracle (its own scalar NTT), and for the whole matmul the
+    reconstruction property (library decrypt + brute-force X.W mod 2^37)."""
     ctx = ctx4096
     cfg = synth.CONFIGS["c2"]
     P = _P(ctx)
-    tile = cfg.tile
-    mm = cfg.matmuls[3]                     # FF2: R = 3072, the longest J reduction
-    X = synth.activations(synth.seed_for(0, 3, "x"), mm.Nb, mm.R)
-    W = synth.weights(synth.seed_for(0, 3, "w"), mm.R, mm.Ma)
-    sk = ctx.keygen(synth.seed_for(0, 3, "key"))
-    ct_in = ctx.encrypt(sk, tile, X, synth.seed_for(0, 3, "enc"))
+    mm = cfg.matmuls[mi]
+    X = synth.activations(synth.seed_for(0, mi, "x"), mm.Nb, mm.R)
+    W = synth.weights(synth.seed_for(0, mi, "w"), mm.R, mm.Ma)
+    sk = ctx.keygen(synth.seed_for(0, mi, "key"))
+    ct_in = ctx.encrypt(sk, tile, X, synth.seed_for(0, mi, "enc"))
     assert np.array_equal(ct_in[:1, :1], ref.encrypt(P, tile, sk, X[:tile[2], :tile[1]],
-                                                     synth.seed_for(0, 3, "enc")))
+                                                     synth.seed_for(0, mi, "enc")))
     wc = ctx.encode_weights(tile, hl.to_device(W))
-    seed = synth.seed_for(0, 3, "mask")
+    seed = synth.seed_for(0, mi, "mask")
     masked, share = ctx.he_matmul_share(tile, wc, mm.Ma, mm.R, mm.Nb, hl.to_device(ct_in), seed=seed)
     nI, nJ, nK = ref.tile_counts(tile, mm.Ma, mm.R, mm.Nb)
     masked = hl.to_host(masked).reshape(nI, nK, -1)
     share = hl.to_host(share).reshape(mm.Nb, mm.Ma)
-    tiles = [(0, 0), (nI - 1, nK - 1), (17, 2)]
+    tiles = [(0, 0), (nI - 1, nK - 1), (17 % nI, 2 % nK)]
     exp_ct = ref.he_matmul_ntt_tiles(P, tile, W, ct_in, mm.Nb, tiles)
     em, kept = ref.mask_tiles(P, tile, exp_ct, nK, tiles, seed, True)
     for o, (I, K) in enumerate(tiles):
