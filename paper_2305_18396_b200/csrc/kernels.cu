@@ -224,20 +224,28 @@ __device__ __forceinline__ void inv_round(double (&a)[16], const double (&wv)[15
   }
 }
 
+// exchange barrier of one transform: the whole CTA (bar < 0) or named barrier `bar` over the
+// transform's NT threads (several transforms per CTA synchronise independently)
+template <int LOGN>
+__device__ __forceinline__ void xsync(int bar) {
+  if (bar < 0) __syncthreads();
+  else asm volatile("bar.sync %0, %1;" ::"r"(bar), "r"(Geom<LOGN>::NT) : "memory");
+}
+
 template <int LOGN, int R>
 __device__ __forceinline__ void fwd_rounds_from(double (&a)[16], double *sm, int t, const double *tw,
-                                                double p, double pinv) {
+                                                double p, double pinv, int bar = -1) {
   if constexpr (R < Geom<LOGN>::NR) {
     double wv[15];
     load_round_tw<LOGN, R>(wv, t, tw);               // in flight during the smem exchange
     if constexpr (R > 0) {
       to_smem<LOGN, R - 1>(a, sm, t);
-      __syncthreads();
+      xsync<LOGN>(bar);
       from_smem<LOGN, R>(a, sm, t);
-      __syncthreads();
+      xsync<LOGN>(bar);
     }
     fwd_round<LOGN, R>(a, wv, p, pinv);
-    fwd_rounds_from<LOGN, R + 1>(a, sm, t, tw, p, pinv);
+    fwd_rounds_from<LOGN, R + 1>(a, sm, t, tw, p, pinv, bar);
   }
 }
 
@@ -379,7 +387,7 @@ k_ntt_fwd_x(const uint64_t *__restrict__ in, uint64_t *__restrict__ out, DevPara
   for (int g = 0; g < GG; g++)
 #pragma unroll
     for (int u = 0; u < (1 << K); u++) a[g * (1 << K) + u] = u2d(__ldcs(in + base + elem_idx<LOGN, 0>(t, g, u)));
-  fwd_rounds_from<LOGN, 0>(a, sm + sub * Gm::SMEM_WORDS, t, tw, pc.pd, pc.pinv);
+  fwd_rounds_from<LOGN, 0>(a, sm + sub * Gm::SMEM_WORDS, t, tw, pc.pd, pc.pinv, G > 1 ? 1 + sub : -1);
   __syncthreads();                                     // every sub-NTT is done with its smem
   uint64_t *xs = reinterpret_cast<uint64_t *>(sm);     // [N][G] canonical residues
 #pragma unroll
@@ -388,6 +396,7 @@ k_ntt_fwd_x(const uint64_t *__restrict__ in, uint64_t *__restrict__ out, DevPara
   const int J = (int)(poly0 / mg.nC), col0 = (int)(poly0 % mg.nC);
   const int cg = col0 / mg.CW, c0 = col0 % mg.CW;
   uint64_t *dst0 = out + ((size_t)cg * mg.LN + (size_t)l * Gm::N) * mg.nJp * mg.CW + (size_t)J * mg.CW + c0;
+#pragma unroll 2
   for (int sl = threadIdx.x; sl < Gm::N; sl += Gm::NT * G) {
     uint64_t *dst = dst0 + (size_t)sl * mg.nJp * mg.CW;
     if constexpr (G == 4) {
@@ -1296,7 +1305,7 @@ void launch_mac_ln(const hl_ctx *c, const MacArgs &A, cudaStream_t st) {
 }
 
 template <int CW>
-void launch_mac_tc_t(const hl_ctx *c, MacTcArgs A, int smem_budget, cudaStream_t st) {
+void launch_mac_tc_t(const hl_ctx *c, MacTcArgs A, int smem_budget, int grid, cudaStream_t st) {
   using T = TcGeom<CW>;
   static bool init = false;
   if (!init) { set_smem(k_mac_tc<CW>, T::SMEM_MAX); init = true; }
@@ -1306,7 +1315,7 @@ void launch_mac_tc_t(const hl_ctx *c, MacTcArgs A, int smem_budget, cudaStream_t
   if (prof) cudaMalloc(&A.prof, 8 * sizeof(unsigned long long)), cudaMemsetAsync(A.prof, 0, 64, st);
   {
   KTimer kt(c, HL_K_MAC, st);
-  k_mac_tc<CW><<<c->num_sms, T::THREADS, A.ring.smem, st>>>(A, c->dp);
+  k_mac_tc<CW><<<grid, T::THREADS, A.ring.smem, st>>>(A, c->dp);
   }
   if (prof) {   // diagnostics: average cycles per CTA waiting, by role
     unsigned long long h[8];
@@ -1325,7 +1334,7 @@ void launch_mac_tc_t(const hl_ctx *c, MacTcArgs A, int smem_budget, cudaStream_t
 inline size_t tc_sched_offset(const MacGeom &g) { return (size_t)g.nJp * g.nC * g.LN * 8; }
 
 void launch_mac_tc(const hl_ctx *c, const void *W, const void *X, uint64_t *out, const MacGeom &g, int smem_budget,
-                   cudaStream_t st) {
+                   int grid, cudaStream_t st) {
   MacTcArgs A;
   A.W = (const uint8_t *)W; A.X = (const uint64_t *)X; A.out = out; A.g = g; A.N = (int)c->N;
   A.sched = (int *)((char *)X + tc_sched_offset(g));
@@ -1338,10 +1347,10 @@ void launch_mac_tc(const hl_ctx *c, const void *W, const void *X, uint64_t *out,
     A.lazy_out = g.nJp <= kMacJChunk;                       // single launch: nobody adds to the outputs
     cudaMemsetAsync(A.sched, 0, sizeof(int), st);
     switch (g.CW) {
-      case 16: launch_mac_tc_t<16>(c, A, smem_budget, st); break;
-      case 8: launch_mac_tc_t<8>(c, A, smem_budget, st); break;
-      case 4: launch_mac_tc_t<4>(c, A, smem_budget, st); break;
-      default: launch_mac_tc_t<2>(c, A, smem_budget, st); break;
+      case 16: launch_mac_tc_t<16>(c, A, smem_budget, grid, st); break;
+      case 8: launch_mac_tc_t<8>(c, A, smem_budget, grid, st); break;
+      case 4: launch_mac_tc_t<4>(c, A, smem_budget, grid, st); break;
+      default: launch_mac_tc_t<2>(c, A, smem_budget, grid, st); break;
     }
   }
 }
@@ -1350,8 +1359,8 @@ constexpr int kMacSmemAlone = 232448;        // the MAC alone on the SM: the dee
 constexpr int kMacSmemShared = 150 * 1024;   // leaves ~77 KB for NTT CTAs running concurrently
 
 void launch_mac(const hl_ctx *c, const uint2 *W, const uint32_t *X, uint64_t *out, const MacGeom &g, cudaStream_t st,
-                int smem_budget = kMacSmemAlone) {
-  if (g.engine == 2) { launch_mac_tc(c, W, X, out, g, smem_budget, st); return; }
+                int smem_budget = kMacSmemAlone, int grid = 0) {
+  if (g.engine == 2) { launch_mac_tc(c, W, X, out, g, smem_budget, grid > 0 ? grid : c->num_sms, st); return; }
   MacArgs A;
   A.W = W; A.X = X; A.out = out; A.g = g; A.N = (int)c->N;
   for (int64_t j0 = 0; j0 < g.nJ; j0 += kMacJChunk) {
@@ -1591,8 +1600,12 @@ static int linear_batch_run(const hl_ctx *c, hl_tile tile, int n, const hl_linea
       const char *e = getenv("HELINEAR_BATCH_MAC_SMEM_KB");
       return e ? atoi(e) * 1024 : kMacSmemShared;
     }();
+    static const int mac_grid = [] {
+      const char *e = getenv("HELINEAR_BATCH_MAC_GRID");
+      return e ? atoi(e) : 0;
+    }();
     launch_mac(c, (const uint2 *)d[i].wcache, (const uint32_t *)d[i].workspace, d[i].ct_out_ntt, E[i].mg, s0,
-               mac_smem);
+               mac_smem, mac_grid);
     cudaEventRecord(e_mac[i], s0);
     if (!split && i + 1 < n) fwd(i + 1);                                 // overlaps MAC(i)
     cudaStreamWaitEvent(s1, e_mac[i], 0);
