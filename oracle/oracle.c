@@ -17,6 +17,11 @@
  *   ct_in  [nJ][nK][2][L][N]       fresh ciphertexts (c0, c1) of pi_B tiles
  *   ct_out [nI][nK][2][L][N]       Enc(c) = sum_J a_IJ * ct_in[J][K]
  *   masked, compressed: [nI][nK]{ c0_kept[L][m*n], c1[L][N] }  (c0 kept index k*m+i)
+ * Every ciphertext carries c0 in coefficient form and c1 in EVALUATION form (reading C26):
+ *   c1_hat[k] = c1(psi_l^(2k+1)) mod p_l, k = 0..N-1 natural order = or_ntt(c1); psi_l is the
+ *   oracle's root (ref.primitive_2n_root: g^((p-1)/2N), g the smallest primitive root).  The
+ *   arithmetic below converts with the oracle's own or_ntt / or_intt at the boundary and keeps
+ *   the definitions themselves in coefficient form.
  *   masked, full:       [nI][nK][2][L][N]
  *   share  [Nb][Ma]                server share S (the mask at the decoded positions)
  *
@@ -215,18 +220,20 @@ static uint64_t signed_mod(int64_t v, uint64_t p) {
   return v >= 0 ? (uint64_t)v % p : (p - ((uint64_t)(-v)) % p) % p;
 }
 
-/* Secret-key BFV encryption of every pi_B tile (O4):
- *   c1 = a_l,  c0 = -a_l * s + e + Delta_l * b   (mod p_l)                                */
-void or_encrypt(uint32_t N, uint32_t L, const uint64_t *primes, const uint64_t *delta_mod,
-                uint32_t m, uint32_t r, uint32_t n, const uint64_t *X, int64_t Nb, int64_t R,
-                const int8_t *sk, uint64_t seed, const uint64_t *cdt, int ncdt, uint64_t *ct_in) {
+/* Secret-key BFV encryption of every pi_B tile (O4, reading C26):
+ *   a_hat_l = PRF (or_sample_a, evaluation form),  a_l = INTT(a_hat_l)
+ *   c1 = a_hat_l (evaluation form),  c0 = -a_l * s + e + Delta_l * b   (mod p_l)             */
+void or_encrypt(uint32_t N, uint32_t L, const uint64_t *primes, const uint64_t *psis,
+                const uint64_t *delta_mod, uint32_t m, uint32_t r, uint32_t n, const uint64_t *X,
+                int64_t Nb, int64_t R, const int8_t *sk, uint64_t seed, const uint64_t *cdt, int ncdt,
+                uint64_t *ct_in) {
   int64_t nJ = (R + r - 1) / r, nK = (Nb + n - 1) / n;
 #pragma omp parallel for schedule(dynamic)
   for (int64_t g = 0; g < nJ * nK; g++) {
     int64_t J = g / nK, K = g % nK;
     uint64_t *b = (uint64_t *)calloc(N, 8);
     int64_t *e = (int64_t *)malloc(8ull * N);
-    uint64_t *a = (uint64_t *)malloc(8ull * N);
+    uint64_t *a = (uint64_t *)malloc(8ull * N), *a_hat = (uint64_t *)malloc(8ull * N);
     u128 *pos = (u128 *)malloc(sizeof(u128) * N), *neg = (u128 *)malloc(sizeof(u128) * N);
     for (uint32_t k = 0; k < n; k++)
       for (uint32_t j = 0; j < r; j++) {
@@ -236,7 +243,8 @@ void or_encrypt(uint32_t N, uint32_t L, const uint64_t *primes, const uint64_t *
     or_sample_e(N, seed, (uint64_t)g, cdt, ncdt, e);
     for (uint32_t l = 0; l < L; l++) {
       uint64_t p = primes[l];
-      or_sample_a(N, seed, (uint64_t)g, l, L, p, a);
+      or_sample_a(N, seed, (uint64_t)g, l, L, p, a_hat);
+      or_intt(N, p, psis[l], a_hat, a);
       /* a * s, schoolbook over the ternary s */
       memset(pos, 0, sizeof(u128) * N); memset(neg, 0, sizeof(u128) * N);
       for (uint32_t j = 0; j < N; j++) {
@@ -256,20 +264,28 @@ void or_encrypt(uint32_t N, uint32_t L, const uint64_t *primes, const uint64_t *
         v = addmod(v, signed_mod(e[k], p), p);
         v = addmod(v, mulmod(delta_mod[l], b[k] % p, p), p);
         c0[k] = v;
-        c1[k] = a[k];
+        c1[k] = a_hat[k];
       }
     }
-    free(b); free(e); free(a); free(pos); free(neg);
+    free(b); free(e); free(a); free(a_hat); free(pos); free(neg);
   }
 }
 
 /* he_matmul, definition (i) of SURVEY.md §8(c):
  *   ct_out[I][K][c] = sum_J a_IJ * ct_in[J][K][c]  mod (X^N+1, p_l)
  * as a sparse schoolbook product: a_IJ has at most m*r nonzero coefficients.   (O6)   */
-void or_he_matmul(uint32_t N, uint32_t L, const uint64_t *primes, uint32_t m, uint32_t r,
-                  uint32_t n, uint32_t t_bits, const uint64_t *W, int64_t R, int64_t Ma,
-                  int64_t Nb, const uint64_t *ct_in, uint64_t *ct_out) {
+void or_he_matmul(uint32_t N, uint32_t L, const uint64_t *primes, const uint64_t *psis, uint32_t m,
+                  uint32_t r, uint32_t n, uint32_t t_bits, const uint64_t *W, int64_t R, int64_t Ma,
+                  int64_t Nb, const uint64_t *ct_in_eval, uint64_t *ct_out) {
   int64_t nI = (Ma + m - 1) / m, nJ = (R + r - 1) / r, nK = (Nb + n - 1) / n;
+  /* boundary (reading C26): c1 halves to coefficient form */
+  uint64_t *ct_in = (uint64_t *)malloc(8ull * nJ * nK * 2 * L * N);
+  memcpy(ct_in, ct_in_eval, 8ull * nJ * nK * 2 * L * N);
+#pragma omp parallel for schedule(dynamic)
+  for (int64_t w = 0; w < nJ * nK * (int64_t)L; w++) {
+    uint64_t *x = ct_in + ((uint64_t)(w / L) * 2 + 1) * L * N + (uint64_t)(w % L) * N;
+    or_intt(N, primes[w % L], psis[w % L], ct_in_eval + (x - ct_in), x);
+  }
   /* independent work items: (output tile (I, K), component c, prime l) */
 #pragma omp parallel for schedule(dynamic)
   for (int64_t w = 0; w < nI * nK * 2 * (int64_t)L; w++) {
@@ -296,8 +312,15 @@ void or_he_matmul(uint32_t N, uint32_t L, const uint64_t *primes, uint32_t m, ui
     uint64_t *y = ct_out + ((uint64_t)(I * nK + K) * 2 + c) * L * N + (uint64_t)l * N;
     for (uint32_t k = 0; k < N; k++)
       y[k] = submod((uint64_t)(pos[k] % p), (uint64_t)(neg[k] % p), p);
+    if (c == 1) {                                  /* boundary (C26): c1 to evaluation form */
+      uint64_t *tmp = (uint64_t *)malloc(8ull * N);
+      or_ntt(N, p, psis[l], y, tmp);
+      memcpy(y, tmp, 8ull * N);
+      free(tmp);
+    }
     free(pos); free(neg);
   }
+  free(ct_in);
 }
 
 /* Same definition evaluated through the oracle's own scalar NTT (or_ntt / or_intt):
@@ -328,10 +351,13 @@ void or_he_matmul_ntt_tiles(uint32_t N, uint32_t L, const uint64_t *primes, cons
             }
           or_ntt(N, p, psis[l], apoly, ahat);
           const uint64_t *x = ct_in + ((uint64_t)(J * nK + K) * 2 + c) * L * N + (uint64_t)l * N;
-          or_ntt(N, p, psis[l], x, xhat);
+          if (c == 0) or_ntt(N, p, psis[l], x, xhat);
+          else memcpy(xhat, x, 8ull * N);            /* c1 is in evaluation form (C26) */
           for (uint32_t k = 0; k < N; k++) acc[k] = addmod(acc[k], mulmod(ahat[k], xhat[k], p), p);
         }
-        or_intt(N, p, psis[l], acc, ct_out + ((uint64_t)o * 2 + c) * L * N + (uint64_t)l * N);
+        uint64_t *y = ct_out + ((uint64_t)o * 2 + c) * L * N + (uint64_t)l * N;
+        if (c == 0) or_intt(N, p, psis[l], acc, y);
+        else memcpy(y, acc, 8ull * N);
       }
     free(apoly); free(ahat); free(xhat); free(acc);
   }
@@ -409,17 +435,19 @@ void or_mask_tiles(uint32_t N, uint32_t L, const uint64_t *primes, const uint64_
  * pos(i,k) only: x_l = c0[pos] + (c1 * s)[pos]  (mod p_l).  The CRT and the rounding
  * y = floor((t*x + floor(q/2)) / q) mod t are done with Python integers (oracle/ref.py). (O10)
  * Output layout: x [nI][nK][L][m*n] (index k*m + i).                                     */
-void or_decrypt_residues(uint32_t N, uint32_t L, const uint64_t *primes, uint32_t m, uint32_t r,
-                         uint32_t n, int64_t Ma, int64_t Nb, const int8_t *sk,
+void or_decrypt_residues(uint32_t N, uint32_t L, const uint64_t *primes, const uint64_t *psis, uint32_t m,
+                         uint32_t r, uint32_t n, int64_t Ma, int64_t Nb, const int8_t *sk,
                          const uint64_t *ct_masked, int compress, uint64_t *x) {
   int64_t nI = (Ma + m - 1) / m, nK = (Nb + n - 1) / n;
   uint64_t per_ct = compress ? (uint64_t)L * (m * n + N) : 2ull * L * N;
 #pragma omp parallel for schedule(dynamic)
   for (int64_t o = 0; o < nI * nK; o++) {
     const uint64_t *ct = ct_masked + (uint64_t)o * per_ct;
+    uint64_t *c1 = (uint64_t *)malloc(8ull * N);
     for (uint32_t l = 0; l < L; l++) {
       uint64_t p = primes[l];
-      const uint64_t *c1 = compress ? ct + (uint64_t)L * m * n + (uint64_t)l * N : ct + (uint64_t)(L + l) * N;
+      /* c1 from evaluation form (C26) */
+      or_intt(N, p, psis[l], compress ? ct + (uint64_t)L * m * n + (uint64_t)l * N : ct + (uint64_t)(L + l) * N, c1);
       for (uint32_t k = 0; k < n; k++)
         for (uint32_t i = 0; i < m; i++) {
           uint32_t pos = k * m * r + i * r + r - 1;
@@ -436,19 +464,21 @@ void or_decrypt_residues(uint32_t N, uint32_t L, const uint64_t *primes, uint32_
           x[((uint64_t)o * L + l) * m * n + k * m + i] = addmod(v, c0, p);
         }
     }
+    free(c1);
   }
 }
 
 /* Full decryption residues of every coefficient (for noise measurements and the
  * "compressed decrypt equals full decrypt" pin): x [nct][L][N] = c0 + c1*s (mod p_l). */
-void or_decrypt_full_residues(uint32_t N, uint32_t L, const uint64_t *primes, const int8_t *sk,
-                              const uint64_t *ct, int64_t nct, uint64_t *x) {
+void or_decrypt_full_residues(uint32_t N, uint32_t L, const uint64_t *primes, const uint64_t *psis,
+                              const int8_t *sk, const uint64_t *ct, int64_t nct, uint64_t *x) {
 #pragma omp parallel for schedule(dynamic)
   for (int64_t o = 0; o < nct; o++)
     for (uint32_t l = 0; l < L; l++) {
       uint64_t p = primes[l];
       const uint64_t *c0 = ct + ((uint64_t)o * 2 + 0) * L * N + (uint64_t)l * N;
-      const uint64_t *c1 = ct + ((uint64_t)o * 2 + 1) * L * N + (uint64_t)l * N;
+      uint64_t *c1 = (uint64_t *)malloc(8ull * N);      /* c1 from evaluation form (C26) */
+      or_intt(N, p, psis[l], ct + ((uint64_t)o * 2 + 1) * L * N + (uint64_t)l * N, c1);
       u128 *pos = (u128 *)calloc(N, sizeof(u128)), *neg = (u128 *)calloc(N, sizeof(u128));
       for (uint32_t j = 0; j < N; j++) {
         if (sk[j] == 0) continue;
@@ -461,6 +491,6 @@ void or_decrypt_full_residues(uint32_t N, uint32_t L, const uint64_t *primes, co
       for (uint32_t k = 0; k < N; k++)
         x[((uint64_t)o * L + l) * N + k] =
             addmod(submod((uint64_t)(pos[k] % p), (uint64_t)(neg[k] % p), p), c0[k], p);
-      free(pos); free(neg);
+      free(pos); free(neg); free(c1);
     }
 }

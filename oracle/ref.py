@@ -292,7 +292,7 @@ def encrypt(P: Params, tile, sk: np.ndarray, X: np.ndarray, seed: int) -> np.nda
     X = np.ascontiguousarray(X, dtype=np.uint64)
     ct = np.zeros((nJ, nK, 2, P.L, P.N), dtype=np.uint64)
     T = _u64arr(cdt_table())
-    lib().or_encrypt(ctypes.c_uint32(P.N), ctypes.c_uint32(P.L), _p(_u64arr(P.primes)),
+    lib().or_encrypt(ctypes.c_uint32(P.N), ctypes.c_uint32(P.L), _p(_u64arr(P.primes)), _p(_u64arr(P.psis)),
                      _p(_u64arr(P.delta_mod)), ctypes.c_uint32(m), ctypes.c_uint32(r),
                      ctypes.c_uint32(n), _p(X), ctypes.c_int64(Nb), ctypes.c_int64(R),
                      _p(np.ascontiguousarray(sk), ctypes.c_int8), ctypes.c_uint64(seed), _p(T),
@@ -308,7 +308,7 @@ def he_matmul(P: Params, tile, W: np.ndarray, ct_in: np.ndarray, Nb: int) -> np.
     nI, nJ, nK = tile_counts(tile, Ma, R, Nb)
     assert ct_in.shape == (nJ, nK, 2, P.L, P.N), ct_in.shape
     out = np.zeros((nI, nK, 2, P.L, P.N), dtype=np.uint64)
-    lib().or_he_matmul(ctypes.c_uint32(P.N), ctypes.c_uint32(P.L), _p(_u64arr(P.primes)),
+    lib().or_he_matmul(ctypes.c_uint32(P.N), ctypes.c_uint32(P.L), _p(_u64arr(P.primes)), _p(_u64arr(P.psis)),
                        ctypes.c_uint32(m), ctypes.c_uint32(r), ctypes.c_uint32(n),
                        ctypes.c_uint32(P.t_bits), _p(np.ascontiguousarray(W, dtype=np.uint64)),
                        ctypes.c_int64(R), ctypes.c_int64(Ma), ctypes.c_int64(Nb),
@@ -381,7 +381,7 @@ def decrypt_share(P: Params, tile, sk: np.ndarray, masked: np.ndarray, Ma: int, 
     nI, _, nK = tile_counts(tile, Ma, 1, Nb)
     x = np.zeros((nI, nK, P.L, m * n), dtype=np.uint64)
     lib().or_decrypt_residues(ctypes.c_uint32(P.N), ctypes.c_uint32(P.L), _p(_u64arr(P.primes)),
-                              ctypes.c_uint32(m), ctypes.c_uint32(r), ctypes.c_uint32(n),
+                              _p(_u64arr(P.psis)), ctypes.c_uint32(m), ctypes.c_uint32(r), ctypes.c_uint32(n),
                               ctypes.c_int64(Ma), ctypes.c_int64(Nb), _p(np.ascontiguousarray(sk), ctypes.c_int8),
                               _p(np.ascontiguousarray(masked)), ctypes.c_int(int(compress)), _p(x))
     out = np.zeros((Nb, Ma), dtype=np.uint64)
@@ -405,7 +405,7 @@ def decrypt_full(P: Params, sk: np.ndarray, ct: np.ndarray):
     nct = ct.reshape(-1, 2, P.L, P.N).shape[0]
     x = np.zeros((nct, P.L, P.N), dtype=np.uint64)
     lib().or_decrypt_full_residues(ctypes.c_uint32(P.N), ctypes.c_uint32(P.L), _p(_u64arr(P.primes)),
-                                   _p(np.ascontiguousarray(sk), ctypes.c_int8),
+                                   _p(_u64arr(P.psis)), _p(np.ascontiguousarray(sk), ctypes.c_int8),
                                    _p(np.ascontiguousarray(ct.reshape(-1))), ctypes.c_int64(nct), _p(x))
     q, t, D = P.q, P.t, P.delta
     pts, noise = [], []
@@ -545,7 +545,7 @@ def pk_gen(P: Params, sk: np.ndarray, seed: int) -> np.ndarray:
 def rerandomize(P: Params, tile, pk: np.ndarray, ct_out: np.ndarray, nK: int, seed: int, flood_bits: int,
                 i_begin: int = 0) -> np.ndarray:
     """c' = c + Enc_pk(0) + (F, 0) for every output ciphertext of ct_out [nI][nK][2][L][N]
-    (coefficient form; global tile index (i_begin + I) nK + K)."""
+    (c0 coefficient form, c1 evaluation form -- reading C26; global tile index (i_begin + I) nK + K)."""
     N = P.N
     out = ct_out.copy()
     for I in range(ct_out.shape[0]):
@@ -566,5 +566,7 @@ def rerandomize(P: Params, tile, pk: np.ndarray, ct_out: np.ndarray, nK: int, se
                 add0 = _to_mod(e1 + F, p)
                 add1 = _to_mod(e2, p)
                 out[I, K, 0, l] = [(int(c) + int(x) + int(y)) % p for c, x, y in zip(out[I, K, 0, l], a0, add0)]
-                out[I, K, 1, l] = [(int(c) + int(x) + int(y)) % p for c, x, y in zip(out[I, K, 1, l], a1, add1)]
+                c1 = intt(N, p, P.psis[l], out[I, K, 1, l])
+                c1 = np.array([(int(c) + int(x) + int(y)) % p for c, x, y in zip(c1, a1, add1)], dtype=np.uint64)
+                out[I, K, 1, l] = ntt(N, p, P.psis[l], c1)
     return out

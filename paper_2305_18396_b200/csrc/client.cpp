@@ -81,18 +81,17 @@ extern "C" int hl_encrypt(const hl_ctx *c, const int8_t *sk, hl_tile tile, const
       }
       for (uint32_t l = 0; l < L; l++) {
         const uint64_t p = c->primes[l];
-        // a_l[i] = (u[2i] + 2^64 u[2i+1]) mod p, stream (A, g*L + l)
+        // a_hat_l[k] = (u[2k] + 2^64 u[2k+1]) mod p, stream (A, g*L + l): the evaluation form of
+        // a (reading C26), natural order k; it is c1 as sent
         for (uint32_t blk = 0; blk < N / 4; blk++) {
           uint64_t w[8];
           hl::chacha_block_u64(seed, hl::kDomA, (uint64_t)gi * L + l, blk, w);
           for (int i = 0; i < 4; i++)
             a[4 * blk + i] = (uint64_t)((((hl_u128)w[2 * i + 1] << 64) | w[2 * i]) % p);
         }
-        // a * s through the host NTT
-        memcpy(as.data(), a.data(), 8ull * N);
-        hl_host_ntt_fwd(c, (int)l, as.data());
+        // a * s = INTT(a_hat . s_hat); the host NTT order is bit-reversed: index i <-> k = brv(i)
         const uint64_t *sh = &shat[(size_t)l * N];
-        for (uint32_t i = 0; i < N; i++) as[i] = h_mulmod(as[i], sh[i], p);
+        for (uint32_t i = 0; i < N; i++) as[i] = h_mulmod(a[c->brv[i]], sh[i], p);
         hl_host_ntt_inv(c, (int)l, as.data());
         uint64_t *c0 = ct_in + ((size_t)gi * 2 + 0) * L * N + (size_t)l * N;
         uint64_t *c1 = ct_in + ((size_t)gi * 2 + 1) * L * N + (size_t)l * N;
@@ -228,12 +227,11 @@ extern "C" int hl_decrypt_share(const hl_ctx *c, const int8_t *sk, hl_tile tile,
       const uint64_t *base = ct + o * per;
       for (uint32_t l = 0; l < L; l++) {
         const uint64_t p = c->primes[l];
+        // c1 arrives in evaluation form (reading C26): c1 * s = INTT(c1_hat . s_hat)
         const uint64_t *c1 = compress ? base + (size_t)L * m * n + (size_t)l * N : base + (size_t)(L + l) * N;
         uint64_t *v = &cs[(size_t)l * N];
-        memcpy(v, c1, 8ull * N);
-        hl_host_ntt_fwd(c, (int)l, v);
         const uint64_t *sh = &shat[(size_t)l * N];
-        for (uint32_t i = 0; i < N; i++) v[i] = h_mulmod(v[i], sh[i], p);
+        for (uint32_t i = 0; i < N; i++) v[i] = h_mulmod(c1[c->brv[i]], sh[i], p);
         hl_host_ntt_inv(c, (int)l, v);
       }
       for (int k = 0; k < n; k++) {

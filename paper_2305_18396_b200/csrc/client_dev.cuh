@@ -4,11 +4,12 @@
 // the host client (client.cpp) and the oracle: same randomness (reading C10), same encodings.
 //
 //   k_encrypt   one CTA per input ciphertext g = J*nK + K, loop over the primes:
-//               e = CDT(u64_E(g)) once (reading C8), a_l = (u[2i] + 2^64 u[2i+1]) mod p_l from
-//               u64_A(g*L + l), c1 = a_l, c0 = -a_l*s + e + Delta_l*pi_B(X), a_l*s
-//               through the forward NTT, the pointwise product with NTT(s) and the inverse NTT.
+//               e = CDT(u64_E(g)) once (reading C8), a_hat_l[k] = (u[2k] + 2^64 u[2k+1]) mod p_l from
+//               u64_A(g*L + l) -- the evaluation form of a (reading C26), sent as c1 --,
+//               c0 = -a_l*s + e + Delta_l*pi_B(X), a_l*s = INTT(a_hat . NTT(s)).
 //   k_decrypt   one CTA per output ciphertext (compressed response, "m = s c1 + c0"):
-//               c1*s per prime through the NTTs, m_l = c0 + c1*s at the kept positions, then the RNS
+//               c1*s = INTT(c1_hat . NTT(s)) per prime (c1 arrives in evaluation form), m_l = c0 + c1*s
+//               at the kept positions, then the RNS
 //               rounding y = round(t x / q) mod t with x = CRT(m_l):  t x / q = sum_l m_l theta_l
 //               (mod t), theta_l = t ((q/p_l)^-1 mod p_l) / p_l = I_l + F_l 2^-64 precomputed; the
 //               truncation of F_l costs < L 2^-14, far inside the decryption margin (|t v / q| <
@@ -67,7 +68,7 @@ k_encrypt(EncArgs E, uint64_t *__restrict__ ct, DevParams P, const uint64_t *__r
 #pragma unroll
       for (int i = 0; i < 4; i++) {
         const uint64_t a = mod_u128(w[2 * i + 1], w[2 * i], pc);
-        a_nat[4 * blk + i] = a;
+        a_nat[pad_idx(4 * blk + i)] = a;
         c1[4 * blk + i] = a;
       }
     }
@@ -75,11 +76,8 @@ k_encrypt(EncArgs E, uint64_t *__restrict__ ct, DevParams P, const uint64_t *__r
     double a[16];
     constexpr int K0 = Gm::k(0), G = 16 >> K0;
 #pragma unroll
-    for (int g = 0; g < G; g++)
-#pragma unroll
-      for (int u = 0; u < (1 << K0); u++) a[g * (1 << K0) + u] = u2d(a_nat[elem_idx<LOGN, 0>(t, g, u)]);
-    __syncthreads();                                   // the NTT reuses the smem
-    fwd_rounds_from<LOGN, 0>(a, sm, t, P.twd_fwd + (size_t)l * Gm::N, pc.pd, pc.pinv);
+    for (int u = 0; u < 16; u++) a[u] = u2d(a_nat[pad_idx(nat_of<LOGN>(t, u))]);   // a_hat in slot order
+    __syncthreads();                                   // the inverse NTT reuses the smem
     const uint64_t *sh = E.s_hat + (size_t)l * Gm::N;
 #pragma unroll
     for (int u = 0; u < 16; u++)
@@ -135,11 +133,7 @@ k_decrypt(const uint64_t *__restrict__ masked, uint64_t *__restrict__ share, Dec
     const uint64_t *c1 = base + (size_t)L * mn + (size_t)l * Gm::N;
     double a[16];
     constexpr int K0 = Gm::k(0), G = 16 >> K0;
-#pragma unroll
-    for (int g = 0; g < G; g++)
-#pragma unroll
-      for (int u = 0; u < (1 << K0); u++) a[g * (1 << K0) + u] = u2d(__ldcs(c1 + elem_idx<LOGN, 0>(t, g, u)));
-    fwd_rounds_from<LOGN, 0>(a, sm, t, P.twd_fwd + (size_t)l * Gm::N, pc.pd, pc.pinv);
+    load_eval_slots<LOGN>(a, c1, reinterpret_cast<uint64_t *>(sm), t, -1);   // c1_hat in slot order (C26)
     const uint64_t *sh = D.s_hat + (size_t)l * Gm::N;
 #pragma unroll
     for (int u = 0; u < 16; u++)
@@ -177,7 +171,7 @@ k_decrypt(const uint64_t *__restrict__ masked, uint64_t *__restrict__ share, Dec
   }
 }
 
-// Seeded ciphertext upload (hl_expand_seeded): c1 = a_l of every input ciphertext regenerated from
+// Seeded ciphertext upload (hl_expand_seeded): c1 = a_hat_l (evaluation form, C26) of every input ciphertext regenerated from
 // the client's encryption seed -- the same PRF stream (A, g*L + l) and the same reduction as
 // k_encrypt / the host client / the oracle (reading C10), so the expanded ciphertext is
 // bit-identical to the one the client encrypted.  One thread per ChaCha block (4 coefficients).

@@ -48,11 +48,21 @@ static bool is_prime_u64(uint64_t n) {
   return true;
 }
 
-// psi with psi^N = -1 (a primitive 2N-th root of unity since 2N is a power of two)
+// psi = g^((p-1)/2N) with g the smallest primitive root mod p (reading C26: the evaluation
+// points psi^(2k+1) of the boundary's evaluation form are ordered by this psi).  p - 1 is
+// factored by trial division: p - 1 = 2N * m with m < 2^38, so divisors up to 2^19 suffice.
 static uint64_t find_psi(uint64_t p, uint32_t N) {
-  for (uint64_t x = 2; x < 1000000; x++) {
-    uint64_t psi = h_powmod(x, (p - 1) / (2ull * N), p);
-    if (h_powmod(psi, N, p) == p - 1) return psi;
+  std::vector<uint64_t> fac;
+  uint64_t m = p - 1;
+  for (uint64_t d = 2; d * d <= m; d++)
+    if (m % d == 0) { fac.push_back(d); while (m % d == 0) m /= d; }
+  if (m > 1) fac.push_back(m);
+  for (uint64_t g = 2; g < 1000000; g++) {
+    bool gen = true;
+    for (uint64_t f : fac) if (h_powmod(g, (p - 1) / f, p) == 1) { gen = false; break; }
+    if (!gen) continue;
+    uint64_t psi = h_powmod(g, (p - 1) / (2ull * N), p);
+    return h_powmod(psi, N, p) == p - 1 ? psi : 0;
   }
   return 0;
 }
@@ -161,6 +171,8 @@ extern "C" int hl_ctx_create(uint32_t N, uint32_t L, uint32_t log2_t, const uint
   // roots and twiddles: tw_fwd[i] = psi^bitrev(i), tw_inv[i] = psi^-bitrev(i)
   c->h_tw_fwd.resize((size_t)L * N); c->h_tw_fwd_sh.resize((size_t)L * N);
   c->h_tw_inv.resize((size_t)L * N); c->h_tw_inv_sh.resize((size_t)L * N);
+  c->brv.resize(N);
+  for (uint32_t i = 0; i < N; i++) c->brv[i] = bitrev(i, logN);
   std::vector<double> tw((size_t)2 * L * N);
   DevParams &dp = c->dp;
   dp.N = (int)N; dp.logN = logN; dp.L = (int)L; dp.t_bits = (int)log2_t;

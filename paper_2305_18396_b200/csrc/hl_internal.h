@@ -54,7 +54,8 @@ struct hl_ctx {
   int num_sms = 148;
   int mac_engine = 2;                 // 0 = IMAD.WIDE limbs, 1 = exact FP64 products, 2 = int8 tensor cores (default)
   std::vector<uint64_t> primes;
-  std::vector<uint64_t> psi;          // primitive 2N-th roots
+  std::vector<uint64_t> psi;          // primitive 2N-th roots: g^((p-1)/2N), g the smallest primitive root (C26)
+  std::vector<uint32_t> brv;          // bit reversal of log2(N) bits: natural evaluation index <-> NTT order
   std::vector<uint64_t> delta_mod;    // Delta mod p_l
   // big-integer constants for host decryption (little-endian u64 limbs, 4 limbs)
   uint64_t q_limbs[4];

@@ -270,6 +270,38 @@ __device__ __forceinline__ void inv_rounds_from(double (&a)[16], double *sm, int
 template <int LOGN>
 __device__ __forceinline__ int slot_of(int t, int u) { return u * Geom<LOGN>::NT + t; }
 
+// Evaluation form at the boundary (reading C26): register u of thread t in slot order holds the
+// CT index idx = 16 t + u, i.e. the evaluation at psi^(2k+1) with natural k = bitrev(idx).
+template <int LOGN>
+__device__ __forceinline__ int nat_of(int t, int u) { return (int)(__brev((unsigned)(16 * t + u)) >> (32 - LOGN)); }
+
+// c1 of a ciphertext (evaluation form, natural order, canonical) -> registers in slot order:
+// coalesced copy through shared memory `stg` (N + N/16 u64, padded, free on entry), then the bit-reversal
+// gather; `stg` is free again on return.  `bar` as xsync.
+template <int LOGN>
+__device__ __forceinline__ void load_eval_slots(double (&a)[16], const uint64_t *src, uint64_t *stg, int t, int bar) {
+  using Gm = Geom<LOGN>;
+#pragma unroll
+  for (int j = 0; j < 16; j++) stg[pad_idx(t + j * Gm::NT)] = __ldcs(src + t + j * Gm::NT);
+  xsync<LOGN>(bar);
+#pragma unroll
+  for (int u = 0; u < 16; u++) a[u] = u2d(stg[pad_idx(nat_of<LOGN>(t, u))]);   // padded: no bank conflicts
+  xsync<LOGN>(bar);
+}
+
+// registers in slot order (canonical residues) -> natural evaluation order in global memory
+// (reading C26), through `stg` (N u64, free on entry and on return)
+template <int LOGN>
+__device__ __forceinline__ void store_eval_slots(const uint64_t (&x)[16], uint64_t *dst, uint64_t *stg, int t, int bar) {
+  using Gm = Geom<LOGN>;
+#pragma unroll
+  for (int u = 0; u < 16; u++) stg[pad_idx(nat_of<LOGN>(t, u))] = x[u];
+  xsync<LOGN>(bar);
+#pragma unroll
+  for (int j = 0; j < 16; j++) dst[t + j * Gm::NT] = stg[pad_idx(t + j * Gm::NT)];
+  xsync<LOGN>(bar);
+}
+
 // ---------------------------------------------------------------------------------------
 // MAC operand layouts in HBM (NTT domain, 25-bit limb pairs).  Both are blocked
 // so that the operands of one (tile, J) step of the MAC kernel are ONE contiguous chunk each,
@@ -285,6 +317,8 @@ struct MacGeom {
   int f64;       // MAC engine: 0 = IMAD.WIDE on 25-bit limbs, 1 = exact FP64 (DFMA) products
   int engine;    // 0 IMAD, 1 FP64, 2 int8 tensor cores (mac_tc.cuh)
   int nIp, nIt, RT, nJp, nJc;   // engine 2: rows padded to 16, nIt balanced I tiles of RT rows, J padded to 32, 32-J steps
+  int cperm;     // MAC column of (K, c): 0 -> 2K + c (the API layout [nK][2]), 1 -> c nK + K (c0 columns
+                 // first: the fused paths, so that the forward NTTs of c0 pair up and the c1 copies do too)
 };
 
 __host__ __device__ __forceinline__ size_t w_index(const MacGeom &g, int iloc, int J, int s) {
@@ -317,6 +351,7 @@ MacGeom mac_geom(const hl_ctx *c, int64_t nIs, int64_t nJ, int64_t nC) {
   if ((int64_t)g.RT * (g.nIt - 1) >= nIs) g.RT = 128;   // never an empty last tile
   g.nJp = (int)((nJ + 31) / 32 * 32);
   g.nJc = g.nJp / 32;
+  g.cperm = 0;
   return g;
 }
 
@@ -337,12 +372,16 @@ k_ntt_fwd(const uint64_t *__restrict__ in, void *__restrict__ out, DevParams P, 
   const double *tw = P.twd_fwd + (size_t)l * Gm::N;
   double a[16];
   constexpr int K = Gm::k(0), G = 16 >> K;
-#pragma unroll
-  for (int g = 0; g < G; g++)
-#pragma unroll
-    for (int u = 0; u < (1 << K); u++) a[g * (1 << K) + u] = u2d(__ldcs(in + base + elem_idx<LOGN, 0>(t, g, u)));
-  fwd_rounds_from<LOGN, 0>(a, sm, t, tw, pc.pd, pc.pinv);
   const int J = (int)(blockIdx.x / (unsigned)max(mg.nC, 1)), col = (int)(blockIdx.x % (unsigned)max(mg.nC, 1));
+  if (MODE == 1 && (col & 1)) {
+    load_eval_slots<LOGN>(a, in + base, reinterpret_cast<uint64_t *>(sm), t, -1);   // c1: evaluation form (C26)
+  } else {
+#pragma unroll
+    for (int g = 0; g < G; g++)
+#pragma unroll
+      for (int u = 0; u < (1 << K); u++) a[g * (1 << K) + u] = u2d(__ldcs(in + base + elem_idx<LOGN, 0>(t, g, u)));
+    fwd_rounds_from<LOGN, 0>(a, sm, t, tw, pc.pd, pc.pinv);
+  }
 #pragma unroll
   for (int u = 0; u < 16; u++) {
     const double xd = canon_d(a[u], pc.pd, pc.pinv);
@@ -383,11 +422,18 @@ k_ntt_fwd_x(const uint64_t *__restrict__ in, uint64_t *__restrict__ out, DevPara
   const double *tw = P.twd_fwd + (size_t)l * Gm::N;
   double a[16];
   constexpr int K = Gm::k(0), GG = 16 >> K;
+  if ((poly0 + sub) % mg.nC & 1) {
+    // c1 (column 2K+1) arrives in evaluation form (reading C26): no transform, only the
+    // permutation from natural order to slots
+    load_eval_slots<LOGN>(a, in + base, reinterpret_cast<uint64_t *>(sm + sub * Gm::SMEM_WORDS), t,
+                          G > 1 ? 1 + sub : -1);
+  } else {
 #pragma unroll
-  for (int g = 0; g < GG; g++)
+    for (int g = 0; g < GG; g++)
 #pragma unroll
-    for (int u = 0; u < (1 << K); u++) a[g * (1 << K) + u] = u2d(__ldcs(in + base + elem_idx<LOGN, 0>(t, g, u)));
-  fwd_rounds_from<LOGN, 0>(a, sm + sub * Gm::SMEM_WORDS, t, tw, pc.pd, pc.pinv, G > 1 ? 1 + sub : -1);
+      for (int u = 0; u < (1 << K); u++) a[g * (1 << K) + u] = u2d(__ldcs(in + base + elem_idx<LOGN, 0>(t, g, u)));
+    fwd_rounds_from<LOGN, 0>(a, sm + sub * Gm::SMEM_WORDS, t, tw, pc.pd, pc.pinv, G > 1 ? 1 + sub : -1);
+  }
   __syncthreads();                                     // every sub-NTT is done with its smem
   uint64_t *xs = reinterpret_cast<uint64_t *>(sm);     // [N][G] canonical residues
 #pragma unroll
@@ -409,6 +455,75 @@ k_ntt_fwd_x(const uint64_t *__restrict__ in, uint64_t *__restrict__ out, DevPara
     } else {
       *dst = xs[sl];
     }
+  }
+}
+
+// (a'') the fused paths' X layout (MacGeom::cperm = 1, c0 columns first): forward NTT of the c0
+//       halves only, two consecutive K of one J per CTA -> adjacent columns, 16-B (slot, J) chunks
+template <int LOGN>
+__global__ void __launch_bounds__(Geom<LOGN>::NT * 2)
+k_ntt_fwd_c0(const uint64_t *__restrict__ in, uint64_t *__restrict__ out, DevParams P, MacGeom mg) {
+  using Gm = Geom<LOGN>;
+  extern __shared__ double sm[];
+  const int sub = threadIdx.x / Gm::NT, t = threadIdx.x % Gm::NT, l = blockIdx.y;
+  const int nK = mg.nC / 2, nKh = (nK + 1) / 2;
+  const int J = (int)(blockIdx.x / (unsigned)nKh), K0 = 2 * (int)(blockIdx.x % (unsigned)nKh), K = K0 + sub;
+  const bool pair = K0 + 1 < nK;
+  const PrimeConsts pc = pick(P, l);
+  double a[16];
+  if (K < nK) {
+    const size_t base = (((size_t)J * nK + K) * 2 * P.L + l) * Gm::N;      // c0 of input ciphertext (J, K)
+    constexpr int KK = Gm::k(0), GG = 16 >> KK;
+#pragma unroll
+    for (int g = 0; g < GG; g++)
+#pragma unroll
+      for (int u = 0; u < (1 << KK); u++) a[g * (1 << KK) + u] = u2d(__ldcs(in + base + elem_idx<LOGN, 0>(t, g, u)));
+    fwd_rounds_from<LOGN, 0>(a, sm + sub * Gm::SMEM_WORDS, t, P.twd_fwd + (size_t)l * Gm::N, pc.pd, pc.pinv, 1 + sub);
+  }
+  __syncthreads();
+  uint64_t *xs = reinterpret_cast<uint64_t *>(sm);     // [N][2] canonical residues
+  if (K < nK) {
+#pragma unroll
+    for (int u = 0; u < 16; u++) xs[slot_of<LOGN>(t, u) * 2 + sub] = d2u(canon_d(a[u], pc.pd, pc.pinv));
+  }
+  __syncthreads();
+  const int cg = K0 / mg.CW, cc = K0 % mg.CW;
+  uint64_t *dst0 = out + ((size_t)cg * mg.LN + (size_t)l * Gm::N) * mg.nJp * mg.CW + (size_t)J * mg.CW + cc;
+#pragma unroll 2
+  for (int sl = threadIdx.x; sl < Gm::N; sl += Gm::NT * 2) {
+    uint64_t *dst = dst0 + (size_t)sl * mg.nJp * mg.CW;
+    if (pair) *reinterpret_cast<ulonglong2 *>(dst) = *reinterpret_cast<const ulonglong2 *>(xs + sl * 2);
+    else *dst = xs[sl * 2];
+  }
+}
+
+// c1 halves (evaluation form, reading C26) into the permuted X layout: no transform, the
+// natural -> slot reordering through shared memory, G1 consecutive K (adjacent columns nK + K)
+// per CTA so that every (slot, J) store is 8 G1 contiguous bytes (G1 = 2 for even nK).
+template <int LOGN, int G1>
+__global__ void __launch_bounds__(Geom<LOGN>::NT)
+k_c1_to_x(const uint64_t *__restrict__ in, uint64_t *__restrict__ out, DevParams P, MacGeom mg) {
+  using Gm = Geom<LOGN>;
+  extern __shared__ double sm[];
+  uint64_t *stg = reinterpret_cast<uint64_t *>(sm);    // [G1][N + N/16] natural order, padded
+  const int t = threadIdx.x, l = blockIdx.y;
+  const int nK = mg.nC / 2, nKg = nK / G1;
+  const int J = (int)(blockIdx.x / (unsigned)nKg), K0 = G1 * (int)(blockIdx.x % (unsigned)nKg);
+#pragma unroll
+  for (int g = 0; g < G1; g++) {
+    const uint64_t *src = in + (((size_t)J * nK + K0 + g) * 2 * P.L + P.L + l) * Gm::N;
+#pragma unroll
+    for (int j = 0; j < 16; j++) stg[g * Gm::SMEM_WORDS + pad_idx(t + j * Gm::NT)] = __ldcs(src + t + j * Gm::NT);
+  }
+  __syncthreads();
+  const int col = nK + K0, cg = col / mg.CW, cc = col % mg.CW;
+  uint64_t *dst0 = out + ((size_t)cg * mg.LN + (size_t)l * Gm::N) * mg.nJp * mg.CW + (size_t)J * mg.CW + cc;
+#pragma unroll 4
+  for (int u = 0; u < 16; u++) {
+    const int k = pad_idx(nat_of<LOGN>(t, u));          // padded: no bank conflicts on the bit-reversal gather
+    uint64_t *dst = dst0 + (size_t)slot_of<LOGN>(t, u) * mg.nJp * mg.CW;
+    if constexpr (G1 == 2) *reinterpret_cast<ulonglong2 *>(dst) = make_ulonglong2(stg[k], stg[Gm::SMEM_WORDS + k]);
+    else *dst = stg[k];
   }
 }
 
@@ -501,7 +616,7 @@ __device__ __forceinline__ void load_ntt_domain(double (&a)[16], const uint64_t 
 
 template <int LOGN>
 __global__ void __launch_bounds__(Geom<LOGN>::NT)
-k_ntt_inv(const uint64_t *in, uint64_t *out, DevParams P) {
+k_ntt_inv(const uint64_t *in, uint64_t *out, DevParams P, int ct_mode) {
   using Gm = Geom<LOGN>;
   extern __shared__ double sm[];
   const int t = threadIdx.x, l = blockIdx.y;
@@ -510,6 +625,13 @@ k_ntt_inv(const uint64_t *in, uint64_t *out, DevParams P) {
   const double *tw = P.twd_inv + (size_t)l * Gm::N;
   double a[16];
   load_ntt_domain<LOGN>(a, in + base, t, pc);
+  if (ct_mode && (blockIdx.x & 1)) {        // ciphertexts: c1 stays in evaluation form (reading C26)
+    uint64_t x[16];
+#pragma unroll
+    for (int u = 0; u < 16; u++) x[u] = d2u(canon_d(a[u], pc.pd, pc.pinv));
+    store_eval_slots<LOGN>(x, out + base, reinterpret_cast<uint64_t *>(sm), t, -1);
+    return;
+  }
   inv_rounds_from<LOGN, Gm::NR - 1>(a, sm, t, tw, pc);
   constexpr int K = Gm::k(0), G = 16 >> K;
 #pragma unroll
@@ -536,7 +658,14 @@ struct MaskArgs {
   const uint64_t *u_hat;    // [nout][L][N] NTT(u) in slot order (k_rr_u)
   const uint64_t *cdt;      // device CDT table
   int flood_bits;
+  int nC, cperm;            // MAC output columns and their order (MacGeom::cperm)
 };
+
+// index of the NTT-domain polynomial (component c of output ciphertext o = I_loc nK + K) in the
+// MAC output [nI_s][nC][L][N]
+__device__ __forceinline__ size_t ct_poly(const MaskArgs &M, int64_t o, int c) {
+  return M.cperm ? (size_t)(o / M.nK) * M.nC + (size_t)c * M.nK + (size_t)(o % M.nK) : (size_t)o * 2 + c;
+}
 
 // e (reading C8) from one PRF word
 __device__ __forceinline__ int cdt_sample(uint64_t w, const uint64_t *cdt) {
@@ -653,20 +782,38 @@ k_ntt_inv_mask(const uint64_t *__restrict__ ct_ntt, uint64_t *__restrict__ maske
     const PrimeConsts pc = pick(P, l);
     const double *tw = P.twd_inv + (size_t)l * Gm::N;
     double a[16];
-    load_ntt_domain<LOGN>(a, ct_ntt + (((size_t)o * 2 + c) * L + l) * Gm::N, t, pc);
+    load_ntt_domain<LOGN>(a, ct_ntt + (ct_poly(M, o, c) * L + l) * Gm::N, t, pc);
     if (rr) rr_add_ntt<LOGN>(a, M, o, c, l, L, t, pc);
-    inv_rounds_from<LOGN, Gm::NR - 1>(a, sm, t, tw, pc);
     constexpr int K0 = Gm::k(0), G = 16 >> K0;
+    if (c == 1) {
+      // c1 leaves in evaluation form (reading C26): no inverse transform, only the reordering
+      // to natural order -- except for re-randomisation, whose e2 is a coefficient-domain term
+      if (rr) {
+        inv_rounds_from<LOGN, Gm::NR - 1>(a, sm, t, tw, pc);
+#pragma unroll
+        for (int g = 0; g < G; g++)
+#pragma unroll
+          for (int u = 0; u < (1 << K0); u++) {
+            double &v = a[g * (1 << K0) + u];
+            v = red_d(__dadd_rn(v, (double)e2_sm[elem_idx<LOGN, 0>(t, g, u)]), pc.pd, pc.pinv);
+          }
+        fwd_rounds_from<LOGN, 0>(a, sm, t, P.twd_fwd + (size_t)l * Gm::N, pc.pd, pc.pinv);
+        __syncthreads();                           // the exchange buffer becomes the staging buffer
+      }
+      uint64_t x[16];
+#pragma unroll
+      for (int u = 0; u < 16; u++) x[u] = d2u(canon_d(a[u], pc.pd, pc.pinv));
+      store_eval_slots<LOGN>(x, dst + (size_t)L * mn + (size_t)l * Gm::N, reinterpret_cast<uint64_t *>(sm), t, -1);
+      continue;
+    }
+    inv_rounds_from<LOGN, Gm::NR - 1>(a, sm, t, tw, pc);
 #pragma unroll
     for (int g = 0; g < G; g++)
 #pragma unroll
       for (int u = 0; u < (1 << K0); u++) {
         uint64_t x = d2u(canon_d(a[g * (1 << K0) + u], pc.pd, pc.pinv));
         const int idx = elem_idx<LOGN, 0>(t, g, u);
-        if (c == 1) {
-          if (rr) { x += smod(e2_sm[idx], pc); x = x >= pc.p ? x - pc.p : x; }
-          dst[(size_t)L * mn + (size_t)l * Gm::N + idx] = x;
-        } else if (idx < mr * M.n && (idx & (M.r - 1)) == M.r - 1) {
+        if (idx < mr * M.n && (idx & (M.r - 1)) == M.r - 1) {
           const int kk = idx >> M.lr;               // = k*m + i for pos(i, k) = (k m + i) r + r - 1
           if (rr) { x += smod(ext_sm[kk], pc); x = x >= pc.p ? x - pc.p : x; }
           uint64_t d = shoup_mul(sig_sm[kk], pc.delta, pc.delta_sh, pc.p);
@@ -731,7 +878,7 @@ k_intt_c0_pruned(const uint64_t *__restrict__ ct_ntt, uint64_t *__restrict__ mas
   for (int l = 0; l < L; l++) {
     const PrimeConsts pc = pick(P, l);
     double a[16];
-    load_ntt_domain<LOGN>(a, ct_ntt + (((size_t)o * 2) * L + l) * Gm::N, t, pc);
+    load_ntt_domain<LOGN>(a, ct_ntt + (ct_poly(M, o, 0) * L + l) * Gm::N, t, pc);
     if constexpr (RR) rr_add_ntt<LOGN>(a, M, o, 0, l, L, t, pc);
     { double wv[15]; load_round_tw<LOGN, Gm::NR - 1>(wv, t, P.twd_inv + (size_t)l * Gm::N); inv_round<LOGN, Gm::NR - 1>(a, wv, pc); }
     to_smem<LOGN, Gm::NR - 1>(a, sm + (size_t)l * Gm::SMEM_WORDS, t);
@@ -1217,12 +1364,12 @@ void launch_fwd(const hl_ctx *c, const uint64_t *in, void *out, int64_t npoly, c
 }
 
 template <int LOGN>
-void launch_inv(const hl_ctx *c, const uint64_t *in, uint64_t *out, int64_t npoly, cudaStream_t st) {
+void launch_inv(const hl_ctx *c, const uint64_t *in, uint64_t *out, int64_t npoly, cudaStream_t st, int ct_mode) {
   static bool init = false;
   if (!init) { set_smem(k_ntt_inv<LOGN>, ntt_smem<LOGN>()); init = true; }
   dim3 grid((unsigned)npoly, c->L);
   KTimer kt(c, HL_K_INTT, st);
-  k_ntt_inv<LOGN><<<grid, Geom<LOGN>::NT, ntt_smem<LOGN>(), st>>>(in, out, c->dp);
+  k_ntt_inv<LOGN><<<grid, Geom<LOGN>::NT, ntt_smem<LOGN>(), st>>>(in, out, c->dp, ct_mode);
 }
 
 template <int LOGN, int G>
@@ -1240,8 +1387,33 @@ static int ntt_group() {
   return g;
 }
 
+template <int LOGN>
+void launch_fwd_cperm(const hl_ctx *c, const uint64_t *in, uint64_t *out, int64_t npoly, const MacGeom &mg,
+                      cudaStream_t st) {
+  const int nK = mg.nC / 2;
+  const int64_t nJ = npoly / mg.nC;
+  constexpr size_t smem2 = ntt_smem<LOGN>() * 2, smem1 = ntt_smem<LOGN>();
+  static bool init = false;
+  if (!init) {
+    set_smem(k_ntt_fwd_c0<LOGN>, smem2);
+    set_smem(k_c1_to_x<LOGN, 2>, 2 * smem1); set_smem(k_c1_to_x<LOGN, 1>, smem1);
+    init = true;
+  }
+  KTimer kt(c, HL_K_NTT_FWD, st);
+  k_ntt_fwd_c0<LOGN><<<dim3((unsigned)(nJ * ((nK + 1) / 2)), c->L), Geom<LOGN>::NT * 2, smem2, st>>>(in, out, c->dp, mg);
+  const int G1 = nK % 2 == 0 ? 2 : 1;
+  const dim3 g1((unsigned)(nJ * (nK / G1)), c->L);
+  if (G1 == 2) k_c1_to_x<LOGN, 2><<<g1, Geom<LOGN>::NT, 2 * smem1, st>>>(in, out, c->dp, mg);
+  else k_c1_to_x<LOGN, 1><<<g1, Geom<LOGN>::NT, smem1, st>>>(in, out, c->dp, mg);
+}
+
 // MODE 0 (u64, slot order) when mg == nullptr, else MODE 1 (the MAC engine's X layout)
 void fwd_ntt(const hl_ctx *c, const uint64_t *in, void *out, int64_t npoly, const MacGeom *mg, cudaStream_t st) {
+  if (mg && mg->engine == 2 && mg->cperm) {
+    if (c->N == 4096) launch_fwd_cperm<12>(c, in, (uint64_t *)out, npoly, *mg, st);
+    else launch_fwd_cperm<13>(c, in, (uint64_t *)out, npoly, *mg, st);
+    return;
+  }
   if (mg && mg->engine == 2) {
     // G consecutive polynomials share J and a column group (G divides CW)
     const int G = (mg->CW % 4 == 0 && ntt_group() >= 4 && c->N == 4096) ? 4 : (ntt_group() >= 2 ? 2 : 1);
@@ -1260,8 +1432,10 @@ void fwd_ntt(const hl_ctx *c, const uint64_t *in, void *out, int64_t npoly, cons
   else { if (mg) launch_fwd<13, 1>(c, in, out, npoly, *mg, st); else launch_fwd<13, 0>(c, in, out, npoly, z, st); }
 }
 
-void inv_ntt(const hl_ctx *c, const uint64_t *in, uint64_t *out, int64_t npoly, cudaStream_t st) {
-  if (c->N == 4096) launch_inv<12>(c, in, out, npoly, st); else launch_inv<13>(c, in, out, npoly, st);
+// ct_mode: the polynomials are ciphertext halves (c0, c1, c0, ...): c1 is only reordered to the
+// boundary's evaluation form (reading C26)
+void inv_ntt(const hl_ctx *c, const uint64_t *in, uint64_t *out, int64_t npoly, cudaStream_t st, int ct_mode = 0) {
+  if (c->N == 4096) launch_inv<12>(c, in, out, npoly, st, ct_mode); else launch_inv<13>(c, in, out, npoly, st, ct_mode);
 }
 
 template <int CW, int LN>
@@ -1488,7 +1662,7 @@ extern "C" int hl_he_matmul(const hl_ctx *c, hl_tile tile, const void *wcache, i
   const MacGeom mg = mac_geom(c, g.nIs, g.nJ, nC);
   fwd_ntt(c, ct_in, workspace, g.nJ * nC, &mg, st);
   launch_mac(c, (const uint2 *)wcache, (const uint32_t *)workspace, ct_out, mg, st);
-  inv_ntt(c, ct_out, ct_out, g.nIs * nC, st);
+  inv_ntt(c, ct_out, ct_out, g.nIs * nC, st, 1);
   return hl_cuda_check("hl_he_matmul: launch");
 }
 
@@ -1498,6 +1672,7 @@ static MaskArgs mask_args(const Geo &g, int64_t Ma, int64_t Nb, uint64_t seed) {
   M.m = g.m; M.r = g.r; M.n = g.n; M.seed = seed;
   M.lm = __builtin_ctz((unsigned)g.m); M.lr = __builtin_ctz((unsigned)g.r);
   M.pk_hat = nullptr; M.u_hat = nullptr; M.cdt = nullptr; M.flood_bits = 0;
+  M.nC = (int)(2 * g.nK); M.cperm = 0;
   return M;
 }
 
@@ -1531,10 +1706,12 @@ extern "C" int hl_he_matmul_share(const hl_ctx *c, hl_tile tile, const void *wca
   }
   cudaStream_t st = (cudaStream_t)stream;
   const int64_t nC = 2 * g.nK;
-  const MacGeom mg = mac_geom(c, g.nIs, g.nJ, nC);
+  MacGeom mg = mac_geom(c, g.nIs, g.nJ, nC);
+  mg.cperm = mg.engine == 2;
   fwd_ntt(c, ct_in, workspace, g.nJ * nC, &mg, st);
   launch_mac(c, (const uint2 *)wcache, (const uint32_t *)workspace, ct_out_ntt, mg, st);
   MaskArgs M = mask_args(g, Ma, Nb, seed);
+  M.cperm = mg.cperm;
   if (c->N == 4096) launch_inv_mask<12>(c, ct_out_ntt, ct_masked, share, M, g.nIs * g.nK, st);
   else launch_inv_mask<13>(c, ct_out_ntt, ct_masked, share, M, g.nIs * g.nK, st);
   return hl_cuda_check("hl_he_matmul_share: launch");
@@ -1564,7 +1741,9 @@ static int linear_batch_run(const hl_ctx *c, hl_tile tile, int n, const hl_linea
       return rc;
     if ((rc = hl_geometry(c, d[i].tile.m ? d[i].tile : tile, d[i].Ma, d[i].R, d[i].Nb, 0, -1, &E[i].g))) return rc;
     E[i].mg = mac_geom(c, E[i].g.nIs, E[i].g.nJ, 2 * E[i].g.nK);
+    E[i].mg.cperm = E[i].mg.engine == 2;
     E[i].M = mask_args(E[i].g, d[i].Ma, d[i].Nb, d[i].seed);
+    E[i].M.cperm = E[i].mg.cperm;
   }
   cudaStream_t sc = (cudaStream_t)stream, s0 = (cudaStream_t)c->mac_stream, s1 = (cudaStream_t)c->aux_stream;
   std::vector<cudaEvent_t> ev(2 * n + 3);
@@ -1917,10 +2096,12 @@ extern "C" int hl_he_matmul_share_rr(const hl_ctx *c, hl_tile tile, const void *
     return hl_fail(HL_ERANGE, "hl_he_matmul_share_rr: flood_bits must be in [0, min(62, log2(Delta) - 1)]");
   cudaStream_t st = (cudaStream_t)stream;
   const int64_t nC = 2 * g.nK, nout = g.nIs * g.nK;
-  const MacGeom mg = mac_geom(c, g.nIs, g.nJ, nC);
+  MacGeom mg = mac_geom(c, g.nIs, g.nJ, nC);
+  mg.cperm = mg.engine == 2;
   fwd_ntt(c, ct_in, workspace, g.nJ * nC, &mg, st);
   launch_mac(c, (const uint2 *)wcache, (const uint32_t *)workspace, ct_out_ntt, mg, st);
   MaskArgs M = mask_args(g, Ma, Nb, seed);
+  M.cperm = mg.cperm;
   M.pk_hat = pk_hat; M.u_hat = rr_ws; M.cdt = c->d_cdt; M.flood_bits = flood_bits;
   {
     KTimer kt(c, HL_K_INTT_MASK, st);

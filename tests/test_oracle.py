@@ -235,6 +235,27 @@ def test_encrypt_decrypt_roundtrip_exact_noise(P4096):
     assert all(v == 0 for row in pts0 for v in row)
 
 
+def test_c1_travels_in_evaluation_form(P4096):
+    """Reading C26: a ciphertext's c1 is carried as c1_hat[k] = c1(psi^(2k+1)) (natural k).  The
+    fresh c1_hat is the evaluation, by the defining O(N^2) sum, of the polynomial a with
+    c0 + a*s = e + Delta*b over the schoolbook product, and decryption of the response is
+    unchanged (the response's c1_hat evaluates sum_J pi_A * a_J)."""
+    P, tile = P4096, (16, 32, 8)
+    X = synth.activations(61, 8, 64)
+    sk = ref.keygen(P, 62)
+    ct = ref.encrypt(P, tile, sk, X, 63)
+    e = ref.sample_e(P, 63, 0)
+    b = ref.encode_B([[int(X[k, j]) for k in range(8)] for j in range(32)], P.N, 16)
+    for l, (p, psi) in enumerate(zip(P.primes, P.psis)):
+        a_hat = ct[0, 0, 1, l]
+        a = ref.intt(P.N, p, psi, a_hat)
+        assert np.array_equal(ref.ntt_naive(P.N, p, psi, a), a_hat)      # the defining sum
+        s_l = np.array([int(v) % p for v in sk], dtype=np.uint64)
+        lhs = (ct[0, 0, 0, l].astype(object) + ref.negacyclic_mul(P.N, p, a, s_l).astype(object)) % p
+        rhs = [(int(ev) + P.delta_mod[l] * bv) % p for ev, bv in zip(e, b)]
+        assert [int(v) for v in lhs] == rhs
+
+
 def test_he_matmul_homomorphism_and_noise(P4096):
     """Dec(he_matmul) = [sum_J pi_A(A_IJ) * pi_B(B_JK)]_t over Z and the
     noise fits the Appendix C bound 2R*max|w|*(r_t + e_max) < Delta/2."""
@@ -421,12 +442,10 @@ def test_rerandomization_defeats_weight_recovery(P4096):
     pk = ref.pk_gen(P4096, sk, 115)
     ct_rr = ref.rerandomize(P4096, tile, pk, ct_out, 1, 116, 0)
     p, psi, N = P4096.primes[0], P4096.psis[0], P4096.N
-    a = ct_in[0, 0, 1, 0]
-    a_hat = ref.ntt(N, p, psi, a)
+    a_hat = ct_in[0, 0, 1, 0]                   # c1 travels in evaluation form (reading C26)
     inv = np.array([pow(int(v), p - 2, p) for v in a_hat], dtype=object)
 
-    def recover(c1):
-        c_hat = ref.ntt(N, p, psi, c1)
+    def recover(c_hat):
         return ref.intt(N, p, psi, np.array([(int(x) * int(y)) % p for x, y in zip(c_hat, inv)], dtype=np.uint64))
 
     wpoly = ref.encode_A([[int(W[j, i]) for j in range(R)] for i in range(Ma)], N, tile[1])
