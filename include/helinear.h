@@ -23,8 +23,13 @@
  *   X          [Nb][R]                      values < 2^log2_t
  *   W          [R][Ma]                      values < 2^log2_t (two's complement of the lift)
  *   sk         int8 [N]                     ternary {-1, 0, 1}
- *   ct_in      [nJ][nK][2][L][N]            (c0, c1) of Enc(pi_B(X^T tile JK)), coefficient form
- *   ct_out     [nI_s][nK][2][L][N]          Enc(c_IK) = sum_J a_IJ * ct_in[J][K], coefficient form
+ *   ct_in      [nJ][nK][2][L][N]            (c0, c1) of Enc(pi_B(X^T tile JK))
+ *   ct_out     [nI_s][nK][2][L][N]          Enc(c_IK) = sum_J a_IJ * ct_in[J][K]
+ * Every ciphertext (input, output, masked) carries c0 in COEFFICIENT form and c1 in EVALUATION
+ * form (reading C26 of DESIGN.md §3): c1_hat[k] = c1(psi_l^(2k+1)) mod p_l, k = 0..N-1 natural
+ * order, psi_l = g_l^((p_l - 1)/2N) with g_l the smallest primitive root mod p_l.  Fresh c1 is
+ * the PRF output itself (uniform in either form), so neither side transforms c1: the server
+ * multiplies it pointwise and the client's decryption needs c1_hat . NTT(s) only.
  *   ct_masked  compressed: [nI_s][nK][ L*m*n (c0 at pos(i,k), index k*m+i) | L*N (c1) ]
  *              full:       [nI_s][nK][2][L][N]
  *   share      [Nb][Ma]                     (server share; a shard writes only its columns)
@@ -34,7 +39,7 @@
  *
  * Randomness (reading C10): a ChaCha20 PRF (RFC 8439 block function), key = LE64(seed) || 0^24,
  * nonce = LE32(domain) || LE64(stream), block counter from 0; u64 word i = LE64(keystream[8i, 8i+8)).
- * Domains: 1 secret key (stream 0), 2 uniform a (stream g*L + l), 3 error (stream g),
+ * Domains: 1 secret key (stream 0), 2 uniform a_hat (stream g*L + l), 3 error (stream g),
  * 4 mask (stream I*nK + K, I global).  g = J*nK + K.
  *
  * Ownership: the caller allocates and owns every buffer (host or device as stated per call).
@@ -133,8 +138,8 @@ int hl_layout_query(const hl_ctx *ctx, hl_tile tile, int64_t Ma, int64_t R, int6
 int hl_keygen(const hl_ctx *ctx, uint64_t seed, int8_t *sk);
 
 /* Alg. 1 step 2: encode every tile with pi_B and encrypt with the secret key:
- *   c1 = a_l, c0 = -a_l*s + e + Delta_l*b (mod p_l), a uniform, e discrete Gaussian sigma=3.2
- *   (CDT, reading C8).  X: host [Nb][R]; ct_in: host [nJ][nK][2][L][N] (layout.ct_in_words).
+ *   c1 = a_hat_l (evaluation form, PRF domain 2), c0 = -a_l*s + e + Delta_l*b (mod p_l) with
+ *   a_l = INTT(a_hat_l), e discrete Gaussian sigma=3.2 (CDT, reading C8).  X: host [Nb][R]; ct_in: host [nJ][nK][2][L][N] (layout.ct_in_words).
  * Errors: HL_ERANGE if some X >= 2^log2_t or sk is not ternary. */
 int hl_encrypt(const hl_ctx *ctx, const int8_t *sk, hl_tile tile, const uint64_t *X, int64_t Nb,
                int64_t R, uint64_t seed, uint64_t *ct_in);
@@ -204,8 +209,9 @@ int hl_encode_weights_strided(const hl_ctx *ctx, hl_tile tile, const uint64_t *W
 /* Alg. 1 step 3, homomorphic part: for every I in the shard and every K,
  *   ct_out[I][K][c] = sum_J a_IJ * ct_in[J][K][c]  mod (X^N + 1, p_l),  c in {0, 1}
  * computed as forward NTT of ct_in -> pointwise multiply-accumulate over J against the cached
- * NTT-domain weights -> inverse NTT.  ct_in: device [nJ][nK][2][L][N]; workspace: device,
- * layout.workspace_bytes; ct_out: device [nI_s][nK][2][L][N], canonical residues. */
+ * NTT-domain weights -> inverse NTT (c0; c1 stays in evaluation form, reading C26).  ct_in: device
+ * [nJ][nK][2][L][N]; workspace: device, layout.workspace_bytes; ct_out: device [nI_s][nK][2][L][N],
+ * canonical residues. */
 int hl_he_matmul(const hl_ctx *ctx, hl_tile tile, const void *wcache, int64_t Ma, int64_t R,
                  int64_t Nb, int64_t i_begin, int64_t i_end, const uint64_t *ct_in,
                  void *workspace, uint64_t *ct_out, void *stream);
@@ -261,8 +267,8 @@ int hl_he_linear_host(const hl_ctx *ctx, hl_tile tile, const void *wcache, int64
 
 /* ---- Seeded ciphertext upload ------------------------------------ */
 
-/* The c1 half of every input ciphertext is a = PRF(enc_seed, A, g*L + l) reduced mod p_l (reading
- * C10; the same stream hl_encrypt / hl_encrypt_device draw), i.e. public randomness the client
+/* The c1 half of every input ciphertext is a_hat = PRF(enc_seed, A, g*L + l) reduced mod p_l
+ * (readings C10, C26; the same stream hl_encrypt / hl_encrypt_device draw), i.e. public randomness the client
  * need not send: it uploads the c0 halves and the seed, and the server regenerates c1.
  * hl_expand_seeded writes the c1 halves of ct_in (device [nJ][nK][2][L][N] for (R, Nb)),
  * leaving the c0 halves untouched; the result is bit-identical to the client's ciphertext.
