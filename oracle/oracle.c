@@ -363,17 +363,28 @@ void or_he_matmul_ntt_tiles(uint32_t N, uint32_t L, const uint64_t *primes, cons
   }
 }
 
-/* Alg. 1 step 3 + §3.1.3 (O7-O9; readings C3, C10-C12) for ONE output ciphertext (I, K):
- *   sigma[i] = u64_MASK(stream I*nK+K)[i] & (2^t_bits - 1)
+/* Reading C27: the mask word of coefficient position pos.  The kept positions
+ * pos(i,k) = (k*m + i)*r + r-1 (all p < m*r*n with p = r-1 mod r) take words 0 .. m*n-1 in
+ * kept-index order k*m + i; every other position takes the next word in increasing position
+ * order, i.e. m*n + (pos - #kept positions below pos).  A permutation of [0, N).             */
+uint64_t or_mask_word(uint32_t m, uint32_t r, uint32_t n, uint64_t pos) {
+  uint64_t mn = (uint64_t)m * n, mrn = mn * r;
+  if (pos < mrn && pos % r == r - 1) return pos / r;
+  return mn + pos - (pos < mrn ? pos / r : mn);
+}
+
+/* Alg. 1 step 3 + §3.1.3 (O7-O9; readings C3, C10-C12, C27) for ONE output ciphertext (I, K):
+ *   sigma[pos] = u64_MASK(stream I*nK+K)[or_mask_word(pos)] & (2^t_bits - 1)
  *   c0 <- c0 - Delta_l * sigma (mod p_l);  keep c1, keep c0 at pos(i,k) = k*m*r + i*r + r-1
  * Writes the masked ciphertext to dst and sigma at the kept positions (index k*m+i) to kept. */
 static void mask_one(uint32_t N, uint32_t L, const uint64_t *primes, const uint64_t *delta_mod,
                      uint32_t t_bits, uint32_t m, uint32_t r, uint32_t n, uint64_t stream,
                      const uint64_t *src, uint64_t seed, int compress, uint64_t *dst, uint64_t *kept) {
   uint64_t tmask = (t_bits == 64) ? ~0ull : ((1ull << t_bits) - 1);
-  uint64_t *sigma = (uint64_t *)malloc(8ull * N);
-  or_prf_u64(seed, DOM_MASK, stream, 0, N, sigma);
-  for (uint32_t i = 0; i < N; i++) sigma[i] &= tmask;
+  uint64_t *sigma = (uint64_t *)malloc(8ull * N), *words = (uint64_t *)malloc(8ull * N);
+  or_prf_u64(seed, DOM_MASK, stream, 0, N, words);
+  for (uint32_t i = 0; i < N; i++) sigma[i] = words[or_mask_word(m, r, n, i)] & tmask;
+  free(words);
   for (uint32_t l = 0; l < L; l++) {
     uint64_t p = primes[l];
     const uint64_t *c0 = src + (uint64_t)l * N, *c1 = src + (uint64_t)(L + l) * N;

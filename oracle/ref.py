@@ -66,6 +66,7 @@ def lib():
                                         ctypes.POINTER(ctypes.c_uint32), ctypes.POINTER(ctypes.c_uint32)]
         L.or_prf_u64.argtypes = [ctypes.c_uint64, ctypes.c_uint32, ctypes.c_uint64, ctypes.c_uint64,
                                  ctypes.c_uint64, u64p]
+        L.or_mask_word.restype = ctypes.c_uint64
         _lib = L
     return _lib
 
@@ -183,6 +184,13 @@ def cdt_table(sigma: float = SIGMA, tail: int = CDT_TAIL) -> list:
 def tile_counts(tile, Ma: int, R: int, Nb: int):
     m, r, n = tile
     return -(-Ma // m), -(-R // r), -(-Nb // n)
+
+
+def mask_word(tile, pos: int) -> int:
+    """Reading C27: index of the MASK-stream word used at coefficient position pos (kept
+    positions first, in kept-index order; the others after, in position order)."""
+    m, r, n = tile
+    return int(lib().or_mask_word(ctypes.c_uint32(m), ctypes.c_uint32(r), ctypes.c_uint32(n), ctypes.c_uint64(pos)))
 
 
 def kept_positions(tile) -> list:

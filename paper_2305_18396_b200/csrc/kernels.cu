@@ -460,15 +460,15 @@ k_ntt_fwd_x(const uint64_t *__restrict__ in, uint64_t *__restrict__ out, DevPara
 
 // (a'') the fused paths' X layout (MacGeom::cperm = 1, c0 columns first): forward NTT of the c0
 //       halves only, two consecutive K of one J per CTA -> adjacent columns, 16-B (slot, J) chunks
-template <int LOGN>
-__global__ void __launch_bounds__(Geom<LOGN>::NT * 2)
+template <int LOGN, int G>
+__global__ void __launch_bounds__(Geom<LOGN>::NT * G)
 k_ntt_fwd_c0(const uint64_t *__restrict__ in, uint64_t *__restrict__ out, DevParams P, MacGeom mg) {
   using Gm = Geom<LOGN>;
   extern __shared__ double sm[];
   const int sub = threadIdx.x / Gm::NT, t = threadIdx.x % Gm::NT, l = blockIdx.y;
-  const int nK = mg.nC / 2, nKh = (nK + 1) / 2;
-  const int J = (int)(blockIdx.x / (unsigned)nKh), K0 = 2 * (int)(blockIdx.x % (unsigned)nKh), K = K0 + sub;
-  const bool pair = K0 + 1 < nK;
+  const int nK = mg.nC / 2, nKh = (nK + G - 1) / G;
+  const int J = (int)(blockIdx.x / (unsigned)nKh), K0 = G * (int)(blockIdx.x % (unsigned)nKh), K = K0 + sub;
+  const bool pair = G == 2 && K0 + 1 < nK;
   const PrimeConsts pc = pick(P, l);
   double a[16];
   if (K < nK) {
@@ -478,7 +478,16 @@ k_ntt_fwd_c0(const uint64_t *__restrict__ in, uint64_t *__restrict__ out, DevPar
     for (int g = 0; g < GG; g++)
 #pragma unroll
       for (int u = 0; u < (1 << KK); u++) a[g * (1 << KK) + u] = u2d(__ldcs(in + base + elem_idx<LOGN, 0>(t, g, u)));
-    fwd_rounds_from<LOGN, 0>(a, sm + sub * Gm::SMEM_WORDS, t, P.twd_fwd + (size_t)l * Gm::N, pc.pd, pc.pinv, 1 + sub);
+    fwd_rounds_from<LOGN, 0>(a, sm + sub * Gm::SMEM_WORDS, t, P.twd_fwd + (size_t)l * Gm::N, pc.pd, pc.pinv,
+                             G > 1 ? 1 + sub : -1);
+  }
+  if constexpr (G == 1) {          // no pairing: stores straight from the registers
+    const int cg = K0 / mg.CW, cc = K0 % mg.CW;
+    uint64_t *dst0 = out + ((size_t)cg * mg.LN + (size_t)l * Gm::N) * mg.nJp * mg.CW + (size_t)J * mg.CW + cc;
+#pragma unroll
+    for (int u = 0; u < 16; u++)
+      dst0[(size_t)slot_of<LOGN>(t, u) * mg.nJp * mg.CW] = d2u(canon_d(a[u], pc.pd, pc.pinv));
+    return;
   }
   __syncthreads();
   uint64_t *xs = reinterpret_cast<uint64_t *>(sm);     // [N][2] canonical residues
@@ -688,6 +697,43 @@ __device__ __forceinline__ int64_t rr_c0_extra(const MaskArgs &M, uint64_t strea
            (1ll << (M.flood_bits - 1));
   return ext;
 }
+// Reading C27: the MASK-stream word order puts the kept positions first, so the m n masks of a
+// compressed response are the stream's first m n words: (m n)/8 ChaCha blocks, not one per kept
+// position.  sigma (kept-index order kk = k m + i) -> sig_sm, the server share, and for row f4
+// the c0 extras e1 + F at the kept positions.
+template <bool RR>
+__device__ __forceinline__ void mask_kept(const MaskArgs &M, uint64_t stream, int64_t I, int64_t K, uint64_t tmask,
+                                          uint64_t *sig_sm, int64_t *ext_sm, uint64_t *share, int t, int nthr) {
+  const int mn = M.m * M.n;
+#pragma unroll 1
+  for (int blk = t; blk < (mn + 7) / 8; blk += nthr) {
+    uint64_t w[8];
+    hl::chacha_block_u64(M.seed, hl::kDomMask, stream, (uint32_t)blk, w);
+#pragma unroll
+    for (int q = 0; q < 8; q++) {
+      const int kk = 8 * blk + q;
+      if (kk >= mn) break;
+      const uint64_t sg = w[q] & tmask;
+      sig_sm[kk] = sg;
+      const int64_t row = K * M.n + (kk >> M.lm), col = I * M.m + (kk & (M.m - 1));
+      if (row < M.Nb && col < M.Ma) share[row * M.Ma + col] = sg;
+    }
+  }
+  if constexpr (RR) {
+#pragma unroll 1
+    for (int kk = t; kk < mn; kk += nthr) ext_sm[kk] = rr_c0_extra(M, stream, (kk << M.lr) + M.r - 1);
+  }
+}
+
+// coefficient position of MASK word w (inverse of the C27 order)
+__device__ __forceinline__ int mask_pos(const MaskArgs &M, int w) {
+  const int mn = M.m * M.n;
+  if (w < mn) return (w << M.lr) + M.r - 1;
+  const int rho = w - mn;
+  if (M.r == 1 || rho >= mn * (M.r - 1)) return rho + mn;
+  return rho + rho / (M.r - 1);
+}
+
 // re-randomisation of a loaded NTT-domain polynomial: a += pk_hat[c] * u_hat  (slot order)
 template <int LOGN>
 __device__ __forceinline__ void rr_add_ntt(double (&a)[16], const MaskArgs &M, int64_t o, int c, int l, int L, int t,
@@ -757,16 +803,7 @@ k_ntt_inv_mask(const uint64_t *__restrict__ ct_ntt, uint64_t *__restrict__ maske
   int8_t *e2_sm = reinterpret_cast<int8_t *>(sig_sm);             // c1: e2 at every position
   const uint64_t stream = (uint64_t)(I * M.nK + K);
   if (c == 0) {
-#pragma unroll 1
-    for (int kk = t; kk < mn; kk += Gm::NT) {
-      const int k = kk >> M.lm, i = kk & (M.m - 1);
-      const int pos = ((k * M.m + i) << M.lr) + M.r - 1;
-      const uint64_t s = hl::prf_u64(M.seed, hl::kDomMask, stream, (uint64_t)pos) & tmask;
-      sig_sm[kk] = s;
-      const int64_t row = K * M.n + k, col = I * M.m + i;
-      if (row < M.Nb && col < M.Ma) share[row * M.Ma + col] = s;
-      if (rr) ext_sm[kk] = rr_c0_extra(M, stream, pos);
-    }
+    mask_kept<RR>(M, stream, I, K, tmask, sig_sm, ext_sm, share, t, Gm::NT);
     __syncthreads();
   } else if (rr) {
 #pragma unroll 1
@@ -865,15 +902,7 @@ k_intt_c0_pruned(const uint64_t *__restrict__ ct_ntt, uint64_t *__restrict__ mas
   const uint64_t tmask = (P.t_bits >= 64) ? ~0ull : ((1ull << P.t_bits) - 1);
   uint64_t *dst = masked + (size_t)o * L * (mn + Gm::N);
   const uint64_t stream = (uint64_t)(I * M.nK + K);
-#pragma unroll 1
-  for (int kk = t; kk < mn; kk += Gm::NT) {
-    const int k = kk >> M.lm, i = kk & (M.m - 1);
-    const uint64_t s = hl::prf_u64(M.seed, hl::kDomMask, stream, (uint64_t)(((k * M.m + i) << M.lr) + M.r - 1)) & tmask;
-    sig_sm[kk] = s;
-    const int64_t row = K * M.n + k, col = I * M.m + i;
-    if (row < M.Nb && col < M.Ma) share[row * M.Ma + col] = s;
-    if constexpr (RR) ext_sm[kk] = rr_c0_extra(M, stream, ((k * M.m + i) << M.lr) + M.r - 1);
-  }
+  mask_kept<RR>(M, stream, I, K, tmask, sig_sm, ext_sm, share, t, Gm::NT);
   // phase A: first inverse round of every prime (all threads)
   for (int l = 0; l < L; l++) {
     const PrimeConsts pc = pick(P, l);
@@ -920,28 +949,24 @@ k_intt_c0_pruned(const uint64_t *__restrict__ ct_ntt, uint64_t *__restrict__ mas
 }
 
 // ---------------------------------------------------------------------------------------
-// Unfused mask_and_share: CTA per output ct, one thread per ChaCha block (8 positions).
+// Unfused mask_and_share: CTA per output ct, one thread per ChaCha block: MASK words 8b .. 8b+7
+// (reading C27 order: positions mask_pos(w)) for c0 and the share, positions 8b .. 8b+7 for c1.
 // ---------------------------------------------------------------------------------------
 __global__ void k_mask(const uint64_t *__restrict__ ct_out, uint64_t *__restrict__ masked,
                        uint64_t *__restrict__ share, MaskArgs M, DevParams P, int compress) {
   const int N = P.N, L = P.L;
   const int64_t o = blockIdx.y;
   const int64_t Iloc = o / M.nK, K = o % M.nK, I = M.i_begin + Iloc;
-  const int b = blockIdx.x * blockDim.x + threadIdx.x;      // ChaCha block: positions 8b .. 8b+7
+  const int b = blockIdx.x * blockDim.x + threadIdx.x;
   if (b >= N / 8) return;
-  const int mn = M.m * M.n, mr = M.m * M.r;
+  const int mn = M.m * M.n;
   const uint64_t tmask = (P.t_bits >= 64) ? ~0ull : ((1ull << P.t_bits) - 1);
   const size_t per = compress ? (size_t)L * (mn + N) : (size_t)2 * L * N;
   const uint64_t *src = ct_out + (size_t)o * 2 * L * N;
   uint64_t *dst = masked + (size_t)o * per;
-  bool any_kept = false;
-#pragma unroll
-  for (int q = 0; q < 8; q++) {
-    const int pos = 8 * b + q;
-    any_kept |= pos < mr * M.n && (pos % M.r) == M.r - 1;
-  }
+  const bool words = !compress || 8 * b < mn;
   uint64_t sig[8];
-  if (!compress || any_kept) {
+  if (words) {
     hl::chacha_block_u64(M.seed, hl::kDomMask, (uint64_t)(I * M.nK + K), (uint32_t)b, sig);
 #pragma unroll
     for (int q = 0; q < 8; q++) sig[q] &= tmask;
@@ -951,34 +976,27 @@ __global__ void k_mask(const uint64_t *__restrict__ ct_out, uint64_t *__restrict
     const uint64_t *c0 = src + (size_t)l * N, *c1 = src + (size_t)(L + l) * N;
 #pragma unroll
     for (int q = 0; q < 8; q++) {
-      const int pos = 8 * b + q;
-      const bool kept = pos < mr * M.n && (pos % M.r) == M.r - 1;
-      if (!compress || kept) {
+      const int w = 8 * b + q;
+      if (words && (!compress || w < mn)) {
+        const int pos = mask_pos(M, w);
         uint64_t d = shoup_mul(sig[q], pc.delta, pc.delta_sh, pc.p);
         d = d >= pc.p ? d - pc.p : d;
         const uint64_t x = c0[pos];
         const uint64_t y = x >= d ? x - d : x + pc.p - d;
-        if (compress) {
-          const int k = pos / mr, i = (pos % mr) / M.r;
-          dst[(size_t)l * mn + k * M.m + i] = y;
-        } else {
-          dst[(size_t)l * N + pos] = y;
-        }
+        if (compress) dst[(size_t)l * mn + w] = y;            // kept word w = kept index k m + i
+        else dst[(size_t)l * N + pos] = y;
       }
-      const uint64_t v1 = c1[pos];
-      if (compress) dst[(size_t)L * mn + (size_t)l * N + pos] = v1;
-      else dst[(size_t)(L + l) * N + pos] = v1;
+      const int pos = 8 * b + q;                                // c1 (evaluation form) passes through
+      if (compress) dst[(size_t)L * mn + (size_t)l * N + pos] = c1[pos];
+      else dst[(size_t)(L + l) * N + pos] = c1[pos];
     }
   }
-  if (any_kept) {
 #pragma unroll
-    for (int q = 0; q < 8; q++) {
-      const int pos = 8 * b + q;
-      if (pos < mr * M.n && (pos % M.r) == M.r - 1) {
-        const int k = pos / mr, i = (pos % mr) / M.r;
-        const int64_t row = K * M.n + k, col = I * M.m + i;
-        if (row < M.Nb && col < M.Ma) share[row * M.Ma + col] = sig[q];
-      }
+  for (int q = 0; q < 8; q++) {
+    const int w = 8 * b + q;
+    if (words && w < mn) {
+      const int64_t row = K * M.n + (w >> M.lm), col = I * M.m + (w & (M.m - 1));
+      if (row < M.Nb && col < M.Ma) share[row * M.Ma + col] = sig[q];
     }
   }
 }
@@ -1395,12 +1413,15 @@ void launch_fwd_cperm(const hl_ctx *c, const uint64_t *in, uint64_t *out, int64_
   constexpr size_t smem2 = ntt_smem<LOGN>() * 2, smem1 = ntt_smem<LOGN>();
   static bool init = false;
   if (!init) {
-    set_smem(k_ntt_fwd_c0<LOGN>, smem2);
+    set_smem(k_ntt_fwd_c0<LOGN, 2>, smem2); set_smem(k_ntt_fwd_c0<LOGN, 1>, smem2 / 2);
     set_smem(k_c1_to_x<LOGN, 2>, 2 * smem1); set_smem(k_c1_to_x<LOGN, 1>, smem1);
     init = true;
   }
   KTimer kt(c, HL_K_NTT_FWD, st);
-  k_ntt_fwd_c0<LOGN><<<dim3((unsigned)(nJ * ((nK + 1) / 2)), c->L), Geom<LOGN>::NT * 2, smem2, st>>>(in, out, c->dp, mg);
+  if (ntt_group() >= 2)
+    k_ntt_fwd_c0<LOGN, 2><<<dim3((unsigned)(nJ * ((nK + 1) / 2)), c->L), Geom<LOGN>::NT * 2, smem2, st>>>(in, out, c->dp, mg);
+  else
+    k_ntt_fwd_c0<LOGN, 1><<<dim3((unsigned)(nJ * nK), c->L), Geom<LOGN>::NT, smem2 / 2, st>>>(in, out, c->dp, mg);
   const int G1 = nK % 2 == 0 ? 2 : 1;
   const dim3 g1((unsigned)(nJ * (nK / G1)), c->L);
   if (G1 == 2) k_c1_to_x<LOGN, 2><<<g1, Geom<LOGN>::NT, 2 * smem1, st>>>(in, out, c->dp, mg);

@@ -327,6 +327,37 @@ def test_compressed_decrypt_equals_full_and_size(P4096):
     assert mc.shape[-1] * 2 * P.N == mf.shape[-1] * (P.N + m * n)
 
 
+@pytest.mark.parametrize("tile", [(16, 8, 32), (4, 32, 32), (8, 8, 64), (16, 32, 8), (1, 1, 1), (32, 16, 16)])
+def test_mask_word_order(P4096, tile):
+    """Reading C27: the mask word order is a permutation of [0, N) that puts the kept positions
+    pos(i,k) first, at word k*m + i, and the other positions after it in increasing order."""
+    m, r, n = tile
+    N = 8192 if m * r * n > 4096 else 4096
+    words = [ref.mask_word(tile, p) for p in range(N)]
+    assert sorted(words) == list(range(N))
+    for k in range(n):
+        for i in range(m):
+            assert words[(k * m + i) * r + r - 1] == k * m + i
+    rest = [w for p, w in enumerate(words) if w >= m * n]
+    assert rest == sorted(rest)
+
+
+def test_mask_share_is_the_stream_prefix(P4096):
+    """Reading C27 end to end: the server share of output ciphertext (I, K) is the first m*n words
+    of its MASK stream (library ChaCha20, pinned above), masked to 37 bits, in kept-index order."""
+    P, tile, (Nb, Ma) = P4096, (16, 8, 32), (64, 32)
+    m, r, n = tile
+    nI, _, nK = ref.tile_counts(tile, Ma, 1, Nb)
+    ct = synth.uniform_below(71, (nI, nK, 2, P.L, P.N), P.primes)
+    _, share = ref.mask_and_share(P, tile, ct, Ma, Nb, 72, True)
+    for I in range(nI):
+        for K in range(nK):
+            w = ref.prf_u64(72, ref.DOM_MASK, I * nK + K, m * n) & np.uint64((1 << 37) - 1)
+            for k in range(n):
+                for i in range(m):
+                    assert share[K * n + k, I * m + i] == w[k * m + i]
+
+
 def test_mask_uniform_chi_squared(P4096):
     """The server share is the mask at the decoded positions: uniform on Z_{2^37}."""
     P, tile = P4096, (16, 8, 32)
