@@ -92,6 +92,34 @@ __device__ __forceinline__ PrimeConsts pick(const DevParams &P, int l) {
   return c;
 }
 
+// mbarrier / bulk-copy (TMA) helpers
+__device__ __forceinline__ uint32_t smem_u32(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+__device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra WAIT_%=;\n}" ::"r"(smem_u32(bar)), "r"(parity) : "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
+__device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+
+__device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t bytes, uint64_t *bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+               ::"r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar)) : "memory");
+}
+
 // ---------------------------------------------------------------------------------------
 // NTT round geometry.  Rounds cover the stages [S0, S0+K) of the log2(N) CT stages; round 0
 // is the short one when log2(N) is not a multiple of 4.  A thread holds G = 16 >> K groups of
@@ -506,33 +534,46 @@ k_ntt_fwd_c0(const uint64_t *__restrict__ in, uint64_t *__restrict__ out, DevPar
   }
 }
 
-// c1 halves (evaluation form, reading C26) into the permuted X layout: no transform, the
-// natural -> slot reordering through shared memory, G1 consecutive K (adjacent columns nK + K)
-// per CTA so that every (slot, J) store is 8 G1 contiguous bytes (G1 = 2 for even nK).
+// c1 halves (evaluation form, reading C26) into the permuted X layout: no transform, only the
+// natural -> slot reordering.  G1 consecutive K (adjacent columns nK + K) per CTA, so that every
+// (slot, J) store is 8 G1 contiguous bytes (a full 32-B sector for G1 = 4).  The G1 natural-order
+// polynomials arrive by bulk copies (TMA); the gather is bank-conflict free because the 16 low
+// lanes of a warp differ in the top bits of t, i.e. in the low bits of the natural index.
 template <int LOGN, int G1>
 __global__ void __launch_bounds__(Geom<LOGN>::NT)
 k_c1_to_x(const uint64_t *__restrict__ in, uint64_t *__restrict__ out, DevParams P, MacGeom mg) {
   using Gm = Geom<LOGN>;
-  extern __shared__ double sm[];
-  uint64_t *stg = reinterpret_cast<uint64_t *>(sm);    // [G1][N + N/16] natural order, padded
-  const int t = threadIdx.x, l = blockIdx.y;
+  extern __shared__ __align__(128) unsigned char smc[];
+  const uint64_t *stg = reinterpret_cast<const uint64_t *>(smc);          // [G1][N] natural order
+  __shared__ __align__(8) uint64_t bar;
+  const int l = blockIdx.y, lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int nK = mg.nC / 2, nKg = nK / G1;
   const int J = (int)(blockIdx.x / (unsigned)nKg), K0 = G1 * (int)(blockIdx.x % (unsigned)nKg);
+  if (threadIdx.x == 0) {
+    mbar_init(&bar, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    mbar_expect_tx(&bar, G1 * Gm::N * 8);
 #pragma unroll
-  for (int g = 0; g < G1; g++) {
-    const uint64_t *src = in + (((size_t)J * nK + K0 + g) * 2 * P.L + P.L + l) * Gm::N;
-#pragma unroll
-    for (int j = 0; j < 16; j++) stg[g * Gm::SMEM_WORDS + pad_idx(t + j * Gm::NT)] = __ldcs(src + t + j * Gm::NT);
+    for (int g = 0; g < G1; g++)
+      bulk_g2s(smc + g * Gm::N * 8, in + (((size_t)J * nK + K0 + g) * 2 * P.L + P.L + l) * Gm::N, Gm::N * 8, &bar);
   }
   __syncthreads();
+  mbar_wait(&bar, 0);
+  const int t = ((lane & 15) << (LOGN - 8)) | ((lane >> 4) << (LOGN - 9)) | warp;
   const int col = nK + K0, cg = col / mg.CW, cc = col % mg.CW;
   uint64_t *dst0 = out + ((size_t)cg * mg.LN + (size_t)l * Gm::N) * mg.nJp * mg.CW + (size_t)J * mg.CW + cc;
 #pragma unroll 4
   for (int u = 0; u < 16; u++) {
-    const int k = pad_idx(nat_of<LOGN>(t, u));          // padded: no bank conflicts on the bit-reversal gather
+    const int k = nat_of<LOGN>(t, u);
     uint64_t *dst = dst0 + (size_t)slot_of<LOGN>(t, u) * mg.nJp * mg.CW;
-    if constexpr (G1 == 2) *reinterpret_cast<ulonglong2 *>(dst) = make_ulonglong2(stg[k], stg[Gm::SMEM_WORDS + k]);
-    else *dst = stg[k];
+    if constexpr (G1 == 4) {
+      reinterpret_cast<ulonglong2 *>(dst)[0] = make_ulonglong2(stg[k], stg[Gm::N + k]);
+      reinterpret_cast<ulonglong2 *>(dst)[1] = make_ulonglong2(stg[2 * Gm::N + k], stg[3 * Gm::N + k]);
+    } else if constexpr (G1 == 2) {
+      *reinterpret_cast<ulonglong2 *>(dst) = make_ulonglong2(stg[k], stg[Gm::N + k]);
+    } else {
+      *dst = stg[k];
+    }
   }
 }
 
@@ -1020,33 +1061,6 @@ struct MacArgs {
   int N, j0, j1, accumulate;
 };
 
-__device__ __forceinline__ uint32_t smem_u32(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
-
-__device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
-}
-
-__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
-  asm volatile(
-      "{\n\t.reg .pred p;\n"
-      "WAIT_%=:\n\t"
-      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
-      "@!p bra WAIT_%=;\n}" ::"r"(smem_u32(bar)), "r"(parity) : "memory");
-}
-
-__device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
-  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
-}
-
-__device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, uint32_t bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
-}
-
-__device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t bytes, uint64_t *bar) {
-  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
-               ::"r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar)) : "memory");
-}
-
 template <int CW>
 struct MacSmem {
   static constexpr int W_BYTES = 32 * 16 * 8;
@@ -1414,7 +1428,8 @@ void launch_fwd_cperm(const hl_ctx *c, const uint64_t *in, uint64_t *out, int64_
   static bool init = false;
   if (!init) {
     set_smem(k_ntt_fwd_c0<LOGN, 2>, smem2); set_smem(k_ntt_fwd_c0<LOGN, 1>, smem2 / 2);
-    set_smem(k_c1_to_x<LOGN, 2>, 2 * smem1); set_smem(k_c1_to_x<LOGN, 1>, smem1);
+    set_smem(k_c1_to_x<LOGN, 4>, 4 * (size_t)Geom<LOGN>::N * 8); set_smem(k_c1_to_x<LOGN, 2>, 2 * (size_t)Geom<LOGN>::N * 8);
+    set_smem(k_c1_to_x<LOGN, 1>, (size_t)Geom<LOGN>::N * 8);
     init = true;
   }
   KTimer kt(c, HL_K_NTT_FWD, st);
@@ -1422,10 +1437,14 @@ void launch_fwd_cperm(const hl_ctx *c, const uint64_t *in, uint64_t *out, int64_
     k_ntt_fwd_c0<LOGN, 2><<<dim3((unsigned)(nJ * ((nK + 1) / 2)), c->L), Geom<LOGN>::NT * 2, smem2, st>>>(in, out, c->dp, mg);
   else
     k_ntt_fwd_c0<LOGN, 1><<<dim3((unsigned)(nJ * nK), c->L), Geom<LOGN>::NT, smem2 / 2, st>>>(in, out, c->dp, mg);
-  const int G1 = nK % 2 == 0 ? 2 : 1;
+  // G1 = 4 needs 4 | nK and 4 | CW (the 4 columns in one group); 4 x 64 KB does not fit at N = 8192
+  static const int g1max = [] { const char *e = getenv("HELINEAR_C1_G"); return e ? atoi(e) : 4; }();
+  const int G1 = (g1max >= 4 && nK % 4 == 0 && mg.CW % 4 == 0 && LOGN == 12) ? 4 : (g1max >= 2 && nK % 2 == 0 ? 2 : 1);
   const dim3 g1((unsigned)(nJ * (nK / G1)), c->L);
-  if (G1 == 2) k_c1_to_x<LOGN, 2><<<g1, Geom<LOGN>::NT, 2 * smem1, st>>>(in, out, c->dp, mg);
-  else k_c1_to_x<LOGN, 1><<<g1, Geom<LOGN>::NT, smem1, st>>>(in, out, c->dp, mg);
+  constexpr size_t pb = (size_t)Geom<LOGN>::N * 8;
+  if (G1 == 4) k_c1_to_x<LOGN, 4><<<g1, Geom<LOGN>::NT, 4 * pb, st>>>(in, out, c->dp, mg);
+  else if (G1 == 2) k_c1_to_x<LOGN, 2><<<g1, Geom<LOGN>::NT, 2 * pb, st>>>(in, out, c->dp, mg);
+  else k_c1_to_x<LOGN, 1><<<g1, Geom<LOGN>::NT, pb, st>>>(in, out, c->dp, mg);
 }
 
 // MODE 0 (u64, slot order) when mg == nullptr, else MODE 1 (the MAC engine's X layout)
