@@ -496,7 +496,7 @@ k_ntt_fwd_c0(const uint64_t *__restrict__ in, uint64_t *__restrict__ out, DevPar
   const int sub = threadIdx.x / Gm::NT, t = threadIdx.x % Gm::NT, l = blockIdx.y;
   const int nK = mg.nC / 2, nKh = (nK + G - 1) / G;
   const int J = (int)(blockIdx.x / (unsigned)nKh), K0 = G * (int)(blockIdx.x % (unsigned)nKh), K = K0 + sub;
-  const bool pair = G == 2 && K0 + 1 < nK;
+  const bool full = K0 + G <= nK;
   const PrimeConsts pc = pick(P, l);
   double a[16];
   if (K < nK) {
@@ -518,19 +518,24 @@ k_ntt_fwd_c0(const uint64_t *__restrict__ in, uint64_t *__restrict__ out, DevPar
     return;
   }
   __syncthreads();
-  uint64_t *xs = reinterpret_cast<uint64_t *>(sm);     // [N][2] canonical residues
+  uint64_t *xs = reinterpret_cast<uint64_t *>(sm);     // [N][G] canonical residues
   if (K < nK) {
 #pragma unroll
-    for (int u = 0; u < 16; u++) xs[slot_of<LOGN>(t, u) * 2 + sub] = d2u(canon_d(a[u], pc.pd, pc.pinv));
+    for (int u = 0; u < 16; u++) xs[slot_of<LOGN>(t, u) * G + sub] = d2u(canon_d(a[u], pc.pd, pc.pinv));
   }
   __syncthreads();
   const int cg = K0 / mg.CW, cc = K0 % mg.CW;
   uint64_t *dst0 = out + ((size_t)cg * mg.LN + (size_t)l * Gm::N) * mg.nJp * mg.CW + (size_t)J * mg.CW + cc;
 #pragma unroll 2
-  for (int sl = threadIdx.x; sl < Gm::N; sl += Gm::NT * 2) {
+  for (int sl = threadIdx.x; sl < Gm::N; sl += Gm::NT * G) {
     uint64_t *dst = dst0 + (size_t)sl * mg.nJp * mg.CW;
-    if (pair) *reinterpret_cast<ulonglong2 *>(dst) = *reinterpret_cast<const ulonglong2 *>(xs + sl * 2);
-    else *dst = xs[sl * 2];
+    const ulonglong2 *src = reinterpret_cast<const ulonglong2 *>(xs + sl * G);
+    if (full) {                                         // G adjacent columns: 8 G contiguous bytes
+#pragma unroll
+      for (int h = 0; h < G / 2; h++) reinterpret_cast<ulonglong2 *>(dst)[h] = src[h];
+    } else {
+      for (int g = 0; g < nK - K0; g++) dst[g] = xs[sl * G + g];
+    }
   }
 }
 
@@ -1428,12 +1433,15 @@ void launch_fwd_cperm(const hl_ctx *c, const uint64_t *in, uint64_t *out, int64_
   static bool init = false;
   if (!init) {
     set_smem(k_ntt_fwd_c0<LOGN, 2>, smem2); set_smem(k_ntt_fwd_c0<LOGN, 1>, smem2 / 2);
+    if constexpr (LOGN == 12) set_smem(k_ntt_fwd_c0<LOGN, 4>, smem2 * 2);
     set_smem(k_c1_to_x<LOGN, 4>, 4 * (size_t)Geom<LOGN>::N * 8); set_smem(k_c1_to_x<LOGN, 2>, 2 * (size_t)Geom<LOGN>::N * 8);
     set_smem(k_c1_to_x<LOGN, 1>, (size_t)Geom<LOGN>::N * 8);
     init = true;
   }
   KTimer kt(c, HL_K_NTT_FWD, st);
-  if (ntt_group() >= 2)
+  if (LOGN == 12 && ntt_group() >= 4 && nK % 4 == 0 && mg.CW % 4 == 0)
+    k_ntt_fwd_c0<12, 4><<<dim3((unsigned)(nJ * (nK / 4)), c->L), Geom<12>::NT * 4, smem2 * 2, st>>>(in, out, c->dp, mg);
+  else if (ntt_group() >= 2)
     k_ntt_fwd_c0<LOGN, 2><<<dim3((unsigned)(nJ * ((nK + 1) / 2)), c->L), Geom<LOGN>::NT * 2, smem2, st>>>(in, out, c->dp, mg);
   else
     k_ntt_fwd_c0<LOGN, 1><<<dim3((unsigned)(nJ * nK), c->L), Geom<LOGN>::NT, smem2 / 2, st>>>(in, out, c->dp, mg);
