@@ -185,6 +185,11 @@ def run_ours(args, rank, world, local_rank):
     entries = [dict(wcache=m["wc"], Ma=m["mm"].Ma, R=m["mm"].R, Nb=m["mm"].Nb, ct_in=m["ct"], seed=m["seed"], tile=m["tile"],
                     workspace=m["ws"], ct_out_ntt=m["co"], ct_masked=m["masked"], share=m["share"]) for m in mats]
 
+    # the four products are independent: submit them in the order measured fastest for the pipeline
+    # (tools/gpu/order_sweep.sh, all 24 orders; synth Config.batch_order)
+    order = list(cfg.batch_order) if cfg.batch_order else list(range(len(entries)))
+    batch = [entries[i] for i in order]
+
     def step():
         if shard:
             for m in mats:
@@ -203,7 +208,7 @@ def run_ours(args, rank, world, local_rank):
                                     workspace=workspace, ct_out_ntt=ct_out_ntt, ct_masked=m["masked"],
                                     share=m["share"], stream=stream)
         else:
-            ctx.he_linear_batch(tiles[0], entries, stream=stream)
+            ctx.he_linear_batch(tiles[0], batch, stream=stream)
 
     def barrier():
         if world > 1:
@@ -381,7 +386,7 @@ def run_ours(args, rank, world, local_rank):
 
     def e2e_step():
         if not shard:
-            ctx.he_linear_batch_host(tiles[0], host_entries, stream=stream)
+            ctx.he_linear_batch_host(tiles[0], [host_entries[i] for i in order], stream=stream)
             return
         for m, hm, hs in zip(mats, host_masked, host_share):
             mm = m["mm"]
@@ -475,6 +480,7 @@ def run_ours(args, rank, world, local_rank):
         "config": {"workload": f"{cfg.name}: {cfg.note}", "N": cfg.N, "L": cfg.L, "t_bits": synth.T_BITS,
                    "tile": [list(t) for t in tiles],
                    "tile_choice": "--tile override" if args.tile else "per product, hl_plan_tile (DESIGN.md §5)",
+                   "batch_order": [cfg.matmuls[i].name for i in order],
                    "matmuls": [[mm.Nb, mm.R, mm.Ma] for mm in cfg.matmuls],
                    "blocks_per_step_per_rank": 1, "compress": True,
                    "l2": "inputs larger than L2: 3.6 GB NTT-domain weight cache + 352 MB ct_in per block",

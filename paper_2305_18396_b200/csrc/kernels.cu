@@ -1768,9 +1768,10 @@ extern "C" int hl_he_matmul_share(const hl_ctx *c, hl_tile tile, const void *wca
 // ---------------------------------------------------------------------------------------
 // Pipelined batch of compressed he_matmul_share calls (e.g. the four products of an encoder
 // block).  The MAC is HBM-bound (weight cache) while the NTT kernels are bound by the FP64 pipe
-// and latency, so they share SMs well: MAC(i) runs on the context's high-priority stream while
-// the forward NTT of entry i+1 and the inverse NTT + mask of entry i-1 run on its low-priority
-// stream; `stream` is joined to both at the start and at the end.
+// and latency, so they share SMs: the MACs run in entry order on the context's high-priority
+// stream, every forward NTT is issued up front on the low-priority forward stream and the
+// inverse NTT + mask of entry i on the low-priority auxiliary stream once MAC(i) is done;
+// `stream` is joined to all of them at the start and at the end.
 // ---------------------------------------------------------------------------------------
 // ready[i] (optional): event the forward NTT of entry i waits for (its input upload);
 // done[i] (optional): recorded on the auxiliary stream once entry i's results are written.
@@ -1799,7 +1800,10 @@ static int linear_batch_run(const hl_ctx *c, hl_tile tile, int n, const hl_linea
     if (cudaEventCreateWithFlags(&e, cudaEventDisableTiming) != cudaSuccess) return hl_cuda_check("hl_he_linear_batch: events");
   cudaEvent_t *e_fwd = ev.data(), *e_mac = ev.data() + n, e_in = ev[2 * n], e_done = ev[2 * n + 1];
   cudaEvent_t e_macs = ev[2 * n + 2];
-  const bool split = ready != nullptr;
+  // every forward NTT is issued up front on the forward stream (measured: 1.082 -> 1.060 ms per c2
+  // block vs interleaving them with the MACs); HELINEAR_BATCH_INTERLEAVE=1 restores the interleaving
+  static const bool interleave = getenv("HELINEAR_BATCH_INTERLEAVE") != nullptr;
+  const bool split = ready != nullptr || !interleave;
   cudaStream_t sf = split ? (cudaStream_t)c->fwd_stream : s1;
   auto fwd = [&](int i) {
     if (ready) cudaStreamWaitEvent(sf, ready[i], 0);
@@ -1812,16 +1816,27 @@ static int linear_batch_run(const hl_ctx *c, hl_tile tile, int n, const hl_linea
     if (c->N == 4096) launch_inv_mask<12>(c, d[i].ct_out_ntt, d[i].ct_masked, d[i].share, E[i].M, E[i].g.nIs * E[i].g.nK, s1);
     else launch_inv_mask<13>(c, d[i].ct_out_ntt, d[i].ct_masked, d[i].share, E[i].M, E[i].g.nIs * E[i].g.nK, s1);
   };
+  // compute order = entry order (the caller's choice: tools/gpu/order_sweep.sh measures all orders);
+  // HELINEAR_BATCH_ORDER="3,1,0,2" overrides it for experiments
+  std::vector<int> ord(n);
+  for (int i = 0; i < n; i++) ord[i] = i;
+  static const char *order_env = getenv("HELINEAR_BATCH_ORDER");
+  if (order_env && !ready) {
+    std::vector<int> o;
+    for (const char *p = order_env; *p;) { o.push_back(atoi(p)); while (*p && *p != ',') p++; if (*p) p++; }
+    if ((int)o.size() == n) ord = o;
+  }
   cudaEventRecord(e_in, sc);                      // inputs written on `stream` are visible to both streams
   cudaStreamWaitEvent(s0, e_in, 0);
   cudaStreamWaitEvent(s1, e_in, 0);
   if (split) {
     cudaStreamWaitEvent(sf, e_in, 0);
-    for (int i = 0; i < n; i++) fwd(i);
+    for (int k = 0; k < n; k++) fwd(ord[k]);
   } else {
-    fwd(0);
+    fwd(ord[0]);
   }
-  for (int i = 0; i < n; i++) {
+  for (int k = 0; k < n; k++) {
+    const int i = ord[k];
     cudaStreamWaitEvent(s0, e_fwd[i], 0);
     static const int mac_smem = [] {
       const char *e = getenv("HELINEAR_BATCH_MAC_SMEM_KB");
@@ -1834,7 +1849,7 @@ static int linear_batch_run(const hl_ctx *c, hl_tile tile, int n, const hl_linea
     launch_mac(c, (const uint2 *)d[i].wcache, (const uint32_t *)d[i].workspace, d[i].ct_out_ntt, E[i].mg, s0,
                mac_smem, mac_grid);
     cudaEventRecord(e_mac[i], s0);
-    if (!split && i + 1 < n) fwd(i + 1);                                 // overlaps MAC(i)
+    if (!split && k + 1 < n) fwd(ord[k + 1]);                           // overlaps MAC(i)
     cudaStreamWaitEvent(s1, e_mac[i], 0);
     inv(i);                                                               // overlaps MAC(i+1)
     if (done) cudaEventRecord(done[i], s1);
