@@ -241,9 +241,13 @@ extern "C" int hl_ctx_create(uint32_t N, uint32_t L, uint32_t log2_t, const uint
     // are placed before queued NTT blocks of the concurrent low-priority stream
     int lo = 0, hi = 0;
     cudaDeviceGetStreamPriorityRange(&lo, &hi);
+    // forward-NTT stream priority (experiment knob HELINEAR_FWD_PRIO: 0 = lowest, 1 = middle, 2 = highest)
+    const char *fp = getenv("HELINEAR_FWD_PRIO");
+    const int fsel = fp ? atoi(fp) : 0;
+    const int fprio = fsel >= 2 ? hi : (fsel == 1 ? (lo + hi) / 2 : lo);
     cudaStream_t aux, mac, up, down, fwd;
     if (cudaStreamCreateWithPriority(&aux, cudaStreamNonBlocking, lo) != cudaSuccess ||
-        cudaStreamCreateWithPriority(&fwd, cudaStreamNonBlocking, lo) != cudaSuccess ||
+        cudaStreamCreateWithPriority(&fwd, cudaStreamNonBlocking, fprio) != cudaSuccess ||
         cudaStreamCreateWithPriority(&mac, cudaStreamNonBlocking, hi) != cudaSuccess ||
         cudaStreamCreateWithFlags(&up, cudaStreamNonBlocking) != cudaSuccess ||
         cudaStreamCreateWithFlags(&down, cudaStreamNonBlocking) != cudaSuccess) {

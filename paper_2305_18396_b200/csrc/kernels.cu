@@ -277,6 +277,28 @@ __device__ __forceinline__ void fwd_rounds_from(double (&a)[16], double *sm, int
   }
 }
 
+// two independent transforms (same prime) in the same threads: shared twiddles, one pair of
+// barriers per exchange for both, twice the independent butterflies per stage
+template <int LOGN, int R>
+__device__ __forceinline__ void fwd_rounds_from2(double (&a)[16], double (&b)[16], double *sma, double *smb, int t,
+                                                 const double *tw, double p, double pinv) {
+  if constexpr (R < Geom<LOGN>::NR) {
+    double wv[15];
+    load_round_tw<LOGN, R>(wv, t, tw);
+    if constexpr (R > 0) {
+      to_smem<LOGN, R - 1>(a, sma, t);
+      to_smem<LOGN, R - 1>(b, smb, t);
+      __syncthreads();
+      from_smem<LOGN, R>(a, sma, t);
+      from_smem<LOGN, R>(b, smb, t);
+      __syncthreads();
+    }
+    fwd_round<LOGN, R>(a, wv, p, pinv);
+    fwd_round<LOGN, R>(b, wv, p, pinv);
+    fwd_rounds_from2<LOGN, R + 1>(a, b, sma, smb, t, tw, p, pinv);
+  }
+}
+
 template <int LOGN, int R>
 __device__ __forceinline__ void inv_rounds_from(double (&a)[16], double *sm, int t, const double *tw,
                                                 const PrimeConsts &pc) {
@@ -536,6 +558,43 @@ k_ntt_fwd_c0(const uint64_t *__restrict__ in, uint64_t *__restrict__ out, DevPar
     } else {
       for (int g = 0; g < nK - K0; g++) dst[g] = xs[sl * G + g];
     }
+  }
+}
+
+// (a''') as k_ntt_fwd_c0<2> with both transforms in the same threads (fwd_rounds_from2): the
+//        pair's values for a slot sit in one thread, so the 16-B (slot, J) chunks are stored
+//        straight from registers (no staging, no output barrier)
+template <int LOGN>
+__global__ void __launch_bounds__(Geom<LOGN>::NT)
+k_ntt_fwd_c0x2(const uint64_t *__restrict__ in, uint64_t *__restrict__ out, DevParams P, MacGeom mg) {
+  using Gm = Geom<LOGN>;
+  extern __shared__ double sm[];
+  const int t = threadIdx.x, l = blockIdx.y;
+  const int nK = mg.nC / 2, nKh = (nK + 1) / 2;
+  const int J = (int)(blockIdx.x / (unsigned)nKh), K0 = 2 * (int)(blockIdx.x % (unsigned)nKh);
+  const bool pair = K0 + 1 < nK;
+  const PrimeConsts pc = pick(P, l);
+  double a[16], b[16];
+  const size_t base0 = (((size_t)J * nK + K0) * 2 * P.L + l) * Gm::N;       // c0 of (J, K0)
+  const size_t base1 = base0 + (pair ? (size_t)2 * P.L * Gm::N : 0);       // c0 of (J, K0 + 1)
+  constexpr int KK = Gm::k(0), GG = 16 >> KK;
+#pragma unroll
+  for (int g = 0; g < GG; g++)
+#pragma unroll
+    for (int u = 0; u < (1 << KK); u++) {
+      const int e = elem_idx<LOGN, 0>(t, g, u);
+      a[g * (1 << KK) + u] = u2d(__ldcs(in + base0 + e));
+      b[g * (1 << KK) + u] = u2d(__ldcs(in + base1 + e));
+    }
+  fwd_rounds_from2<LOGN, 0>(a, b, sm, sm + Gm::SMEM_WORDS, t, P.twd_fwd + (size_t)l * Gm::N, pc.pd, pc.pinv);
+  const int cg = K0 / mg.CW, cc = K0 % mg.CW;
+  uint64_t *dst0 = out + ((size_t)cg * mg.LN + (size_t)l * Gm::N) * mg.nJp * mg.CW + (size_t)J * mg.CW + cc;
+#pragma unroll
+  for (int u = 0; u < 16; u++) {
+    uint64_t *dst = dst0 + (size_t)slot_of<LOGN>(t, u) * mg.nJp * mg.CW;
+    const uint64_t x0 = d2u(canon_d(a[u], pc.pd, pc.pinv)), x1 = d2u(canon_d(b[u], pc.pd, pc.pinv));
+    if (pair) *reinterpret_cast<ulonglong2 *>(dst) = make_ulonglong2(x0, x1);
+    else *dst = x0;
   }
 }
 
@@ -1434,12 +1493,16 @@ void launch_fwd_cperm(const hl_ctx *c, const uint64_t *in, uint64_t *out, int64_
   if (!init) {
     set_smem(k_ntt_fwd_c0<LOGN, 2>, smem2); set_smem(k_ntt_fwd_c0<LOGN, 1>, smem2 / 2);
     if constexpr (LOGN == 12) set_smem(k_ntt_fwd_c0<LOGN, 4>, smem2 * 2);
+    set_smem(k_ntt_fwd_c0x2<LOGN>, smem2);
     set_smem(k_c1_to_x<LOGN, 4>, 4 * (size_t)Geom<LOGN>::N * 8); set_smem(k_c1_to_x<LOGN, 2>, 2 * (size_t)Geom<LOGN>::N * 8);
     set_smem(k_c1_to_x<LOGN, 1>, (size_t)Geom<LOGN>::N * 8);
     init = true;
   }
   KTimer kt(c, HL_K_NTT_FWD, st);
-  if (LOGN == 12 && ntt_group() >= 4 && nK % 4 == 0 && mg.CW % 4 == 0)
+  static const bool x2 = [] { const char *e = getenv("HELINEAR_NTT_X2"); return e ? atoi(e) != 0 : true; }();
+  if (x2)
+    k_ntt_fwd_c0x2<LOGN><<<dim3((unsigned)(nJ * ((nK + 1) / 2)), c->L), Geom<LOGN>::NT, smem2, st>>>(in, out, c->dp, mg);
+  else if (LOGN == 12 && ntt_group() >= 4 && nK % 4 == 0 && mg.CW % 4 == 0)
     k_ntt_fwd_c0<12, 4><<<dim3((unsigned)(nJ * (nK / 4)), c->L), Geom<12>::NT * 4, smem2 * 2, st>>>(in, out, c->dp, mg);
   else if (ntt_group() >= 2)
     k_ntt_fwd_c0<LOGN, 2><<<dim3((unsigned)(nJ * ((nK + 1) / 2)), c->L), Geom<LOGN>::NT * 2, smem2, st>>>(in, out, c->dp, mg);
