@@ -1500,7 +1500,7 @@ void launch_fwd_cperm(const hl_ctx *c, const uint64_t *in, uint64_t *out, int64_
   }
   KTimer kt(c, HL_K_NTT_FWD, st);
   static const bool x2 = [] { const char *e = getenv("HELINEAR_NTT_X2"); return e ? atoi(e) != 0 : true; }();
-  if (x2)
+  if (x2)   // default; four transforms per thread (254 registers) measured slower
     k_ntt_fwd_c0x2<LOGN><<<dim3((unsigned)(nJ * ((nK + 1) / 2)), c->L), Geom<LOGN>::NT, smem2, st>>>(in, out, c->dp, mg);
   else if (LOGN == 12 && ntt_group() >= 4 && nK % 4 == 0 && mg.CW % 4 == 0)
     k_ntt_fwd_c0<12, 4><<<dim3((unsigned)(nJ * (nK / 4)), c->L), Geom<12>::NT * 4, smem2 * 2, st>>>(in, out, c->dp, mg);
