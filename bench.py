@@ -337,26 +337,28 @@ def run_ours(args, rank, world, local_rank):
 
     # ---------------- row f2: the server side of one BERT-base block's attention
     # cross terms, 12 heads x (Q K^T: 128x64 . 64x128, A V: 128x128 . 128x64), both inputs shared;
-    # N=8192, L=3 (uniform shares as server operands need q ~ 2^150), tile (32, 16, 16).
+    # N=8192, L=3 (uniform shares as server operands need q ~ 2^150), per-term planner tiles.
     att_info = None
     if not shard and not args.no_attention:
         from paper_2305_18396_b200 import attention
         actx = hl.Context(8192, 3, synth.T_BITS, device=local_rank)
-        atile = (32, 16, 16)
         heads = []
+        atiles = {}
         for h in range(12):
             for (n, d, n2) in ((128, 64, 128), (128, 128, 64)):
+                # per-term tiles from the planner (term 1: Ma = n, R = d, Nb = n2; term 2: Ma = n2, Nb = n)
+                at = atiles.setdefault((n, d, n2), (actx.plan_tile(n, d, n2), actx.plan_tile(n2, d, n)))
                 sd = synth.seed_for(block, 50 + h, "x") + 10 * d
                 X0, X1 = synth.activations(sd, n, d), synth.activations(sd + 1, n, d)
                 Y0, Y1 = synth.activations(sd + 2, d, n2), synth.activations(sd + 3, d, n2)
                 sk1, sk2 = actx.keygen(sd + 4), actx.keygen(sd + 5)
-                heads.append(dict(X1=hl.to_device(X1, dev), Y1=hl.to_device(Y1, dev),
-                                  ct1=hl.to_device(actx.encrypt(sk1, atile, np.ascontiguousarray(Y0.T), sd + 6), dev),
-                                  ct2=hl.to_device(actx.encrypt(sk2, atile, X0, sd + 7), dev), seeds=(sd + 8, sd + 9)))
+                heads.append(dict(X1=hl.to_device(X1, dev), Y1=hl.to_device(Y1, dev), tiles=at,
+                                  ct1=hl.to_device(actx.encrypt(sk1, at[0], np.ascontiguousarray(Y0.T), sd + 6), dev),
+                                  ct2=hl.to_device(actx.encrypt(sk2, at[1], X0, sd + 7), dev), seeds=(sd + 8, sd + 9)))
 
         def att_step():
             for hd_ in heads:
-                attention.server_cross_product(actx, atile, hd_["X1"], hd_["Y1"], hd_["ct1"], hd_["ct2"],
+                attention.server_cross_product(actx, hd_["tiles"], hd_["X1"], hd_["Y1"], hd_["ct1"], hd_["ct2"],
                                                hd_["seeds"], stream=stream)
         att_step()
         torch.cuda.synchronize()
@@ -369,7 +371,8 @@ def run_ours(args, rank, world, local_rank):
         torch.cuda.synchronize()
         att_info = {"what": "server side of the attention cross terms of one BERT-base block (row f2, "
                             "PAPER.md:113-118): 12 heads x (QK^T, AV), 2 Pi_MatMul + local product each, online "
-                            "pi_A encoding of the server's shares, N=8192 L=3, tile (32,16,16)",
+                            "pi_A encoding of the server's shares (two-pass, no sync), N=8192 L=3, per-term "
+                            "tiles from hl_plan_tile: " + "; ".join(f"{k}: {v}" for k, v in atiles.items()),
                     "ms_per_block": round(a0.elapsed_time(a1) / nrep, 3), "cross_products": len(heads)}
         del actx
 

@@ -191,6 +191,17 @@ int hl_he_matmul_share_rr(const hl_ctx *ctx, hl_tile tile, const void *wcache, i
 
 /* ---- server side (device memory, stream-ordered) ----------------------------------------- */
 
+/* hl_encode_weights_strided in two passes with a caller-provided device scratch of
+ * nI_shard * nJ * L * N u64 words (layout.nI_shard, layout.nJ): the forward NTTs write u64
+ * residues to scratch with coalesced stores, then one pass writes the tensor-core cache's byte
+ * planes in 16-B chunks (the one-pass form scatters single bytes).  Bit-identical cache.
+ * check = 0 skips the range / noise-bound verification and its stream synchronisation (online
+ * encodings of operands the caller already bounds, e.g. the server's 37-bit shares of row f2);
+ * check != 0 behaves as hl_encode_weights.  Other MAC engines ignore scratch. */
+int hl_encode_weights_scratch(const hl_ctx *ctx, hl_tile tile, const uint64_t *W, int64_t R, int64_t Ma,
+                              int64_t ld_row, int64_t ld_col, int64_t i_begin, int64_t i_end, void *wcache,
+                              uint64_t *scratch, int check, void *stream);
+
 /* Alg. 1 step 1 for the server + the NTT of PAPER.md:156 fn: pi_A of every
  * (I, J) tile with I in [i_begin, i_end), lifted (C6), reduced mod p_l, forward-NTT'd into
  * `wcache` (layout.wcache_bytes, device).  W: device [R][Ma].  Synchronises `stream` once to

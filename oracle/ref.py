@@ -495,12 +495,14 @@ def fc_protocol(P: Params, tile, X: np.ndarray, X1: np.ndarray, W: np.ndarray, b
 # ----------------------------------------------------------------------------------------
 def attention_protocol(P: Params, tile, X0: np.ndarray, X1: np.ndarray, Y0: np.ndarray, Y1: np.ndarray,
                        seeds=(1, 2, 3, 4, 5, 6)):
-    """Returns (client share Z0, server share Z1) of Z = (X0+X1)(Y0+Y1) mod 2^t."""
+    """Returns (client share Z0, server share Z1) of Z = (X0+X1)(Y0+Y1) mod 2^t.
+    tile: one (m, r, n) for both Pi_MatMul invocations, or a pair (term 1, term 2)."""
     tmask = np.uint64((1 << P.t_bits) - 1)
+    tile1, tile2 = (tile[0], tile[1]) if isinstance(tile[0], (tuple, list)) else (tile, tile)
     # term 1: X1 Y0 = (Y0^T X1^T)^T -- client operand Y0^T, server operand X1^T
-    t1 = matmul_protocol(P, tile, np.ascontiguousarray(Y0.T), np.ascontiguousarray(X1.T), *seeds[0:3])
+    t1 = matmul_protocol(P, tile1, np.ascontiguousarray(Y0.T), np.ascontiguousarray(X1.T), *seeds[0:3])
     # term 2: X0 Y1 -- client operand X0, server operand Y1
-    t2 = matmul_protocol(P, tile, X0, Y1, *seeds[3:6])
+    t2 = matmul_protocol(P, tile2, X0, Y1, *seeds[3:6])
     with np.errstate(over="ignore"):
         Z0 = (t1["share_client"].T + t2["share_client"] + matmul_mod_t(X0, Y0, P.t_bits)) & tmask
         Z1 = (t1["share_server"].T + t2["share_server"] + matmul_mod_t(X1, Y1, P.t_bits)) & tmask

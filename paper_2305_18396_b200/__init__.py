@@ -32,7 +32,7 @@ EXPORTS = ("hl_last_error", "hl_ctx_create", "hl_ctx_destroy", "hl_ctx_params", 
            "hl_keygen", "hl_encrypt", "hl_decrypt_share", "hl_encode_weights", "hl_he_matmul",
            "hl_mask_and_share", "hl_he_matmul_share", "hl_he_linear_batch", "hl_he_linear_host", "hl_poly_mul",
            "hl_ntt_roundtrip", "hl_timing_enable", "hl_timing_read", "hl_fc_layout", "hl_fc_encode_weights",
-           "hl_fc_local_share", "hl_encode_weights_strided", "hl_share_accumulate", "hl_sk_prepare",
+           "hl_fc_local_share", "hl_encode_weights_strided", "hl_encode_weights_scratch", "hl_share_accumulate", "hl_sk_prepare",
            "hl_encrypt_device", "hl_decrypt_share_device", "hl_pk_gen", "hl_pk_prepare", "hl_he_matmul_share_rr",
            "hl_expand_seeded", "hl_he_linear_batch_host")
 KERNELS = ("ntt_fwd", "mac", "intt_mask", "intt", "mask", "encode", "other", "fc")   # HL_K_* order
@@ -121,6 +121,7 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
         "hl_timing_enable": [vp, i32],
         "hl_fc_layout": [vp, i64, i64, i64, ctypes.POINTER(i64), ctypes.POINTER(i64)],
         "hl_encode_weights_strided": [vp, Tile, vp, i64, i64, i64, i64, i64, i64, vp, vp],
+        "hl_encode_weights_scratch": [vp, Tile, vp, i64, i64, i64, i64, i64, i64, vp, vp, ctypes.c_int, vp],
         "hl_share_accumulate": [vp, vp, vp, i64, i64, i32, vp],
         "hl_sk_prepare": [vp, vp, vp, vp],
         "hl_encrypt_device": [vp, vp, Tile, vp, i64, i64, u64, vp, vp],
@@ -316,24 +317,28 @@ class Context:
         return cm, sh
 
     # ---------------------------------------------------------------- server (device memory)
-    def encode_weights(self, tile, W, i_begin: int = 0, i_end: int = -1, wcache=None, stream=None):
-        """W: CUDA tensor [R][Ma] (int64/uint64 bits).  Returns the opaque NTT-domain cache."""
+    def encode_weights(self, tile, W, i_begin: int = 0, i_end: int = -1, wcache=None, stream=None,
+                       check: bool = True):
+        """W: CUDA tensor [R][Ma] (int64/uint64 bits).  Returns the opaque NTT-domain cache
+        (hl_encode_weights_scratch: two passes through a scratch buffer allocated here).
+        check=False skips the range / noise-bound check and its synchronisation."""
         R, Ma = W.shape
+        return self._encode(tile, W, R, Ma, Ma, 1, i_begin, i_end, wcache, stream, check)
+
+    def encode_weights_T(self, tile, M, i_begin: int = 0, i_end: int = -1, wcache=None, stream=None,
+                         check: bool = True):
+        """Encode W = M^T for a CUDA tensor M [Ma][R] without materialising the transpose."""
+        Ma, R = M.shape
+        return self._encode(tile, M, R, Ma, 1, R, i_begin, i_end, wcache, stream, check)
+
+    def _encode(self, tile, W, R, Ma, ld_row, ld_col, i_begin, i_end, wcache, stream, check):
         lay = self.layout(tile, Ma, R, 1, i_begin, i_end)
         if wcache is None:
             wcache = _dev_empty(lay.wcache_bytes // 8, W.device)
-        _check(_lib.hl_encode_weights(self._h, _tile(tile), _dptr(W), R, Ma, i_begin, i_end, _dptr(wcache),
-                                      _stream(stream)))
-        return wcache
-
-    def encode_weights_T(self, tile, M, i_begin: int = 0, i_end: int = -1, wcache=None, stream=None):
-        """Encode W = M^T for a CUDA tensor M [Ma][R] without materialising the transpose."""
-        Ma, R = M.shape
-        lay = self.layout(tile, Ma, R, 1, i_begin, i_end)
-        if wcache is None:
-            wcache = _dev_empty(lay.wcache_bytes // 8, M.device)
-        _check(_lib.hl_encode_weights_strided(self._h, _tile(tile), _dptr(M), R, Ma, 1, R, i_begin, i_end,
-                                              _dptr(wcache), _stream(stream)))
+        scratch = _dev_empty(lay.nI_shard * lay.nJ * self.L * self.N, W.device)
+        _check(_lib.hl_encode_weights_scratch(self._h, _tile(tile), _dptr(W), R, Ma, ld_row, ld_col, i_begin, i_end,
+                                              _dptr(wcache), _dptr(scratch), int(bool(check)), _stream(stream)))
+        self._enc_scratch = scratch          # alive until the next encode (stream-ordered use)
         return wcache
 
     def share_accumulate(self, dst, src, rows: int, cols: int, transpose: bool = False, stream=None):

@@ -21,13 +21,17 @@ def server_cross_product(ctx, tile, X1, Y1, ct_Y0T, ct_X0, seeds, stream=None):
     ct_X0: the client's encryption of X0 ([n][d]); seeds: the two mask seeds.
     Returns (masked_1, masked_2, Z1): the compressed responses of term 1 ((X1 Y0)^T, layout
     [n2][n] after decryption) and term 2 (X0 Y1, [n][n2]) for the client, and the server's share
-    Z1 [n][n2] of X Y (mod 2^t)."""
+    Z1 [n][n2] of X Y (mod 2^t).  tile: one (m, r, n) for both terms, or a pair (term 1, term 2)
+    (e.g. hl_plan_tile's choices for (n, d, n2) and (n2, d, n)); the client encrypts with the same."""
     n, d = X1.shape
     n2 = Y1.shape[1]
-    w1 = ctx.encode_weights_T(tile, X1, stream=stream)                     # W = X1^T: R = d, Ma = n
-    m1, s1 = ctx.he_matmul_share(tile, w1, n, d, n2, ct_Y0T, seed=seeds[0], stream=stream)   # s1 [n2][n]
-    w2 = ctx.encode_weights(tile, Y1, stream=stream)                       # W = Y1: R = d, Ma = n2
-    m2, z1 = ctx.he_matmul_share(tile, w2, n2, d, n, ct_X0, seed=seeds[1], stream=stream)    # z1 [n][n2]
+    t1, t2 = (tile[0], tile[1]) if isinstance(tile[0], (tuple, list)) else (tile, tile)
+    # the server's shares are < 2^t by construction and the N=8192/L=3 set bounds the noise of any
+    # 37-bit operand (reading C23): online encodings skip the range check and its sync
+    w1 = ctx.encode_weights_T(t1, X1, stream=stream, check=False)          # W = X1^T: R = d, Ma = n
+    m1, s1 = ctx.he_matmul_share(t1, w1, n, d, n2, ct_Y0T, seed=seeds[0], stream=stream)     # s1 [n2][n]
+    w2 = ctx.encode_weights(t2, Y1, stream=stream, check=False)            # W = Y1: R = d, Ma = n2
+    m2, z1 = ctx.he_matmul_share(t2, w2, n2, d, n, ct_X0, seed=seeds[1], stream=stream)      # z1 [n][n2]
     ctx.share_accumulate(z1, s1, n, n2, transpose=True, stream=stream)     # + <X1 Y0>_1^T
     ctx.fc_local_share(X1, ctx.fc_encode_weights(Y1, stream=stream), n2, z1, stream=stream)   # + X1 Y1
     return m1, m2, z1

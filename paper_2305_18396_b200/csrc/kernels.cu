@@ -653,7 +653,7 @@ struct EncodeArgs {
 
 template <int LOGN>
 __global__ void __launch_bounds__(Geom<LOGN>::NT)
-k_encode_weights(EncodeArgs A, uint2 *__restrict__ wcache, DevParams P, uint32_t *flags) {
+k_encode_weights(EncodeArgs A, uint2 *__restrict__ wcache, DevParams P, uint32_t *flags, uint64_t *__restrict__ scratch) {
   using Gm = Geom<LOGN>;
   extern __shared__ double sm[];
   const int t = threadIdx.x, l = blockIdx.y;
@@ -702,7 +702,9 @@ k_encode_weights(EncodeArgs A, uint2 *__restrict__ wcache, DevParams P, uint32_t
     const double xd = canon_d(a[u], pc.pd, pc.pinv);
     const uint64_t x = d2u(xd);
     const int s = l * Gm::N + slot_of<LOGN>(t, u);
-    if (A.mg.engine == 2) {
+    if (scratch) {                      // engine 2, two-pass: u64 residues now, byte planes by k_wplanes
+      if (Iloc < A.nIs) scratch[((size_t)Iloc * A.nJ + J) * A.mg.LN + s] = x;
+    } else if (A.mg.engine == 2) {
       // 7 byte planes, UMMA canonical K-major: [I tile][slot][32-J step][plane][K half][row][16 B]
       const int tt = (int)(Iloc / A.mg.RT), row = (int)(Iloc % A.mg.RT);
       const int rows = min(A.mg.RT, A.mg.nIp - A.mg.RT * tt);
@@ -753,6 +755,45 @@ k_ntt_inv(const uint64_t *in, uint64_t *out, DevParams P, int ct_mode) {
 #pragma unroll
     for (int u = 0; u < (1 << K); u++)
       out[base + elem_idx<LOGN, 0>(t, g, u)] = d2u(canon_d(a[g * (1 << K) + u], pc.pd, pc.pinv));
+}
+
+// Second pass of the two-pass weight encoding (hl_encode_weights_scratch): u64 NTT-domain
+// residues scratch [nIs][nJ][LN] -> the 7 byte planes of the tensor-core MAC's A operand
+// ([I tile][slot][32-J step][plane][K half][row][16 B]).  One thread per (I tile, 32-J step, row,
+// slot), lanes over consecutive slots (coalesced reads); every 16-B chunk of the cache is written
+// (padded rows and J are zero), so no memset is needed.
+__global__ void k_wplanes(const uint64_t *__restrict__ scratch, uint8_t *__restrict__ wcache, MacGeom g, int64_t total) {
+  const int64_t id = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (id >= total) return;
+  const int s = (int)(id % g.LN);
+  int64_t r = id / g.LN;
+  const int row = (int)(r % g.RT); r /= g.RT;
+  const int jc = (int)(r % g.nJc);
+  const int tt = (int)(r / g.nJc);
+  const int rows = min(g.RT, g.nIp - g.RT * tt);
+  if (row >= rows) return;
+  const int Iloc = tt * g.RT + row;
+  uint64_t v[32];
+#pragma unroll
+  for (int j = 0; j < 32; j++) {
+    const int J = jc * 32 + j;
+    v[j] = (Iloc < g.nIs && J < g.nJ) ? __ldcs(scratch + ((size_t)Iloc * g.nJ + J) * g.LN + s) : 0;
+  }
+  uint8_t *wb = wcache + (size_t)tt * g.RT * g.LN * g.nJp * 7 + ((size_t)s * g.nJc + jc) * 224 * rows + row * 16;
+#pragma unroll
+  for (int a = 0; a < 7; a++)
+#pragma unroll
+    for (int h = 0; h < 2; h++) {
+      uint32_t w[4];
+#pragma unroll
+      for (int q = 0; q < 4; q++) {
+        uint32_t x = 0;
+#pragma unroll
+        for (int b = 0; b < 4; b++) x |= (uint32_t)((v[h * 16 + q * 4 + b] >> (8 * a)) & 0xff) << (8 * b);
+        w[q] = x;
+      }
+      *reinterpret_cast<uint4 *>(wb + (size_t)a * 32 * rows + h * rows * 16) = make_uint4(w[0], w[1], w[2], w[3]);
+    }
 }
 
 // ---------------------------------------------------------------------------------------
@@ -1709,21 +1750,30 @@ static int check_ptrs(std::initializer_list<const void *> ps, const char *who) {
 }
 
 static int encode_weights_impl(const hl_ctx *c, hl_tile tile, const uint64_t *W, int64_t R, int64_t Ma, int64_t ld_r,
-                               int64_t ld_c, int64_t i_begin, int64_t i_end, void *wcache, void *stream);
+                               int64_t ld_c, int64_t i_begin, int64_t i_end, void *wcache, uint64_t *scratch, int check,
+                               void *stream);
 
 extern "C" int hl_encode_weights(const hl_ctx *c, hl_tile tile, const uint64_t *W, int64_t R, int64_t Ma,
                                  int64_t i_begin, int64_t i_end, void *wcache, void *stream) {
-  return encode_weights_impl(c, tile, W, R, Ma, Ma, 1, i_begin, i_end, wcache, stream);
+  return encode_weights_impl(c, tile, W, R, Ma, Ma, 1, i_begin, i_end, wcache, nullptr, 1, stream);
 }
 
 extern "C" int hl_encode_weights_strided(const hl_ctx *c, hl_tile tile, const uint64_t *W, int64_t R, int64_t Ma,
                                          int64_t ld_row, int64_t ld_col, int64_t i_begin, int64_t i_end, void *wcache,
                                          void *stream) {
-  return encode_weights_impl(c, tile, W, R, Ma, ld_row, ld_col, i_begin, i_end, wcache, stream);
+  return encode_weights_impl(c, tile, W, R, Ma, ld_row, ld_col, i_begin, i_end, wcache, nullptr, 1, stream);
+}
+
+extern "C" int hl_encode_weights_scratch(const hl_ctx *c, hl_tile tile, const uint64_t *W, int64_t R, int64_t Ma,
+                                         int64_t ld_row, int64_t ld_col, int64_t i_begin, int64_t i_end, void *wcache,
+                                         uint64_t *scratch, int check, void *stream) {
+  if (!scratch) return hl_fail(HL_EINVAL, "hl_encode_weights_scratch: scratch is NULL");
+  return encode_weights_impl(c, tile, W, R, Ma, ld_row, ld_col, i_begin, i_end, wcache, scratch, check, stream);
 }
 
 static int encode_weights_impl(const hl_ctx *c, hl_tile tile, const uint64_t *W, int64_t R, int64_t Ma, int64_t ld_r,
-                               int64_t ld_c, int64_t i_begin, int64_t i_end, void *wcache, void *stream) {
+                               int64_t ld_c, int64_t i_begin, int64_t i_end, void *wcache, uint64_t *scratch, int check,
+                               void *stream) {
   int rc;
   if ((rc = check_ptrs({c, W, wcache}, "hl_encode_weights"))) return rc;
   Geo g;
@@ -1732,23 +1782,29 @@ static int encode_weights_impl(const hl_ctx *c, hl_tile tile, const uint64_t *W,
   cudaSetDevice(c->device);
   cudaMemsetAsync(c->d_flags, 0, 8, st);
   const MacGeom mg = mac_geom(c, g.nIs, g.nJ, 2 * g.nK);
-  if (mg.engine == 2 && mg.nJp != mg.nJ)      // J padded to the 32-J MMA step: zero weight planes
+  if (mg.engine != 2) scratch = nullptr;       // the two-pass form is the tensor-core cache's
+  if (mg.engine == 2 && mg.nJp != mg.nJ && !scratch)   // J padded to the 32-J MMA step: zero weight planes
     cudaMemsetAsync(wcache, 0, (size_t)mg.nIp * mg.LN * mg.nJp * 7, st);
   EncodeArgs A{W, R, Ma, g.nJ, g.nIs, g.i_begin, g.m, g.r, mg, ld_r, ld_c};
-  dim3 grid((unsigned)((int64_t)mg.nIb * 16 * g.nJ), c->L);
+  dim3 grid((unsigned)((int64_t)(scratch ? g.nIs : (int64_t)mg.nIb * 16) * g.nJ), c->L);
   {
   KTimer kt(c, HL_K_ENCODE, st);
   if (c->N == 4096) {
     static bool init = false;
     if (!init) { set_smem(k_encode_weights<12>, ntt_smem<12>()); init = true; }
-    k_encode_weights<12><<<grid, Geom<12>::NT, ntt_smem<12>(), st>>>(A, (uint2 *)wcache, c->dp, c->d_flags);
+    k_encode_weights<12><<<grid, Geom<12>::NT, ntt_smem<12>(), st>>>(A, (uint2 *)wcache, c->dp, c->d_flags, scratch);
   } else {
     static bool init = false;
     if (!init) { set_smem(k_encode_weights<13>, ntt_smem<13>()); init = true; }
-    k_encode_weights<13><<<grid, Geom<13>::NT, ntt_smem<13>(), st>>>(A, (uint2 *)wcache, c->dp, c->d_flags);
+    k_encode_weights<13><<<grid, Geom<13>::NT, ntt_smem<13>(), st>>>(A, (uint2 *)wcache, c->dp, c->d_flags, scratch);
+  }
+  if (scratch) {
+    const int64_t total = (int64_t)mg.nIt * mg.nJc * mg.RT * mg.LN;
+    k_wplanes<<<(unsigned)((total + 255) / 256), 256, 0, st>>>(scratch, (uint8_t *)wcache, mg, total);
   }
   }
   if ((rc = hl_cuda_check("hl_encode_weights: launch"))) return rc;
+  if (!check) return HL_OK;                    // the caller vouches for the range and the noise bound
   uint32_t flags[2];
   if (cudaMemcpyAsync(flags, c->d_flags, 8, cudaMemcpyDeviceToHost, st) != cudaSuccess ||
       cudaStreamSynchronize(st) != cudaSuccess)

@@ -363,6 +363,30 @@ def test_bert_base_full_size_sampled(hl, ctx4096, mi, tile):
     assert np.array_equal(got, ref.matmul_mod_t(X, W))
 
 
+@pytest.mark.parametrize("N,shape,tile,shard", [
+    (4096, (768, 768), (16, 8, 32), (0, -1)),        # c2 O/QKV-like, no padding
+    (4096, (40, 50), (16, 8, 32), (0, -1)),          # ragged: J padded to 32, rows to 16
+    (4096, (64, 160), (16, 8, 32), (3, 9)),          # I-tile shard
+    (8192, (64, 128), (8, 8, 128), (0, -1)),         # row f2 shape, N=8192 L=3
+])
+def test_encode_two_pass_equals_one_pass(hl, ctx4096, ctx8192, N, shape, tile, shard):
+    """hl_encode_weights_scratch (u64 scratch + byte-plane pass, the binding's encode) writes the
+    same tensor-core weight cache, byte for byte, as the one-pass hl_encode_weights."""
+    import ctypes
+    ctx = ctx4096 if N == 4096 else ctx8192
+    R, Ma = shape
+    W = hl.to_device(synth.weights(777 + R, R, Ma))
+    i0, i1 = shard
+    lay = ctx.layout(tile, Ma, R, 1, i0, i1)
+    one = hl._dev_empty(lay.wcache_bytes // 8, W.device)
+    one.fill_(0x5A)
+    rc = hl._lib.hl_encode_weights(ctx._h, hl._tile(tile), hl._dptr(W), R, Ma, i0, i1, hl._dptr(one), None)
+    assert rc == 0, hl._lib.hl_last_error()
+    two = ctx.encode_weights(tile, W, i0, i1)
+    _sync()
+    assert hl.to_host(one).tobytes() == hl.to_host(two).tobytes()
+
+
 # ------------------------------------------------------------------------- errors
 def test_encode_weights_errors(hl, ctx4096):
     ctx = ctx4096
@@ -489,8 +513,11 @@ def test_fc_protocol_end_to_end(hl, ctx4096):
 
 
 # ------------------------------------------------------------------------- attention (row f2)
-@pytest.mark.parametrize("n,d,n2", [(24, 20, 24), (128, 64, 128)])
-def test_attention_cross_terms_vs_oracle(hl, ctx8192, n, d, n2):
+@pytest.mark.parametrize("n,d,n2,tiles", [
+    (24, 20, 24, None), (128, 64, 128, None),
+    (128, 128, 64, "plan"),       # the bench's per-term planner tiles (A V of one head)
+])
+def test_attention_cross_terms_vs_oracle(hl, ctx8192, n, d, n2, tiles):
     """Server side of Z = X.Y with both inputs shared: the responses and the
     server share equal the oracle's bit for bit, and with the client's decryptions plus its local
     product X0.Y0 the shares reconstruct X.Y mod 2^37 (N=8192, L=3; (128, 64, 128) = one BERT
@@ -498,20 +525,21 @@ def test_attention_cross_terms_vs_oracle(hl, ctx8192, n, d, n2):
     from paper_2305_18396_b200 import attention
     ctx = ctx8192
     P = _P(ctx)
-    tile = (32, 16, 16)
+    tile = (32, 16, 16) if tiles is None else (ctx.plan_tile(n, d, n2), ctx.plan_tile(n2, d, n))
+    t1, t2 = (tile, tile) if tiles is None else tile
     X0, X1 = synth.activations(921, n, d), synth.activations(922, n, d)
     Y0, Y1 = synth.activations(923, d, n2), synth.activations(924, d, n2)
     seeds = (931, 932, 933, 934, 935, 936)          # (key, enc, mask) of term 1, then of term 2
     sk1, sk2 = ref.keygen(P, seeds[0]), ref.keygen(P, seeds[3])
-    ct1 = ref.encrypt(P, tile, sk1, np.ascontiguousarray(Y0.T), seeds[1])
-    ct2 = ref.encrypt(P, tile, sk2, X0, seeds[4])
+    ct1 = ref.encrypt(P, t1, sk1, np.ascontiguousarray(Y0.T), seeds[1])
+    ct2 = ref.encrypt(P, t2, sk2, X0, seeds[4])
     m1, m2, z1 = attention.server_cross_product(ctx, tile, hl.to_device(X1), hl.to_device(Y1), hl.to_device(ct1),
                                                 hl.to_device(ct2), (seeds[2], seeds[5]))
     _sync()
     Z0, Z1 = ref.attention_protocol(P, tile, X0, X1, Y0, Y1, seeds)
     assert np.array_equal(hl.to_host(z1).reshape(n, n2), Z1)
-    c1 = ctx.decrypt_share(sk1, tile, hl.to_host(m1), n, n2, True)        # [n2][n]
-    c2 = ctx.decrypt_share(sk2, tile, hl.to_host(m2), n2, n, True)        # [n][n2]
+    c1 = ctx.decrypt_share(sk1, t1, hl.to_host(m1), n, n2, True)          # [n2][n]
+    c2 = ctx.decrypt_share(sk2, t2, hl.to_host(m2), n2, n, True)          # [n][n2]
     tm = np.uint64((1 << 37) - 1)
     z0 = (c1.T + c2 + ref.matmul_mod_t(X0, Y0)) & tm
     assert np.array_equal(z0, Z0)
