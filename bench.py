@@ -356,10 +356,11 @@ def run_ours(args, rank, world, local_rank):
                                   ct1=hl.to_device(actx.encrypt(sk1, at[0], np.ascontiguousarray(Y0.T), sd + 6), dev),
                                   ct2=hl.to_device(actx.encrypt(sk2, at[1], X0, sd + 7), dev), seeds=(sd + 8, sd + 9)))
 
-        def att_step():
-            for hd_ in heads:
-                attention.server_cross_product(actx, hd_["tiles"], hd_["X1"], hd_["Y1"], hd_["ct1"], hd_["ct2"],
-                                               hd_["seeds"], stream=stream)
+        items = [dict(tile=hd_["tiles"], X1=hd_["X1"], Y1=hd_["Y1"], ct_Y0T=hd_["ct1"], ct_X0=hd_["ct2"],
+                      seeds=hd_["seeds"]) for hd_ in heads]
+
+        def att_step():      # the block's 48 Pi_MatMul products as one pipelined batch
+            attention.server_cross_products(actx, items, stream=stream)
         att_step()
         torch.cuda.synchronize()
         nrep = max(2, min(args.steps, 5))
@@ -370,7 +371,8 @@ def run_ours(args, rank, world, local_rank):
         a1.record(stream)
         torch.cuda.synchronize()
         att_info = {"what": "server side of the attention cross terms of one BERT-base block (row f2, "
-                            "PAPER.md:113-118): 12 heads x (QK^T, AV), 2 Pi_MatMul + local product each, online "
+                            "PAPER.md:113-118): 12 heads x (QK^T, AV), 2 Pi_MatMul + local product each (the 48 "
+                            "products as one hl_he_linear_batch), online "
                             "pi_A encoding of the server's shares (two-pass, no sync), N=8192 L=3, per-term "
                             "tiles from hl_plan_tile: " + "; ".join(f"{k}: {v}" for k, v in atiles.items()),
                     "ms_per_block": round(a0.elapsed_time(a1) / nrep, 3), "cross_products": len(heads)}

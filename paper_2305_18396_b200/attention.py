@@ -35,3 +35,32 @@ def server_cross_product(ctx, tile, X1, Y1, ct_Y0T, ct_X0, seeds, stream=None):
     ctx.share_accumulate(z1, s1, n, n2, transpose=True, stream=stream)     # + <X1 Y0>_1^T
     ctx.fc_local_share(X1, ctx.fc_encode_weights(Y1, stream=stream), n2, z1, stream=stream)   # + X1 Y1
     return m1, m2, z1
+
+
+def server_cross_products(ctx, items, stream=None):
+    """Many cross products at once (e.g. every head of a block): items = dicts with tile (one or a
+    pair, as server_cross_product), X1, Y1, ct_Y0T, ct_X0, seeds.  The 2 len(items) Pi_MatMul
+    products run as ONE pipelined hl_he_linear_batch (each entry with its own tile), then the
+    transposed share accumulation and the local products.  Results equal server_cross_product's
+    item by item; returns [(masked_1, masked_2, Z1), ...]."""
+    entries, meta = [], []
+    for it in items:
+        tile = it["tile"]
+        t1, t2 = (tile[0], tile[1]) if isinstance(tile[0], (tuple, list)) else (tile, tile)
+        X1, Y1 = it["X1"], it["Y1"]
+        n, d = X1.shape
+        n2 = Y1.shape[1]
+        w1 = ctx.encode_weights_T(t1, X1, stream=stream, check=False)
+        entries.append(dict(wcache=w1, Ma=n, R=d, Nb=n2, ct_in=it["ct_Y0T"], seed=it["seeds"][0], tile=t1))
+        w2 = ctx.encode_weights(t2, Y1, stream=stream, check=False)
+        entries.append(dict(wcache=w2, Ma=n2, R=d, Nb=n, ct_in=it["ct_X0"], seed=it["seeds"][1], tile=t2))
+        meta.append((n, n2))
+    outs = ctx.he_linear_batch(entries[0]["tile"], entries, stream=stream)
+    res = []
+    for k, it in enumerate(items):
+        n, n2 = meta[k]
+        (m1, s1), (m2, z1) = outs[2 * k], outs[2 * k + 1]
+        ctx.share_accumulate(z1, s1, n, n2, transpose=True, stream=stream)
+        ctx.fc_local_share(it["X1"], ctx.fc_encode_weights(it["Y1"], stream=stream), n2, z1, stream=stream)
+        res.append((m1, m2, z1))
+    return res

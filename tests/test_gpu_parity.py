@@ -546,6 +546,33 @@ def test_attention_cross_terms_vs_oracle(hl, ctx8192, n, d, n2, tiles):
     assert np.array_equal((z0 + hl.to_host(z1).reshape(n, n2)) & tm, ref.matmul_mod_t((X0 + X1) & tm, (Y0 + Y1) & tm))
 
 
+def test_attention_batched_equals_single(hl, ctx8192):
+    """server_cross_products (every head's two Pi_MatMul in one hl_he_linear_batch, the bench's
+    row-f2 call) is bit-identical to server_cross_product per item (itself checked against the
+    oracle above), for a mix of head shapes and tiles."""
+    from paper_2305_18396_b200 import attention
+    ctx = ctx8192
+    items = []
+    for h, (n, d, n2) in enumerate([(128, 64, 128), (128, 128, 64), (24, 20, 24)]):
+        tiles = (ctx.plan_tile(n, d, n2), ctx.plan_tile(n2, d, n)) if h != 2 else (32, 16, 16)
+        t1, t2 = (tiles, tiles) if h == 2 else tiles
+        sd = 950 + 10 * h
+        X0, X1 = synth.activations(sd, n, d), synth.activations(sd + 1, n, d)
+        Y0, Y1 = synth.activations(sd + 2, d, n2), synth.activations(sd + 3, d, n2)
+        sk1, sk2 = ctx.keygen(sd + 4), ctx.keygen(sd + 5)
+        items.append(dict(tile=tiles, X1=hl.to_device(X1), Y1=hl.to_device(Y1),
+                          ct_Y0T=hl.to_device(ctx.encrypt(sk1, t1, np.ascontiguousarray(Y0.T), sd + 6)),
+                          ct_X0=hl.to_device(ctx.encrypt(sk2, t2, X0, sd + 7)), seeds=(sd + 8, sd + 9)))
+    single = [tuple(hl.to_host(x) for x in attention.server_cross_product(
+        ctx, it["tile"], it["X1"], it["Y1"], it["ct_Y0T"], it["ct_X0"], it["seeds"])) for it in items]
+    for _ in range(2):
+        batched = attention.server_cross_products(ctx, items)
+        _sync()
+        for k, (b, s_) in enumerate(zip(batched, single)):
+            for x, y in zip(b, s_):
+                assert np.array_equal(hl.to_host(x), y), k
+
+
 def test_share_accumulate_transpose(hl, ctx4096):
     """hl_share_accumulate: dst += src^T (and src) mod 2^37 on ragged 32x32 tiles."""
     ctx = ctx4096
