@@ -564,11 +564,12 @@ k_ntt_fwd_c0(const uint64_t *__restrict__ in, uint64_t *__restrict__ out, DevPar
 // (a''') as k_ntt_fwd_c0<2> with both transforms in the same threads (fwd_rounds_from2): the
 //        pair's values for a slot sit in one thread, so the 16-B (slot, J) chunks are stored
 //        straight from registers (no staging, no output barrier)
-template <int LOGN>
+template <int LOGN, bool C1>
 __global__ void __launch_bounds__(Geom<LOGN>::NT)
 k_ntt_fwd_c0x2(const uint64_t *__restrict__ in, uint64_t *__restrict__ out, DevParams P, MacGeom mg) {
   using Gm = Geom<LOGN>;
   extern __shared__ double sm[];
+  __shared__ __align__(8) uint64_t c1bar;
   const int t = threadIdx.x, l = blockIdx.y;
   const int nK = mg.nC / 2, nKh = (nK + 1) / 2;
   const int J = (int)(blockIdx.x / (unsigned)nKh), K0 = 2 * (int)(blockIdx.x % (unsigned)nKh);
@@ -587,6 +588,19 @@ k_ntt_fwd_c0x2(const uint64_t *__restrict__ in, uint64_t *__restrict__ out, DevP
       b[g * (1 << KK) + u] = u2d(__ldcs(in + base1 + e));
     }
   fwd_rounds_from2<LOGN, 0>(a, b, sm, sm + Gm::SMEM_WORDS, t, P.twd_fwd + (size_t)l * Gm::N, pc.pd, pc.pinv);
+  if constexpr (C1) {
+    // fused c1 pair (evaluation form, C26): the exchange buffers are free once every thread is
+    // past the last exchange; the bulk copies land while the c0 results are stored
+    __syncthreads();
+    if (t == 0) {
+      mbar_init(&c1bar, 1);
+      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+      mbar_expect_tx(&c1bar, (pair ? 2 : 1) * Gm::N * 8);
+      const uint64_t *c1src = in + (((size_t)J * nK + K0) * 2 * P.L + P.L + l) * Gm::N;
+      bulk_g2s(sm, c1src, Gm::N * 8, &c1bar);
+      if (pair) bulk_g2s(reinterpret_cast<uint64_t *>(sm) + Gm::N, c1src + (size_t)2 * P.L * Gm::N, Gm::N * 8, &c1bar);
+    }
+  }
   const int cg = K0 / mg.CW, cc = K0 % mg.CW;
   uint64_t *dst0 = out + ((size_t)cg * mg.LN + (size_t)l * Gm::N) * mg.nJp * mg.CW + (size_t)J * mg.CW + cc;
 #pragma unroll
@@ -595,6 +609,22 @@ k_ntt_fwd_c0x2(const uint64_t *__restrict__ in, uint64_t *__restrict__ out, DevP
     const uint64_t x0 = d2u(canon_d(a[u], pc.pd, pc.pinv)), x1 = d2u(canon_d(b[u], pc.pd, pc.pinv));
     if (pair) *reinterpret_cast<ulonglong2 *>(dst) = make_ulonglong2(x0, x1);
     else *dst = x0;
+  }
+  if constexpr (C1) {
+    __syncthreads();                                  // the barrier init is visible to every thread
+    mbar_wait(&c1bar, 0);
+    const uint64_t *stg = reinterpret_cast<const uint64_t *>(sm);
+    const int lane = t & 31, warp = t >> 5;
+    const int tr = ((lane & 15) << (LOGN - 8)) | ((lane >> 4) << (LOGN - 9)) | warp;   // conflict-free gather
+    const int col = nK + K0, cg1 = col / mg.CW, cc1 = col % mg.CW;
+    uint64_t *d1 = out + ((size_t)cg1 * mg.LN + (size_t)l * Gm::N) * mg.nJp * mg.CW + (size_t)J * mg.CW + cc1;
+#pragma unroll 4
+    for (int u = 0; u < 16; u++) {
+      const int k = nat_of<LOGN>(tr, u);
+      uint64_t *dst = d1 + (size_t)slot_of<LOGN>(tr, u) * mg.nJp * mg.CW;
+      if (pair) *reinterpret_cast<ulonglong2 *>(dst) = make_ulonglong2(stg[k], stg[Gm::N + k]);
+      else *dst = stg[k];
+    }
   }
 }
 
@@ -1534,15 +1564,21 @@ void launch_fwd_cperm(const hl_ctx *c, const uint64_t *in, uint64_t *out, int64_
   if (!init) {
     set_smem(k_ntt_fwd_c0<LOGN, 2>, smem2); set_smem(k_ntt_fwd_c0<LOGN, 1>, smem2 / 2);
     if constexpr (LOGN == 12) set_smem(k_ntt_fwd_c0<LOGN, 4>, smem2 * 2);
-    set_smem(k_ntt_fwd_c0x2<LOGN>, smem2);
+    set_smem(k_ntt_fwd_c0x2<LOGN, false>, smem2); set_smem(k_ntt_fwd_c0x2<LOGN, true>, smem2);
     set_smem(k_c1_to_x<LOGN, 4>, 4 * (size_t)Geom<LOGN>::N * 8); set_smem(k_c1_to_x<LOGN, 2>, 2 * (size_t)Geom<LOGN>::N * 8);
     set_smem(k_c1_to_x<LOGN, 1>, (size_t)Geom<LOGN>::N * 8);
     init = true;
   }
   KTimer kt(c, HL_K_NTT_FWD, st);
   static const bool x2 = [] { const char *e = getenv("HELINEAR_NTT_X2"); return e ? atoi(e) != 0 : true; }();
+  static const bool fuse_c1 = [] { const char *e = getenv("HELINEAR_FUSE_C1"); return e ? atoi(e) != 0 : true; }();
+  const bool fused = x2 && fuse_c1 && (nK % 2 == 0);   // c1 pairs (K0, K0+1) adjacent in the c1 column range
+  if (fused) {
+    k_ntt_fwd_c0x2<LOGN, true><<<dim3((unsigned)(nJ * ((nK + 1) / 2)), c->L), Geom<LOGN>::NT, smem2, st>>>(in, out, c->dp, mg);
+    return;
+  }
   if (x2)   // default; four transforms per thread (254 registers) measured slower
-    k_ntt_fwd_c0x2<LOGN><<<dim3((unsigned)(nJ * ((nK + 1) / 2)), c->L), Geom<LOGN>::NT, smem2, st>>>(in, out, c->dp, mg);
+    k_ntt_fwd_c0x2<LOGN, false><<<dim3((unsigned)(nJ * ((nK + 1) / 2)), c->L), Geom<LOGN>::NT, smem2, st>>>(in, out, c->dp, mg);
   else if (LOGN == 12 && ntt_group() >= 4 && nK % 4 == 0 && mg.CW % 4 == 0)
     k_ntt_fwd_c0<12, 4><<<dim3((unsigned)(nJ * (nK / 4)), c->L), Geom<12>::NT * 4, smem2 * 2, st>>>(in, out, c->dp, mg);
   else if (ntt_group() >= 2)
