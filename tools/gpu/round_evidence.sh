@@ -6,5 +6,5 @@ timeout 900 python bench.py > gpurun_out/bench.json 2> gpurun_out/bench.err; ech
 timeout 300 python bench.py --mode shard --no-cpu-baseline > gpurun_out/bench_shard.json 2> gpurun_out/bench_shard.err; echo shard=$?
 timeout 300 python bench.py --impl reference --steps 2 --warmup 1 > gpurun_out/bench_ref.json 2> gpurun_out/bench_ref.err; echo ref=$?
 timeout 300 python bench.py --steps 2 --warmup 3 --no-cpu-baseline --no-attention > gpurun_out/plain.log 2>&1 && \
-ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none -k regex:"k_mac_tc|k_ntt_fwd_c0|k_c1_to_x|k_ntt_inv_mask|k_intt_c0" -s 51 -c 34 --csv --log-file gpurun_out/launches.csv python bench.py --steps 2 --warmup 3 --no-cpu-baseline --no-attention > gpurun_out/ncu1.log 2>&1; echo ncu1=$?
-ncu --set full --clock-control none --import-source on -k regex:"k_mac_tc|k_ntt_fwd_c0|k_c1_to_x|k_ntt_inv_mask|k_intt_c0" -s 17 -c 17 -o gpurun_out/prof_full python bench.py --steps 2 --warmup 3 --no-cpu-baseline > gpurun_out/ncu2.log 2>&1; echo ncu2=$?
+ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none -k regex:"k_mac_tc|k_ntt_fwd_c0|k_ntt_inv_mask|k_intt_c0" -s 45 -c 30 --csv --log-file gpurun_out/launches.csv python bench.py --steps 2 --warmup 3 --no-cpu-baseline --no-attention > gpurun_out/ncu1.log 2>&1; echo ncu1=$?
+ncu --set full --clock-control none --import-source on -k regex:"k_mac_tc|k_ntt_fwd_c0|k_ntt_inv_mask|k_intt_c0" -s 15 -c 15 -o gpurun_out/prof_full python bench.py --steps 2 --warmup 3 --no-cpu-baseline > gpurun_out/ncu2.log 2>&1; echo ncu2=$?
