@@ -1718,7 +1718,7 @@ void launch_mac_tc(const hl_ctx *c, const void *W, const void *X, uint64_t *out,
 }
 
 constexpr int kMacSmemAlone = 232448;        // the MAC alone on the SM: the deepest ring that fits
-constexpr int kMacSmemShared = 150 * 1024;   // leaves ~77 KB for NTT CTAs running concurrently
+constexpr int kMacSmemShared = 155 * 1024;   // leaves room for one NTT CTA (~70 KB) beside the MAC (sweep: tools/gpu/ring_sweep*.sh)
 
 void launch_mac(const hl_ctx *c, const uint2 *W, const uint32_t *X, uint64_t *out, const MacGeom &g, cudaStream_t st,
                 int smem_budget = kMacSmemAlone, int grid = 0) {
