@@ -189,6 +189,8 @@ def run_ours(args, rank, world, local_rank):
     # (tools/gpu/order_sweep.sh, all 24 orders; synth Config.batch_order)
     order = list(cfg.batch_order) if cfg.batch_order else list(range(len(entries)))
     batch = [entries[i] for i in order]
+    # e2e: PCIe-bound (the downloads start once the first product is done): experiment knob
+    e2e_order = [int(x) for x in os.environ["BENCH_E2E_ORDER"].split(",")] if os.environ.get("BENCH_E2E_ORDER") else order
 
     def step():
         if shard:
@@ -379,19 +381,26 @@ def run_ours(args, rank, world, local_rank):
         del actx
 
     # ---------------- end to end through the public API on pinned host buffers
-    host_masked = [torch.empty(m["lay"].ct_masked_words, dtype=torch.int64).pin_memory() for m in mats]
+    # weak mode: the 50-bit wire format (hl_pack50) both ways -- the client packs its c0 halves
+    # (untimed, like its encryption) and unpacks the responses when it decrypts
+    packed = not shard and not os.environ.get("BENCH_E2E_UNPACKED")
+    mwords = [int(hl._lib.hl_packed50_words(m["lay"].ct_masked_words)) if packed else m["lay"].ct_masked_words
+              for m in mats]
+    host_masked = [torch.empty(w, dtype=torch.int64).pin_memory() for w in mwords]
     host_share = [torch.empty(m["lay"].share_words, dtype=torch.int64).pin_memory() for m in mats]
     dev_ct_in = torch.empty(max(m["lay"].ct_in_words for m in mats), dtype=torch.int64, device=dev)
 
     # weak mode: the pipelined seeded batch (hl_he_linear_batch_host): c0 halves + encryption seeds
     # up, c1 regenerated on the device, compressed responses + shares down, overlapped per product
     up_bufs = [torch.empty(m["lay"].ct_in_words, dtype=torch.int64, device=dev) for m in mats] if not shard else []
-    host_entries = [dict(e, ct_in=u, c0_host=m["c0_host"], enc_seed=m["enc_seed"], masked_host=hm, share_host=hs)
-                    for e, m, u, hm, hs in zip(entries, mats, up_bufs, host_masked, host_share)]
+    c0_up = [torch.from_numpy(hl.Context.pack50(m["c0_host"].numpy().view(np.uint64)).view(np.int64)).pin_memory()
+             if packed else m["c0_host"] for m in mats]
+    host_entries = [dict(e, ct_in=u, c0_host=c0, enc_seed=m["enc_seed"], masked_host=hm, share_host=hs, packed=packed)
+                    for e, m, u, c0, hm, hs in zip(entries, mats, up_bufs, c0_up, host_masked, host_share)]
 
     def e2e_step():
         if not shard:
-            ctx.he_linear_batch_host(tiles[0], [host_entries[i] for i in order], stream=stream)
+            ctx.he_linear_batch_host(tiles[0], [host_entries[i] for i in e2e_order], stream=stream)
             return
         for m, hm, hs in zip(mats, host_masked, host_share):
             mm = m["mm"]
@@ -405,7 +414,11 @@ def run_ours(args, rank, world, local_rank):
     e2e_checked = False
     if not shard:       # the host results are the device path's, bit for bit (the e2e leg does the real work)
         for m, hm, hs in zip(mats, host_masked, host_share):
-            assert torch.equal(hm, m["masked"].cpu()) and torch.equal(hs, m["share"].cpu()), "e2e results differ"
+            got = hm.numpy().view(np.uint64)
+            if packed:
+                got = hl.Context.unpack50(got, m["lay"].ct_masked_words)
+            assert np.array_equal(got, m["masked"].cpu().numpy().view(np.uint64)) and torch.equal(hs, m["share"].cpu()), \
+                "e2e results differ"
         e2e_checked = True
     barrier()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -416,8 +429,8 @@ def run_ours(args, rank, world, local_rank):
     torch.cuda.synchronize()
     barrier()
     e2e_ms = max_over_ranks(e0.elapsed_time(e1)) / e2e_steps
-    h2d = sum(m["lay"].ct_in_words * 8 // (1 if shard else 2) for m in mats)   # seeded: c0 halves only
-    d2h = sum((m["lay"].ct_masked_words + m["lay"].share_words) * 8 for m in mats)
+    h2d = sum(c0.numel() * 8 for c0 in c0_up) if not shard else sum(m["lay"].ct_in_words * 8 for m in mats)
+    d2h = sum((w + m["lay"].share_words) * 8 for w, m in zip(mwords, mats))
 
     if rank != 0:
         return None
@@ -502,7 +515,8 @@ def run_ours(args, rank, world, local_rank):
         "e2e": {"value": round(e2e_ms, 4), "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                 "call": "hl_he_linear_host per product (shard mode)" if shard else
                         "hl_he_linear_batch_host: seeded upload (c0 halves + encryption seed; c1 = a regenerated on "
-                        "the device), upload / compute / download pipelined per product",
+                        "the device), upload / compute / download pipelined per product" +
+                        (", 50-bit wire format both ways (hl_pack50)" if packed else ""),
                 "checked_equal_to_device_path": e2e_checked},
         "clocks": clk,
     }

@@ -295,12 +295,24 @@ typedef struct {
   uint64_t enc_seed;          /* the client's encryption seed (c1 regenerated on the device)       */
   uint64_t *ct_masked_host;   /* pinned host, layout.ct_masked_words (compressed response)         */
   uint64_t *share_host;       /* pinned host [Nb][Ma] server share                                 */
+  int32_t packed;             /* 1: 50-bit wire format (hl_pack50) for c0_host and ct_masked_host  */
 } hl_linear_host_desc;
 
+/* 50-bit wire format for residues (every residue is < p_l < 2^50): each group of 32 words becomes
+ * 25 words, residue i of a group at bit 50 i of the group's 1600-bit little-endian block; a last
+ * partial group is zero-filled.  Packed length of w words: hl_packed50_words(w) = ceil(w/32)*25.
+ * Host memory, OpenMP.  hl_pack50: HL_ERANGE if a word is >= 2^50. */
+int64_t hl_packed50_words(int64_t words);
+int hl_pack50(const uint64_t *in, int64_t words, uint64_t *out);
+int hl_unpack50(const uint64_t *in, int64_t words, uint64_t *out);
+
 /* The end-to-end form of hl_he_linear_batch (bench.py's e2e leg): for every entry, the c0 halves
- * are copied host->device (strided into dev.ct_in) and c1 is expanded from enc_seed, the product
+ * are copied host->device (strided into dev.ct_in; packed = 1: the 50-bit stream of the c0 halves,
+ * unpacked on the device through dev.workspace) and c1 is expanded from enc_seed, the product
  * runs as in hl_he_linear_batch, and the compressed response + share are copied back to the host
- * buffers.  Entry i+1 uploads and entry i-1 downloads while entry i computes (the context's upload
+ * buffers (packed = 1: the response in the 50-bit format, packed on the device through
+ * dev.ct_out_ntt, hl_packed50_words(layout.ct_masked_words) words; the share stays u64).  The
+ * packed format moves 25/32 of the bytes over PCIe, which bounds this call.  Entry i+1 uploads and entry i-1 downloads while entry i computes (the context's upload
  * / download streams).  Stream-ordered on `stream`: synchronise it before reading the host
  * outputs.  Results are bit-identical to hl_he_matmul_share on the client's full ciphertexts.
  * Do not run two batches on one context concurrently. */

@@ -34,7 +34,7 @@ EXPORTS = ("hl_last_error", "hl_ctx_create", "hl_ctx_destroy", "hl_ctx_params", 
            "hl_ntt_roundtrip", "hl_timing_enable", "hl_timing_read", "hl_fc_layout", "hl_fc_encode_weights",
            "hl_fc_local_share", "hl_encode_weights_strided", "hl_encode_weights_scratch", "hl_share_accumulate", "hl_sk_prepare",
            "hl_encrypt_device", "hl_decrypt_share_device", "hl_pk_gen", "hl_pk_prepare", "hl_he_matmul_share_rr",
-           "hl_expand_seeded", "hl_he_linear_batch_host")
+           "hl_expand_seeded", "hl_he_linear_batch_host", "hl_packed50_words", "hl_pack50", "hl_unpack50")
 KERNELS = ("ntt_fwd", "mac", "intt_mask", "intt", "mask", "encode", "other", "fc")   # HL_K_* order
 
 
@@ -68,7 +68,7 @@ class LinearDesc(ctypes.Structure):
 class LinearHostDesc(ctypes.Structure):
     """hl_linear_host_desc: one product of hl_he_linear_batch_host (device + pinned host pointers)."""
     _fields_ = [("dev", LinearDesc), ("c0_host", ctypes.c_void_p), ("enc_seed", ctypes.c_uint64),
-                ("ct_masked_host", ctypes.c_void_p), ("share_host", ctypes.c_void_p)]
+                ("ct_masked_host", ctypes.c_void_p), ("share_host", ctypes.c_void_p), ("packed", ctypes.c_int32)]
 
 
 @dataclass(frozen=True)
@@ -133,15 +133,19 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
         "hl_fc_local_share": [vp, vp, vp, vp, i64, i64, i64, vp, vp, vp],
         "hl_timing_read": [vp, vp, vp],
         "hl_expand_seeded": [vp, Tile, i64, i64, u64, vp, vp],
+        "hl_pack50": [vp, i64, vp],
+        "hl_unpack50": [vp, i64, vp],
         "hl_he_linear_batch_host": [vp, Tile, i32, ctypes.POINTER(LinearHostDesc), vp],
     }
-    missing = set(EXPORTS) - set(sig) - {"hl_last_error"}
+    missing = set(EXPORTS) - set(sig) - {"hl_last_error", "hl_packed50_words"}
     if missing:     # an entry point without a prototype would be called with C-int arguments
         raise ImportError(f"libhelinear binding: no signature for {sorted(missing)}")
     for name, args in sig.items():
         f = getattr(L, name)
         f.argtypes = args
         f.restype = ctypes.c_int
+    L.hl_packed50_words.argtypes = [i64]
+    L.hl_packed50_words.restype = i64
     _lib = L
     return L
 
@@ -430,16 +434,34 @@ class Context:
         """End-to-end pipelined batch on pinned host buffers (hl_he_linear_batch_host).  entries:
         the he_linear_batch dicts (ct_in = the device upload buffer, distinct per entry) plus
         c0_host (pinned CPU int64 [nJ][nK][L][N], see c0_halves), enc_seed, masked_host and
-        share_host (pinned CPU int64).  Stream-ordered: synchronise before reading the host outputs."""
+        share_host (pinned CPU int64), and optionally packed=True (c0_host and masked_host in the
+        50-bit wire format of pack50).  Stream-ordered: synchronise before reading the host outputs."""
         descs = (LinearHostDesc * len(entries))()
         keep, outs = [], []
         for d, e in zip(descs, entries):
             self._fill_desc(tile, d.dev, e, keep, outs)
             d.c0_host, d.enc_seed = e["c0_host"].data_ptr(), int(e["enc_seed"])
+            d.packed = int(bool(e.get("packed", False)))
             d.ct_masked_host, d.share_host = e["masked_host"].data_ptr(), e["share_host"].data_ptr()
             keep += [e["c0_host"], e["masked_host"], e["share_host"]] + [o for o in outs[-1]]
         _check(_lib.hl_he_linear_batch_host(self._h, _tile(tile), len(entries), descs, _stream(stream)))
         self._batch_keep = keep
+
+    @staticmethod
+    def pack50(words: np.ndarray) -> np.ndarray:
+        """50-bit wire format (hl_pack50) of uint64 words < 2^50."""
+        w = np.ascontiguousarray(words, dtype=np.uint64).reshape(-1)
+        out = np.zeros(int(_lib.hl_packed50_words(w.size)), dtype=np.uint64)
+        _check(_lib.hl_pack50(w.ctypes.data, w.size, out.ctypes.data))
+        return out
+
+    @staticmethod
+    def unpack50(packed: np.ndarray, words: int) -> np.ndarray:
+        """Inverse of pack50: the first `words` residues."""
+        p = np.ascontiguousarray(packed, dtype=np.uint64).reshape(-1)
+        out = np.zeros(words, dtype=np.uint64)
+        _check(_lib.hl_unpack50(p.ctypes.data, words, out.ctypes.data))
+        return out
 
     @staticmethod
     def c0_halves(ct):

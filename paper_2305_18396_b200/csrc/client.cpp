@@ -11,6 +11,47 @@
 
 using hl::prf_u64;
 
+// ---- 50-bit wire format (include/helinear.h) ------------------------------------------------
+extern "C" int64_t hl_packed50_words(int64_t words) { return words <= 0 ? 0 : (words + 31) / 32 * 25; }
+
+extern "C" int hl_pack50(const uint64_t *in, int64_t words, uint64_t *out) {
+  if (!in || !out || words < 0) return hl_fail(HL_EINVAL, "hl_pack50: bad arguments");
+  const int64_t ng = (words + 31) / 32;
+  int bad = 0;
+#pragma omp parallel for schedule(static) reduction(| : bad)
+  for (int64_t g = 0; g < ng; g++) {
+    uint64_t w[25] = {0};
+    for (int i = 0; i < 32; i++) {
+      const int64_t e = g * 32 + i;
+      const uint64_t v = e < words ? in[e] : 0;
+      bad |= (v >> 50) != 0;
+      const int b = 50 * i, q = b >> 6, r = b & 63;
+      w[q] |= v << r;
+      if (r > 14) w[q + 1] |= v >> (64 - r);
+    }
+    memcpy(out + g * 25, w, sizeof(w));
+  }
+  return bad ? hl_fail(HL_ERANGE, "hl_pack50: word >= 2^50") : HL_OK;
+}
+
+extern "C" int hl_unpack50(const uint64_t *in, int64_t words, uint64_t *out) {
+  if (!in || !out || words < 0) return hl_fail(HL_EINVAL, "hl_unpack50: bad arguments");
+  const int64_t ng = (words + 31) / 32;
+#pragma omp parallel for schedule(static)
+  for (int64_t g = 0; g < ng; g++) {
+    const uint64_t *w = in + g * 25;
+    for (int i = 0; i < 32; i++) {
+      const int64_t e = g * 32 + i;
+      if (e >= words) break;
+      const int b = 50 * i, q = b >> 6, r = b & 63;
+      uint64_t v = w[q] >> r;
+      if (r > 14) v |= w[q + 1] << (64 - r);
+      out[e] = v & ((1ull << 50) - 1);
+    }
+  }
+  return HL_OK;
+}
+
 extern "C" int hl_keygen(const hl_ctx *c, uint64_t seed, int8_t *sk) {
   if (!c || !sk) return hl_fail(HL_EINVAL, "hl_keygen: NULL argument");
   // s_i = (u64_SK[i] mod 3) - 1  (reading C7); one ChaCha block serves 8 coefficients

@@ -1702,6 +1702,8 @@ void launch_mac_tc(const hl_ctx *c, const void *W, const void *X, uint64_t *out,
   A.sched = (int *)((char *)X + tc_sched_offset(g));
   static const int ko = [] { const char *e = getenv("HELINEAR_MAC_KO"); return e ? atoi(e) : 0; }();
   A.ko = ko;
+  static const int pf = [] { const char *e = getenv("HELINEAR_MAC_PF"); return e ? atoi(e) : 0; }();
+  A.pf = pf;
   for (int64_t j0 = 0; j0 < g.nJp; j0 += kMacJChunk) {     // S_d < 7 * 4096 * 255^2 < 2^31 per launch
     A.jc0 = (int)(j0 / 32);
     A.njc = (int)((std::min<int64_t>(g.nJp, j0 + kMacJChunk) - j0) / 32);
@@ -1777,6 +1779,7 @@ void launch_inv_mask(const hl_ctx *c, const uint64_t *ct_ntt, uint64_t *masked, 
 // =========================================================================================
 // entry points
 // =========================================================================================
+// the first pointer must be the context
 static int check_ptrs(std::initializer_list<const void *> ps, const char *who) {
   for (const void *p : ps)
     if (!p) return hl_fail(HL_EINVAL, std::string(who) + ": NULL argument");
@@ -2045,6 +2048,35 @@ extern "C" int hl_expand_seeded(const hl_ctx *c, hl_tile tile, int64_t R, int64_
   return hl_cuda_check("hl_expand_seeded: launch");
 }
 
+// 50-bit wire format on the device (include/helinear.h hl_pack50).  Coalesced both ways: one
+// thread per packed word (gathers the <= 3 residues overlapping its 64 bits) / per residue
+// (reads the <= 2 packed words holding its 50 bits).
+__global__ void k_pack50(const uint64_t *__restrict__ in, int64_t words, uint64_t *__restrict__ out) {
+  const int64_t o = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;     // packed word
+  const int64_t g = o / 25, q = o % 25;
+  if (g * 32 >= words) return;
+  const int lo = (int)(64 * q), hi = lo + 64;                            // bit range in the group
+  uint64_t w = 0;
+  for (int i = lo / 50; i < 32 && 50 * i < hi; i++) {
+    const int64_t e = g * 32 + i;
+    const uint64_t v = e < words ? __ldg(in + e) : 0;
+    const int sh = 50 * i - lo;                                          // in (-50, 64)
+    w |= sh >= 0 ? v << sh : v >> -sh;
+  }
+  out[o] = w;
+}
+// unpack into the c0 halves of ciphertexts [nct][2][L][N] (ln = L*N words per half)
+__global__ void k_unpack50_c0(const uint64_t *__restrict__ in, int64_t words, uint64_t *__restrict__ ct, int64_t ln) {
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;     // residue
+  if (e >= words) return;
+  const int64_t g = e / 32;
+  const int b = 50 * (int)(e % 32), q = b >> 6, r = b & 63;
+  const uint64_t *w = in + g * 25;
+  uint64_t v = __ldg(w + q) >> r;
+  if (r > 14) v |= __ldg(w + q + 1) << (64 - r);
+  ct[(e / ln) * 2 * ln + e % ln] = v & ((1ull << 50) - 1);
+}
+
 // End-to-end batch on host buffers: a three-stage pipeline over the entries -- upload of entry
 // i+1 (c0 halves, strided H2D on the context's upload stream, then the c1 expansion) while entry
 // i computes (hl_he_linear_batch's streams) while entry i-1's results download (download stream).
@@ -2056,7 +2088,7 @@ extern "C" int hl_he_linear_batch_host(const hl_ctx *c, hl_tile tile, int n, con
   std::vector<hl_linear_desc> d(n);
   std::vector<hl_layout> lay(n);
   for (int i = 0; i < n; i++) {
-    if ((rc = check_ptrs({h[i].c0_host, h[i].ct_masked_host, h[i].share_host, h[i].dev.ct_in},
+    if ((rc = check_ptrs({c, h[i].c0_host, h[i].ct_masked_host, h[i].share_host, h[i].dev.ct_in},
                          "hl_he_linear_batch_host")))
       return rc;
     if ((rc = hl_layout_query(c, h[i].dev.tile.m ? h[i].dev.tile : tile, h[i].dev.Ma, h[i].dev.R, h[i].dev.Nb, 0,
@@ -2077,17 +2109,32 @@ extern "C" int hl_he_linear_batch_host(const hl_ctx *c, hl_tile tile, int n, con
   std::vector<uint64_t> seeds(n);
   for (int i = 0; i < n; i++) {
     const int64_t nct = lay[i].ct_in_words / (2 * c->L * c->N);
-    if (cudaMemcpy2DAsync(const_cast<uint64_t *>(d[i].ct_in), 2 * half, h[i].c0_host, half, half, (size_t)nct, cudaMemcpyHostToDevice,
-                          su) != cudaSuccess)
+    if (h[i].packed) {            // 50-bit stream of the c0 halves -> workspace -> unpacked into ct_in
+      const int64_t words = nct * c->L * c->N, pw = hl_packed50_words(words);
+      uint64_t *stage = reinterpret_cast<uint64_t *>(d[i].workspace);
+      if (cudaMemcpyAsync(stage, h[i].c0_host, (size_t)pw * 8, cudaMemcpyHostToDevice, su) != cudaSuccess)
+        return hl_cuda_check("hl_he_linear_batch_host: H2D");
+      k_unpack50_c0<<<(unsigned)((words + 255) / 256), 256, 0, su>>>(stage, words, const_cast<uint64_t *>(d[i].ct_in),
+                                                                   (int64_t)c->L * c->N);
+    } else if (cudaMemcpy2DAsync(const_cast<uint64_t *>(d[i].ct_in), 2 * half, h[i].c0_host, half, half, (size_t)nct,
+                                 cudaMemcpyHostToDevice, su) != cudaSuccess) {
       return hl_cuda_check("hl_he_linear_batch_host: H2D");
+    }
     cudaEventRecord(e_up[i], su);
     seeds[i] = h[i].enc_seed;
   }
   if ((rc = linear_batch_run(c, tile, n, d.data(), stream, e_up, e_res, seeds.data()))) return rc;
   for (int i = 0; i < n; i++) {
     cudaStreamWaitEvent(sd, e_res[i], 0);
-    if (cudaMemcpyAsync(h[i].ct_masked_host, d[i].ct_masked, (size_t)lay[i].ct_masked_words * 8,
-                        cudaMemcpyDeviceToHost, sd) != cudaSuccess ||
+    const uint64_t *resp = d[i].ct_masked;
+    size_t resp_bytes = (size_t)lay[i].ct_masked_words * 8;
+    if (h[i].packed) {            // packed on the device into the (now free) NTT-domain scratch
+      const int64_t words = lay[i].ct_masked_words, pw = hl_packed50_words(words);
+      k_pack50<<<(unsigned)((pw + 255) / 256), 256, 0, sd>>>(d[i].ct_masked, words, d[i].ct_out_ntt);
+      resp = d[i].ct_out_ntt;
+      resp_bytes = (size_t)hl_packed50_words(words) * 8;
+    }
+    if (cudaMemcpyAsync(h[i].ct_masked_host, resp, resp_bytes, cudaMemcpyDeviceToHost, sd) != cudaSuccess ||
         cudaMemcpyAsync(h[i].share_host, d[i].share, (size_t)lay[i].share_words * 8, cudaMemcpyDeviceToHost,
                         sd) != cudaSuccess)
       return hl_cuda_check("hl_he_linear_batch_host: D2H");

@@ -111,6 +111,26 @@ def test_plan_tile(hl):
     assert e.value.code == hl.HL_EINVAL
 
 
+def test_pack50_roundtrip(hl):
+    """50-bit wire format: exact round trip (full and partial last group, residues up to 2^50-1),
+    25/32 of the words, HL_ERANGE for a word >= 2^50."""
+    rng = np.random.default_rng(5)
+    for words in (32, 96, 1000, 1, 0):
+        v = rng.integers(0, 1 << 50, size=words, dtype=np.uint64)
+        if words:
+            v[0] = (1 << 50) - 1
+        p = hl.Context.pack50(v)
+        assert p.size == -(-words // 32) * 25
+        assert np.array_equal(hl.Context.unpack50(p, words), v)
+    # bit layout: residue i of a group starts at bit 50 i
+    v = np.zeros(32, np.uint64); v[1] = 1; v[31] = 3
+    p = hl.Context.pack50(v)
+    assert int(p[0]) == 1 << 50 and int(p[24]) == 3 << (1550 - 1536)
+    with pytest.raises(hl.HLError) as e:
+        hl.Context.pack50(np.array([1 << 50], dtype=np.uint64))
+    assert e.value.code == hl.HL_ERANGE
+
+
 def test_keygen_matches_oracle(hl):
     ctx = hl.Context(4096, 2, 37, device=-1)
     P = ref.bfv_params(4096, 2, 37)

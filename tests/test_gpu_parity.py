@@ -292,10 +292,12 @@ def test_expand_seeded_vs_oracle_encrypt(hl, ctx4096, ctx8192, N):
     assert np.array_equal(hl.to_host(dev).reshape(ct.shape), ct)
 
 
-def test_linear_batch_host_seeded_c1_vs_oracle(hl, ctx4096):
+@pytest.mark.parametrize("packed", [False, True])
+def test_linear_batch_host_seeded_c1_vs_oracle(hl, ctx4096, packed):
     """hl_he_linear_batch_host (bench.py's e2e call): only the c0 halves + the encryption seed go
     host->device, results come back to pinned host buffers; every product's compressed response
-    and share bit-exact against the oracle client + server, repeated to catch stream races."""
+    and share bit-exact against the oracle client + server, repeated to catch stream races.
+    packed: c0 halves up and responses down in the 50-bit wire format (hl_pack50)."""
     import torch
     ctx = ctx4096
     cfg = synth.CONFIGS["c1"]
@@ -309,11 +311,14 @@ def test_linear_batch_host_seeded_c1_vs_oracle(hl, ctx4096):
         ct = ref.encrypt(P, cfg.tile, sk, X, es)
         seed = synth.seed_for(0, mi, "mask")
         lay = ctx.layout(cfg.tile, mm.Ma, mm.R, mm.Nb)
-        c0 = torch.from_numpy(hl.Context.c0_halves(ct).view(np.int64).reshape(-1)).pin_memory()
+        c0 = hl.Context.c0_halves(ct)
+        c0 = hl.Context.pack50(c0) if packed else c0
+        c0 = torch.from_numpy(c0.view(np.int64).reshape(-1)).pin_memory()
+        mw = hl.Context.pack50(np.zeros(lay.ct_masked_words, np.uint64)).size if packed else lay.ct_masked_words
         entries.append(dict(wcache=ctx.encode_weights(cfg.tile, hl.to_device(W)), Ma=mm.Ma, R=mm.R, Nb=mm.Nb,
                             ct_in=torch.full((lay.ct_in_words,), 7, dtype=torch.int64, device="cuda"),
-                            seed=seed, c0_host=c0, enc_seed=es,
-                            masked_host=torch.zeros(lay.ct_masked_words, dtype=torch.int64).pin_memory(),
+                            seed=seed, c0_host=c0, enc_seed=es, packed=packed,
+                            masked_host=torch.zeros(mw, dtype=torch.int64).pin_memory(),
                             share_host=torch.zeros(lay.share_words, dtype=torch.int64).pin_memory()))
         exp.append(ref.mask_and_share(P, cfg.tile, ref.he_matmul(P, cfg.tile, W, ct, mm.Nb), mm.Ma, mm.Nb, seed))
     for rep in range(3):
@@ -323,7 +328,9 @@ def test_linear_batch_host_seeded_c1_vs_oracle(hl, ctx4096):
         ctx.he_linear_batch_host(cfg.tile, entries)
         _sync()
         for mm, e, (em, es_) in zip(cfg.matmuls, entries, exp):
-            assert np.array_equal(e["masked_host"].numpy().view(np.uint64).reshape(em.shape), em), (rep, mm.name)
+            got = e["masked_host"].numpy().view(np.uint64)
+            got = hl.Context.unpack50(got, em.size) if packed else got
+            assert np.array_equal(got.reshape(em.shape), em), (rep, mm.name)
             assert np.array_equal(e["share_host"].numpy().view(np.uint64).reshape(es_.shape), es_), (rep, mm.name)
 
 
