@@ -564,8 +564,8 @@ k_ntt_fwd_c0(const uint64_t *__restrict__ in, uint64_t *__restrict__ out, DevPar
 // (a''') as k_ntt_fwd_c0<2> with both transforms in the same threads (fwd_rounds_from2): the
 //        pair's values for a slot sit in one thread, so the 16-B (slot, J) chunks are stored
 //        straight from registers (no staging, no output barrier)
-template <int LOGN, bool C1>
-__global__ void __launch_bounds__(Geom<LOGN>::NT)
+template <int LOGN, bool C1, int MB = 1>
+__global__ void __launch_bounds__(Geom<LOGN>::NT, MB)
 k_ntt_fwd_c0x2(const uint64_t *__restrict__ in, uint64_t *__restrict__ out, DevParams P, MacGeom mg) {
   using Gm = Geom<LOGN>;
   extern __shared__ double sm[];
@@ -1565,6 +1565,9 @@ void launch_fwd_cperm(const hl_ctx *c, const uint64_t *in, uint64_t *out, int64_
     set_smem(k_ntt_fwd_c0<LOGN, 2>, smem2); set_smem(k_ntt_fwd_c0<LOGN, 1>, smem2 / 2);
     if constexpr (LOGN == 12) set_smem(k_ntt_fwd_c0<LOGN, 4>, smem2 * 2);
     set_smem(k_ntt_fwd_c0x2<LOGN, false>, smem2); set_smem(k_ntt_fwd_c0x2<LOGN, true>, smem2);
+    if constexpr (LOGN == 12) {
+      set_smem(k_ntt_fwd_c0x2<LOGN, true, 2>, smem2); set_smem(k_ntt_fwd_c0x2<LOGN, true, 3>, smem2);
+    }
     set_smem(k_c1_to_x<LOGN, 4>, 4 * (size_t)Geom<LOGN>::N * 8); set_smem(k_c1_to_x<LOGN, 2>, 2 * (size_t)Geom<LOGN>::N * 8);
     set_smem(k_c1_to_x<LOGN, 1>, (size_t)Geom<LOGN>::N * 8);
     init = true;
@@ -1573,6 +1576,16 @@ void launch_fwd_cperm(const hl_ctx *c, const uint64_t *in, uint64_t *out, int64_
   static const bool x2 = [] { const char *e = getenv("HELINEAR_NTT_X2"); return e ? atoi(e) != 0 : true; }();
   static const bool fuse_c1 = [] { const char *e = getenv("HELINEAR_FUSE_C1"); return e ? atoi(e) != 0 : true; }();
   const bool fused = x2 && fuse_c1 && (nK % 2 == 0);   // c1 pairs (K0, K0+1) adjacent in the c1 column range
+  // N = 4096: 3 CTAs per SM (80 registers, a few bytes of spill; measured best) or 2 (<= 128)
+  static const int minb = [] { const char *e = getenv("HELINEAR_X2_MINB"); return e ? atoi(e) : 3; }();
+  if constexpr (LOGN == 12) {
+    if (fused) {
+      const dim3 gx((unsigned)(nJ * ((nK + 1) / 2)), c->L);
+      if (minb >= 3) k_ntt_fwd_c0x2<LOGN, true, 3><<<gx, Geom<LOGN>::NT, smem2, st>>>(in, out, c->dp, mg);
+      else k_ntt_fwd_c0x2<LOGN, true, 2><<<gx, Geom<LOGN>::NT, smem2, st>>>(in, out, c->dp, mg);
+      return;
+    }
+  }
   if (fused) {
     k_ntt_fwd_c0x2<LOGN, true><<<dim3((unsigned)(nJ * ((nK + 1) / 2)), c->L), Geom<LOGN>::NT, smem2, st>>>(in, out, c->dp, mg);
     return;
