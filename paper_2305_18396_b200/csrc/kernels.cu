@@ -1038,6 +1038,32 @@ k_ntt_inv_mask(const uint64_t *__restrict__ ct_ntt, uint64_t *__restrict__ maske
   }
 }
 
+// c1 of the compressed response (plain responses, reading C26): the MAC output reordered from
+// slot order to natural evaluation order and reduced from the MAC's lazy range (< 4p); no
+// transform, so a light kernel (few registers, one staging buffer) instead of k_ntt_inv_mask
+template <int LOGN>
+__global__ void __launch_bounds__(Geom<LOGN>::NT)
+k_c1_out(const uint64_t *__restrict__ ct_ntt, uint64_t *__restrict__ masked, MaskArgs M, DevParams P) {
+  using Gm = Geom<LOGN>;
+  extern __shared__ double sm[];
+  const int t = threadIdx.x, L = P.L;
+  const int64_t o = blockIdx.x;
+  const int mn = M.m * M.n;
+  uint64_t *dst = masked + (size_t)o * L * (mn + Gm::N) + (size_t)L * mn;
+  for (int l = 0; l < L; l++) {
+    const uint64_t p = pick(P, l).p;
+    const uint64_t *src = ct_ntt + (ct_poly(M, o, 1) * L + l) * Gm::N;
+    uint64_t x[16];
+#pragma unroll
+    for (int u = 0; u < 16; u++) {
+      uint64_t v = __ldcs(src + slot_of<LOGN>(t, u));
+      v = v >= 2 * p ? v - 2 * p : v;
+      x[u] = v >= p ? v - p : v;
+    }
+    store_eval_slots<LOGN>(x, dst + (size_t)l * Gm::N, reinterpret_cast<uint64_t *>(sm), t, -1);
+  }
+}
+
 // ---------------------------------------------------------------------------------------
 // c0 of the compressed response, pruned (k_ntt_inv_mask computes c1).  Only the coefficients
 // pos(i,k) = (k m + i) r + r - 1, the residue class r-1 mod r, are kept.  The
@@ -1762,6 +1788,7 @@ void launch_inv_mask_t(const hl_ctx *c, const uint64_t *ct_ntt, uint64_t *masked
   if (!init) {
     set_smem(k_ntt_inv_mask<LOGN, RR>, ntt_smem<LOGN>() + (size_t)Gm::N * 16);
     set_smem(k_intt_c0_pruned<LOGN, RR>, 232448);
+    set_smem(k_c1_out<LOGN>, ntt_smem<LOGN>());
     init = true;
   }
   // the pruned c0 transform needs r in {2..16} and one warp group per prime within the CTA
@@ -1774,7 +1801,9 @@ void launch_inv_mask_t(const hl_ctx *c, const uint64_t *ct_ntt, uint64_t *masked
   KTimer kt(c, HL_K_INTT_MASK, st);
   if (prune) {
     k_intt_c0_pruned<LOGN, RR><<<(unsigned)nout, Gm::NT, smem_c0, st>>>(ct_ntt, masked, share, M, c->dp);
-    k_ntt_inv_mask<LOGN, RR><<<(unsigned)nout, Gm::NT, smem, st>>>(ct_ntt, masked, share, M, c->dp, 1);
+    static const bool light = [] { const char *e = getenv("HELINEAR_C1_LIGHT"); return e ? atoi(e) != 0 : true; }();
+    if (!RR && light) k_c1_out<LOGN><<<(unsigned)nout, Gm::NT, ntt_smem<LOGN>(), st>>>(ct_ntt, masked, M, c->dp);
+    else k_ntt_inv_mask<LOGN, RR><<<(unsigned)nout, Gm::NT, smem, st>>>(ct_ntt, masked, share, M, c->dp, 1);
   } else {
     k_ntt_inv_mask<LOGN, RR><<<(unsigned)(nout * 2), Gm::NT, smem, st>>>(ct_ntt, masked, share, M, c->dp, 0);
   }
