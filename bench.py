@@ -133,7 +133,9 @@ def run_ours(args, rank, world, local_rank):
     cfg = synth.CONFIGS[args.config]
     tiles = _tiles(cfg, args)
     ctx = hl.Context(cfg.N, cfg.L, synth.T_BITS, device=local_rank)
-    if not args.tile and cfg.tiles:     # the bench's tiles are the library planner's choices (hl_plan_tile)
+    if args.plan:                        # every product at the planner's tile (configs without recorded tiles)
+        tiles = [tuple(ctx.plan_tile(mm.Ma, mm.R, mm.Nb)) for mm in cfg.matmuls]
+    elif not args.tile and cfg.tiles:    # the bench's tiles are the library planner's choices (hl_plan_tile)
         assert all(ctx.plan_tile(mm.Ma, mm.R, mm.Nb) == t for mm, t in zip(cfg.matmuls, tiles)), 'planner drift'
     shard = args.mode == "shard"
     # weak: every rank owns one independently seeded block, no data-path collective.
@@ -497,7 +499,8 @@ def run_ours(args, rank, world, local_rank):
         "vs_baseline": None, "dtype": "u64", "data": "synthetic",
         "config": {"workload": f"{cfg.name}: {cfg.note}", "N": cfg.N, "L": cfg.L, "t_bits": synth.T_BITS,
                    "tile": [list(t) for t in tiles],
-                   "tile_choice": "--tile override" if args.tile else "per product, hl_plan_tile (DESIGN.md §5)",
+                   "tile_choice": ("--tile override" if args.tile else "per product, hl_plan_tile (DESIGN.md §5)"
+                                   if args.plan or cfg.tiles else "config default tile"),
                    "batch_order": [cfg.matmuls[i].name for i in order],
                    "matmuls": [[mm.Nb, mm.R, mm.Ma] for mm in cfg.matmuls],
                    "blocks_per_step_per_rank": 1, "compress": True,
@@ -621,6 +624,7 @@ def main():
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--config", default="c2", choices=sorted(synth.CONFIGS))
     ap.add_argument("--tile", type=int, nargs=3, default=None)
+    ap.add_argument("--plan", action="store_true", help="every product at hl_plan_tile's tile")
     ap.add_argument("--cpu-itiles", type=int, default=2)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--sequential", action="store_true", help="one he_matmul_share per product (no 2-stream pipeline)")
