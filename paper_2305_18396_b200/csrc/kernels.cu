@@ -1088,14 +1088,49 @@ __device__ __forceinline__ void inv_rounds_live(double (&a)[16], double *sm, int
   }
 }
 
-template <int LOGN, bool RR>
-__global__ void __launch_bounds__(Geom<LOGN>::NT)
+// compact parking of the live class (q = idx >> log2 r, padded every 16): N/r words per prime
+// instead of a full exchange buffer, so more CTAs fit per SM (and beside a co-resident MAC)
+__device__ __forceinline__ int cpad(int q) { return q + (q >> 4); }
+template <int LOGN, int R>
+__device__ __forceinline__ void c_to_smem(const double (&a)[16], double *cv, int tv, int lr) {
+  constexpr int K = Geom<LOGN>::k(R), G = 16 >> K;
+#pragma unroll
+  for (int g = 0; g < G; g++)
+#pragma unroll
+    for (int u = 0; u < (1 << K); u++) cv[cpad(elem_idx<LOGN, R>(tv, g, u) >> lr)] = a[g * (1 << K) + u];
+}
+template <int LOGN, int R>
+__device__ __forceinline__ void c_from_smem(double (&a)[16], const double *cv, int tv, int lr) {
+  constexpr int K = Geom<LOGN>::k(R), G = 16 >> K;
+#pragma unroll
+  for (int g = 0; g < G; g++)
+#pragma unroll
+    for (int u = 0; u < (1 << K); u++) a[g * (1 << K) + u] = cv[cpad(elem_idx<LOGN, R>(tv, g, u) >> lr)];
+}
+template <int LOGN, int R>
+__device__ __forceinline__ void inv_rounds_live_c(double (&a)[16], double *cv, int tv, int lr, bool act, int bar,
+                                                  int nbar, const double *tw, const PrimeConsts &pc) {
+  if constexpr (R >= 0) {
+    double wv[15];
+    if (act) c_to_smem<LOGN, R + 1>(a, cv, tv, lr);
+    asm volatile("bar.sync %0, %1;" ::"r"(bar), "r"(nbar) : "memory");
+    if (act) c_from_smem<LOGN, R>(a, cv, tv, lr);
+    asm volatile("bar.sync %0, %1;" ::"r"(bar), "r"(nbar) : "memory");
+    if (act) load_round_tw<LOGN, R>(wv, tv, tw);
+    if (act) inv_round<LOGN, R>(a, wv, pc);
+    inv_rounds_live_c<LOGN, R - 1>(a, cv, tv, lr, act, bar, nbar, tw, pc);
+  }
+}
+
+template <int LOGN, bool RR, bool CMP = false>
+__global__ void __launch_bounds__(Geom<LOGN>::NT, (CMP && LOGN == 12) ? 4 : (LOGN == 12 ? 2 : 1))
 k_intt_c0_pruned(const uint64_t *__restrict__ ct_ntt, uint64_t *__restrict__ masked, uint64_t *__restrict__ share,
                  MaskArgs M, DevParams P) {
   using Gm = Geom<LOGN>;
   extern __shared__ double sm[];
   const int L = P.L;
-  uint64_t *sig_sm = reinterpret_cast<uint64_t *>(sm + (size_t)L * Gm::SMEM_WORDS);
+  const int cw = cpad(Gm::N >> M.lr);                  // compact words per prime (CMP)
+  uint64_t *sig_sm = reinterpret_cast<uint64_t *>(sm + (size_t)L * (CMP ? cw : Gm::SMEM_WORDS));
   int64_t *ext_sm = reinterpret_cast<int64_t *>(sig_sm + M.m * M.n);   // row f4: e1 + F at the kept positions
   const int t = threadIdx.x, warp = t >> 5;
   const int64_t o = blockIdx.x;                        // I_loc * nK + K
@@ -1112,7 +1147,18 @@ k_intt_c0_pruned(const uint64_t *__restrict__ ct_ntt, uint64_t *__restrict__ mas
     load_ntt_domain<LOGN>(a, ct_ntt + (ct_poly(M, o, 0) * L + l) * Gm::N, t, pc);
     if constexpr (RR) rr_add_ntt<LOGN>(a, M, o, 0, l, L, t, pc);
     { double wv[15]; load_round_tw<LOGN, Gm::NR - 1>(wv, t, P.twd_inv + (size_t)l * Gm::N); inv_round<LOGN, Gm::NR - 1>(a, wv, pc); }
-    to_smem<LOGN, Gm::NR - 1>(a, sm + (size_t)l * Gm::SMEM_WORDS, t);
+    if constexpr (CMP) {                                // only the live class r-1 mod r is parked
+      constexpr int K1 = Gm::k(Gm::NR - 1), G1 = 16 >> K1;
+#pragma unroll
+      for (int g = 0; g < G1; g++)
+#pragma unroll
+        for (int v = 0; v < (1 << K1); v++) {
+          const int idx = elem_idx<LOGN, Gm::NR - 1>(t, g, v);
+          if ((idx & (M.r - 1)) == M.r - 1) sm[(size_t)l * cw + cpad(idx >> M.lr)] = a[g * (1 << K1) + v];
+        }
+    } else {
+      to_smem<LOGN, Gm::NR - 1>(a, sm + (size_t)l * Gm::SMEM_WORDS, t);
+    }
   }
   __syncthreads();
   // phase B: prime l on warps [l*wpp, (l+1)*wpp)
@@ -1123,15 +1169,17 @@ k_intt_c0_pruned(const uint64_t *__restrict__ ct_ntt, uint64_t *__restrict__ mas
   const int tv = ((p / nlive) << 4) | (M.r * (p % nlive) + M.r - 1);
   const PrimeConsts pc = pick(P, l);
   const double *tw = P.twd_inv + (size_t)l * Gm::N;
-  double *sml = sm + (size_t)l * Gm::SMEM_WORDS;
+  double *sml = sm + (size_t)l * (CMP ? cw : Gm::SMEM_WORDS);
   double a[16];
   if (act) {
     double wv[15];
     load_round_tw<LOGN, Gm::NR - 2>(wv, tv, tw);
-    from_smem<LOGN, Gm::NR - 2>(a, sml, tv);
+    if constexpr (CMP) c_from_smem<LOGN, Gm::NR - 2>(a, sml, tv, M.lr);
+    else from_smem<LOGN, Gm::NR - 2>(a, sml, tv);
     inv_round<LOGN, Gm::NR - 2>(a, wv, pc);
   }
-  inv_rounds_live<LOGN, Gm::NR - 3>(a, sml, tv, act, 1 + l, wpp * 32, tw, pc);
+  if constexpr (CMP) inv_rounds_live_c<LOGN, Gm::NR - 3>(a, sml, tv, M.lr, act, 1 + l, wpp * 32, tw, pc);
+  else inv_rounds_live<LOGN, Gm::NR - 3>(a, sml, tv, act, 1 + l, wpp * 32, tw, pc);
   if (!act) return;
   constexpr int K0 = Gm::k(0), G = 16 >> K0;
 #pragma unroll
@@ -1788,6 +1836,7 @@ void launch_inv_mask_t(const hl_ctx *c, const uint64_t *ct_ntt, uint64_t *masked
   if (!init) {
     set_smem(k_ntt_inv_mask<LOGN, RR>, ntt_smem<LOGN>() + (size_t)Gm::N * 16);
     set_smem(k_intt_c0_pruned<LOGN, RR>, 232448);
+    set_smem(k_intt_c0_pruned<LOGN, RR, true>, 232448);
     set_smem(k_c1_out<LOGN>, ntt_smem<LOGN>());
     init = true;
   }
@@ -1800,7 +1849,14 @@ void launch_inv_mask_t(const hl_ctx *c, const uint64_t *ct_ntt, uint64_t *masked
   const size_t smem = ntt_smem<LOGN>() + (RR ? std::max((size_t)M.m * M.n * 16, (size_t)Gm::N) : (size_t)M.m * M.n * 8);
   KTimer kt(c, HL_K_INTT_MASK, st);
   if (prune) {
-    k_intt_c0_pruned<LOGN, RR><<<(unsigned)nout, Gm::NT, smem_c0, st>>>(ct_ntt, masked, share, M, c->dp);
+    static const bool cmp = [] { const char *e = getenv("HELINEAR_C0_COMPACT"); return e ? atoi(e) != 0 : true; }();
+    if (cmp) {
+      const size_t cwords = (size_t)(Gm::N / M.r) + (size_t)(Gm::N / M.r) / 16;
+      const size_t smem_cmp = cwords * 8 * c->L + (size_t)M.m * M.n * ext;
+      k_intt_c0_pruned<LOGN, RR, true><<<(unsigned)nout, Gm::NT, smem_cmp, st>>>(ct_ntt, masked, share, M, c->dp);
+    } else {
+      k_intt_c0_pruned<LOGN, RR><<<(unsigned)nout, Gm::NT, smem_c0, st>>>(ct_ntt, masked, share, M, c->dp);
+    }
     static const bool light = [] { const char *e = getenv("HELINEAR_C1_LIGHT"); return e ? atoi(e) != 0 : true; }();
     if (!RR && light) k_c1_out<LOGN><<<(unsigned)nout, Gm::NT, ntt_smem<LOGN>(), st>>>(ct_ntt, masked, M, c->dp);
     else k_ntt_inv_mask<LOGN, RR><<<(unsigned)nout, Gm::NT, smem, st>>>(ct_ntt, masked, share, M, c->dp, 1);
