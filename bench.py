@@ -34,7 +34,15 @@ METRIC = "ms per BERT-base encoder block's encrypted matmuls"
 IMAD_WIDE_PER_CLK_SM = 24.4      # measured peak, profiles/r01/microbench_intpipe3.log
 DFMA_PER_CLK_SM = 57.3           # measured peak (same run): the FP64 pipe of the default MAC engine
 FP64_OPS_PER_MAC = 4.125         # 3 DFMA + 1 DADD per modular MAC + 1 DMUL per 8 (k_mac_f64)
+FP64_OPS_PER_BFLY = 10.0         # exact modular butterfly (mm_d 6 + add/sub 2) + reductions (2 amortised)
 UNIT = "ms"
+
+
+def ref_primes(cfg):
+    """The primes of the config (reading C4) from the library's own context -- for input ranges only."""
+    import paper_2305_18396_b200 as hl
+    c = hl.Context(cfg.N, cfg.L, synth.T_BITS, device=-1)
+    return c.primes
 
 
 def _peaks():
@@ -249,6 +257,42 @@ def run_ours(args, rank, world, local_rank):
     elapsed = max_over_ranks(ev0.elapsed_time(ev1))
     ktimes = ctx.timing_read()
     clk = clocks.stop() if clocks else None
+
+    # ---------------- standalone batched NTT microbenchmark: forward + inverse
+    # negacyclic transforms of 4096 polynomials x L primes in place (hl_ntt_roundtrip), CUDA events
+    ntt_info = None
+    if not shard:
+        npoly = 4096
+        xs = hl.to_device(synth.uniform_below(77, (npoly, cfg.L, cfg.N), ref_primes(cfg)), dev)
+        scratch = torch.empty_like(xs)
+        for _ in range(3):
+            ctx.ntt_roundtrip(xs, scratch, stream=stream)
+        torch.cuda.synchronize()
+        ctx.timing_enable(True)
+        ctx.timing_read()
+        n0, n1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        nrep = 10
+        n0.record(stream)
+        for _ in range(nrep):
+            ctx.ntt_roundtrip(xs, scratch, stream=stream)
+        n1.record(stream)
+        torch.cuda.synchronize()
+        kt = ctx.timing_read()
+        ctx.timing_enable(False)
+        transforms = 2 * npoly * cfg.L * nrep
+        logn = cfg.N.bit_length() - 1
+        bfly = transforms * (cfg.N // 2) * logn
+        sec = n0.elapsed_time(n1) * 1e-3
+        peak_bfly = DFMA_PER_CLK_SM * 148 * (_peaks().get("sm_max_mhz") or 1965.0) * 1e6 / FP64_OPS_PER_BFLY
+        ntt_info = {"what": f"forward + inverse negacyclic NTT, {npoly} polynomials x {cfg.L} primes, N={cfg.N}, "
+                            "exact FP64 butterflies (hl_ntt_roundtrip)",
+                    "transforms_per_s": round(transforms / sec, 1), "butterflies_per_s": round(bfly / sec, 1),
+                    "fp64_roofline_frac": round(bfly / sec / peak_bfly, 3),
+                    "roofline_note": f"peak = DFMA {DFMA_PER_CLK_SM}/clk/SM x 148 SMs x max clock / "
+                                     f"{FP64_OPS_PER_BFLY} FP64 ops per butterfly (8 for the exact modular "
+                                     "butterfly + 2 for the lazy reductions every other stage)",
+                    "kernel_ms": {k: round(v[0] / nrep, 4) for k, v in kt.items() if v[1]}}
+        del xs, scratch
 
     # ---------------- row f1: the server's FC share assembly, share += X1.W + b,
     # timed separately (it is not part of the Pi_MatMul metric): device-resident inputs, events
@@ -523,6 +567,8 @@ def run_ours(args, rank, world, local_rank):
                 "checked_equal_to_device_path": e2e_checked},
         "clocks": clk,
     }
+    if ntt_info:
+        line["ntt_microbench"] = ntt_info
     if fc_info:
         line["fc_local_share"] = fc_info
     if att_info:
