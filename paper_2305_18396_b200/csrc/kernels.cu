@@ -2060,6 +2060,12 @@ static int linear_batch_run(const hl_ctx *c, hl_tile tile, int n, const hl_linea
   // block vs interleaving them with the MACs); HELINEAR_BATCH_INTERLEAVE=1 restores the interleaving
   static const bool interleave = getenv("HELINEAR_BATCH_INTERLEAVE") != nullptr;
   const bool split = ready != nullptr || !interleave;
+  // adaptive policy: with many columns per weight byte (nK >= 8, e.g. c3/c4: 8-16x c2's NTT work per
+  // byte) co-resident kernels slow each other more than they overlap -- issue the products one after
+  // the other on the forward / MAC / inverse streams without the cross-product overlap
+  static const int serial_nk = [] { const char *e = getenv("HELINEAR_BATCH_SERIAL_NK"); return e ? atoi(e) : 8; }();
+  bool serial = !ready;
+  for (int i = 0; i < n; i++) serial = serial && E[i].g.nK >= serial_nk;
   cudaStream_t sf = split ? (cudaStream_t)c->fwd_stream : s1;
   auto fwd = [&](int i) {
     if (ready) cudaStreamWaitEvent(sf, ready[i], 0);
@@ -2081,6 +2087,17 @@ static int linear_batch_run(const hl_ctx *c, hl_tile tile, int n, const hl_linea
     std::vector<int> o;
     for (const char *p = order_env; *p;) { o.push_back(atoi(p)); while (*p && *p != ',') p++; if (*p) p++; }
     if ((int)o.size() == n) ord = o;
+  }
+  if (serial) {                                   // the products one after the other on `stream`
+    for (int k = 0; k < n; k++) {
+      const int i = ord[k];
+      fwd_ntt(c, d[i].ct_in, d[i].workspace, E[i].g.nJ * 2 * E[i].g.nK, &E[i].mg, sc);
+      launch_mac(c, (const uint2 *)d[i].wcache, (const uint32_t *)d[i].workspace, d[i].ct_out_ntt, E[i].mg, sc);
+      if (c->N == 4096) launch_inv_mask<12>(c, d[i].ct_out_ntt, d[i].ct_masked, d[i].share, E[i].M, E[i].g.nIs * E[i].g.nK, sc);
+      else launch_inv_mask<13>(c, d[i].ct_out_ntt, d[i].ct_masked, d[i].share, E[i].M, E[i].g.nIs * E[i].g.nK, sc);
+    }
+    for (auto &e : ev) cudaEventDestroy(e);
+    return hl_cuda_check("hl_he_linear_batch: launch");
   }
   cudaEventRecord(e_in, sc);                      // inputs written on `stream` are visible to both streams
   cudaStreamWaitEvent(s0, e_in, 0);
