@@ -381,8 +381,12 @@ enum {
 int hl_timing_enable(hl_ctx *ctx, int on);
 
 /* Wait for the recorded events, ADD the summed durations (ms) and launch counts per kernel
- * class into ms[HL_K_COUNT] and count[HL_K_COUNT], then clear the record. */
+ * class into ms[HL_K_COUNT] and count[HL_K_COUNT], then clear the record.  A timed section may
+ * hold several kernels (e.g. the pruned c0 inverse + the c1 reorder): count[] counts sections. */
 int hl_timing_read(hl_ctx *ctx, double *ms, int64_t *count);
+
+/* Number of kernel launches inside the timed sections since the last call (then reset). */
+int hl_timing_kernels(hl_ctx *ctx, int64_t *n);
 
 #ifdef __cplusplus
 }

@@ -34,7 +34,8 @@ EXPORTS = ("hl_last_error", "hl_ctx_create", "hl_ctx_destroy", "hl_ctx_params", 
            "hl_ntt_roundtrip", "hl_timing_enable", "hl_timing_read", "hl_fc_layout", "hl_fc_encode_weights",
            "hl_fc_local_share", "hl_encode_weights_strided", "hl_encode_weights_scratch", "hl_share_accumulate", "hl_sk_prepare",
            "hl_encrypt_device", "hl_decrypt_share_device", "hl_pk_gen", "hl_pk_prepare", "hl_he_matmul_share_rr",
-           "hl_expand_seeded", "hl_he_linear_batch_host", "hl_packed50_words", "hl_pack50", "hl_unpack50")
+           "hl_expand_seeded", "hl_he_linear_batch_host", "hl_packed50_words", "hl_pack50", "hl_unpack50",
+           "hl_timing_kernels")
 KERNELS = ("ntt_fwd", "mac", "intt_mask", "intt", "mask", "encode", "other", "fc")   # HL_K_* order
 
 
@@ -134,6 +135,7 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
         "hl_timing_read": [vp, vp, vp],
         "hl_expand_seeded": [vp, Tile, i64, i64, u64, vp, vp],
         "hl_pack50": [vp, i64, vp],
+        "hl_timing_kernels": [vp, ctypes.POINTER(i64)],
         "hl_unpack50": [vp, i64, vp],
         "hl_he_linear_batch_host": [vp, Tile, i32, ctypes.POINTER(LinearHostDesc), vp],
     }
@@ -505,6 +507,12 @@ class Context:
     # ---------------------------------------------------------------- timing
     def timing_enable(self, on: bool = True):
         _check(_lib.hl_timing_enable(self._h, int(bool(on))))
+
+    def timing_kernels(self) -> int:
+        """Kernel launches inside the timed sections since the last call (hl_timing_kernels)."""
+        n = ctypes.c_int64()
+        _check(_lib.hl_timing_kernels(self._h, ctypes.byref(n)))
+        return n.value
 
     def timing_read(self) -> dict:
         """{kernel: (total_ms, launches)} since the last read (synchronises the recorded events)."""

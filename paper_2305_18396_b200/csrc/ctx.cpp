@@ -286,6 +286,14 @@ KTimer::~KTimer() {
   if (!ev0 || !ev1) return;
   cudaEventRecord((cudaEvent_t)ev1, (cudaStream_t)stream);
   c->timing->rec.push_back({kid, {ev0, ev1}});
+  c->timing->kernels += nk;
+}
+
+extern "C" int hl_timing_kernels(hl_ctx *c, int64_t *n) {
+  if (!c || !n) return hl_fail(HL_EINVAL, "hl_timing_kernels: NULL argument");
+  *n = c->timing ? c->timing->kernels : 0;
+  if (c->timing) c->timing->kernels = 0;
+  return HL_OK;
 }
 
 extern "C" int hl_timing_enable(hl_ctx *c, int on) {

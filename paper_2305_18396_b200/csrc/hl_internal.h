@@ -46,6 +46,7 @@ struct TimingState {
   bool on = false;
   std::vector<void *> pool;                        // free cudaEvent_t
   std::vector<std::pair<int, std::pair<void *, void *>>> rec;   // (kernel class, (start, stop))
+  int64_t kernels = 0;                             // kernel launches inside the timed sections
 };
 
 struct hl_ctx {
@@ -82,6 +83,7 @@ struct hl_ctx {
 // RAII event pair around one kernel launch when timing is on
 struct KTimer {
   const hl_ctx *c; int kid; void *stream; void *ev0 = nullptr, *ev1 = nullptr;
+  int nk = 1;                                      // kernels launched inside this section
   KTimer(const hl_ctx *c_, int kid_, void *stream_);
   ~KTimer();
 };

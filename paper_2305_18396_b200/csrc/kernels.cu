@@ -1652,6 +1652,7 @@ void launch_fwd_cperm(const hl_ctx *c, const uint64_t *in, uint64_t *out, int64_
   const bool fused = x2 && fuse_c1 && (nK % 2 == 0);   // c1 pairs (K0, K0+1) adjacent in the c1 column range
   // N = 4096: 3 CTAs per SM (80 registers, a few bytes of spill; measured best) or 2 (<= 128)
   static const int minb = [] { const char *e = getenv("HELINEAR_X2_MINB"); return e ? atoi(e) : 3; }();
+  kt.nk = fused ? 1 : 2;
   if constexpr (LOGN == 12) {
     if (fused) {
       const dim3 gx((unsigned)(nJ * ((nK + 1) / 2)), c->L);
@@ -1848,6 +1849,7 @@ void launch_inv_mask_t(const hl_ctx *c, const uint64_t *ct_ntt, uint64_t *masked
   const bool prune = !no_prune && M.r >= 2 && M.r <= 16 && (int)c->L * wpp <= Gm::NT / 32 && smem_c0 <= 232448;
   const size_t smem = ntt_smem<LOGN>() + (RR ? std::max((size_t)M.m * M.n * 16, (size_t)Gm::N) : (size_t)M.m * M.n * 8);
   KTimer kt(c, HL_K_INTT_MASK, st);
+  kt.nk = prune ? 2 : 1;
   if (prune) {
     static const bool cmp = [] { const char *e = getenv("HELINEAR_C0_COMPACT"); return e ? atoi(e) != 0 : true; }();
     if (cmp) {
