@@ -508,62 +508,10 @@ k_ntt_fwd_x(const uint64_t *__restrict__ in, uint64_t *__restrict__ out, DevPara
   }
 }
 
-// (a'') the fused paths' X layout (MacGeom::cperm = 1, c0 columns first): forward NTT of the c0
-//       halves only, two consecutive K of one J per CTA -> adjacent columns, 16-B (slot, J) chunks
-template <int LOGN, int G>
-__global__ void __launch_bounds__(Geom<LOGN>::NT * G)
-k_ntt_fwd_c0(const uint64_t *__restrict__ in, uint64_t *__restrict__ out, DevParams P, MacGeom mg) {
-  using Gm = Geom<LOGN>;
-  extern __shared__ double sm[];
-  const int sub = threadIdx.x / Gm::NT, t = threadIdx.x % Gm::NT, l = blockIdx.y;
-  const int nK = mg.nC / 2, nKh = (nK + G - 1) / G;
-  const int J = (int)(blockIdx.x / (unsigned)nKh), K0 = G * (int)(blockIdx.x % (unsigned)nKh), K = K0 + sub;
-  const bool full = K0 + G <= nK;
-  const PrimeConsts pc = pick(P, l);
-  double a[16];
-  if (K < nK) {
-    const size_t base = (((size_t)J * nK + K) * 2 * P.L + l) * Gm::N;      // c0 of input ciphertext (J, K)
-    constexpr int KK = Gm::k(0), GG = 16 >> KK;
-#pragma unroll
-    for (int g = 0; g < GG; g++)
-#pragma unroll
-      for (int u = 0; u < (1 << KK); u++) a[g * (1 << KK) + u] = u2d(__ldcs(in + base + elem_idx<LOGN, 0>(t, g, u)));
-    fwd_rounds_from<LOGN, 0>(a, sm + sub * Gm::SMEM_WORDS, t, P.twd_fwd + (size_t)l * Gm::N, pc.pd, pc.pinv,
-                             G > 1 ? 1 + sub : -1);
-  }
-  if constexpr (G == 1) {          // no pairing: stores straight from the registers
-    const int cg = K0 / mg.CW, cc = K0 % mg.CW;
-    uint64_t *dst0 = out + ((size_t)cg * mg.LN + (size_t)l * Gm::N) * mg.nJp * mg.CW + (size_t)J * mg.CW + cc;
-#pragma unroll
-    for (int u = 0; u < 16; u++)
-      dst0[(size_t)slot_of<LOGN>(t, u) * mg.nJp * mg.CW] = d2u(canon_d(a[u], pc.pd, pc.pinv));
-    return;
-  }
-  __syncthreads();
-  uint64_t *xs = reinterpret_cast<uint64_t *>(sm);     // [N][G] canonical residues
-  if (K < nK) {
-#pragma unroll
-    for (int u = 0; u < 16; u++) xs[slot_of<LOGN>(t, u) * G + sub] = d2u(canon_d(a[u], pc.pd, pc.pinv));
-  }
-  __syncthreads();
-  const int cg = K0 / mg.CW, cc = K0 % mg.CW;
-  uint64_t *dst0 = out + ((size_t)cg * mg.LN + (size_t)l * Gm::N) * mg.nJp * mg.CW + (size_t)J * mg.CW + cc;
-#pragma unroll 2
-  for (int sl = threadIdx.x; sl < Gm::N; sl += Gm::NT * G) {
-    uint64_t *dst = dst0 + (size_t)sl * mg.nJp * mg.CW;
-    const ulonglong2 *src = reinterpret_cast<const ulonglong2 *>(xs + sl * G);
-    if (full) {                                         // G adjacent columns: 8 G contiguous bytes
-#pragma unroll
-      for (int h = 0; h < G / 2; h++) reinterpret_cast<ulonglong2 *>(dst)[h] = src[h];
-    } else {
-      for (int g = 0; g < nK - K0; g++) dst[g] = xs[sl * G + g];
-    }
-  }
-}
-
-// (a''') as k_ntt_fwd_c0<2> with both transforms in the same threads (fwd_rounds_from2): the
-//        pair's values for a slot sit in one thread, so the 16-B (slot, J) chunks are stored
-//        straight from registers (no staging, no output barrier)
+// (a'') the fused paths' X layout (MacGeom::cperm = 1, c0 columns first): the forward NTTs of the
+//       c0 halves of two adjacent columns (K0, K0+1) in the SAME threads (fwd_rounds_from2): the
+//       pair's values for a slot sit in one thread, so the 16-B (slot, J) chunks are stored
+//       straight from registers (no staging, no output barrier)
 template <int LOGN, bool C1, int MB = 1>
 __global__ void __launch_bounds__(Geom<LOGN>::NT, MB)
 k_ntt_fwd_c0x2(const uint64_t *__restrict__ in, uint64_t *__restrict__ out, DevParams P, MacGeom mg) {
@@ -1633,12 +1581,11 @@ void launch_fwd_cperm(const hl_ctx *c, const uint64_t *in, uint64_t *out, int64_
                       cudaStream_t st) {
   const int nK = mg.nC / 2;
   const int64_t nJ = npoly / mg.nC;
-  constexpr size_t smem2 = ntt_smem<LOGN>() * 2, smem1 = ntt_smem<LOGN>();
+  constexpr size_t smem2 = ntt_smem<LOGN>() * 2;
+  constexpr int MB2 = LOGN == 12 ? 2 : 1;             // explicit: minBlocks 1 lets the kernel grow to 1 CTA/SM
   static bool init = false;
   if (!init) {
-    set_smem(k_ntt_fwd_c0<LOGN, 2>, smem2); set_smem(k_ntt_fwd_c0<LOGN, 1>, smem2 / 2);
-    if constexpr (LOGN == 12) set_smem(k_ntt_fwd_c0<LOGN, 4>, smem2 * 2);
-    set_smem(k_ntt_fwd_c0x2<LOGN, false>, smem2); set_smem(k_ntt_fwd_c0x2<LOGN, true>, smem2);
+    set_smem(k_ntt_fwd_c0x2<LOGN, false, MB2>, smem2); set_smem(k_ntt_fwd_c0x2<LOGN, true>, smem2);
     if constexpr (LOGN == 12) {
       set_smem(k_ntt_fwd_c0x2<LOGN, true, 2>, smem2); set_smem(k_ntt_fwd_c0x2<LOGN, true, 3>, smem2);
     }
@@ -1647,9 +1594,8 @@ void launch_fwd_cperm(const hl_ctx *c, const uint64_t *in, uint64_t *out, int64_
     init = true;
   }
   KTimer kt(c, HL_K_NTT_FWD, st);
-  static const bool x2 = [] { const char *e = getenv("HELINEAR_NTT_X2"); return e ? atoi(e) != 0 : true; }();
   static const bool fuse_c1 = [] { const char *e = getenv("HELINEAR_FUSE_C1"); return e ? atoi(e) != 0 : true; }();
-  const bool fused = x2 && fuse_c1 && (nK % 2 == 0);   // c1 pairs (K0, K0+1) adjacent in the c1 column range
+  const bool fused = fuse_c1 && (nK % 2 == 0);   // c1 pairs (K0, K0+1) adjacent in the c1 column range
   // N = 4096: 3 CTAs per SM (80 registers, a few bytes of spill; measured best) or 2 (<= 128)
   static const int minb = [] { const char *e = getenv("HELINEAR_X2_MINB"); return e ? atoi(e) : 3; }();
   kt.nk = fused ? 1 : 2;
@@ -1665,14 +1611,8 @@ void launch_fwd_cperm(const hl_ctx *c, const uint64_t *in, uint64_t *out, int64_
     k_ntt_fwd_c0x2<LOGN, true><<<dim3((unsigned)(nJ * ((nK + 1) / 2)), c->L), Geom<LOGN>::NT, smem2, st>>>(in, out, c->dp, mg);
     return;
   }
-  if (x2)   // default; four transforms per thread (254 registers) measured slower
-    k_ntt_fwd_c0x2<LOGN, false><<<dim3((unsigned)(nJ * ((nK + 1) / 2)), c->L), Geom<LOGN>::NT, smem2, st>>>(in, out, c->dp, mg);
-  else if (LOGN == 12 && ntt_group() >= 4 && nK % 4 == 0 && mg.CW % 4 == 0)
-    k_ntt_fwd_c0<12, 4><<<dim3((unsigned)(nJ * (nK / 4)), c->L), Geom<12>::NT * 4, smem2 * 2, st>>>(in, out, c->dp, mg);
-  else if (ntt_group() >= 2)
-    k_ntt_fwd_c0<LOGN, 2><<<dim3((unsigned)(nJ * ((nK + 1) / 2)), c->L), Geom<LOGN>::NT * 2, smem2, st>>>(in, out, c->dp, mg);
-  else
-    k_ntt_fwd_c0<LOGN, 1><<<dim3((unsigned)(nJ * nK), c->L), Geom<LOGN>::NT, smem2 / 2, st>>>(in, out, c->dp, mg);
+  // odd nK: the c0 pairs without their c1, then the c1 reordering
+  k_ntt_fwd_c0x2<LOGN, false, MB2><<<dim3((unsigned)(nJ * ((nK + 1) / 2)), c->L), Geom<LOGN>::NT, smem2, st>>>(in, out, c->dp, mg);
   // G1 = 4 needs 4 | nK and 4 | CW (the 4 columns in one group); 4 x 64 KB does not fit at N = 8192
   static const int g1max = [] { const char *e = getenv("HELINEAR_C1_G"); return e ? atoi(e) : 4; }();
   const int G1 = (g1max >= 4 && nK % 4 == 0 && mg.CW % 4 == 0 && LOGN == 12) ? 4 : (g1max >= 2 && nK % 2 == 0 ? 2 : 1);
@@ -1790,8 +1730,6 @@ void launch_mac_tc(const hl_ctx *c, const void *W, const void *X, uint64_t *out,
   A.sched = (int *)((char *)X + tc_sched_offset(g));
   static const int ko = [] { const char *e = getenv("HELINEAR_MAC_KO"); return e ? atoi(e) : 0; }();
   A.ko = ko;
-  static const int pf = [] { const char *e = getenv("HELINEAR_MAC_PF"); return e ? atoi(e) : 0; }();
-  A.pf = pf;
   for (int64_t j0 = 0; j0 < g.nJp; j0 += kMacJChunk) {     // S_d < 7 * 4096 * 255^2 < 2^31 per launch
     A.jc0 = (int)(j0 / 32);
     A.njc = (int)((std::min<int64_t>(g.nJp, j0 + kMacJChunk) - j0) / 32);

@@ -79,7 +79,6 @@ struct MacTcArgs {
   unsigned long long *prof;   // diagnostics (HELINEAR_MAC_PROF): per-CTA cycles spent waiting, by role
   int *sched;                 // work counter (zeroed before the launch; in the caller's workspace)
   int ko;                     // diagnostics (HELINEAR_MAC_KO bitmask): 1 skip MMAs, 2 skip conversion, 4 skip epilogue math
-  int pf;                     // L2 prefetch distance in weight chunks (0: off)
   int lazy_out;               // 1: outputs only < 2^52 (= residue + k p, k < 4): fine for the inverse NTT's input
 };
 
@@ -106,11 +105,6 @@ __device__ __forceinline__ void umma_commit(uint64_t *bar) {
 __device__ __forceinline__ void bulk_g2s_hint(void *dst, const void *src, uint32_t bytes, uint64_t *bar, uint64_t pol) {
   asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;"
                ::"r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(pol) : "memory");
-}
-// L2 prefetch of a weight chunk the producer will load a few stages later (hides HBM latency
-// behind the ring without spending shared memory)
-__device__ __forceinline__ void prefetch_l2(const void *src, uint32_t bytes) {
-  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");
 }
 __device__ __forceinline__ bool elect_one() {
   uint32_t pred;
@@ -265,17 +259,10 @@ k_mac_tc(MacTcArgs A, DevParams P) {
         const int rows = min(g.RT, g.nIp - g.RT * it.t);
         const uint32_t abytes = 224u * rows;
         const uint8_t *wt = A.W + (size_t)it.t * g.RT * g.LN * g.nJp * 7;
-        const int steps = T::SPI * A.njc;
-        if (A.pf > 0)                                   // the item's first PF chunks
-          for (int q = 0; q < min(A.pf, steps); q++)
-            prefetch_l2(wt + ((size_t)(it.sq * T::SPI + q / A.njc) * g.nJc + A.jc0 + q % A.njc) * abytes, abytes);
         for (int si = 0; si < T::SPI; si++) {
           const int s = it.sq * T::SPI + si;
           for (int kk = 0; kk < A.njc; kk++) {
             const int jc = A.jc0 + kk;
-            const int fut = si * A.njc + kk + A.pf;      // chunk pf steps ahead within the item
-            if (A.pf > 0 && fut < steps)
-              prefetch_l2(wt + ((size_t)(it.sq * T::SPI + fut / A.njc) * g.nJc + A.jc0 + fut % A.njc) * abytes, abytes);
             mbar_wait_p(&empty[st], ph, A.prof ? &pw[0] : nullptr);
             unsigned char *dst = smem + st * SB;
             mbar_expect_tx(&full[st], abytes + T::RAW_BYTES);
