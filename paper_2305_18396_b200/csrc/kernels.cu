@@ -737,41 +737,49 @@ k_ntt_inv(const uint64_t *in, uint64_t *out, DevParams P, int ct_mode) {
 
 // Second pass of the two-pass weight encoding (hl_encode_weights_scratch): u64 NTT-domain
 // residues scratch [nIs][nJ][LN] -> the 7 byte planes of the tensor-core MAC's A operand
-// ([I tile][slot][32-J step][plane][K half][row][16 B]).  One thread per (I tile, 32-J step, row,
-// slot), lanes over consecutive slots (coalesced reads); every 16-B chunk of the cache is written
-// (padded rows and J are zero), so no memset is needed.
-__global__ void k_wplanes(const uint64_t *__restrict__ scratch, uint8_t *__restrict__ wcache, MacGeom g, int64_t total) {
-  const int64_t id = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (id >= total) return;
-  const int s = (int)(id % g.LN);
-  int64_t r = id / g.LN;
-  const int row = (int)(r % g.RT); r /= g.RT;
-  const int jc = (int)(r % g.nJc);
-  const int tt = (int)(r / g.nJc);
+// ([I tile][slot][32-J step][plane][K half][row][16 B]).  A tiled transpose: one CTA per
+// (I tile, 32-J step, block of 16 rows, block of 16 slots) stages [slot][row][J] in shared memory
+// (reads: 128-B runs of consecutive slots), then writes each slot's 16 rows x 14 pieces of 16 B
+// (256-B runs per (plane, K half)); padded rows and J are zero, so no memset is needed.
+constexpr int kWpS = 16, kWpR = 16;
+__global__ void __launch_bounds__(256) k_wplanes(const uint64_t *__restrict__ scratch, uint8_t *__restrict__ wcache,
+                                                 MacGeom g) {
+  extern __shared__ uint64_t vsd[];                                // [kWpS][kWpR][33] (+1: bank spread)
+  auto vs = [&](int si, int r, int j) -> uint64_t & { return vsd[(si * kWpR + r) * 33 + j]; };
+  const int nsb = g.LN / kWpS, nrb = (g.RT + kWpR - 1) / kWpR;
+  int b = blockIdx.x;
+  const int sb = b % nsb; b /= nsb;
+  const int rb = b % nrb; b /= nrb;
+  const int jc = b % g.nJc, tt = b / g.nJc;
   const int rows = min(g.RT, g.nIp - g.RT * tt);
-  if (row >= rows) return;
-  const int Iloc = tt * g.RT + row;
-  uint64_t v[32];
-#pragma unroll
-  for (int j = 0; j < 32; j++) {
-    const int J = jc * 32 + j;
-    v[j] = (Iloc < g.nIs && J < g.nJ) ? __ldcs(scratch + ((size_t)Iloc * g.nJ + J) * g.LN + s) : 0;
+  if (rb * kWpR >= rows) return;
+  const int s0 = sb * kWpS;
+  for (int e = threadIdx.x; e < kWpR * 32 * kWpS; e += blockDim.x) {
+    const int si = e % kWpS, j = (e / kWpS) % 32, r = e / kWpS / 32;
+    const int row = rb * kWpR + r, Iloc = tt * g.RT + row, J = jc * 32 + j;
+    vs(si, r, j) = (row < rows && Iloc < g.nIs && J < g.nJ) ? __ldcs(scratch + ((size_t)Iloc * g.nJ + J) * g.LN + s0 + si) : 0;
   }
-  uint8_t *wb = wcache + (size_t)tt * g.RT * g.LN * g.nJp * 7 + ((size_t)s * g.nJc + jc) * 224 * rows + row * 16;
+  __syncthreads();
+  const int rr = min(kWpR, rows - rb * kWpR);
+  for (int e = threadIdx.x; e < kWpS * 14 * rr; e += blockDim.x) {
+    const int r = e % rr, ah = (e / rr) % 14, si = e / rr / 14;
+    const int a = ah >> 1, h = ah & 1;
+    const uint32_t bb = a & 3, sel = bb | ((bb + 4) << 4);
+    uint32_t w[4];
 #pragma unroll
-  for (int a = 0; a < 7; a++)
+    for (int q = 0; q < 4; q++) {
+      uint32_t x[4];
 #pragma unroll
-    for (int h = 0; h < 2; h++) {
-      uint32_t w[4];
-#pragma unroll
-      for (int q = 0; q < 4; q++) {
-        uint32_t x = 0;
-#pragma unroll
-        for (int b = 0; b < 4; b++) x |= (uint32_t)((v[h * 16 + q * 4 + b] >> (8 * a)) & 0xff) << (8 * b);
-        w[q] = x;
+      for (int t = 0; t < 4; t++) {
+        const uint64_t v = vs(si, r, h * 16 + 4 * q + t);
+        x[t] = a < 4 ? (uint32_t)v : (uint32_t)(v >> 32);
       }
-      *reinterpret_cast<uint4 *>(wb + (size_t)a * 32 * rows + h * rows * 16) = make_uint4(w[0], w[1], w[2], w[3]);
+      w[q] = __byte_perm(__byte_perm(x[0], x[1], sel), __byte_perm(x[2], x[3], sel), 0x5410);
     }
+    uint8_t *chunk = wcache + (size_t)tt * g.RT * g.LN * g.nJp * 7 + ((size_t)(s0 + si) * g.nJc + jc) * 224 * rows;
+    *reinterpret_cast<uint4 *>(chunk + (size_t)a * 32 * rows + h * rows * 16 + (rb * kWpR + r) * 16) =
+        make_uint4(w[0], w[1], w[2], w[3]);
+  }
 }
 
 // ---------------------------------------------------------------------------------------
@@ -1876,8 +1884,11 @@ static int encode_weights_impl(const hl_ctx *c, hl_tile tile, const uint64_t *W,
     k_encode_weights<13><<<grid, Geom<13>::NT, ntt_smem<13>(), st>>>(A, (uint2 *)wcache, c->dp, c->d_flags, scratch);
   }
   if (scratch) {
-    const int64_t total = (int64_t)mg.nIt * mg.nJc * mg.RT * mg.LN;
-    k_wplanes<<<(unsigned)((total + 255) / 256), 256, 0, st>>>(scratch, (uint8_t *)wcache, mg, total);
+    const int64_t nb = (int64_t)mg.nIt * mg.nJc * ((mg.RT + kWpR - 1) / kWpR) * (mg.LN / kWpS);
+    constexpr size_t wsm = (size_t)kWpS * kWpR * 33 * 8;
+    static bool winit = false;
+    if (!winit) { set_smem(k_wplanes, wsm); winit = true; }
+    k_wplanes<<<(unsigned)nb, 256, wsm, st>>>(scratch, (uint8_t *)wcache, mg);
   }
   }
   if ((rc = hl_cuda_check("hl_encode_weights: launch"))) return rc;
