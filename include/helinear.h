@@ -121,11 +121,11 @@ int hl_ctx_params(const hl_ctx *ctx, uint64_t *primes_out, uint64_t *delta_mod_o
  * decrypts with the tile the server announces).  Among the power-of-two tiles with m*r*n <= N,
  * m <= Ma, r <= R, n <= Nb (each rounded up to a power of two) it returns the one minimising a
  * cost model of the GPU path, calibrated on B200:
- *   T = Wbytes / (6.2 TB/s * e_mac) + 0.14 us * nJ*nK + 0.10 us * (r <= 16 ? 1 : 1.5) * nI*nK
+ *   T = Wbytes / (6.2 TB/s * e_mac) + 0.14 us * nJ*nK + 0.10 us * nI*nK
  * Wbytes = the padded weight cache (layout.wcache_bytes), nJ*nK forward and nI*nK inverse
- * transforms (ciphertexts; the c0 inverse is pruned for r <= 16), e_mac = (nC <= 4 ? 1 : nC <= 8 ? 0.85 : 0.5) * min(1, nI/96), nC = 2 nK
+ * transforms (ciphertexts; the c0 inverse is pruned), e_mac = (nC <= 4 ? 1 : nC <= 8 ? 0.85 : 0.5) * min(1, nI/96), nC = 2 nK
  * the MAC's columns.  Ties keep the first candidate (m, then r, then n descending).
- * c2 (BERT-base): QKV, FF1 -> (16, 8, 32); O -> (8, 8, 64); FF2 -> (8, 16, 32). */
+ * c2 (BERT-base): QKV, FF1 -> (16, 8, 32); O -> (8, 8, 64); FF2 -> (4, 32, 32). */
 int hl_plan_tile(const hl_ctx *ctx, int64_t Ma, int64_t R, int64_t Nb, hl_tile *out);
 
 /* Sizes of every buffer of one matmul (Ma x R weights, Nb tokens) for I-tile shard [i_begin, i_end). */

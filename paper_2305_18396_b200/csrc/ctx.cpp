@@ -419,9 +419,9 @@ extern "C" int hl_plan_tile(const hl_ctx *c, int64_t Ma, int64_t R, int64_t Nb, 
       if (hl_layout_query(c, t, Ma, R, Nb, 0, -1, &lay) != HL_OK) continue;
       const double nC = 2.0 * lay.nK;
       const double e_mac = (nC <= 4 ? 1.0 : nC <= 8 ? 0.85 : 0.5) * std::min(1.0, (double)lay.nI / 96.0);
-      // the c0 inverse is pruned to the kept residue class only for r <= 16 (k_intt_c0_pruned)
+      // the c0 inverse is pruned (to the class 15 mod 16 for r > 16, k_intt_c0_pruned)
       const double cost = (double)lay.wcache_bytes / (6.2e12 * e_mac) + 0.14e-6 * (double)(lay.nJ * lay.nK) +
-                          0.10e-6 * (t.r <= 16 ? 1.0 : 1.5) * (double)(lay.nI * lay.nK);
+                          0.10e-6 * (double)(lay.nI * lay.nK);
       if (!found || cost < best) { best = cost; *out = t; found = true; }
     }
   if (!found) return hl_fail(HL_EDIM, "hl_plan_tile: no tile fits the problem");

@@ -1085,7 +1085,11 @@ k_intt_c0_pruned(const uint64_t *__restrict__ ct_ntt, uint64_t *__restrict__ mas
   using Gm = Geom<LOGN>;
   extern __shared__ double sm[];
   const int L = P.L;
-  const int cw = cpad(Gm::N >> M.lr);                  // compact words per prime (CMP)
+  // the live class: r-1 mod re with re = min(r, 16) -- every stage after the first round pairs
+  // indices >= 16 apart, so for r = 32 the kept class r-1 mod 32 needs its distance-16 partners
+  // (class 15 mod 32) through the next stage: the class 15 mod 16 covers both
+  const int re = M.r < 16 ? M.r : 16, lre = M.lr < 4 ? M.lr : 4;
+  const int cw = cpad(Gm::N >> lre);                   // compact words per prime (CMP)
   uint64_t *sig_sm = reinterpret_cast<uint64_t *>(sm + (size_t)L * (CMP ? cw : Gm::SMEM_WORDS));
   int64_t *ext_sm = reinterpret_cast<int64_t *>(sig_sm + M.m * M.n);   // row f4: e1 + F at the kept positions
   const int t = threadIdx.x, warp = t >> 5;
@@ -1110,7 +1114,7 @@ k_intt_c0_pruned(const uint64_t *__restrict__ ct_ntt, uint64_t *__restrict__ mas
 #pragma unroll
         for (int v = 0; v < (1 << K1); v++) {
           const int idx = elem_idx<LOGN, Gm::NR - 1>(t, g, v);
-          if ((idx & (M.r - 1)) == M.r - 1) sm[(size_t)l * cw + cpad(idx >> M.lr)] = a[g * (1 << K1) + v];
+          if ((idx & (re - 1)) == re - 1) sm[(size_t)l * cw + cpad(idx >> lre)] = a[g * (1 << K1) + v];
         }
     } else {
       to_smem<LOGN, Gm::NR - 1>(a, sm + (size_t)l * Gm::SMEM_WORDS, t);
@@ -1118,11 +1122,11 @@ k_intt_c0_pruned(const uint64_t *__restrict__ ct_ntt, uint64_t *__restrict__ mas
   }
   __syncthreads();
   // phase B: prime l on warps [l*wpp, (l+1)*wpp)
-  const int nlive = 16 / M.r, nact = Gm::NT / M.r, wpp = (nact + 31) / 32;
+  const int nlive = 16 / re, nact = Gm::NT / re, wpp = (nact + 31) / 32;
   if (warp >= L * wpp) return;
   const int l = warp / wpp, p = (warp % wpp) * 32 + (t & 31);
   const bool act = p < nact;
-  const int tv = ((p / nlive) << 4) | (M.r * (p % nlive) + M.r - 1);
+  const int tv = ((p / nlive) << 4) | (re * (p % nlive) + re - 1);
   const PrimeConsts pc = pick(P, l);
   const double *tw = P.twd_inv + (size_t)l * Gm::N;
   double *sml = sm + (size_t)l * (CMP ? cw : Gm::SMEM_WORDS);
@@ -1130,11 +1134,11 @@ k_intt_c0_pruned(const uint64_t *__restrict__ ct_ntt, uint64_t *__restrict__ mas
   if (act) {
     double wv[15];
     load_round_tw<LOGN, Gm::NR - 2>(wv, tv, tw);
-    if constexpr (CMP) c_from_smem<LOGN, Gm::NR - 2>(a, sml, tv, M.lr);
+    if constexpr (CMP) c_from_smem<LOGN, Gm::NR - 2>(a, sml, tv, lre);
     else from_smem<LOGN, Gm::NR - 2>(a, sml, tv);
     inv_round<LOGN, Gm::NR - 2>(a, wv, pc);
   }
-  if constexpr (CMP) inv_rounds_live_c<LOGN, Gm::NR - 3>(a, sml, tv, M.lr, act, 1 + l, wpp * 32, tw, pc);
+  if constexpr (CMP) inv_rounds_live_c<LOGN, Gm::NR - 3>(a, sml, tv, lre, act, 1 + l, wpp * 32, tw, pc);
   else inv_rounds_live<LOGN, Gm::NR - 3>(a, sml, tv, act, 1 + l, wpp * 32, tw, pc);
   if (!act) return;
   constexpr int K0 = Gm::k(0), G = 16 >> K0;
@@ -1143,7 +1147,7 @@ k_intt_c0_pruned(const uint64_t *__restrict__ ct_ntt, uint64_t *__restrict__ mas
 #pragma unroll
     for (int u = 0; u < (1 << K0); u++) {
       const int idx = elem_idx<LOGN, 0>(tv, g, u);
-      if (idx < mr * M.n) {                            // idx = r-1 mod r by construction
+      if (idx < mr * M.n && (idx & (M.r - 1)) == M.r - 1) {   // r-1 mod re by construction; kept: r-1 mod r
         uint64_t x = d2u(canon_d(a[g * (1 << K0) + u], pc.pd, pc.pinv));
         const int kk = idx >> M.lr;
         if constexpr (RR) { x += smod(ext_sm[kk], pc); x = x >= pc.p ? x - pc.p : x; }
@@ -1789,17 +1793,18 @@ void launch_inv_mask_t(const hl_ctx *c, const uint64_t *ct_ntt, uint64_t *masked
   }
   // the pruned c0 transform needs r in {2..16} and one warp group per prime within the CTA
   static const bool no_prune = getenv("HELINEAR_NO_PRUNE") != nullptr;
-  const int wpp = (Gm::NT / std::max(M.r, 1) + 31) / 32;
+  const int re = std::min(M.r, 16);                   // the pruned kernel's live class (see there)
+  const int wpp = (Gm::NT / std::max(re, 1) + 31) / 32;
   const size_t ext = RR ? 16 : 8;                      // sigma (+ row f4: e1 + F) per kept position
   const size_t smem_c0 = ntt_smem<LOGN>() * c->L + (size_t)M.m * M.n * ext;
-  const bool prune = !no_prune && M.r >= 2 && M.r <= 16 && (int)c->L * wpp <= Gm::NT / 32 && smem_c0 <= 232448;
+  const bool prune = !no_prune && M.r >= 2 && (int)c->L * wpp <= Gm::NT / 32 && smem_c0 <= 232448;
   const size_t smem = ntt_smem<LOGN>() + (RR ? std::max((size_t)M.m * M.n * 16, (size_t)Gm::N) : (size_t)M.m * M.n * 8);
   KTimer kt(c, HL_K_INTT_MASK, st);
   kt.nk = prune ? 2 : 1;
   if (prune) {
     static const bool cmp = [] { const char *e = getenv("HELINEAR_C0_COMPACT"); return e ? atoi(e) != 0 : true; }();
     if (cmp) {
-      const size_t cwords = (size_t)(Gm::N / M.r) + (size_t)(Gm::N / M.r) / 16;
+      const size_t cwords = (size_t)(Gm::N / re) + (size_t)(Gm::N / re) / 16;
       const size_t smem_cmp = cwords * 8 * c->L + (size_t)M.m * M.n * ext;
       k_intt_c0_pruned<LOGN, RR, true><<<(unsigned)nout, Gm::NT, smem_cmp, st>>>(ct_ntt, masked, share, M, c->dp);
     } else {
