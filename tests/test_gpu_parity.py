@@ -358,8 +358,8 @@ def test_linear_batch_host_seeded_c1_vs_oracle(hl, ctx4096, packed):
 
 @pytest.mark.parametrize("mi,tile", [
     (3, (16, 8, 32)),     # FF2 (R = 3072, the longest J reduction) at the default tile
-    (3, (8, 16, 32)),     # FF2 at the planner's tile (bench): r = 16, nI = 96, nJ = 192
-    (3, (4, 32, 32)),     # FF2, r = 32: unpruned c0 inverse, nI = 192
+    (3, (8, 16, 32)),     # FF2, r = 16, nI = 96, nJ = 192
+    (3, (4, 32, 32)),     # FF2 at the planner's tile (bench): r = 32, c0 inverse pruned to 15 mod 16, nI = 192
     (1, (8, 8, 64)),      # O at the planner's tile (bench): nK = 2, 4 MAC columns (CW = 4)
 ])
 def test_bert_base_full_size_sampled(hl, ctx4096, mi, tile):
