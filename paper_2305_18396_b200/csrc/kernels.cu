@@ -707,6 +707,18 @@ __device__ __forceinline__ void load_ntt_domain(double (&a)[16], const uint64_t 
 #pragma unroll
   for (int u = 0; u < 16; u++) a[u] = red_d(u2d(__ldcs(src + slot_of<LOGN>(t, u))), pc.pd, pc.pinv);
 }
+// Quad order of the MAC output (MacTcArgs::qperm): position 4 q + i of a row holds slot
+// u NT + t' + {0, 2, 1, 3}[i] NT/4 (q = u NT/4 + t'), so that the 4 slots of a MAC work item are 4
+// consecutive natural evaluation points (k_mac_tc's direct c1 store).  Slot u NT + t is therefore
+// read from u NT + 4 (t mod NT/4) + brev2(t / (NT/4)); a warp's 32 loads touch 32 sectors that the
+// CTA's other three quarter-warps complete (L1-cached loads).
+template <int LOGN>
+__device__ __forceinline__ void load_ntt_domain_q(double (&a)[16], const uint64_t *src, int t, const PrimeConsts &pc) {
+  constexpr int NT = Geom<LOGN>::NT, Q = NT / 4;
+  const int h = t / Q, off = 4 * (t % Q) + ((h & 1) << 1 | (h >> 1));
+#pragma unroll
+  for (int u = 0; u < 16; u++) a[u] = red_d(u2d(__ldg(src + u * NT + off)), pc.pd, pc.pinv);
+}
 
 template <int LOGN>
 __global__ void __launch_bounds__(Geom<LOGN>::NT)
@@ -800,6 +812,7 @@ struct MaskArgs {
   const uint64_t *cdt;      // device CDT table
   int flood_bits;
   int nC, cperm;            // MAC output columns and their order (MacGeom::cperm)
+  int c1_done;              // the MAC already wrote the c1 halves of the response (MacTcArgs::c1_out)
 };
 
 // index of the NTT-domain polynomial (component c of output ciphertext o = I_loc nK + K) in the
@@ -1104,7 +1117,8 @@ k_intt_c0_pruned(const uint64_t *__restrict__ ct_ntt, uint64_t *__restrict__ mas
   for (int l = 0; l < L; l++) {
     const PrimeConsts pc = pick(P, l);
     double a[16];
-    load_ntt_domain<LOGN>(a, ct_ntt + (ct_poly(M, o, 0) * L + l) * Gm::N, t, pc);
+    if (M.c1_done) load_ntt_domain_q<LOGN>(a, ct_ntt + (ct_poly(M, o, 0) * L + l) * Gm::N, t, pc);
+    else load_ntt_domain<LOGN>(a, ct_ntt + (ct_poly(M, o, 0) * L + l) * Gm::N, t, pc);
     if constexpr (RR) rr_add_ntt<LOGN>(a, M, o, 0, l, L, t, pc);
     { double wv[15]; load_round_tw<LOGN, Gm::NR - 1>(wv, t, P.twd_inv + (size_t)l * Gm::N); inv_round<LOGN, Gm::NR - 1>(a, wv, pc); }
     if constexpr (CMP) {                                // only the live class r-1 mod r is parked
@@ -1736,9 +1750,14 @@ void launch_mac_tc_t(const hl_ctx *c, MacTcArgs A, int smem_budget, int grid, cu
 inline size_t tc_sched_offset(const MacGeom &g) { return (size_t)g.nJp * g.nC * g.LN * 8; }
 
 void launch_mac_tc(const hl_ctx *c, const void *W, const void *X, uint64_t *out, const MacGeom &g, int smem_budget,
-                   int grid, cudaStream_t st) {
+                   int grid, cudaStream_t st, const MaskArgs *c1m = nullptr, uint64_t *c1_masked = nullptr) {
   MacTcArgs A;
   A.W = (const uint8_t *)W; A.X = (const uint64_t *)X; A.out = out; A.g = g; A.N = (int)c->N;
+  A.c1_out = c1m ? c1_masked : nullptr;
+  A.c1_nK = c1m ? (int)c1m->nK : 0;
+  A.c1_mn = c1m ? c1m->m * c1m->n : 0;
+  A.c1_lognt = (c->N == 4096 ? 12 : 13) - 4;
+  A.qperm = A.c1_out != nullptr;
   A.sched = (int *)((char *)X + tc_sched_offset(g));
   static const int ko = [] { const char *e = getenv("HELINEAR_MAC_KO"); return e ? atoi(e) : 0; }();
   A.ko = ko;
@@ -1761,8 +1780,11 @@ constexpr int kMacSmemAlone = 232448;        // the MAC alone on the SM: the dee
 constexpr int kMacSmemShared = 155 * 1024;   // leaves room for one NTT CTA (~70 KB) beside the MAC (sweep: tools/gpu/ring_sweep*.sh)
 
 void launch_mac(const hl_ctx *c, const uint2 *W, const uint32_t *X, uint64_t *out, const MacGeom &g, cudaStream_t st,
-                int smem_budget = kMacSmemAlone, int grid = 0) {
-  if (g.engine == 2) { launch_mac_tc(c, W, X, out, g, smem_budget, grid > 0 ? grid : c->num_sms, st); return; }
+                int smem_budget = kMacSmemAlone, int grid = 0, const MaskArgs *c1m = nullptr, uint64_t *c1_masked = nullptr) {
+  if (g.engine == 2) {
+    launch_mac_tc(c, W, X, out, g, smem_budget, grid > 0 ? grid : c->num_sms, st, c1m, c1_masked);
+    return;
+  }
   MacArgs A;
   A.W = W; A.X = X; A.out = out; A.g = g; A.N = (int)c->N;
   for (int64_t j0 = 0; j0 < g.nJ; j0 += kMacJChunk) {
@@ -1779,6 +1801,34 @@ void launch_mac(const hl_ctx *c, const uint2 *W, const uint32_t *X, uint64_t *ou
   }
 }
 
+// the pruned c0 transform needs r >= 2 and one warp group per prime within the CTA
+template <int LOGN, bool RR>
+bool inv_prunes(const hl_ctx *c, const MaskArgs &M) {
+  using Gm = Geom<LOGN>;
+  static const bool no_prune = getenv("HELINEAR_NO_PRUNE") != nullptr;
+  const int re = std::min(M.r, 16);                   // the pruned kernel's live class (see there)
+  const int wpp = (Gm::NT / std::max(re, 1) + 31) / 32;
+  const size_t ext = RR ? 16 : 8;                      // sigma (+ row f4: e1 + F) per kept position
+  const size_t smem_c0 = ntt_smem<LOGN>() * c->L + (size_t)M.m * M.n * ext;
+  return !no_prune && M.r >= 2 && (int)c->L * wpp <= Gm::NT / 32 && smem_c0 <= 232448;
+}
+static bool c1_light() {
+  static const bool light = [] { const char *e = getenv("HELINEAR_C1_LIGHT"); return e ? atoi(e) != 0 : true; }();
+  return light;
+}
+// May the MAC write the c1 halves of the response itself (MacTcArgs::c1_out)?  Only where the
+// inverse would otherwise just reorder them (k_c1_out): pruned c0 inverse, no re-randomisation,
+// tensor-core MAC in one launch with c0 columns first.  HELINEAR_C1_DIRECT=0 turns it off.
+template <int LOGN>
+bool c1_direct_ok(const hl_ctx *c, const MacGeom &g, const MaskArgs &M) {
+  static const bool on = [] { const char *e = getenv("HELINEAR_C1_DIRECT"); return e ? atoi(e) != 0 : true; }();
+  return on && g.engine == 2 && g.cperm && g.nJp <= kMacJChunk && !M.pk_hat && c1_light() &&
+         inv_prunes<LOGN, false>(c, M);
+}
+inline bool c1_direct(const hl_ctx *c, const MacGeom &g, const MaskArgs &M) {
+  return c->N == 4096 ? c1_direct_ok<12>(c, g, M) : c1_direct_ok<13>(c, g, M);
+}
+
 template <int LOGN, bool RR>
 void launch_inv_mask_t(const hl_ctx *c, const uint64_t *ct_ntt, uint64_t *masked, uint64_t *share, MaskArgs M,
                        int64_t nout, cudaStream_t st) {
@@ -1791,16 +1841,13 @@ void launch_inv_mask_t(const hl_ctx *c, const uint64_t *ct_ntt, uint64_t *masked
     set_smem(k_c1_out<LOGN>, ntt_smem<LOGN>());
     init = true;
   }
-  // the pruned c0 transform needs r in {2..16} and one warp group per prime within the CTA
-  static const bool no_prune = getenv("HELINEAR_NO_PRUNE") != nullptr;
-  const int re = std::min(M.r, 16);                   // the pruned kernel's live class (see there)
-  const int wpp = (Gm::NT / std::max(re, 1) + 31) / 32;
-  const size_t ext = RR ? 16 : 8;                      // sigma (+ row f4: e1 + F) per kept position
+  const int re = std::min(M.r, 16);
+  const size_t ext = RR ? 16 : 8;
   const size_t smem_c0 = ntt_smem<LOGN>() * c->L + (size_t)M.m * M.n * ext;
-  const bool prune = !no_prune && M.r >= 2 && (int)c->L * wpp <= Gm::NT / 32 && smem_c0 <= 232448;
+  const bool prune = inv_prunes<LOGN, RR>(c, M);
   const size_t smem = ntt_smem<LOGN>() + (RR ? std::max((size_t)M.m * M.n * 16, (size_t)Gm::N) : (size_t)M.m * M.n * 8);
   KTimer kt(c, HL_K_INTT_MASK, st);
-  kt.nk = prune ? 2 : 1;
+  kt.nk = prune && !M.c1_done ? 2 : 1;
   if (prune) {
     static const bool cmp = [] { const char *e = getenv("HELINEAR_C0_COMPACT"); return e ? atoi(e) != 0 : true; }();
     if (cmp) {
@@ -1810,8 +1857,8 @@ void launch_inv_mask_t(const hl_ctx *c, const uint64_t *ct_ntt, uint64_t *masked
     } else {
       k_intt_c0_pruned<LOGN, RR><<<(unsigned)nout, Gm::NT, smem_c0, st>>>(ct_ntt, masked, share, M, c->dp);
     }
-    static const bool light = [] { const char *e = getenv("HELINEAR_C1_LIGHT"); return e ? atoi(e) != 0 : true; }();
-    if (!RR && light) k_c1_out<LOGN><<<(unsigned)nout, Gm::NT, ntt_smem<LOGN>(), st>>>(ct_ntt, masked, M, c->dp);
+    if (M.c1_done) return;                             // the MAC wrote c1 (c1_direct_ok)
+    if (!RR && c1_light()) k_c1_out<LOGN><<<(unsigned)nout, Gm::NT, ntt_smem<LOGN>(), st>>>(ct_ntt, masked, M, c->dp);
     else k_ntt_inv_mask<LOGN, RR><<<(unsigned)nout, Gm::NT, smem, st>>>(ct_ntt, masked, share, M, c->dp, 1);
   } else {
     k_ntt_inv_mask<LOGN, RR><<<(unsigned)(nout * 2), Gm::NT, smem, st>>>(ct_ntt, masked, share, M, c->dp, 0);
@@ -1932,7 +1979,7 @@ static MaskArgs mask_args(const Geo &g, int64_t Ma, int64_t Nb, uint64_t seed) {
   M.m = g.m; M.r = g.r; M.n = g.n; M.seed = seed;
   M.lm = __builtin_ctz((unsigned)g.m); M.lr = __builtin_ctz((unsigned)g.r);
   M.pk_hat = nullptr; M.u_hat = nullptr; M.cdt = nullptr; M.flood_bits = 0;
-  M.nC = (int)(2 * g.nK); M.cperm = 0;
+  M.nC = (int)(2 * g.nK); M.cperm = 0; M.c1_done = 0;
   return M;
 }
 
@@ -1969,9 +2016,11 @@ extern "C" int hl_he_matmul_share(const hl_ctx *c, hl_tile tile, const void *wca
   MacGeom mg = mac_geom(c, g.nIs, g.nJ, nC);
   mg.cperm = mg.engine == 2;
   fwd_ntt(c, ct_in, workspace, g.nJ * nC, &mg, st);
-  launch_mac(c, (const uint2 *)wcache, (const uint32_t *)workspace, ct_out_ntt, mg, st);
   MaskArgs M = mask_args(g, Ma, Nb, seed);
   M.cperm = mg.cperm;
+  M.c1_done = c1_direct(c, mg, M);
+  launch_mac(c, (const uint2 *)wcache, (const uint32_t *)workspace, ct_out_ntt, mg, st, kMacSmemAlone, 0,
+             M.c1_done ? &M : nullptr, ct_masked);
   if (c->N == 4096) launch_inv_mask<12>(c, ct_out_ntt, ct_masked, share, M, g.nIs * g.nK, st);
   else launch_inv_mask<13>(c, ct_out_ntt, ct_masked, share, M, g.nIs * g.nK, st);
   return hl_cuda_check("hl_he_matmul_share: launch");
@@ -2005,6 +2054,7 @@ static int linear_batch_run(const hl_ctx *c, hl_tile tile, int n, const hl_linea
     E[i].mg.cperm = E[i].mg.engine == 2;
     E[i].M = mask_args(E[i].g, d[i].Ma, d[i].Nb, d[i].seed);
     E[i].M.cperm = E[i].mg.cperm;
+    E[i].M.c1_done = c1_direct(c, E[i].mg, E[i].M);
   }
   cudaStream_t sc = (cudaStream_t)stream, s0 = (cudaStream_t)c->mac_stream, s1 = (cudaStream_t)c->aux_stream;
   std::vector<cudaEvent_t> ev(2 * n + 3);
@@ -2048,7 +2098,8 @@ static int linear_batch_run(const hl_ctx *c, hl_tile tile, int n, const hl_linea
     for (int k = 0; k < n; k++) {
       const int i = ord[k];
       fwd_ntt(c, d[i].ct_in, d[i].workspace, E[i].g.nJ * 2 * E[i].g.nK, &E[i].mg, sc);
-      launch_mac(c, (const uint2 *)d[i].wcache, (const uint32_t *)d[i].workspace, d[i].ct_out_ntt, E[i].mg, sc);
+      launch_mac(c, (const uint2 *)d[i].wcache, (const uint32_t *)d[i].workspace, d[i].ct_out_ntt, E[i].mg, sc,
+                 kMacSmemAlone, 0, E[i].M.c1_done ? &E[i].M : nullptr, d[i].ct_masked);
       if (c->N == 4096) launch_inv_mask<12>(c, d[i].ct_out_ntt, d[i].ct_masked, d[i].share, E[i].M, E[i].g.nIs * E[i].g.nK, sc);
       else launch_inv_mask<13>(c, d[i].ct_out_ntt, d[i].ct_masked, d[i].share, E[i].M, E[i].g.nIs * E[i].g.nK, sc);
     }
@@ -2076,7 +2127,7 @@ static int linear_batch_run(const hl_ctx *c, hl_tile tile, int n, const hl_linea
       return e ? atoi(e) : 0;
     }();
     launch_mac(c, (const uint2 *)d[i].wcache, (const uint32_t *)d[i].workspace, d[i].ct_out_ntt, E[i].mg, s0,
-               mac_smem, mac_grid);
+               mac_smem, mac_grid, E[i].M.c1_done ? &E[i].M : nullptr, d[i].ct_masked);
     cudaEventRecord(e_mac[i], s0);
     if (!split && k + 1 < n) fwd(ord[k + 1]);                           // overlaps MAC(i)
     cudaStreamWaitEvent(s1, e_mac[i], 0);

@@ -80,7 +80,23 @@ struct MacTcArgs {
   int *sched;                 // work counter (zeroed before the launch; in the caller's workspace)
   int ko;                     // diagnostics (HELINEAR_MAC_KO bitmask): 1 skip MMAs, 2 skip conversion, 4 skip epilogue math
   int lazy_out;               // 1: outputs only < 2^52 (= residue + k p, k < 4): fine for the inverse NTT's input
+  // c1 straight into the compressed response (fused paths, cperm, one launch): columns C >= c1_nK
+  // (the c1 halves) are written canonical, in natural evaluation order (reading C26), at
+  // c1_out + o L (mn + N) + L mn + l N + k, o = row nK + (C - nK) -- k_c1_out's result, without the
+  // NTT-domain round trip through `out`.  c1_out == nullptr: off.
+  uint64_t *c1_out;
+  int c1_nK, c1_mn, c1_lognt;
+  int qperm;                  // quad order (load_ntt_domain_q): set with c1_out
 };
+
+// slot of the si-th output of slot quad sq: consecutive slots, or (qperm) the quad order
+// u NT + t' + {0, 2, 1, 3}[si] NT/4 whose natural evaluation points are 4 consecutive k
+__device__ __forceinline__ int tc_slot(const MacTcArgs &A, int sq, int si) {
+  if (!A.qperm) return sq * 4 + si;
+  const int pos = sq * 4, l = pos / A.N, rem = pos - l * A.N;
+  const int nt = 1 << A.c1_lognt, u = rem >> A.c1_lognt, tq = (rem & (nt - 1)) >> 2;
+  return l * A.N + u * nt + tq + ((si & 1) << 1 | (si >> 1)) * (nt >> 2);
+}
 
 // UMMA shared-memory descriptor: K-major, no swizzle; core matrix = 8 rows x 16 B contiguous.
 // lbo = byte distance between the two 16-B K halves, sbo = between 8-row groups; version 1 (sm_100).
@@ -260,7 +276,7 @@ k_mac_tc(MacTcArgs A, DevParams P) {
         const uint32_t abytes = 224u * rows;
         const uint8_t *wt = A.W + (size_t)it.t * g.RT * g.LN * g.nJp * 7;
         for (int si = 0; si < T::SPI; si++) {
-          const int s = it.sq * T::SPI + si;
+          const int s = tc_slot(A, it.sq, si);
           for (int kk = 0; kk < A.njc; kk++) {
             const int jc = A.jc0 + kk;
             mbar_wait_p(&empty[st], ph, A.prof ? &pw[0] : nullptr);
@@ -460,6 +476,24 @@ k_mac_tc(MacTcArgs A, DevParams P) {
         const int rr = e / CW, c = e % CW;
         const uint64_t *sv = stg + rr * T::STG_STRIDE + c * T::SPI;
         uint64_t v0 = sv[0], v1 = sv[1], v2 = sv[2], v3 = sv[3];
+        const int col = it.cg * CW + c;
+        if (A.c1_out && col >= A.c1_nK) {
+          // quad order (tc_slot): slot u NT + t' + {0,2,1,3}[i] NT/4 holds natural k = k0 + i,
+          // k0 = brev4(u) NT + brev(t') (nat_of) -- one 32-B sector of the response's c1
+          const int sl = (int)(s0 - (size_t)l * A.N), nt = 1 << A.c1_lognt;
+          const int u = sl >> A.c1_lognt, tq = (sl & (nt - 1)) >> 2;
+          const int k0 = (int)(__brev((unsigned)u) >> 28) * nt + (int)(__brev((unsigned)tq) >> (32 - A.c1_lognt));
+          const int64_t o = (int64_t)(g.RT * it.t + rr) * A.c1_nK + (col - A.c1_nK);
+          ulonglong2 *dst = reinterpret_cast<ulonglong2 *>(
+              A.c1_out + (size_t)o * P.L * (A.c1_mn + A.N) + (size_t)P.L * A.c1_mn + (size_t)l * A.N + k0);
+          v0 = v0 >= pc.two_p ? v0 - pc.two_p : v0; v0 = v0 >= pc.p ? v0 - pc.p : v0;
+          v1 = v1 >= pc.two_p ? v1 - pc.two_p : v1; v1 = v1 >= pc.p ? v1 - pc.p : v1;
+          v2 = v2 >= pc.two_p ? v2 - pc.two_p : v2; v2 = v2 >= pc.p ? v2 - pc.p : v2;
+          v3 = v3 >= pc.two_p ? v3 - pc.two_p : v3; v3 = v3 >= pc.p ? v3 - pc.p : v3;
+          dst[0] = make_ulonglong2(v0, v1);
+          dst[1] = make_ulonglong2(v2, v3);
+          continue;
+        }
         ulonglong2 *dst = reinterpret_cast<ulonglong2 *>(
             A.out + ((size_t)(g.RT * it.t + rr) * g.nC + it.cg * CW + c) * g.LN + s0);
         if (A.accumulate) {
