@@ -306,11 +306,19 @@ extern "C" int hl_timing_enable(hl_ctx *c, int on) {
 extern "C" int hl_timing_read(hl_ctx *c, double *ms, int64_t *count) {
   if (!c || !ms || !count) return hl_fail(HL_EINVAL, "hl_timing_read: NULL argument");
   if (!c->timing) return HL_OK;
+  // diagnostics: HELINEAR_TIMELINE=1 prints every section's (class, start, end) in ms relative to
+  // the first recorded start (tools/gpu/timeline.py)
+  static const bool timeline = getenv("HELINEAR_TIMELINE") != nullptr;
   for (auto &r : c->timing->rec) {
     float t = 0;
     if (cudaEventSynchronize((cudaEvent_t)r.second.second) != cudaSuccess ||
         cudaEventElapsedTime(&t, (cudaEvent_t)r.second.first, (cudaEvent_t)r.second.second) != cudaSuccess)
       return hl_cuda_check("hl_timing_read");
+    if (timeline && !c->timing->rec.empty()) {
+      float t0 = 0;
+      cudaEventElapsedTime(&t0, (cudaEvent_t)c->timing->rec[0].second.first, (cudaEvent_t)r.second.first);
+      fprintf(stderr, "[timeline] %d %.4f %.4f\n", r.first, t0, t0 + t);
+    }
     if (r.first >= 0 && r.first < HL_K_COUNT) { ms[r.first] += t; count[r.first] += 1; }
     c->timing->pool.push_back(r.second.first);
     c->timing->pool.push_back(r.second.second);

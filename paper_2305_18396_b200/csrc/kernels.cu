@@ -396,9 +396,11 @@ MacGeom mac_geom(const hl_ctx *c, int64_t nIs, int64_t nJ, int64_t nC) {
   g.nSb = g.LN / 32;
   g.f64 = c->mac_engine == 1;
   g.nIp = g.nIb * 16;
-  g.nIt = (g.nIp + 127) / 128;
+  // tile rows per MMA: <= 128 (M = 128; tiles of <= 64 rows use M = 64); HELINEAR_MAC_RT_MAX=64 (experiment)
+  static const int rt_max = [] { const char *e = getenv("HELINEAR_MAC_RT_MAX"); return e ? atoi(e) : 128; }();
+  g.nIt = (g.nIp + rt_max - 1) / rt_max;
   g.RT = ((g.nIp + g.nIt - 1) / g.nIt + 7) / 8 * 8;      // balanced tiles, multiple of 8 (UMMA core rows)
-  if ((int64_t)g.RT * (g.nIt - 1) >= nIs) g.RT = 128;   // never an empty last tile
+  if ((int64_t)g.RT * (g.nIt - 1) >= nIs) g.RT = rt_max;   // never an empty last tile
   g.nJp = (int)((nJ + 31) / 32 * 32);
   g.nJc = g.nJp / 32;
   g.cperm = 0;
@@ -2115,6 +2117,10 @@ static int linear_batch_run(const hl_ctx *c, hl_tile tile, int n, const hl_linea
   } else {
     fwd(ord[0]);
   }
+  // experiment knob: HELINEAR_BATCH_FWD_FIRST=1 starts the first MAC only after every forward NTT
+  static const bool fwd_first = getenv("HELINEAR_BATCH_FWD_FIRST") != nullptr;
+  if (fwd_first && split)
+    for (int k = 0; k < n; k++) cudaStreamWaitEvent(s0, e_fwd[ord[k]], 0);
   for (int k = 0; k < n; k++) {
     const int i = ord[k];
     cudaStreamWaitEvent(s0, e_fwd[i], 0);
