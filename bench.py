@@ -169,11 +169,15 @@ def run_ours(args, rank, world, local_rank):
         ct_dev = ctx.encrypt_device(s_hat, tile, dX, synth.seed_for(block, mi, "enc"))   # row f3, == encrypt()
         ct_host = hl.to_host(ct_dev)
         dW = hl.to_device(W, dev)
+        # offline encoding, timed warm: the first call pays one-off costs (lazy module loading, the
+        # allocation of the cache), so it is repeated and the second call timed
+        del_wc = ctx.encode_weights(tile, dW, i0, i1)
         torch.cuda.synchronize()
         t0 = time.perf_counter()
         wc = ctx.encode_weights(tile, dW, i0, i1)
         torch.cuda.synchronize()
         t_enc += time.perf_counter() - t0
+        del del_wc
         del dW
         mats.append(dict(mm=mm, tile=tile, lay=lay, wc=wc, ct=ct_dev, i0=i0, i1=i1, nI_full=nI_full, s_hat=s_hat, dX=dX,
                          ct_host=torch.from_numpy(ct_host.view(np.int64).reshape(-1)).pin_memory(),
@@ -411,7 +415,8 @@ def run_ours(args, rank, world, local_rank):
 
         def att_step():      # the block's 48 Pi_MatMul products as one pipelined batch
             attention.server_cross_products(actx, items, stream=stream)
-        att_step()
+        for _ in range(2):   # warm-up: the first calls pay module loading and allocator growth
+            att_step()
         torch.cuda.synchronize()
         nrep = max(2, min(args.steps, 5))
         a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)

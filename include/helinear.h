@@ -336,6 +336,12 @@ int hl_fc_layout(const hl_ctx *ctx, int64_t Nb, int64_t R, int64_t Ma, int64_t *
  * wplanes (device, opaque byte planes). */
 int hl_fc_encode_weights(const hl_ctx *ctx, const uint64_t *W, int64_t R, int64_t Ma, void *wplanes,
                          void *stream);
+/* Same, with the range check optional: check = 0 skips the status readback and its stream
+ * synchronisation (the caller vouches for W < 2^log2_t, e.g. the server's own shares, which are
+ * reduced mod 2^log2_t by construction -- row f2's online encodings); values
+ * out of range then give unspecified (but memory-safe) results.  check != 0: hl_fc_encode_weights. */
+int hl_fc_encode_weights_chk(const hl_ctx *ctx, const uint64_t *W, int64_t R, int64_t Ma, void *wplanes,
+                             int check, void *stream);
 
 /* Online: X1 device [Nb][R] (the server's share of the input, taken mod 2^log2_t), bias device [Ma]
  * or NULL, share device [Nb][Ma] (in/out), workspace device (hl_fc_layout). Stream-ordered. */

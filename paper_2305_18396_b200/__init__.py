@@ -31,7 +31,7 @@ EXPORTS = ("hl_last_error", "hl_ctx_create", "hl_ctx_destroy", "hl_ctx_params", 
            "hl_layout_query",
            "hl_keygen", "hl_encrypt", "hl_decrypt_share", "hl_encode_weights", "hl_he_matmul",
            "hl_mask_and_share", "hl_he_matmul_share", "hl_he_linear_batch", "hl_he_linear_host", "hl_poly_mul",
-           "hl_ntt_roundtrip", "hl_timing_enable", "hl_timing_read", "hl_fc_layout", "hl_fc_encode_weights",
+           "hl_ntt_roundtrip", "hl_timing_enable", "hl_timing_read", "hl_fc_layout", "hl_fc_encode_weights", "hl_fc_encode_weights_chk",
            "hl_fc_local_share", "hl_encode_weights_strided", "hl_encode_weights_scratch", "hl_share_accumulate", "hl_sk_prepare",
            "hl_encrypt_device", "hl_decrypt_share_device", "hl_pk_gen", "hl_pk_prepare", "hl_he_matmul_share_rr",
            "hl_expand_seeded", "hl_he_linear_batch_host", "hl_packed50_words", "hl_pack50", "hl_unpack50",
@@ -131,6 +131,7 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
         "hl_pk_prepare": [vp, vp, vp, vp],
         "hl_he_matmul_share_rr": [vp, Tile, vp, i64, i64, i64, i64, i64, vp, vp, vp, vp, i32, vp, u64, vp, vp, vp],
         "hl_fc_encode_weights": [vp, vp, i64, i64, vp, vp],
+        "hl_fc_encode_weights_chk": [vp, vp, i64, i64, vp, ctypes.c_int, vp],
         "hl_fc_local_share": [vp, vp, vp, vp, i64, i64, i64, vp, vp, vp],
         "hl_timing_read": [vp, vp, vp],
         "hl_expand_seeded": [vp, Tile, i64, i64, u64, vp, vp],
@@ -486,12 +487,14 @@ class Context:
         _check(_lib.hl_fc_layout(self._h, Nb, R, Ma, ctypes.byref(wb), ctypes.byref(ws)))
         return wb.value, ws.value
 
-    def fc_encode_weights(self, W, stream=None):
-        """W: CUDA tensor [R][Ma] (< 2^t).  Returns the opaque byte-plane form."""
+    def fc_encode_weights(self, W, stream=None, check: bool = True):
+        """W: CUDA tensor [R][Ma] (< 2^t).  Returns the opaque byte-plane form.  check=False skips
+        the range check and its stream synchronisation (hl_fc_encode_weights_chk)."""
         R, Ma = W.shape
         wb, _ = self.fc_layout(1, R, Ma)
         wp = _dev_empty(-(-wb // 8), W.device)
-        _check(_lib.hl_fc_encode_weights(self._h, _dptr(W), R, Ma, _dptr(wp), _stream(stream)))
+        _check(_lib.hl_fc_encode_weights_chk(self._h, _dptr(W), R, Ma, _dptr(wp), int(bool(check)),
+                                             _stream(stream)))
         return wp
 
     def fc_local_share(self, X1, wplanes, Ma: int, share, bias=None, workspace=None, stream=None):

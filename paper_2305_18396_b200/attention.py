@@ -33,7 +33,7 @@ def server_cross_product(ctx, tile, X1, Y1, ct_Y0T, ct_X0, seeds, stream=None):
     w2 = ctx.encode_weights(t2, Y1, stream=stream, check=False)            # W = Y1: R = d, Ma = n2
     m2, z1 = ctx.he_matmul_share(t2, w2, n2, d, n, ct_X0, seed=seeds[1], stream=stream)      # z1 [n][n2]
     ctx.share_accumulate(z1, s1, n, n2, transpose=True, stream=stream)     # + <X1 Y0>_1^T
-    ctx.fc_local_share(X1, ctx.fc_encode_weights(Y1, stream=stream), n2, z1, stream=stream)   # + X1 Y1
+    ctx.fc_local_share(X1, ctx.fc_encode_weights(Y1, stream=stream, check=False), n2, z1, stream=stream)   # + X1 Y1
     return m1, m2, z1
 
 
@@ -61,6 +61,7 @@ def server_cross_products(ctx, items, stream=None):
         n, n2 = meta[k]
         (m1, s1), (m2, z1) = outs[2 * k], outs[2 * k + 1]
         ctx.share_accumulate(z1, s1, n, n2, transpose=True, stream=stream)
-        ctx.fc_local_share(it["X1"], ctx.fc_encode_weights(it["Y1"], stream=stream), n2, z1, stream=stream)
+        ctx.fc_local_share(it["X1"], ctx.fc_encode_weights(it["Y1"], stream=stream, check=False), n2, z1,
+                           stream=stream)
         res.append((m1, m2, z1))
     return res

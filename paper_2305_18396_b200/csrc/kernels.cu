@@ -2421,6 +2421,11 @@ extern "C" int hl_fc_layout(const hl_ctx *c, int64_t Nb, int64_t R, int64_t Ma, 
 
 extern "C" int hl_fc_encode_weights(const hl_ctx *c, const uint64_t *W, int64_t R, int64_t Ma, void *wplanes,
                                     void *stream) {
+  return hl_fc_encode_weights_chk(c, W, R, Ma, wplanes, 1, stream);
+}
+
+extern "C" int hl_fc_encode_weights_chk(const hl_ctx *c, const uint64_t *W, int64_t R, int64_t Ma, void *wplanes,
+                                        int check, void *stream) {
   int rc;
   if ((rc = check_ptrs({c, W, wplanes}, "hl_fc_encode_weights"))) return rc;
   FcGeom g;
@@ -2433,6 +2438,7 @@ extern "C" int hl_fc_encode_weights(const hl_ctx *c, const uint64_t *W, int64_t 
     k_fc_w_planes<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(W, (uint8_t *)wplanes, g, c->d_flags);
   }
   if ((rc = hl_cuda_check("hl_fc_encode_weights: launch"))) return rc;
+  if (!check) return HL_OK;
   uint32_t flags[2];
   if (cudaMemcpyAsync(flags, c->d_flags, 8, cudaMemcpyDeviceToHost, st) != cudaSuccess ||
       cudaStreamSynchronize(st) != cudaSuccess)

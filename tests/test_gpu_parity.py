@@ -512,6 +512,8 @@ def test_fc_local_share_vs_oracle(hl, ctx4096, Nb, R, Ma):
         X1[:] = (1 << 37) - 1
         W[:7] = (1 << 37) - 1
     wp = ctx.fc_encode_weights(hl.to_device(W))
+    # the unchecked online form (hl_fc_encode_weights_chk, check = 0) writes the same planes
+    assert np.array_equal(hl.to_host(ctx.fc_encode_weights(hl.to_device(W), check=False)), hl.to_host(wp))
     share = hl.to_device(S)
     ctx.fc_local_share(hl.to_device(X1), wp, Ma, share, bias=hl.to_device(b))
     _sync()
