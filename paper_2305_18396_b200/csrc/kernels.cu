@@ -400,6 +400,9 @@ MacGeom mac_geom(const hl_ctx *c, int64_t nIs, int64_t nJ, int64_t nC) {
   static const int rt_max = [] { const char *e = getenv("HELINEAR_MAC_RT_MAX"); return e ? atoi(e) : 128; }();
   g.nIt = (g.nIp + rt_max - 1) / rt_max;
   g.RT = ((g.nIp + g.nIt - 1) / g.nIt + 7) / 8 * 8;      // balanced tiles, multiple of 8 (UMMA core rows)
+  // experiment: HELINEAR_MAC_GREEDY=1 -> full 128-row tiles + one short last tile (M = 64 if <= 64 rows)
+  static const bool greedy = getenv("HELINEAR_MAC_GREEDY") != nullptr;
+  if (greedy && g.nIt > 1) g.RT = rt_max;
   if ((int64_t)g.RT * (g.nIt - 1) >= nIs) g.RT = rt_max;   // never an empty last tile
   g.nJp = (int)((nJ + 31) / 32 * 32);
   g.nJc = g.nJp / 32;

@@ -297,7 +297,9 @@ k_mac_tc(MacTcArgs A, DevParams P) {
     // single-lane branch costs more than the MMA itself (profiles/r01/microbench_umma_i8_cost.log).
     // tiles of <= 64 rows use M = 64 (half the A-operand shared-memory reads per MMA); the
     // accumulator rows then sit in lanes 32(r/16) + r%16 (profiles/r01/microbench_umma_i8.log)
-    const uint32_t idesc = umma_idesc_u8(g.RT <= 64 ? 64 : 128, (A.ko & 8) ? 16 : T::NM);   // ko 8: timing only
+    // M per item: tiles of <= 64 rows (also a short last tile of uneven tiling) use M = 64
+    const uint32_t idesc128 = umma_idesc_u8(128, (A.ko & 8) ? 16 : T::NM);   // ko 8: timing only
+    const uint32_t idesc64 = umma_idesc_u8(64, (A.ko & 8) ? 16 : T::NM);
     int st = 0;
     uint32_t ph = 0;
     uint32_t tile_no = 0, zseq = 0;
@@ -307,6 +309,7 @@ k_mac_tc(MacTcArgs A, DevParams P) {
       const TcItem it = tc_decode(g, item);
       const int rows = min(g.RT, g.nIp - g.RT * it.t);
       const uint32_t plane = 32u * rows, lbo_a = 16u * rows;
+      const uint32_t idesc = rows <= 64 ? idesc64 : idesc128;
       for (int si = 0; si < T::SPI; si++, tile_no++) {
         const uint32_t buf = tile_no % T::NBUF, tph = (tile_no / T::NBUF) & 1;
         mbar_wait_p(&tempty[buf], tph ^ 1, (A.prof && lane == 0) ? &pw[1] : nullptr);
@@ -388,8 +391,6 @@ k_mac_tc(MacTcArgs A, DevParams P) {
     // reduced as Barrett(L) + Shoup(M, 2^40 mod p) + Shoup(H, 2^72 mod p), each in [0, 2p).
     constexpr int CH = CW / 2;
     const int q = warp & 3, hh = (warp - 4) >> 2;
-    const bool m64 = g.RT <= 64;
-    const int row = m64 ? (lane < 16 ? 16 * q + lane : 1 << 20) : 32 * q + lane;   // tile row held by this lane
     const int et = threadIdx.x - 128;
     uint32_t tile_no = 0;
     for (uint32_t seq = 0;; seq++) {
@@ -399,6 +400,8 @@ k_mac_tc(MacTcArgs A, DevParams P) {
       const int l = (it.sq * T::SPI) / A.N;
       const PrimeConsts pc = pick(P, l);
       const int rows_valid = min(g.RT, g.nIs - g.RT * it.t);
+      const bool m64 = min(g.RT, g.nIp - g.RT * it.t) <= 64;   // this item's MMA M (as the MMA warp)
+      const int row = m64 ? (lane < 16 ? 16 * q + lane : 1 << 20) : 32 * q + lane;   // tile row held by this lane
       const bool active = (m64 ? 16 : 32) * q < rows_valid;   // warp-uniform: this quadrant holds outputs
       for (int si = 0; si < T::SPI; si++, tile_no++) {
         const uint32_t buf = tile_no % T::NBUF, tph = (tile_no / T::NBUF) & 1;
