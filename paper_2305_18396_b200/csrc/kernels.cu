@@ -21,6 +21,7 @@
 // Operands are stored as 25-bit limb pairs (x = x0 + 2^25 x1); each modular MAC costs three
 // IMAD.WIDE.U32 (Karatsuba: x0*y0, x1*y1, (x0+x1)(y0+y1)) into three exact 64-bit lazy
 // accumulators; one 128-bit reduction per output.
+#include <cuda.h>   // CUtensorMap (the MAC's c1 loads; encoded through the runtime's driver entry point)
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -369,6 +370,10 @@ struct MacGeom {
   int nIp, nIt, RT, nJp, nJc;   // engine 2: rows padded to 16, nIt balanced I tiles of RT rows, J padded to 32, 32-J steps
   int cperm;     // MAC column of (K, c): 0 -> 2K + c (the API layout [nK][2]), 1 -> c nK + K (c0 columns
                  // first: the fused paths, so that the forward NTTs of c0 pair up and the c1 copies do too)
+  int c1_in;     // 1: the MAC loads the c1 halves straight from the ciphertexts (tensor-map TMA, quad
+                 // order) and the forward kernel transforms c0 only
+  int xw;        // X row width (u64 per (slot, J)): CW, or nK when c1_in with one column group (X then
+                 // holds only the c0 columns)
 };
 
 __host__ __device__ __forceinline__ size_t w_index(const MacGeom &g, int iloc, int J, int s) {
@@ -407,6 +412,8 @@ MacGeom mac_geom(const hl_ctx *c, int64_t nIs, int64_t nJ, int64_t nC) {
   g.nJp = (int)((nJ + 31) / 32 * 32);
   g.nJc = g.nJp / 32;
   g.cperm = 0;
+  g.c1_in = 0;
+  g.xw = g.CW;
   return g;
 }
 
@@ -555,10 +562,10 @@ k_ntt_fwd_c0x2(const uint64_t *__restrict__ in, uint64_t *__restrict__ out, DevP
     }
   }
   const int cg = K0 / mg.CW, cc = K0 % mg.CW;
-  uint64_t *dst0 = out + ((size_t)cg * mg.LN + (size_t)l * Gm::N) * mg.nJp * mg.CW + (size_t)J * mg.CW + cc;
+  uint64_t *dst0 = out + ((size_t)cg * mg.LN + (size_t)l * Gm::N) * mg.nJp * mg.xw + (size_t)J * mg.xw + cc;
 #pragma unroll
   for (int u = 0; u < 16; u++) {
-    uint64_t *dst = dst0 + (size_t)slot_of<LOGN>(t, u) * mg.nJp * mg.CW;
+    uint64_t *dst = dst0 + (size_t)slot_of<LOGN>(t, u) * mg.nJp * mg.xw;
     const uint64_t x0 = d2u(canon_d(a[u], pc.pd, pc.pinv)), x1 = d2u(canon_d(b[u], pc.pd, pc.pinv));
     if (pair) *reinterpret_cast<ulonglong2 *>(dst) = make_ulonglong2(x0, x1);
     else *dst = x0;
@@ -1619,6 +1626,7 @@ void launch_fwd_cperm(const hl_ctx *c, const uint64_t *in, uint64_t *out, int64_
     set_smem(k_ntt_fwd_c0x2<LOGN, false, MB2>, smem2); set_smem(k_ntt_fwd_c0x2<LOGN, true>, smem2);
     if constexpr (LOGN == 12) {
       set_smem(k_ntt_fwd_c0x2<LOGN, true, 2>, smem2); set_smem(k_ntt_fwd_c0x2<LOGN, true, 3>, smem2);
+      set_smem(k_ntt_fwd_c0x2<LOGN, false, 3>, smem2);
     }
     set_smem(k_c1_to_x<LOGN, 4>, 4 * (size_t)Geom<LOGN>::N * 8); set_smem(k_c1_to_x<LOGN, 2>, 2 * (size_t)Geom<LOGN>::N * 8);
     set_smem(k_c1_to_x<LOGN, 1>, (size_t)Geom<LOGN>::N * 8);
@@ -1626,6 +1634,12 @@ void launch_fwd_cperm(const hl_ctx *c, const uint64_t *in, uint64_t *out, int64_
   }
   KTimer kt(c, HL_K_NTT_FWD, st);
   static const bool fuse_c1 = [] { const char *e = getenv("HELINEAR_FUSE_C1"); return e ? atoi(e) != 0 : true; }();
+  if (mg.c1_in) {                                  // c1 is read by the MAC itself: c0 pairs only
+    const dim3 gx((unsigned)(nJ * ((nK + 1) / 2)), c->L);
+    if constexpr (LOGN == 12) k_ntt_fwd_c0x2<LOGN, false, 3><<<gx, Geom<LOGN>::NT, smem2, st>>>(in, out, c->dp, mg);
+    else k_ntt_fwd_c0x2<LOGN, false, MB2><<<gx, Geom<LOGN>::NT, smem2, st>>>(in, out, c->dp, mg);
+    return;
+  }
   const bool fused = fuse_c1 && (nK % 2 == 0);   // c1 pairs (K0, K0+1) adjacent in the c1 column range
   // N = 4096: 3 CTAs per SM (80 registers, a few bytes of spill; measured best) or 2 (<= 128)
   static const int minb = [] { const char *e = getenv("HELINEAR_X2_MINB"); return e ? atoi(e) : 3; }();
@@ -1730,7 +1744,7 @@ void launch_mac_tc_t(const hl_ctx *c, MacTcArgs A, int smem_budget, int grid, cu
   using T = TcGeom<CW>;
   static bool init = false;
   if (!init) { set_smem(k_mac_tc<CW>, T::SMEM_MAX); init = true; }
-  A.ring = tc_ring<CW>(A.g.RT, smem_budget);
+  A.ring = tc_ring<CW>(A.g.RT, smem_budget, A.c1_bytes);
   static const bool prof = getenv("HELINEAR_MAC_PROF") != nullptr;
   A.prof = nullptr;
   if (prof) cudaMalloc(&A.prof, 8 * sizeof(unsigned long long)), cudaMemsetAsync(A.prof, 0, 64, st);
@@ -1754,9 +1768,45 @@ void launch_mac_tc_t(const hl_ctx *c, MacTcArgs A, int smem_budget, int grid, cu
 // the tensor-core engine's workspace = X residues [nCg][LN][nJp][CW] u64 + 256 B of scheduler state
 inline size_t tc_sched_offset(const MacGeom &g) { return (size_t)g.nJp * g.nC * g.LN * 8; }
 
+// cuTensorMapEncodeTiled through the runtime (no -lcuda): nullptr if the driver lacks it
+using TmapEncodeFn = CUresult (*)(CUtensorMap *, CUtensorMapDataType, cuuint32_t, void *, const cuuint64_t *,
+                                  const cuuint64_t *, const cuuint32_t *, const cuuint32_t *, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+static TmapEncodeFn tmap_encode() {
+  static TmapEncodeFn fn = [] {
+    void *p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      p = nullptr;
+    return (TmapEncodeFn)p;
+  }();
+  return fn;
+}
+// the c1 halves of ct_in [nJ][nK][2][L][N] as a 3-D tensor (k over all primes, K, J) of u64; a box
+// is {2 natural points, the group's c1 columns, 32 J} -> shared [J][K][2] (rows J >= nJ zero-filled)
+static bool c1_tmap(CUtensorMap *m, const uint64_t *ct_in, int64_t LN, int64_t nK, int64_t nJ, int cols) {
+  const TmapEncodeFn enc = tmap_encode();
+  if (!enc) return false;
+  const cuuint64_t dims[3] = {(cuuint64_t)LN, (cuuint64_t)nK, (cuuint64_t)nJ};
+  const cuuint64_t strides[2] = {(cuuint64_t)(2 * LN * 8), (cuuint64_t)(nK * 2 * LN * 8)};
+  const cuuint32_t box[3] = {2, (cuuint32_t)cols, 32}, es[3] = {1, 1, 1};
+  return enc(m, CU_TENSOR_MAP_DATA_TYPE_UINT64, 3, const_cast<uint64_t *>(ct_in + LN), dims, strides, box, es,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 void launch_mac_tc(const hl_ctx *c, const void *W, const void *X, uint64_t *out, const MacGeom &g, int smem_budget,
-                   int grid, cudaStream_t st, const MaskArgs *c1m = nullptr, uint64_t *c1_masked = nullptr) {
+                   int grid, cudaStream_t st, const MaskArgs *c1m = nullptr, uint64_t *c1_masked = nullptr,
+                   const uint64_t *ct_in = nullptr) {
   MacTcArgs A;
+  A.c1_in = 0; A.c1_cols = 0; A.c1_bytes = 0;
+  if (g.c1_in && c1m && ct_in) {
+    A.c1_cols = (int)std::min<int64_t>(g.CW, c1m->nK);
+    A.c1_bytes = 2 * A.c1_cols * 32 * 8;
+    c1_tmap(&A.c1map, ct_in, g.LN, c1m->nK, g.nJ, A.c1_cols);   // validated by c1_in_ok
+    A.c1_in = 1;
+  }
   A.W = (const uint8_t *)W; A.X = (const uint64_t *)X; A.out = out; A.g = g; A.N = (int)c->N;
   A.c1_out = c1m ? c1_masked : nullptr;
   A.c1_nK = c1m ? (int)c1m->nK : 0;
@@ -1785,9 +1835,10 @@ constexpr int kMacSmemAlone = 232448;        // the MAC alone on the SM: the dee
 constexpr int kMacSmemShared = 155 * 1024;   // leaves room for one NTT CTA (~70 KB) beside the MAC (sweep: tools/gpu/ring_sweep*.sh)
 
 void launch_mac(const hl_ctx *c, const uint2 *W, const uint32_t *X, uint64_t *out, const MacGeom &g, cudaStream_t st,
-                int smem_budget = kMacSmemAlone, int grid = 0, const MaskArgs *c1m = nullptr, uint64_t *c1_masked = nullptr) {
+                int smem_budget = kMacSmemAlone, int grid = 0, const MaskArgs *c1m = nullptr, uint64_t *c1_masked = nullptr,
+                const uint64_t *ct_in = nullptr) {
   if (g.engine == 2) {
-    launch_mac_tc(c, W, X, out, g, smem_budget, grid > 0 ? grid : c->num_sms, st, c1m, c1_masked);
+    launch_mac_tc(c, W, X, out, g, smem_budget, grid > 0 ? grid : c->num_sms, st, c1m, c1_masked, ct_in);
     return;
   }
   MacArgs A;
@@ -1832,6 +1883,15 @@ bool c1_direct_ok(const hl_ctx *c, const MacGeom &g, const MaskArgs &M) {
 }
 inline bool c1_direct(const hl_ctx *c, const MacGeom &g, const MaskArgs &M) {
   return c->N == 4096 ? c1_direct_ok<12>(c, g, M) : c1_direct_ok<13>(c, g, M);
+}
+// May the MAC also READ c1 from the ciphertexts (MacGeom::c1_in)?  With the quad order (c1_direct)
+// a work item's slots are 4 consecutive natural points; the column groups must be pure c0 / pure c1
+// or a single group.  HELINEAR_C1_TMA=0 turns it off.
+inline bool c1_in_ok(const MacGeom &g, const MaskArgs &M, const uint64_t *ct_in) {
+  static const bool on = [] { const char *e = getenv("HELINEAR_C1_TMA"); return e ? atoi(e) != 0 : true; }();
+  if (!(on && M.c1_done && (g.nCg == 1 || M.nK % g.CW == 0))) return false;
+  CUtensorMap probe;                                    // the launch re-encodes the same map
+  return c1_tmap(&probe, ct_in, g.LN, M.nK, g.nJ, (int)std::min<int64_t>(g.CW, M.nK));
 }
 
 template <int LOGN, bool RR>
@@ -2020,12 +2080,14 @@ extern "C" int hl_he_matmul_share(const hl_ctx *c, hl_tile tile, const void *wca
   const int64_t nC = 2 * g.nK;
   MacGeom mg = mac_geom(c, g.nIs, g.nJ, nC);
   mg.cperm = mg.engine == 2;
-  fwd_ntt(c, ct_in, workspace, g.nJ * nC, &mg, st);
   MaskArgs M = mask_args(g, Ma, Nb, seed);
   M.cperm = mg.cperm;
   M.c1_done = c1_direct(c, mg, M);
+  mg.c1_in = c1_in_ok(mg, M, ct_in);
+  if (mg.c1_in && mg.nCg == 1) mg.xw = (int)g.nK;
+  fwd_ntt(c, ct_in, workspace, g.nJ * nC, &mg, st);
   launch_mac(c, (const uint2 *)wcache, (const uint32_t *)workspace, ct_out_ntt, mg, st, kMacSmemAlone, 0,
-             M.c1_done ? &M : nullptr, ct_masked);
+             M.c1_done ? &M : nullptr, ct_masked, ct_in);
   if (c->N == 4096) launch_inv_mask<12>(c, ct_out_ntt, ct_masked, share, M, g.nIs * g.nK, st);
   else launch_inv_mask<13>(c, ct_out_ntt, ct_masked, share, M, g.nIs * g.nK, st);
   return hl_cuda_check("hl_he_matmul_share: launch");
@@ -2060,6 +2122,8 @@ static int linear_batch_run(const hl_ctx *c, hl_tile tile, int n, const hl_linea
     E[i].M = mask_args(E[i].g, d[i].Ma, d[i].Nb, d[i].seed);
     E[i].M.cperm = E[i].mg.cperm;
     E[i].M.c1_done = c1_direct(c, E[i].mg, E[i].M);
+    E[i].mg.c1_in = c1_in_ok(E[i].mg, E[i].M, d[i].ct_in);
+    if (E[i].mg.c1_in && E[i].mg.nCg == 1) E[i].mg.xw = (int)E[i].g.nK;
   }
   cudaStream_t sc = (cudaStream_t)stream, s0 = (cudaStream_t)c->mac_stream, s1 = (cudaStream_t)c->aux_stream;
   std::vector<cudaEvent_t> ev(2 * n + 3);
@@ -2104,7 +2168,7 @@ static int linear_batch_run(const hl_ctx *c, hl_tile tile, int n, const hl_linea
       const int i = ord[k];
       fwd_ntt(c, d[i].ct_in, d[i].workspace, E[i].g.nJ * 2 * E[i].g.nK, &E[i].mg, sc);
       launch_mac(c, (const uint2 *)d[i].wcache, (const uint32_t *)d[i].workspace, d[i].ct_out_ntt, E[i].mg, sc,
-                 kMacSmemAlone, 0, E[i].M.c1_done ? &E[i].M : nullptr, d[i].ct_masked);
+                 kMacSmemAlone, 0, E[i].M.c1_done ? &E[i].M : nullptr, d[i].ct_masked, d[i].ct_in);
       if (c->N == 4096) launch_inv_mask<12>(c, d[i].ct_out_ntt, d[i].ct_masked, d[i].share, E[i].M, E[i].g.nIs * E[i].g.nK, sc);
       else launch_inv_mask<13>(c, d[i].ct_out_ntt, d[i].ct_masked, d[i].share, E[i].M, E[i].g.nIs * E[i].g.nK, sc);
     }
@@ -2136,7 +2200,7 @@ static int linear_batch_run(const hl_ctx *c, hl_tile tile, int n, const hl_linea
       return e ? atoi(e) : 0;
     }();
     launch_mac(c, (const uint2 *)d[i].wcache, (const uint32_t *)d[i].workspace, d[i].ct_out_ntt, E[i].mg, s0,
-               mac_smem, mac_grid, E[i].M.c1_done ? &E[i].M : nullptr, d[i].ct_masked);
+               mac_smem, mac_grid, E[i].M.c1_done ? &E[i].M : nullptr, d[i].ct_masked, d[i].ct_in);
     cudaEventRecord(e_mac[i], s0);
     if (!split && k + 1 < n) fwd(ord[k + 1]);                           // overlaps MAC(i)
     cudaStreamWaitEvent(s1, e_mac[i], 0);

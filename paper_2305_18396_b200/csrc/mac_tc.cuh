@@ -51,14 +51,16 @@ struct TcGeom {
 };
 
 // ring geometry for a launch: rt rows per I tile (balanced tiles, multiple of 8)
-struct TcRing { int nst, sbytes, z_off, stg_off, bar_off, smem; };
+struct TcRing { int nst, sbytes, c1_off, z_off, stg_off, bar_off, smem; };
 template <int CW>
-TcRing tc_ring(int rt, int smem_budget) {
+TcRing tc_ring(int rt, int smem_budget, int c1_bytes = 0) {
   using T = TcGeom<CW>;
   TcRing r;
   // the M = 128 MMA reads 128 rows of every plane (rows >= rt are don't-care): plane 6 starts at
-  // 192 rt, row 127 of its second K half ends 2048 + 16 rt later -> 208 rt + 2048 >= 224 rt bytes
-  r.sbytes = (T::A_OFF + 208 * rt + 2048 + 127) / 128 * 128;
+  // 192 rt, row 127 of its second K half ends 2048 + 16 rt later -> 208 rt + 2048 >= 224 rt bytes;
+  // then (MacTcArgs::c1_in) the c1 box of the stage
+  r.c1_off = (T::A_OFF + 208 * rt + 2048 + 127) / 128 * 128;
+  r.sbytes = r.c1_off + (c1_bytes + 127) / 128 * 128;
   const int stg = (rt * T::STG_STRIDE * 8 + 127) / 128 * 128;
   const int fixed = T::NZ * T::Z_BYTES + stg + T::BAR_BYTES;
   r.nst = std::max(2, std::min(T::MAX_NST, (std::min(smem_budget, T::SMEM_MAX) - fixed) / r.sbytes));
@@ -70,6 +72,9 @@ TcRing tc_ring(int rt, int smem_budget) {
 }
 
 struct MacTcArgs {
+  // c1 halves read straight from the ciphertexts (MacGeom::c1_in): 3-D tensor map over ct_in's c1
+  // (natural evaluation points of all primes, K, J); per stage a box {2 points, c1_cols, 32 J}
+  CUtensorMap c1map;
   const uint8_t *W;       // weight planes (encode_weights, engine 2 layout)
   const uint64_t *X;      // NTT-domain ct_in residues [nCg][LN][nJp][CW]
   uint64_t *out;          // [nIs][nC][LN] canonical residues
@@ -87,7 +92,25 @@ struct MacTcArgs {
   uint64_t *c1_out;
   int c1_nK, c1_mn, c1_lognt;
   int qperm;                  // quad order (load_ntt_domain_q): set with c1_out
+  int c1_in, c1_cols, c1_bytes;   // c1 from c1map (requires qperm): columns per c1 group, box bytes
 };
+
+// natural evaluation point (prime offset l N included) of the first slot of quad sq (quad order)
+__device__ __forceinline__ int tc_quad_k0(const MacTcArgs &A, int sq) {
+  const int pos = sq * 4, l = pos / A.N, rem = pos - l * A.N;
+  const int nt = 1 << A.c1_lognt, u = rem >> A.c1_lognt, tq = (rem & (nt - 1)) >> 2;
+  return l * A.N + (int)(__brev((unsigned)u) >> 28) * nt + (int)(__brev((unsigned)tq) >> (32 - A.c1_lognt));
+}
+// first c1 column of column group cg (CW columns; c1 columns are those >= nK), CW if none
+template <int CW>
+__device__ __forceinline__ int tc_c1_lo(const MacTcArgs &A, int cg) {
+  return A.c1_in ? max(0, min(CW, A.c1_nK - cg * CW)) : CW;
+}
+__device__ __forceinline__ void tma_load_3d(void *dst, const CUtensorMap *map, int x, int y, int z, uint64_t *bar) {
+  asm volatile("cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];"
+               ::"r"(smem_u32(dst)), "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(z), "r"(smem_u32(bar))
+               : "memory");
+}
 
 // slot of the si-th output of slot quad sq: consecutive slots, or (qperm) the quad order
 // u NT + t' + {0, 2, 1, 3}[si] NT/4 whose natural evaluation points are 4 consecutive k
@@ -205,7 +228,7 @@ template <int CW>
 // <= 80 registers for CW <= 8 (minBlocks 2): leaves room for NTT CTAs on the same SM when the
 // MAC of one matmul runs concurrently with the NTTs of its neighbours (hl_he_linear_batch)
 __global__ void __launch_bounds__(TcGeom<CW>::THREADS, (CW <= 8 ? 2 : 1))
-k_mac_tc(MacTcArgs A, DevParams P) {
+k_mac_tc(const __grid_constant__ MacTcArgs A, DevParams P) {
   using T = TcGeom<CW>;
   const int NST = A.ring.nst, SB = A.ring.sbytes;
   extern __shared__ __align__(128) unsigned char smem[];
@@ -275,16 +298,24 @@ k_mac_tc(MacTcArgs A, DevParams P) {
         const int rows = min(g.RT, g.nIp - g.RT * it.t);
         const uint32_t abytes = 224u * rows;
         const uint8_t *wt = A.W + (size_t)it.t * g.RT * g.LN * g.nJp * 7;
+        const int c1lo = tc_c1_lo<CW>(A, it.cg);
+        const bool xraw = c1lo > 0, xc1 = c1lo < CW;             // this group's c0 / c1 columns
+        const int kq0 = xc1 ? tc_quad_k0(A, it.sq) : 0;
+        const int K1 = xc1 ? it.cg * CW + c1lo - A.c1_nK : 0;     // first c1 column's K
+        const uint32_t rawb = 256u * g.xw;                        // 32 J x xw u64
+        const uint32_t tx = abytes + (xraw ? rawb : 0) + (xc1 ? A.c1_bytes : 0);
         for (int si = 0; si < T::SPI; si++) {
           const int s = tc_slot(A, it.sq, si);
           for (int kk = 0; kk < A.njc; kk++) {
             const int jc = A.jc0 + kk;
             mbar_wait_p(&empty[st], ph, A.prof ? &pw[0] : nullptr);
             unsigned char *dst = smem + st * SB;
-            mbar_expect_tx(&full[st], abytes + T::RAW_BYTES);
+            mbar_expect_tx(&full[st], tx);
             bulk_g2s_hint(dst + T::A_OFF, wt + ((size_t)s * g.nJc + jc) * abytes, abytes, &full[st], pol_w);
-            bulk_g2s(dst, A.X + (((size_t)it.cg * g.LN + s) * g.nJp + (size_t)jc * 32) * CW,
-                     T::RAW_BYTES, &full[st]);
+            if (xraw)
+              bulk_g2s(dst, A.X + (((size_t)it.cg * g.LN + s) * g.nJp + (size_t)jc * 32) * g.xw, rawb, &full[st]);
+            if (xc1)   // natural points k0 + (si & 2) .. +1 of the group's c1 columns, 32 J
+              tma_load_3d(dst + A.ring.c1_off, &A.c1map, kq0 + (si & 2), K1, jc * 32, &full[st]);
             if (++st == NST) { st = 0; ph ^= 1; }
           }
         }
@@ -350,12 +381,14 @@ k_mac_tc(MacTcArgs A, DevParams P) {
     for (uint32_t seq = 0;; seq++) {
       const int item = tc_next_item(ifull, iempty, itm, seq);
       if (item < 0) break;
+      const int c1lo = tc_c1_lo<CW>(A, tc_decode(g, item).cg);
       for (int si = 0; si < T::SPI; si++) {
         for (int kk = 0; kk < A.njc; kk++, zseq++) {
           const uint32_t zi = zseq % T::NZ, zph = (zseq / T::NZ) & 1;
           mbar_wait_p(&full[st], ph, (A.prof && ct == 0) ? &pw[4] : nullptr);
           mbar_wait(&zempty[zi], zph ^ 1);
           const uint64_t *raw = reinterpret_cast<const uint64_t *>(smem + st * SB);
+          const uint64_t *c1b = reinterpret_cast<const uint64_t *>(smem + st * SB + A.ring.c1_off) + (si & 1);
           unsigned char *z = zring + zi * T::Z_BYTES;
           for (int q = ct; q < ((A.ko & 2) ? 0 : CW * 8); q += 64) {
             const int c = q >> 3, h = (q >> 2) & 1, gq = q & 3;
@@ -363,7 +396,8 @@ k_mac_tc(MacTcArgs A, DevParams P) {
             uint32_t lo[4], hi[4];
 #pragma unroll
             for (int j = 0; j < 4; j++) {
-              const uint64_t x = raw[(j0 + j) * CW + c];
+              // c0 columns from the forward NTT's X chunk [J][CW]; c1 columns from the box [J][K][2]
+              const uint64_t x = c < c1lo ? raw[(j0 + j) * g.xw + c] : c1b[((j0 + j) * A.c1_cols + (c - c1lo)) * 2];
               lo[j] = (uint32_t)x; hi[j] = (uint32_t)(x >> 32);
             }
             uint32_t *zrow = reinterpret_cast<uint32_t *>(z + ((size_t)h * T::ZR + c) * 16) + gq;
