@@ -143,7 +143,7 @@ def run_ours(args, rank, world, local_rank):
     ctx = hl.Context(cfg.N, cfg.L, synth.T_BITS, device=local_rank)
     if args.plan:                        # every product at the planner's tile (configs without recorded tiles)
         tiles = [tuple(ctx.plan_tile(mm.Ma, mm.R, mm.Nb)) for mm in cfg.matmuls]
-    elif not args.tile and cfg.tiles:    # the bench's tiles are the library planner's choices (hl_plan_tile)
+    elif not args.tile and not args.tiles and cfg.tiles:    # the bench's tiles are the library planner's choices (hl_plan_tile)
         assert all(ctx.plan_tile(mm.Ma, mm.R, mm.Nb) == t for mm, t in zip(cfg.matmuls, tiles)), 'planner drift'
     shard = args.mode == "shard"
     # weak: every rank owns one independently seeded block, no data-path collective.
@@ -625,6 +625,8 @@ def oracle_baseline(cfg, tiles, itiles: int, ktiles: int = 0):
 
 def _tiles(cfg, args):
     """Per-product tiles: --tile for all, else the config's (synth: hl_plan_tile's choices for c2)."""
+    if getattr(args, "tiles", None):    # experiment: per-product tiles "m,r,n;m,r,n;..."
+        return [tuple(int(v) for v in t.split(",")) for t in args.tiles.split(";")]
     return [tuple(args.tile)] * len(cfg.matmuls) if args.tile else [cfg.tile_of(i) for i in range(len(cfg.matmuls))]
 
 
@@ -677,6 +679,7 @@ def main():
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--config", default="c2", choices=sorted(synth.CONFIGS))
     ap.add_argument("--tile", type=int, nargs=3, default=None)
+    ap.add_argument("--tiles", default=None, help='per-product tiles, e.g. "32,8,16;8,8,64;32,8,16;8,16,32"')
     ap.add_argument("--plan", action="store_true", help="every product at hl_plan_tile's tile")
     ap.add_argument("--cpu-itiles", type=int, default=2)
     ap.add_argument("--no-cpu-baseline", action="store_true")
