@@ -1832,7 +1832,10 @@ void launch_mac_tc(const hl_ctx *c, const void *W, const void *X, uint64_t *out,
 }
 
 constexpr int kMacSmemAlone = 232448;        // the MAC alone on the SM: the deepest ring that fits
-constexpr int kMacSmemShared = 155 * 1024;   // leaves room for one NTT CTA (~70 KB) beside the MAC (sweep: tools/gpu/ring_sweep*.sh)
+// the batch's MAC ring: since the c1 TMA path (c0-only forward kernels) the full ring wins again
+// (tools/gpu/ring_sweep3.sh: 155 KB, one forward CTA beside the MAC, 0.911 ms; 227 KB, the forward
+// NTTs fill the SMs between MAC launches and beside the inverse, 0.905 ms)
+constexpr int kMacSmemShared = 232448;
 
 void launch_mac(const hl_ctx *c, const uint2 *W, const uint32_t *X, uint64_t *out, const MacGeom &g, cudaStream_t st,
                 int smem_budget = kMacSmemAlone, int grid = 0, const MaskArgs *c1m = nullptr, uint64_t *c1_masked = nullptr,
