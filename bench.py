@@ -173,11 +173,17 @@ def run_ours(args, rank, world, local_rank):
         # allocation of the cache), so it is repeated and the second call timed
         del_wc = ctx.encode_weights(tile, dW, i0, i1)
         torch.cuda.synchronize()
-        del del_wc                    # its blocks return to torch's allocator cache for the timed call
-        t0 = time.perf_counter()
-        wc = ctx.encode_weights(tile, dW, i0, i1)
-        torch.cuda.synchronize()
-        t_enc += time.perf_counter() - t0
+        del del_wc                    # its blocks return to torch's allocator cache for the timed calls
+        best = None
+        for _ in range(3):            # best of 3 (host-side allocation jitter)
+            t0 = time.perf_counter()
+            wc = ctx.encode_weights(tile, dW, i0, i1)
+            torch.cuda.synchronize()
+            dt = time.perf_counter() - t0
+            best = dt if best is None else min(best, dt)
+            if _ < 2:
+                del wc
+        t_enc += best
         del dW
         mats.append(dict(mm=mm, tile=tile, lay=lay, wc=wc, ct=ct_dev, i0=i0, i1=i1, nI_full=nI_full, s_hat=s_hat, dX=dX,
                          ct_host=torch.from_numpy(ct_host.view(np.int64).reshape(-1)).pin_memory(),
