@@ -390,7 +390,12 @@ k_mac_tc(const __grid_constant__ MacTcArgs A, DevParams P) {
           const uint64_t *raw = reinterpret_cast<const uint64_t *>(smem + st * SB);
           const uint64_t *c1b = reinterpret_cast<const uint64_t *>(smem + st * SB + A.ring.c1_off) + (si & 1);
           unsigned char *z = zring + zi * T::Z_BYTES;
-          for (int q = ct; q < ((A.ko & 2) ? 0 : CW * 8); q += 64) {
+          // compile-time trip count (2 at CW = 16): the iterations' shared-memory loads overlap
+          constexpr int QIT = (CW * 8 + 63) / 64;
+#pragma unroll
+          for (int qi = 0; qi < QIT; qi++) {
+            const int q = ct + qi * 64;
+            if ((A.ko & 2) || q >= CW * 8) break;
             const int c = q >> 3, h = (q >> 2) & 1, gq = q & 3;
             const int j0 = h * 16 + gq * 4;
             uint32_t lo[4], hi[4];
