@@ -556,12 +556,13 @@ def run_ours(args, rank, world, local_rank):
         "vs_baseline": None, "dtype": "u64", "data": "synthetic",
         "config": {"workload": f"{cfg.name}: {cfg.note}", "N": cfg.N, "L": cfg.L, "t_bits": synth.T_BITS,
                    "tile": [list(t) for t in tiles],
-                   "tile_choice": ("--tile override" if args.tile else "per product, hl_plan_tile (DESIGN.md §5)"
+                   "tile_choice": ("--tile/--tiles override" if (args.tile or args.tiles) else "per product, hl_plan_tile (DESIGN.md §5)"
                                    if args.plan or cfg.tiles else "config default tile"),
                    "batch_order": [cfg.matmuls[i].name for i in order],
                    "matmuls": [[mm.Nb, mm.R, mm.Ma] for mm in cfg.matmuls],
                    "blocks_per_step_per_rank": 1, "compress": True,
-                   "l2": "inputs larger than L2: 3.6 GB NTT-domain weight cache + 352 MB ct_in per block",
+                   "l2": (f"inputs larger than L2: {sum(m['lay'].wcache_bytes for m in mats) / 1e9:.2f} GB NTT-domain "
+                          f"weight cache + {sum(m['ct'].numel() for m in mats) * 8 / 1e6:.0f} MB ct_in per block"),
                    "parallelism": (f"shard x{world} (I tiles of one block per rank, responses gathered to rank 0)"
                                    if shard else f"weak x{world} (one block per rank)")},
         "poly_products_per_s": (sum(m["nI_full"] * m["lay"].nJ * m["lay"].nK for m in mats) if shard
