@@ -210,7 +210,8 @@ def run_ours(args, rank, world, local_rank):
     order = list(cfg.batch_order) if cfg.batch_order else list(range(len(entries)))
     batch = [entries[i] for i in order]
     # e2e: PCIe-bound (the downloads start once the first product is done): experiment knob
-    e2e_order = [int(x) for x in os.environ["BENCH_E2E_ORDER"].split(",")] if os.environ.get("BENCH_E2E_ORDER") else order
+    e2e_order = ([int(x) for x in os.environ["BENCH_E2E_ORDER"].split(",")] if os.environ.get("BENCH_E2E_ORDER")
+                 else list(cfg.e2e_order) if cfg.e2e_order else order)
 
     def step():
         if shard:

@@ -42,6 +42,7 @@ class Config:
     note: str = ""
     tiles: tuple = ()    # per-product tiles (the library's hl_plan_tile choice); () = `tile` for all
     batch_order: tuple = ()   # bench submission order of the products to hl_he_linear_batch; () = as listed
+    e2e_order: tuple = ()     # the same for the end-to-end (host buffers, PCIe-bound) call; () = batch_order
 
     def tile_of(self, mi: int) -> tuple:
         return self.tiles[mi] if self.tiles else self.tile
@@ -66,7 +67,7 @@ CONFIGS = {
     # c2: BERT-base block, seq 128, hidden 768, FFN 3072  (the bench workload)
     "c2": Config("c2", 4096, 2, (16, 8, 32), _block(128, 768, 3072),
                  note="BERT-base-shaped encoder block, seq 128",
-                 tiles=((16, 8, 32), (8, 8, 64), (16, 8, 32), (4, 32, 32)), batch_order=(2, 0, 3, 1)),
+                 tiles=((16, 8, 32), (8, 8, 64), (16, 8, 32), (4, 32, 32)), batch_order=(3, 1, 2, 0), e2e_order=(2, 0, 3, 1)),
     # c3: 12 BERT-base blocks x 8 sequences (Nb = 8*128)
     "c3": Config("c3", 4096, 2, (16, 8, 32), _block(1024, 768, 3072), blocks=12,
                  note="12 BERT-base blocks, 8 sequences x 128 tokens"),
