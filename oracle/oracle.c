@@ -83,7 +83,14 @@ void or_prf_u64(uint64_t seed, uint32_t domain, uint64_t stream, uint64_t first,
   for (uint64_t i = 0; i < count; i++) out[i] = prf_word(seed, domain, stream, first + i);
 }
 
-enum { DOM_SK = 1, DOM_A = 2, DOM_E = 3, DOM_MASK = 4 };
+enum { DOM_SK = 1, DOM_A = 2, DOM_E = 3, DOM_MASK = 4, DOM_PUB = 10 };
+
+/* Reading C28 (the paper is silent on how the client draws its randomness,
+ * PAPER.md:99): the uniform polynomials a are public (they are c1), the errors e are not.  The
+ * A domain is therefore keyed by a PUBLIC seed derived one-way from the client's private
+ * encryption seed, a_seed = u64 word 0 of stream (seed, PUB = 10, 0); the E domain stays keyed by
+ * the private seed.  A seeded upload ships a_seed only, which does not determine e.           */
+uint64_t or_public_seed(uint64_t seed) { return prf_word(seed, DOM_PUB, 0, 0); }
 
 /* ------------------------------------------------------------------------------------
  * Samplers (O3, O4; readings C7, C8)
@@ -93,12 +100,13 @@ void or_keygen(uint32_t N, uint64_t seed, int8_t *sk) {
   for (uint32_t i = 0; i < N; i++) sk[i] = (int8_t)((int)(prf_word(seed, DOM_SK, 0, i) % 3) - 1);
 }
 
-/* uniform a_l[i] = (u64_A[2i] + 2^64 u64_A[2i+1]) mod p_l, stream g*L + l              (O4) */
-void or_sample_a(uint32_t N, uint64_t seed, uint64_t g, uint32_t l, uint32_t L, uint64_t p,
+/* uniform a_l[i] = (u64_A[2i] + 2^64 u64_A[2i+1]) mod p_l, stream g*L + l, keyed by the
+ * public seed a_seed (O4, reading C28)                                                      */
+void or_sample_a(uint32_t N, uint64_t a_seed, uint64_t g, uint32_t l, uint32_t L, uint64_t p,
                  uint64_t *a) {
   for (uint32_t i = 0; i < N; i++) {
-    uint64_t lo = prf_word(seed, DOM_A, g * L + l, 2ull * i);
-    uint64_t hi = prf_word(seed, DOM_A, g * L + l, 2ull * i + 1);
+    uint64_t lo = prf_word(a_seed, DOM_A, g * L + l, 2ull * i);
+    uint64_t hi = prf_word(a_seed, DOM_A, g * L + l, 2ull * i + 1);
     a[i] = (uint64_t)((((u128)hi << 64) | lo) % p);
   }
 }
@@ -220,14 +228,16 @@ static uint64_t signed_mod(int64_t v, uint64_t p) {
   return v >= 0 ? (uint64_t)v % p : (p - ((uint64_t)(-v)) % p) % p;
 }
 
-/* Secret-key BFV encryption of every pi_B tile (O4, reading C26):
- *   a_hat_l = PRF (or_sample_a, evaluation form),  a_l = INTT(a_hat_l)
+/* Secret-key BFV encryption of every pi_B tile (O4, readings C26, C28):
+ *   a_hat_l = PRF keyed by or_public_seed(seed) (or_sample_a, evaluation form),  a_l = INTT(a_hat_l),
+ *   e = CDT(PRF keyed by seed itself)
  *   c1 = a_hat_l (evaluation form),  c0 = -a_l * s + e + Delta_l * b   (mod p_l)             */
 void or_encrypt(uint32_t N, uint32_t L, const uint64_t *primes, const uint64_t *psis,
                 const uint64_t *delta_mod, uint32_t m, uint32_t r, uint32_t n, const uint64_t *X,
                 int64_t Nb, int64_t R, const int8_t *sk, uint64_t seed, const uint64_t *cdt, int ncdt,
                 uint64_t *ct_in) {
   int64_t nJ = (R + r - 1) / r, nK = (Nb + n - 1) / n;
+  const uint64_t a_seed = or_public_seed(seed);
 #pragma omp parallel for schedule(dynamic)
   for (int64_t g = 0; g < nJ * nK; g++) {
     int64_t J = g / nK, K = g % nK;
@@ -243,7 +253,7 @@ void or_encrypt(uint32_t N, uint32_t L, const uint64_t *primes, const uint64_t *
     or_sample_e(N, seed, (uint64_t)g, cdt, ncdt, e);
     for (uint32_t l = 0; l < L; l++) {
       uint64_t p = primes[l];
-      or_sample_a(N, seed, (uint64_t)g, l, L, p, a_hat);
+      or_sample_a(N, a_seed, (uint64_t)g, l, L, p, a_hat);
       or_intt(N, p, psis[l], a_hat, a);
       /* a * s, schoolbook over the ternary s */
       memset(pos, 0, sizeof(u128) * N); memset(neg, 0, sizeof(u128) * N);

@@ -15,6 +15,8 @@ SURVEY.md §8(c) C1-C21, restated in DESIGN.md §3.
 Parity status per function (DESIGN.md §3 lists the pins):
   params/primes/Delta      pinned (closed form, independent Miller-Rabin in tests)
   chacha20 / prf           pinned (cryptography's ChaCha20)
+  keygen / sample_a /      pinned (each stream recomputed from cryptography's ChaCha20 with the
+    sample_e / public_seed   formula of O3/O4/C28; chi-squared uniformity of a mod p_l)
   cdt_table                pinned (closed-form moments, monotonicity, tail)
   encode_A/B, decode_C     pinned (SPEC.md worked values; brute-force matmul)
   negacyclic products/NTT  pinned (special cases, schoolbook vs NTT vs numpy fold)
@@ -39,6 +41,7 @@ _LIB_PATH = os.path.join(_HERE, "liboracle.so")
 _SRC = os.path.join(_HERE, "oracle.c")
 
 DOM_SK, DOM_A, DOM_E, DOM_MASK = 1, 2, 3, 4   # PRF domains
+DOM_PUB = 10                                  # public-seed derivation (reading C28)
 SIGMA = 3.2                                   # error std (BASELINE.json)
 CDT_TAIL = 41                                 # support [-41, 41]  (reading C8)
 
@@ -67,6 +70,8 @@ def lib():
         L.or_prf_u64.argtypes = [ctypes.c_uint64, ctypes.c_uint32, ctypes.c_uint64, ctypes.c_uint64,
                                  ctypes.c_uint64, u64p]
         L.or_mask_word.restype = ctypes.c_uint64
+        L.or_public_seed.restype = ctypes.c_uint64
+        L.or_public_seed.argtypes = [ctypes.c_uint64]
         _lib = L
     return _lib
 
@@ -250,6 +255,20 @@ def keygen(P: Params, seed: int) -> np.ndarray:
     return sk
 
 
+def public_seed(seed: int) -> int:
+    """Reading C28: the public seed of the A domain, u64 word 0 of stream (seed, PUB, 0).  A seeded
+    upload (c1 regenerated by the server) ships this value, never `seed`, which keys the errors."""
+    return int(lib().or_public_seed(ctypes.c_uint64(seed)))
+
+
+def sample_a(P: Params, a_seed: int, g: int, l: int) -> np.ndarray:
+    """O4: a_hat_l[i] = (u64_A[2i] + 2^64 u64_A[2i+1]) mod p_l, stream g*L + l, key a_seed (C28)."""
+    a = np.zeros(P.N, dtype=np.uint64)
+    lib().or_sample_a(ctypes.c_uint32(P.N), ctypes.c_uint64(a_seed), ctypes.c_uint64(g), ctypes.c_uint32(l),
+                      ctypes.c_uint32(P.L), ctypes.c_uint64(P.primes[l]), _p(a))
+    return a
+
+
 def sample_e(P: Params, seed: int, g: int) -> np.ndarray:
     T = _u64arr(cdt_table())
     e = np.zeros(P.N, dtype=np.int64)
@@ -292,7 +311,8 @@ def negacyclic_mul_ntt(N: int, p: int, psi: int, a, b) -> np.ndarray:
 
 
 def encrypt(P: Params, tile, sk: np.ndarray, X: np.ndarray, seed: int) -> np.ndarray:
-    """O4: pi_B tiles of X^T, secret-key BFV: c1 = a, c0 = -a*s + e + Delta*b (mod p_l).
+    """O4: pi_B tiles of X^T, secret-key BFV: c1 = a, c0 = -a*s + e + Delta*b (mod p_l); a keyed by
+    public_seed(seed), e by seed (reading C28).
     Returns ct_in uint64 [nJ][nK][2][L][N]."""
     m, r, n = tile
     Nb, R = X.shape

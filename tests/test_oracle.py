@@ -215,6 +215,86 @@ def test_keygen_ternary_and_balanced(P4096):
     assert np.array_equal(sk, ref.keygen(P4096, 7))   # deterministic per seed
 
 
+def test_keygen_is_the_sk_stream(P4096, P8192):
+    """O3 recomputed from the library ChaCha20: s_i = (u64_SK[i] mod 3) - 1, stream (seed, 1, 0)."""
+    for P, seed in ((P4096, 7), (P8192, 2**64 - 3)):
+        u = _lib_chacha_u64(seed, 1, 0, P.N)
+        assert np.array_equal(ref.keygen(P, seed), ((u % np.uint64(3)).astype(np.int64) - 1).astype(np.int8))
+
+
+def test_public_seed_is_the_pub_stream_and_hides_the_error_key():
+    """Reading C28: a_seed = word 0 of the library ChaCha20 stream (seed, 10, 0); distinct seeds give
+    distinct public seeds, and the public seed is not the private one."""
+    seeds = [0, 1, 5, 0x230518396 + 3, 2**64 - 1]
+    pubs = [ref.public_seed(s) for s in seeds]
+    for s, a in zip(seeds, pubs):
+        assert a == int(_lib_chacha_u64(s, 10, 0, 1)[0]) and a != s
+    assert len(set(pubs)) == len(pubs)
+
+
+@pytest.mark.parametrize("NL", [(4096, 2), (8192, 3)])
+def test_encrypt_c1_is_the_a_stream(NL, P4096, P8192):
+    """O4 + C26 + C28 recomputed from the library ChaCha20: the c1 half of input ciphertext g for
+    prime l is a_hat[i] = (u[2i] + 2^64 u[2i+1]) mod p_l over stream (public_seed(seed), 2, g*L + l),
+    computed with Python integers.  A short word (u[2i] alone), a wrong stream index or the private
+    seed as key would all fail."""
+    P = P4096 if NL[0] == 4096 else P8192
+    tile = (16, 32, 8) if P.N == 4096 else (32, 16, 16)
+    X = synth.activations(41, 2 * tile[2], 2 * tile[1])        # nJ = nK = 2: g = 0..3
+    seed = 0x5EED
+    ct = ref.encrypt(P, tile, ref.keygen(P, 1), X, seed)
+    a_seed = int(_lib_chacha_u64(seed, 10, 0, 1)[0])
+    for J in range(2):
+        for K in range(2):
+            g = J * 2 + K
+            for l, p in enumerate(P.primes):
+                u = _lib_chacha_u64(a_seed, 2, g * P.L + l, 2 * P.N)
+                want = [(int(u[2 * i]) + (int(u[2 * i + 1]) << 64)) % p for i in range(P.N)]
+                assert [int(v) for v in ct[J, K, 1, l]] == want
+                assert np.array_equal(ref.sample_a(P, a_seed, g, l), np.array(want, dtype=np.uint64))
+
+
+def test_sample_a_uniform_chi_squared(P4096):
+    """a mod p_l is uniform on [0, p_l): 64 equal-width buckets, chi^2_63 < 103.4 (p = 0.001), and
+    the top bit of the 50-bit residues is set about (p - 2^49)/p of the time (a 64-bit or 32-bit
+    reduction would skew both)."""
+    for l, p in enumerate(P4096.primes):
+        a = np.concatenate([ref.sample_a(P4096, 77, g, l) for g in range(8)]).astype(object)
+        assert max(a) < p
+        counts = np.bincount(np.array([(int(v) * 64) // p for v in a], dtype=np.int64), minlength=64)
+        exp = len(a) / 64
+        assert ((counts - exp) ** 2 / exp).sum() < 103.4
+        top = sum(1 for v in a if int(v) >= (1 << 49)) / len(a)
+        assert abs(top - (p - (1 << 49)) / p) < 0.02
+
+
+def test_sample_e_is_the_error_stream(P4096):
+    """O4 + C8 recomputed: e[i] = sign(u) * min{k : (u & (2^63-1)) < T[k]} over the library ChaCha20
+    stream (seed, 3, g) keyed by the PRIVATE seed (C28); T is the closed-form-pinned CDT table."""
+    T = np.array(ref.cdt_table(), dtype=np.uint64)
+    for seed, g in ((99, 0), (99, 17), (2**63 + 5, 3)):
+        u = _lib_chacha_u64(seed, 3, g, P4096.N)
+        mag = np.array([int(np.searchsorted(T, v & np.uint64((1 << 63) - 1), side="right")) for v in u])
+        want = np.where((u >> np.uint64(63)) != 0, -mag, mag)
+        assert np.array_equal(ref.sample_e(P4096, seed, g), want)
+    # the encryption noise is that stream: fresh ct decrypts to Delta*b + e exactly (below)
+
+
+def test_psi_matches_appendix_a(P4096, P8192):
+    """psi_l = g_l^((p_l - 1)/2N) with g_l the SMALLEST primitive root (reading C26).  The N=4096
+    values are the ones SURVEY.md Appendix A prints; g_l itself is re-derived here from the
+    factorisation of p - 1 (g is a primitive root iff g^((p-1)/f) != 1 for every prime f | p-1) and
+    no smaller g qualifies."""
+    import sympy
+    assert P4096.psis == (990116967873799, 702736788773885)
+    for P, gens in ((P4096, (22, 10)), (P8192, (22, 10, 7))):
+        for p, psi, g in zip(P.primes, P.psis, gens):
+            fs = list(sympy.factorint(p - 1))
+            is_gen = lambda x: all(pow(x, (p - 1) // f, p) != 1 for f in fs)
+            assert is_gen(g) and not any(is_gen(x) for x in range(2, g))
+            assert psi == pow(g, (p - 1) // (2 * P.N), p)
+
+
 def test_encrypt_decrypt_roundtrip_exact_noise(P4096):
     """Fresh ct: c0 + c1*s = Delta*b + e exactly, so Dec = pi_B(X tile) and the measured
     noise equals the sampled error polynomial e (reading C8)."""
