@@ -188,7 +188,7 @@ def run_ours(args, rank, world, local_rank):
         mats.append(dict(mm=mm, tile=tile, lay=lay, wc=wc, ct=ct_dev, i0=i0, i1=i1, nI_full=nI_full, s_hat=s_hat, dX=dX,
                          ct_host=torch.from_numpy(ct_host.view(np.int64).reshape(-1)).pin_memory(),
                          c0_host=torch.from_numpy(hl.Context.c0_halves(ct_host.reshape(lay.nJ, lay.nK, 2, -1)).view(np.int64).reshape(-1)).pin_memory(),
-                         enc_seed=synth.seed_for(block, mi, "enc"),
+                         a_seed=hl.public_seed(synth.seed_for(block, mi, "enc")),   # reading C28
                          seed=synth.seed_for(block, mi, "mask")))
     ws_words = max(m["lay"].workspace_bytes // 8 for m in mats)
     out_words = max(m["lay"].ct_out_words for m in mats)
@@ -450,12 +450,14 @@ def run_ours(args, rank, world, local_rank):
     host_share = [torch.empty(m["lay"].share_words, dtype=torch.int64).pin_memory() for m in mats]
     dev_ct_in = torch.empty(max(m["lay"].ct_in_words for m in mats), dtype=torch.int64, device=dev)
 
-    # weak mode: the pipelined seeded batch (hl_he_linear_batch_host): c0 halves + encryption seeds
+    # weak mode: the pipelined seeded batch (hl_he_linear_batch_host): c0 halves + public seeds
     # up, c1 regenerated on the device, compressed responses + shares down, overlapped per product
     up_bufs = [torch.empty(m["lay"].ct_in_words, dtype=torch.int64, device=dev) for m in mats] if not shard else []
     c0_up = [torch.from_numpy(hl.Context.pack50(m["c0_host"].numpy().view(np.uint64)).view(np.int64)).pin_memory()
              if packed else m["c0_host"] for m in mats]
-    host_entries = [dict(e, ct_in=u, c0_host=c0, enc_seed=m["enc_seed"], masked_host=hm, share_host=hs, packed=packed)
+    # own device output buffers: the check below compares the e2e results with the device batch's
+    host_entries = [dict(e, ct_in=u, c0_host=c0, a_seed=m["a_seed"], masked_host=hm, share_host=hs, packed=packed,
+                         ct_masked=torch.empty_like(m["masked"]), share=torch.zeros_like(m["share"]))
                     for e, m, u, c0, hm, hs in zip(entries, mats, up_bufs, c0_up, host_masked, host_share)]
 
     def e2e_step():

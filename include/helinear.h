@@ -40,7 +40,9 @@
  * Randomness (reading C10): a ChaCha20 PRF (RFC 8439 block function), key = LE64(seed) || 0^24,
  * nonce = LE32(domain) || LE64(stream), block counter from 0; u64 word i = LE64(keystream[8i, 8i+8)).
  * Domains: 1 secret key (stream 0), 2 uniform a_hat (stream g*L + l), 3 error (stream g),
- * 4 mask (stream I*nK + K, I global).  g = J*nK + K.
+ * 4 mask (stream I*nK + K, I global).  g = J*nK + K.  Reading C28: domain 2 (the public a_hat = c1)
+ * is keyed by the PUBLIC seed hl_public_seed(seed) = word 0 of stream (seed, domain 10, 0); domain 3
+ * (the errors) by the client's private encryption seed itself, which never leaves the client.
  *
  * Ownership: the caller allocates and owns every buffer (host or device as stated per call).
  * The library owns only the context: parameters, per-prime constants and twiddle tables
@@ -134,12 +136,17 @@ int hl_layout_query(const hl_ctx *ctx, hl_tile tile, int64_t Ma, int64_t R, int6
 
 /* ---- client side (host memory; the boundary of the server path) ------------------------- */
 
+/* Reading C28: the public seed of the A domain derived one-way from the private encryption seed
+ * (u64 word 0 of the ChaCha20 stream (enc_seed, domain 10, stream 0)).  The seeded upload ships it. */
+uint64_t hl_public_seed(uint64_t enc_seed);
+
 /* Secret key s_i = (u64_SK[i] mod 3) - 1 (reading C7).  sk: host int8[N]. */
 int hl_keygen(const hl_ctx *ctx, uint64_t seed, int8_t *sk);
 
 /* Alg. 1 step 2: encode every tile with pi_B and encrypt with the secret key:
- *   c1 = a_hat_l (evaluation form, PRF domain 2), c0 = -a_l*s + e + Delta_l*b (mod p_l) with
- *   a_l = INTT(a_hat_l), e discrete Gaussian sigma=3.2 (CDT, reading C8).  X: host [Nb][R]; ct_in: host [nJ][nK][2][L][N] (layout.ct_in_words).
+ *   c1 = a_hat_l (evaluation form, PRF domain 2 keyed by hl_public_seed(seed)),
+ *   c0 = -a_l*s + e + Delta_l*b (mod p_l) with
+ *   a_l = INTT(a_hat_l), e discrete Gaussian sigma=3.2 (CDT, reading C8; domain 3 keyed by seed).  X: host [Nb][R]; ct_in: host [nJ][nK][2][L][N] (layout.ct_in_words).
  * Errors: HL_ERANGE if some X >= 2^log2_t or sk is not ternary. */
 int hl_encrypt(const hl_ctx *ctx, const int8_t *sk, hl_tile tile, const uint64_t *X, int64_t Nb,
                int64_t R, uint64_t seed, uint64_t *ct_in);
@@ -278,13 +285,15 @@ int hl_he_linear_host(const hl_ctx *ctx, hl_tile tile, const void *wcache, int64
 
 /* ---- Seeded ciphertext upload ------------------------------------ */
 
-/* The c1 half of every input ciphertext is a_hat = PRF(enc_seed, A, g*L + l) reduced mod p_l
- * (readings C10, C26; the same stream hl_encrypt / hl_encrypt_device draw), i.e. public randomness the client
- * need not send: it uploads the c0 halves and the seed, and the server regenerates c1.
+/* The c1 half of every input ciphertext is a_hat = PRF(a_seed, A, g*L + l) reduced mod p_l with
+ * a_seed = hl_public_seed(enc_seed) (readings C10, C26, C28; the same stream hl_encrypt /
+ * hl_encrypt_device draw), i.e. public randomness the client need not send: it uploads the c0 halves
+ * and a_seed, and the server regenerates c1.  a_seed does not determine the error stream (keyed by
+ * the private enc_seed), so the server learns nothing it could not read from the full ciphertext.
  * hl_expand_seeded writes the c1 halves of ct_in (device [nJ][nK][2][L][N] for (R, Nb)),
  * leaving the c0 halves untouched; the result is bit-identical to the client's ciphertext.
  * Stream-ordered; errors: HL_EINVAL (bad tile / sizes / null). */
-int hl_expand_seeded(const hl_ctx *ctx, hl_tile tile, int64_t R, int64_t Nb, uint64_t enc_seed,
+int hl_expand_seeded(const hl_ctx *ctx, hl_tile tile, int64_t R, int64_t Nb, uint64_t a_seed,
                      uint64_t *ct_in, void *stream);
 
 /* One entry of hl_he_linear_batch_host: the device buffers of a hl_he_linear_batch entry
@@ -292,7 +301,7 @@ int hl_expand_seeded(const hl_ctx *ctx, hl_tile tile, int64_t R, int64_t Nb, uin
 typedef struct {
   hl_linear_desc dev;
   const uint64_t *c0_host;    /* pinned host [nJ][nK][L][N]: the c0 halves of the input ciphertexts */
-  uint64_t enc_seed;          /* the client's encryption seed (c1 regenerated on the device)       */
+  uint64_t a_seed;            /* hl_public_seed(client's encryption seed): c1 regenerated on device */
   uint64_t *ct_masked_host;   /* pinned host, layout.ct_masked_words (compressed response)         */
   uint64_t *share_host;       /* pinned host [Nb][Ma] server share                                 */
   int32_t packed;             /* 1: 50-bit wire format (hl_pack50) for c0_host and ct_masked_host  */
@@ -308,7 +317,7 @@ int hl_unpack50(const uint64_t *in, int64_t words, uint64_t *out);
 
 /* The end-to-end form of hl_he_linear_batch (bench.py's e2e leg): for every entry, the c0 halves
  * are copied host->device (strided into dev.ct_in; packed = 1: the 50-bit stream of the c0 halves,
- * unpacked on the device through dev.workspace) and c1 is expanded from enc_seed, the product
+ * unpacked on the device through dev.workspace) and c1 is expanded from a_seed, the product
  * runs as in hl_he_linear_batch, and the compressed response + share are copied back to the host
  * buffers (packed = 1: the response in the 50-bit format, packed on the device through
  * dev.ct_out_ntt, hl_packed50_words(layout.ct_masked_words) words; the share stays u64).  The

@@ -35,7 +35,7 @@ EXPORTS = ("hl_last_error", "hl_ctx_create", "hl_ctx_destroy", "hl_ctx_params", 
            "hl_fc_local_share", "hl_encode_weights_strided", "hl_encode_weights_scratch", "hl_share_accumulate", "hl_sk_prepare",
            "hl_encrypt_device", "hl_decrypt_share_device", "hl_pk_gen", "hl_pk_prepare", "hl_he_matmul_share_rr",
            "hl_expand_seeded", "hl_he_linear_batch_host", "hl_packed50_words", "hl_pack50", "hl_unpack50",
-           "hl_timing_kernels")
+           "hl_timing_kernels", "hl_public_seed")
 KERNELS = ("ntt_fwd", "mac", "intt_mask", "intt", "mask", "encode", "other", "fc")   # HL_K_* order
 
 
@@ -68,7 +68,7 @@ class LinearDesc(ctypes.Structure):
 
 class LinearHostDesc(ctypes.Structure):
     """hl_linear_host_desc: one product of hl_he_linear_batch_host (device + pinned host pointers)."""
-    _fields_ = [("dev", LinearDesc), ("c0_host", ctypes.c_void_p), ("enc_seed", ctypes.c_uint64),
+    _fields_ = [("dev", LinearDesc), ("c0_host", ctypes.c_void_p), ("a_seed", ctypes.c_uint64),
                 ("ct_masked_host", ctypes.c_void_p), ("share_host", ctypes.c_void_p), ("packed", ctypes.c_int32)]
 
 
@@ -109,6 +109,7 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
         "hl_layout_query": [vp, Tile, i64, i64, i64, i64, i64, ctypes.POINTER(_Layout)],
         "hl_plan_tile": [vp, i64, i64, i64, ctypes.POINTER(Tile)],
         "hl_keygen": [vp, u64, vp],
+        "hl_public_seed": [u64],
         "hl_encrypt": [vp, vp, Tile, vp, i64, i64, u64, vp],
         "hl_decrypt_share": [vp, vp, Tile, vp, i32, i64, i64, vp],
         "hl_encode_weights": [vp, Tile, vp, i64, i64, i64, i64, vp, vp],
@@ -149,6 +150,7 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
         f.restype = ctypes.c_int
     L.hl_packed50_words.argtypes = [i64]
     L.hl_packed50_words.restype = i64
+    L.hl_public_seed.restype = u64
     _lib = L
     return L
 
@@ -427,23 +429,24 @@ class Context:
         keep += [ws, co]
         outs.append((cm, sh))
 
-    def expand_seeded(self, tile, R: int, Nb: int, enc_seed: int, ct_in, stream=None):
+    def expand_seeded(self, tile, R: int, Nb: int, a_seed: int, ct_in, stream=None):
         """hl_expand_seeded: regenerate the c1 = a halves of ct_in (CUDA int64 [nJ][nK][2][L][N])
-        from the client's encryption seed."""
-        _check(_lib.hl_expand_seeded(self._h, _tile(tile), R, Nb, enc_seed, _dptr(ct_in), _stream(stream)))
+        from the client's PUBLIC seed a_seed = public_seed(enc_seed) (reading C28)."""
+        _check(_lib.hl_expand_seeded(self._h, _tile(tile), R, Nb, a_seed, _dptr(ct_in), _stream(stream)))
         return ct_in
 
     def he_linear_batch_host(self, tile, entries, stream=None):
         """End-to-end pipelined batch on pinned host buffers (hl_he_linear_batch_host).  entries:
         the he_linear_batch dicts (ct_in = the device upload buffer, distinct per entry) plus
-        c0_host (pinned CPU int64 [nJ][nK][L][N], see c0_halves), enc_seed, masked_host and
+        c0_host (pinned CPU int64 [nJ][nK][L][N], see c0_halves), a_seed (= public_seed(enc seed),
+        reading C28: the private encryption seed never crosses the boundary), masked_host and
         share_host (pinned CPU int64), and optionally packed=True (c0_host and masked_host in the
         50-bit wire format of pack50).  Stream-ordered: synchronise before reading the host outputs."""
         descs = (LinearHostDesc * len(entries))()
         keep, outs = [], []
         for d, e in zip(descs, entries):
             self._fill_desc(tile, d.dev, e, keep, outs)
-            d.c0_host, d.enc_seed = e["c0_host"].data_ptr(), int(e["enc_seed"])
+            d.c0_host, d.a_seed = e["c0_host"].data_ptr(), int(e["a_seed"])
             d.packed = int(bool(e.get("packed", False)))
             d.ct_masked_host, d.share_host = e["masked_host"].data_ptr(), e["share_host"].data_ptr()
             keep += [e["c0_host"], e["masked_host"], e["share_host"]] + [o for o in outs[-1]]
@@ -540,6 +543,11 @@ class Context:
             scratch = _dev_empty(x.numel(), x.device)
         _check(_lib.hl_ntt_roundtrip(self._h, _dptr(x), npoly, _dptr(scratch), _stream(stream)))
         return x
+
+
+def public_seed(enc_seed: int) -> int:
+    """hl_public_seed (reading C28): the public A-domain seed of a private encryption seed."""
+    return int(load_library().hl_public_seed(enc_seed))
 
 
 def to_device(a: np.ndarray, device="cuda"):

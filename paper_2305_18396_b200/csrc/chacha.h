@@ -12,7 +12,8 @@
 namespace hl {
 
 enum : uint32_t { kDomSK = 1, kDomA = 2, kDomE = 3, kDomMask = 4,
-                  kDomPkA = 5, kDomPkE = 6, kDomRrU = 7, kDomRrE = 8, kDomRrF = 9 };   // 5-9: row f4 (reading C22)
+                  kDomPkA = 5, kDomPkE = 6, kDomRrU = 7, kDomRrE = 8, kDomRrF = 9,   // 5-9: row f4 (reading C22)
+                  kDomPub = 10 };                                                     // reading C28
 
 HL_HD uint32_t rotl(uint32_t x, int n) {
 #ifdef __CUDA_ARCH__
@@ -63,6 +64,14 @@ HL_HD uint64_t prf_u64(uint64_t seed, uint32_t domain, uint64_t stream, uint64_t
 #pragma unroll
   for (int i = 1; i < 8; i++) r = ((idx & 7) == (uint64_t)i) ? w[i] : r;
   return r;
+}
+
+// Reading C28: the A domain (the public c1 = a_hat) is keyed by a public seed derived one-way from
+// the client's private encryption seed; the E domain (the errors) by the private seed itself.
+HL_HD uint64_t public_seed(uint64_t enc_seed) {
+  uint64_t w[8];
+  chacha_block_u64(enc_seed, kDomPub, 0, 0, w);
+  return w[0];
 }
 
 }  // namespace hl

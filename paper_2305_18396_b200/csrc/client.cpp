@@ -52,6 +52,8 @@ extern "C" int hl_unpack50(const uint64_t *in, int64_t words, uint64_t *out) {
   return HL_OK;
 }
 
+extern "C" uint64_t hl_public_seed(uint64_t enc_seed) { return hl::public_seed(enc_seed); }
+
 extern "C" int hl_keygen(const hl_ctx *c, uint64_t seed, int8_t *sk) {
   if (!c || !sk) return hl_fail(HL_EINVAL, "hl_keygen: NULL argument");
   // s_i = (u64_SK[i] mod 3) - 1  (reading C7); one ChaCha block serves 8 coefficients
@@ -95,6 +97,7 @@ extern "C" int hl_encrypt(const hl_ctx *c, const int8_t *sk, hl_tile tile, const
   std::vector<uint64_t> shat;
   sk_ntt(c, sk, shat);
   const int64_t nct = g.nJ * g.nK;
+  const uint64_t a_seed = hl::public_seed(seed);     // reading C28: a is keyed by the public seed
 #pragma omp parallel
   {
     std::vector<uint64_t> b(N), a(N), as(N);
@@ -122,11 +125,11 @@ extern "C" int hl_encrypt(const hl_ctx *c, const int8_t *sk, hl_tile tile, const
       }
       for (uint32_t l = 0; l < L; l++) {
         const uint64_t p = c->primes[l];
-        // a_hat_l[k] = (u[2k] + 2^64 u[2k+1]) mod p, stream (A, g*L + l): the evaluation form of
+        // a_hat_l[k] = (u[2k] + 2^64 u[2k+1]) mod p, stream (a_seed, A, g*L + l): the evaluation form of
         // a (reading C26), natural order k; it is c1 as sent
         for (uint32_t blk = 0; blk < N / 4; blk++) {
           uint64_t w[8];
-          hl::chacha_block_u64(seed, hl::kDomA, (uint64_t)gi * L + l, blk, w);
+          hl::chacha_block_u64(a_seed, hl::kDomA, (uint64_t)gi * L + l, blk, w);
           for (int i = 0; i < 4; i++)
             a[4 * blk + i] = (uint64_t)((((hl_u128)w[2 * i + 1] << 64) | w[2 * i]) % p);
         }

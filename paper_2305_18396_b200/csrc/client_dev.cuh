@@ -20,7 +20,8 @@ struct EncArgs {
   const uint64_t *X;            // [Nb][R] < 2^t
   int64_t Nb, R, nK;
   int m, r, n, lm, lr;
-  uint64_t seed;
+  uint64_t seed;                // private encryption seed: keys the errors (domain E)
+  uint64_t a_seed;              // hl::public_seed(seed): keys the public a_hat (domain A, reading C28)
   const uint64_t *s_hat;        // [L][N] NTT(s) in slot order (hl_sk_prepare)
 };
 
@@ -64,7 +65,7 @@ k_encrypt(EncArgs E, uint64_t *__restrict__ ct, DevParams P, const uint64_t *__r
 #pragma unroll 1
     for (int blk = t; blk < Gm::N / 4; blk += Gm::NT) {
       uint64_t w[8];
-      hl::chacha_block_u64(E.seed, hl::kDomA, (uint64_t)gi * L + l, (uint32_t)blk, w);
+      hl::chacha_block_u64(E.a_seed, hl::kDomA, (uint64_t)gi * L + l, (uint32_t)blk, w);
 #pragma unroll
       for (int i = 0; i < 4; i++) {
         const uint64_t a = mod_u128(w[2 * i + 1], w[2 * i], pc);
@@ -172,10 +173,10 @@ k_decrypt(const uint64_t *__restrict__ masked, uint64_t *__restrict__ share, Dec
 }
 
 // Seeded ciphertext upload (hl_expand_seeded): c1 = a_hat_l (evaluation form, C26) of every input ciphertext regenerated from
-// the client's encryption seed -- the same PRF stream (A, g*L + l) and the same reduction as
+// the client's PUBLIC seed a_seed = hl::public_seed(enc_seed) (reading C28; the private seed never reaches the server) -- the same PRF stream (A, g*L + l) and the same reduction as
 // k_encrypt / the host client / the oracle (reading C10), so the expanded ciphertext is
 // bit-identical to the one the client encrypted.  One thread per ChaCha block (4 coefficients).
-__global__ void k_expand_a(uint64_t *__restrict__ ct, int64_t nct, int logn, uint64_t seed, DevParams P) {
+__global__ void k_expand_a(uint64_t *__restrict__ ct, int64_t nct, int logn, uint64_t a_seed, DevParams P) {
   const int L = P.L, N = 1 << logn;
   const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int64_t per = (int64_t)L * (N / 4);
@@ -184,7 +185,7 @@ __global__ void k_expand_a(uint64_t *__restrict__ ct, int64_t nct, int logn, uin
   const int l = (int)((tid % per) / (N / 4)), blk = (int)(tid % (N / 4));
   const PrimeConsts pc = pick(P, l);
   uint64_t w[8];
-  hl::chacha_block_u64(seed, hl::kDomA, (uint64_t)gi * L + l, (uint32_t)blk, w);
+  hl::chacha_block_u64(a_seed, hl::kDomA, (uint64_t)gi * L + l, (uint32_t)blk, w);
   uint64_t a[4];
 #pragma unroll
   for (int i = 0; i < 4; i++) a[i] = mod_u128(w[2 * i + 1], w[2 * i], pc);

@@ -2109,7 +2109,7 @@ extern "C" int hl_he_matmul_share(const hl_ctx *c, hl_tile tile, const void *wca
 // expand_seed (optional, with ready): per entry, the c1 halves are regenerated from this seed on the
 // forward stream before the forward NTT, and every forward NTT is issued up front on the context's
 // upload-side NTT stream so that no entry's inverse NTT queues behind a later entry's upload.
-static void expand_seeded(const hl_ctx *c, int64_t nct, uint64_t enc_seed, uint64_t *ct_in, cudaStream_t st);
+static void expand_seeded(const hl_ctx *c, int64_t nct, uint64_t a_seed, uint64_t *ct_in, cudaStream_t st);
 static int linear_batch_run(const hl_ctx *c, hl_tile tile, int n, const hl_linear_desc *d, void *stream,
                             const cudaEvent_t *ready, const cudaEvent_t *done, const uint64_t *expand_seed) {
   int rc;
@@ -2230,19 +2230,19 @@ extern "C" int hl_he_linear_batch(const hl_ctx *c, hl_tile tile, int n, const hl
 // Seeded ciphertext upload: c1 = a is PRF output of the client's
 // encryption seed (reading C10), so only c0 crosses PCIe and the device regenerates c1.
 // ---------------------------------------------------------------------------------------
-static void expand_seeded(const hl_ctx *c, int64_t nct, uint64_t enc_seed, uint64_t *ct_in, cudaStream_t st) {
+static void expand_seeded(const hl_ctx *c, int64_t nct, uint64_t a_seed, uint64_t *ct_in, cudaStream_t st) {
   const int64_t nth = nct * c->L * (c->N / 4);
   KTimer kt(c, HL_K_OTHER, st);
-  k_expand_a<<<(unsigned)((nth + 255) / 256), 256, 0, st>>>(ct_in, nct, __builtin_ctz((unsigned)c->N), enc_seed, c->dp);
+  k_expand_a<<<(unsigned)((nth + 255) / 256), 256, 0, st>>>(ct_in, nct, __builtin_ctz((unsigned)c->N), a_seed, c->dp);
 }
 
-extern "C" int hl_expand_seeded(const hl_ctx *c, hl_tile tile, int64_t R, int64_t Nb, uint64_t enc_seed,
+extern "C" int hl_expand_seeded(const hl_ctx *c, hl_tile tile, int64_t R, int64_t Nb, uint64_t a_seed,
                                 uint64_t *ct_in, void *stream) {
   int rc;
   if ((rc = check_ptrs({c, ct_in}, "hl_expand_seeded"))) return rc;
   Geo g;
   if ((rc = hl_geometry(c, tile, 1, R, Nb, 0, -1, &g))) return rc;
-  expand_seeded(c, g.nJ * g.nK, enc_seed, ct_in, (cudaStream_t)stream);
+  expand_seeded(c, g.nJ * g.nK, a_seed, ct_in, (cudaStream_t)stream);
   return hl_cuda_check("hl_expand_seeded: launch");
 }
 
@@ -2319,7 +2319,7 @@ extern "C" int hl_he_linear_batch_host(const hl_ctx *c, hl_tile tile, int n, con
       return hl_cuda_check("hl_he_linear_batch_host: H2D");
     }
     cudaEventRecord(e_up[i], su);
-    seeds[i] = h[i].enc_seed;
+    seeds[i] = h[i].a_seed;
   }
   if ((rc = linear_batch_run(c, tile, n, d.data(), stream, e_up, e_res, seeds.data()))) return rc;
   for (int i = 0; i < n; i++) {
@@ -2371,7 +2371,7 @@ extern "C" int hl_encrypt_device(const hl_ctx *c, const uint64_t *s_hat, hl_tile
   if ((rc = hl_geometry(c, tile, 1, R, Nb, 0, -1, &g))) return rc;
   cudaStream_t st = (cudaStream_t)stream;
   cudaMemsetAsync(c->d_flags, 0, 8, st);
-  EncArgs E{X, Nb, R, g.nK, g.m, g.r, g.n, __builtin_ctz((unsigned)g.m), __builtin_ctz((unsigned)g.r), seed, s_hat};
+  EncArgs E{X, Nb, R, g.nK, g.m, g.r, g.n, __builtin_ctz((unsigned)g.m), __builtin_ctz((unsigned)g.r), seed, hl::public_seed(seed), s_hat};
   const unsigned nct = (unsigned)(g.nJ * g.nK);
   {
     KTimer kt(c, HL_K_OTHER, st);

@@ -160,6 +160,12 @@ def test_encrypt_bit_exact_vs_oracle(hl, N, L, shape, tile):
     assert np.array_equal(ctx.encrypt(sk, tile, X, 103), ref.encrypt(P, tile, sk, X, 103))
 
 
+def test_public_seed_matches_oracle(hl):
+    """Reading C28: the library's public seed (shipped by the seeded upload) equals the oracle's."""
+    for s in (0, 103, 0x230518396 + 3, 2**64 - 1):
+        assert hl.public_seed(s) == ref.public_seed(s)
+
+
 @pytest.mark.parametrize("compress", [True, False])
 def test_decrypt_share_matches_oracle(hl, compress):
     ctx = hl.Context(4096, 2, 37, device=-1)

@@ -298,8 +298,9 @@ def test_linear_batch_c2_equals_single_calls(hl, ctx4096):
 
 @pytest.mark.parametrize("N", [4096, 8192])
 def test_expand_seeded_vs_oracle_encrypt(hl, ctx4096, ctx8192, N):
-    """Seeded upload: c1 regenerated on the device from the encryption seed equals the oracle
-    client's c1 = a bit for bit (both PRF streams, reading C10); c0 halves are left untouched."""
+    """Seeded upload: c1 regenerated on the device from the PUBLIC seed (reading C28: the oracle's
+    public_seed of the encryption seed) equals the oracle client's c1 = a bit for bit (both PRF
+    streams, reading C10); c0 halves are left untouched."""
     import torch
     ctx = ctx4096 if N == 4096 else ctx8192
     P = _P(ctx)
@@ -311,14 +312,15 @@ def test_expand_seeded_vs_oracle_encrypt(hl, ctx4096, ctx8192, N):
     up = ct.copy()
     up[:, :, 1] = 0x5a5a5a5a                       # garbage where c1 will be regenerated
     dev = hl.to_device(up)
-    ctx.expand_seeded(tile, R, Nb, seed + 2, dev)
+    assert hl.public_seed(seed + 2) == ref.public_seed(seed + 2)
+    ctx.expand_seeded(tile, R, Nb, ref.public_seed(seed + 2), dev)
     _sync()
     assert np.array_equal(hl.to_host(dev).reshape(ct.shape), ct)
 
 
 @pytest.mark.parametrize("packed", [False, True])
 def test_linear_batch_host_seeded_c1_vs_oracle(hl, ctx4096, packed):
-    """hl_he_linear_batch_host (bench.py's e2e call): only the c0 halves + the encryption seed go
+    """hl_he_linear_batch_host (bench.py's e2e call): only the c0 halves + the PUBLIC seed (C28) go
     host->device, results come back to pinned host buffers; every product's compressed response
     and share bit-exact against the oracle client + server, repeated to catch stream races.
     packed: c0 halves up and responses down in the 50-bit wire format (hl_pack50)."""
@@ -341,7 +343,7 @@ def test_linear_batch_host_seeded_c1_vs_oracle(hl, ctx4096, packed):
         mw = hl.Context.pack50(np.zeros(lay.ct_masked_words, np.uint64)).size if packed else lay.ct_masked_words
         entries.append(dict(wcache=ctx.encode_weights(cfg.tile, hl.to_device(W)), Ma=mm.Ma, R=mm.R, Nb=mm.Nb,
                             ct_in=torch.full((lay.ct_in_words,), 7, dtype=torch.int64, device="cuda"),
-                            seed=seed, c0_host=c0, enc_seed=es, packed=packed,
+                            seed=seed, c0_host=c0, a_seed=ref.public_seed(es), packed=packed,
                             masked_host=torch.zeros(mw, dtype=torch.int64).pin_memory(),
                             share_host=torch.zeros(lay.share_words, dtype=torch.int64).pin_memory()))
         exp.append(ref.mask_and_share(P, cfg.tile, ref.he_matmul(P, cfg.tile, W, ct, mm.Nb), mm.Ma, mm.Nb, seed))
