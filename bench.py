@@ -267,6 +267,8 @@ def run_ours(args, rank, world, local_rank):
     barrier()
     ctx.timing_enable(False)
     elapsed = max_over_ranks(ev0.elapsed_time(ev1))
+    # the device path's results, kept for the e2e check (rows f1/f4 below write into m["share"])
+    dev_results = [(m["masked"].clone(), m["share"].clone()) for m in mats]
     ktimes = ctx.timing_read()
     kernels_launched = ctx.timing_kernels()
     clk = clocks.stop() if clocks else None
@@ -475,11 +477,11 @@ def run_ours(args, rank, world, local_rank):
     torch.cuda.synchronize()
     e2e_checked = False
     if not shard:       # the host results are the device path's, bit for bit (the e2e leg does the real work)
-        for m, hm, hs in zip(mats, host_masked, host_share):
+        for m, hm, hs, (dm, ds) in zip(mats, host_masked, host_share, dev_results):
             got = hm.numpy().view(np.uint64)
             if packed:
                 got = hl.Context.unpack50(got, m["lay"].ct_masked_words)
-            assert np.array_equal(got, m["masked"].cpu().numpy().view(np.uint64)) and torch.equal(hs, m["share"].cpu()), \
+            assert np.array_equal(got, dm.cpu().numpy().view(np.uint64)) and torch.equal(hs, ds.cpu()), \
                 "e2e results differ"
         e2e_checked = True
     barrier()
@@ -510,7 +512,7 @@ def run_ours(args, rank, world, local_rank):
     # ALU peaks, measured on this B200 by tools/microbench/intpipe3.cu
     # (profiles/r01/microbench_intpipe3.log): IMAD.WIDE.U32 24.4 /clk/SM (the IMAD engine's
     # multiply), DFMA 57.3 /clk/SM (the default FP64 engine); x 148 SMs x max SM clock.
-    engine = os.environ.get("HELINEAR_MAC_ENGINE", "tc")
+    engine = "tc"
     if engine == "tc":
         ops_per_mac, alu_peak, alu_unit = 0.0, 1.0, ""
     elif engine == "imad":

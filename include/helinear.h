@@ -111,8 +111,7 @@ int hl_ctx_destroy(hl_ctx *ctx);
  * 1 = exact FP64 products (error-free DFMA transformations), 2 = exact products on the int8
  * tensor cores (tcgen05.mma kind::i8, 7 byte limbs, TMEM accumulators; default).  Results are
  * bit-identical; the NTT-domain weight cache and workspace formats (and sizes, see
- * hl_layout_query) differ, so a cache must be encoded and used under the same engine.  The
- * environment variable HELINEAR_MAC_ENGINE=imad|f64|tc selects the engine at context creation.
+ * hl_layout_query) differ, so a cache must be encoded and used under the same engine.
  * Not thread-safe against concurrent calls on ctx. */
 int hl_ctx_set_mac_engine(hl_ctx *ctx, int engine);
 

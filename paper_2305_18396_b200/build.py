@@ -29,7 +29,8 @@ CXX_FLAGS = ["-O2", "-std=c++17", "-fPIC", "-fopenmp", "-Wall", "-Wno-unknown-pr
 
 CU_SOURCES = ["kernels.cu"]
 CXX_SOURCES = ["ctx.cpp", "client.cpp"]
-HEADERS = ["hl_internal.h", "chacha.h", "mac_tc.cuh"]
+# every header under csrc/ (and include/helinear.h): an edit to any of them rebuilds every object
+HEADERS = sorted(f for f in os.listdir(CSRC) if f.endswith((".h", ".cuh")))
 
 
 def _newer(src_list, target) -> bool:

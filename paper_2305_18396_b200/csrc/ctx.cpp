@@ -212,8 +212,6 @@ extern "C" int hl_ctx_create(uint32_t N, uint32_t L, uint32_t log2_t, const uint
     pc.ninv_d = (double)pc.ninv; pc.ninv_w1_d = (double)pc.ninv_w1;
   }
   build_cdt(c->cdt);
-  if (const char *e = getenv("HELINEAR_MAC_ENGINE"))
-    c->mac_engine = (strcmp(e, "imad") == 0) ? 0 : ((strcmp(e, "f64") == 0) ? 1 : 2);
   // device tables (device < 0: host-only context for the client calls; no CUDA needed)
   if (device < 0) {
     dp.twd_fwd = dp.twd_inv = nullptr;
@@ -241,10 +239,7 @@ extern "C" int hl_ctx_create(uint32_t N, uint32_t L, uint32_t log2_t, const uint
     // are placed before queued NTT blocks of the concurrent low-priority stream
     int lo = 0, hi = 0;
     cudaDeviceGetStreamPriorityRange(&lo, &hi);
-    // forward-NTT stream priority (experiment knob HELINEAR_FWD_PRIO: 0 = lowest, 1 = middle, 2 = highest)
-    const char *fp = getenv("HELINEAR_FWD_PRIO");
-    const int fsel = fp ? atoi(fp) : 0;
-    const int fprio = fsel >= 2 ? hi : (fsel == 1 ? (lo + hi) / 2 : lo);
+    const int fprio = lo;     // forward NTTs at the lowest priority (middle / highest measured no better)
     cudaStream_t aux, mac, up, down, fwd;
     if (cudaStreamCreateWithPriority(&aux, cudaStreamNonBlocking, lo) != cudaSuccess ||
         cudaStreamCreateWithPriority(&fwd, cudaStreamNonBlocking, fprio) != cudaSuccess ||

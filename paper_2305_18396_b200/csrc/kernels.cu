@@ -25,6 +25,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <atomic>
 #include <cstdio>
 #include <cstdlib>
 #include <initializer_list>
@@ -401,13 +402,12 @@ MacGeom mac_geom(const hl_ctx *c, int64_t nIs, int64_t nJ, int64_t nC) {
   g.nSb = g.LN / 32;
   g.f64 = c->mac_engine == 1;
   g.nIp = g.nIb * 16;
-  // tile rows per MMA: <= 128 (M = 128; tiles of <= 64 rows use M = 64); HELINEAR_MAC_RT_MAX=64 (experiment)
-  static const int rt_max = [] { const char *e = getenv("HELINEAR_MAC_RT_MAX"); return e ? atoi(e) : 128; }();
+  // tile rows per MMA: <= 128 (M = 128; tiles of <= 64 rows use M = 64), balanced tiles in multiples
+  // of 8 (UMMA core rows).  Measured alternatives: tiles of <= 64 rows, and full
+  // 128-row tiles + one short last tile, were both slower on c2.
+  constexpr int rt_max = 128;
   g.nIt = (g.nIp + rt_max - 1) / rt_max;
-  g.RT = ((g.nIp + g.nIt - 1) / g.nIt + 7) / 8 * 8;      // balanced tiles, multiple of 8 (UMMA core rows)
-  // experiment: HELINEAR_MAC_GREEDY=1 -> full 128-row tiles + one short last tile (M = 64 if <= 64 rows)
-  static const bool greedy = getenv("HELINEAR_MAC_GREEDY") != nullptr;
-  if (greedy && g.nIt > 1) g.RT = rt_max;
+  g.RT = ((g.nIp + g.nIt - 1) / g.nIt + 7) / 8 * 8;
   if ((int64_t)g.RT * (g.nIt - 1) >= nIs) g.RT = rt_max;   // never an empty last tile
   g.nJp = (int)((nJ + 31) / 32 * 32);
   g.nJc = g.nJp / 32;
@@ -1573,6 +1573,18 @@ __global__ void k_pointwise(const uint64_t *a, const uint64_t *b, uint64_t *out,
 // ---------------------------------------------------------------------------------------
 // launch helpers
 // ---------------------------------------------------------------------------------------
+// one-time kernel attribute setup per DEVICE (cudaFuncSetAttribute applies to the current device):
+// a second context on another device in the same process sets its own
+struct PerDevice {
+  std::atomic<uint64_t> done{0};
+  bool first() {
+    int d = 0;
+    cudaGetDevice(&d);
+    const uint64_t b = 1ull << (d & 63);
+    return (done.fetch_or(b) & b) == 0;
+  }
+};
+
 template <typename Kern>
 void set_smem(Kern k, size_t bytes) {
   cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
@@ -1583,8 +1595,8 @@ constexpr size_t ntt_smem() { return (size_t)Geom<LOGN>::SMEM_WORDS * 8; }
 
 template <int LOGN, int MODE>
 void launch_fwd(const hl_ctx *c, const uint64_t *in, void *out, int64_t npoly, const MacGeom &mg, cudaStream_t st) {
-  static bool init = false;
-  if (!init) { set_smem(k_ntt_fwd<LOGN, MODE>, ntt_smem<LOGN>()); init = true; }
+  static PerDevice init;
+  if (init.first()) { set_smem(k_ntt_fwd<LOGN, MODE>, ntt_smem<LOGN>()); }
   dim3 grid((unsigned)npoly, c->L);
   KTimer kt(c, MODE ? HL_K_NTT_FWD : HL_K_OTHER, st);
   k_ntt_fwd<LOGN, MODE><<<grid, Geom<LOGN>::NT, ntt_smem<LOGN>(), st>>>(in, out, c->dp, mg);
@@ -1592,8 +1604,8 @@ void launch_fwd(const hl_ctx *c, const uint64_t *in, void *out, int64_t npoly, c
 
 template <int LOGN>
 void launch_inv(const hl_ctx *c, const uint64_t *in, uint64_t *out, int64_t npoly, cudaStream_t st, int ct_mode) {
-  static bool init = false;
-  if (!init) { set_smem(k_ntt_inv<LOGN>, ntt_smem<LOGN>()); init = true; }
+  static PerDevice init;
+  if (init.first()) { set_smem(k_ntt_inv<LOGN>, ntt_smem<LOGN>()); }
   dim3 grid((unsigned)npoly, c->L);
   KTimer kt(c, HL_K_INTT, st);
   k_ntt_inv<LOGN><<<grid, Geom<LOGN>::NT, ntt_smem<LOGN>(), st>>>(in, out, c->dp, ct_mode);
@@ -1602,17 +1614,13 @@ void launch_inv(const hl_ctx *c, const uint64_t *in, uint64_t *out, int64_t npol
 template <int LOGN, int G>
 void launch_fwd_x(const hl_ctx *c, const uint64_t *in, void *out, int64_t npoly, const MacGeom &mg, cudaStream_t st) {
   constexpr size_t smem = ntt_smem<LOGN>() * G;
-  static bool init = false;
-  if (!init) { set_smem(k_ntt_fwd_x<LOGN, G>, smem); init = true; }
+  static PerDevice init;
+  if (init.first()) { set_smem(k_ntt_fwd_x<LOGN, G>, smem); }
   dim3 grid((unsigned)(npoly / G), c->L);
   KTimer kt(c, HL_K_NTT_FWD, st);
   k_ntt_fwd_x<LOGN, G><<<grid, Geom<LOGN>::NT * G, smem, st>>>(in, (uint64_t *)out, c->dp, mg);
 }
 
-static int ntt_group() {
-  static int g = [] { const char *e = getenv("HELINEAR_NTT_G"); return e ? atoi(e) : 2; }();
-  return g;
-}
 
 template <int LOGN>
 void launch_fwd_cperm(const hl_ctx *c, const uint64_t *in, uint64_t *out, int64_t npoly, const MacGeom &mg,
@@ -1621,34 +1629,29 @@ void launch_fwd_cperm(const hl_ctx *c, const uint64_t *in, uint64_t *out, int64_
   const int64_t nJ = npoly / mg.nC;
   constexpr size_t smem2 = ntt_smem<LOGN>() * 2;
   constexpr int MB2 = LOGN == 12 ? 2 : 1;             // explicit: minBlocks 1 lets the kernel grow to 1 CTA/SM
-  static bool init = false;
-  if (!init) {
+  static PerDevice init;
+  if (init.first()) {
     set_smem(k_ntt_fwd_c0x2<LOGN, false, MB2>, smem2); set_smem(k_ntt_fwd_c0x2<LOGN, true>, smem2);
     if constexpr (LOGN == 12) {
-      set_smem(k_ntt_fwd_c0x2<LOGN, true, 2>, smem2); set_smem(k_ntt_fwd_c0x2<LOGN, true, 3>, smem2);
+      set_smem(k_ntt_fwd_c0x2<LOGN, true, 3>, smem2);
       set_smem(k_ntt_fwd_c0x2<LOGN, false, 3>, smem2);
     }
     set_smem(k_c1_to_x<LOGN, 4>, 4 * (size_t)Geom<LOGN>::N * 8); set_smem(k_c1_to_x<LOGN, 2>, 2 * (size_t)Geom<LOGN>::N * 8);
     set_smem(k_c1_to_x<LOGN, 1>, (size_t)Geom<LOGN>::N * 8);
-    init = true;
   }
   KTimer kt(c, HL_K_NTT_FWD, st);
-  static const bool fuse_c1 = [] { const char *e = getenv("HELINEAR_FUSE_C1"); return e ? atoi(e) != 0 : true; }();
   if (mg.c1_in) {                                  // c1 is read by the MAC itself: c0 pairs only
     const dim3 gx((unsigned)(nJ * ((nK + 1) / 2)), c->L);
     if constexpr (LOGN == 12) k_ntt_fwd_c0x2<LOGN, false, 3><<<gx, Geom<LOGN>::NT, smem2, st>>>(in, out, c->dp, mg);
     else k_ntt_fwd_c0x2<LOGN, false, MB2><<<gx, Geom<LOGN>::NT, smem2, st>>>(in, out, c->dp, mg);
     return;
   }
-  const bool fused = fuse_c1 && (nK % 2 == 0);   // c1 pairs (K0, K0+1) adjacent in the c1 column range
-  // N = 4096: 3 CTAs per SM (80 registers, a few bytes of spill; measured best) or 2 (<= 128)
-  static const int minb = [] { const char *e = getenv("HELINEAR_X2_MINB"); return e ? atoi(e) : 3; }();
+  const bool fused = nK % 2 == 0;                // c1 pairs (K0, K0+1) adjacent in the c1 column range
   kt.nk = fused ? 1 : 2;
   if constexpr (LOGN == 12) {
-    if (fused) {
+    if (fused) {   // N = 4096: 3 CTAs per SM (80 registers, a few bytes of spill; measured best)
       const dim3 gx((unsigned)(nJ * ((nK + 1) / 2)), c->L);
-      if (minb >= 3) k_ntt_fwd_c0x2<LOGN, true, 3><<<gx, Geom<LOGN>::NT, smem2, st>>>(in, out, c->dp, mg);
-      else k_ntt_fwd_c0x2<LOGN, true, 2><<<gx, Geom<LOGN>::NT, smem2, st>>>(in, out, c->dp, mg);
+      k_ntt_fwd_c0x2<LOGN, true, 3><<<gx, Geom<LOGN>::NT, smem2, st>>>(in, out, c->dp, mg);
       return;
     }
   }
@@ -1659,8 +1662,7 @@ void launch_fwd_cperm(const hl_ctx *c, const uint64_t *in, uint64_t *out, int64_
   // odd nK: the c0 pairs without their c1, then the c1 reordering
   k_ntt_fwd_c0x2<LOGN, false, MB2><<<dim3((unsigned)(nJ * ((nK + 1) / 2)), c->L), Geom<LOGN>::NT, smem2, st>>>(in, out, c->dp, mg);
   // G1 = 4 needs 4 | nK and 4 | CW (the 4 columns in one group); 4 x 64 KB does not fit at N = 8192
-  static const int g1max = [] { const char *e = getenv("HELINEAR_C1_G"); return e ? atoi(e) : 4; }();
-  const int G1 = (g1max >= 4 && nK % 4 == 0 && mg.CW % 4 == 0 && LOGN == 12) ? 4 : (g1max >= 2 && nK % 2 == 0 ? 2 : 1);
+  const int G1 = (nK % 4 == 0 && mg.CW % 4 == 0 && LOGN == 12) ? 4 : (nK % 2 == 0 ? 2 : 1);
   const dim3 g1((unsigned)(nJ * (nK / G1)), c->L);
   constexpr size_t pb = (size_t)Geom<LOGN>::N * 8;
   if (G1 == 4) k_c1_to_x<LOGN, 4><<<g1, Geom<LOGN>::NT, 4 * pb, st>>>(in, out, c->dp, mg);
@@ -1677,15 +1679,9 @@ void fwd_ntt(const hl_ctx *c, const uint64_t *in, void *out, int64_t npoly, cons
   }
   if (mg && mg->engine == 2) {
     // G consecutive polynomials share J and a column group (G divides CW)
-    const int G = (mg->CW % 4 == 0 && ntt_group() >= 4 && c->N == 4096) ? 4 : (ntt_group() >= 2 ? 2 : 1);
-    if (c->N == 4096) {
-      if (G == 4) launch_fwd_x<12, 4>(c, in, out, npoly, *mg, st);
-      else if (G == 2) launch_fwd_x<12, 2>(c, in, out, npoly, *mg, st);
-      else launch_fwd_x<12, 1>(c, in, out, npoly, *mg, st);
-    } else {
-      if (G >= 2) launch_fwd_x<13, 2>(c, in, out, npoly, *mg, st);
-      else launch_fwd_x<13, 1>(c, in, out, npoly, *mg, st);
-    }
+    // (CW >= 2 always, so 2 divides it)
+    if (c->N == 4096) launch_fwd_x<12, 2>(c, in, out, npoly, *mg, st);
+    else launch_fwd_x<13, 2>(c, in, out, npoly, *mg, st);
     return;
   }
   MacGeom z{};
@@ -1703,8 +1699,8 @@ template <int CW, int LN>
 void launch_mac_t(const hl_ctx *c, const MacArgs &A, cudaStream_t st) {
   using S = MacSmem<CW>;
   constexpr size_t smem = (size_t)kMacStages * S::STAGE + S::E_BYTES + 2 * kMacStages * 8;
-  static bool init = false;
-  if (!init) { set_smem(k_mac<CW, LN, kMacStages>, smem); init = true; }
+  static PerDevice init;
+  if (init.first()) { set_smem(k_mac<CW, LN, kMacStages>, smem); }
   const int ntiles = A.g.nIb * A.g.nCg * A.g.nSb;
   const int grid = std::min(ntiles, c->num_sms);
   KTimer kt(c, HL_K_MAC, st);
@@ -1718,8 +1714,8 @@ template <int CW, int LN>
 void launch_mac_f64_t(const hl_ctx *c, const MacArgs &A, cudaStream_t st) {
   using S = MacSmemF64<CW, kMacF64Jps>;
   constexpr size_t smem = (size_t)kMacF64Stages * S::STAGE + S::E_BYTES + 2 * kMacF64Stages * 8;
-  static bool init = false;
-  if (!init) { set_smem(k_mac_f64<CW, LN, kMacF64Stages, kMacF64Jps>, smem); init = true; }
+  static PerDevice init;
+  if (init.first()) { set_smem(k_mac_f64<CW, LN, kMacF64Stages, kMacF64Jps>, smem); }
   const int ntiles = A.g.nIb * A.g.nCg * A.g.nSb;
   const int grid = std::min(ntiles, c->num_sms);
   KTimer kt(c, HL_K_MAC, st);
@@ -1742,8 +1738,8 @@ void launch_mac_ln(const hl_ctx *c, const MacArgs &A, cudaStream_t st) {
 template <int CW>
 void launch_mac_tc_t(const hl_ctx *c, MacTcArgs A, int smem_budget, int grid, cudaStream_t st) {
   using T = TcGeom<CW>;
-  static bool init = false;
-  if (!init) { set_smem(k_mac_tc<CW>, T::SMEM_MAX); init = true; }
+  static PerDevice init;
+  if (init.first()) { set_smem(k_mac_tc<CW>, T::SMEM_MAX); }
   A.ring = tc_ring<CW>(A.g.RT, smem_budget, A.c1_bytes);
   static const bool prof = getenv("HELINEAR_MAC_PROF") != nullptr;
   A.prof = nullptr;
@@ -1814,8 +1810,6 @@ void launch_mac_tc(const hl_ctx *c, const void *W, const void *X, uint64_t *out,
   A.c1_lognt = (c->N == 4096 ? 12 : 13) - 4;
   A.qperm = A.c1_out != nullptr;
   A.sched = (int *)((char *)X + tc_sched_offset(g));
-  static const int ko = [] { const char *e = getenv("HELINEAR_MAC_KO"); return e ? atoi(e) : 0; }();
-  A.ko = ko;
   for (int64_t j0 = 0; j0 < g.nJp; j0 += kMacJChunk) {     // S_d < 7 * 4096 * 255^2 < 2^31 per launch
     A.jc0 = (int)(j0 / 32);
     A.njc = (int)((std::min<int64_t>(g.nJp, j0 + kMacJChunk) - j0) / 32);
@@ -1864,24 +1858,18 @@ void launch_mac(const hl_ctx *c, const uint2 *W, const uint32_t *X, uint64_t *ou
 template <int LOGN, bool RR>
 bool inv_prunes(const hl_ctx *c, const MaskArgs &M) {
   using Gm = Geom<LOGN>;
-  static const bool no_prune = getenv("HELINEAR_NO_PRUNE") != nullptr;
   const int re = std::min(M.r, 16);                   // the pruned kernel's live class (see there)
   const int wpp = (Gm::NT / std::max(re, 1) + 31) / 32;
   const size_t ext = RR ? 16 : 8;                      // sigma (+ row f4: e1 + F) per kept position
   const size_t smem_c0 = ntt_smem<LOGN>() * c->L + (size_t)M.m * M.n * ext;
-  return !no_prune && M.r >= 2 && (int)c->L * wpp <= Gm::NT / 32 && smem_c0 <= 232448;
-}
-static bool c1_light() {
-  static const bool light = [] { const char *e = getenv("HELINEAR_C1_LIGHT"); return e ? atoi(e) != 0 : true; }();
-  return light;
+  return M.r >= 2 && (int)c->L * wpp <= Gm::NT / 32 && smem_c0 <= 232448;
 }
 // May the MAC write the c1 halves of the response itself (MacTcArgs::c1_out)?  Only where the
 // inverse would otherwise just reorder them (k_c1_out): pruned c0 inverse, no re-randomisation,
-// tensor-core MAC in one launch with c0 columns first.  HELINEAR_C1_DIRECT=0 turns it off.
+// tensor-core MAC in one launch with c0 columns first.
 template <int LOGN>
 bool c1_direct_ok(const hl_ctx *c, const MacGeom &g, const MaskArgs &M) {
-  static const bool on = [] { const char *e = getenv("HELINEAR_C1_DIRECT"); return e ? atoi(e) != 0 : true; }();
-  return on && g.engine == 2 && g.cperm && g.nJp <= kMacJChunk && !M.pk_hat && c1_light() &&
+  return g.engine == 2 && g.cperm && g.nJp <= kMacJChunk && !M.pk_hat &&
          inv_prunes<LOGN, false>(c, M);
 }
 inline bool c1_direct(const hl_ctx *c, const MacGeom &g, const MaskArgs &M) {
@@ -1889,10 +1877,9 @@ inline bool c1_direct(const hl_ctx *c, const MacGeom &g, const MaskArgs &M) {
 }
 // May the MAC also READ c1 from the ciphertexts (MacGeom::c1_in)?  With the quad order (c1_direct)
 // a work item's slots are 4 consecutive natural points; the column groups must be pure c0 / pure c1
-// or a single group.  HELINEAR_C1_TMA=0 turns it off.
+// or a single group.
 inline bool c1_in_ok(const MacGeom &g, const MaskArgs &M, const uint64_t *ct_in) {
-  static const bool on = [] { const char *e = getenv("HELINEAR_C1_TMA"); return e ? atoi(e) != 0 : true; }();
-  if (!(on && M.c1_done && (g.nCg == 1 || M.nK % g.CW == 0))) return false;
+  if (!(M.c1_done && (g.nCg == 1 || M.nK % g.CW == 0))) return false;
   CUtensorMap probe;                                    // the launch re-encodes the same map
   return c1_tmap(&probe, ct_in, g.LN, M.nK, g.nJ, (int)std::min<int64_t>(g.CW, M.nK));
 }
@@ -1901,32 +1888,24 @@ template <int LOGN, bool RR>
 void launch_inv_mask_t(const hl_ctx *c, const uint64_t *ct_ntt, uint64_t *masked, uint64_t *share, MaskArgs M,
                        int64_t nout, cudaStream_t st) {
   using Gm = Geom<LOGN>;
-  static bool init = false;
-  if (!init) {
+  static PerDevice init;
+  if (init.first()) {
     set_smem(k_ntt_inv_mask<LOGN, RR>, ntt_smem<LOGN>() + (size_t)Gm::N * 16);
-    set_smem(k_intt_c0_pruned<LOGN, RR>, 232448);
     set_smem(k_intt_c0_pruned<LOGN, RR, true>, 232448);
     set_smem(k_c1_out<LOGN>, ntt_smem<LOGN>());
-    init = true;
   }
   const int re = std::min(M.r, 16);
   const size_t ext = RR ? 16 : 8;
-  const size_t smem_c0 = ntt_smem<LOGN>() * c->L + (size_t)M.m * M.n * ext;
   const bool prune = inv_prunes<LOGN, RR>(c, M);
   const size_t smem = ntt_smem<LOGN>() + (RR ? std::max((size_t)M.m * M.n * 16, (size_t)Gm::N) : (size_t)M.m * M.n * 8);
   KTimer kt(c, HL_K_INTT_MASK, st);
   kt.nk = prune && !M.c1_done ? 2 : 1;
-  if (prune) {
-    static const bool cmp = [] { const char *e = getenv("HELINEAR_C0_COMPACT"); return e ? atoi(e) != 0 : true; }();
-    if (cmp) {
-      const size_t cwords = (size_t)(Gm::N / re) + (size_t)(Gm::N / re) / 16;
-      const size_t smem_cmp = cwords * 8 * c->L + (size_t)M.m * M.n * ext;
-      k_intt_c0_pruned<LOGN, RR, true><<<(unsigned)nout, Gm::NT, smem_cmp, st>>>(ct_ntt, masked, share, M, c->dp);
-    } else {
-      k_intt_c0_pruned<LOGN, RR><<<(unsigned)nout, Gm::NT, smem_c0, st>>>(ct_ntt, masked, share, M, c->dp);
-    }
+  if (prune) {   // compact parking of the live class (4 CTAs/SM; the full-size parking measured slower)
+    const size_t cwords = (size_t)(Gm::N / re) + (size_t)(Gm::N / re) / 16;
+    const size_t smem_cmp = cwords * 8 * c->L + (size_t)M.m * M.n * ext;
+    k_intt_c0_pruned<LOGN, RR, true><<<(unsigned)nout, Gm::NT, smem_cmp, st>>>(ct_ntt, masked, share, M, c->dp);
     if (M.c1_done) return;                             // the MAC wrote c1 (c1_direct_ok)
-    if (!RR && c1_light()) k_c1_out<LOGN><<<(unsigned)nout, Gm::NT, ntt_smem<LOGN>(), st>>>(ct_ntt, masked, M, c->dp);
+    if (!RR) k_c1_out<LOGN><<<(unsigned)nout, Gm::NT, ntt_smem<LOGN>(), st>>>(ct_ntt, masked, M, c->dp);
     else k_ntt_inv_mask<LOGN, RR><<<(unsigned)nout, Gm::NT, smem, st>>>(ct_ntt, masked, share, M, c->dp, 1);
   } else {
     k_ntt_inv_mask<LOGN, RR><<<(unsigned)(nout * 2), Gm::NT, smem, st>>>(ct_ntt, masked, share, M, c->dp, 0);
@@ -1945,6 +1924,17 @@ void launch_inv_mask(const hl_ctx *c, const uint64_t *ct_ntt, uint64_t *masked, 
 // =========================================================================================
 // entry points
 // =========================================================================================
+// Every device entry point runs on the context's device and restores the caller's current device.
+struct DeviceGuard {
+  int prev = -1, dev = -1;
+  explicit DeviceGuard(const hl_ctx *c) {
+    if (!c || c->device < 0) return;
+    cudaGetDevice(&prev);
+    if (prev != c->device) { dev = c->device; cudaSetDevice(dev); }
+  }
+  ~DeviceGuard() { if (dev >= 0) cudaSetDevice(prev); }
+};
+
 // the first pointer must be the context
 static int check_ptrs(std::initializer_list<const void *> ps, const char *who) {
   for (const void *p : ps)
@@ -1960,18 +1950,21 @@ static int encode_weights_impl(const hl_ctx *c, hl_tile tile, const uint64_t *W,
 
 extern "C" int hl_encode_weights(const hl_ctx *c, hl_tile tile, const uint64_t *W, int64_t R, int64_t Ma,
                                  int64_t i_begin, int64_t i_end, void *wcache, void *stream) {
+  DeviceGuard dg_(c);
   return encode_weights_impl(c, tile, W, R, Ma, Ma, 1, i_begin, i_end, wcache, nullptr, 1, stream);
 }
 
 extern "C" int hl_encode_weights_strided(const hl_ctx *c, hl_tile tile, const uint64_t *W, int64_t R, int64_t Ma,
                                          int64_t ld_row, int64_t ld_col, int64_t i_begin, int64_t i_end, void *wcache,
                                          void *stream) {
+  DeviceGuard dg_(c);
   return encode_weights_impl(c, tile, W, R, Ma, ld_row, ld_col, i_begin, i_end, wcache, nullptr, 1, stream);
 }
 
 extern "C" int hl_encode_weights_scratch(const hl_ctx *c, hl_tile tile, const uint64_t *W, int64_t R, int64_t Ma,
                                          int64_t ld_row, int64_t ld_col, int64_t i_begin, int64_t i_end, void *wcache,
                                          uint64_t *scratch, int check, void *stream) {
+  DeviceGuard dg_(c);
   if (!scratch) return hl_fail(HL_EINVAL, "hl_encode_weights_scratch: scratch is NULL");
   return encode_weights_impl(c, tile, W, R, Ma, ld_row, ld_col, i_begin, i_end, wcache, scratch, check, stream);
 }
@@ -1984,7 +1977,6 @@ static int encode_weights_impl(const hl_ctx *c, hl_tile tile, const uint64_t *W,
   Geo g;
   if ((rc = hl_geometry(c, tile, Ma, R, 1, i_begin, i_end, &g))) return rc;
   cudaStream_t st = (cudaStream_t)stream;
-  cudaSetDevice(c->device);
   cudaMemsetAsync(c->d_flags, 0, 8, st);
   const MacGeom mg = mac_geom(c, g.nIs, g.nJ, 2 * g.nK);
   if (mg.engine != 2) scratch = nullptr;       // the two-pass form is the tensor-core cache's
@@ -1995,19 +1987,19 @@ static int encode_weights_impl(const hl_ctx *c, hl_tile tile, const uint64_t *W,
   {
   KTimer kt(c, HL_K_ENCODE, st);
   if (c->N == 4096) {
-    static bool init = false;
-    if (!init) { set_smem(k_encode_weights<12>, ntt_smem<12>()); init = true; }
+    static PerDevice init;
+    if (init.first()) { set_smem(k_encode_weights<12>, ntt_smem<12>()); }
     k_encode_weights<12><<<grid, Geom<12>::NT, ntt_smem<12>(), st>>>(A, (uint2 *)wcache, c->dp, c->d_flags, scratch);
   } else {
-    static bool init = false;
-    if (!init) { set_smem(k_encode_weights<13>, ntt_smem<13>()); init = true; }
+    static PerDevice init;
+    if (init.first()) { set_smem(k_encode_weights<13>, ntt_smem<13>()); }
     k_encode_weights<13><<<grid, Geom<13>::NT, ntt_smem<13>(), st>>>(A, (uint2 *)wcache, c->dp, c->d_flags, scratch);
   }
   if (scratch) {
     const int64_t nb = (int64_t)mg.nIt * mg.nJc * ((mg.RT + kWpR - 1) / kWpR) * (mg.LN / kWpS);
     constexpr size_t wsm = (size_t)kWpS * kWpR * 33 * 8;
-    static bool winit = false;
-    if (!winit) { set_smem(k_wplanes, wsm); winit = true; }
+    static PerDevice winit;
+    if (winit.first()) { set_smem(k_wplanes, wsm); }
     k_wplanes<<<(unsigned)nb, 256, wsm, st>>>(scratch, (uint8_t *)wcache, mg);
   }
   }
@@ -2028,6 +2020,7 @@ static int encode_weights_impl(const hl_ctx *c, hl_tile tile, const uint64_t *W,
 extern "C" int hl_he_matmul(const hl_ctx *c, hl_tile tile, const void *wcache, int64_t Ma, int64_t R, int64_t Nb,
                             int64_t i_begin, int64_t i_end, const uint64_t *ct_in, void *workspace,
                             uint64_t *ct_out, void *stream) {
+  DeviceGuard dg_(c);
   int rc;
   if ((rc = check_ptrs({c, wcache, ct_in, workspace, ct_out}, "hl_he_matmul"))) return rc;
   Geo g;
@@ -2054,6 +2047,7 @@ static MaskArgs mask_args(const Geo &g, int64_t Ma, int64_t Nb, uint64_t seed) {
 extern "C" int hl_mask_and_share(const hl_ctx *c, hl_tile tile, int64_t Ma, int64_t Nb, int64_t i_begin,
                                  int64_t i_end, const uint64_t *ct_out, uint64_t seed, int compress,
                                  uint64_t *ct_masked, uint64_t *share, void *stream) {
+  DeviceGuard dg_(c);
   int rc;
   if ((rc = check_ptrs({c, ct_out, ct_masked, share}, "hl_mask_and_share"))) return rc;
   Geo g;
@@ -2069,6 +2063,7 @@ extern "C" int hl_he_matmul_share(const hl_ctx *c, hl_tile tile, const void *wca
                                   int64_t Nb, int64_t i_begin, int64_t i_end, const uint64_t *ct_in,
                                   void *workspace, uint64_t *ct_out_ntt, uint64_t seed, int compress,
                                   uint64_t *ct_masked, uint64_t *share, void *stream) {
+  DeviceGuard dg_(c);
   int rc;
   if ((rc = check_ptrs({c, wcache, ct_in, workspace, ct_out_ntt, ct_masked, share}, "hl_he_matmul_share")))
     return rc;
@@ -2135,16 +2130,14 @@ static int linear_batch_run(const hl_ctx *c, hl_tile tile, int n, const hl_linea
   cudaEvent_t *e_fwd = ev.data(), *e_mac = ev.data() + n, e_in = ev[2 * n], e_done = ev[2 * n + 1];
   cudaEvent_t e_macs = ev[2 * n + 2];
   // every forward NTT is issued up front on the forward stream (measured: 1.082 -> 1.060 ms per c2
-  // block vs interleaving them with the MACs); HELINEAR_BATCH_INTERLEAVE=1 restores the interleaving
-  static const bool interleave = getenv("HELINEAR_BATCH_INTERLEAVE") != nullptr;
-  const bool split = ready != nullptr || !interleave;
+  // block vs interleaving them with the MACs)
   // adaptive policy: with many columns per weight byte (nK >= 8, e.g. c3/c4: 8-16x c2's NTT work per
   // byte) co-resident kernels slow each other more than they overlap -- issue the products one after
   // the other on the forward / MAC / inverse streams without the cross-product overlap
-  static const int serial_nk = [] { const char *e = getenv("HELINEAR_BATCH_SERIAL_NK"); return e ? atoi(e) : 8; }();
+  constexpr int serial_nk = 8;
   bool serial = !ready;
   for (int i = 0; i < n; i++) serial = serial && E[i].g.nK >= serial_nk;
-  cudaStream_t sf = split ? (cudaStream_t)c->fwd_stream : s1;
+  cudaStream_t sf = (cudaStream_t)c->fwd_stream;
   auto fwd = [&](int i) {
     if (ready) cudaStreamWaitEvent(sf, ready[i], 0);
     if (expand_seed)
@@ -2156,16 +2149,9 @@ static int linear_batch_run(const hl_ctx *c, hl_tile tile, int n, const hl_linea
     if (c->N == 4096) launch_inv_mask<12>(c, d[i].ct_out_ntt, d[i].ct_masked, d[i].share, E[i].M, E[i].g.nIs * E[i].g.nK, s1);
     else launch_inv_mask<13>(c, d[i].ct_out_ntt, d[i].ct_masked, d[i].share, E[i].M, E[i].g.nIs * E[i].g.nK, s1);
   };
-  // compute order = entry order (the caller's choice: tools/gpu/order_sweep.sh measures all orders);
-  // HELINEAR_BATCH_ORDER="3,1,0,2" overrides it for experiments
+  // compute order = entry order (the caller's choice: tools/gpu/order_sweep.sh measures all orders)
   std::vector<int> ord(n);
   for (int i = 0; i < n; i++) ord[i] = i;
-  static const char *order_env = getenv("HELINEAR_BATCH_ORDER");
-  if (order_env && !ready) {
-    std::vector<int> o;
-    for (const char *p = order_env; *p;) { o.push_back(atoi(p)); while (*p && *p != ',') p++; if (*p) p++; }
-    if ((int)o.size() == n) ord = o;
-  }
   if (serial) {                                   // the products one after the other on `stream`
     for (int k = 0; k < n; k++) {
       const int i = ord[k];
@@ -2181,31 +2167,14 @@ static int linear_batch_run(const hl_ctx *c, hl_tile tile, int n, const hl_linea
   cudaEventRecord(e_in, sc);                      // inputs written on `stream` are visible to both streams
   cudaStreamWaitEvent(s0, e_in, 0);
   cudaStreamWaitEvent(s1, e_in, 0);
-  if (split) {
-    cudaStreamWaitEvent(sf, e_in, 0);
-    for (int k = 0; k < n; k++) fwd(ord[k]);
-  } else {
-    fwd(ord[0]);
-  }
-  // experiment knob: HELINEAR_BATCH_FWD_FIRST=1 starts the first MAC only after every forward NTT
-  static const bool fwd_first = getenv("HELINEAR_BATCH_FWD_FIRST") != nullptr;
-  if (fwd_first && split)
-    for (int k = 0; k < n; k++) cudaStreamWaitEvent(s0, e_fwd[ord[k]], 0);
+  cudaStreamWaitEvent(sf, e_in, 0);
+  for (int k = 0; k < n; k++) fwd(ord[k]);
   for (int k = 0; k < n; k++) {
     const int i = ord[k];
     cudaStreamWaitEvent(s0, e_fwd[i], 0);
-    static const int mac_smem = [] {
-      const char *e = getenv("HELINEAR_BATCH_MAC_SMEM_KB");
-      return e ? atoi(e) * 1024 : kMacSmemShared;
-    }();
-    static const int mac_grid = [] {
-      const char *e = getenv("HELINEAR_BATCH_MAC_GRID");
-      return e ? atoi(e) : 0;
-    }();
     launch_mac(c, (const uint2 *)d[i].wcache, (const uint32_t *)d[i].workspace, d[i].ct_out_ntt, E[i].mg, s0,
-               mac_smem, mac_grid, E[i].M.c1_done ? &E[i].M : nullptr, d[i].ct_masked, d[i].ct_in);
+               kMacSmemShared, 0, E[i].M.c1_done ? &E[i].M : nullptr, d[i].ct_masked, d[i].ct_in);
     cudaEventRecord(e_mac[i], s0);
-    if (!split && k + 1 < n) fwd(ord[k + 1]);                           // overlaps MAC(i)
     cudaStreamWaitEvent(s1, e_mac[i], 0);
     inv(i);                                                               // overlaps MAC(i+1)
     if (done) cudaEventRecord(done[i], s1);
@@ -2214,12 +2183,13 @@ static int linear_batch_run(const hl_ctx *c, hl_tile tile, int n, const hl_linea
   cudaEventRecord(e_macs, s0);
   cudaStreamWaitEvent(sc, e_done, 0);
   cudaStreamWaitEvent(sc, e_macs, 0);
-  // (split: every forward NTT precedes a MAC, so sf is joined through s0)
+  // (every forward NTT precedes a MAC, so sf is joined through s0)
   for (auto &e : ev) cudaEventDestroy(e);         // released once the recorded work completes
   return hl_cuda_check("hl_he_linear_batch: launch");
 }
 
 extern "C" int hl_he_linear_batch(const hl_ctx *c, hl_tile tile, int n, const hl_linear_desc *d, void *stream) {
+  DeviceGuard dg_(c);
   int rc;
   if ((rc = check_ptrs({c, d}, "hl_he_linear_batch"))) return rc;
   if (n <= 0) return hl_fail(HL_EINVAL, "hl_he_linear_batch: n must be positive");
@@ -2238,6 +2208,7 @@ static void expand_seeded(const hl_ctx *c, int64_t nct, uint64_t a_seed, uint64_
 
 extern "C" int hl_expand_seeded(const hl_ctx *c, hl_tile tile, int64_t R, int64_t Nb, uint64_t a_seed,
                                 uint64_t *ct_in, void *stream) {
+  DeviceGuard dg_(c);
   int rc;
   if ((rc = check_ptrs({c, ct_in}, "hl_expand_seeded"))) return rc;
   Geo g;
@@ -2280,6 +2251,7 @@ __global__ void k_unpack50_c0(const uint64_t *__restrict__ in, int64_t words, ui
 // i computes (hl_he_linear_batch's streams) while entry i-1's results download (download stream).
 extern "C" int hl_he_linear_batch_host(const hl_ctx *c, hl_tile tile, int n, const hl_linear_host_desc *h,
                                        void *stream) {
+  DeviceGuard dg_(c);
   int rc;
   if ((rc = check_ptrs({c, h}, "hl_he_linear_batch_host"))) return rc;
   if (n <= 0) return hl_fail(HL_EINVAL, "hl_he_linear_batch_host: n must be positive");
@@ -2347,6 +2319,7 @@ extern "C" int hl_he_linear_batch_host(const hl_ctx *c, hl_tile tile, int n, con
 // the client side on the GPU (client_dev.cuh)
 // ---------------------------------------------------------------------------------------
 extern "C" int hl_sk_prepare(const hl_ctx *c, const int8_t *sk, uint64_t *s_hat, void *stream) {
+  DeviceGuard dg_(c);
   int rc;
   if ((rc = check_ptrs({c, sk, s_hat}, "hl_sk_prepare"))) return rc;
   std::vector<uint64_t> res((size_t)c->L * c->N);
@@ -2365,6 +2338,7 @@ extern "C" int hl_sk_prepare(const hl_ctx *c, const int8_t *sk, uint64_t *s_hat,
 
 extern "C" int hl_encrypt_device(const hl_ctx *c, const uint64_t *s_hat, hl_tile tile, const uint64_t *X, int64_t Nb,
                                  int64_t R, uint64_t seed, uint64_t *ct_in, void *stream) {
+  DeviceGuard dg_(c);
   int rc;
   if ((rc = check_ptrs({c, s_hat, X, ct_in}, "hl_encrypt_device"))) return rc;
   Geo g;
@@ -2377,13 +2351,13 @@ extern "C" int hl_encrypt_device(const hl_ctx *c, const uint64_t *s_hat, hl_tile
     KTimer kt(c, HL_K_OTHER, st);
     if (c->N == 4096) {
       constexpr size_t sm = ntt_smem<12>() + 4096;
-      static bool init = false;
-      if (!init) { set_smem(k_encrypt<12>, sm); init = true; }
+      static PerDevice init;
+      if (init.first()) { set_smem(k_encrypt<12>, sm); }
       k_encrypt<12><<<nct, Geom<12>::NT, sm, st>>>(E, ct_in, c->dp, c->d_cdt, c->d_flags);
     } else {
       constexpr size_t sm = ntt_smem<13>() + 8192;
-      static bool init = false;
-      if (!init) { set_smem(k_encrypt<13>, sm); init = true; }
+      static PerDevice init;
+      if (init.first()) { set_smem(k_encrypt<13>, sm); }
       k_encrypt<13><<<nct, Geom<13>::NT, sm, st>>>(E, ct_in, c->dp, c->d_cdt, c->d_flags);
     }
   }
@@ -2398,6 +2372,7 @@ extern "C" int hl_encrypt_device(const hl_ctx *c, const uint64_t *s_hat, hl_tile
 
 extern "C" int hl_decrypt_share_device(const hl_ctx *c, const uint64_t *s_hat, hl_tile tile, const uint64_t *ct_masked,
                                        int64_t Ma, int64_t Nb, uint64_t *share_client, void *stream) {
+  DeviceGuard dg_(c);
   int rc;
   if ((rc = check_ptrs({c, s_hat, ct_masked, share_client}, "hl_decrypt_share_device"))) return rc;
   Geo g;
@@ -2409,13 +2384,13 @@ extern "C" int hl_decrypt_share_device(const hl_ctx *c, const uint64_t *s_hat, h
   KTimer kt(c, HL_K_OTHER, st);
   if (c->N == 4096) {
     const size_t sm = ntt_smem<12>() + res;
-    static bool init = false;
-    if (!init) { set_smem(k_decrypt<12>, 232448); init = true; }
+    static PerDevice init;
+    if (init.first()) { set_smem(k_decrypt<12>, 232448); }
     k_decrypt<12><<<nout, Geom<12>::NT, sm, st>>>(ct_masked, share_client, D, c->dp);
   } else {
     const size_t sm = ntt_smem<13>() + res;
-    static bool init = false;
-    if (!init) { set_smem(k_decrypt<13>, 232448); init = true; }
+    static PerDevice init;
+    if (init.first()) { set_smem(k_decrypt<13>, 232448); }
     k_decrypt<13><<<nout, Geom<13>::NT, sm, st>>>(ct_masked, share_client, D, c->dp);
   }
   return hl_cuda_check("hl_decrypt_share_device: launch");
@@ -2449,6 +2424,7 @@ __global__ void k_share_acc(uint64_t *__restrict__ dst, const uint64_t *__restri
 
 extern "C" int hl_share_accumulate(const hl_ctx *c, uint64_t *dst, const uint64_t *src, int64_t rows, int64_t cols,
                                    int transpose, void *stream) {
+  DeviceGuard dg_(c);
   int rc;
   if ((rc = check_ptrs({c, dst, src}, "hl_share_accumulate"))) return rc;
   if (rows <= 0 || cols <= 0) return hl_fail(HL_EINVAL, "hl_share_accumulate: rows, cols must be positive");
@@ -2481,6 +2457,7 @@ static int fc_geom(const hl_ctx *c, int64_t Nb, int64_t R, int64_t Ma, FcGeom *g
 
 extern "C" int hl_fc_layout(const hl_ctx *c, int64_t Nb, int64_t R, int64_t Ma, int64_t *wplanes_bytes,
                             int64_t *workspace_bytes) {
+  DeviceGuard dg_(c);
   FcGeom g;
   int rc;
   if ((rc = fc_geom(c, Nb, R, Ma, &g))) return rc;
@@ -2491,11 +2468,13 @@ extern "C" int hl_fc_layout(const hl_ctx *c, int64_t Nb, int64_t R, int64_t Ma, 
 
 extern "C" int hl_fc_encode_weights(const hl_ctx *c, const uint64_t *W, int64_t R, int64_t Ma, void *wplanes,
                                     void *stream) {
+  DeviceGuard dg_(c);
   return hl_fc_encode_weights_chk(c, W, R, Ma, wplanes, 1, stream);
 }
 
 extern "C" int hl_fc_encode_weights_chk(const hl_ctx *c, const uint64_t *W, int64_t R, int64_t Ma, void *wplanes,
                                         int check, void *stream) {
+  DeviceGuard dg_(c);
   int rc;
   if ((rc = check_ptrs({c, W, wplanes}, "hl_fc_encode_weights"))) return rc;
   FcGeom g;
@@ -2519,13 +2498,14 @@ extern "C" int hl_fc_encode_weights_chk(const hl_ctx *c, const uint64_t *W, int6
 
 extern "C" int hl_fc_local_share(const hl_ctx *c, const uint64_t *X1, const void *wplanes, const uint64_t *bias,
                                  int64_t Nb, int64_t R, int64_t Ma, void *workspace, uint64_t *share, void *stream) {
+  DeviceGuard dg_(c);
   int rc;
   if ((rc = check_ptrs({c, X1, wplanes, workspace, share}, "hl_fc_local_share"))) return rc;
   FcGeom g;
   if ((rc = fc_geom(c, Nb, R, Ma, &g))) return rc;
   cudaStream_t st = (cudaStream_t)stream;
-  static bool init = false;
-  if (!init) { set_smem(k_fc_gemm, kFcSmem); init = true; }
+  static PerDevice init;
+  if (init.first()) { set_smem(k_fc_gemm, kFcSmem); }
   KTimer kt(c, HL_K_FC, st);
   const int64_t n = (int64_t)g.nMt * kFcMT * g.nKc * 8;
   k_fc_x_planes<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(X1, (uint8_t *)workspace, g);
@@ -2540,6 +2520,7 @@ extern "C" int hl_fc_local_share(const hl_ctx *c, const uint64_t *X1, const void
 // re-randomised responses (reading C22)
 // ---------------------------------------------------------------------------------------
 extern "C" int hl_pk_prepare(const hl_ctx *c, const uint64_t *pk, uint64_t *pk_hat, void *stream) {
+  DeviceGuard dg_(c);
   int rc;
   if ((rc = check_ptrs({c, pk, pk_hat}, "hl_pk_prepare"))) return rc;
   cudaStream_t st = (cudaStream_t)stream;
@@ -2555,6 +2536,7 @@ extern "C" int hl_he_matmul_share_rr(const hl_ctx *c, hl_tile tile, const void *
                                      void *workspace, uint64_t *ct_out_ntt, const uint64_t *pk_hat, int flood_bits,
                                      uint64_t *rr_ws, uint64_t seed, uint64_t *ct_masked, uint64_t *share,
                                      void *stream) {
+  DeviceGuard dg_(c);
   int rc;
   if ((rc = check_ptrs({c, wcache, ct_in, workspace, ct_out_ntt, pk_hat, rr_ws, ct_masked, share},
                        "hl_he_matmul_share_rr")))
@@ -2575,12 +2557,12 @@ extern "C" int hl_he_matmul_share_rr(const hl_ctx *c, hl_tile tile, const void *
   {
     KTimer kt(c, HL_K_INTT_MASK, st);
     if (c->N == 4096) {
-      static bool init = false;
-      if (!init) { set_smem(k_rr_u<12>, ntt_smem<12>() + 4096); init = true; }
+      static PerDevice init;
+      if (init.first()) { set_smem(k_rr_u<12>, ntt_smem<12>() + 4096); }
       k_rr_u<12><<<(unsigned)nout, Geom<12>::NT, ntt_smem<12>() + 4096, st>>>(rr_ws, M, c->dp);
     } else {
-      static bool init = false;
-      if (!init) { set_smem(k_rr_u<13>, ntt_smem<13>() + 8192); init = true; }
+      static PerDevice init;
+      if (init.first()) { set_smem(k_rr_u<13>, ntt_smem<13>() + 8192); }
       k_rr_u<13><<<(unsigned)nout, Geom<13>::NT, ntt_smem<13>() + 8192, st>>>(rr_ws, M, c->dp);
     }
   }
@@ -2594,6 +2576,7 @@ extern "C" int hl_he_linear_host(const hl_ctx *c, hl_tile tile, const void *wcac
                                  uint64_t *ct_masked_host, uint64_t *share_host, uint64_t *dev_ct_in,
                                  void *workspace, uint64_t *dev_ct_out_ntt, uint64_t *dev_ct_masked,
                                  uint64_t *dev_share, void *stream) {
+  DeviceGuard dg_(c);
   int rc;
   if ((rc = check_ptrs({c, wcache, ct_in_host, ct_masked_host, share_host, dev_ct_in, workspace,
                         dev_ct_out_ntt, dev_ct_masked, dev_share}, "hl_he_linear_host")))
@@ -2615,6 +2598,7 @@ extern "C" int hl_he_linear_host(const hl_ctx *c, hl_tile tile, const void *wcac
 
 extern "C" int hl_poly_mul(const hl_ctx *c, const uint64_t *a, const uint64_t *b, uint64_t *out, int64_t npoly,
                            void *scratch, void *stream) {
+  DeviceGuard dg_(c);
   int rc;
   if ((rc = check_ptrs({c, a, b, out, scratch}, "hl_poly_mul"))) return rc;
   if (npoly <= 0) return hl_fail(HL_EINVAL, "hl_poly_mul: npoly must be positive");
@@ -2630,6 +2614,7 @@ extern "C" int hl_poly_mul(const hl_ctx *c, const uint64_t *a, const uint64_t *b
 }
 
 extern "C" int hl_ntt_roundtrip(const hl_ctx *c, uint64_t *x, int64_t npoly, void *scratch, void *stream) {
+  DeviceGuard dg_(c);
   int rc;
   if ((rc = check_ptrs({c, x, scratch}, "hl_ntt_roundtrip"))) return rc;
   if (npoly <= 0) return hl_fail(HL_EINVAL, "hl_ntt_roundtrip: npoly must be positive");

@@ -83,7 +83,6 @@ struct MacTcArgs {
   int N, jc0, njc, accumulate;
   unsigned long long *prof;   // diagnostics (HELINEAR_MAC_PROF): per-CTA cycles spent waiting, by role
   int *sched;                 // work counter (zeroed before the launch; in the caller's workspace)
-  int ko;                     // diagnostics (HELINEAR_MAC_KO bitmask): 1 skip MMAs, 2 skip conversion, 4 skip epilogue math
   int lazy_out;               // 1: outputs only < 2^52 (= residue + k p, k < 4): fine for the inverse NTT's input
   // c1 straight into the compressed response (fused paths, cperm, one launch): columns C >= c1_nK
   // (the c1 halves) are written canonical, in natural evaluation order (reading C26), at
@@ -329,8 +328,8 @@ k_mac_tc(const __grid_constant__ MacTcArgs A, DevParams P) {
     // tiles of <= 64 rows use M = 64 (half the A-operand shared-memory reads per MMA); the
     // accumulator rows then sit in lanes 32(r/16) + r%16 (profiles/r01/microbench_umma_i8.log)
     // M per item: tiles of <= 64 rows (also a short last tile of uneven tiling) use M = 64
-    const uint32_t idesc128 = umma_idesc_u8(128, (A.ko & 8) ? 16 : T::NM);   // ko 8: timing only
-    const uint32_t idesc64 = umma_idesc_u8(64, (A.ko & 8) ? 16 : T::NM);
+    const uint32_t idesc128 = umma_idesc_u8(128, T::NM);
+    const uint32_t idesc64 = umma_idesc_u8(64, T::NM);
     int st = 0;
     uint32_t ph = 0;
     uint32_t tile_no = 0, zseq = 0;
@@ -357,7 +356,6 @@ k_mac_tc(const __grid_constant__ MacTcArgs A, DevParams P) {
           if (elect_one()) {
 #pragma unroll
             for (int a = 0; a < 7; a++) {
-              if (A.ko & 1) break;
               const uint64_t ad = umma_sdesc(a0 + a * plane, lbo_a, 128);
               const uint64_t bd = umma_sdesc(z0, T::ZR * 16, 128);
               umma_i8(dcol + a * CW, ad, bd, idesc, (kk | a) ? 1u : 0u);   // D window shifted by a*CW
@@ -395,7 +393,7 @@ k_mac_tc(const __grid_constant__ MacTcArgs A, DevParams P) {
 #pragma unroll
           for (int qi = 0; qi < QIT; qi++) {
             const int q = ct + qi * 64;
-            if ((A.ko & 2) || q >= CW * 8) break;
+            if (q >= CW * 8) break;
             const int c = q >> 3, h = (q >> 2) & 1, gq = q & 3;
             const int j0 = h * 16 + gq * 4;
             uint32_t lo[4], hi[4];
@@ -448,7 +446,7 @@ k_mac_tc(const __grid_constant__ MacTcArgs A, DevParams P) {
         tc_fence_after();
         // three column groups (d < 5 -> L, 5..8 -> M, 9..12 -> H) loaded and folded one at a time
         uint64_t L[CH], M[CH], H[CH];
-        if (active && !(A.ko & 4)) {
+        if (active) {
           const uint32_t base = tmem + ((uint32_t)(32 * q) << 16) + buf * T::N + hh * CH;
           uint32_t v[5][CH];
 #pragma unroll
@@ -490,7 +488,7 @@ k_mac_tc(const __grid_constant__ MacTcArgs A, DevParams P) {
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(&tempty[buf]);
-        if (active && !(A.ko & 4)) {
+        if (active) {
 #pragma unroll
           for (int c = 0; c < CH; c++) {
             // V = L + M 2^40 + H 2^72 < 2^124 exactly; V mod p = Shoup(V_hi, 2^64 mod p) + (V_lo mod p)

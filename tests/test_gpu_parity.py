@@ -274,10 +274,65 @@ def test_linear_batch_serial_policy_vs_oracle(hl, ctx4096):
         assert np.array_equal(hl.to_host(sh).reshape(es.shape), es)
 
 
+def _sample_tiles(nI, nK, mac_rows):
+    """Output tiles (I, K) covering the MAC's row-tile boundaries (first / last row of every MAC
+    I tile of `mac_rows` rows), both ends of K and an interior point."""
+    Is = {0, nI - 1, nI // 2, (17 * nI) // 29}
+    for t0 in range(0, nI, mac_rows):
+        Is |= {t0, min(nI, t0 + mac_rows) - 1}
+    out = []
+    for n, I in enumerate(sorted(Is)):
+        out.append((I, n % nK))
+    out += [(0, nK - 1), (nI - 1, 0)]
+    return sorted(set(out))
+
+
+def test_linear_batch_c2_vs_oracle_sampled(hl, ctx4096):
+    """The bench's call on the bench's workload: the four c2 products (QKV, O, FF1, FF2) at the
+    planner's tiles through hl_he_linear_batch in the bench's submission order, with uniform
+    full-range ciphertext residues.  For every product, sampled output ciphertexts (compressed
+    response + server share) bit-exact against the oracle's scalar-NTT path + mask, at both sides of
+    every MAC row tile (QKV: nI = 144 in two 72-row M = 128 tiles; FF1: 192 = 2 x 96; O, FF2: one
+    48/192-row tile), every K; repeated twice to catch cross-stream races."""
+    ctx = ctx4096
+    cfg = synth.CONFIGS["c2"]
+    P = _P(ctx)
+    tiles = [tuple(ctx.plan_tile(mm.Ma, mm.R, mm.Nb)) for mm in cfg.matmuls]
+    assert tiles == [cfg.tile_of(mi) for mi in range(len(cfg.matmuls))]
+    ins = _block_inputs(ctx, cfg, tiles=tiles)
+    entries = [dict(wcache=ctx.encode_weights(t, hl.to_device(W)), Ma=mm.Ma, R=mm.R, Nb=mm.Nb, tile=t,
+                    ct_in=hl.to_device(ct_in), seed=seed) for t, (mm, W, ct_in, seed) in zip(tiles, ins)]
+    order = list(cfg.batch_order)
+    exp = []
+    for t, (mm, W, ct_in, seed) in zip(tiles, ins):
+        nI, nJ, nK = ref.tile_counts(t, mm.Ma, mm.R, mm.Nb)
+        nIp = (nI + 15) // 16 * 16
+        rows = (nIp + (nIp + 127) // 128 - 1) // ((nIp + 127) // 128)       # balanced MAC row tiles
+        smp = _sample_tiles(nI, nK, (rows + 7) // 8 * 8)
+        ect = ref.he_matmul_ntt_tiles(P, t, W, ct_in, mm.Nb, smp)
+        em, kept = ref.mask_tiles(P, t, ect, nK, smp, seed, True)
+        exp.append((smp, em, kept, nI, nK))
+    for rep in range(2):
+        outs = ctx.he_linear_batch(cfg.tile, [entries[i] for i in order])
+        _sync()
+        for k, i in enumerate(order):
+            (mm, *_), t, (smp, em, kept, nI, nK) = ins[i], tiles[i], exp[i]
+            m_, r_, n_ = t
+            masked = hl.to_host(outs[k][0]).reshape(nI, nK, -1)
+            share = hl.to_host(outs[k][1]).reshape(mm.Nb, mm.Ma)
+            for o, (I, K) in enumerate(smp):
+                assert np.array_equal(masked[I, K], em[o]), (rep, mm.name, I, K)
+                for kk in range(n_):
+                    for ii in range(m_):
+                        if K * n_ + kk < mm.Nb and I * m_ + ii < mm.Ma:
+                            assert share[K * n_ + kk, I * m_ + ii] == kept[o, kk * m_ + ii], (rep, mm.name, I, K)
+
+
 def test_linear_batch_c2_equals_single_calls(hl, ctx4096):
     """Config c2 at full size in the bench's launch configuration (batch of the four products, each
-    with its planned tile): bit-identical to four he_matmul_share calls (each checked against the
-    oracle by test_bert_base_full_size_sampled), repeated twice to catch cross-stream races."""
+    with its planned tile): bit-identical to four he_matmul_share calls, repeated twice to catch
+    cross-stream races (the batch itself is checked against the oracle by
+    test_linear_batch_c2_vs_oracle_sampled)."""
     ctx = ctx4096
     cfg = synth.CONFIGS["c2"]
     tiles = [cfg.tile_of(mi) for mi in range(len(cfg.matmuls))]
