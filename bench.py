@@ -6,9 +6,13 @@
 A step is one pass of the whole hot path over one BERT-base
 block: for each of the four encrypted products X.W_qkv, X.W_o, X.W_1, H.W_2 -- forward NTT
 of the client's ciphertexts, modular MAC against the cached NTT-domain weights, inverse NTT,
-mask + compression + server share (hl_he_matmul_share).  Weights are encoded once before
-timing (offline, reported separately); input ciphertexts are resident in HBM.  Multi-GPU:
-weak scaling -- every rank runs its own block (independently seeded), no data-path collective.
+mask + compression + server share (hl_he_linear_batch).  Weights are encoded once before
+timing (offline, reported separately); input ciphertexts are resident in HBM.  Multi-GPU
+(default for N > 1, BASELINE config 2 "sharded by output columns"): strong scaling -- the I
+tiles of every product are split over the ranks and the compressed responses are gathered to
+rank 0 point to point inside the timed region (paper_2305_18396_b200/dist.py); `--mode weak`
+runs one independent block per rank instead.  `--config c3|c4` runs the stacks of BASELINE
+configs 3 and 4 (bench_stack.py).
 
 Prints ONE JSON line (rank 0).  `--impl reference` times the CPU oracle (oracle/) on a
 bounded sample of the same workload instead (the reference arm of this tier).
@@ -76,8 +80,70 @@ def counts(cfg, lay_by_mm, tiles):
             inv_bytes=8 * (nI * nC * L * N + nI * nK * L * (m * n + N) + mm.Nb * mm.Ma),
             # whole-path algorithmic bytes (SURVEY.md §8(d) "Bytes")
             path_bytes=8 * (nJ * nK * 2 * L * N + nI * nJ * L * N + nI * nK * L * (N + m * n) + mm.Nb * mm.Ma),
+            # the method's transforms (reading C26: c1 travels in evaluation form, so only the c0
+            # halves are transformed, forward for the inputs, inverse for the outputs)
+            bfly_c0=(nJ * nK + nI * nK) * L * (N // 2) * logN,
         ))
     return out
+
+
+U8_PER_MAC = 49                  # 7 x 7 byte-limb products per modular MAC on the int8 tensor cores
+INT8_PER_BF16 = 2.0              # nominal dense ratio int8 / bf16 (B200_PROFILING.md: 4.5 vs 2.25 PFLOP/s)
+
+
+def peak_rates(peaks):
+    """(HBM B/s, int8 tensor op/s, FP64 butterflies/s) and their sources."""
+    hbm = peaks.get("hbm_gbs")
+    hbm_src = "measured (MEASURED_PEAKS.json hbm_gbs)" if hbm else "fallback 6650 GB/s (B200_PROFILING.md)"
+    hbm = (hbm or 6650.0) * 1e9
+    bf16 = peaks.get("bf16_tflops")
+    tc = (bf16 or 2250.0) * INT8_PER_BF16 * 1e12
+    tc_src = ("MEASURED_PEAKS.json bf16_tflops (burst) x 2 (nominal int8/bf16 ratio)" if bf16
+              else "fallback 4.5 POPS int8 dense (B200_PROFILING.md)")
+    sm_max = peaks.get("sm_max_mhz") or 1965.0
+    bfly = DFMA_PER_CLK_SM * 148 * sm_max * 1e6 / FP64_OPS_PER_BFLY
+    return hbm, tc, bfly, {"hbm": hbm_src, "tc": tc_src,
+                           "fp64": f"DFMA {DFMA_PER_CLK_SM}/clk/SM (tools/microbench/intpipe3.cu) x 148 x sm_max / "
+                                   f"{FP64_OPS_PER_BFLY} FP64 ops per butterfly"}
+
+
+def path_roofline(cnt, ms, peaks):
+    """Whole-path roofline: the slowest of HBM (algorithmic bytes), the int8
+    tensor cores (49 u8 MACs per modular MAC, 2 ops each) and the FP64 pipe (c0 transforms) bounds
+    the step; frac = that bound / the measured time."""
+    hbm, tc, bfly, _ = peak_rates(peaks)
+    t = {"hbm": sum(c["path_bytes"] for c in cnt) / hbm,
+         "tensor": 2 * U8_PER_MAC * sum(c["mac"] for c in cnt) / tc,
+         "fp64": sum(c["bfly_c0"] for c in cnt) / bfly}
+    bound = max(t, key=t.get)
+    return {"t_hbm_ms": t["hbm"] * 1e3, "t_tensor_ms": t["tensor"] * 1e3, "t_fp64_ms": t["fp64"] * 1e3,
+            "bound": bound, "frac": t[bound] * 1e3 / ms,
+            "note": "max(T_hbm, T_tensor, T_fp64) / measured ms per block; the three overlap in the pipeline"}
+
+
+def mac_roofline(cnt, ktimes, peaks):
+    """Roofline object of the dominant kernel k_mac_tc: the binding one of HBM (weight planes +
+    NTT-domain inputs + outputs, per launch) and the int8 tensor cores (49 u8 MACs per modular MAC)."""
+    hbm, tc, _, src = peak_rates(peaks)
+    mac_ms, mac_n = ktimes["mac"]
+    mac_avg_s = mac_ms / max(mac_n, 1) * 1e-3
+    n = len(cnt)
+    per_bytes = sum(c["mac_bytes_tc"] for c in cnt) / n
+    per_ops = 2 * U8_PER_MAC * sum(c["mac"] for c in cnt) / n
+    if per_ops / tc > per_bytes / hbm:
+        roof = {"bound": "tensor", "achieved": per_ops / mac_avg_s / 1e12, "peak": tc / 1e12, "unit": "TOPS (int8)",
+                "peak_source": src["tc"]}
+    else:
+        roof = {"bound": "hbm", "achieved": per_bytes / mac_avg_s / 1e9, "peak": hbm / 1e9, "unit": "GB/s",
+                "peak_source": src["hbm"]}
+    roof["frac"] = roof["achieved"] / roof["peak"]
+    roof["hbm_frac_same_kernel"] = per_bytes / mac_avg_s / hbm
+    roof["tensor_frac_same_kernel"] = per_ops / mac_avg_s / tc
+    roof["algorithmic_bytes_per_launch"] = per_bytes
+    roof["algorithmic_int8_ops_per_launch"] = per_ops
+    roof["kernel"] = "k_mac_tc (slot-parallel modular MAC, int8 tensor cores)"
+    roof["traffic"] = None
+    return roof
 
 
 # ----------------------------------------------------------------------------- clocks sampler
@@ -145,10 +211,12 @@ def run_ours(args, rank, world, local_rank):
         tiles = [tuple(ctx.plan_tile(mm.Ma, mm.R, mm.Nb)) for mm in cfg.matmuls]
     elif not args.tile and not args.tiles and cfg.tiles:    # the bench's tiles are the library planner's choices (hl_plan_tile)
         assert all(ctx.plan_tile(mm.Ma, mm.R, mm.Nb) == t for mm, t in zip(cfg.matmuls, tiles)), 'planner drift'
-    shard = args.mode == "shard"
-    # weak: every rank owns one independently seeded block, no data-path collective.
-    # shard: one block; its I tiles (output columns) are split over the ranks,
-    #        the compressed responses and share columns are gathered to rank 0 (NCCL) every step.
+    # shard (the default for N > 1, BASELINE config 2 "sharded by output columns"): one block; the I
+    #   tiles (output columns) of its four products are split over the ranks, every
+    #   rank runs hl_he_linear_batch on its shards and the compressed responses are gathered to rank 0
+    #   point to point, overlapped with the next step's compute (two alternating output sets).
+    # weak (--mode weak): every rank owns one independently seeded block, no data-path collective.
+    shard = args.mode == "shard" or (args.mode == "auto" and world > 1)
     block = 0 if shard else rank
     stream = torch.cuda.current_stream()
 
@@ -194,16 +262,33 @@ def run_ours(args, rank, world, local_rank):
     out_words = max(m["lay"].ct_out_words for m in mats)
     workspace = torch.empty(ws_words, dtype=torch.int64, device=dev)
     ct_out_ntt = torch.empty(out_words, dtype=torch.int64, device=dev)
-    for m in mats:
-        m["masked"] = torch.empty(m["lay"].ct_masked_words, dtype=torch.int64, device=dev)
-        m["share"] = torch.zeros(m["lay"].share_words, dtype=torch.int64, device=dev)
+    nsets = 2 if shard and world > 1 else 1          # output sets alternate between steps when gathering
+    gathers, full = [], [[None] * len(mats) for _ in range(nsets)]
+    for mi, m in enumerate(mats):
+        mm, tile = m["mm"], m["tile"]
+        per_ct = cfg.L * (tile[0] * tile[2] + cfg.N)
+        m["per_ct"] = per_ct
+        m["sets"] = []
+        if shard and world > 1:
+            g = hd.ResponseGather(m["nI_full"], m["lay"].nK, per_ct, dst=0)
+            gathers.append(g)
+        for si in range(nsets):
+            if shard and world > 1 and rank == 0:       # rank 0 computes its rows in place in the full buffer
+                full[si][mi] = torch.empty(m["nI_full"] * m["lay"].nK * per_ct, dtype=torch.int64, device=dev)
+                w0, w1 = gathers[-1].words(0)
+                masked = full[si][mi][w0:w1]
+            else:
+                masked = torch.empty(max(m["lay"].ct_masked_words, 1), dtype=torch.int64, device=dev)
+            m["sets"].append((masked, torch.zeros(m["lay"].share_words, dtype=torch.int64, device=dev)))
+        m["masked"], m["share"] = m["sets"][0]
 
     # every product gets its own scratch: the batch call pipelines them over two streams
     for m in mats:
         m["ws"] = torch.empty(m["lay"].workspace_bytes // 8, dtype=torch.int64, device=dev)
         m["co"] = torch.empty(m["lay"].ct_out_words, dtype=torch.int64, device=dev)
     entries = [dict(wcache=m["wc"], Ma=m["mm"].Ma, R=m["mm"].R, Nb=m["mm"].Nb, ct_in=m["ct"], seed=m["seed"], tile=m["tile"],
-                    workspace=m["ws"], ct_out_ntt=m["co"], ct_masked=m["masked"], share=m["share"]) for m in mats]
+                    workspace=m["ws"], ct_out_ntt=m["co"], ct_masked=m["masked"], share=m["share"],
+                    i_begin=m["i0"], i_end=m["i1"]) for m in mats]
 
     # the four products are independent: submit them in the order measured fastest for the pipeline
     # (tools/gpu/order_sweep.sh, all 24 orders; synth Config.batch_order)
@@ -213,17 +298,19 @@ def run_ours(args, rank, world, local_rank):
     e2e_order = ([int(x) for x in os.environ["BENCH_E2E_ORDER"].split(",")] if os.environ.get("BENCH_E2E_ORDER")
                  else list(cfg.e2e_order) if cfg.e2e_order else order)
 
+    pending = [[] for _ in range(nsets)]
+    nstep = [0]
+
     def step():
         if shard:
-            for m in mats:
-                mm, tile = m["mm"], m["tile"]
-                per_ct = cfg.L * (tile[0] * tile[2] + cfg.N)
-                ctx.he_matmul_share(tile, m["wc"], mm.Ma, mm.R, mm.Nb, m["ct"], m["seed"], True, m["i0"], m["i1"],
-                                    workspace=workspace, ct_out_ntt=ct_out_ntt, ct_masked=m["masked"],
-                                    share=m["share"], stream=stream)
-                if world > 1:
-                    hd.gather_responses(m["masked"], m["share"], m["lay"].nI, m["lay"].nK, per_ct, tile, mm.Ma,
-                                        mm.Nb, dst=0)
+            si = nstep[0] % nsets
+            nstep[0] += 1
+            for w in pending[si]:          # the gather that last read this output set is done
+                w.wait()
+            ents = [dict(entries[i], ct_masked=mats[i]["sets"][si][0], share=mats[i]["sets"][si][1]) for i in order]
+            ctx.he_linear_batch(tiles[0], ents, stream=stream)
+            if world > 1:                  # P2P to rank 0 on NCCL's stream, overlapping the next step
+                pending[si] = [w for i in order for w in gathers[i].post(mats[i]["sets"][si][0], full[si][i])]
         elif args.sequential:
             for m in mats:
                 mm, tile = m["mm"], m["tile"]
@@ -262,6 +349,10 @@ def run_ours(args, rank, world, local_rank):
     ev0.record(stream)
     for _ in range(args.steps):
         step()
+    for ws_ in pending:                    # the timed region ends when rank 0 holds every response
+        for w in ws_:
+            w.wait()
+    pending = [[] for _ in range(nsets)]
     ev1.record(stream)
     torch.cuda.synchronize()
     barrier()
@@ -454,7 +545,7 @@ def run_ours(args, rank, world, local_rank):
 
     # weak mode: the pipelined seeded batch (hl_he_linear_batch_host): c0 halves + public seeds
     # up, c1 regenerated on the device, compressed responses + shares down, overlapped per product
-    up_bufs = [torch.empty(m["lay"].ct_in_words, dtype=torch.int64, device=dev) for m in mats] if not shard else []
+    up_bufs = [torch.empty(m["lay"].ct_in_words, dtype=torch.int64, device=dev) for m in mats]
     c0_up = [torch.from_numpy(hl.Context.pack50(m["c0_host"].numpy().view(np.uint64)).view(np.int64)).pin_memory()
              if packed else m["c0_host"] for m in mats]
     # own device output buffers: the check below compares the e2e results with the device batch's
@@ -462,14 +553,34 @@ def run_ours(args, rank, world, local_rank):
                          ct_masked=torch.empty_like(m["masked"]), share=torch.zeros_like(m["share"]))
                     for e, m, u, c0, hm, hs in zip(entries, mats, up_bufs, c0_up, host_masked, host_share)]
 
+    # shard mode: every rank uploads the c0 halves into its ct_in and regenerates c1 from the public
+    # seed (hl_expand_seeded), runs its shards (hl_he_linear_batch), the responses are gathered to
+    # rank 0 (P2P) and rank 0 downloads the whole block's responses; every rank downloads the server
+    # share of its own columns (the server's output share stays on its rank)
+    if shard:
+        host_full = [torch.empty(m["nI_full"] * m["lay"].nK * m["per_ct"], dtype=torch.int64).pin_memory()
+                     if rank == 0 else None for m in mats]
+        mwords = [m["nI_full"] * m["lay"].nK * m["per_ct"] if rank == 0 else 0 for m in mats]
+
     def e2e_step():
         if not shard:
             ctx.he_linear_batch_host(tiles[0], [host_entries[i] for i in e2e_order], stream=stream)
             return
-        for m, hm, hs in zip(mats, host_masked, host_share):
-            mm = m["mm"]
-            ctx.he_linear_host(m["tile"], m["wc"], mm.Ma, mm.R, mm.Nb, m["ct_host"], m["seed"], hm, hs, dev_ct_in,
-                               workspace, ct_out_ntt, m["masked"], m["share"], compress=True, stream=stream)
+        LN = cfg.L * cfg.N
+        for i in order:
+            m, u = mats[i], up_bufs[i]
+            u.view(-1, 2, LN)[:, 0].copy_(m["c0_host"].view(-1, LN), non_blocking=True)
+            ctx.expand_seeded(m["tile"], m["mm"].R, m["mm"].Nb, m["a_seed"], u, stream=stream)
+        ents = [dict(entries[i], ct_in=up_bufs[i], ct_masked=mats[i]["sets"][0][0], share=mats[i]["sets"][0][1])
+                for i in order]
+        ctx.he_linear_batch(tiles[0], ents, stream=stream)
+        works = [w for i in order for w in gathers[i].post(mats[i]["sets"][0][0], full[0][i])] if world > 1 else []
+        for w in works:
+            w.wait()
+        for i in order:
+            if rank == 0:
+                host_full[i].copy_(full[0][i] if world > 1 else mats[i]["sets"][0][0], non_blocking=True)
+            host_share[i].copy_(mats[i]["sets"][0][1], non_blocking=True)
 
     e2e_steps = max(3, min(args.steps, 20))
     for _ in range(2):
@@ -493,7 +604,7 @@ def run_ours(args, rank, world, local_rank):
     torch.cuda.synchronize()
     barrier()
     e2e_ms = max_over_ranks(e0.elapsed_time(e1)) / e2e_steps
-    h2d = sum(c0.numel() * 8 for c0 in c0_up) if not shard else sum(m["lay"].ct_in_words * 8 for m in mats)
+    h2d = sum(c0.numel() * 8 for c0 in c0_up) if not shard else sum(m["c0_host"].numel() * 8 for m in mats)
     d2h = sum((w + m["lay"].share_words) * 8 for w, m in zip(mwords, mats))
 
     if rank != 0:
@@ -505,49 +616,15 @@ def run_ours(args, rank, world, local_rank):
     cnt = counts(cfg, [m["lay"] for m in mats], tiles)
     products = sum(c["products"] for c in cnt)
     peaks = _peaks()
-    hbm = peaks.get("hbm_gbs")
-    hbm_src = "measured (MEASURED_PEAKS.json hbm_gbs)" if hbm else "fallback 6650 GB/s (B200_PROFILING.md)"
-    hbm = hbm or 6650.0
-    sm_max = (peaks.get("sm_max_mhz") or 1965.0)
-    # ALU peaks, measured on this B200 by tools/microbench/intpipe3.cu
-    # (profiles/r01/microbench_intpipe3.log): IMAD.WIDE.U32 24.4 /clk/SM (the IMAD engine's
-    # multiply), DFMA 57.3 /clk/SM (the default FP64 engine); x 148 SMs x max SM clock.
-    engine = "tc"
-    if engine == "tc":
-        ops_per_mac, alu_peak, alu_unit = 0.0, 1.0, ""
-    elif engine == "imad":
-        ops_per_mac, alu_peak, alu_unit = 3.0, IMAD_WIDE_PER_CLK_SM * 148 * sm_max * 1e6, "T IMAD.WIDE/s (3 per modular MAC)"
-    else:
-        ops_per_mac, alu_peak, alu_unit = FP64_OPS_PER_MAC, DFMA_PER_CLK_SM * 148 * sm_max * 1e6, \
-            "T FP64 op/s (4.125 per modular MAC)"
-    mac_ms, mac_n = ktimes["mac"]
-    mac_avg_s = mac_ms / max(mac_n, 1) * 1e-3
-    per_launch_mac = sum(c["mac"] for c in cnt) / len(cnt)
-    per_launch_bytes = sum(c["mac_bytes_tc" if engine == "tc" else "mac_bytes"] for c in cnt) / len(cnt)
-    # bound of the MAC kernel: the slower of the ALU pipe and HBM (the tensor-core engine's int8
-    # MMA time is < 1/3 of its HBM time at these shapes: HBM-bound)
-    t_alu = ops_per_mac * per_launch_mac / alu_peak
-    t_hbm = per_launch_bytes / (hbm * 1e9)
-    if t_alu >= t_hbm:
-        roof = {"bound": "alu", "achieved": ops_per_mac * per_launch_mac / mac_avg_s / 1e12, "peak": alu_peak / 1e12,
-                "unit": alu_unit}
-    else:
-        roof = {"bound": "hbm", "achieved": per_launch_bytes / mac_avg_s / 1e9, "peak": hbm, "unit": "GB/s"}
-    roof["frac"] = roof["achieved"] / roof["peak"]
-    roof["traffic"] = None
+    hbm = (peaks.get("hbm_gbs") or 6650.0)
+    roof = mac_roofline(cnt, ktimes, peaks)
     try:   # per-launch DRAM bytes of the same kernel from the committed ncu --set full capture
         tr = json.load(open(os.path.join(ROOT, "profiles", "traffic.json")))
-        if tr.get("kernel") in roof.get("kernel", "") or engine == "tc" and tr.get("kernel") == "k_mac_tc":
+        if tr.get("kernel") == "k_mac_tc" and tr.get("config", "c2") == cfg.name:
             roof["traffic"] = tr["per_launch_bytes"]
             roof["traffic_source"] = tr["source"]
-            roof["algorithmic_bytes_per_launch"] = per_launch_bytes
     except Exception:
         pass
-    roof["kernel"] = {"tc": "k_mac_tc", "f64": "k_mac_f64", "imad": "k_mac"}[engine] + " (slot-parallel modular MAC)"
-    roof["peak_source"] = (("measured DFMA 57.3" if engine != "imad" else "measured IMAD.WIDE 24.4") +
-                           "/clk/SM x 148 SMs x sm_max_mhz (DESIGN.md §6)" if roof["bound"] == "alu" else hbm_src)
-    roof["engine"] = engine
-    roof["hbm_frac_same_kernel"] = per_launch_bytes / mac_avg_s / 1e9 / hbm
     total_k = sum(v[0] for v in ktimes.values())
     kernel_share = {k: {"ms_per_step": v[0] / args.steps, "launches_per_step": v[1] / args.steps,
                         "share": v[0] / total_k if total_k else None} for k, v in ktimes.items() if v[1]}
@@ -574,13 +651,16 @@ def run_ours(args, rank, world, local_rank):
                                 else products * world) * args.steps / (elapsed * 1e-3),
         "path_bytes_per_block": path_bytes,
         "path_hbm_frac": path_bytes / (value * 1e-3) / (hbm * 1e9),
+        "path_roofline": path_roofline(cnt, value, peaks),
         "roofline": roof,
         "kernels": kernel_share,
         "gpu_launches": launches,
         "encode_weights_ms": round(t_enc * 1e3, 3),
         "e2e": {"value": round(e2e_ms, 4), "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
-                "call": "hl_he_linear_host per product (shard mode)" if shard else
-                        "hl_he_linear_batch_host: seeded upload (c0 halves + encryption seed; c1 = a regenerated on "
+                "call": ("shard mode: c0 halves H2D into every rank's ct_in + hl_expand_seeded (public seed), "
+                         "hl_he_linear_batch on the rank's I shards, P2P gather of the responses to rank 0, D2H of "
+                         "the whole block's responses on rank 0 and of each rank's share") if shard else
+                        "hl_he_linear_batch_host: seeded upload (c0 halves + public seed; c1 = a regenerated on "
                         "the device), upload / compute / download pipelined per product" +
                         (", 50-bit wire format both ways (hl_pack50)" if packed else ""),
                 "checked_equal_to_device_path": e2e_checked},
@@ -658,16 +738,26 @@ def run_reference(args, rank, world):
     cfg = synth.CONFIGS[args.config]
     tiles = _tiles(cfg, args)
     vals = []
-    # the same bounded sample as our arm's cpu_baseline (first 2 I tiles x all K tiles of each product:
-    # 32 output ciphertexts, enough OpenMP tasks for the host's cores), extrapolated to the block
+    if cfg.blocks > 1:      # c3 / c4: the stack sampler of our arm's cpu_baseline (bench_stack.py)
+        import bench_stack
+        import paper_2305_18396_b200 as hl
+        hctx = hl.Context(cfg.N, cfg.L, synth.T_BITS, device=-1)
+        tiles, _ = bench_stack.choose_tiles(hctx, cfg, cfg.blocks, 178.35 * 2**30, args.tile)   # ours at N = 1
+        sample = lambda: bench_stack.stack_oracle_baseline(cfg, tiles, args.cpu_frac)   # noqa: E731
+        base = bench_stack.stack_oracle_baseline.__doc__
+    else:
+        # the same bounded sample as our arm's cpu_baseline (first 2 I tiles x all K tiles of each product:
+        # 32 output ciphertexts, enough OpenMP tasks for the host's cores), extrapolated to the block
+        sample = lambda: oracle_baseline(cfg, tiles, 2, 0)       # noqa: E731
+        base = oracle_baseline.__doc__
     for _ in range(min(args.warmup, 1)):
-        oracle_baseline(cfg, tiles, 2, 0)
+        sample()
     t0 = time.perf_counter()
     for _ in range(args.steps):
-        vals.append(oracle_baseline(cfg, tiles, 2, 0)["value"])
+        s_ = sample()
+        vals.append(s_["value"])
     wall = time.perf_counter() - t0
     v = float(np.mean(vals))
-    base = oracle_baseline.__doc__
     cores = len(os.sched_getaffinity(0))
     return {"metric": METRIC, "value": round(v, 1), "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": round(v, 1), "higher_is_better": False, "scaling": "weak",
@@ -675,8 +765,7 @@ def run_reference(args, rank, world):
             "config": {"workload": f"{cfg.name}: {cfg.note}", "N": cfg.N, "L": cfg.L, "t_bits": synth.T_BITS,
                        "tile": [list(t) for t in tiles], "parallelism": "CPU oracle, OpenMP over output tiles"},
             "cpu_baseline": {"value": round(v, 1), "unit": UNIT, "cores": cores, "kind": "oracle",
-                             "sample": "per step: the first 2 I tiles x all K tiles of each of the 4 matmuls, "
-                                       "extrapolated linearly to the block",
+                             "sample": s_["sample"],
                              "cpu": _cpu_model(),
                              "wall_s": round(wall, 2)},
             "e2e": {"value": round(v, 1), "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -684,6 +773,8 @@ def run_reference(args, rank, world):
 
 
 def main():
+    # the stacks allocate tens of GB in few large buffers: avoid allocator fragmentation (c4 fills HBM)
+    os.environ.setdefault("PYTORCH_CUDA_ALLOC_CONF", "expandable_segments:True")
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=50)
@@ -694,11 +785,16 @@ def main():
     ap.add_argument("--tiles", default=None, help='per-product tiles, e.g. "32,8,16;8,8,64;32,8,16;8,16,32"')
     ap.add_argument("--plan", action="store_true", help="every product at hl_plan_tile's tile")
     ap.add_argument("--cpu-itiles", type=int, default=2)
+    ap.add_argument("--cpu-frac", type=float, default=None,
+                    help="c3/c4: sampled fraction of one block's output ciphertexts for the oracle baseline "
+                         "(default c3 1 %%, c4 0.2 %%)")
+    ap.add_argument("--e2e-items", type=int, default=1, help="c4: items measured end to end (scaled to the stack)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--sequential", action="store_true", help="one he_matmul_share per product (no 2-stream pipeline)")
     ap.add_argument("--no-attention", action="store_true", help="skip the row-f2 attention measurement")
-    ap.add_argument("--mode", choices=["weak", "shard"], default="weak",
-                    help="weak: one block per rank; shard: one block split by I tiles + gather to rank 0")
+    ap.add_argument("--mode", choices=["auto", "weak", "shard"], default="auto",
+                    help="auto: shard for N > 1 (BASELINE config 2: sharded by output columns), the whole block "
+                         "at N = 1; weak: one block per rank; shard: one block split by I tiles + gather to rank 0")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "ours":
         args.warmup = 3
@@ -711,8 +807,14 @@ def main():
         import torch.distributed as dist
         torch.cuda.set_device(local_rank)
         dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    stack = synth.CONFIGS[args.config].blocks > 1
+    if args.cpu_frac is None:
+        args.cpu_frac = 0.002 if args.config == "c4" else 0.01
     if args.impl == "reference":
         line = run_reference(args, rank, world)
+    elif stack:
+        import bench_stack
+        line = bench_stack.run_stack(args, rank, world, local_rank, sys.modules[__name__])
     else:
         line = run_ours(args, rank, world, local_rank)
     if rank == 0 and line is not None:

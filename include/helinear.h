@@ -251,7 +251,11 @@ int hl_he_matmul_share(const hl_ctx *ctx, hl_tile tile, const void *wcache, int6
                        void *workspace, uint64_t *ct_out_ntt, uint64_t seed, int compress,
                        uint64_t *ct_masked, uint64_t *share_server, void *stream);
 
-/* One entry of hl_he_linear_batch: a whole product (shard [0, nI)), compressed responses. */
+/* One entry of hl_he_linear_batch: a product or an I-tile shard [i_begin, i_end) of it (the column
+ * split of SURVEY.md §8(e): wcache holds that shard, ct_masked its nI_shard x nK responses, share
+ * only its columns are written; mask streams use the global I, so shards are bit-identical slices
+ * of the whole product), compressed responses.  i_end = -1 means nI; i_begin == i_end: the entry
+ * is skipped (an empty shard of a rank when nI < ranks). */
 typedef struct {
   const void *wcache;         /* hl_encode_weights output for this (Ma, R), device                */
   int64_t Ma, R, Nb;
@@ -262,6 +266,7 @@ typedef struct {
   uint64_t *ct_masked;        /* device, layout.ct_masked_words (compressed response)              */
   uint64_t *share;            /* device [Nb][Ma] server share                                      */
   hl_tile tile;               /* this product's tile; m == 0: the tile argument of the batch call  */
+  int64_t i_begin, i_end;     /* I-tile shard (0, -1: the whole product)                           */
 } hl_linear_desc;
 
 /* n compressed hl_he_matmul_share calls, e.g. the four products of an encoder block; results are

@@ -63,7 +63,7 @@ class LinearDesc(ctypes.Structure):
     _fields_ = [("wcache", ctypes.c_void_p), ("Ma", ctypes.c_int64), ("R", ctypes.c_int64), ("Nb", ctypes.c_int64),
                 ("ct_in", ctypes.c_void_p), ("workspace", ctypes.c_void_p), ("ct_out_ntt", ctypes.c_void_p),
                 ("seed", ctypes.c_uint64), ("ct_masked", ctypes.c_void_p), ("share", ctypes.c_void_p),
-                ("tile", Tile)]
+                ("tile", Tile), ("i_begin", ctypes.c_int64), ("i_end", ctypes.c_int64)]
 
 
 class LinearHostDesc(ctypes.Structure):
@@ -401,8 +401,8 @@ class Context:
     def he_linear_batch(self, tile, entries, stream=None):
         """Pipelined compressed he_matmul_share over several products (hl_he_linear_batch).
         entries: dicts with wcache, Ma, R, Nb, ct_in, seed and optionally tile (this product's tile;
-        default: `tile`), workspace, ct_out_ntt, ct_masked, share (allocated here if absent; every
-        entry gets its own buffers).
+        default: `tile`), i_begin / i_end (an I-tile shard, default the whole product), workspace,
+        ct_out_ntt, ct_masked, share (allocated here if absent; every entry gets its own buffers).
         Returns [(ct_masked, share), ...]."""
         descs = (LinearDesc * len(entries))()
         keep, outs = [], []
@@ -416,7 +416,8 @@ class Context:
         import torch
         Ma, R, Nb = int(e["Ma"]), int(e["R"]), int(e["Nb"])
         tile = tuple(e["tile"]) if e.get("tile") is not None else tuple(tile)
-        lay = self.layout(tile, Ma, R, Nb)
+        i0, i1 = int(e.get("i_begin", 0)), int(e.get("i_end", -1))
+        lay = self.layout(tile, Ma, R, Nb, i0, i1)
         dev = e["ct_in"].device
         ws = e.get("workspace") if e.get("workspace") is not None else _dev_empty(lay.workspace_bytes // 8, dev)
         co = e.get("ct_out_ntt") if e.get("ct_out_ntt") is not None else _dev_empty(lay.ct_out_words, dev)
@@ -426,6 +427,7 @@ class Context:
         d.ct_in, d.workspace, d.ct_out_ntt = _dptr(e["ct_in"]), _dptr(ws), _dptr(co)
         d.seed, d.ct_masked, d.share = int(e["seed"]), _dptr(cm), _dptr(sh)
         d.tile = _tile(tile)
+        d.i_begin, d.i_end = i0, i1
         keep += [ws, co]
         outs.append((cm, sh))
 

@@ -249,6 +249,8 @@ extern "C" int hl_ctx_create(uint32_t N, uint32_t L, uint32_t log2_t, const uint
       cudaFree(c->d_tw); cudaFree(c->d_flags); delete c;
       return hl_cuda_check("hl_ctx_create: pipeline streams");
     }
+    c->ev_pool[0] = new std::vector<void *>();
+    c->ev_pool[1] = new std::vector<void *>();
     c->aux_stream = (void *)aux;
     c->mac_stream = (void *)mac;
     c->up_stream = (void *)up;
@@ -328,6 +330,11 @@ extern "C" int hl_ctx_destroy(hl_ctx *c) {
     for (void *e : c->timing->pool) cudaEventDestroy((cudaEvent_t)e);
     for (auto &r : c->timing->rec) { cudaEventDestroy((cudaEvent_t)r.second.first); cudaEventDestroy((cudaEvent_t)r.second.second); }
     delete c->timing;
+  }
+  for (auto *pool : c->ev_pool) {
+    if (!pool) continue;
+    for (void *e : *pool) cudaEventDestroy((cudaEvent_t)e);
+    delete pool;
   }
   if (c->aux_stream) cudaStreamDestroy((cudaStream_t)c->aux_stream);
   if (c->mac_stream) cudaStreamDestroy((cudaStream_t)c->mac_stream);

@@ -78,6 +78,9 @@ struct hl_ctx {
   void *up_stream = nullptr;          // cudaStream_t (non-blocking): hl_he_linear_batch_host's uploads
   void *down_stream = nullptr;        // cudaStream_t (non-blocking): hl_he_linear_batch_host's downloads
   TimingState *timing = nullptr;      // owned; mutable through const hl_ctx*
+  // cached cudaEvent_t of the batch calls (0: hl_he_linear_batch's pipeline, 1: the host batch's
+  // copy stages), created on first use and reused: a call records and waits on them in stream order
+  std::vector<void *> *ev_pool[2] = {nullptr, nullptr};   // owned; mutable through const hl_ctx*
 };
 
 // RAII event pair around one kernel launch when timing is on

@@ -2099,6 +2099,17 @@ extern "C" int hl_he_matmul_share(const hl_ctx *c, hl_tile tile, const void *wca
 // inverse NTT + mask of entry i on the low-priority auxiliary stream once MAC(i) is done;
 // `stream` is joined to all of them at the start and at the end.
 // ---------------------------------------------------------------------------------------
+// n events of the context's pool `which` (grown on demand, never destroyed before the context)
+static cudaEvent_t *ctx_events(const hl_ctx *c, int which, size_t n) {
+  std::vector<void *> &pool = *c->ev_pool[which];
+  while (pool.size() < n) {
+    cudaEvent_t e;
+    if (cudaEventCreateWithFlags(&e, cudaEventDisableTiming) != cudaSuccess) return nullptr;
+    pool.push_back((void *)e);
+  }
+  return reinterpret_cast<cudaEvent_t *>(pool.data());
+}
+
 // ready[i] (optional): event the forward NTT of entry i waits for (its input upload);
 // done[i] (optional): recorded on the auxiliary stream once entry i's results are written.
 // expand_seed (optional, with ready): per entry, the c1 halves are regenerated from this seed on the
@@ -2110,11 +2121,20 @@ static int linear_batch_run(const hl_ctx *c, hl_tile tile, int n, const hl_linea
   int rc;
   struct Entry { Geo g; MacGeom mg; MaskArgs M; };
   std::vector<Entry> E(n);
+  std::vector<int> ord;     // compute order = entry order of the non-empty entries (the caller's choice:
+                            // the bench submits the order measured fastest, synth Config.batch_order)
   for (int i = 0; i < n; i++) {
+    if (d[i].i_end >= 0 && d[i].i_begin == d[i].i_end) {        // an empty I-tile shard: nothing to do
+      if (ready || done) return hl_fail(HL_EINVAL, "hl_he_linear_batch_host: empty shards are not supported");
+      continue;
+    }
     if ((rc = check_ptrs({c, d[i].wcache, d[i].ct_in, d[i].workspace, d[i].ct_out_ntt, d[i].ct_masked, d[i].share},
                          "hl_he_linear_batch")))
       return rc;
-    if ((rc = hl_geometry(c, d[i].tile.m ? d[i].tile : tile, d[i].Ma, d[i].R, d[i].Nb, 0, -1, &E[i].g))) return rc;
+    if ((rc = hl_geometry(c, d[i].tile.m ? d[i].tile : tile, d[i].Ma, d[i].R, d[i].Nb, d[i].i_begin, d[i].i_end,
+                          &E[i].g)))
+      return rc;
+    ord.push_back(i);
     E[i].mg = mac_geom(c, E[i].g.nIs, E[i].g.nJ, 2 * E[i].g.nK);
     E[i].mg.cperm = E[i].mg.engine == 2;
     E[i].M = mask_args(E[i].g, d[i].Ma, d[i].Nb, d[i].seed);
@@ -2124,10 +2144,9 @@ static int linear_batch_run(const hl_ctx *c, hl_tile tile, int n, const hl_linea
     if (E[i].mg.c1_in && E[i].mg.nCg == 1) E[i].mg.xw = (int)E[i].g.nK;
   }
   cudaStream_t sc = (cudaStream_t)stream, s0 = (cudaStream_t)c->mac_stream, s1 = (cudaStream_t)c->aux_stream;
-  std::vector<cudaEvent_t> ev(2 * n + 3);
-  for (auto &e : ev)
-    if (cudaEventCreateWithFlags(&e, cudaEventDisableTiming) != cudaSuccess) return hl_cuda_check("hl_he_linear_batch: events");
-  cudaEvent_t *e_fwd = ev.data(), *e_mac = ev.data() + n, e_in = ev[2 * n], e_done = ev[2 * n + 1];
+  cudaEvent_t *ev = ctx_events(c, 0, 2 * (size_t)n + 3);
+  if (!ev) return hl_cuda_check("hl_he_linear_batch: events");
+  cudaEvent_t *e_fwd = ev, *e_mac = ev + n, e_in = ev[2 * n], e_done = ev[2 * n + 1];
   cudaEvent_t e_macs = ev[2 * n + 2];
   // every forward NTT is issued up front on the forward stream (measured: 1.082 -> 1.060 ms per c2
   // block vs interleaving them with the MACs)
@@ -2136,7 +2155,7 @@ static int linear_batch_run(const hl_ctx *c, hl_tile tile, int n, const hl_linea
   // the other on the forward / MAC / inverse streams without the cross-product overlap
   constexpr int serial_nk = 8;
   bool serial = !ready;
-  for (int i = 0; i < n; i++) serial = serial && E[i].g.nK >= serial_nk;
+  for (int i : ord) serial = serial && E[i].g.nK >= serial_nk;
   cudaStream_t sf = (cudaStream_t)c->fwd_stream;
   auto fwd = [&](int i) {
     if (ready) cudaStreamWaitEvent(sf, ready[i], 0);
@@ -2149,11 +2168,10 @@ static int linear_batch_run(const hl_ctx *c, hl_tile tile, int n, const hl_linea
     if (c->N == 4096) launch_inv_mask<12>(c, d[i].ct_out_ntt, d[i].ct_masked, d[i].share, E[i].M, E[i].g.nIs * E[i].g.nK, s1);
     else launch_inv_mask<13>(c, d[i].ct_out_ntt, d[i].ct_masked, d[i].share, E[i].M, E[i].g.nIs * E[i].g.nK, s1);
   };
-  // compute order = entry order (the caller's choice: tools/gpu/order_sweep.sh measures all orders)
-  std::vector<int> ord(n);
-  for (int i = 0; i < n; i++) ord[i] = i;
+  const int na = (int)ord.size();
+  if (na == 0) return HL_OK;
   if (serial) {                                   // the products one after the other on `stream`
-    for (int k = 0; k < n; k++) {
+    for (int k = 0; k < na; k++) {
       const int i = ord[k];
       fwd_ntt(c, d[i].ct_in, d[i].workspace, E[i].g.nJ * 2 * E[i].g.nK, &E[i].mg, sc);
       launch_mac(c, (const uint2 *)d[i].wcache, (const uint32_t *)d[i].workspace, d[i].ct_out_ntt, E[i].mg, sc,
@@ -2161,15 +2179,14 @@ static int linear_batch_run(const hl_ctx *c, hl_tile tile, int n, const hl_linea
       if (c->N == 4096) launch_inv_mask<12>(c, d[i].ct_out_ntt, d[i].ct_masked, d[i].share, E[i].M, E[i].g.nIs * E[i].g.nK, sc);
       else launch_inv_mask<13>(c, d[i].ct_out_ntt, d[i].ct_masked, d[i].share, E[i].M, E[i].g.nIs * E[i].g.nK, sc);
     }
-    for (auto &e : ev) cudaEventDestroy(e);
     return hl_cuda_check("hl_he_linear_batch: launch");
   }
   cudaEventRecord(e_in, sc);                      // inputs written on `stream` are visible to both streams
   cudaStreamWaitEvent(s0, e_in, 0);
   cudaStreamWaitEvent(s1, e_in, 0);
   cudaStreamWaitEvent(sf, e_in, 0);
-  for (int k = 0; k < n; k++) fwd(ord[k]);
-  for (int k = 0; k < n; k++) {
+  for (int k = 0; k < na; k++) fwd(ord[k]);
+  for (int k = 0; k < na; k++) {
     const int i = ord[k];
     cudaStreamWaitEvent(s0, e_fwd[i], 0);
     launch_mac(c, (const uint2 *)d[i].wcache, (const uint32_t *)d[i].workspace, d[i].ct_out_ntt, E[i].mg, s0,
@@ -2184,7 +2201,6 @@ static int linear_batch_run(const hl_ctx *c, hl_tile tile, int n, const hl_linea
   cudaStreamWaitEvent(sc, e_done, 0);
   cudaStreamWaitEvent(sc, e_macs, 0);
   // (every forward NTT precedes a MAC, so sf is joined through s0)
-  for (auto &e : ev) cudaEventDestroy(e);         // released once the recorded work completes
   return hl_cuda_check("hl_he_linear_batch: launch");
 }
 
@@ -2264,14 +2280,14 @@ extern "C" int hl_he_linear_batch_host(const hl_ctx *c, hl_tile tile, int n, con
     if ((rc = hl_layout_query(c, h[i].dev.tile.m ? h[i].dev.tile : tile, h[i].dev.Ma, h[i].dev.R, h[i].dev.Nb, 0,
                               -1, &lay[i])))
       return rc;
+    if (!(h[i].dev.i_begin == 0 && (h[i].dev.i_end == -1 || h[i].dev.i_end == lay[i].nI)))
+      return hl_fail(HL_EINVAL, "hl_he_linear_batch_host: whole products only (i_begin = 0, i_end = -1 or nI)");
     d[i] = h[i].dev;
   }
   cudaStream_t sc = (cudaStream_t)stream, su = (cudaStream_t)c->up_stream, sd = (cudaStream_t)c->down_stream;
-  std::vector<cudaEvent_t> ev(2 * n + 2);
-  for (auto &e : ev)
-    if (cudaEventCreateWithFlags(&e, cudaEventDisableTiming) != cudaSuccess)
-      return hl_cuda_check("hl_he_linear_batch_host: events");
-  cudaEvent_t *e_up = ev.data(), *e_res = ev.data() + n, e_in = ev[2 * n], e_down = ev[2 * n + 1];
+  cudaEvent_t *ev = ctx_events(c, 1, 2 * (size_t)n + 2);
+  if (!ev) return hl_cuda_check("hl_he_linear_batch_host: events");
+  cudaEvent_t *e_up = ev, *e_res = ev + n, e_in = ev[2 * n], e_down = ev[2 * n + 1];
   cudaEventRecord(e_in, sc);                      // the buffers are free once earlier work on `stream` is done
   cudaStreamWaitEvent(su, e_in, 0);
   cudaStreamWaitEvent(sd, e_in, 0);
@@ -2311,7 +2327,6 @@ extern "C" int hl_he_linear_batch_host(const hl_ctx *c, hl_tile tile, int n, con
   }
   cudaEventRecord(e_down, sd);
   cudaStreamWaitEvent(sc, e_down, 0);
-  for (auto &e : ev) cudaEventDestroy(e);
   return hl_cuda_check("hl_he_linear_batch_host: launch");
 }
 

@@ -43,6 +43,12 @@ class Config:
     tiles: tuple = ()    # per-product tiles (the library's hl_plan_tile choice); () = `tile` for all
     batch_order: tuple = ()   # bench submission order of the products to hl_he_linear_batch; () = as listed
     e2e_order: tuple = ()     # the same for the end-to-end (host buffers, PCIe-bound) call; () = batch_order
+    seqs: int = 1             # independent sequences per block (c3: 8, c4: 4); Nb = seqs * seq_len
+    seq_len: int = 128
+
+    def block_shapes(self, nseq: int) -> tuple:
+        """The block's products over `nseq` of its sequences (Nb = nseq * seq_len)."""
+        return tuple(MatmulShape(mm.name, nseq * self.seq_len, mm.R, mm.Ma) for mm in self.matmuls)
 
     def tile_of(self, mi: int) -> tuple:
         return self.tiles[mi] if self.tiles else self.tile
@@ -70,10 +76,10 @@ CONFIGS = {
                  tiles=((16, 8, 32), (8, 8, 64), (16, 8, 32), (4, 32, 32)), batch_order=(3, 1, 2, 0), e2e_order=(2, 0, 3, 1)),
     # c3: 12 BERT-base blocks x 8 sequences (Nb = 8*128)
     "c3": Config("c3", 4096, 2, (16, 8, 32), _block(1024, 768, 3072), blocks=12,
-                 note="12 BERT-base blocks, 8 sequences x 128 tokens"),
+                 note="12 BERT-base blocks, 8 sequences x 128 tokens", seqs=8, seq_len=128),
     # c4: BERT-large 24 blocks, seq 512 x batch 4, N=8192, L=3
     "c4": Config("c4", 8192, 3, (32, 16, 16), _block(2048, 1024, 4096), blocks=24,
-                 note="24 BERT-large blocks, 4 sequences x 512 tokens"),
+                 note="24 BERT-large blocks, 4 sequences x 512 tokens", seqs=4, seq_len=512),
 }
 
 
@@ -87,6 +93,16 @@ def activations(seed: int, Nb: int, R: int, t_bits: int = T_BITS) -> np.ndarray:
     """Client share X: uint64 [Nb][R], uniform in [0, 2^t_bits)."""
     rng = np.random.default_rng(seed)
     return rng.integers(0, 1 << t_bits, size=(Nb, R), dtype=np.uint64)
+
+
+def activations_seq(seed: int, seq0: int, seq1: int, seq_len: int, R: int, t_bits: int = T_BITS) -> np.ndarray:
+    """Client shares X [(seq1 - seq0) * seq_len][R] of sequences [seq0, seq1) of a stacked block
+    (c3, c4): sequence s's rows are activations(seed + 7919 * (s + 1), seq_len, R), so any
+    sequence range of a block is generated without materialising the others."""
+    out = np.empty(((seq1 - seq0) * seq_len, R), dtype=np.uint64)
+    for s in range(seq0, seq1):
+        out[(s - seq0) * seq_len:(s - seq0 + 1) * seq_len] = activations(seed + 7919 * (s + 1), seq_len, R, t_bits)
+    return out
 
 
 def weights(seed: int, R: int, Ma: int, t_bits: int = T_BITS, frac_bits: int = FRAC_BITS,
