@@ -129,6 +129,17 @@ int hl_ctx_params(const hl_ctx *ctx, uint64_t *primes_out, uint64_t *delta_mod_o
  * c2 (BERT-base): QKV, FF1 -> (16, 8, 32); O -> (8, 8, 64); FF2 -> (4, 32, 32). */
 int hl_plan_tile(const hl_ctx *ctx, int64_t Ma, int64_t R, int64_t Nb, hl_tile *out);
 
+/* hl_plan_tile under a weight-cache budget: only tiles whose layout.wcache_bytes <= max_wcache_bytes
+ * (<= 0: unlimited) are candidates -- a stack of layers must keep every layer's cache resident
+ * (c4 on one GPU: 24 x 4.2 GB at n = 16 fits, the unconstrained choice at n = 32/64 does not).  The
+ * cost model adds, for products with many columns per weight byte (c3, c4), the tensor-core time of
+ * the MAC as issued (balanced row tiles at M = 64 / 128, J padded to 32, 49 limb products per
+ * modular MAC) and scales the transform terms by N L log N relative to N = 4096, L = 2:
+ *   T = max(Wbytes / (6.2 TB/s e_mac), T_tensor) + s (0.14 us nJ nK + 0.10 us nI nK).
+ * HL_EDIM if no tile fits the budget. */
+int hl_plan_tile_budget(const hl_ctx *ctx, int64_t Ma, int64_t R, int64_t Nb, int64_t max_wcache_bytes,
+                        hl_tile *out);
+
 /* Sizes of every buffer of one matmul (Ma x R weights, Nb tokens) for I-tile shard [i_begin, i_end). */
 int hl_layout_query(const hl_ctx *ctx, hl_tile tile, int64_t Ma, int64_t R, int64_t Nb,
                     int64_t i_begin, int64_t i_end, hl_layout *out);

@@ -35,7 +35,7 @@ EXPORTS = ("hl_last_error", "hl_ctx_create", "hl_ctx_destroy", "hl_ctx_params", 
            "hl_fc_local_share", "hl_encode_weights_strided", "hl_encode_weights_scratch", "hl_share_accumulate", "hl_sk_prepare",
            "hl_encrypt_device", "hl_decrypt_share_device", "hl_pk_gen", "hl_pk_prepare", "hl_he_matmul_share_rr",
            "hl_expand_seeded", "hl_he_linear_batch_host", "hl_packed50_words", "hl_pack50", "hl_unpack50",
-           "hl_timing_kernels", "hl_public_seed")
+           "hl_timing_kernels", "hl_public_seed", "hl_plan_tile_budget")
 KERNELS = ("ntt_fwd", "mac", "intt_mask", "intt", "mask", "encode", "other", "fc")   # HL_K_* order
 
 
@@ -108,6 +108,7 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
         "hl_ctx_set_mac_engine": [vp, i32],
         "hl_layout_query": [vp, Tile, i64, i64, i64, i64, i64, ctypes.POINTER(_Layout)],
         "hl_plan_tile": [vp, i64, i64, i64, ctypes.POINTER(Tile)],
+        "hl_plan_tile_budget": [vp, i64, i64, i64, i64, ctypes.POINTER(Tile)],
         "hl_keygen": [vp, u64, vp],
         "hl_public_seed": [u64],
         "hl_encrypt": [vp, vp, Tile, vp, i64, i64, u64, vp],
@@ -235,10 +236,14 @@ class Context:
         return Layout(*[getattr(out, f) for f, _ in _Layout._fields_])
 
     # ---------------------------------------------------------------- client (host memory)
-    def plan_tile(self, Ma: int, R: int, Nb: int) -> tuple:
-        """hl_plan_tile: the planner's (m, r, n) for an Nb x R . R x Ma product."""
+    def plan_tile(self, Ma: int, R: int, Nb: int, max_wcache_bytes: int = 0) -> tuple:
+        """hl_plan_tile(_budget): the planner's (m, r, n) for an Nb x R . R x Ma product, optionally
+        under a weight-cache budget in bytes."""
         t = Tile()
-        _check(_lib.hl_plan_tile(self._h, Ma, R, Nb, ctypes.byref(t)))
+        if max_wcache_bytes > 0:
+            _check(_lib.hl_plan_tile_budget(self._h, Ma, R, Nb, int(max_wcache_bytes), ctypes.byref(t)))
+        else:
+            _check(_lib.hl_plan_tile(self._h, Ma, R, Nb, ctypes.byref(t)))
         return (t.m, t.r, t.n)
 
     def keygen(self, seed: int) -> np.ndarray:

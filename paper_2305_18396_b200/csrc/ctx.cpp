@@ -413,8 +413,19 @@ extern "C" int hl_layout_query(const hl_ctx *c, hl_tile tile, int64_t Ma, int64_
 // tools/gpu/tile_sweep.py).  Candidates: powers of two with m*r*n <= N and
 // m <= Ma, r <= R, n <= Nb rounded up to a power of two (padded tiles cost what they move).
 extern "C" int hl_plan_tile(const hl_ctx *c, int64_t Ma, int64_t R, int64_t Nb, hl_tile *out) {
+  return hl_plan_tile_budget(c, Ma, R, Nb, 0, out);
+}
+
+// Effective rate of the tensor-core MAC on fat products (u8 limb MACs per second over the issued
+// M = 64 / 128 rows), measured on c3/c4
+static constexpr double kMacTcRate = 1.4e15;
+
+extern "C" int hl_plan_tile_budget(const hl_ctx *c, int64_t Ma, int64_t R, int64_t Nb, int64_t max_wcache_bytes,
+                                   hl_tile *out) {
   if (!c || !out) return hl_fail(HL_EINVAL, "hl_plan_tile: ctx or out is NULL");
   if (Ma <= 0 || R <= 0 || Nb <= 0) return hl_fail(HL_EINVAL, "hl_plan_tile: Ma, R, Nb must be positive");
+  // transform cost per ciphertext relative to the calibration point N = 4096, L = 2
+  const double ntt_scale = (double)c->N * c->L * (31 - __builtin_clz(c->N)) / (4096.0 * 2 * 12);
   auto ceil_pow2 = [](int64_t v) { int64_t p = 1; while (p < v) p <<= 1; return p; };
   const int64_t N = c->N, mmax = std::min<int64_t>(ceil_pow2(Ma), N), rmax = std::min<int64_t>(ceil_pow2(R), N),
                 nmax = std::min<int64_t>(ceil_pow2(Nb), N);
@@ -427,14 +438,21 @@ extern "C" int hl_plan_tile(const hl_ctx *c, int64_t Ma, int64_t R, int64_t Nb, 
       hl_tile t{(int32_t)m, (int32_t)r, (int32_t)n};
       hl_layout lay;
       if (hl_layout_query(c, t, Ma, R, Nb, 0, -1, &lay) != HL_OK) continue;
+      if (max_wcache_bytes > 0 && lay.wcache_bytes > max_wcache_bytes) continue;
       const double nC = 2.0 * lay.nK;
       const double e_mac = (nC <= 4 ? 1.0 : nC <= 8 ? 0.85 : 0.5) * std::min(1.0, (double)lay.nI / 96.0);
+      // tensor-core work of the MAC as issued: balanced row tiles of <= 128 rows at M = 64 / 128,
+      // J padded to the 32-J step, 49 limb products per modular MAC
+      const int64_t nIp = (lay.nI + 15) / 16 * 16, nIt = (nIp + 127) / 128;
+      const int64_t rt = ((nIp + nIt - 1) / nIt + 7) / 8 * 8;
+      const double rows = (double)nIt * (rt <= 64 ? 64 : 128), nJp = (double)((lay.nJ + 31) / 32 * 32);
+      const double t_tc = 49.0 * 2 * c->L * c->N * rows * nJp * (double)lay.nK / kMacTcRate;
       // the c0 inverse is pruned (to the class 15 mod 16 for r > 16, k_intt_c0_pruned)
-      const double cost = (double)lay.wcache_bytes / (6.2e12 * e_mac) + 0.14e-6 * (double)(lay.nJ * lay.nK) +
-                          0.10e-6 * (double)(lay.nI * lay.nK);
+      const double cost = std::max((double)lay.wcache_bytes / (6.2e12 * e_mac), t_tc) +
+                          ntt_scale * (0.14e-6 * (double)(lay.nJ * lay.nK) + 0.10e-6 * (double)(lay.nI * lay.nK));
       if (!found || cost < best) { best = cost; *out = t; found = true; }
     }
-  if (!found) return hl_fail(HL_EDIM, "hl_plan_tile: no tile fits the problem");
+  if (!found) return hl_fail(HL_EDIM, "hl_plan_tile: no tile fits the problem (or the weight-cache budget)");
   return HL_OK;
 }
 

@@ -1740,7 +1740,8 @@ void launch_mac_tc_t(const hl_ctx *c, MacTcArgs A, int smem_budget, int grid, cu
   using T = TcGeom<CW>;
   static PerDevice init;
   if (init.first()) { set_smem(k_mac_tc<CW>, T::SMEM_MAX); }
-  A.ring = tc_ring<CW>(A.g.RT, smem_budget, A.c1_bytes);
+  // pure column groups (every group all c0 or all c1): a stage holds the X residues or the c1 box
+  A.ring = tc_ring<CW>(A.g.RT, smem_budget, A.c1_bytes, A.c1_in && A.c1_nK % CW == 0);
   static const bool prof = getenv("HELINEAR_MAC_PROF") != nullptr;
   A.prof = nullptr;
   if (prof) cudaMalloc(&A.prof, 8 * sizeof(unsigned long long)), cudaMemsetAsync(A.prof, 0, 64, st);

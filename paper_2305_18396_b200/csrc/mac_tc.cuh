@@ -41,27 +41,48 @@ struct TcGeom {
   static constexpr int A_OFF = RAW_BYTES;                // TMA stage layout: [RAW][A (224 B per I row)]
   static constexpr int SPI = 4;                          // slots per work item (32-B output sectors)
   static constexpr int STG_STRIDE = CW * SPI + 1;        // u64 per staged row (+1: bank spread)
+  // CW = 16: the epilogue keeps 2 slots x 8 columns of its row in registers and stores them
+  // directly (16-B halves of the 32-B sectors, merged in L2) -- the 48 KB staging buffer would cost
+  // the ring a stage; 4 slots in registers would exceed the 128 registers of 14 warps per SM
+  static constexpr bool REG_EPI = CW >= 16;
   static constexpr int NBUF = 4 * N <= 512 ? 4 : 2;      // TMEM accumulators in flight (MMA runs ahead of the epilogue)
   static constexpr int TCOLS = NBUF * N <= 64 ? 64 : (NBUF * N <= 128 ? 128 : (NBUF * N <= 256 ? 256 : 512));
   static constexpr int MAX_NST = 24;
   static constexpr int BAR_BYTES = (2 * MAX_NST + 2 * NZ + 2 * NBUF + 2 * 4) * 8 + 4 * 4 + 16;
-  static constexpr int THREADS = 384;                    // 4 role warps + 8 epilogue warps
+  // converter warps: each converts whole stages, the warps taking turns (stage z to warp z mod
+  // NCONV), so NCONV stages are converted concurrently.  2 (12 warps per CTA: 3 per SM
+  // sub-partition, so up to 168 registers per thread -- 4 converters would cap them at 128 and spill)
+  static constexpr int NCONV = 2;
+  // CW = 16: the converter warps take turns (one warp converts a whole stage, 2 stages in flight);
+  // CW <= 8: both warps convert each stage (its conversion is short; measured faster on c2)
+  static constexpr bool ALT_CONV = CW >= 16;
+  static constexpr int EPI0 = 2 + NCONV;                 // first epilogue warp
+  static constexpr int THREADS = 32 * (EPI0 + 8);        // producer + MMA + converters + 8 epilogue warps
   static constexpr int SMEM_MAX = 232448;                // 227 KB opt-in per CTA
   static_assert(A_OFF % 16 == 0 && Z_BYTES % 128 == 0, "alignment");
 };
 
 // ring geometry for a launch: rt rows per I tile (balanced tiles, multiple of 8)
-struct TcRing { int nst, sbytes, c1_off, z_off, stg_off, bar_off, smem; };
+struct TcRing { int nst, sbytes, a_off, c1_off, z_off, stg_off, bar_off, smem; };
 template <int CW>
-TcRing tc_ring(int rt, int smem_budget, int c1_bytes = 0) {
+TcRing tc_ring(int rt, int smem_budget, int c1_bytes = 0, bool x_union = false) {
   using T = TcGeom<CW>;
   TcRing r;
   // the M = 128 MMA reads 128 rows of every plane (rows >= rt are don't-care): plane 6 starts at
-  // 192 rt, row 127 of its second K half ends 2048 + 16 rt later -> 208 rt + 2048 >= 224 rt bytes;
-  // then (MacTcArgs::c1_in) the c1 box of the stage
-  r.c1_off = (T::A_OFF + 208 * rt + 2048 + 127) / 128 * 128;
-  r.sbytes = r.c1_off + (c1_bytes + 127) / 128 * 128;
-  const int stg = (rt * T::STG_STRIDE * 8 + 127) / 128 * 128;
+  // 192 rt, row 127 of its second K half ends 2048 + 16 rt later -> 208 rt + 2048 >= 224 rt bytes.
+  // Stage layout [X residues][A planes][c1 box]; x_union (every column group is pure c0 or pure c1,
+  // so a stage holds either the X residues or the c1 box): [X residues | c1 box][A planes]
+  const int a_end = 208 * rt + 2048;
+  if (x_union) {
+    r.c1_off = 0;
+    r.a_off = (std::max(T::RAW_BYTES, c1_bytes) + 127) / 128 * 128;
+    r.sbytes = (r.a_off + a_end + 127) / 128 * 128;
+  } else {
+    r.a_off = T::A_OFF;
+    r.c1_off = (T::A_OFF + a_end + 127) / 128 * 128;
+    r.sbytes = r.c1_off + (c1_bytes + 127) / 128 * 128;
+  }
+  const int stg = T::REG_EPI ? 0 : (rt * T::STG_STRIDE * 8 + 127) / 128 * 128;
   const int fixed = T::NZ * T::Z_BYTES + stg + T::BAR_BYTES;
   r.nst = std::max(2, std::min(T::MAX_NST, (std::min(smem_budget, T::SMEM_MAX) - fixed) / r.sbytes));
   r.z_off = r.nst * r.sbytes;
@@ -212,7 +233,7 @@ __device__ __forceinline__ TcItem tc_decode(const MacGeom &g, int item) {
   return it;
 }
 constexpr int kItemRing = 4;
-constexpr int kItemConsumers = 11;    // MMA warp + 2 converter warps + 8 epilogue warps (lane 0 each)
+// consumers of an item: the MMA warp + the converter warps + 8 epilogue warps (lane 0 each)
 // consumer side: wait for item number `seq`, read it, release the ring slot; returns -1 at the end
 __device__ __forceinline__ int tc_next_item(uint64_t *ifull, uint64_t *iempty, const volatile int *itm, uint32_t seq) {
   const int slot = seq % kItemRing;
@@ -221,6 +242,30 @@ __device__ __forceinline__ int tc_next_item(uint64_t *ifull, uint64_t *iempty, c
   __syncwarp();
   if ((threadIdx.x & 31) == 0) mbar_arrive(&iempty[slot]);
   return item;
+}
+
+// one converter unit: the limb rows b*CW + c and b*CW + c + 1 (b < 7) for the 4 consecutive J of
+// 32-bit word gq in K half h of the Toeplitz image z, from the 4 x 2 residues x0 (column c) and x1
+// (column c+1).  Lanes of a warp cover the column pairs fastest: with the two stores in a lane-
+// dependent order (swap = column pair >= 4) a warp's 32 stores hit 32 distinct banks.
+template <int CW, int ZR>
+__device__ __forceinline__ void conv_unit(unsigned char *z, int h, int c, int gq, const uint64_t (&x0)[4],
+                                          const uint64_t (&x1)[4], bool swap) {
+  uint32_t *row = reinterpret_cast<uint32_t *>(z + ((size_t)h * ZR + c) * 16) + gq;
+  const uint32_t l0[4] = {(uint32_t)x0[0], (uint32_t)x0[1], (uint32_t)x0[2], (uint32_t)x0[3]};
+  const uint32_t h0[4] = {(uint32_t)(x0[0] >> 32), (uint32_t)(x0[1] >> 32), (uint32_t)(x0[2] >> 32), (uint32_t)(x0[3] >> 32)};
+  const uint32_t l1[4] = {(uint32_t)x1[0], (uint32_t)x1[1], (uint32_t)x1[2], (uint32_t)x1[3]};
+  const uint32_t h1[4] = {(uint32_t)(x1[0] >> 32), (uint32_t)(x1[1] >> 32), (uint32_t)(x1[2] >> 32), (uint32_t)(x1[3] >> 32)};
+  const int f = swap ? 4 : 0;                            // u32 offset of the first store (column c+1 if swap)
+#pragma unroll
+  for (int b = 0; b < 7; b++) {
+    const uint32_t *s0 = b < 4 ? l0 : h0, *s1 = b < 4 ? l1 : h1;
+    const uint32_t bb = b & 3, sel = bb | ((bb + 4) << 4);
+    const uint32_t w0 = __byte_perm(__byte_perm(s0[0], s0[1], sel), __byte_perm(s0[2], s0[3], sel), 0x5410);
+    const uint32_t w1 = __byte_perm(__byte_perm(s1[0], s1[1], sel), __byte_perm(s1[2], s1[3], sel), 0x5410);
+    row[b * CW * 4 + f] = swap ? w1 : w0;
+    row[b * CW * 4 + (4 - f)] = swap ? w0 : w1;
+  }
 }
 
 template <int CW>
@@ -249,9 +294,9 @@ k_mac_tc(const __grid_constant__ MacTcArgs A, DevParams P) {
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
   if (threadIdx.x == 0) {
     for (int i = 0; i < NST; i++) { mbar_init(&full[i], 1); mbar_init(&empty[i], 1); }
-    for (int i = 0; i < T::NZ; i++) { mbar_init(&zfull[i], 64); mbar_init(&zempty[i], 1); }
+    for (int i = 0; i < T::NZ; i++) { mbar_init(&zfull[i], T::ALT_CONV ? 32 : 64); mbar_init(&zempty[i], 1); }
     for (int i = 0; i < T::NBUF; i++) { mbar_init(&tfull[i], 1); mbar_init(&tempty[i], 8); }
-    for (int i = 0; i < kItemRing; i++) { mbar_init(&ifull[i], 1); mbar_init(&iempty[i], kItemConsumers); }
+    for (int i = 0; i < kItemRing; i++) { mbar_init(&ifull[i], 1); mbar_init(&iempty[i], 1 + T::NCONV + 8); }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 1) {
@@ -266,10 +311,10 @@ k_mac_tc(const __grid_constant__ MacTcArgs A, DevParams P) {
   // The limb-plane MMA a accumulates into the column window [a*CW, a*CW + NM) of its buffer (the
   // Toeplitz shift lives in the accumulator address): columns [NM, N) must start at zero.  The
   // epilogue re-zeroes them after draining a buffer; here every buffer is zeroed once.
-  if (warp >= 4) {
+  if (warp >= T::EPI0) {
     const uint32_t lanes = (uint32_t)(32 * (warp & 3)) << 16;
     for (int b = 0; b < T::NBUF; b++)
-      for (int col = T::NM + ((warp - 4) >> 2); col < T::N; col += 2)
+      for (int col = T::NM + ((warp - T::EPI0) >> 2); col < T::N; col += 2)
         asm volatile("tcgen05.st.sync.aligned.32x32b.x1.b32 [%0], {%1};" ::"r"(tmem + lanes + b * T::N + col), "r"(0u));
     asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
   }
@@ -310,7 +355,7 @@ k_mac_tc(const __grid_constant__ MacTcArgs A, DevParams P) {
             mbar_wait_p(&empty[st], ph, A.prof ? &pw[0] : nullptr);
             unsigned char *dst = smem + st * SB;
             mbar_expect_tx(&full[st], tx);
-            bulk_g2s_hint(dst + T::A_OFF, wt + ((size_t)s * g.nJc + jc) * abytes, abytes, &full[st], pol_w);
+            bulk_g2s_hint(dst + A.ring.a_off, wt + ((size_t)s * g.nJc + jc) * abytes, abytes, &full[st], pol_w);
             if (xraw)
               bulk_g2s(dst, A.X + (((size_t)it.cg * g.LN + s) * g.nJp + (size_t)jc * 32) * g.xw, rawb, &full[st]);
             if (xc1)   // natural points k0 + (si & 2) .. +1 of the group's c1 columns, 32 J
@@ -351,7 +396,7 @@ k_mac_tc(const __grid_constant__ MacTcArgs A, DevParams P) {
           mbar_wait_p(&zfull[zi], zph, (A.prof && lane == 0) ? &pw[3] : nullptr);
           tc_fence_after();
           const long long ti0 = A.prof ? clock64() : 0;
-          const uint32_t a0 = smem_u32(smem + st * SB) + T::A_OFF;
+          const uint32_t a0 = smem_u32(smem + st * SB) + A.ring.a_off;
           const uint32_t z0 = smem_u32(zring + zi * T::Z_BYTES);
           if (elect_one()) {
 #pragma unroll
@@ -371,8 +416,10 @@ k_mac_tc(const __grid_constant__ MacTcArgs A, DevParams P) {
         __syncwarp();
       }
     }
-  } else if (warp < 4) {
+  } else if (warp < T::EPI0) {
     // ------------------------------------------------------------------ converters
+    // CW <= 8: both converter warps convert every stage, one column of 4 J per thread
+    if constexpr (!T::ALT_CONV) {
     const int ct = threadIdx.x - 64;
     int st = 0;
     uint32_t ph = 0, zseq = 0;
@@ -388,7 +435,6 @@ k_mac_tc(const __grid_constant__ MacTcArgs A, DevParams P) {
           const uint64_t *raw = reinterpret_cast<const uint64_t *>(smem + st * SB);
           const uint64_t *c1b = reinterpret_cast<const uint64_t *>(smem + st * SB + A.ring.c1_off) + (si & 1);
           unsigned char *z = zring + zi * T::Z_BYTES;
-          // compile-time trip count (2 at CW = 16): the iterations' shared-memory loads overlap
           constexpr int QIT = (CW * 8 + 63) / 64;
 #pragma unroll
           for (int qi = 0; qi < QIT; qi++) {
@@ -420,6 +466,73 @@ k_mac_tc(const __grid_constant__ MacTcArgs A, DevParams P) {
         }
       }
     }
+    } else {
+    // Converter warp cw converts the stages z = cw, cw + NCONV, ... of the sequence: the u64 residues
+    // of 32 J x CW columns -> the byte rows of the Toeplitz image (row b*CW + c, 32 J bytes split
+    // in two 16-B K halves).  A unit = 2 columns x 4 J (one u32 word per limb row and column):
+    // CW*4 units per stage over the warp's 32 lanes, column pairs fastest so that the 16-B loads of
+    // a warp cover whole 128-B rows of the stage's [J][xw] residues (no bank conflicts at xw = 16).
+    const int cw = warp - 2;
+    constexpr int NPAIR = CW / 2, UNITS = NPAIR * 8, UIT = (UNITS + 31) / 32;
+    uint32_t zseq = 0;
+    for (uint32_t seq = 0;; seq++) {
+      const int item = tc_next_item(ifull, iempty, itm, seq);
+      if (item < 0) break;
+      const int c1lo = tc_c1_lo<CW>(A, tc_decode(g, item).cg);
+      for (int si = 0; si < T::SPI; si++) {
+        for (int kk = 0; kk < A.njc; kk++, zseq++) {
+          if ((int)(zseq % T::NCONV) != cw) continue;
+          const int st = (int)(zseq % (uint32_t)NST);
+          const uint32_t ph = (zseq / (uint32_t)NST) & 1;
+          const uint32_t zi = zseq % T::NZ, zph = (zseq / T::NZ) & 1;
+          mbar_wait_p(&full[st], ph, (A.prof && lane == 0 && cw == 0) ? &pw[4] : nullptr);
+          mbar_wait(&zempty[zi], zph ^ 1);
+          const uint64_t *raw = reinterpret_cast<const uint64_t *>(smem + st * SB);
+          const uint64_t *c1b = reinterpret_cast<const uint64_t *>(smem + st * SB + A.ring.c1_off) + (si & 1);
+          const ulonglong2 *c1q = reinterpret_cast<const ulonglong2 *>(smem + st * SB + A.ring.c1_off);
+          unsigned char *z = zring + zi * T::Z_BYTES;
+#pragma unroll
+          for (int ui = 0; ui < UIT; ui++) {
+            const int u = lane + 32 * ui;
+            if (u >= UNITS) break;
+            const int cp = u % NPAIR, hg = u / NPAIR, h = hg >> 2, gq = hg & 3;
+            const int c = 2 * cp, j0 = h * 16 + gq * 4;
+            uint64_t x0[4], x1[4];
+            if (c + 1 < c1lo && !(g.xw & 1)) {                  // both c0: one 16-B load per J
+#pragma unroll
+              for (int j = 0; j < 4; j++) {
+                const ulonglong2 v = *reinterpret_cast<const ulonglong2 *>(raw + (j0 + j) * g.xw + c);
+                x0[j] = v.x; x1[j] = v.y;
+              }
+            } else if (c >= c1lo) {
+              // both c1, from the box [J][K][2 points]: the 16-B (point 0, point 1) pair of each
+              // column, the two loads in a lane-dependent order so that a warp's loads cover all
+              // 32 banks; the stage's point is si & 1
+              const int k0 = c - c1lo, f = (cp & 4) ? 1 : 0;
+#pragma unroll
+              for (int j = 0; j < 4; j++) {
+                const ulonglong2 *rw = c1q + (j0 + j) * A.c1_cols + k0;
+                const ulonglong2 va = rw[f], vb = rw[1 - f];
+                const ulonglong2 v0 = f ? vb : va, v1 = f ? va : vb;
+                x0[j] = (si & 1) ? v0.y : v0.x;
+                x1[j] = (si & 1) ? v1.y : v1.x;
+              }
+            } else {                                           // a c0 / c1 boundary pair (odd nK)
+#pragma unroll
+              for (int j = 0; j < 4; j++) {
+                x0[j] = c < c1lo ? raw[(j0 + j) * g.xw + c] : c1b[((j0 + j) * A.c1_cols + (c - c1lo)) * 2];
+                x1[j] = c + 1 < c1lo ? raw[(j0 + j) * g.xw + c + 1]
+                                     : c1b[((j0 + j) * A.c1_cols + (c + 1 - c1lo)) * 2];
+              }
+            }
+            conv_unit<CW, T::ZR>(z, h, c, gq, x0, x1, (cp & 4) != 0);
+          }
+          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+          mbar_arrive(&zfull[zi]);                             // every lane (count 32)
+        }
+      }
+    }
+    }
   } else {
     // ------------------------------------------------------------------ epilogue
     // warp w (4..11): TMEM lanes 32*(w&3).. (the hardware quadrant of w), columns c in half hh.
@@ -427,8 +540,8 @@ k_mac_tc(const __grid_constant__ MacTcArgs A, DevParams P) {
     // H = sum_{d=9..12} S_d 2^(8(d-9)) < 2^56 (S_d < 2^31), sum_J W X = L + M 2^40 + H 2^72,
     // reduced as Barrett(L) + Shoup(M, 2^40 mod p) + Shoup(H, 2^72 mod p), each in [0, 2p).
     constexpr int CH = CW / 2;
-    const int q = warp & 3, hh = (warp - 4) >> 2;
-    const int et = threadIdx.x - 128;
+    const int q = warp & 3, hh = (warp - T::EPI0) >> 2;
+    const int et = threadIdx.x - 32 * T::EPI0;
     uint32_t tile_no = 0;
     for (uint32_t seq = 0;; seq++) {
       const int item = tc_next_item(ifull, iempty, itm, seq);
@@ -440,6 +553,63 @@ k_mac_tc(const __grid_constant__ MacTcArgs A, DevParams P) {
       const bool m64 = min(g.RT, g.nIp - g.RT * it.t) <= 64;   // this item's MMA M (as the MMA warp)
       const int row = m64 ? (lane < 16 ? 16 * q + lane : 1 << 20) : 32 * q + lane;   // tile row held by this lane
       const bool active = (m64 ? 16 : 32) * q < rows_valid;   // warp-uniform: this quadrant holds outputs
+      const size_t s0 = (size_t)it.sq * T::SPI;
+      // full 32-B sector stores of out[I][col][s0 .. s0+3] (c1 columns: into the response)
+      // (store2: the 16-B half h of the sector)
+      auto store2 = [&](int rr, int c, int h, uint64_t v0, uint64_t v1) {
+        const int col = it.cg * CW + c;
+        if (A.c1_out && col >= A.c1_nK) {
+          const int sl = (int)(s0 - (size_t)l * A.N), nt = 1 << A.c1_lognt;
+          const int u = sl >> A.c1_lognt, tq = (sl & (nt - 1)) >> 2;
+          const int k0 = (int)(__brev((unsigned)u) >> 28) * nt + (int)(__brev((unsigned)tq) >> (32 - A.c1_lognt));
+          const int64_t o = (int64_t)(g.RT * it.t + rr) * A.c1_nK + (col - A.c1_nK);
+          v0 = v0 >= pc.two_p ? v0 - pc.two_p : v0; v0 = v0 >= pc.p ? v0 - pc.p : v0;
+          v1 = v1 >= pc.two_p ? v1 - pc.two_p : v1; v1 = v1 >= pc.p ? v1 - pc.p : v1;
+          *reinterpret_cast<ulonglong2 *>(A.c1_out + (size_t)o * P.L * (A.c1_mn + A.N) + (size_t)P.L * A.c1_mn +
+                                          (size_t)l * A.N + k0 + 2 * h) = make_ulonglong2(v0, v1);
+          return;
+        }
+        ulonglong2 *dst = reinterpret_cast<ulonglong2 *>(
+            A.out + ((size_t)(g.RT * it.t + rr) * g.nC + it.cg * CW + c) * g.LN + s0 + 2 * h);
+        if (A.accumulate) {
+          const ulonglong2 o0 = dst[0];
+          v0 += o0.x; v1 += o0.y;
+          v0 = v0 >= pc.p ? v0 - pc.p : v0; v1 = v1 >= pc.p ? v1 - pc.p : v1;
+        }
+        dst[0] = make_ulonglong2(v0, v1);
+      };
+      auto store4 = [&](int rr, int c, uint64_t v0, uint64_t v1, uint64_t v2, uint64_t v3) {
+        const int col = it.cg * CW + c;
+        if (A.c1_out && col >= A.c1_nK) {
+          // quad order (tc_slot): slot u NT + t' + {0,2,1,3}[i] NT/4 holds natural k = k0 + i,
+          // k0 = brev4(u) NT + brev(t') (nat_of) -- one 32-B sector of the response's c1
+          const int sl = (int)(s0 - (size_t)l * A.N), nt = 1 << A.c1_lognt;
+          const int u = sl >> A.c1_lognt, tq = (sl & (nt - 1)) >> 2;
+          const int k0 = (int)(__brev((unsigned)u) >> 28) * nt + (int)(__brev((unsigned)tq) >> (32 - A.c1_lognt));
+          const int64_t o = (int64_t)(g.RT * it.t + rr) * A.c1_nK + (col - A.c1_nK);
+          ulonglong2 *dst = reinterpret_cast<ulonglong2 *>(
+              A.c1_out + (size_t)o * P.L * (A.c1_mn + A.N) + (size_t)P.L * A.c1_mn + (size_t)l * A.N + k0);
+          v0 = v0 >= pc.two_p ? v0 - pc.two_p : v0; v0 = v0 >= pc.p ? v0 - pc.p : v0;
+          v1 = v1 >= pc.two_p ? v1 - pc.two_p : v1; v1 = v1 >= pc.p ? v1 - pc.p : v1;
+          v2 = v2 >= pc.two_p ? v2 - pc.two_p : v2; v2 = v2 >= pc.p ? v2 - pc.p : v2;
+          v3 = v3 >= pc.two_p ? v3 - pc.two_p : v3; v3 = v3 >= pc.p ? v3 - pc.p : v3;
+          dst[0] = make_ulonglong2(v0, v1);
+          dst[1] = make_ulonglong2(v2, v3);
+          return;
+        }
+        ulonglong2 *dst = reinterpret_cast<ulonglong2 *>(
+            A.out + ((size_t)(g.RT * it.t + rr) * g.nC + it.cg * CW + c) * g.LN + s0);
+        if (A.accumulate) {
+          const ulonglong2 o0 = dst[0], o1 = dst[1];
+          v0 += o0.x; v1 += o0.y; v2 += o1.x; v3 += o1.y;
+          v0 = v0 >= pc.p ? v0 - pc.p : v0; v1 = v1 >= pc.p ? v1 - pc.p : v1;
+          v2 = v2 >= pc.p ? v2 - pc.p : v2; v3 = v3 >= pc.p ? v3 - pc.p : v3;
+        }
+        dst[0] = make_ulonglong2(v0, v1);
+        dst[1] = make_ulonglong2(v2, v3);
+      };
+      uint64_t acc[T::REG_EPI ? CH : 1][2];                     // REG_EPI: 2 slots of this lane's outputs
+#pragma unroll
       for (int si = 0; si < T::SPI; si++, tile_no++) {
         const uint32_t buf = tile_no % T::NBUF, tph = (tile_no / T::NBUF) & 1;
         mbar_wait_p(&tfull[buf], tph, (A.prof && et == 0) ? &pw[5] : nullptr);
@@ -505,47 +675,26 @@ k_mac_tc(const __grid_constant__ MacTcArgs A, DevParams P) {
               r = r >= pc.two_p ? r - pc.two_p : r;
               r = r >= pc.p ? r - pc.p : r;
             }
-            if (row < rows_valid) stg[row * T::STG_STRIDE + (hh * CH + c) * T::SPI + si] = r;
+            if constexpr (T::REG_EPI) acc[c][si & 1] = r;
+            else if (row < rows_valid) stg[row * T::STG_STRIDE + (hh * CH + c) * T::SPI + si] = r;
+          }
+        }
+        if constexpr (T::REG_EPI) {
+          if ((si & 1) && active && row < rows_valid) {
+#pragma unroll
+            for (int c = 0; c < CH; c++) store2(row, hh * CH + c, si >> 1, acc[c][0], acc[c][1]);
           }
         }
       }
-      // 4 slots staged: full 32-B sector stores of out[I][col][s0 .. s0+3]
-      asm volatile("bar.sync 2, 256;" ::: "memory");
-      const size_t s0 = (size_t)it.sq * T::SPI;
-      for (int e = et; e < rows_valid * CW; e += 256) {
-        const int rr = e / CW, c = e % CW;
-        const uint64_t *sv = stg + rr * T::STG_STRIDE + c * T::SPI;
-        uint64_t v0 = sv[0], v1 = sv[1], v2 = sv[2], v3 = sv[3];
-        const int col = it.cg * CW + c;
-        if (A.c1_out && col >= A.c1_nK) {
-          // quad order (tc_slot): slot u NT + t' + {0,2,1,3}[i] NT/4 holds natural k = k0 + i,
-          // k0 = brev4(u) NT + brev(t') (nat_of) -- one 32-B sector of the response's c1
-          const int sl = (int)(s0 - (size_t)l * A.N), nt = 1 << A.c1_lognt;
-          const int u = sl >> A.c1_lognt, tq = (sl & (nt - 1)) >> 2;
-          const int k0 = (int)(__brev((unsigned)u) >> 28) * nt + (int)(__brev((unsigned)tq) >> (32 - A.c1_lognt));
-          const int64_t o = (int64_t)(g.RT * it.t + rr) * A.c1_nK + (col - A.c1_nK);
-          ulonglong2 *dst = reinterpret_cast<ulonglong2 *>(
-              A.c1_out + (size_t)o * P.L * (A.c1_mn + A.N) + (size_t)P.L * A.c1_mn + (size_t)l * A.N + k0);
-          v0 = v0 >= pc.two_p ? v0 - pc.two_p : v0; v0 = v0 >= pc.p ? v0 - pc.p : v0;
-          v1 = v1 >= pc.two_p ? v1 - pc.two_p : v1; v1 = v1 >= pc.p ? v1 - pc.p : v1;
-          v2 = v2 >= pc.two_p ? v2 - pc.two_p : v2; v2 = v2 >= pc.p ? v2 - pc.p : v2;
-          v3 = v3 >= pc.two_p ? v3 - pc.two_p : v3; v3 = v3 >= pc.p ? v3 - pc.p : v3;
-          dst[0] = make_ulonglong2(v0, v1);
-          dst[1] = make_ulonglong2(v2, v3);
-          continue;
+      if constexpr (!T::REG_EPI) {
+        asm volatile("bar.sync 2, 256;" ::: "memory");      // 4 slots staged
+        for (int e = et; e < rows_valid * CW; e += 256) {
+          const int rr = e / CW, c = e % CW;
+          const uint64_t *sv = stg + rr * T::STG_STRIDE + c * T::SPI;
+          store4(rr, c, sv[0], sv[1], sv[2], sv[3]);
         }
-        ulonglong2 *dst = reinterpret_cast<ulonglong2 *>(
-            A.out + ((size_t)(g.RT * it.t + rr) * g.nC + it.cg * CW + c) * g.LN + s0);
-        if (A.accumulate) {
-          const ulonglong2 o0 = dst[0], o1 = dst[1];
-          v0 += o0.x; v1 += o0.y; v2 += o1.x; v3 += o1.y;
-          v0 = v0 >= pc.p ? v0 - pc.p : v0; v1 = v1 >= pc.p ? v1 - pc.p : v1;
-          v2 = v2 >= pc.p ? v2 - pc.p : v2; v3 = v3 >= pc.p ? v3 - pc.p : v3;
-        }
-        dst[0] = make_ulonglong2(v0, v1);
-        dst[1] = make_ulonglong2(v2, v3);
+        asm volatile("bar.sync 2, 256;" ::: "memory");
       }
-      asm volatile("bar.sync 2, 256;" ::: "memory");
     }
   }
 
@@ -555,7 +704,7 @@ k_mac_tc(const __grid_constant__ MacTcArgs A, DevParams P) {
     if (threadIdx.x == 0) { atomicAdd(&A.prof[0], pw[0]); atomicAdd(&A.prof[7], tot); }
     if (threadIdx.x == 32) { atomicAdd(&A.prof[1], pw[1]); atomicAdd(&A.prof[2], pw[2]); atomicAdd(&A.prof[3], pw[3]); atomicAdd(&A.prof[6], pw[6]); }
     if (threadIdx.x == 64) atomicAdd(&A.prof[4], pw[4]);
-    if (threadIdx.x == 128) atomicAdd(&A.prof[5], pw[5]);
+    if (threadIdx.x == 32 * T::EPI0) atomicAdd(&A.prof[5], pw[5]);
   }
   tc_fence_before();
   __syncthreads();
