@@ -245,7 +245,10 @@ int hl_he_matmul(const hl_ctx *ctx, hl_tile tile, const void *wcache, int64_t Ma
                  void *workspace, uint64_t *ct_out, void *stream);
 
 /* Alg. 1 step 3, masking + §3.1.3 compression:
- *   sigma = u64_MASK(stream I*nK+K)[0..N) & (t-1);  c0 <- c0 - Delta_l*sigma (mod p_l);
+ *   sigma[pos] = u64_MASK(stream I*nK+K)[w(pos)] & (t-1), with the word order of reading C27: the
+ *   kept positions pos(i,k) = k*m*r + i*r + r-1 take words 0 .. m*n-1 in kept-index order k*m+i,
+ *   every other position the next word in position order (a permutation of [0, N));
+ *   c0 <- c0 - Delta_l*sigma (mod p_l);
  *   compress != 0: keep c1 and c0 at pos(i,k) only;  share_server[K*n+k][I*m+i] = sigma[pos(i,k)].
  * ct_out: device [nI_s][nK][2][L][N]; ct_masked: device (layout.ct_masked_words or
  * ct_full_words); share_server: device [Nb][Ma], only the shard's columns are written. */

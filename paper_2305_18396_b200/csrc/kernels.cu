@@ -593,6 +593,36 @@ k_ntt_fwd_c0x2(const uint64_t *__restrict__ in, uint64_t *__restrict__ out, DevP
 // (slot, J) store is 8 G1 contiguous bytes (a full 32-B sector for G1 = 4).  The G1 natural-order
 // polynomials arrive by bulk copies (TMA); the gather is bank-conflict free because the 16 low
 // lanes of a warp differ in the top bits of t, i.e. in the low bits of the natural index.
+// c1 halves (evaluation form, natural order, reading C26) of whole CW = 16 column groups into the
+// X layout for the tensor-core MAC (the c1 columns of the fat products c3/c4, where the MAC's own
+// gather of c1 through a tensor-map box moves 16-B pieces): a CTA takes one J, one c1 column group
+// (16 ciphertexts K0 .. K0+15) and 256 natural points of one prime; coalesced 8-B loads of the 16
+// rows into shared memory (rows padded to 257 words: conflict-free both ways), then every point's
+// 16 columns as one 128-B line X[cg][l N + slot(k)][J][0..16) -- full lines, 4 sectors each.
+template <int LOGN>
+__global__ void __launch_bounds__(256)
+k_c1_tx16(const uint64_t *__restrict__ in, uint64_t *__restrict__ out, DevParams P, MacGeom mg) {
+  constexpr int N = 1 << LOGN, PTS = 256, ROW = PTS + 1;
+  __shared__ uint64_t stg[16 * ROW];
+  const int t = threadIdx.x, l = blockIdx.z;
+  const int nK = mg.nC / 2, ncg1 = nK / 16;
+  const int J = (int)(blockIdx.y / (unsigned)ncg1), g1 = (int)(blockIdx.y % (unsigned)ncg1);
+  const int k0 = blockIdx.x * PTS, K0 = g1 * 16;
+#pragma unroll
+  for (int c = 0; c < 16; c++)
+    stg[c * ROW + t] = __ldcs(in + (((size_t)J * nK + K0 + c) * 2 * P.L + P.L + l) * N + k0 + t);
+  __syncthreads();
+  const int cg = (nK + K0) / 16, c = t & 15;
+  uint64_t *dst0 = out + ((size_t)cg * mg.LN + (size_t)l * N) * mg.nJp * 16 + (size_t)J * 16 + c;
+#pragma unroll 4
+  for (int it = 0; it < PTS / 16; it++) {
+    const int kk = it * 16 + (t >> 4), k = k0 + kk;
+    const int idx = (int)(__brev((unsigned)k) >> (32 - LOGN));          // CT index of natural point k
+    const int s = (idx & 15) * (N / 16) + (idx >> 4);                    // its slot (slot_of)
+    dst0[(size_t)s * mg.nJp * 16] = stg[c * ROW + kk];
+  }
+}
+
 template <int LOGN, int G1>
 __global__ void __launch_bounds__(Geom<LOGN>::NT)
 k_c1_to_x(const uint64_t *__restrict__ in, uint64_t *__restrict__ out, DevParams P, MacGeom mg) {
@@ -1646,7 +1676,9 @@ void launch_fwd_cperm(const hl_ctx *c, const uint64_t *in, uint64_t *out, int64_
     else k_ntt_fwd_c0x2<LOGN, false, MB2><<<gx, Geom<LOGN>::NT, smem2, st>>>(in, out, c->dp, mg);
     return;
   }
-  const bool fused = nK % 2 == 0;                // c1 pairs (K0, K0+1) adjacent in the c1 column range
+  // c1 pairs (K0, K0+1) adjacent in the c1 column range, copied by the c0 kernel; whole 16-column
+  // c1 groups go to k_c1_tx16 instead (128-B line stores)
+  const bool fused = nK % 2 == 0 && !(mg.CW == 16 && nK % 16 == 0);
   kt.nk = fused ? 1 : 2;
   if constexpr (LOGN == 12) {
     if (fused) {   // N = 4096: 3 CTAs per SM (80 registers, a few bytes of spill; measured best)
@@ -1659,8 +1691,12 @@ void launch_fwd_cperm(const hl_ctx *c, const uint64_t *in, uint64_t *out, int64_
     k_ntt_fwd_c0x2<LOGN, true><<<dim3((unsigned)(nJ * ((nK + 1) / 2)), c->L), Geom<LOGN>::NT, smem2, st>>>(in, out, c->dp, mg);
     return;
   }
-  // odd nK: the c0 pairs without their c1, then the c1 reordering
+  // odd nK (or whole 16-column c1 groups): the c0 pairs without their c1, then the c1 reordering
   k_ntt_fwd_c0x2<LOGN, false, MB2><<<dim3((unsigned)(nJ * ((nK + 1) / 2)), c->L), Geom<LOGN>::NT, smem2, st>>>(in, out, c->dp, mg);
+  if (mg.CW == 16 && nK % 16 == 0) {
+    k_c1_tx16<LOGN><<<dim3((unsigned)(Geom<LOGN>::N / 256), (unsigned)(nJ * (nK / 16)), c->L), 256, 0, st>>>(in, out, c->dp, mg);
+    return;
+  }
   // G1 = 4 needs 4 | nK and 4 | CW (the 4 columns in one group); 4 x 64 KB does not fit at N = 8192
   const int G1 = (nK % 4 == 0 && mg.CW % 4 == 0 && LOGN == 12) ? 4 : (nK % 2 == 0 ? 2 : 1);
   const dim3 g1((unsigned)(nJ * (nK / G1)), c->L);
@@ -1880,6 +1916,9 @@ inline bool c1_direct(const hl_ctx *c, const MacGeom &g, const MaskArgs &M) {
 // a work item's slots are 4 consecutive natural points; the column groups must be pure c0 / pure c1
 // or a single group.
 inline bool c1_in_ok(const MacGeom &g, const MaskArgs &M, const uint64_t *ct_in) {
+  // whole 16-column c1 groups: the forward stage transposes c1 into X (k_c1_tx16, full 128-B lines)
+  // -- the MAC's box gather would move 16-B pieces (and twice: a box carries 2 points per stage)
+  if (g.CW == 16 && M.nK % 16 == 0) return false;
   if (!(M.c1_done && (g.nCg == 1 || M.nK % g.CW == 0))) return false;
   CUtensorMap probe;                                    // the launch re-encodes the same map
   return c1_tmap(&probe, ct_in, g.LN, M.nK, g.nJ, (int)std::min<int64_t>(g.CW, M.nK));
