@@ -198,6 +198,11 @@ extern "C" int hl_ctx_create(uint32_t N, uint32_t L, uint32_t log2_t, const uint
     pc.r64_sh = h_shoup(pc.r64, p);
     pc.c40 = h_powmod(2, 40, p); pc.c40_sh = h_shoup(pc.c40, p);
     pc.mc = ((1ull << 50) - p) < (1ull << 32) ? (1ull << 50) - p : 0;
+    for (int d = 7; d <= 12; d++) {
+      const uint64_t k = h_powmod(2, 8 * d, p);
+      pc.ek0[d - 7] = (uint32_t)(k & ((1u << 25) - 1));
+      pc.ek1[d - 7] = (uint32_t)(k >> 25);
+    }
     {   // RNS decryption constants: theta_l = t * inv_l / p_l = I + F / 2^64  (inv_l = (q/p_l)^-1 mod p_l)
       const hl_u128 ti = ((hl_u128)1 << log2_t) * c->Ml_inv[l];
       pc.dec_I = (uint64_t)(ti / p);

@@ -24,6 +24,9 @@ struct PrimeConsts {
   uint64_t c40, c40_sh, c72, c72_sh;   // 2^40, 2^72 mod p (tensor-core MAC recombination) + Shoup
   uint64_t dec_I, dec_F;   // theta_l = t ((q/p)^-1 mod p) / p = dec_I + dec_F 2^-64 (RNS decryption, row f3)
   uint64_t mc;             // 2^50 - p if < 2^32 (pseudo-Mersenne fold 2^50 = mc mod p), else 0
+  // tensor-core MAC epilogue (mac_tc.cuh): k_d = 2^(8d) mod p for the diagonals d = 7..12 as two
+  // 25-bit limbs (k_d = ek0 + ek1 2^25); the fast recombination needs mc < 2^27
+  uint32_t ek0[6], ek1[6];
   uint64_t delta;     // Delta mod p, Delta = floor(q / t)
   uint64_t delta_sh;  // Shoup companion of delta
   uint64_t ninv;      // N^-1 mod p

@@ -23,6 +23,7 @@
 // accumulators; one 128-bit reduction per output.
 #include <cuda.h>   // CUtensorMap (the MAC's c1 loads; encoded through the runtime's driver entry point)
 #include <cuda_runtime.h>
+#include <nvtx3/nvToolsExt.h>   // header-only NVTX v3: named ranges for nsys / Nsight timelines
 
 #include <algorithm>
 #include <atomic>
@@ -1775,25 +1776,28 @@ template <int CW>
 void launch_mac_tc_t(const hl_ctx *c, MacTcArgs A, int smem_budget, int grid, cudaStream_t st) {
   using T = TcGeom<CW>;
   static PerDevice init;
-  if (init.first()) { set_smem(k_mac_tc<CW>, T::SMEM_MAX); }
+  if (init.first()) { set_smem(k_mac_tc<CW, true>, T::SMEM_MAX); set_smem(k_mac_tc<CW, false>, T::SMEM_MAX); }
+  bool fast = true;             // the fast epilogue recombination needs 2^50 - p < 2^27 for every prime
+  for (uint32_t l = 0; l < c->L; l++) fast = fast && c->dp.pc[l].mc != 0 && c->dp.pc[l].mc < (1ull << 27);
   // pure column groups (every group all c0 or all c1): a stage holds the X residues or the c1 box
   A.ring = tc_ring<CW>(A.g.RT, smem_budget, A.c1_bytes, A.c1_in && A.c1_nK % CW == 0);
   static const bool prof = getenv("HELINEAR_MAC_PROF") != nullptr;
   A.prof = nullptr;
-  if (prof) cudaMalloc(&A.prof, 8 * sizeof(unsigned long long)), cudaMemsetAsync(A.prof, 0, 64, st);
+  if (prof) cudaMalloc(&A.prof, 10 * sizeof(unsigned long long)), cudaMemsetAsync(A.prof, 0, 80, st);
   {
   KTimer kt(c, HL_K_MAC, st);
-  k_mac_tc<CW><<<grid, T::THREADS, A.ring.smem, st>>>(A, c->dp);
+  if (fast) k_mac_tc<CW, true><<<grid, T::THREADS, A.ring.smem, st>>>(A, c->dp);
+  else k_mac_tc<CW, false><<<grid, T::THREADS, A.ring.smem, st>>>(A, c->dp);
   }
   if (prof) {   // diagnostics: average cycles per CTA waiting, by role
-    unsigned long long h[8];
-    cudaMemcpyAsync(h, A.prof, 64, cudaMemcpyDeviceToHost, st);
+    unsigned long long h[10];
+    cudaMemcpyAsync(h, A.prof, 80, cudaMemcpyDeviceToHost, st);
     cudaStreamSynchronize(st);
     const double n = c->num_sms;
-    fprintf(stderr, "[mac_tc CW=%d nIs=%d nJ=%d RT=%d nst=%d sb=%d] total %.0f | prod.empty %.0f | mma.tempty %.0f "
-            "mma.full %.0f mma.zfull %.0f mma.issue %.0f | conv.full %.0f | epi.tfull %.0f (cycles/CTA)\n", CW, A.g.nIs,
-            A.g.nJ, A.g.RT, A.ring.nst, A.ring.sbytes, h[7] / n, h[0] / n, h[1] / n, h[2] / n, h[3] / n, h[6] / n,
-            h[4] / n, h[5] / n);
+    fprintf(stderr, "[mac_tc CW=%d nIs=%d nJ=%d RT=%d nst=%d sb=%d] total %.0f | prod.empty %.0f | mma.item %.0f mma.tempty %.0f "
+            "mma.full %.0f mma.zfull %.0f mma.issue %.0f | conv.full %.0f | epi.item %.0f epi.tfull %.0f (cycles/CTA)\n", CW,
+            A.g.nIs, A.g.nJ, A.g.RT, A.ring.nst, A.ring.sbytes, h[7] / n, h[0] / n, h[8] / n, h[1] / n, h[2] / n, h[3] / n,
+            h[6] / n, h[4] / n, h[9] / n, h[5] / n);
     cudaFree(A.prof);
   }
 }
@@ -1964,6 +1968,13 @@ void launch_inv_mask(const hl_ctx *c, const uint64_t *ct_ntt, uint64_t *masked, 
 // =========================================================================================
 // entry points
 // =========================================================================================
+// NVTX range over a host-side scope (an API call or one pipeline stage of it): nsys / Nsight Systems
+// show the library's phases on the CPU timeline and correlate the launches inside them.
+struct NvtxRange {
+  explicit NvtxRange(const char *name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+};
+
 // Every device entry point runs on the context's device and restores the caller's current device.
 struct DeviceGuard {
   int prev = -1, dev = -1;
@@ -1991,6 +2002,7 @@ static int encode_weights_impl(const hl_ctx *c, hl_tile tile, const uint64_t *W,
 extern "C" int hl_encode_weights(const hl_ctx *c, hl_tile tile, const uint64_t *W, int64_t R, int64_t Ma,
                                  int64_t i_begin, int64_t i_end, void *wcache, void *stream) {
   DeviceGuard dg_(c);
+  NvtxRange nvtx_("hl_encode_weights");
   return encode_weights_impl(c, tile, W, R, Ma, Ma, 1, i_begin, i_end, wcache, nullptr, 1, stream);
 }
 
@@ -1998,6 +2010,7 @@ extern "C" int hl_encode_weights_strided(const hl_ctx *c, hl_tile tile, const ui
                                          int64_t ld_row, int64_t ld_col, int64_t i_begin, int64_t i_end, void *wcache,
                                          void *stream) {
   DeviceGuard dg_(c);
+  NvtxRange nvtx_("hl_encode_weights_strided");
   return encode_weights_impl(c, tile, W, R, Ma, ld_row, ld_col, i_begin, i_end, wcache, nullptr, 1, stream);
 }
 
@@ -2005,6 +2018,7 @@ extern "C" int hl_encode_weights_scratch(const hl_ctx *c, hl_tile tile, const ui
                                          int64_t ld_row, int64_t ld_col, int64_t i_begin, int64_t i_end, void *wcache,
                                          uint64_t *scratch, int check, void *stream) {
   DeviceGuard dg_(c);
+  NvtxRange nvtx_("hl_encode_weights_scratch");
   if (!scratch) return hl_fail(HL_EINVAL, "hl_encode_weights_scratch: scratch is NULL");
   return encode_weights_impl(c, tile, W, R, Ma, ld_row, ld_col, i_begin, i_end, wcache, scratch, check, stream);
 }
@@ -2061,6 +2075,7 @@ extern "C" int hl_he_matmul(const hl_ctx *c, hl_tile tile, const void *wcache, i
                             int64_t i_begin, int64_t i_end, const uint64_t *ct_in, void *workspace,
                             uint64_t *ct_out, void *stream) {
   DeviceGuard dg_(c);
+  NvtxRange nvtx_("hl_he_matmul");
   int rc;
   if ((rc = check_ptrs({c, wcache, ct_in, workspace, ct_out}, "hl_he_matmul"))) return rc;
   Geo g;
@@ -2088,6 +2103,7 @@ extern "C" int hl_mask_and_share(const hl_ctx *c, hl_tile tile, int64_t Ma, int6
                                  int64_t i_end, const uint64_t *ct_out, uint64_t seed, int compress,
                                  uint64_t *ct_masked, uint64_t *share, void *stream) {
   DeviceGuard dg_(c);
+  NvtxRange nvtx_("hl_mask_and_share");
   int rc;
   if ((rc = check_ptrs({c, ct_out, ct_masked, share}, "hl_mask_and_share"))) return rc;
   Geo g;
@@ -2104,6 +2120,7 @@ extern "C" int hl_he_matmul_share(const hl_ctx *c, hl_tile tile, const void *wca
                                   void *workspace, uint64_t *ct_out_ntt, uint64_t seed, int compress,
                                   uint64_t *ct_masked, uint64_t *share, void *stream) {
   DeviceGuard dg_(c);
+  NvtxRange nvtx_("hl_he_matmul_share");
   int rc;
   if ((rc = check_ptrs({c, wcache, ct_in, workspace, ct_out_ntt, ct_masked, share}, "hl_he_matmul_share")))
     return rc;
@@ -2198,6 +2215,7 @@ static int linear_batch_run(const hl_ctx *c, hl_tile tile, int n, const hl_linea
   for (int i : ord) serial = serial && E[i].g.nK >= serial_nk;
   cudaStream_t sf = (cudaStream_t)c->fwd_stream;
   auto fwd = [&](int i) {
+    NvtxRange nr("hl.batch.forward_ntt");
     if (ready) cudaStreamWaitEvent(sf, ready[i], 0);
     if (expand_seed)
       expand_seeded(c, E[i].g.nJ * E[i].g.nK, expand_seed[i], const_cast<uint64_t *>(d[i].ct_in), sf);
@@ -2205,6 +2223,7 @@ static int linear_batch_run(const hl_ctx *c, hl_tile tile, int n, const hl_linea
     cudaEventRecord(e_fwd[i], sf);
   };
   auto inv = [&](int i) {
+    NvtxRange nr("hl.batch.inverse_ntt_mask");
     if (c->N == 4096) launch_inv_mask<12>(c, d[i].ct_out_ntt, d[i].ct_masked, d[i].share, E[i].M, E[i].g.nIs * E[i].g.nK, s1);
     else launch_inv_mask<13>(c, d[i].ct_out_ntt, d[i].ct_masked, d[i].share, E[i].M, E[i].g.nIs * E[i].g.nK, s1);
   };
@@ -2229,6 +2248,7 @@ static int linear_batch_run(const hl_ctx *c, hl_tile tile, int n, const hl_linea
   for (int k = 0; k < na; k++) {
     const int i = ord[k];
     cudaStreamWaitEvent(s0, e_fwd[i], 0);
+    NvtxRange nr("hl.batch.mac");
     launch_mac(c, (const uint2 *)d[i].wcache, (const uint32_t *)d[i].workspace, d[i].ct_out_ntt, E[i].mg, s0,
                kMacSmemShared, 0, E[i].M.c1_done ? &E[i].M : nullptr, d[i].ct_masked, d[i].ct_in);
     cudaEventRecord(e_mac[i], s0);
@@ -2246,6 +2266,7 @@ static int linear_batch_run(const hl_ctx *c, hl_tile tile, int n, const hl_linea
 
 extern "C" int hl_he_linear_batch(const hl_ctx *c, hl_tile tile, int n, const hl_linear_desc *d, void *stream) {
   DeviceGuard dg_(c);
+  NvtxRange nvtx_("hl_he_linear_batch");
   int rc;
   if ((rc = check_ptrs({c, d}, "hl_he_linear_batch"))) return rc;
   if (n <= 0) return hl_fail(HL_EINVAL, "hl_he_linear_batch: n must be positive");
@@ -2265,6 +2286,7 @@ static void expand_seeded(const hl_ctx *c, int64_t nct, uint64_t a_seed, uint64_
 extern "C" int hl_expand_seeded(const hl_ctx *c, hl_tile tile, int64_t R, int64_t Nb, uint64_t a_seed,
                                 uint64_t *ct_in, void *stream) {
   DeviceGuard dg_(c);
+  NvtxRange nvtx_("hl_expand_seeded");
   int rc;
   if ((rc = check_ptrs({c, ct_in}, "hl_expand_seeded"))) return rc;
   Geo g;
@@ -2308,6 +2330,7 @@ __global__ void k_unpack50_c0(const uint64_t *__restrict__ in, int64_t words, ui
 extern "C" int hl_he_linear_batch_host(const hl_ctx *c, hl_tile tile, int n, const hl_linear_host_desc *h,
                                        void *stream) {
   DeviceGuard dg_(c);
+  NvtxRange nvtx_("hl_he_linear_batch_host");
   int rc;
   if ((rc = check_ptrs({c, h}, "hl_he_linear_batch_host"))) return rc;
   if (n <= 0) return hl_fail(HL_EINVAL, "hl_he_linear_batch_host: n must be positive");
@@ -2375,6 +2398,7 @@ extern "C" int hl_he_linear_batch_host(const hl_ctx *c, hl_tile tile, int n, con
 // ---------------------------------------------------------------------------------------
 extern "C" int hl_sk_prepare(const hl_ctx *c, const int8_t *sk, uint64_t *s_hat, void *stream) {
   DeviceGuard dg_(c);
+  NvtxRange nvtx_("hl_sk_prepare");
   int rc;
   if ((rc = check_ptrs({c, sk, s_hat}, "hl_sk_prepare"))) return rc;
   std::vector<uint64_t> res((size_t)c->L * c->N);
@@ -2394,6 +2418,7 @@ extern "C" int hl_sk_prepare(const hl_ctx *c, const int8_t *sk, uint64_t *s_hat,
 extern "C" int hl_encrypt_device(const hl_ctx *c, const uint64_t *s_hat, hl_tile tile, const uint64_t *X, int64_t Nb,
                                  int64_t R, uint64_t seed, uint64_t *ct_in, void *stream) {
   DeviceGuard dg_(c);
+  NvtxRange nvtx_("hl_encrypt_device");
   int rc;
   if ((rc = check_ptrs({c, s_hat, X, ct_in}, "hl_encrypt_device"))) return rc;
   Geo g;
@@ -2428,6 +2453,7 @@ extern "C" int hl_encrypt_device(const hl_ctx *c, const uint64_t *s_hat, hl_tile
 extern "C" int hl_decrypt_share_device(const hl_ctx *c, const uint64_t *s_hat, hl_tile tile, const uint64_t *ct_masked,
                                        int64_t Ma, int64_t Nb, uint64_t *share_client, void *stream) {
   DeviceGuard dg_(c);
+  NvtxRange nvtx_("hl_decrypt_share_device");
   int rc;
   if ((rc = check_ptrs({c, s_hat, ct_masked, share_client}, "hl_decrypt_share_device"))) return rc;
   Geo g;
@@ -2480,6 +2506,7 @@ __global__ void k_share_acc(uint64_t *__restrict__ dst, const uint64_t *__restri
 extern "C" int hl_share_accumulate(const hl_ctx *c, uint64_t *dst, const uint64_t *src, int64_t rows, int64_t cols,
                                    int transpose, void *stream) {
   DeviceGuard dg_(c);
+  NvtxRange nvtx_("hl_share_accumulate");
   int rc;
   if ((rc = check_ptrs({c, dst, src}, "hl_share_accumulate"))) return rc;
   if (rows <= 0 || cols <= 0) return hl_fail(HL_EINVAL, "hl_share_accumulate: rows, cols must be positive");
@@ -2513,6 +2540,7 @@ static int fc_geom(const hl_ctx *c, int64_t Nb, int64_t R, int64_t Ma, FcGeom *g
 extern "C" int hl_fc_layout(const hl_ctx *c, int64_t Nb, int64_t R, int64_t Ma, int64_t *wplanes_bytes,
                             int64_t *workspace_bytes) {
   DeviceGuard dg_(c);
+  NvtxRange nvtx_("hl_fc_layout");
   FcGeom g;
   int rc;
   if ((rc = fc_geom(c, Nb, R, Ma, &g))) return rc;
@@ -2524,12 +2552,14 @@ extern "C" int hl_fc_layout(const hl_ctx *c, int64_t Nb, int64_t R, int64_t Ma, 
 extern "C" int hl_fc_encode_weights(const hl_ctx *c, const uint64_t *W, int64_t R, int64_t Ma, void *wplanes,
                                     void *stream) {
   DeviceGuard dg_(c);
+  NvtxRange nvtx_("hl_fc_encode_weights");
   return hl_fc_encode_weights_chk(c, W, R, Ma, wplanes, 1, stream);
 }
 
 extern "C" int hl_fc_encode_weights_chk(const hl_ctx *c, const uint64_t *W, int64_t R, int64_t Ma, void *wplanes,
                                         int check, void *stream) {
   DeviceGuard dg_(c);
+  NvtxRange nvtx_("hl_fc_encode_weights_chk");
   int rc;
   if ((rc = check_ptrs({c, W, wplanes}, "hl_fc_encode_weights"))) return rc;
   FcGeom g;
@@ -2554,6 +2584,7 @@ extern "C" int hl_fc_encode_weights_chk(const hl_ctx *c, const uint64_t *W, int6
 extern "C" int hl_fc_local_share(const hl_ctx *c, const uint64_t *X1, const void *wplanes, const uint64_t *bias,
                                  int64_t Nb, int64_t R, int64_t Ma, void *workspace, uint64_t *share, void *stream) {
   DeviceGuard dg_(c);
+  NvtxRange nvtx_("hl_fc_local_share");
   int rc;
   if ((rc = check_ptrs({c, X1, wplanes, workspace, share}, "hl_fc_local_share"))) return rc;
   FcGeom g;
@@ -2576,6 +2607,7 @@ extern "C" int hl_fc_local_share(const hl_ctx *c, const uint64_t *X1, const void
 // ---------------------------------------------------------------------------------------
 extern "C" int hl_pk_prepare(const hl_ctx *c, const uint64_t *pk, uint64_t *pk_hat, void *stream) {
   DeviceGuard dg_(c);
+  NvtxRange nvtx_("hl_pk_prepare");
   int rc;
   if ((rc = check_ptrs({c, pk, pk_hat}, "hl_pk_prepare"))) return rc;
   cudaStream_t st = (cudaStream_t)stream;
@@ -2592,6 +2624,7 @@ extern "C" int hl_he_matmul_share_rr(const hl_ctx *c, hl_tile tile, const void *
                                      uint64_t *rr_ws, uint64_t seed, uint64_t *ct_masked, uint64_t *share,
                                      void *stream) {
   DeviceGuard dg_(c);
+  NvtxRange nvtx_("hl_he_matmul_share_rr");
   int rc;
   if ((rc = check_ptrs({c, wcache, ct_in, workspace, ct_out_ntt, pk_hat, rr_ws, ct_masked, share},
                        "hl_he_matmul_share_rr")))
@@ -2632,6 +2665,7 @@ extern "C" int hl_he_linear_host(const hl_ctx *c, hl_tile tile, const void *wcac
                                  void *workspace, uint64_t *dev_ct_out_ntt, uint64_t *dev_ct_masked,
                                  uint64_t *dev_share, void *stream) {
   DeviceGuard dg_(c);
+  NvtxRange nvtx_("hl_he_linear_host");
   int rc;
   if ((rc = check_ptrs({c, wcache, ct_in_host, ct_masked_host, share_host, dev_ct_in, workspace,
                         dev_ct_out_ntt, dev_ct_masked, dev_share}, "hl_he_linear_host")))
@@ -2654,6 +2688,7 @@ extern "C" int hl_he_linear_host(const hl_ctx *c, hl_tile tile, const void *wcac
 extern "C" int hl_poly_mul(const hl_ctx *c, const uint64_t *a, const uint64_t *b, uint64_t *out, int64_t npoly,
                            void *scratch, void *stream) {
   DeviceGuard dg_(c);
+  NvtxRange nvtx_("hl_poly_mul");
   int rc;
   if ((rc = check_ptrs({c, a, b, out, scratch}, "hl_poly_mul"))) return rc;
   if (npoly <= 0) return hl_fail(HL_EINVAL, "hl_poly_mul: npoly must be positive");
@@ -2670,6 +2705,7 @@ extern "C" int hl_poly_mul(const hl_ctx *c, const uint64_t *a, const uint64_t *b
 
 extern "C" int hl_ntt_roundtrip(const hl_ctx *c, uint64_t *x, int64_t npoly, void *scratch, void *stream) {
   DeviceGuard dg_(c);
+  NvtxRange nvtx_("hl_ntt_roundtrip");
   int rc;
   if ((rc = check_ptrs({c, x, scratch}, "hl_ntt_roundtrip"))) return rc;
   if (npoly <= 0) return hl_fail(HL_EINVAL, "hl_ntt_roundtrip: npoly must be positive");

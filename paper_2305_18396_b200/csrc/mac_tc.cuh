@@ -56,6 +56,11 @@ struct TcGeom {
   // CW = 16: the converter warps take turns (one warp converts a whole stage, 2 stages in flight);
   // CW <= 8: both warps convert each stage (its conversion is short; measured faster on c2)
   static constexpr bool ALT_CONV = CW >= 16;
+  // CW = 16: the accumulator columns [NM, N) that the a = 0 MMA does not initialise are zeroed by
+  // one extra MMA per slot (A x a zero B image of N - NM = 96 rows, accumulate off) instead of
+  // tcgen05.st by the epilogue warps (a 96-column store + wait per warp and slot)
+  static constexpr bool ZMMA = CW >= 16;
+  static constexpr int ZZ_BYTES = ZMMA ? 2 * (N - NM) * 16 : 0;   // the zero B image
   static constexpr int EPI0 = 2 + NCONV;                 // first epilogue warp
   static constexpr int THREADS = 32 * (EPI0 + 8);        // producer + MMA + converters + 8 epilogue warps
   static constexpr int SMEM_MAX = 232448;                // 227 KB opt-in per CTA
@@ -83,10 +88,10 @@ TcRing tc_ring(int rt, int smem_budget, int c1_bytes = 0, bool x_union = false) 
     r.sbytes = r.c1_off + (c1_bytes + 127) / 128 * 128;
   }
   const int stg = T::REG_EPI ? 0 : (rt * T::STG_STRIDE * 8 + 127) / 128 * 128;
-  const int fixed = T::NZ * T::Z_BYTES + stg + T::BAR_BYTES;
+  const int fixed = T::NZ * T::Z_BYTES + T::ZZ_BYTES + stg + T::BAR_BYTES;
   r.nst = std::max(2, std::min(T::MAX_NST, (std::min(smem_budget, T::SMEM_MAX) - fixed) / r.sbytes));
   r.z_off = r.nst * r.sbytes;
-  r.stg_off = r.z_off + T::NZ * T::Z_BYTES;
+  r.stg_off = r.z_off + T::NZ * T::Z_BYTES + T::ZZ_BYTES;
   r.bar_off = r.stg_off + stg;
   r.smem = r.bar_off + T::BAR_BYTES;
   return r;
@@ -268,7 +273,8 @@ __device__ __forceinline__ void conv_unit(unsigned char *z, int h, int c, int gq
   }
 }
 
-template <int CW>
+// FAST: every prime has 2^50 - p < 2^27 (the fast epilogue recombination; the launch checks)
+template <int CW, bool FAST>
 // <= 80 registers for CW <= 8 (minBlocks 2): leaves room for NTT CTAs on the same SM when the
 // MAC of one matmul runs concurrently with the NTTs of its neighbours (hl_he_linear_batch)
 __global__ void __launch_bounds__(TcGeom<CW>::THREADS, (CW <= 8 ? 2 : 1))
@@ -289,7 +295,7 @@ k_mac_tc(const __grid_constant__ MacTcArgs A, DevParams P) {
   const int total_items = g.nIt * g.nCg * (g.LN / 4);
 
   // ---- setup: zero the Toeplitz images (only data rows are rewritten), barriers, TMEM
-  for (int i = threadIdx.x; i < T::NZ * T::Z_BYTES / 16; i += blockDim.x)
+  for (int i = threadIdx.x; i < (T::NZ * T::Z_BYTES + T::ZZ_BYTES) / 16; i += blockDim.x)
     reinterpret_cast<uint4 *>(zring)[i] = make_uint4(0, 0, 0, 0);
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
   if (threadIdx.x == 0) {
@@ -311,7 +317,7 @@ k_mac_tc(const __grid_constant__ MacTcArgs A, DevParams P) {
   // The limb-plane MMA a accumulates into the column window [a*CW, a*CW + NM) of its buffer (the
   // Toeplitz shift lives in the accumulator address): columns [NM, N) must start at zero.  The
   // epilogue re-zeroes them after draining a buffer; here every buffer is zeroed once.
-  if (warp >= T::EPI0) {
+  if (!T::ZMMA && warp >= T::EPI0) {
     const uint32_t lanes = (uint32_t)(32 * (warp & 3)) << 16;
     for (int b = 0; b < T::NBUF; b++)
       for (int col = T::NM + ((warp - T::EPI0) >> 2); col < T::N; col += 2)
@@ -321,7 +327,7 @@ k_mac_tc(const __grid_constant__ MacTcArgs A, DevParams P) {
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
-  unsigned long long pw[8] = {0, 0, 0, 0, 0, 0, 0, 0};   // profiling accumulators (registers)
+  unsigned long long pw[10] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0};   // profiling accumulators (registers)
   const long long t_start = clock64();
 
   if (warp == 0) {
@@ -373,13 +379,18 @@ k_mac_tc(const __grid_constant__ MacTcArgs A, DevParams P) {
     // tiles of <= 64 rows use M = 64 (half the A-operand shared-memory reads per MMA); the
     // accumulator rows then sit in lanes 32(r/16) + r%16 (profiles/r01/microbench_umma_i8.log)
     // M per item: tiles of <= 64 rows (also a short last tile of uneven tiling) use M = 64
+    const uint32_t zdesc128 = umma_idesc_u8(128, T::ZMMA ? T::N - T::NM : 16);
+    const uint32_t zdesc64 = umma_idesc_u8(64, T::ZMMA ? T::N - T::NM : 16);
+    const uint32_t zz = smem_u32(zring + T::NZ * T::Z_BYTES);     // the zero B image (ZMMA)
     const uint32_t idesc128 = umma_idesc_u8(128, T::NM);
     const uint32_t idesc64 = umma_idesc_u8(64, T::NM);
     int st = 0;
     uint32_t ph = 0;
     uint32_t tile_no = 0, zseq = 0;
     for (uint32_t seq = 0;; seq++) {
+      const long long tw0_ = A.prof ? clock64() : 0;
       const int item = tc_next_item(ifull, iempty, itm, seq);
+      if (A.prof && lane == 0) pw[8] += (unsigned long long)(clock64() - tw0_);
       if (item < 0) break;
       const TcItem it = tc_decode(g, item);
       const int rows = min(g.RT, g.nIp - g.RT * it.t);
@@ -399,6 +410,11 @@ k_mac_tc(const __grid_constant__ MacTcArgs A, DevParams P) {
           const uint32_t a0 = smem_u32(smem + st * SB) + A.ring.a_off;
           const uint32_t z0 = smem_u32(zring + zi * T::Z_BYTES);
           if (elect_one()) {
+            if constexpr (T::ZMMA) {
+              if (kk == 0)       // zero the columns [NM, N) the a = 0 MMA does not write
+                umma_i8(dcol + T::NM, umma_sdesc(a0, lbo_a, 128), umma_sdesc(zz, (T::N - T::NM) * 16, 128),
+                        rows <= 64 ? zdesc64 : zdesc128, 0u);
+            }
 #pragma unroll
             for (int a = 0; a < 7; a++) {
               const uint64_t ad = umma_sdesc(a0 + a * plane, lbo_a, 128);
@@ -544,7 +560,9 @@ k_mac_tc(const __grid_constant__ MacTcArgs A, DevParams P) {
     const int et = threadIdx.x - 32 * T::EPI0;
     uint32_t tile_no = 0;
     for (uint32_t seq = 0;; seq++) {
+      const long long tw0_ = A.prof ? clock64() : 0;
       const int item = tc_next_item(ifull, iempty, itm, seq);
+      if (A.prof && et == 0) pw[9] += (unsigned long long)(clock64() - tw0_);
       if (item < 0) break;
       const TcItem it = tc_decode(g, item);
       const int l = (it.sq * T::SPI) / A.N;
@@ -614,9 +632,48 @@ k_mac_tc(const __grid_constant__ MacTcArgs A, DevParams P) {
         const uint32_t buf = tile_no % T::NBUF, tph = (tile_no / T::NBUF) & 1;
         mbar_wait_p(&tfull[buf], tph, (A.prof && et == 0) ? &pw[5] : nullptr);
         tc_fence_after();
-        // three column groups (d < 5 -> L, 5..8 -> M, 9..12 -> H) loaded and folded one at a time
+        // Fast recombination (pc.mc < 2^27, every prime of reading C4): with k_d = 2^(8d) mod p in
+        // 25-bit limbs, sum_d S_d 2^(8d) = A0 + A1 2^25 (mod p), accumulated from the diagonals as
+        // they are loaded:  A0 = S_0 + S_1 2^8 + S_2 2^16 + S_3 2^24 + sum_{d>=7} S_d k_d0 < 2^59,
+        // A1 = S_4 2^7 + S_5 2^15 + S_6 2^23 + sum_{d>=7} S_d k_d1 < 2^60 (2^(8d) < p for d <= 6);
+        // then two pseudo-Mersenne folds (2^50 = mc mod p) -- one third of the integer multiplies of
+        // the general path (L + M 2^40 + H 2^72 as a 124-bit value, Shoup + Barrett), which made this
+        // epilogue the bottleneck of the fat products (c3, c4).
+        // General path: three column groups (d < 5 -> L, 5..8 -> M, 9..12 -> H), one at a time.
+        constexpr bool fastr = FAST;
         uint64_t L[CH], M[CH], H[CH];
-        if (active) {
+        if (active && fastr) {
+          const uint32_t base = tmem + ((uint32_t)(32 * q) << 16) + buf * T::N + hh * CH;
+          uint32_t v[5][CH];
+#pragma unroll
+          for (int d = 0; d < 5; d++) tmem_ld_cw<CH>(base + d * CW, v[d]);
+          asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+          for (int c = 0; c < CH; c++) {
+            L[c] = (uint64_t)v[0][c] + ((uint64_t)v[1][c] << 8) + ((uint64_t)v[2][c] << 16) + ((uint64_t)v[3][c] << 24);
+            M[c] = (uint64_t)v[4][c] << 7;
+          }
+#pragma unroll
+          for (int d = 0; d < 4; d++) tmem_ld_cw<CH>(base + (5 + d) * CW, v[d]);
+          asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+          for (int c = 0; c < CH; c++) {
+            M[c] += ((uint64_t)v[0][c] << 15) + ((uint64_t)v[1][c] << 23);
+            L[c] += (uint64_t)v[2][c] * pc.ek0[0] + (uint64_t)v[3][c] * pc.ek0[1];
+            M[c] += (uint64_t)v[2][c] * pc.ek1[0] + (uint64_t)v[3][c] * pc.ek1[1];
+          }
+#pragma unroll
+          for (int d = 0; d < 4; d++) tmem_ld_cw<CH>(base + (9 + d) * CW, v[d]);
+          asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+          for (int c = 0; c < CH; c++) {
+#pragma unroll
+            for (int d = 0; d < 4; d++) {
+              L[c] += (uint64_t)v[d][c] * pc.ek0[2 + d];
+              M[c] += (uint64_t)v[d][c] * pc.ek1[2 + d];
+            }
+          }
+        } else if (active) {
           const uint32_t base = tmem + ((uint32_t)(32 * q) << 16) + buf * T::N + hh * CH;
           uint32_t v[5][CH];
 #pragma unroll
@@ -648,7 +705,7 @@ k_mac_tc(const __grid_constant__ MacTcArgs A, DevParams P) {
             for (int d = 1; d < 4; d++) H[c] += (uint64_t)v[d][c] << (8 * d);
           }
         }
-        {   // re-zero the columns no a = 0 MMA initialises (see the setup) -- only columns of this
+        if constexpr (!T::ZMMA) {   // re-zero the columns no a = 0 MMA initialises (see the setup) -- only columns of this
             // warp's own half (c / CH == hh): the other warp of the quadrant may still be reading its half
           const uint32_t zb = tmem + ((uint32_t)(32 * q) << 16) + buf * T::N + hh * CH;
 #pragma unroll
@@ -661,16 +718,27 @@ k_mac_tc(const __grid_constant__ MacTcArgs A, DevParams P) {
         if (active) {
 #pragma unroll
           for (int c = 0; c < CH; c++) {
+            uint64_t r;
+            if (fastr) {
+              // T = A0 + A1 2^25 < 2^86 = th 2^50 + tl;  T = tl + th mc (mod p) < 2^50 + 2^63;
+              // fold once more: < 2^50 + 2^41 < 2p
+              const uint64_t lo = L[c] + (M[c] << 25);
+              const uint64_t hi = (M[c] >> 39) + (lo < L[c] ? 1 : 0);
+              const uint64_t th = (lo >> 50) | (hi << 14);
+              uint64_t t = (lo & ((1ull << 50) - 1)) + th * pc.mc;
+              r = (t & ((1ull << 50) - 1)) + (t >> 50) * pc.mc;          // [0, 2p)
+            } else {
             // V = L + M 2^40 + H 2^72 < 2^124 exactly; V mod p = Shoup(V_hi, 2^64 mod p) + (V_lo mod p)
             const hl_u128 V = (hl_u128)L[c] + ((hl_u128)M[c] << 40) + ((hl_u128)H[c] << 72);
             const uint64_t vh = (uint64_t)(V >> 64), vl = (uint64_t)V;
-            uint64_t r = shoup_mul(vh, pc.r64, pc.r64_sh, pc.p);           // [0, 2p)
+            r = shoup_mul(vh, pc.r64, pc.r64_sh, pc.p);                    // [0, 2p)
             if (pc.mc) {
               // pseudo-Mersenne fold, 2^50 = mc (mod p): vl = a 2^50 + b -> b + a mc < 2^50 + 2^46 < 2p
               r += (vl & ((1ull << 50) - 1)) + (vl >> 50) * pc.mc;
             } else {
               r += vl - __umul64hi(vl, pc.mu) * pc.p;                      // [0, 2p)
             }                                                              // r in [0, 4p) < 2^52
+            }
             if (!A.lazy_out) {
               r = r >= pc.two_p ? r - pc.two_p : r;
               r = r >= pc.p ? r - pc.p : r;
@@ -702,9 +770,9 @@ k_mac_tc(const __grid_constant__ MacTcArgs A, DevParams P) {
   if (A.prof) {
     const unsigned long long tot = (unsigned long long)(clock64() - t_start);
     if (threadIdx.x == 0) { atomicAdd(&A.prof[0], pw[0]); atomicAdd(&A.prof[7], tot); }
-    if (threadIdx.x == 32) { atomicAdd(&A.prof[1], pw[1]); atomicAdd(&A.prof[2], pw[2]); atomicAdd(&A.prof[3], pw[3]); atomicAdd(&A.prof[6], pw[6]); }
+    if (threadIdx.x == 32) { atomicAdd(&A.prof[1], pw[1]); atomicAdd(&A.prof[2], pw[2]); atomicAdd(&A.prof[3], pw[3]); atomicAdd(&A.prof[6], pw[6]); atomicAdd(&A.prof[8], pw[8]); }
     if (threadIdx.x == 64) atomicAdd(&A.prof[4], pw[4]);
-    if (threadIdx.x == 32 * T::EPI0) atomicAdd(&A.prof[5], pw[5]);
+    if (threadIdx.x == 32 * T::EPI0) { atomicAdd(&A.prof[5], pw[5]); atomicAdd(&A.prof[9], pw[9]); }
   }
   tc_fence_before();
   __syncthreads();

@@ -475,6 +475,34 @@ def test_encode_two_pass_equals_one_pass(hl, ctx4096, ctx8192, N, shape, tile, s
     assert hl.to_host(one).tobytes() == hl.to_host(two).tobytes()
 
 
+@pytest.mark.parametrize("mc_bits", [30, 45])
+def test_mac_general_epilogue_non_pseudo_mersenne_primes(hl, mc_bits):
+    """Primes far below 2^50 (2^50 - p >= 2^27): the tensor-core MAC's general epilogue
+    (124-bit recombination, Shoup + Barrett / pseudo-Mersenne with a 30-bit fold constant) instead of
+    the fast 25-bit-limb one, through the fused batch call on a ragged shape, CW = 16 and CW = 4:
+    bit-exact against the oracle with the same explicit primes (reading C4 allows any NTT-friendly
+    primes in (2^49, 2^50) through hl_ctx_create)."""
+    N, L = 4096, 2
+    primes, p = [], (((1 << 50) - (1 << mc_bits)) // (2 * N)) * (2 * N) + 1
+    while len(primes) < L:
+        if ref._is_prime(p):
+            primes.append(p)
+        p -= 2 * N
+    ctx = hl.Context(N, L, 37, primes=primes, device=0)
+    P = ref.bfv_params(N, L, 37, primes=primes)
+    for (Nb, R, Ma, tile) in [(256, 48, 40, (16, 8, 16)), (40, 24, 40, (16, 8, 32))]:
+        nI, nJ, nK = ref.tile_counts(tile, Ma, R, Nb)
+        W = synth.weights(1300 + Nb, R, Ma)
+        ct_in = synth.uniform_below(1310 + Nb, (nJ, nK, 2, P.L, P.N), P.primes)
+        e = dict(wcache=ctx.encode_weights(tile, hl.to_device(W)), Ma=Ma, R=R, Nb=Nb, tile=tile,
+                 ct_in=hl.to_device(ct_in), seed=1320)
+        (m, sh), = ctx.he_linear_batch(tile, [e])
+        _sync()
+        em, es = ref.mask_and_share(P, tile, ref.he_matmul(P, tile, W, ct_in, Nb), Ma, Nb, 1320)
+        assert np.array_equal(hl.to_host(m).reshape(em.shape), em)
+        assert np.array_equal(hl.to_host(sh).reshape(es.shape), es)
+
+
 # ------------------------------------------------------------------------- errors
 def test_encode_weights_errors(hl, ctx4096):
     ctx = ctx4096
