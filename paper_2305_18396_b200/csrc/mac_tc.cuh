@@ -62,7 +62,11 @@ struct TcGeom {
   static constexpr bool ZMMA = CW >= 16;
   static constexpr int ZZ_BYTES = ZMMA ? 2 * (N - NM) * 16 : 0;   // the zero B image
   static constexpr int EPI0 = 2 + NCONV;                 // first epilogue warp
-  static constexpr int THREADS = 32 * (EPI0 + 8);        // producer + MMA + converters + 8 epilogue warps
+  // epilogue warps: 2 per TMEM lane quadrant (4 per quadrant measured: c4 -4 %, c3 +9 %: more warps
+  // share the MMA warp's scheduler)
+  static constexpr int NEPI = 8;
+  static constexpr int CH = CW * 4 / NEPI;               // columns per epilogue warp
+  static constexpr int THREADS = 32 * (EPI0 + NEPI);     // producer + MMA + converters + epilogue warps
   static constexpr int SMEM_MAX = 232448;                // 227 KB opt-in per CTA
   static_assert(A_OFF % 16 == 0 && Z_BYTES % 128 == 0, "alignment");
 };
@@ -301,8 +305,8 @@ k_mac_tc(const __grid_constant__ MacTcArgs A, DevParams P) {
   if (threadIdx.x == 0) {
     for (int i = 0; i < NST; i++) { mbar_init(&full[i], 1); mbar_init(&empty[i], 1); }
     for (int i = 0; i < T::NZ; i++) { mbar_init(&zfull[i], T::ALT_CONV ? 32 : 64); mbar_init(&zempty[i], 1); }
-    for (int i = 0; i < T::NBUF; i++) { mbar_init(&tfull[i], 1); mbar_init(&tempty[i], 8); }
-    for (int i = 0; i < kItemRing; i++) { mbar_init(&ifull[i], 1); mbar_init(&iempty[i], 1 + T::NCONV + 8); }
+    for (int i = 0; i < T::NBUF; i++) { mbar_init(&tfull[i], 1); mbar_init(&tempty[i], T::NEPI); }
+    for (int i = 0; i < kItemRing; i++) { mbar_init(&ifull[i], 1); mbar_init(&iempty[i], 1 + T::NCONV + T::NEPI); }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 1) {
@@ -327,7 +331,7 @@ k_mac_tc(const __grid_constant__ MacTcArgs A, DevParams P) {
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
-  unsigned long long pw[10] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0};   // profiling accumulators (registers)
+  unsigned long long pw[12] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};   // profiling accumulators (registers)
   const long long t_start = clock64();
 
   if (warp == 0) {
@@ -403,33 +407,38 @@ k_mac_tc(const __grid_constant__ MacTcArgs A, DevParams P) {
         const uint32_t dcol = tmem + buf * T::N;
         for (int kk = 0; kk < A.njc; kk++, zseq++) {
           const uint32_t zi = zseq % T::NZ, zph = (zseq / T::NZ) & 1;
+          if (A.prof && lane == 0 && (kk > 0)) pw[11] += (unsigned long long)clock64();
           mbar_wait_p(&full[st], ph, (A.prof && lane == 0) ? &pw[2] : nullptr);
           mbar_wait_p(&zfull[zi], zph, (A.prof && lane == 0) ? &pw[3] : nullptr);
           tc_fence_after();
           const long long ti0 = A.prof ? clock64() : 0;
           const uint32_t a0 = smem_u32(smem + st * SB) + A.ring.a_off;
           const uint32_t z0 = smem_u32(zring + zi * T::Z_BYTES);
+          // descriptors computed by the whole warp (warp-uniform values, before the elected branch):
+          // plane a's descriptor is plane 0's plus a * plane / 16 in the 14-bit address field
+          const uint64_t ad0 = umma_sdesc(a0, lbo_a, 128), bd = umma_sdesc(z0, T::ZR * 16, 128);
+          const uint64_t zd = umma_sdesc(zz, (T::N - T::NM) * 16, 128);
+          const uint32_t pl16 = plane >> 4;
+          const uint32_t zidesc = rows <= 64 ? zdesc64 : zdesc128;
           if (elect_one()) {
             if constexpr (T::ZMMA) {
               if (kk == 0)       // zero the columns [NM, N) the a = 0 MMA does not write
-                umma_i8(dcol + T::NM, umma_sdesc(a0, lbo_a, 128), umma_sdesc(zz, (T::N - T::NM) * 16, 128),
-                        rows <= 64 ? zdesc64 : zdesc128, 0u);
+                umma_i8(dcol + T::NM, ad0, zd, zidesc, 0u);
             }
 #pragma unroll
-            for (int a = 0; a < 7; a++) {
-              const uint64_t ad = umma_sdesc(a0 + a * plane, lbo_a, 128);
-              const uint64_t bd = umma_sdesc(z0, T::ZR * 16, 128);
-              umma_i8(dcol + a * CW, ad, bd, idesc, (kk | a) ? 1u : 0u);   // D window shifted by a*CW
-            }
+            for (int a = 0; a < 7; a++)
+              umma_i8(dcol + a * CW, ad0 + (uint64_t)(a * pl16), bd, idesc, (kk | a) ? 1u : 0u);   // D window shifted by a*CW
             umma_commit(&empty[st]);
             umma_commit(&zempty[zi]);
           }
           __syncwarp();
-          if (A.prof && lane == 0) pw[6] += (unsigned long long)(clock64() - ti0);
+          if (A.prof && lane == 0) { const long long t1_ = clock64(); pw[6] += (unsigned long long)(t1_ - ti0); if (kk + 1 < A.njc) pw[11] -= (unsigned long long)t1_; }
           if (++st == NST) { st = 0; ph ^= 1; }
         }
+        const long long tc0_ = A.prof ? clock64() : 0;
         if (elect_one()) umma_commit(&tfull[buf]);
         __syncwarp();
+        if (A.prof && lane == 0) pw[10] += (unsigned long long)(clock64() - tc0_);
       }
     }
   } else if (warp < T::EPI0) {
@@ -555,7 +564,7 @@ k_mac_tc(const __grid_constant__ MacTcArgs A, DevParams P) {
     // Recombination: L = sum_{d<5} S_d 2^(8d) < 2^64, M = sum_{d=5..8} S_d 2^(8(d-5)) < 2^56,
     // H = sum_{d=9..12} S_d 2^(8(d-9)) < 2^56 (S_d < 2^31), sum_J W X = L + M 2^40 + H 2^72,
     // reduced as Barrett(L) + Shoup(M, 2^40 mod p) + Shoup(H, 2^72 mod p), each in [0, 2p).
-    constexpr int CH = CW / 2;
+    constexpr int CH = T::CH;
     const int q = warp & 3, hh = (warp - T::EPI0) >> 2;
     const int et = threadIdx.x - 32 * T::EPI0;
     uint32_t tile_no = 0;
@@ -642,7 +651,24 @@ k_mac_tc(const __grid_constant__ MacTcArgs A, DevParams P) {
         // General path: three column groups (d < 5 -> L, 5..8 -> M, 9..12 -> H), one at a time.
         constexpr bool fastr = FAST;
         uint64_t L[CH], M[CH], H[CH];
-        if (active && fastr) {
+        if (active && fastr && CW >= 16) {
+          // all 13 diagonals of the warp's 4 columns in flight at once (one wait)
+          const uint32_t base = tmem + ((uint32_t)(32 * q) << 16) + buf * T::N + hh * CH;
+          uint32_t v[13][CH];
+#pragma unroll
+          for (int d = 0; d < 13; d++) tmem_ld_cw<CH>(base + d * CW, v[d]);
+          asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+          for (int c = 0; c < CH; c++) {
+            L[c] = (uint64_t)v[0][c] + ((uint64_t)v[1][c] << 8) + ((uint64_t)v[2][c] << 16) + ((uint64_t)v[3][c] << 24);
+            M[c] = ((uint64_t)v[4][c] << 7) + ((uint64_t)v[5][c] << 15) + ((uint64_t)v[6][c] << 23);
+#pragma unroll
+            for (int d = 7; d < 13; d++) {
+              L[c] += (uint64_t)v[d][c] * pc.ek0[d - 7];
+              M[c] += (uint64_t)v[d][c] * pc.ek1[d - 7];
+            }
+          }
+        } else if (active && fastr) {
           const uint32_t base = tmem + ((uint32_t)(32 * q) << 16) + buf * T::N + hh * CH;
           uint32_t v[5][CH];
 #pragma unroll
@@ -770,7 +796,7 @@ k_mac_tc(const __grid_constant__ MacTcArgs A, DevParams P) {
   if (A.prof) {
     const unsigned long long tot = (unsigned long long)(clock64() - t_start);
     if (threadIdx.x == 0) { atomicAdd(&A.prof[0], pw[0]); atomicAdd(&A.prof[7], tot); }
-    if (threadIdx.x == 32) { atomicAdd(&A.prof[1], pw[1]); atomicAdd(&A.prof[2], pw[2]); atomicAdd(&A.prof[3], pw[3]); atomicAdd(&A.prof[6], pw[6]); atomicAdd(&A.prof[8], pw[8]); }
+    if (threadIdx.x == 32) { atomicAdd(&A.prof[1], pw[1]); atomicAdd(&A.prof[2], pw[2]); atomicAdd(&A.prof[3], pw[3]); atomicAdd(&A.prof[6], pw[6]); atomicAdd(&A.prof[8], pw[8]); atomicAdd(&A.prof[10], pw[10]); atomicAdd(&A.prof[11], pw[11]); }
     if (threadIdx.x == 64) atomicAdd(&A.prof[4], pw[4]);
     if (threadIdx.x == 32 * T::EPI0) { atomicAdd(&A.prof[5], pw[5]); atomicAdd(&A.prof[9], pw[9]); }
   }
