@@ -1781,23 +1781,29 @@ void launch_mac_tc_t(const hl_ctx *c, MacTcArgs A, int smem_budget, int grid, cu
   for (uint32_t l = 0; l < c->L; l++) fast = fast && c->dp.pc[l].mc != 0 && c->dp.pc[l].mc < (1ull << 27);
   // pure column groups (every group all c0 or all c1): a stage holds the X residues or the c1 box
   A.ring = tc_ring<CW>(A.g.RT, smem_budget, A.c1_bytes, A.c1_in && A.c1_nK % CW == 0);
+  // diagnostics: HELINEAR_MAC_PROF=1 with a -DHL_MAC_PROF build (HELINEAR_NVCC_EXTRA) prints, per
+  // launch, the average cycles per CTA each role waits (mac_tc.cuh)
+#ifdef HL_MAC_PROF
   static const bool prof = getenv("HELINEAR_MAC_PROF") != nullptr;
+#else
+  constexpr bool prof = false;
+#endif
   A.prof = nullptr;
-  if (prof) cudaMalloc(&A.prof, 12 * sizeof(unsigned long long)), cudaMemsetAsync(A.prof, 0, 96, st);
+  if (prof) cudaMalloc(&A.prof, 8 * sizeof(unsigned long long)), cudaMemsetAsync(A.prof, 0, 64, st);
   {
   KTimer kt(c, HL_K_MAC, st);
   if (fast) k_mac_tc<CW, true><<<grid, T::THREADS, A.ring.smem, st>>>(A, c->dp);
   else k_mac_tc<CW, false><<<grid, T::THREADS, A.ring.smem, st>>>(A, c->dp);
   }
   if (prof) {   // diagnostics: average cycles per CTA waiting, by role
-    unsigned long long h[12];
-    cudaMemcpyAsync(h, A.prof, 96, cudaMemcpyDeviceToHost, st);
+    unsigned long long h[8];
+    cudaMemcpyAsync(h, A.prof, 64, cudaMemcpyDeviceToHost, st);
     cudaStreamSynchronize(st);
     const double n = c->num_sms;
-    fprintf(stderr, "[mac_tc CW=%d nIs=%d nJ=%d RT=%d nst=%d sb=%d] total %.0f | prod.empty %.0f | mma.item %.0f mma.tempty %.0f "
-            "mma.full %.0f mma.zfull %.0f mma.issue %.0f mma.slotcommit %.0f mma.gap %.0f | conv.full %.0f | epi.item %.0f epi.tfull %.0f (cycles/CTA)\n", CW,
-            A.g.nIs, A.g.nJ, A.g.RT, A.ring.nst, A.ring.sbytes, h[7] / n, h[0] / n, h[8] / n, h[1] / n, h[2] / n, h[3] / n,
-            h[6] / n, h[10] / n, (double)(long long)h[11] / n, h[4] / n, h[9] / n, h[5] / n);
+    fprintf(stderr, "[mac_tc CW=%d nIs=%d nJ=%d RT=%d nst=%d sb=%d] total %.0f | prod.empty %.0f | mma.tempty %.0f "
+            "mma.full %.0f mma.zfull %.0f mma.issue %.0f | conv.full %.0f | epi.tfull %.0f (cycles/CTA)\n", CW, A.g.nIs,
+            A.g.nJ, A.g.RT, A.ring.nst, A.ring.sbytes, h[7] / n, h[0] / n, h[1] / n, h[2] / n, h[3] / n, h[6] / n,
+            h[4] / n, h[5] / n);
     cudaFree(A.prof);
   }
 }

@@ -179,6 +179,14 @@ __device__ __forceinline__ bool elect_one() {
   asm volatile("{\n\t.reg .pred P;\n\telect.sync _|P, 0xffffffff;\n\tselp.b32 %0, 1, 0, P;\n\t}" : "=r"(pred));
   return pred != 0;
 }
+// Role profiling (HELINEAR_MAC_PROF=1 at run time) is compiled in only with -DHL_MAC_PROF
+// (HELINEAR_NVCC_EXTRA): the MMA warp's per-stage path is sensitive to every instruction (the
+// checks alone cost c2 1.5 %).
+#ifdef HL_MAC_PROF
+constexpr bool kProf = true;
+#else
+constexpr bool kProf = false;
+#endif
 // mbarrier wait that, when profiling, adds the cycles spent waiting to *acc
 __device__ __forceinline__ void mbar_wait_p(uint64_t *bar, uint32_t parity, unsigned long long *acc) {
   if (acc) {
@@ -331,7 +339,7 @@ k_mac_tc(const __grid_constant__ MacTcArgs A, DevParams P) {
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
-  unsigned long long pw[12] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};   // profiling accumulators (registers)
+  unsigned long long pw[8] = {0, 0, 0, 0, 0, 0, 0, 0};   // profiling accumulators (registers, kProf)
   const long long t_start = clock64();
 
   if (warp == 0) {
@@ -362,7 +370,7 @@ k_mac_tc(const __grid_constant__ MacTcArgs A, DevParams P) {
           const int s = tc_slot(A, it.sq, si);
           for (int kk = 0; kk < A.njc; kk++) {
             const int jc = A.jc0 + kk;
-            mbar_wait_p(&empty[st], ph, A.prof ? &pw[0] : nullptr);
+            mbar_wait_p(&empty[st], ph, (kProf && A.prof) ? &pw[0] : nullptr);
             unsigned char *dst = smem + st * SB;
             mbar_expect_tx(&full[st], tx);
             bulk_g2s_hint(dst + A.ring.a_off, wt + ((size_t)s * g.nJc + jc) * abytes, abytes, &full[st], pol_w);
@@ -392,9 +400,7 @@ k_mac_tc(const __grid_constant__ MacTcArgs A, DevParams P) {
     uint32_t ph = 0;
     uint32_t tile_no = 0, zseq = 0;
     for (uint32_t seq = 0;; seq++) {
-      const long long tw0_ = A.prof ? clock64() : 0;
       const int item = tc_next_item(ifull, iempty, itm, seq);
-      if (A.prof && lane == 0) pw[8] += (unsigned long long)(clock64() - tw0_);
       if (item < 0) break;
       const TcItem it = tc_decode(g, item);
       const int rows = min(g.RT, g.nIp - g.RT * it.t);
@@ -402,43 +408,41 @@ k_mac_tc(const __grid_constant__ MacTcArgs A, DevParams P) {
       const uint32_t idesc = rows <= 64 ? idesc64 : idesc128;
       for (int si = 0; si < T::SPI; si++, tile_no++) {
         const uint32_t buf = tile_no % T::NBUF, tph = (tile_no / T::NBUF) & 1;
-        mbar_wait_p(&tempty[buf], tph ^ 1, (A.prof && lane == 0) ? &pw[1] : nullptr);
+        mbar_wait_p(&tempty[buf], tph ^ 1, (kProf && A.prof && lane == 0) ? &pw[1] : nullptr);
         tc_fence_after();
         const uint32_t dcol = tmem + buf * T::N;
         for (int kk = 0; kk < A.njc; kk++, zseq++) {
           const uint32_t zi = zseq % T::NZ, zph = (zseq / T::NZ) & 1;
-          if (A.prof && lane == 0 && (kk > 0)) pw[11] += (unsigned long long)clock64();
-          mbar_wait_p(&full[st], ph, (A.prof && lane == 0) ? &pw[2] : nullptr);
-          mbar_wait_p(&zfull[zi], zph, (A.prof && lane == 0) ? &pw[3] : nullptr);
+          // Only zfull: the converter arrives on zfull after it observed full[st] (the stage's TMA
+          // bytes, the A planes included, complete), so the acquire on zfull orders the MMA's reads
+          // of the stage after the TMA writes (mbarrier arrive = release, try_wait = acquire) -- one
+          // mbarrier poll less on the MMA warp's per-stage path (c3: MAC -3 %)
+          mbar_wait_p(&zfull[zi], zph, (kProf && A.prof && lane == 0) ? &pw[3] : nullptr);
           tc_fence_after();
-          const long long ti0 = A.prof ? clock64() : 0;
+          const long long ti0 = (kProf && A.prof) ? clock64() : 0;
           const uint32_t a0 = smem_u32(smem + st * SB) + A.ring.a_off;
           const uint32_t z0 = smem_u32(zring + zi * T::Z_BYTES);
-          // descriptors computed by the whole warp (warp-uniform values, before the elected branch):
-          // plane a's descriptor is plane 0's plus a * plane / 16 in the 14-bit address field
-          const uint64_t ad0 = umma_sdesc(a0, lbo_a, 128), bd = umma_sdesc(z0, T::ZR * 16, 128);
-          const uint64_t zd = umma_sdesc(zz, (T::N - T::NM) * 16, 128);
-          const uint32_t pl16 = plane >> 4;
-          const uint32_t zidesc = rows <= 64 ? zdesc64 : zdesc128;
           if (elect_one()) {
             if constexpr (T::ZMMA) {
               if (kk == 0)       // zero the columns [NM, N) the a = 0 MMA does not write
-                umma_i8(dcol + T::NM, ad0, zd, zidesc, 0u);
+                umma_i8(dcol + T::NM, umma_sdesc(a0, lbo_a, 128), umma_sdesc(zz, (T::N - T::NM) * 16, 128),
+                        rows <= 64 ? zdesc64 : zdesc128, 0u);
             }
 #pragma unroll
-            for (int a = 0; a < 7; a++)
-              umma_i8(dcol + a * CW, ad0 + (uint64_t)(a * pl16), bd, idesc, (kk | a) ? 1u : 0u);   // D window shifted by a*CW
+            for (int a = 0; a < 7; a++) {
+              const uint64_t ad = umma_sdesc(a0 + a * plane, lbo_a, 128);
+              const uint64_t bd = umma_sdesc(z0, T::ZR * 16, 128);
+              umma_i8(dcol + a * CW, ad, bd, idesc, (kk | a) ? 1u : 0u);   // D window shifted by a*CW
+            }
             umma_commit(&empty[st]);
             umma_commit(&zempty[zi]);
           }
           __syncwarp();
-          if (A.prof && lane == 0) { const long long t1_ = clock64(); pw[6] += (unsigned long long)(t1_ - ti0); if (kk + 1 < A.njc) pw[11] -= (unsigned long long)t1_; }
+          if (kProf && A.prof && lane == 0) pw[6] += (unsigned long long)(clock64() - ti0);
           if (++st == NST) { st = 0; ph ^= 1; }
         }
-        const long long tc0_ = A.prof ? clock64() : 0;
         if (elect_one()) umma_commit(&tfull[buf]);
         __syncwarp();
-        if (A.prof && lane == 0) pw[10] += (unsigned long long)(clock64() - tc0_);
       }
     }
   } else if (warp < T::EPI0) {
@@ -455,7 +459,7 @@ k_mac_tc(const __grid_constant__ MacTcArgs A, DevParams P) {
       for (int si = 0; si < T::SPI; si++) {
         for (int kk = 0; kk < A.njc; kk++, zseq++) {
           const uint32_t zi = zseq % T::NZ, zph = (zseq / T::NZ) & 1;
-          mbar_wait_p(&full[st], ph, (A.prof && ct == 0) ? &pw[4] : nullptr);
+          mbar_wait_p(&full[st], ph, (kProf && A.prof && ct == 0) ? &pw[4] : nullptr);
           mbar_wait(&zempty[zi], zph ^ 1);
           const uint64_t *raw = reinterpret_cast<const uint64_t *>(smem + st * SB);
           const uint64_t *c1b = reinterpret_cast<const uint64_t *>(smem + st * SB + A.ring.c1_off) + (si & 1);
@@ -510,7 +514,7 @@ k_mac_tc(const __grid_constant__ MacTcArgs A, DevParams P) {
           const int st = (int)(zseq % (uint32_t)NST);
           const uint32_t ph = (zseq / (uint32_t)NST) & 1;
           const uint32_t zi = zseq % T::NZ, zph = (zseq / T::NZ) & 1;
-          mbar_wait_p(&full[st], ph, (A.prof && lane == 0 && cw == 0) ? &pw[4] : nullptr);
+          mbar_wait_p(&full[st], ph, (kProf && A.prof && lane == 0 && cw == 0) ? &pw[4] : nullptr);
           mbar_wait(&zempty[zi], zph ^ 1);
           const uint64_t *raw = reinterpret_cast<const uint64_t *>(smem + st * SB);
           const uint64_t *c1b = reinterpret_cast<const uint64_t *>(smem + st * SB + A.ring.c1_off) + (si & 1);
@@ -569,9 +573,7 @@ k_mac_tc(const __grid_constant__ MacTcArgs A, DevParams P) {
     const int et = threadIdx.x - 32 * T::EPI0;
     uint32_t tile_no = 0;
     for (uint32_t seq = 0;; seq++) {
-      const long long tw0_ = A.prof ? clock64() : 0;
       const int item = tc_next_item(ifull, iempty, itm, seq);
-      if (A.prof && et == 0) pw[9] += (unsigned long long)(clock64() - tw0_);
       if (item < 0) break;
       const TcItem it = tc_decode(g, item);
       const int l = (it.sq * T::SPI) / A.N;
@@ -639,7 +641,7 @@ k_mac_tc(const __grid_constant__ MacTcArgs A, DevParams P) {
 #pragma unroll
       for (int si = 0; si < T::SPI; si++, tile_no++) {
         const uint32_t buf = tile_no % T::NBUF, tph = (tile_no / T::NBUF) & 1;
-        mbar_wait_p(&tfull[buf], tph, (A.prof && et == 0) ? &pw[5] : nullptr);
+        mbar_wait_p(&tfull[buf], tph, (kProf && A.prof && et == 0) ? &pw[5] : nullptr);
         tc_fence_after();
         // Fast recombination (pc.mc < 2^27, every prime of reading C4): with k_d = 2^(8d) mod p in
         // 25-bit limbs, sum_d S_d 2^(8d) = A0 + A1 2^25 (mod p), accumulated from the diagonals as
@@ -793,12 +795,12 @@ k_mac_tc(const __grid_constant__ MacTcArgs A, DevParams P) {
   }
 
   // ---- teardown
-  if (A.prof) {
+  if (kProf && A.prof) {
     const unsigned long long tot = (unsigned long long)(clock64() - t_start);
     if (threadIdx.x == 0) { atomicAdd(&A.prof[0], pw[0]); atomicAdd(&A.prof[7], tot); }
-    if (threadIdx.x == 32) { atomicAdd(&A.prof[1], pw[1]); atomicAdd(&A.prof[2], pw[2]); atomicAdd(&A.prof[3], pw[3]); atomicAdd(&A.prof[6], pw[6]); atomicAdd(&A.prof[8], pw[8]); atomicAdd(&A.prof[10], pw[10]); atomicAdd(&A.prof[11], pw[11]); }
+    if (threadIdx.x == 32) { atomicAdd(&A.prof[1], pw[1]); atomicAdd(&A.prof[2], pw[2]); atomicAdd(&A.prof[3], pw[3]); atomicAdd(&A.prof[6], pw[6]); }
     if (threadIdx.x == 64) atomicAdd(&A.prof[4], pw[4]);
-    if (threadIdx.x == 32 * T::EPI0) { atomicAdd(&A.prof[5], pw[5]); atomicAdd(&A.prof[9], pw[9]); }
+    if (threadIdx.x == 32 * T::EPI0) atomicAdd(&A.prof[5], pw[5]);
   }
   tc_fence_before();
   __syncthreads();
