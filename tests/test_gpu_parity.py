@@ -820,3 +820,95 @@ def test_rerandomized_response_vs_oracle(hl, ctx4096, ctx8192, N, shape, tile, f
     assert np.array_equal(hl.to_host(share).reshape(es.shape), es)
     share_c = ctx.decrypt_share(sk, tile, hl.to_host(masked), Ma, Nb, True)
     assert np.array_equal((share_c + es) & np.uint64((1 << 37) - 1), ref.matmul_mod_t(X, W))
+
+
+# ------------------------------------------------------------------------- write bounds (memcheck stand-in)
+_GUARD = 8192          # words of guard band before and after every buffer
+
+
+def _guarded(nwords, fill=None):
+    """A device buffer of nwords with guard bands of a known pattern on both sides; returns
+    (full tensor, view).  compute-sanitizer is refused on this pool (profiles/r02), so the tests
+    check the library's writes against buffer bounds this way."""
+    import torch
+    full = torch.full((nwords + 2 * _GUARD,), 0x5A5A5A5A5A5A5A5A - (1 << 63), dtype=torch.int64, device="cuda")
+    view = full[_GUARD:_GUARD + nwords]
+    if fill is not None:
+        view.copy_(fill)
+    return full, view
+
+
+def _guards_intact(full, nwords):
+    g = 0x5A5A5A5A5A5A5A5A - (1 << 63)
+    return bool((full[:_GUARD] == g).all()) and bool((full[_GUARD + nwords:] == g).all())
+
+
+@pytest.mark.parametrize("case", ["c1_batch", "fat_cw16", "c0_fused", "c1_host_seeded", "ragged_shard"])
+def test_writes_stay_in_bounds(hl, ctx4096, case):
+    """Every buffer the server calls write (workspace, NTT-domain scratch, compressed responses,
+    share) sits between guard bands that must come back untouched, the read-only inputs (ct_in,
+    weight caches) must come back unchanged, and the results must still equal the oracle's; the
+    calls cover the batch (two streams), the CW = 16 MAC with the c1 transposition, the fused single
+    call, the host batch with the seeded upload and an I-tile shard of a ragged product."""
+    import torch
+    ctx = ctx4096
+    P = _P(ctx)
+    if case == "c1_batch":
+        cfg = synth.CONFIGS["c1"]
+        specs = [(mm.Nb, mm.R, mm.Ma, cfg.tile, 0, -1) for mm in cfg.matmuls]
+    elif case == "fat_cw16":
+        specs = [(256, 48, 40, (16, 8, 16), 0, -1)]
+    elif case == "c0_fused":
+        specs = [(8, 64, 64, (16, 32, 8), 0, -1)]
+    elif case == "c1_host_seeded":
+        cfg = synth.CONFIGS["c1"]
+        specs = [(mm.Nb, mm.R, mm.Ma, cfg.tile, 0, -1) for mm in cfg.matmuls[:2]]
+    else:
+        specs = [(40, 72, 168, (16, 8, 32), 3, 8)]
+    ents, checks = [], []
+    for k, (Nb, R, Ma, tile, i0, i1) in enumerate(specs):
+        lay = ctx.layout(tile, Ma, R, Nb, i0, i1)
+        W = synth.weights(1500 + k, R, Ma)
+        X = synth.activations(1510 + k, Nb, R)
+        sk = ref.keygen(P, 1520 + k)
+        ct = ref.encrypt(P, tile, sk, X, 1530 + k)
+        wc = ctx.encode_weights(tile, hl.to_device(W), i0, i1)
+        wc_sum = wc.clone()
+        ct_dev = hl.to_device(ct)
+        bufs = {name: _guarded(n) for name, n in (("ws", lay.workspace_bytes // 8), ("co", lay.ct_out_words),
+                                                  ("cm", lay.ct_masked_words), ("sh", lay.share_words))}
+        e = dict(wcache=wc, Ma=Ma, R=R, Nb=Nb, tile=tile, ct_in=ct_dev, seed=1540 + k, i_begin=i0, i_end=i1,
+                 workspace=bufs["ws"][1], ct_out_ntt=bufs["co"][1], ct_masked=bufs["cm"][1], share=bufs["sh"][1])
+        if case == "c1_host_seeded":
+            up = _guarded(lay.ct_in_words)
+            bufs["up"] = up
+            c0 = torch.from_numpy(hl.Context.c0_halves(ct).view(np.int64).reshape(-1)).pin_memory()
+            e.update(ct_in=up[1], c0_host=c0, a_seed=ref.public_seed(1530 + k), packed=False,
+                     masked_host=torch.zeros(lay.ct_masked_words, dtype=torch.int64).pin_memory(),
+                     share_host=torch.zeros(lay.share_words, dtype=torch.int64).pin_memory())
+        ents.append(e)
+        nI = lay.nI
+        ct_full = ref.he_matmul(P, tile, W, ct, Nb)
+        em, es = ref.mask_and_share(P, tile, ct_full, Ma, Nb, 1540 + k)
+        checks.append((lay, bufs, wc, wc_sum, ct_dev, ct.copy(), em[i0:(i1 if i1 >= 0 else nI)], es, i0, i1, tile, Ma))
+    if case == "c0_fused":
+        e = ents[0]
+        ctx.he_matmul_share(e["tile"], e["wcache"], e["Ma"], e["R"], e["Nb"], e["ct_in"], e["seed"], True,
+                            workspace=e["workspace"], ct_out_ntt=e["ct_out_ntt"], ct_masked=e["ct_masked"],
+                            share=e["share"])
+    elif case == "c1_host_seeded":
+        ctx.he_linear_batch_host(specs[0][3], ents)
+    else:
+        ctx.he_linear_batch(specs[0][3], ents)
+    _sync()
+    for (lay, bufs, wc, wc_sum, ct_dev, ct_h, em, es, i0, i1, tile, Ma) in checks:
+        for name, (full, view) in bufs.items():
+            assert _guards_intact(full, view.numel()), (case, name)
+        assert torch.equal(wc, wc_sum), (case, "weight cache written")
+        assert np.array_equal(hl.to_host(ct_dev).reshape(ct_h.shape), ct_h), (case, "ct_in written")
+        got = hl.to_host(bufs["cm"][1]).reshape(em.shape)
+        assert np.array_equal(got, em), case
+        m = tile[0]
+        c0_, c1_ = i0 * m, min((i1 if i1 >= 0 else lay.nI) * m, Ma)
+        sh = hl.to_host(bufs["sh"][1]).reshape(es.shape)
+        assert np.array_equal(sh[:, c0_:c1_], es[:, c0_:c1_]), case
