@@ -1789,21 +1789,21 @@ void launch_mac_tc_t(const hl_ctx *c, MacTcArgs A, int smem_budget, int grid, cu
   constexpr bool prof = false;
 #endif
   A.prof = nullptr;
-  if (prof) cudaMalloc(&A.prof, 8 * sizeof(unsigned long long)), cudaMemsetAsync(A.prof, 0, 64, st);
+  if (prof) cudaMalloc(&A.prof, 10 * sizeof(unsigned long long)), cudaMemsetAsync(A.prof, 0, 80, st);
   {
   KTimer kt(c, HL_K_MAC, st);
   if (fast) k_mac_tc<CW, true><<<grid, T::THREADS, A.ring.smem, st>>>(A, c->dp);
   else k_mac_tc<CW, false><<<grid, T::THREADS, A.ring.smem, st>>>(A, c->dp);
   }
   if (prof) {   // diagnostics: average cycles per CTA waiting, by role
-    unsigned long long h[8];
-    cudaMemcpyAsync(h, A.prof, 64, cudaMemcpyDeviceToHost, st);
+    unsigned long long h[10];
+    cudaMemcpyAsync(h, A.prof, 80, cudaMemcpyDeviceToHost, st);
     cudaStreamSynchronize(st);
     const double n = c->num_sms;
     fprintf(stderr, "[mac_tc CW=%d nIs=%d nJ=%d RT=%d nst=%d sb=%d] total %.0f | prod.empty %.0f | mma.tempty %.0f "
-            "mma.full %.0f mma.zfull %.0f mma.issue %.0f | conv.full %.0f | epi.tfull %.0f (cycles/CTA)\n", CW, A.g.nIs,
+            "mma.full %.0f mma.zfull %.0f mma.issue %.0f | conv.full %.0f | epi.tfull %.0f epi.drain %.0f epi.fold_store %.0f (cycles/CTA)\n", CW, A.g.nIs,
             A.g.nJ, A.g.RT, A.ring.nst, A.ring.sbytes, h[7] / n, h[0] / n, h[1] / n, h[2] / n, h[3] / n, h[6] / n,
-            h[4] / n, h[5] / n);
+            h[4] / n, h[5] / n, h[8] / n, h[9] / n);
     cudaFree(A.prof);
   }
 }

@@ -584,29 +584,6 @@ k_mac_tc(const __grid_constant__ MacTcArgs A, DevParams P) {
       const bool active = (m64 ? 16 : 32) * q < rows_valid;   // warp-uniform: this quadrant holds outputs
       const size_t s0 = (size_t)it.sq * T::SPI;
       // full 32-B sector stores of out[I][col][s0 .. s0+3] (c1 columns: into the response)
-      // (store2: the 16-B half h of the sector)
-      auto store2 = [&](int rr, int c, int h, uint64_t v0, uint64_t v1) {
-        const int col = it.cg * CW + c;
-        if (A.c1_out && col >= A.c1_nK) {
-          const int sl = (int)(s0 - (size_t)l * A.N), nt = 1 << A.c1_lognt;
-          const int u = sl >> A.c1_lognt, tq = (sl & (nt - 1)) >> 2;
-          const int k0 = (int)(__brev((unsigned)u) >> 28) * nt + (int)(__brev((unsigned)tq) >> (32 - A.c1_lognt));
-          const int64_t o = (int64_t)(g.RT * it.t + rr) * A.c1_nK + (col - A.c1_nK);
-          v0 = v0 >= pc.two_p ? v0 - pc.two_p : v0; v0 = v0 >= pc.p ? v0 - pc.p : v0;
-          v1 = v1 >= pc.two_p ? v1 - pc.two_p : v1; v1 = v1 >= pc.p ? v1 - pc.p : v1;
-          *reinterpret_cast<ulonglong2 *>(A.c1_out + (size_t)o * P.L * (A.c1_mn + A.N) + (size_t)P.L * A.c1_mn +
-                                          (size_t)l * A.N + k0 + 2 * h) = make_ulonglong2(v0, v1);
-          return;
-        }
-        ulonglong2 *dst = reinterpret_cast<ulonglong2 *>(
-            A.out + ((size_t)(g.RT * it.t + rr) * g.nC + it.cg * CW + c) * g.LN + s0 + 2 * h);
-        if (A.accumulate) {
-          const ulonglong2 o0 = dst[0];
-          v0 += o0.x; v1 += o0.y;
-          v0 = v0 >= pc.p ? v0 - pc.p : v0; v1 = v1 >= pc.p ? v1 - pc.p : v1;
-        }
-        dst[0] = make_ulonglong2(v0, v1);
-      };
       auto store4 = [&](int rr, int c, uint64_t v0, uint64_t v1, uint64_t v2, uint64_t v3) {
         const int col = it.cg * CW + c;
         if (A.c1_out && col >= A.c1_nK) {
@@ -637,11 +614,12 @@ k_mac_tc(const __grid_constant__ MacTcArgs A, DevParams P) {
         dst[0] = make_ulonglong2(v0, v1);
         dst[1] = make_ulonglong2(v2, v3);
       };
-      uint64_t acc[T::REG_EPI ? CH : 1][2];                     // REG_EPI: 2 slots of this lane's outputs
+      uint64_t acc[T::REG_EPI ? CH : 1][4];                     // REG_EPI: the item's 4 slots of this lane's outputs
 #pragma unroll
       for (int si = 0; si < T::SPI; si++, tile_no++) {
         const uint32_t buf = tile_no % T::NBUF, tph = (tile_no / T::NBUF) & 1;
         mbar_wait_p(&tfull[buf], tph, (kProf && A.prof && et == 0) ? &pw[5] : nullptr);
+        const long long te0 = (kProf && A.prof) ? clock64() : 0;
         tc_fence_after();
         // Fast recombination (pc.mc < 2^27, every prime of reading C4): with k_d = 2^(8d) mod p in
         // 25-bit limbs, sum_d S_d 2^(8d) = A0 + A1 2^25 (mod p), accumulated from the diagonals as
@@ -654,20 +632,23 @@ k_mac_tc(const __grid_constant__ MacTcArgs A, DevParams P) {
         constexpr bool fastr = FAST;
         uint64_t L[CH], M[CH], H[CH];
         if (active && fastr && CW >= 16) {
-          // all 13 diagonals of the warp's 4 columns in flight at once (one wait)
+          // the 13 diagonals of 4 of the warp's columns in flight at once (one wait per half)
           const uint32_t base = tmem + ((uint32_t)(32 * q) << 16) + buf * T::N + hh * CH;
-          uint32_t v[13][CH];
 #pragma unroll
-          for (int d = 0; d < 13; d++) tmem_ld_cw<CH>(base + d * CW, v[d]);
-          asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+          for (int c0 = 0; c0 < CH; c0 += 4) {
+            uint32_t v[13][4];
 #pragma unroll
-          for (int c = 0; c < CH; c++) {
-            L[c] = (uint64_t)v[0][c] + ((uint64_t)v[1][c] << 8) + ((uint64_t)v[2][c] << 16) + ((uint64_t)v[3][c] << 24);
-            M[c] = ((uint64_t)v[4][c] << 7) + ((uint64_t)v[5][c] << 15) + ((uint64_t)v[6][c] << 23);
+            for (int d = 0; d < 13; d++) tmem_ld_cw<4>(base + d * CW + c0, v[d]);
+            asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 #pragma unroll
-            for (int d = 7; d < 13; d++) {
-              L[c] += (uint64_t)v[d][c] * pc.ek0[d - 7];
-              M[c] += (uint64_t)v[d][c] * pc.ek1[d - 7];
+            for (int c = 0; c < 4; c++) {
+              L[c0 + c] = (uint64_t)v[0][c] + ((uint64_t)v[1][c] << 8) + ((uint64_t)v[2][c] << 16) + ((uint64_t)v[3][c] << 24);
+              M[c0 + c] = ((uint64_t)v[4][c] << 7) + ((uint64_t)v[5][c] << 15) + ((uint64_t)v[6][c] << 23);
+#pragma unroll
+              for (int d = 7; d < 13; d++) {
+                L[c0 + c] += (uint64_t)v[d][c] * pc.ek0[d - 7];
+                M[c0 + c] += (uint64_t)v[d][c] * pc.ek1[d - 7];
+              }
             }
           }
         } else if (active && fastr) {
@@ -743,6 +724,8 @@ k_mac_tc(const __grid_constant__ MacTcArgs A, DevParams P) {
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(&tempty[buf]);
+        const long long te1 = (kProf && A.prof) ? clock64() : 0;
+        if (kProf && A.prof && et == 0) pw[2] += (unsigned long long)(te1 - te0);   // TMEM drain + accumulate
         if (active) {
 #pragma unroll
           for (int c = 0; c < CH; c++) {
@@ -771,16 +754,17 @@ k_mac_tc(const __grid_constant__ MacTcArgs A, DevParams P) {
               r = r >= pc.two_p ? r - pc.two_p : r;
               r = r >= pc.p ? r - pc.p : r;
             }
-            if constexpr (T::REG_EPI) acc[c][si & 1] = r;
+            if constexpr (T::REG_EPI) acc[c][si] = r;
             else if (row < rows_valid) stg[row * T::STG_STRIDE + (hh * CH + c) * T::SPI + si] = r;
           }
         }
         if constexpr (T::REG_EPI) {
-          if ((si & 1) && active && row < rows_valid) {
+          if (si == 3 && active && row < rows_valid) {      // full 32-B sectors (no partial-sector writes)
 #pragma unroll
-            for (int c = 0; c < CH; c++) store2(row, hh * CH + c, si >> 1, acc[c][0], acc[c][1]);
+            for (int c = 0; c < CH; c++) store4(row, hh * CH + c, acc[c][0], acc[c][1], acc[c][2], acc[c][3]);
           }
         }
+        if (kProf && A.prof && et == 0) pw[3] += (unsigned long long)(clock64() - te1);   // folds + stores
       }
       if constexpr (!T::REG_EPI) {
         asm volatile("bar.sync 2, 256;" ::: "memory");      // 4 slots staged
@@ -800,7 +784,7 @@ k_mac_tc(const __grid_constant__ MacTcArgs A, DevParams P) {
     if (threadIdx.x == 0) { atomicAdd(&A.prof[0], pw[0]); atomicAdd(&A.prof[7], tot); }
     if (threadIdx.x == 32) { atomicAdd(&A.prof[1], pw[1]); atomicAdd(&A.prof[2], pw[2]); atomicAdd(&A.prof[3], pw[3]); atomicAdd(&A.prof[6], pw[6]); }
     if (threadIdx.x == 64) atomicAdd(&A.prof[4], pw[4]);
-    if (threadIdx.x == 32 * T::EPI0) atomicAdd(&A.prof[5], pw[5]);
+    if (threadIdx.x == 32 * T::EPI0) { atomicAdd(&A.prof[5], pw[5]); atomicAdd(&A.prof[8], pw[2]); atomicAdd(&A.prof[9], pw[3]); }
   }
   tc_fence_before();
   __syncthreads();
