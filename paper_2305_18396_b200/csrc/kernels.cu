@@ -1856,6 +1856,8 @@ void launch_mac_tc(const hl_ctx *c, const void *W, const void *X, uint64_t *out,
   A.c1_mn = c1m ? c1m->m * c1m->n : 0;
   A.c1_lognt = (c->N == 4096 ? 12 : 13) - 4;
   A.qperm = A.c1_out != nullptr;
+  A.out_v4 = ((uintptr_t)out % 32) == 0;
+  A.c1_v4 = A.c1_out && ((uintptr_t)A.c1_out % 32) == 0 && (A.c1_mn % 4 == 0 || c->L % 4 == 0);
   A.sched = (int *)((char *)X + tc_sched_offset(g));
   for (int64_t j0 = 0; j0 < g.nJp; j0 += kMacJChunk) {     // S_d < 7 * 4096 * 255^2 < 2^31 per launch
     A.jc0 = (int)(j0 / 32);

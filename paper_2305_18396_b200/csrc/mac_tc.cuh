@@ -122,7 +122,21 @@ struct MacTcArgs {
   int c1_nK, c1_mn, c1_lognt;
   int qperm;                  // quad order (load_ntt_domain_q): set with c1_out
   int c1_in, c1_cols, c1_bytes;   // c1 from c1map (requires qperm): columns per c1 group, box bytes
+  int out_v4, c1_v4;          // the output sectors (out / c1_out) are 32-B aligned: 256-bit stores
 };
+
+// one 32-B output sector: a single 256-bit store (STG.256, sm_100) when 32-B aligned, else two 16-B
+// halves.  The epilogue's stores are scattered sectors (one per output row and column of an item):
+// one instruction per sector instead of two halved its store-side stall (c4 MAC 707 -> 445 ms per
+// stack, c3 27.0 -> 25.2 ms, c2 0.780 -> 0.766 ms per block)
+__device__ __forceinline__ void st_sector(uint64_t *dst, uint64_t v0, uint64_t v1, uint64_t v2, uint64_t v3, int v4) {
+  if (v4) {
+    asm volatile("st.global.v4.u64 [%0], {%1, %2, %3, %4};" ::"l"(dst), "l"(v0), "l"(v1), "l"(v2), "l"(v3) : "memory");
+  } else {
+    reinterpret_cast<ulonglong2 *>(dst)[0] = make_ulonglong2(v0, v1);
+    reinterpret_cast<ulonglong2 *>(dst)[1] = make_ulonglong2(v2, v3);
+  }
+}
 
 // natural evaluation point (prime offset l N included) of the first slot of quad sq (quad order)
 __device__ __forceinline__ int tc_quad_k0(const MacTcArgs &A, int sq) {
@@ -593,26 +607,22 @@ k_mac_tc(const __grid_constant__ MacTcArgs A, DevParams P) {
           const int u = sl >> A.c1_lognt, tq = (sl & (nt - 1)) >> 2;
           const int k0 = (int)(__brev((unsigned)u) >> 28) * nt + (int)(__brev((unsigned)tq) >> (32 - A.c1_lognt));
           const int64_t o = (int64_t)(g.RT * it.t + rr) * A.c1_nK + (col - A.c1_nK);
-          ulonglong2 *dst = reinterpret_cast<ulonglong2 *>(
-              A.c1_out + (size_t)o * P.L * (A.c1_mn + A.N) + (size_t)P.L * A.c1_mn + (size_t)l * A.N + k0);
+          uint64_t *dst = A.c1_out + (size_t)o * P.L * (A.c1_mn + A.N) + (size_t)P.L * A.c1_mn + (size_t)l * A.N + k0;
           v0 = v0 >= pc.two_p ? v0 - pc.two_p : v0; v0 = v0 >= pc.p ? v0 - pc.p : v0;
           v1 = v1 >= pc.two_p ? v1 - pc.two_p : v1; v1 = v1 >= pc.p ? v1 - pc.p : v1;
           v2 = v2 >= pc.two_p ? v2 - pc.two_p : v2; v2 = v2 >= pc.p ? v2 - pc.p : v2;
           v3 = v3 >= pc.two_p ? v3 - pc.two_p : v3; v3 = v3 >= pc.p ? v3 - pc.p : v3;
-          dst[0] = make_ulonglong2(v0, v1);
-          dst[1] = make_ulonglong2(v2, v3);
+          st_sector(dst, v0, v1, v2, v3, A.c1_v4);
           return;
         }
-        ulonglong2 *dst = reinterpret_cast<ulonglong2 *>(
-            A.out + ((size_t)(g.RT * it.t + rr) * g.nC + it.cg * CW + c) * g.LN + s0);
+        uint64_t *dst = A.out + ((size_t)(g.RT * it.t + rr) * g.nC + it.cg * CW + c) * g.LN + s0;
         if (A.accumulate) {
-          const ulonglong2 o0 = dst[0], o1 = dst[1];
+          const ulonglong2 o0 = reinterpret_cast<const ulonglong2 *>(dst)[0], o1 = reinterpret_cast<const ulonglong2 *>(dst)[1];
           v0 += o0.x; v1 += o0.y; v2 += o1.x; v3 += o1.y;
           v0 = v0 >= pc.p ? v0 - pc.p : v0; v1 = v1 >= pc.p ? v1 - pc.p : v1;
           v2 = v2 >= pc.p ? v2 - pc.p : v2; v3 = v3 >= pc.p ? v3 - pc.p : v3;
         }
-        dst[0] = make_ulonglong2(v0, v1);
-        dst[1] = make_ulonglong2(v2, v3);
+        st_sector(dst, v0, v1, v2, v3, A.out_v4);
       };
       uint64_t acc[T::REG_EPI ? CH : 1][4];                     // REG_EPI: the item's 4 slots of this lane's outputs
 #pragma unroll
