@@ -118,6 +118,10 @@ __device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, uint32_t bytes) {
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
 }
 
+// bulk prefetch of [src, src + bytes) into L2 (no completion tracking; bytes a multiple of 16)
+__device__ __forceinline__ void prefetch_l2(const void *src, uint32_t bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");
+}
 __device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t bytes, uint64_t *bar) {
   asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
                ::"r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar)) : "memory");
@@ -374,6 +378,7 @@ struct MacGeom {
                  // first: the fused paths, so that the forward NTTs of c0 pair up and the c1 copies do too)
   int c1_in;     // 1: the MAC loads the c1 halves straight from the ciphertexts (tensor-map TMA, quad
                  // order) and the forward kernel transforms c0 only
+  int pf;        // forward kernels: L2 prefetch distance in CTAs (one wave), 0: off
   int xw;        // X row width (u64 per (slot, J)): CW, or nK when c1_in with one column group (X then
                  // holds only the c0 columns)
 };
@@ -414,6 +419,7 @@ MacGeom mac_geom(const hl_ctx *c, int64_t nIs, int64_t nJ, int64_t nC) {
   g.nJc = g.nJp / 32;
   g.cperm = 0;
   g.c1_in = 0;
+  g.pf = 0;
   g.xw = g.CW;
   return g;
 }
@@ -539,6 +545,20 @@ k_ntt_fwd_c0x2(const uint64_t *__restrict__ in, uint64_t *__restrict__ out, DevP
   double a[16], b[16];
   const size_t base0 = (((size_t)J * nK + K0) * 2 * P.L + l) * Gm::N;       // c0 of (J, K0)
   const size_t base1 = base0 + (pair ? (size_t)2 * P.L * Gm::N : 0);       // c0 of (J, K0 + 1)
+  if (t == 0 && mg.pf > 0) {
+    // the inputs of the CTA one wave ahead (CTAs are dispatched x fastest) into L2: its loads at
+    // start-up no longer wait for DRAM.  N = 8192 only (launch_fwd_cperm): one 512-thread CTA per
+    // SM exposes that latency (c4 forward 238 -> 227 ms per stack); at N = 4096 (2-3 CTAs per SM)
+    // it measured slower (c3 11.2 -> 11.6 ms)
+    const unsigned lin = blockIdx.y * gridDim.x + blockIdx.x + (unsigned)mg.pf;
+    if (lin < gridDim.x * gridDim.y) {
+      const int x2 = (int)(lin % gridDim.x), l2 = (int)(lin / gridDim.x);
+      const int J2 = x2 / nKh, K2 = 2 * (x2 % nKh);
+      const uint64_t *b2 = in + (((size_t)J2 * nK + K2) * 2 * P.L + l2) * Gm::N;
+      prefetch_l2(b2, Gm::N * 8);
+      if (K2 + 1 < nK) prefetch_l2(b2 + (size_t)2 * P.L * Gm::N, Gm::N * 8);
+    }
+  }
   constexpr int KK = Gm::k(0), GG = 16 >> KK;
 #pragma unroll
   for (int g = 0; g < GG; g++)
@@ -1653,9 +1673,19 @@ void launch_fwd_x(const hl_ctx *c, const uint64_t *in, void *out, int64_t npoly,
 }
 
 
+// CTAs of kernel k resident on the device at once (one wave): the L2 prefetch distance of the NTT kernels
+template <typename Kern>
+int wave_ctas(const hl_ctx *c, Kern k, int threads, size_t smem) {
+  if (threads < 512) return 0;             // N = 4096 kernels: off (see k_ntt_fwd_c0x2)
+  int n = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k, threads, smem) != cudaSuccess) { cudaGetLastError(); return 0; }
+  return n * c->num_sms;
+}
+
 template <int LOGN>
-void launch_fwd_cperm(const hl_ctx *c, const uint64_t *in, uint64_t *out, int64_t npoly, const MacGeom &mg,
+void launch_fwd_cperm(const hl_ctx *c, const uint64_t *in, uint64_t *out, int64_t npoly, const MacGeom &mg_in,
                       cudaStream_t st) {
+  MacGeom mg = mg_in;
   const int nK = mg.nC / 2;
   const int64_t nJ = npoly / mg.nC;
   constexpr size_t smem2 = ntt_smem<LOGN>() * 2;
@@ -1673,8 +1703,14 @@ void launch_fwd_cperm(const hl_ctx *c, const uint64_t *in, uint64_t *out, int64_
   KTimer kt(c, HL_K_NTT_FWD, st);
   if (mg.c1_in) {                                  // c1 is read by the MAC itself: c0 pairs only
     const dim3 gx((unsigned)(nJ * ((nK + 1) / 2)), c->L);
-    if constexpr (LOGN == 12) k_ntt_fwd_c0x2<LOGN, false, 3><<<gx, Geom<LOGN>::NT, smem2, st>>>(in, out, c->dp, mg);
-    else k_ntt_fwd_c0x2<LOGN, false, MB2><<<gx, Geom<LOGN>::NT, smem2, st>>>(in, out, c->dp, mg);
+    if constexpr (LOGN == 12) {
+      mg.pf = wave_ctas(c, k_ntt_fwd_c0x2<LOGN, false, 3>, Geom<LOGN>::NT, smem2);
+      k_ntt_fwd_c0x2<LOGN, false, 3><<<gx, Geom<LOGN>::NT, smem2, st>>>(in, out, c->dp, mg);
+    }
+    else {
+      mg.pf = wave_ctas(c, k_ntt_fwd_c0x2<LOGN, false, MB2>, Geom<LOGN>::NT, smem2);
+      k_ntt_fwd_c0x2<LOGN, false, MB2><<<gx, Geom<LOGN>::NT, smem2, st>>>(in, out, c->dp, mg);
+    }
     return;
   }
   // c1 pairs (K0, K0+1) adjacent in the c1 column range, copied by the c0 kernel; whole 16-column
@@ -1684,16 +1720,25 @@ void launch_fwd_cperm(const hl_ctx *c, const uint64_t *in, uint64_t *out, int64_
   if constexpr (LOGN == 12) {
     if (fused) {   // N = 4096: 3 CTAs per SM (80 registers, a few bytes of spill; measured best)
       const dim3 gx((unsigned)(nJ * ((nK + 1) / 2)), c->L);
-      k_ntt_fwd_c0x2<LOGN, true, 3><<<gx, Geom<LOGN>::NT, smem2, st>>>(in, out, c->dp, mg);
+      {
+        mg.pf = wave_ctas(c, k_ntt_fwd_c0x2<LOGN, true, 3>, Geom<LOGN>::NT, smem2);
+        k_ntt_fwd_c0x2<LOGN, true, 3><<<gx, Geom<LOGN>::NT, smem2, st>>>(in, out, c->dp, mg);
+      }
       return;
     }
   }
   if (fused) {
-    k_ntt_fwd_c0x2<LOGN, true><<<dim3((unsigned)(nJ * ((nK + 1) / 2)), c->L), Geom<LOGN>::NT, smem2, st>>>(in, out, c->dp, mg);
+    {
+      mg.pf = wave_ctas(c, k_ntt_fwd_c0x2<LOGN, true>, Geom<LOGN>::NT, smem2);
+      k_ntt_fwd_c0x2<LOGN, true><<<dim3((unsigned)(nJ * ((nK + 1) / 2)), c->L), Geom<LOGN>::NT, smem2, st>>>(in, out, c->dp, mg);
+    }
     return;
   }
   // odd nK (or whole 16-column c1 groups): the c0 pairs without their c1, then the c1 reordering
-  k_ntt_fwd_c0x2<LOGN, false, MB2><<<dim3((unsigned)(nJ * ((nK + 1) / 2)), c->L), Geom<LOGN>::NT, smem2, st>>>(in, out, c->dp, mg);
+  {
+    mg.pf = wave_ctas(c, k_ntt_fwd_c0x2<LOGN, false, MB2>, Geom<LOGN>::NT, smem2);
+    k_ntt_fwd_c0x2<LOGN, false, MB2><<<dim3((unsigned)(nJ * ((nK + 1) / 2)), c->L), Geom<LOGN>::NT, smem2, st>>>(in, out, c->dp, mg);
+  }
   if (mg.CW == 16 && nK % 16 == 0) {
     k_c1_tx16<LOGN><<<dim3((unsigned)(Geom<LOGN>::N / 256), (unsigned)(nJ * (nK / 16)), c->L), 256, 0, st>>>(in, out, c->dp, mg);
     return;

@@ -1,7 +1,8 @@
-"""Per-product tile sweep on the GPU (experiment): time hl_he_matmul_share of each c2 product
-under candidate tiles (m, r, n), per kernel (library CUDA events), sequential, after warm-up.
+"""Per-product tile sweep on the GPU (experiment): time hl_he_matmul_share of each product of a
+config's block under candidate tiles (m, r, n), per kernel (library CUDA events), sequential, after
+warm-up.
 
-    python tools/gpu/tile_sweep.py [steps]
+    python tools/gpu/tile_sweep.py [steps] [config] ["m,r,n;m,r,n;..."]
 """
 import os
 import sys
@@ -14,11 +15,13 @@ import paper_2305_18396_b200 as hl  # noqa: E402
 import synth  # noqa: E402
 
 steps = int(sys.argv[1]) if len(sys.argv) > 1 else 20
-cfg = synth.CONFIGS["c2"]
+cfg = synth.CONFIGS[sys.argv[2] if len(sys.argv) > 2 else "c2"]
 ctx = hl.Context(cfg.N, cfg.L, synth.T_BITS, device=0)
 dev = torch.device("cuda", 0)
 cands = [(16, 8, 32), (8, 16, 32), (32, 8, 16), (4, 32, 32), (8, 8, 64), (16, 16, 16), (32, 4, 32)]
-for mi, mm in enumerate(cfg.matmuls):
+if len(sys.argv) > 3:
+    cands = [tuple(int(v) for v in t.split(",")) for t in sys.argv[3].split(";")]
+for mi, mm in enumerate(cfg.block_shapes(cfg.seqs) if hasattr(cfg, "block_shapes") else cfg.matmuls):
     X = synth.activations(synth.seed_for(0, mi, "x"), mm.Nb, mm.R)
     W = synth.weights(synth.seed_for(0, mi, "w"), mm.R, mm.Ma)
     sk = ctx.keygen(synth.seed_for(0, mi, "key"))
