@@ -2261,8 +2261,8 @@ static int linear_batch_run(const hl_ctx *c, hl_tile tile, int n, const hl_linea
   // every forward NTT is issued up front on the forward stream (measured: 1.082 -> 1.060 ms per c2
   // block vs interleaving them with the MACs)
   // adaptive policy: with many columns per weight byte (nK >= 8, e.g. c3/c4: 8-16x c2's NTT work per
-  // byte) co-resident kernels slow each other more than they overlap -- issue the products one after
-  // the other on the forward / MAC / inverse streams without the cross-product overlap
+  // byte) a MAC sharing its SMs with NTT kernels slows down more than the overlap gains -- run every
+  // MAC alone and overlap only the NTT stages of neighbouring products (serial branch below)
   constexpr int serial_nk = 8;
   bool serial = !ready;
   for (int i : ord) serial = serial && E[i].g.nK >= serial_nk;
@@ -2282,21 +2282,33 @@ static int linear_batch_run(const hl_ctx *c, hl_tile tile, int n, const hl_linea
   };
   const int na = (int)ord.size();
   if (na == 0) return HL_OK;
-  if (serial) {                                   // the products one after the other on `stream`
-    for (int k = 0; k < na; k++) {
-      const int i = ord[k];
-      fwd_ntt(c, d[i].ct_in, d[i].workspace, E[i].g.nJ * 2 * E[i].g.nK, &E[i].mg, sc);
-      launch_mac(c, (const uint2 *)d[i].wcache, (const uint32_t *)d[i].workspace, d[i].ct_out_ntt, E[i].mg, sc,
-                 kMacSmemAlone, 0, E[i].M.c1_done ? &E[i].M : nullptr, d[i].ct_masked, d[i].ct_in);
-      if (c->N == 4096) launch_inv_mask<12>(c, d[i].ct_out_ntt, d[i].ct_masked, d[i].share, E[i].M, E[i].g.nIs * E[i].g.nK, sc);
-      else launch_inv_mask<13>(c, d[i].ct_out_ntt, d[i].ct_masked, d[i].share, E[i].M, E[i].g.nIs * E[i].g.nK, sc);
-    }
-    return hl_cuda_check("hl_he_linear_batch: launch");
-  }
   cudaEventRecord(e_in, sc);                      // inputs written on `stream` are visible to both streams
   cudaStreamWaitEvent(s0, e_in, 0);
   cudaStreamWaitEvent(s1, e_in, 0);
   cudaStreamWaitEvent(sf, e_in, 0);
+  if (serial) {
+    // every MAC alone on the device (it takes every SM's shared memory and registers), and the two
+    // NTT stages of neighbouring products side by side: the forward NTT of product k+1 starts when
+    // MAC(k) is done, beside the inverse NTT + mask of product k (both FP64- and latency-bound at
+    // low occupancy).  MAC(k+1) waits for its forward NTT only.
+    for (int k = 0; k < na; k++) {
+      const int i = ord[k];
+      if (k == 0) fwd(i);
+      cudaStreamWaitEvent(s0, e_fwd[i], 0);
+      {
+        NvtxRange nr("hl.batch.mac");
+        launch_mac(c, (const uint2 *)d[i].wcache, (const uint32_t *)d[i].workspace, d[i].ct_out_ntt, E[i].mg, s0,
+                   kMacSmemAlone, 0, E[i].M.c1_done ? &E[i].M : nullptr, d[i].ct_masked, d[i].ct_in);
+      }
+      cudaEventRecord(e_mac[i], s0);
+      if (k + 1 < na) {
+        cudaStreamWaitEvent(sf, e_mac[i], 0);
+        fwd(ord[k + 1]);
+      }
+      cudaStreamWaitEvent(s1, e_mac[i], 0);
+      inv(i);
+    }
+  } else {
   for (int k = 0; k < na; k++) fwd(ord[k]);
   for (int k = 0; k < na; k++) {
     const int i = ord[k];
@@ -2308,6 +2320,7 @@ static int linear_batch_run(const hl_ctx *c, hl_tile tile, int n, const hl_linea
     cudaStreamWaitEvent(s1, e_mac[i], 0);
     inv(i);                                                               // overlaps MAC(i+1)
     if (done) cudaEventRecord(done[i], s1);
+  }
   }
   cudaEventRecord(e_done, s1);
   cudaEventRecord(e_macs, s0);

@@ -81,6 +81,8 @@ CASES = [
     (4096, (40, 24, 40), (16, 8, 32)),     # ragged in every dimension, several tiles
     (4096, (64, 48, 100), (4, 8, 16)),     # nC = 8, ragged I tail (nI = 25)
     (4096, (3, 5, 7), (1, 1, 1)),          # degenerate 1x1x1 tile, nC = 6
+    (4096, (6, 10, 7), (1, 4, 2)),         # m n = 2: the fused MAC's c1 sectors in the response are only
+                                           # 16-B aligned (two 16-B stores instead of one 256-bit store)
     (8192, (32, 48, 40), (32, 16, 16)),    # c4 parameters (N=8192, L=3) at small size
     (4096, (256, 40, 50), (16, 8, 32)),    # nC = 16: the MAC's 16-column groups (CW = 16)
     (4096, (520, 24, 40), (16, 8, 32)),    # nC = 34 -> CW = 2, 17 column groups, ragged K tail
