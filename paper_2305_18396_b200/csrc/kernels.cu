@@ -1155,7 +1155,9 @@ __device__ __forceinline__ void inv_rounds_live_c(double (&a)[16], double *cv, i
 }
 
 template <int LOGN, bool RR, bool CMP = false>
-__global__ void __launch_bounds__(Geom<LOGN>::NT, (CMP && LOGN == 12) ? 4 : (LOGN == 12 ? 2 : 1))
+// (N = 8192 with compact parking: 2 CTAs per SM at 64 registers, a few bytes of spill -- phase B runs
+// on 1/re of the threads, so a second CTA's phase A fills the SM: c4 inverse 126 -> 102 ms per stack)
+__global__ void __launch_bounds__(Geom<LOGN>::NT, (CMP && LOGN == 12) ? 4 : (LOGN == 12 || CMP ? 2 : 1))
 k_intt_c0_pruned(const uint64_t *__restrict__ ct_ntt, uint64_t *__restrict__ masked, uint64_t *__restrict__ share,
                  MaskArgs M, DevParams P) {
   using Gm = Geom<LOGN>;

@@ -87,6 +87,8 @@ CASES = [
     (4096, (256, 40, 50), (16, 8, 32)),    # nC = 16: the MAC's 16-column groups (CW = 16)
     (4096, (520, 24, 40), (16, 8, 32)),    # nC = 34 -> CW = 2, 17 column groups, ragged K tail
     (8192, (288, 48, 40), (32, 16, 16)),   # c4 tile, nC = 36 (CW = 4, 9 groups), N=8192 L=3
+    (8192, (256, 48, 40), (32, 16, 16)),   # c4 tile, nK = 16: whole 16-column groups at N = 8192 (the
+                                           # single-column forward kernel, c1 by k_c1_tx16)
     (4096, (512, 24, 40), (16, 8, 32)),    # nK = 16: pure c0 / c1 column groups (CW = 16, 2 groups;
                                            # the fused MAC reads c1 by tensor-map TMA, group 1 has no X)
 ]
