@@ -258,11 +258,14 @@ def test_linear_batch_mixed_tiles_vs_oracle(hl, ctx4096):
 
 def test_linear_batch_serial_policy_vs_oracle(hl, ctx4096):
     """hl_he_linear_batch with nK >= 8 for every entry (c3/c4-sized token counts) takes the
-    adaptive serial policy (products one after the other): bit-exact against the oracle."""
+    adaptive serial policy (every MAC alone; the forward NTT of entry k+1 beside the inverse NTT +
+    mask of entry k): bit-exact against the oracle, twice over (the cross-stream ordering is
+    re-exercised), including a CW = 16 entry with whole c1 column groups (k_c1_tx16)."""
     ctx = ctx4096
     P = _P(ctx)
     ins = []
-    for k, (Nb, R, Ma, tile) in enumerate([(256, 48, 40, (16, 8, 16)), (160, 40, 72, (8, 8, 16))]):
+    for k, (Nb, R, Ma, tile) in enumerate([(256, 48, 40, (16, 8, 16)), (512, 24, 40, (16, 8, 32)),
+                                           (160, 40, 72, (8, 8, 16))]):
         nI, nJ, nK = ref.tile_counts(tile, Ma, R, Nb)
         assert nK >= 8
         W = synth.weights(1200 + k, R, Ma)
@@ -270,12 +273,13 @@ def test_linear_batch_serial_policy_vs_oracle(hl, ctx4096):
         ins.append((Nb, R, Ma, tile, W, ct_in, 1220 + k))
     entries = [dict(wcache=ctx.encode_weights(t, hl.to_device(W)), Ma=Ma, R=R, Nb=Nb, tile=t,
                     ct_in=hl.to_device(ct), seed=sd) for Nb, R, Ma, t, W, ct, sd in ins]
-    outs = ctx.he_linear_batch((1, 1, 1), entries)
-    _sync()
-    for (Nb, R, Ma, t, W, ct, sd), (m, sh) in zip(ins, outs):
-        em, es = ref.mask_and_share(P, t, ref.he_matmul(P, t, W, ct, Nb), Ma, Nb, sd)
-        assert np.array_equal(hl.to_host(m).reshape(em.shape), em)
-        assert np.array_equal(hl.to_host(sh).reshape(es.shape), es)
+    exp = [ref.mask_and_share(P, t, ref.he_matmul(P, t, W, ct, Nb), Ma, Nb, sd) for Nb, R, Ma, t, W, ct, sd in ins]
+    for _ in range(2):
+        outs = ctx.he_linear_batch((1, 1, 1), entries)
+        _sync()
+        for (em, es), (m, sh) in zip(exp, outs):
+            assert np.array_equal(hl.to_host(m).reshape(em.shape), em)
+            assert np.array_equal(hl.to_host(sh).reshape(es.shape), es)
 
 
 def _sample_tiles(nI, nK, mac_rows):
