@@ -284,11 +284,15 @@ typedef struct {
 } hl_linear_desc;
 
 /* n compressed hl_he_matmul_share calls, e.g. the four products of an encoder block; results are
- * bit-identical to the calls made one after the other on `stream`.  The calls are pipelined: the
- * MAC of entry i (HBM-bound) runs on `stream` while the forward NTT of entry i+1 and the inverse
- * NTT + mask of entry i-1 (FP64-pipe-bound) run on the context's auxiliary stream; `stream`
- * waits for all of it before later work.  Uses the context's auxiliary stream: do not run two
- * batches on one context concurrently. */
+ * bit-identical to the calls made one after the other on `stream`.  The calls are pipelined over
+ * the context's internal streams (joined to `stream` at entry and exit, so the call is ordered on
+ * `stream` like a single kernel): the MACs in entry order on a high-priority stream, the forward
+ * NTTs on a forward stream and each inverse NTT + mask on an auxiliary stream behind its MAC.  Two
+ * schedules: with few columns per weight byte (some entry with nK < 8, e.g. c2)
+ * every forward NTT is issued up front and shares SMs with the MACs; otherwise (c3/c4 token
+ * counts) every MAC runs alone and only the forward NTT of entry i+1 overlaps the inverse of entry
+ * i.  The internal streams are per context: batches issued concurrently on one context from
+ * different caller streams serialise on them (use one context per concurrent caller). */
 int hl_he_linear_batch(const hl_ctx *ctx, hl_tile tile, int n, const hl_linear_desc *descs, void *stream);
 
 /* End-to-end server call on HOST buffers (the e2e path of bench.py): copies ct_in_host
