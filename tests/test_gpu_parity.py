@@ -256,6 +256,32 @@ def test_linear_batch_mixed_tiles_vs_oracle(hl, ctx4096):
             assert np.array_equal(hl.to_host(sh).reshape(es.shape), es), (rep, mm.name)
 
 
+def test_linear_batch_pipelined_with_fat_product_vs_oracle(hl, ctx4096):
+    """The pipelined schedule (some entry has nK < 8, so every forward NTT is issued up front and
+    shares SMs with the MACs) with a fat CW = 16 entry among thin ones: the c1 transposition
+    (k_c1_tx16), the CW = 16 MAC and the CW = 4/8 MACs with the c1 tensor-map path interleaved
+    over the context's streams; bit-exact against the oracle, three times over."""
+    ctx = ctx4096
+    P = _P(ctx)
+    ins = []
+    for k, (Nb, R, Ma, tile) in enumerate([(128, 40, 72, (8, 8, 32)), (512, 24, 40, (16, 8, 32)),
+                                           (64, 48, 40, (4, 16, 32))]):
+        W = synth.weights(1400 + k, R, Ma)
+        nI, nJ, nK = ref.tile_counts(tile, Ma, R, Nb)
+        ct_in = synth.uniform_below(1410 + k, (nJ, nK, 2, P.L, P.N), P.primes)
+        ins.append((Nb, R, Ma, tile, W, ct_in, 1420 + k))
+    assert min(ref.tile_counts(t, Ma, R, Nb)[2] for Nb, R, Ma, t, *_ in ins) < 8
+    entries = [dict(wcache=ctx.encode_weights(t, hl.to_device(W)), Ma=Ma, R=R, Nb=Nb, tile=t,
+                    ct_in=hl.to_device(ct), seed=sd) for Nb, R, Ma, t, W, ct, sd in ins]
+    exp = [ref.mask_and_share(P, t, ref.he_matmul(P, t, W, ct, Nb), Ma, Nb, sd) for Nb, R, Ma, t, W, ct, sd in ins]
+    for rep in range(3):
+        outs = ctx.he_linear_batch((1, 1, 1), entries)
+        _sync()
+        for (em, es), (m, sh) in zip(exp, outs):
+            assert np.array_equal(hl.to_host(m).reshape(em.shape), em), rep
+            assert np.array_equal(hl.to_host(sh).reshape(es.shape), es), rep
+
+
 def test_linear_batch_serial_policy_vs_oracle(hl, ctx4096):
     """hl_he_linear_batch with nK >= 8 for every entry (c3/c4-sized token counts) takes the
     adaptive serial policy (every MAC alone; the forward NTT of entry k+1 beside the inverse NTT +
